@@ -1,0 +1,173 @@
+/*
+ * pxst_b200.h -- C ABI of the B200-native PXST hot path (arXiv 2003.12726).
+ *
+ * One shared library, libpxst_b200.so, hand-written CUDA for sm_100a.  Every
+ * entry point takes DEVICE pointers owned by the caller plus a cudaStream_t
+ * passed as `void*` (NULL = legacy default stream), enqueues its kernels on
+ * that stream and returns a status code; nothing is synchronised unless the
+ * function says so.  No torch types cross this boundary.  The library keeps
+ * no global state except a thread-local error string; scratch memory is
+ * taken from the stream-ordered allocator (cudaMallocAsync) and released on
+ * the same stream before the call returns.
+ *
+ * The reference (pure NumPy, /root/reference/pkg/src/pxst) has no FFI; the
+ * entry points below are what its Python hot path binds to through ctypes
+ * (see INTEGRATION.md).  Each cites the reference function it replaces.
+ *
+ * Conventions shared with the reference (data_model.py:3-12):
+ *   - axis order [slow-scan (ss), fast-scan (fs)], row-major, fs fastest;
+ *   - u: [2, ss, fs] float64 pixel map in reference-grid pixels;
+ *   - di, dj: [n_frames] float64 translations (reference-grid pixels);
+ *   - reference grid origin (n0, m0) is subtracted from u - delta.
+ */
+#ifndef PXST_B200_H
+#define PXST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PXST_ABI_VERSION 1
+
+/* status codes */
+#define PXST_OK 0
+#define PXST_EINVAL 1   /* bad argument: maps to ValueError in the Python shim   */
+#define PXST_ECUDA 2    /* CUDA runtime / launch error: maps to RuntimeError     */
+#define PXST_ENOMEM 3   /* device allocation failed                              */
+
+/* A scan resident on one device.  Mirrors recon._work_set (recon.py:81-96):
+ * the kernels read the stack in place; work pixels are work[ss,fs] != 0
+ * (mask & W > 0 & inside the half-open ROI), good frames are good[0..n_good). */
+typedef struct pxst_scan {
+  const float* frames;    /* [n_frames, ss, fs] float32                          */
+  int64_t n_frames, ss, fs;
+  const int32_t* good;    /* [n_good] frame indices, ascending                   */
+  int64_t n_good;
+  const double* w64;      /* [ss, fs] whitefield, float64                        */
+  const float* w32;       /* [ss, fs] whitefield, float32 copy                   */
+  const uint8_t* work;    /* [ss, fs] work-pixel flags                           */
+  int64_t roi[4];         /* ss_min, ss_max, fs_min, fs_max (half-open)          */
+} pxst_scan;
+
+/* Per-scan statistics, iteration invariant.  Device buffers
+ * allocated by the caller; filled by pxst_stack_stats. */
+typedef struct pxst_stats {
+  double* var_pm;      /* [ss*fs] sum_n (I-W)^2, pixel-map normaliser (recon.py:257-263) */
+  double* sigma2;      /* [ss*fs] population variance over good frames, floored
+                          at 1e-8 max(W)^2 (recon.py:410-412); 0 off the work set  */
+  double* frame_norm;  /* [n_good] sum_p (I_n-W)^2 (recon.py:367)                   */
+  double* scalars;     /* [4]: max W over work px, sum |I| W, n_work, sum |I|        */
+} pxst_stats;
+
+/* Reference image on device: fm = i_ref where valid else 0 (float32),
+ * valid = wsum > 0 (data_model.py:186-188). */
+typedef struct pxst_ref {
+  const float* fm;        /* [os, of] */
+  const uint8_t* valid;   /* [os, of] */
+  int64_t os, of;
+  int64_t n0, m0;
+} pxst_ref;
+
+int pxst_abi_version(void);
+const char* pxst_last_error(void);
+/* Number of kernels this thread has launched through the library (for the
+ * bench's gpu_launches count). */
+int64_t pxst_launch_count(void);
+
+/* K0: per-scan statistics.  Replaces the fallback/variance/normaliser
+ * computations at recon.py:257-260, :367 and :410-412.  `fw` (nullable,
+ * [n_frames, ss, fs] float32) gives frame weights; then var_pm is
+ * sum_n fw (I-W)^2 as at recon.py:258-260. */
+int pxst_stack_stats(const pxst_scan* scan, const float* fw, const pxst_stats* st,
+                     void* stream);
+
+/* Bounding box of u over work pixels and of (di, dj) over good frames:
+ * out[8] (device, float64) = min u0, max u0, min u1, max u1, min di, max di,
+ * min dj, max dj.  Feeds the grid rule of recon.py:126-132. */
+int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const double* dj,
+              double* out, void* stream);
+
+/* K1 object formation, splat half (recon.py:99-138; interp.py:88-123).
+ * Adds, for every good frame in [frame_lo, frame_hi) of scan->good and work
+ * pixel, I*W*w_c to num_fx and W^2*w_c to den_fx at the four corners of
+ * (u0 - di - n0, u1 - dj - m0).  Accumulators are int64 fixed point with
+ * scales num_scale / den_scale (powers of two, see pxst_fixed_scales), so the
+ * sum is exact, order independent and bit-reproducible, also after an
+ * integer all-reduce across GPUs.  Points outside [0,os-1]x[0,of-1] are
+ * dropped whole; their count is added to *n_dropped (device, nullable). */
+int pxst_object_splat(const pxst_scan* scan, const double* u, const double* di,
+                      const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
+                      int64_t frame_lo, int64_t frame_hi, double num_scale, double den_scale,
+                      int64_t* num_fx, int64_t* den_fx, unsigned long long* n_dropped,
+                      void* stream);
+
+/* K1 normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0,
+ * wsum = den; also writes the float32 masked image fm and valid flags used by
+ * the search kernels.  Any of the four outputs may be NULL. */
+int pxst_object_finish(const int64_t* num_fx, const int64_t* den_fx, int64_t n,
+                       double num_scale, double den_scale, double* i_ref, double* wsum,
+                       float* fm, uint8_t* valid, void* stream);
+
+/* Power-of-two fixed-point scales such that |sum| < 2^61 for any cell given
+ * the total absolute mass `mass` splatted (host helper, no device work). */
+double pxst_fixed_scale(double mass);
+
+/* Convenience: bbox-free object map for a known grid = splat + finish with
+ * internal accumulators.  Replaces recon.make_reference after the bbox. */
+int pxst_object_map(const pxst_scan* scan, const pxst_stats* st, const double* u,
+                    const double* di, const double* dj, int64_t n0, int64_t m0, int64_t os,
+                    int64_t of, double* i_ref, double* wsum, float* fm, uint8_t* valid,
+                    void* stream);
+
+/* K2 pixel-map grid search + argmin + paraboloid refinement
+ * (recon.py:144-170, 183-207, 221-296 with sigma = 0, integrate = False).
+ * subpixel_step = 0 selects the integer grid -half..half; otherwise
+ * step*(-k..k), k = round(half/step) (recon.py:51-57).  fw / var_fw
+ * (nullable) carry frame weights and their normaliser.  u_out [2,ss,fs] is
+ * a copy of u_in with work pixels updated; err_out [ss,fs] is the selected
+ * normalised error (0 off the work set and for static pixels). */
+int pxst_pixel_map_search(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                          const double* u_in, const double* di, const double* dj,
+                          int64_t half_ss, int64_t half_fs, double subpixel_step, int refine,
+                          const float* fw, const double* var_fw, double* u_out,
+                          double* err_out, void* stream);
+
+/* K3 per-frame translation grid search (recon.py:336-385), including the
+ * reference's quirks: offsets enter as u - (d + off) and the paraboloid
+ * offset (grid-index units) is added in pixels whenever the argmin is
+ * interior.  Frames in [frame_lo, frame_hi) of scan->good are searched;
+ * di_out / dj_out [n_frames] must already hold the input translations (only
+ * searched frames with a positive normaliser are overwritten).  err_out
+ * (nullable) receives the normalised [n_searched, Ka, Kb] error grids. */
+int pxst_translation_search(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                            const double* u, const double* di, const double* dj,
+                            int64_t half_ss, int64_t half_fs, double subpixel_step,
+                            int64_t frame_lo, int64_t frame_hi, double* di_out,
+                            double* dj_out, double* err_out, void* stream);
+
+/* K4 error maps (recon.py:388-438).  per_frame [n_frames] (0 for frames not
+ * good), per_pixel [ss,fs], ref_plane [os,of] (normalised reference-plane
+ * projection of the residuals), total (device scalar).  ref_num_fx /
+ * ref_den_fx (nullable) receive the un-normalised fixed-point accumulators
+ * (scale = *plane_scale on return, host) for multi-GPU reduction. */
+int pxst_error_maps(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                    const double* u, const double* di, const double* dj, double* per_frame,
+                    double* per_pixel, double* ref_plane, double* total, void* stream);
+
+/* Interpolation primitives (interp.py:53-85 and :88-123), for the drop-in
+ * interp module and the parity tests.  gather: vals/ok at n points of the
+ * masked image.  splat: float64 accumulation into acc_v/acc_w [os,of]
+ * (adds to their current contents); returns the dropped count in *n_dropped
+ * (host, synchronises the stream). */
+int pxst_gather(const pxst_ref* ref, const double* x, const double* y, int64_t n,
+                double* vals, uint8_t* ok, void* stream);
+int pxst_splat(double* acc_v, double* acc_w, int64_t os, int64_t of, const double* x,
+               const double* y, const double* value, const double* weight, int64_t n,
+               int64_t* n_dropped, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PXST_B200_H */

@@ -1,0 +1,122 @@
+"""ctypes binding of ``libpxst_b200.so`` (the C ABI in ``include/pxst_b200.h``).
+
+This is the only door to the GPU kernels.  There is no CPU fallback: if the
+library is missing or no CUDA device is present, :func:`lib` raises.
+Status codes map to exceptions as the reference's errors do: PXST_EINVAL ->
+``ValueError`` (bad window, empty work set, ...), everything else ->
+``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint8, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("PXST_LIB", os.path.join(HERE, "libpxst_b200.so"))
+ABI_VERSION = 1
+
+PXST_OK, PXST_EINVAL, PXST_ECUDA, PXST_ENOMEM = 0, 1, 2, 3
+
+
+class PxstScan(ctypes.Structure):
+    _fields_ = [("frames", c_void_p), ("n_frames", c_int64), ("ss", c_int64), ("fs", c_int64),
+                ("good", c_void_p), ("n_good", c_int64), ("w64", c_void_p), ("w32", c_void_p),
+                ("work", c_void_p), ("roi", c_int64 * 4)]
+
+
+class PxstStats(ctypes.Structure):
+    _fields_ = [("var_pm", c_void_p), ("sigma2", c_void_p), ("frame_norm", c_void_p),
+                ("scalars", c_void_p)]
+
+
+class PxstRef(ctypes.Structure):
+    _fields_ = [("fm", c_void_p), ("valid", c_void_p), ("os", c_int64), ("of", c_int64),
+                ("n0", c_int64), ("m0", c_int64)]
+
+
+_SIGS = {
+    "pxst_abi_version": (c_int, []),
+    "pxst_last_error": (c_char_p, []),
+    "pxst_launch_count": (c_int64, []),
+    "pxst_stack_stats": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_void_p]),
+    "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_object_splat": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
+                                  c_int64, c_int64, c_int64, c_int64, c_int64, c_double,
+                                  c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_object_finish": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_fixed_scale": (c_double, [c_double]),
+    "pxst_object_map": (c_int, [POINTER(PxstScan), POINTER(PxstStats), c_void_p, c_void_p,
+                                c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p]),
+    "pxst_pixel_map_search": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
+                                      c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                      c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_translation_search": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
+                                        c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                        c_double, c_int64, c_int64, c_void_p, c_void_p,
+                                        c_void_p, c_void_p]),
+    "pxst_error_maps": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p]),
+    "pxst_gather": (c_int, [POINTER(PxstRef), c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                            c_void_p]),
+    "pxst_splat": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                           c_void_p, c_int64, POINTER(c_int64), c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load and type the shared library (no CUDA device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"libpxst_b200.so not found at {path}; build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'`")
+        cdll = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(cdll, name)
+            fn.restype = res
+            fn.argtypes = args
+        if cdll.pxst_abi_version() != ABI_VERSION:
+            raise RuntimeError("libpxst_b200.so ABI version mismatch; rebuild it")
+        _lib = cdll
+        return cdll
+
+
+def lib() -> ctypes.CDLL:
+    """The library, with a CUDA device required (no CPU fallback exists)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2003_12726_b200 needs a CUDA (B200) device; none is visible")
+    return load_library()
+
+
+def check(rc: int) -> None:
+    if rc == PXST_OK:
+        return
+    msg = (_lib.pxst_last_error() or b"").decode(errors="replace")
+    if rc == PXST_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"pxst CUDA error ({rc}): {msg}")
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(load_library().pxst_launch_count())

@@ -1,0 +1,27 @@
+// C ABI glue: thread-local error string, status codes, launch counter.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace pxst {
+namespace {
+thread_local char g_err[1024] = "";
+thread_local int64_t g_launches = 0;
+}  // namespace
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+}  // namespace pxst
+
+extern "C" int pxst_abi_version(void) { return PXST_ABI_VERSION; }
+extern "C" const char* pxst_last_error(void) { return pxst::g_err; }
+extern "C" int64_t pxst_launch_count(void) { return pxst::g_launches; }

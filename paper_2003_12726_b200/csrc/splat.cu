@@ -1,0 +1,261 @@
+// K1 object formation (recon.py:99-141) and the interp primitives
+// (interp.py:53-135).
+//
+// The reference accumulates the bilinear splat in float64 with np.bincount
+// (interp.py:114-122), deterministic by construction.  Here every corner
+// contribution is rounded once to int64 fixed point (power-of-two scale
+// chosen from the total absolute mass so that no cell can overflow) and
+// added with a native 64-bit RED.ADD.  Integer addition is associative, so
+// the result is bit-reproducible regardless of thread order and identical
+// after an integer all-reduce over frame shards (multi-GPU).  Relative error
+// vs the float64 reference is ~1e-12 on populated cells, far inside the
+// 1e-5 object-map bar.
+#include "common.cuh"
+
+namespace pxst {
+namespace {
+
+constexpr int kTC = 128;        // threads per block along fs
+constexpr int kFrameChunk = 16; // frames per block (grid.z)
+
+// One thread per work pixel, looping over a chunk of good frames.  Lanes of
+// a warp are consecutive fs pixels, so the corner REDs of a warp land on a
+// few consecutive cells (the cheap, row-coalesced atomic pattern).
+__global__ void __launch_bounds__(kTC)
+k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
+               const double* __restrict__ dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
+               int64_t frame_lo, int64_t frame_hi, double num_scale, double den_scale,
+               int64_t* __restrict__ num, int64_t* __restrict__ den,
+               unsigned long long* __restrict__ n_drop) {
+  const int64_t c = sc.roi[2] + blockIdx.x * (int64_t)kTC + threadIdx.x;
+  const int64_t r = sc.roi[0] + blockIdx.y;
+  const int64_t k_lo = frame_lo + (int64_t)blockIdx.z * kFrameChunk;
+  const int64_t k_hi = min(frame_hi, k_lo + kFrameChunk);
+  if (c >= sc.roi[3]) return;
+  const int64_t p = r * sc.fs + c;
+  if (!sc.work[p]) return;
+  const int64_t plane = sc.ss * sc.fs;
+  const double u0 = u[p], u1 = u[plane + p];
+  const double w = sc.w64[p];
+  const double w2 = w * w;                       // recon.py:136
+  unsigned long long dropped = 0;
+  for (int64_t k = k_lo; k < k_hi; ++k) {
+    const int64_t f = sc.good[k];
+    const double x = u0 - __ldg(di + f) - static_cast<double>(n0);   // recon.py:138
+    const double y = u1 - __ldg(dj + f) - static_cast<double>(m0);
+    if (!(x >= 0.0 && x <= static_cast<double>(os - 1) && y >= 0.0 &&
+          y <= static_cast<double>(of - 1))) {   // interp.py:103-107
+      ++dropped;
+      continue;
+    }
+    const Split sx = split(x), sy = split(y);
+    const double I = static_cast<double>(__ldg(sc.frames + f * plane + p));
+    const double vw = (I / w) * w2;              // value * weight (interp.py:112)
+    const int r0 = sx.i, c0 = sy.i;
+    const int r1 = min(r0 + 1, static_cast<int>(os - 1));
+    const int c1 = min(c0 + 1, static_cast<int>(of - 1));
+    const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
+    const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
+    const int64_t cell[4] = {(int64_t)r0 * of + c0, (int64_t)r0 * of + c1,
+                             (int64_t)r1 * of + c0, (int64_t)r1 * of + c1};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red_add(num + cell[q], to_fixed(vw * cw[q] * num_scale));
+      red_add(den + cell[q], to_fixed(w2 * cw[q] * den_scale));
+    }
+  }
+  if (n_drop && dropped) atomicAdd(n_drop, dropped);
+}
+
+// Normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0.
+__global__ void k_object_finish(const int64_t* __restrict__ num, const int64_t* __restrict__ den,
+                                int64_t n, double inv_num_scale, double inv_den_scale,
+                                double* i_ref, double* wsum, float* fm, uint8_t* valid) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double vv = static_cast<double>(num[q]) * inv_num_scale;
+    const double ww = static_cast<double>(den[q]) * inv_den_scale;
+    const bool ok = ww > 0.0;
+    const double out = ok ? vv / ww : 0.0;
+    if (i_ref) i_ref[q] = out;
+    if (wsum) wsum[q] = ww;
+    if (fm) fm[q] = static_cast<float>(out);
+    if (valid) valid[q] = ok ? 1 : 0;
+  }
+}
+
+__global__ void k_gather(pxst_ref ref, const double* __restrict__ x, const double* __restrict__ y,
+                         int64_t n, double* vals, uint8_t* ok) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double xx = x[q], yy = y[q];
+    float v = 0.f;
+    bool good = false;
+    if (isfinite(xx) && isfinite(yy) && fabs(xx) < 2e9 && fabs(yy) < 2e9) {
+      const Split sx = split(xx), sy = split(yy);
+      good = masked_read(ref.fm, ref.valid, ref.os, ref.of, sx.i, sy.i, sx.f, sy.f, v);
+    }
+    vals[q] = good ? static_cast<double>(v) : 0.0;
+    ok[q] = good ? 1 : 0;
+  }
+}
+
+__global__ void k_splat_f64(double* acc_v, double* acc_w, int64_t os, int64_t of,
+                            const double* __restrict__ x, const double* __restrict__ y,
+                            const double* __restrict__ value, const double* __restrict__ weight,
+                            int64_t n, unsigned long long* n_drop) {
+  unsigned long long dropped = 0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double xx = x[q], yy = y[q];
+    if (!(xx >= 0.0 && xx <= static_cast<double>(os - 1) && yy >= 0.0 &&
+          yy <= static_cast<double>(of - 1))) {
+      ++dropped;
+      continue;
+    }
+    const Split sx = split(xx), sy = split(yy);
+    const double wt = weight ? weight[q] : 1.0;
+    const double vw = value[q] * wt;
+    const int r0 = sx.i, c0 = sy.i;
+    const int r1 = min(r0 + 1, static_cast<int>(os - 1));
+    const int c1 = min(c0 + 1, static_cast<int>(of - 1));
+    const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
+    const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
+    const int64_t cell[4] = {(int64_t)r0 * of + c0, (int64_t)r0 * of + c1,
+                             (int64_t)r1 * of + c0, (int64_t)r1 * of + c1};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      atomicAdd(acc_v + cell[k], vw * cw[k]);
+      atomicAdd(acc_w + cell[k], wt * cw[k]);
+    }
+  }
+  if (dropped) atomicAdd(n_drop, dropped);
+}
+
+int grid_1d(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+int check_scan(const pxst_scan* sc);
+
+int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
+                        const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
+                        int64_t frame_lo, int64_t frame_hi, double num_scale, double den_scale,
+                        int64_t* num, int64_t* den, unsigned long long* n_drop,
+                        cudaStream_t s) {
+  const int64_t nk = frame_hi - frame_lo;
+  if (nk <= 0) return PXST_OK;
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
+  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)rw,
+         (unsigned)((nk + kFrameChunk - 1) / kFrameChunk));
+  k_object_splat<<<g, kTC, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi,
+                                   num_scale, den_scale, num, den, n_drop);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+int launch_object_finish(const int64_t* num, const int64_t* den, int64_t n, double num_scale,
+                         double den_scale, double* i_ref, double* wsum, float* fm,
+                         uint8_t* valid, cudaStream_t s) {
+  k_object_finish<<<grid_1d(n, 256), 256, 0, s>>>(num, den, n, 1.0 / num_scale,
+                                                  1.0 / den_scale, i_ref, wsum, fm, valid);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+}  // namespace pxst
+
+using namespace pxst;
+
+extern "C" double pxst_fixed_scale(double mass) {
+  // Largest power of two with mass * scale <= 2^61: every cell total and the
+  // per-contribution rounding (<= 0.5 each) then stay below 2^62.
+  if (!(mass > 0.0) || !isfinite(mass)) return 1.0;
+  int e;
+  frexp(mass, &e);  // mass in [2^(e-1), 2^e)
+  return ldexp(1.0, 61 - e);
+}
+
+extern "C" int pxst_object_splat(const pxst_scan* sc, const double* u, const double* di,
+                                 const double* dj, int64_t n0, int64_t m0, int64_t os,
+                                 int64_t of, int64_t frame_lo, int64_t frame_hi, double num_scale,
+                                 double den_scale, int64_t* num_fx, int64_t* den_fx,
+                                 unsigned long long* n_dropped, void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(u && di && dj && num_fx && den_fx, "NULL pointer");
+  PXST_REQUIRE(os > 0 && of > 0 && os * of < (int64_t(1) << 40), "bad grid shape");
+  PXST_REQUIRE(0 <= frame_lo && frame_lo <= frame_hi && frame_hi <= sc->n_good,
+               "bad frame range");
+  return launch_object_splat(sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, num_scale,
+                             den_scale, num_fx, den_fx, n_dropped, as_stream(stream));
+}
+
+extern "C" int pxst_object_finish(const int64_t* num_fx, const int64_t* den_fx, int64_t n,
+                                  double num_scale, double den_scale, double* i_ref,
+                                  double* wsum, float* fm, uint8_t* valid, void* stream) {
+  PXST_REQUIRE(num_fx && den_fx && n > 0, "bad accumulators");
+  return launch_object_finish(num_fx, den_fx, n, num_scale, den_scale, i_ref, wsum, fm, valid,
+                              as_stream(stream));
+}
+
+extern "C" int pxst_object_map(const pxst_scan* sc, const pxst_stats* st, const double* u,
+                               const double* di, const double* dj, int64_t n0, int64_t m0,
+                               int64_t os, int64_t of, double* i_ref, double* wsum, float* fm,
+                               uint8_t* valid, void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(st && st->scalars, "stats descriptor is NULL");
+  PXST_REQUIRE(os > 0 && of > 0 && os * of < (int64_t(1) << 40), "bad grid shape");
+  cudaStream_t s = as_stream(stream);
+  double sc4[4];
+  PXST_CHECK_CUDA(cudaMemcpyAsync(sc4, st->scalars, sizeof(sc4), cudaMemcpyDeviceToHost, s));
+  PXST_CHECK_CUDA(cudaStreamSynchronize(s));
+  const double num_scale = pxst_fixed_scale(sc4[1]);
+  const double den_scale =
+      pxst_fixed_scale(sc4[0] * sc4[0] * sc4[2] * static_cast<double>(sc->n_good));
+  const int64_t n = os * of;
+  Scratch acc;
+  if (int e = acc.alloc(sizeof(int64_t) * 2 * n, s)) return e;
+  int64_t* num = acc.as<int64_t>();
+  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 2 * n, s));
+  if (int e = launch_object_splat(sc, u, di, dj, n0, m0, os, of, 0, sc->n_good, num_scale,
+                                  den_scale, num, num + n, nullptr, s))
+    return e;
+  return launch_object_finish(num, num + n, n, num_scale, den_scale, i_ref, wsum, fm, valid, s);
+}
+
+extern "C" int pxst_gather(const pxst_ref* ref, const double* x, const double* y, int64_t n,
+                           double* vals, uint8_t* ok, void* stream) {
+  PXST_REQUIRE(ref && ref->fm && ref->valid && ref->os > 0 && ref->of > 0, "bad reference");
+  PXST_REQUIRE(x && y && vals && ok, "NULL pointer");
+  if (n <= 0) return PXST_OK;
+  k_gather<<<grid_1d(n, 256), 256, 0, as_stream(stream)>>>(*ref, x, y, n, vals, ok);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+extern "C" int pxst_splat(double* acc_v, double* acc_w, int64_t os, int64_t of, const double* x,
+                          const double* y, const double* value, const double* weight, int64_t n,
+                          int64_t* n_dropped, void* stream) {
+  PXST_REQUIRE(acc_v && acc_w && os > 0 && of > 0, "bad accumulators");
+  PXST_REQUIRE(x && y && value, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  Scratch cnt;
+  if (int e = cnt.alloc(sizeof(unsigned long long), s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), s));
+  if (n > 0) {
+    k_splat_f64<<<grid_1d(n, 256), 256, 0, s>>>(acc_v, acc_w, os, of, x, y, value, weight, n,
+                                                 cnt.as<unsigned long long>());
+    PXST_CHECK_LAUNCH();
+  }
+  unsigned long long h = 0;
+  PXST_CHECK_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  PXST_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (n_dropped) *n_dropped = static_cast<int64_t>(h);
+  return PXST_OK;
+}

@@ -1,0 +1,265 @@
+// K0 stack statistics and bbox reductions.
+//
+// var_pm      recon.py:257-260   sum_n (I-W)^2 (times fw when given)
+// sigma2      recon.py:410-412   population variance over good frames,
+//                                floored at 1e-8 * max(W_work)^2
+// frame_norm  recon.py:367       sum_p (I_n - W)^2
+// bbox        recon.py:126-132   min/max of u over work px, of di/dj over good frames
+#include "common.cuh"
+
+namespace pxst {
+namespace {
+
+constexpr int kThreads = 256;
+
+// Deterministic block reduction helpers (fixed tree).
+template <class T, class Op>
+__device__ T block_reduce(T v, Op op, T* sh) {
+  const T ident = Op::identity();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < nw ? sh[lane] : ident;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;  // valid in thread 0
+}
+
+struct Sum {
+  __device__ static double identity() { return 0.0; }
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+struct Min {
+  __device__ static double identity() { return INFINITY; }
+  __device__ double operator()(double a, double b) const { return fmin(a, b); }
+};
+struct Max {
+  __device__ static double identity() { return -INFINITY; }
+  __device__ double operator()(double a, double b) const { return fmax(a, b); }
+};
+
+// Block partials of max W and work-pixel count over the ROI rectangle.
+__global__ void k_wmax_partial(pxst_scan sc, double* part_max, double* part_cnt) {
+  __shared__ double sh[32];
+  const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
+  const int64_t n = rw * cw;
+  double mx = -INFINITY, cnt = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = sc.roi[0] + k / cw, c = sc.roi[2] + k % cw;
+    const int64_t p = r * sc.fs + c;
+    if (sc.work[p]) { mx = fmax(mx, sc.w64[p]); cnt += 1; }
+  }
+  mx = block_reduce(mx, Max(), sh);
+  cnt = block_reduce(cnt, Sum(), sh);
+  if (threadIdx.x == 0) { part_max[blockIdx.x] = mx; part_cnt[blockIdx.x] = cnt; }
+}
+
+__global__ void k_wmax_final(const double* part_max, const double* part_cnt, int nb,
+                             double* scalars) {
+  __shared__ double sh[32];
+  double mx = -INFINITY, cnt = 0;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) { mx = fmax(mx, part_max[k]); cnt += part_cnt[k]; }
+  mx = block_reduce(mx, Max(), sh);
+  cnt = block_reduce(cnt, Sum(), sh);
+  if (threadIdx.x == 0) {
+    scalars[0] = cnt > 0 ? mx : 1.0;   // recon.py:411 uses 1.0 for an empty set
+    scalars[2] = cnt;
+  }
+}
+
+// Per-pixel statistics: one thread per ROI pixel, sequential over good
+// frames (the same order as numpy's axis-0 reduction).
+__global__ void k_pixel_stats(pxst_scan sc, const float* __restrict__ fw,
+                              const double* __restrict__ scalars, double* var_pm,
+                              double* sigma2) {
+  const int64_t c = sc.roi[2] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = sc.roi[0] + blockIdx.y;
+  if (c >= sc.roi[3]) return;
+  const int64_t p = r * sc.fs + c;
+  if (!sc.work[p]) return;
+  const double w = sc.w64[p];
+  const int64_t plane = sc.ss * sc.fs;
+  double vs = 0.0, sum = 0.0;
+  for (int64_t k = 0; k < sc.n_good; ++k) {
+    const int64_t f = sc.good[k];
+    const double I = static_cast<double>(__ldg(sc.frames + f * plane + p));
+    const double d = I - w;
+    double t = d * d;
+    if (fw) t = static_cast<double>(__ldg(fw + f * plane + p)) * t;
+    vs += t;
+    sum += I;
+  }
+  const double mean = sum / static_cast<double>(sc.n_good);
+  double ss = 0.0;
+  for (int64_t k = 0; k < sc.n_good; ++k) {
+    const int64_t f = sc.good[k];
+    const double d = static_cast<double>(__ldg(sc.frames + f * plane + p)) - mean;
+    ss += d * d;
+  }
+  const double wmax = scalars[0];
+  const double floor_ = 1e-8 * wmax * wmax;
+  var_pm[p] = vs;
+  sigma2[p] = fmax(ss / static_cast<double>(sc.n_good), floor_);
+}
+
+// Per-frame normaliser and |I|W mass: one block per good frame.
+__global__ void k_frame_stats(pxst_scan sc, double* frame_norm, double* frame_iw,
+                              double* frame_i) {
+  __shared__ double sh[32];
+  const int64_t k = blockIdx.x;
+  const int64_t f = sc.good[k];
+  const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
+  const int64_t n = rw * cw;
+  const float* fr = sc.frames + f * sc.ss * sc.fs;
+  double acc = 0.0, iw = 0.0, ia = 0.0;
+  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
+    const int64_t p = (sc.roi[0] + q / cw) * sc.fs + sc.roi[2] + q % cw;
+    if (!sc.work[p]) continue;
+    const double I = static_cast<double>(__ldg(fr + p));
+    const double d = I - sc.w64[p];
+    acc += d * d;
+    iw += fabs(I) * sc.w64[p];
+    ia += fabs(I);
+  }
+  acc = block_reduce(acc, Sum(), sh);
+  iw = block_reduce(iw, Sum(), sh);
+  ia = block_reduce(ia, Sum(), sh);
+  if (threadIdx.x == 0) { frame_norm[k] = acc; frame_iw[k] = iw; frame_i[k] = ia; }
+}
+
+__global__ void k_sum_final(const double* a, const double* b, int64_t n, double* out_a,
+                            double* out_b) {
+  __shared__ double sh[32];
+  double sa = 0, sb = 0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) { sa += a[k]; sb += b[k]; }
+  sa = block_reduce(sa, Sum(), sh);
+  sb = block_reduce(sb, Sum(), sh);
+  if (threadIdx.x == 0) { *out_a = sa; *out_b = sb; }
+}
+
+// bbox partials over work pixels: min/max of u0, u1.
+__global__ void k_bbox_partial(pxst_scan sc, const double* __restrict__ u, double* part) {
+  __shared__ double sh[32];
+  const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
+  const int64_t n = rw * cw, plane = sc.ss * sc.fs;
+  double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = (sc.roi[0] + k / cw) * sc.fs + sc.roi[2] + k % cw;
+    if (!sc.work[p]) continue;
+    const double x = u[p], y = u[plane + p];
+    a0 = fmin(a0, x); b0 = fmax(b0, x); a1 = fmin(a1, y); b1 = fmax(b1, y);
+  }
+  a0 = block_reduce(a0, Min(), sh);
+  b0 = block_reduce(b0, Max(), sh);
+  a1 = block_reduce(a1, Min(), sh);
+  b1 = block_reduce(b1, Max(), sh);
+  if (threadIdx.x == 0) {
+    double* o = part + 4 * blockIdx.x;
+    o[0] = a0; o[1] = b0; o[2] = a1; o[3] = b1;
+  }
+}
+
+__global__ void k_bbox_final(pxst_scan sc, const double* part, int nb, const double* di,
+                             const double* dj, double* out) {
+  __shared__ double sh[32];
+  double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
+  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
+    a0 = fmin(a0, part[4 * k]); b0 = fmax(b0, part[4 * k + 1]);
+    a1 = fmin(a1, part[4 * k + 2]); b1 = fmax(b1, part[4 * k + 3]);
+  }
+  double c0 = INFINITY, d0 = -INFINITY, c1 = INFINITY, d1 = -INFINITY;
+  for (int64_t k = threadIdx.x; k < sc.n_good; k += blockDim.x) {
+    const int64_t f = sc.good[k];
+    c0 = fmin(c0, di[f]); d0 = fmax(d0, di[f]); c1 = fmin(c1, dj[f]); d1 = fmax(d1, dj[f]);
+  }
+  a0 = block_reduce(a0, Min(), sh); b0 = block_reduce(b0, Max(), sh);
+  a1 = block_reduce(a1, Min(), sh); b1 = block_reduce(b1, Max(), sh);
+  c0 = block_reduce(c0, Min(), sh); d0 = block_reduce(d0, Max(), sh);
+  c1 = block_reduce(c1, Min(), sh); d1 = block_reduce(d1, Max(), sh);
+  if (threadIdx.x == 0) {
+    out[0] = a0; out[1] = b0; out[2] = a1; out[3] = b1;
+    out[4] = c0; out[5] = d0; out[6] = c1; out[7] = d1;
+  }
+}
+
+int partial_blocks(const pxst_scan* sc) {
+  const int64_t n = (sc->roi[1] - sc->roi[0]) * (sc->roi[3] - sc->roi[2]);
+  int64_t nb = (n + kThreads * 8 - 1) / (kThreads * 8);
+  if (nb < 1) nb = 1;
+  if (nb > 1184) nb = 1184;  // 8 x 148 SMs
+  return static_cast<int>(nb);
+}
+
+}  // namespace
+
+int check_scan(const pxst_scan* sc) {
+  PXST_REQUIRE(sc != nullptr, "scan descriptor is NULL");
+  PXST_REQUIRE(sc->frames && sc->good && sc->w64 && sc->w32 && sc->work,
+               "scan descriptor has a NULL device pointer");
+  PXST_REQUIRE(sc->n_frames > 0 && sc->ss > 0 && sc->fs > 0, "empty frame stack");
+  PXST_REQUIRE(sc->n_good >= 0 && sc->n_good <= sc->n_frames, "bad n_good");
+  PXST_REQUIRE(0 <= sc->roi[0] && sc->roi[0] < sc->roi[1] && sc->roi[1] <= sc->ss &&
+                   0 <= sc->roi[2] && sc->roi[2] < sc->roi[3] && sc->roi[3] <= sc->fs,
+               "empty or out-of-range ROI");
+  PXST_REQUIRE(sc->ss * sc->fs < (int64_t(1) << 31), "detector too large");
+  return PXST_OK;
+}
+
+}  // namespace pxst
+
+using namespace pxst;
+
+extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst_stats* st,
+                                void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(st && st->var_pm && st->sigma2 && st->frame_norm && st->scalars,
+               "stats descriptor has a NULL pointer");
+  PXST_REQUIRE(sc->n_good > 0, "no good frames");
+  cudaStream_t s = as_stream(stream);
+  const int64_t plane = sc->ss * sc->fs;
+  PXST_CHECK_CUDA(cudaMemsetAsync(st->var_pm, 0, sizeof(double) * plane, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(st->sigma2, 0, sizeof(double) * plane, s));
+  const int nb = partial_blocks(sc);
+  Scratch part;
+  if (int e = part.alloc(sizeof(double) * (2 * nb + 3 * sc->n_good), s)) return e;
+  double* pm = part.as<double>();
+  double* pc = pm + nb;
+  double* fiw = pc + nb;
+  double* fi = fiw + sc->n_good;
+  k_wmax_partial<<<nb, kThreads, 0, s>>>(*sc, pm, pc);
+  PXST_CHECK_LAUNCH();
+  k_wmax_final<<<1, 1024, 0, s>>>(pm, pc, nb, st->scalars);
+  PXST_CHECK_LAUNCH();
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  dim3 g((unsigned)((cw + 127) / 128), (unsigned)rw);
+  PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
+  k_pixel_stats<<<g, 128, 0, s>>>(*sc, fw, st->scalars, st->var_pm, st->sigma2);
+  PXST_CHECK_LAUNCH();
+  k_frame_stats<<<(unsigned)sc->n_good, 512, 0, s>>>(*sc, st->frame_norm, fiw, fi);
+  PXST_CHECK_LAUNCH();
+  k_sum_final<<<1, 1024, 0, s>>>(fiw, fi, sc->n_good, st->scalars + 1, st->scalars + 3);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+extern "C" int pxst_bbox(const pxst_scan* sc, const double* u, const double* di,
+                         const double* dj, double* out, void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(u && di && dj && out, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  const int nb = partial_blocks(sc);
+  Scratch part;
+  if (int e = part.alloc(sizeof(double) * 4 * nb, s)) return e;
+  k_bbox_partial<<<nb, kThreads, 0, s>>>(*sc, u, part.as<double>());
+  PXST_CHECK_LAUNCH();
+  k_bbox_final<<<1, 1024, 0, s>>>(*sc, part.as<double>(), nb, di, dj, out);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}

@@ -1,0 +1,334 @@
+"""Device-resident state of one scan and thin wrappers over the C ABI.
+
+``DeviceScan`` owns the device copies (torch CUDA tensors -- torch is only
+the allocator/stream plumbing) of one scan's frame stack, whitefield, work
+mask and good-frame list, plus the iteration-invariant statistics (K0), and
+exposes one method per kernel family:
+
+==========================  =======================  ===========================
+method                      C entry point            reference
+==========================  =======================  ===========================
+``object_map``              pxst_bbox, pxst_object_  recon.make_reference
+                            splat/finish             (recon.py:99-141)
+``pixel_map_search``        pxst_pixel_map_search    recon.update_pixel_map
+                                                     (recon.py:221-315)
+``translation_search``      pxst_translation_search  recon.update_translations
+                                                     (recon.py:336-385)
+``error_maps``              pxst_error_maps          recon.calc_error
+                                                     (recon.py:388-438)
+==========================  =======================  ===========================
+
+Work-set semantics follow ``recon._work_set`` (recon.py:81-96): good frames
+are ``np.flatnonzero(good_frames)``; work pixels are ``mask & (W > 0)``
+inside the half-open ROI (numpy-slice clipped to the detector).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import PxstRef, PxstScan, PxstStats, check, stream_ptr
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _device() -> torch.device:
+    _native.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
+    """Host -> device copy of a contiguous array in the requested dtype."""
+    h = np.ascontiguousarray(a, dtype=dtype)
+    t = torch.from_numpy(h)
+    if t.is_pinned():
+        return t.to(device, non_blocking=True)
+    return t.to(device)
+
+
+def clip_roi(roi, shape) -> tuple[int, int, int, int]:
+    """ROI as numpy slicing would apply it (recon.py:84-85)."""
+    ss, fs = shape
+    if roi is None:
+        return 0, ss, 0, fs
+    r0, r1, c0, c1 = (int(v) for v in (roi.ss_min, roi.ss_max, roi.fs_min, roi.fs_max))
+    return min(r0, ss), min(r1, ss), min(c0, fs), min(c1, fs)
+
+
+@dataclass
+class DeviceRef:
+    """Reference image on device (f64 for the boundary, f32 masked for kernels)."""
+
+    i_ref: torch.Tensor | None   # [os, of] f64 (None when built from a host image)
+    wsum: torch.Tensor | None
+    fm: torch.Tensor             # [os, of] f32, 0 where invalid
+    valid: torch.Tensor          # [os, of] u8
+    origin: tuple[int, int]
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return tuple(self.fm.shape)
+
+    def struct(self) -> PxstRef:
+        os_, of = self.fm.shape
+        return PxstRef(self.fm.data_ptr(), self.valid.data_ptr(), os_, of, int(self.origin[0]),
+                       int(self.origin[1]))
+
+    @classmethod
+    def from_host(cls, i_ref, wsum, origin, device) -> "DeviceRef":
+        i_ref = np.asarray(i_ref, dtype=np.float64)
+        ok = np.asarray(wsum) > 0                      # data_model.py:186-188
+        fm = np.where(ok, i_ref, 0.0).astype(np.float32)
+        return cls(None, None, to_device(fm, np.float32, device),
+                   to_device(ok.astype(np.uint8), np.uint8, device),
+                   (int(origin[0]), int(origin[1])))
+
+
+class DeviceScan:
+    """One scan + whitefield + mask + ROI resident on the current CUDA device."""
+
+    def __init__(self, frames, good_frames, W, mask, roi=None, device=None,
+                 frames_dev: torch.Tensor | None = None):
+        self.device = device or _device()
+        self.lib = _native.lib()
+        frames_shape = tuple(frames_dev.shape) if frames_dev is not None else np.shape(frames)
+        if len(frames_shape) != 3:
+            raise ValueError("frames must be 3-D [N, SS, FS]")
+        self.n_frames, self.ss, self.fs = (int(v) for v in frames_shape)
+        self.roi = clip_roi(roi, (self.ss, self.fs))
+        r0, r1, c0, c1 = self.roi
+        W = np.asarray(W)
+        mask = np.asarray(mask)
+        work = np.zeros((self.ss, self.fs), dtype=np.uint8)
+        if r1 > r0 and c1 > c0:
+            work[r0:r1, c0:c1] = (mask[r0:r1, c0:c1] & (W[r0:r1, c0:c1] > 0)) != 0
+        self.n_work = int(work.sum())
+        self.good_idx = np.flatnonzero(np.asarray(good_frames)).astype(np.int32)
+        self.n_good = int(self.good_idx.size)
+        dev = self.device
+        if frames_dev is None:
+            frames_dev = to_device(frames, np.float32, dev)
+        self.frames = frames_dev
+        self.good = to_device(self.good_idx if self.n_good else np.zeros(1, np.int32), np.int32, dev)
+        self.w64 = to_device(W, np.float64, dev)
+        self.w32 = self.w64.to(torch.float32)
+        self.work = to_device(work, np.uint8, dev)
+        roi4 = (ctypes.c_int64 * 4)(r0, max(r1, r0 + 1), c0, max(c1, c0 + 1))
+        self.c_scan = PxstScan(self.frames.data_ptr(), self.n_frames, self.ss, self.fs,
+                               self.good.data_ptr(), self.n_good, self.w64.data_ptr(),
+                               self.w32.data_ptr(), self.work.data_ptr(), roi4)
+        self.empty = self.n_work == 0 or self.n_good == 0 or r1 <= r0 or c1 <= c0
+        plane = self.ss * self.fs
+        self.var_pm = torch.zeros(plane, dtype=torch.float64, device=dev)
+        self.sigma2 = torch.zeros(plane, dtype=torch.float64, device=dev)
+        self.frame_norm = torch.zeros(max(self.n_good, 1), dtype=torch.float64, device=dev)
+        self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.c_stats = PxstStats(self.var_pm.data_ptr(), self.sigma2.data_ptr(),
+                                 self.frame_norm.data_ptr(), self.scalars.data_ptr())
+        if not self.empty:
+            check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), None,
+                                            ctypes.byref(self.c_stats), stream_ptr()))
+            self.scalars_host = self.scalars.cpu().numpy().copy()
+        else:
+            self.scalars_host = np.array([1.0, 0.0, 0.0, 0.0])
+
+    # ------------------------------------------------------------------ utils
+    def upload_u(self, u) -> torch.Tensor:
+        u = np.asarray(u)
+        if u.shape != (2, self.ss, self.fs):
+            raise ValueError(f"pixel map must have shape (2, {self.ss}, {self.fs})")
+        return to_device(u, np.float64, self.device)
+
+    def upload_t(self, di, dj) -> tuple[torch.Tensor, torch.Tensor]:
+        di = np.asarray(di, dtype=np.float64)
+        dj = np.asarray(dj, dtype=np.float64)
+        if di.shape != (self.n_frames,) or dj.shape != (self.n_frames,):
+            raise ValueError(f"translations must have shape ({self.n_frames},)")
+        return to_device(di, np.float64, self.device), to_device(dj, np.float64, self.device)
+
+    # -------------------------------------------------------------- K1 object
+    def bbox(self, u_t, di_t, dj_t) -> tuple[int, int, tuple[int, int]]:
+        """Grid origin and shape by the rule of recon.py:126-132."""
+        out = torch.empty(8, dtype=torch.float64, device=self.device)
+        check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
+                                 dj_t.data_ptr(), out.data_ptr(), stream_ptr()))
+        u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = out.cpu().tolist()
+        n0 = int(math.floor(u0min - dimax))
+        m0 = int(math.floor(u1min - djmax))
+        shape = (int(math.floor(u0max - dimin)) - n0 + 2, int(math.floor(u1max - djmin)) - m0 + 2)
+        return n0, m0, shape
+
+    def fixed_scales(self) -> tuple[float, float]:
+        wmax, iw_mass, n_work, _ = (float(v) for v in self.scalars_host)
+        num = self.lib.pxst_fixed_scale(iw_mass)
+        den = self.lib.pxst_fixed_scale(wmax * wmax * n_work * self.n_good)
+        return num, den
+
+    def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
+                     acc: torch.Tensor | None = None) -> torch.Tensor:
+        """Fixed-point num/den accumulators [2, os*of] int64 for a frame range."""
+        os_, of = shape
+        if acc is None:
+            acc = torch.zeros((2, os_ * of), dtype=torch.int64, device=self.device)
+        hi = self.n_good if frame_hi is None else frame_hi
+        ns, ds = self.fixed_scales()
+        check(self.lib.pxst_object_splat(
+            ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0, m0,
+            os_, of, frame_lo, hi, ns, ds, acc[0].data_ptr(), acc[1].data_ptr(), None,
+            stream_ptr()))
+        return acc
+
+    def object_finish(self, acc, origin, shape) -> DeviceRef:
+        os_, of = shape
+        n = os_ * of
+        ns, ds = self.fixed_scales()
+        i_ref = torch.empty(n, dtype=torch.float64, device=self.device)
+        wsum = torch.empty(n, dtype=torch.float64, device=self.device)
+        fm = torch.empty(n, dtype=torch.float32, device=self.device)
+        valid = torch.empty(n, dtype=torch.uint8, device=self.device)
+        check(self.lib.pxst_object_finish(acc[0].data_ptr(), acc[1].data_ptr(), n, ns, ds,
+                                          i_ref.data_ptr(), wsum.data_ptr(), fm.data_ptr(),
+                                          valid.data_ptr(), stream_ptr()))
+        return DeviceRef(i_ref.view(os_, of), wsum.view(os_, of), fm.view(os_, of),
+                         valid.view(os_, of), (int(origin[0]), int(origin[1])))
+
+    def object_map(self, u_t, di_t, dj_t) -> DeviceRef:
+        if self.empty:
+            raise ValueError("make_reference: empty good pixel/frame set")  # recon.py:116-117
+        n0, m0, shape = self.bbox(u_t, di_t, dj_t)
+        acc = self.object_splat(u_t, di_t, dj_t, n0, m0, shape)
+        return self.object_finish(acc, (n0, m0), shape)
+
+    # ---------------------------------------------------------- K2 pixel map
+    def frame_weight_stats(self, fw_t: torch.Tensor) -> torch.Tensor:
+        var_fw = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        tmp_s2 = torch.zeros_like(var_fw)
+        fn = torch.zeros_like(self.frame_norm)
+        sc = torch.zeros_like(self.scalars)
+        st = PxstStats(var_fw.data_ptr(), tmp_s2.data_ptr(), fn.data_ptr(), sc.data_ptr())
+        check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), fw_t.data_ptr(),
+                                        ctypes.byref(st), stream_ptr()))
+        return var_fw
+
+    def pixel_map_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
+                         subpixel_grid=None, refine=True, fw_t=None):
+        u_out = torch.empty_like(u_t)
+        err = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        if self.empty:
+            u_out.copy_(u_t)
+            err.zero_()
+            return u_out, err.view(self.ss, self.fs)
+        var_fw = self.frame_weight_stats(fw_t) if fw_t is not None else None
+        c_ref = ref.struct()
+        check(self.lib.pxst_pixel_map_search(
+            ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+            u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), int(half_ss), int(half_fs),
+            float(subpixel_grid or 0.0), int(bool(refine)), _ptr(fw_t), _ptr(var_fw),
+            u_out.data_ptr(), err.data_ptr(), stream_ptr()))
+        return u_out, err.view(self.ss, self.fs)
+
+    # ------------------------------------------------------- K3 translations
+    def translation_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
+                           subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None):
+        di_out = di_t.clone()
+        dj_out = dj_t.clone()
+        if self.empty:
+            return di_out, dj_out
+        hi = self.n_good if frame_hi is None else frame_hi
+        c_ref = ref.struct()
+        check(self.lib.pxst_translation_search(
+            ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+            u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), int(half_ss), int(half_fs),
+            float(subpixel_grid or 0.0), int(frame_lo), int(hi), di_out.data_ptr(),
+            dj_out.data_ptr(), _ptr(err_out), stream_ptr()))
+        return di_out, dj_out
+
+    # ---------------------------------------------------------- K4 error maps
+    def error_maps(self, ref: DeviceRef, u_t, di_t, dj_t):
+        per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)
+        per_pixel = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        plane = torch.zeros(ref.fm.numel(), dtype=torch.float64, device=self.device)
+        total = torch.zeros(1, dtype=torch.float64, device=self.device)
+        if not self.empty:
+            c_ref = ref.struct()
+            check(self.lib.pxst_error_maps(
+                ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+                u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
+                per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), stream_ptr()))
+        return (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
+                self.sigma2.view(self.ss, self.fs))
+
+
+# ---------------------------------------------------------------------------
+# identity cache of device scans (value-object convention, data_model.py:13)
+# ---------------------------------------------------------------------------
+class _ScanCache:
+    """Caches DeviceScan objects keyed by the identity of the host arrays.
+
+    The reference treats its dataclasses as immutable value objects
+    (data_model.py:13: "construct once, then share read-only"); the cache
+    relies on that: an array mutated in place after a call must be passed as
+    a new array, or the cache cleared with :func:`clear_cache`.  W, mask and
+    good_frames (small) are additionally checked by content.
+    """
+
+    def __init__(self, max_entries: int = 2):
+        self.entries: list[tuple[tuple, list, DeviceScan]] = []
+        self.max_entries = max_entries
+        self.enabled = True
+
+    @staticmethod
+    def _ident(a):
+        a = np.asarray(a)
+        return (id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str, a.strides)
+
+    @staticmethod
+    def _digest(a):
+        a = np.ascontiguousarray(a)
+        return hash(a.tobytes())
+
+    def get(self, scan, w, m, roi) -> DeviceScan:
+        frames = scan.frames
+        key = (self._ident(frames), self._digest(scan.good_frames), self._digest(w.w),
+               self._digest(m.mask), None if roi is None else clip_roi(roi, scan.shape))
+        if self.enabled:
+            for k, refs, ds in self.entries:
+                if k == key and all(r() is not None for r in refs):
+                    return ds
+        frames_dev = None
+        if self.enabled:
+            # reuse an uploaded stack when only W / mask / ROI / good frames differ
+            for k, refs, ds in self.entries:
+                if k[0] == key[0] and refs[0]() is not None:
+                    frames_dev = ds.frames
+                    break
+        ds = DeviceScan(frames, scan.good_frames, w.w, m.mask, roi, frames_dev=frames_dev)
+        if self.enabled:
+            refs = []
+            try:
+                refs.append(weakref.ref(frames))
+            except TypeError:
+                refs.append(lambda: frames)
+            self.entries.append((key, refs, ds))
+            del self.entries[:-self.max_entries]
+        return ds
+
+    def clear(self):
+        self.entries.clear()
+
+
+SCAN_CACHE = _ScanCache()
+
+
+def clear_cache() -> None:
+    SCAN_CACHE.clear()
+    torch.cuda.empty_cache()

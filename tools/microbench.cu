@@ -1,0 +1,237 @@
+// Pipe-rate microbenchmarks for the PXST kernel design on B200 (sm_100a).
+// Measures: FFMA (3-register form), FFMA2 (packed f32x2), LDS.32 and LDS.128
+// shared-memory bandwidth, REDG.ADD (u64 and f64) spread-address throughput,
+// and DFMA. Prints one JSON object. Build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); return 1; } } while (0)
+
+constexpr int CH = 16;
+
+__global__ void k_ffma(float* out, float b, float c, int iters) {
+  float a[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) a[i] = fmaf(a[i], b, c + 0.0f * a[(i + 1) % CH]);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// acc_i = fma(r_i, r_i, acc_i) with r_i = fma(-A, h_i, I): the trial kernel's mix.
+__global__ void k_ffma_mix(float* out, float A, float I, int iters) {
+  float acc[CH], h[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) { acc[i] = 0.f; h[i] = threadIdx.x * 1e-3f + i; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      float r = fmaf(-A, h[i], I);
+      acc[i] = fmaf(r, r, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < CH; ++i) h[i] = h[i] * 0.999f;
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+
+__global__ void k_ffma2(float* out, float b, float c, int iters) {
+  unsigned long long a[CH / 2];
+  float2 bb = make_float2(b, b), cc = make_float2(c, c);
+  unsigned long long br = f2u(bb), cr = f2u(cc);
+#pragma unroll
+  for (int i = 0; i < CH / 2; ++i) a[i] = f2u(make_float2(threadIdx.x * 1e-3f + i, i + 0.5f));
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < CH / 2; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(br), "l"(cr));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < CH / 2; ++i) { float2 v = u2f(a[i]); s += v.x + v.y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_dfma(double* out, double b, double c, int iters) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// Each lane reads its own conflict-free word: bank = lane.
+__global__ void k_lds32(float* out, int iters, int stride) {
+  __shared__ float sm[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) sm[i] = i * 0.5f;
+  __syncthreads();
+  float s = 0;
+  int base = (threadIdx.x & 31) + (threadIdx.x >> 5) * 32;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += sm[(base + (it * 16 + k) * stride) & 8191];
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_lds128(float* out, int iters) {
+  __shared__ float4 sm[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = make_float4(i, i + 1, i + 2, i + 3);
+  __syncthreads();
+  float s = 0;
+  int base = threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) { float4 v = sm[(base + (it * 16 + k) * 64) & 2047]; s += v.x + v.w; }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_red64(unsigned long long* acc, int n_cells, int iters) {
+  unsigned int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    unsigned int h = (tid * 2654435761u + it * 40503u) % n_cells;
+    atomicAdd(&acc[h], 1ull);
+  }
+}
+
+__global__ void k_redf64(double* acc, int n_cells, int iters) {
+  unsigned int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    unsigned int h = (tid * 2654435761u + it * 40503u) % n_cells;
+    atomicAdd(&acc[h], 1.0);
+  }
+}
+
+// Coalesced row-contiguous atomics (neighbouring lanes hit neighbouring cells),
+// the pattern of a bilinear splat along a detector row.
+__global__ void k_redf64_rows(double* acc, int n_cells, int iters) {
+  unsigned int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    unsigned int h = ((tid >> 5) * 977u + it * 131u) * 32u % (n_cells - 64) + (threadIdx.x & 31);
+    atomicAdd(&acc[h], 1.0);
+  }
+}
+
+
+__global__ void k_lds_cyc(float* out, long long* cyc, int iters, int mode) {
+  __shared__ float sm[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) sm[i] = i * 0.5f;
+  __syncthreads();
+  long long t0 = clock64();
+  float s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float* p = sm + w * 64 + lane;
+  if (mode == 0) {
+    for (int it = 0; it < iters; ++it) {
+      const float* q = p + ((it * 256) & 4095);
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) { s0 += q[k * 64]; s1 += q[k * 64 + 64]; s2 += q[k * 64 + 128]; s3 += q[k * 64 + 192]; }
+    }
+  } else if (mode == 1) {
+    const float2* p2 = reinterpret_cast<const float2*>(sm) + w * 32 + lane;
+    for (int it = 0; it < iters; ++it) {
+      const float2* q = p2 + ((it * 128) & 2047);
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) { float2 a = q[k * 64]; float2 b = q[k * 64 + 64]; s0 += a.x; s1 += a.y; s2 += b.x; s3 += b.y; }
+    }
+  } else {
+    const float4* p4 = reinterpret_cast<const float4*>(sm) + w * 32 + lane;
+    for (int it = 0; it < iters; ++it) {
+      const float4* q = p4 + ((it * 64) & 1023);
+#pragma unroll
+      for (int k = 0; k < 4; k += 1) { float4 a = q[k * 128]; s0 += a.x; s1 += a.y; s2 += a.z; s3 += a.w; }
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s0 + s1 + s2 + s3;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+int main() {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  int sms = prop.multiProcessorCount;
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  float* fout; double* dout;
+  CK(cudaMalloc(&fout, sizeof(float) * sms * 64 * 1024));
+  CK(cudaMalloc(&dout, sizeof(double) * sms * 64 * 1024));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float ms;
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_khz_attr\": %d", prop.name, sms, clk_khz);
+
+  auto timeit = [&](auto launch) -> float {
+    launch(); cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    for (int r = 0; r < 3; ++r) launch();
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float t; cudaEventElapsedTime(&t, e0, e1); return t / 3;
+  };
+  const int threads = 256, blocks = sms * 8, iters = 4096;
+  double lanes = double(blocks) * threads;
+  ms = timeit([&] { k_ffma<<<blocks, threads>>>(fout, 0.999f, 1e-4f, iters); });
+  printf(", \"ffma_tflops\": %.2f", lanes * iters * CH * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_ffma_mix<<<blocks, threads>>>(fout, 0.5f, 3.0f, iters / 2); });
+  printf(", \"ffma_mix_tflops\": %.2f", lanes * (iters / 2) * (CH * 2 + CH) * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_ffma2<<<blocks, threads>>>(fout, 0.999f, 1e-4f, iters); });
+  printf(", \"ffma2_tflops\": %.2f", lanes * iters * CH * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_dfma<<<blocks, threads>>>(dout, 0.999, 1e-4, iters / 8); });
+  printf(", \"dfma_tflops\": %.2f", lanes * (iters / 8) * 8 * 2 / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_lds32<<<blocks, threads>>>(fout, iters / 4, 32); });
+  double lds_bytes = lanes * (iters / 4) * 16 * 4;
+  printf(", \"lds32_TBps\": %.2f, \"lds32_B_per_clk_sm\": %.1f", lds_bytes / (ms * 1e-3) / 1e12,
+         lds_bytes / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+  ms = timeit([&] { k_lds32<<<blocks, threads>>>(fout, iters / 4, 33); });
+  printf(", \"lds32_stride33_TBps\": %.2f", lds_bytes / (ms * 1e-3) / 1e12);
+  ms = timeit([&] { k_lds128<<<blocks, threads>>>(fout, iters / 4); });
+  printf(", \"lds128_TBps\": %.2f", lanes * (iters / 4) * 16 * 16 / (ms * 1e-3) / 1e12);
+  int n_cells = 1 << 22;
+  unsigned long long* acc;
+  CK(cudaMalloc(&acc, sizeof(double) * n_cells));
+  CK(cudaMemset(acc, 0, sizeof(double) * n_cells));
+  int aiters = 64;
+  ms = timeit([&] { k_red64<<<blocks, threads>>>(acc, n_cells, aiters); });
+  printf(", \"redg_u64_Gops\": %.1f", lanes * aiters / (ms * 1e-3) / 1e9);
+  ms = timeit([&] { k_redf64<<<blocks, threads>>>((double*)acc, n_cells, aiters); });
+  printf(", \"redg_f64_Gops\": %.1f", lanes * aiters / (ms * 1e-3) / 1e9);
+  ms = timeit([&] { k_redf64_rows<<<blocks, threads>>>((double*)acc, n_cells, aiters); });
+  printf(", \"redg_f64_rows_Gops\": %.1f", lanes * aiters / (ms * 1e-3) / 1e9);
+
+  {
+    long long* cyc; CK(cudaMalloc(&cyc, sizeof(long long) * sms));
+    long long hc[1024];
+    for (int mode = 0; mode < 3; ++mode) {
+      int it = 2048;
+      k_lds_cyc<<<sms, 1024>>>(fout, cyc, it, mode);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(hc, cyc, sizeof(long long) * sms, cudaMemcpyDeviceToHost));
+      double mean = 0; for (int i = 0; i < sms; ++i) mean += hc[i]; mean /= sms;
+      double bytes = 1024.0 * it * 64;  // 16 floats per iter per thread
+      printf(", \"lds_mode%d_B_per_clk_sm\": %.1f", mode, bytes / mean);
+    }
+  }
+  printf("}\n");
+  CK(cudaGetLastError());
+  return 0;
+}
