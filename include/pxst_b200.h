@@ -91,35 +91,27 @@ int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const do
 
 /* K1 object formation, splat half (recon.py:99-138; interp.py:88-123).
  * Adds, for every good frame in [frame_lo, frame_hi) of scan->good and work
- * pixel, I*W*w_c to num_fx and W^2*w_c to den_fx at the four corners of
- * (u0 - di - n0, u1 - dj - m0).  Accumulators are int64 fixed point with
- * scales num_scale / den_scale (powers of two, see pxst_fixed_scales), so the
- * sum is exact, order independent and bit-reproducible, also after an
- * integer all-reduce across GPUs.  Points outside [0,os-1]x[0,of-1] are
- * dropped whole; their count is added to *n_dropped (device, nullable). */
+ * pixel, I*W*w_c to num and W^2*w_c to den (float64, [os*of]) at the four
+ * bilinear corners of (u0 - di - n0, u1 - dj - m0).  Points outside
+ * [0,os-1]x[0,of-1] are dropped whole; their count is added to *n_dropped
+ * (device, nullable).  Frame ranges let frame shards accumulate partial
+ * images that are summed (all-reduce) before pxst_object_finish. */
 int pxst_object_splat(const pxst_scan* scan, const double* u, const double* di,
                       const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-                      int64_t frame_lo, int64_t frame_hi, double num_scale, double den_scale,
-                      int64_t* num_fx, int64_t* den_fx, unsigned long long* n_dropped,
-                      void* stream);
+                      int64_t frame_lo, int64_t frame_hi, double* num, double* den,
+                      unsigned long long* n_dropped, void* stream);
 
 /* K1 normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0,
- * wsum = den; also writes the float32 masked image fm and valid flags used by
- * the search kernels.  Any of the four outputs may be NULL. */
-int pxst_object_finish(const int64_t* num_fx, const int64_t* den_fx, int64_t n,
-                       double num_scale, double den_scale, double* i_ref, double* wsum,
-                       float* fm, uint8_t* valid, void* stream);
+ * wsum = den; also writes the float32 masked image fm and validity flags the
+ * search kernels read.  Any of the four outputs may be NULL. */
+int pxst_object_finish(const double* num, const double* den, int64_t n, double* i_ref,
+                       double* wsum, float* fm, uint8_t* valid, void* stream);
 
-/* Power-of-two fixed-point scales such that |sum| < 2^61 for any cell given
- * the total absolute mass `mass` splatted (host helper, no device work). */
-double pxst_fixed_scale(double mass);
-
-/* Convenience: bbox-free object map for a known grid = splat + finish with
- * internal accumulators.  Replaces recon.make_reference after the bbox. */
-int pxst_object_map(const pxst_scan* scan, const pxst_stats* st, const double* u,
-                    const double* di, const double* dj, int64_t n0, int64_t m0, int64_t os,
-                    int64_t of, double* i_ref, double* wsum, float* fm, uint8_t* valid,
-                    void* stream);
+/* Convenience: splat + finish over all good frames for a known grid
+ * (recon.make_reference after the bbox of pxst_bbox). */
+int pxst_object_map(const pxst_scan* scan, const double* u, const double* di, const double* dj,
+                    int64_t n0, int64_t m0, int64_t os, int64_t of, double* i_ref, double* wsum,
+                    float* fm, uint8_t* valid, void* stream);
 
 /* K2 pixel-map grid search + argmin + paraboloid refinement
  * (recon.py:144-170, 183-207, 221-296 with sigma = 0, integrate = False).
@@ -147,11 +139,10 @@ int pxst_translation_search(const pxst_scan* scan, const pxst_stats* st, const p
                             int64_t frame_lo, int64_t frame_hi, double* di_out,
                             double* dj_out, double* err_out, void* stream);
 
-/* K4 error maps (recon.py:388-438).  per_frame [n_frames] (0 for frames not
- * good), per_pixel [ss,fs], ref_plane [os,of] (normalised reference-plane
- * projection of the residuals), total (device scalar).  ref_num_fx /
- * ref_den_fx (nullable) receive the un-normalised fixed-point accumulators
- * (scale = *plane_scale on return, host) for multi-GPU reduction. */
+/* K4 error maps (recon.py:388-438), one pass over the stack: per_frame
+ * [n_frames] (0 for frames not good), per_pixel [ss,fs], ref_plane [os,of]
+ * (normalised reference-plane projection of the residuals, every work sample
+ * splatted with weight 1), total (device scalar). */
 int pxst_error_maps(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
                     const double* u, const double* di, const double* dj, double* per_frame,
                     double* per_pixel, double* ref_plane, double* total, void* stream);

@@ -44,14 +44,13 @@ _SIGS = {
     "pxst_stack_stats": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_void_p]),
     "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pxst_object_splat": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
-                                  c_int64, c_int64, c_int64, c_int64, c_int64, c_double,
-                                  c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "pxst_object_finish": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p,
-                                   c_void_p, c_void_p, c_void_p, c_void_p]),
-    "pxst_fixed_scale": (c_double, [c_double]),
-    "pxst_object_map": (c_int, [POINTER(PxstScan), POINTER(PxstStats), c_void_p, c_void_p,
-                                c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p,
-                                c_void_p, c_void_p, c_void_p]),
+                                  c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "pxst_object_finish": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p]),
+    "pxst_object_map": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
+                                c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p]),
     "pxst_pixel_map_search": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                       c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
                                       c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

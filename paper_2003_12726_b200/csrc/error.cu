@@ -1,20 +1,19 @@
-// K4 error maps (recon.py:388-438).
+// K4 error maps (recon.py:388-438), one pass over the stack.
 //
 // eps = (valid ? (I - W v)^2 : (I - W)^2) / sigma2 per (frame, work pixel);
 // per_pixel = sum over frames (float64, in-thread), per_frame = sum over
 // pixels (deterministic: per-CTA partials, fixed-order final sum), total =
 // sum of per_frame, reference_plane = normalise(splat(eps, weight 1)) where
-// every sample is splatted, invalid ones included (A10), out-of-grid points
-// dropped (interp.py:103-107).  The splat uses the same int64 fixed-point
-// accumulation as K1; its scale comes from the total of pass 1.
+// every sample is splatted, invalid ones included, out-of-grid
+// points dropped (interp.py:103-107).  The splat accumulates in float64 with
+// RED.ADD.F64 like K1.
 #include "common.cuh"
 
 namespace pxst {
 
 int check_scan(const pxst_scan* sc);
-int launch_object_finish(const int64_t* num, const int64_t* den, int64_t n, double num_scale,
-                         double den_scale, double* i_ref, double* wsum, float* fm,
-                         uint8_t* valid, cudaStream_t s);
+int launch_object_finish(const double* num, const double* den, int64_t n, double* i_ref,
+                         double* wsum, float* fm, uint8_t* valid, cudaStream_t s);
 
 namespace {
 
@@ -30,23 +29,13 @@ struct ErrArgs {
   const uint8_t* valid;
   int64_t os, of, n0, m0;
   const double* sigma2;
+  double* num;   // reference-plane accumulators [os*of]
+  double* den;
 };
 
-__device__ __forceinline__ double sample_eps(const ErrArgs& a, double x, double y, float I,
-                                             float W, double s2) {
-  float v = 0.f;
-  bool ok = false;
-  if (fabs(x) < 1e9 && fabs(y) < 1e9) {
-    const Split sx = split(x), sy = split(y);
-    ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
-  }
-  const float r = ok ? fmaf(-W, v, I) : I - W;
-  return static_cast<double>(r * r) / s2;
-}
-
-// Pass 1: per-pixel sums and per-(frame, CTA) partials.
-__global__ void __launch_bounds__(kThreads) k_err_pass1(ErrArgs a, double* per_pixel,
-                                                        double* part, int64_t n_ctas) {
+// Per-pixel sums, per-(frame, CTA) partials, reference-plane splat.
+__global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pixel,
+                                                       double* part, int64_t n_ctas) {
   __shared__ double red[kThreads / 32][kFB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
@@ -59,6 +48,7 @@ __global__ void __launch_bounds__(kThreads) k_err_pass1(ErrArgs a, double* per_p
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
   const float W = live ? a.sc.w32[p] : 0.f;
   const double s2 = live ? a.sigma2[p] : 1.0;
+  const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
   double pix = 0.0;
   for (int64_t k0 = 0; k0 < a.sc.n_good; k0 += kFB) {
     double e[kFB];
@@ -71,8 +61,33 @@ __global__ void __launch_bounds__(kThreads) k_err_pass1(ErrArgs a, double* per_p
         const double x = u0 - a.di[f] - static_cast<double>(a.n0);   // recon.py:418
         const double y = u1 - a.dj[f] - static_cast<double>(a.m0);
         const float I = __ldg(a.sc.frames + f * plane + p);
-        e[b] = sample_eps(a, x, y, I, W, s2);
-        pix += e[b];
+        const bool in = x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
+        float v = 0.f;
+        bool ok = false;
+        Split sx{0, 0.0}, sy{0, 0.0};
+        if (in) {
+          sx = split(x);
+          sy = split(y);
+          ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
+        }
+        const float r = ok ? fmaf(-W, v, I) : I - W;                  // recon.py:421
+        const double eps = static_cast<double>(r * r) / s2;           // recon.py:422
+        e[b] = eps;
+        pix += eps;
+        if (in) {                                                     // recon.py:425
+          const int r0 = sx.i, c0 = sy.i;
+          const int r1 = min(r0 + 1, static_cast<int>(a.os - 1));
+          const int c1 = min(c0 + 1, static_cast<int>(a.of - 1));
+          const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
+          const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
+          const int64_t cell[4] = {(int64_t)r0 * a.of + c0, (int64_t)r0 * a.of + c1,
+                                   (int64_t)r1 * a.of + c0, (int64_t)r1 * a.of + c1};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            atomicAdd(a.num + cell[q], eps * cw[q]);
+            atomicAdd(a.den + cell[q], cw[q]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -127,44 +142,6 @@ __global__ void k_err_total(const double* __restrict__ frame_tmp, int64_t n, dou
   }
 }
 
-// Pass 2: reference-plane splat of eps with weight 1 (recon.py:425).
-__global__ void __launch_bounds__(kThreads) k_err_splat(ErrArgs a, double num_scale,
-                                                        double den_scale, int64_t* num,
-                                                        int64_t* den) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
-  const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kTC + lane;
-  if (row >= a.sc.roi[1] || col >= a.sc.roi[3]) return;
-  const int64_t p = row * a.sc.fs + col;
-  if (!a.sc.work[p]) return;
-  const int64_t plane = a.sc.ss * a.sc.fs;
-  const double u0 = a.u[p], u1 = a.u[plane + p];
-  const float W = a.sc.w32[p];
-  const double s2 = a.sigma2[p];
-  const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
-  for (int64_t k = blockIdx.z; k < a.sc.n_good; k += gridDim.z) {
-    const int64_t f = a.sc.good[k];
-    const double x = u0 - a.di[f] - static_cast<double>(a.n0);
-    const double y = u1 - a.dj[f] - static_cast<double>(a.m0);
-    if (!(x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1)) continue;
-    const float I = __ldg(a.sc.frames + f * plane + p);
-    const double eps = sample_eps(a, x, y, I, W, s2);
-    const Split sx = split(x), sy = split(y);
-    const int r0 = sx.i, c0 = sy.i;
-    const int r1 = min(r0 + 1, static_cast<int>(a.os - 1));
-    const int c1 = min(c0 + 1, static_cast<int>(a.of - 1));
-    const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
-    const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
-    const int64_t cell[4] = {(int64_t)r0 * a.of + c0, (int64_t)r0 * a.of + c1,
-                             (int64_t)r1 * a.of + c0, (int64_t)r1 * a.of + c1};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      red_add(num + cell[q], to_fixed(eps * cw[q] * num_scale));
-      red_add(den + cell[q], to_fixed(cw[q] * den_scale));
-    }
-  }
-}
-
 }  // namespace
 }  // namespace pxst
 
@@ -176,7 +153,7 @@ extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const 
                                double* total, void* stream) {
   if (int e = check_scan(sc)) return e;
   PXST_REQUIRE(ref && ref->fm && ref->valid && ref->os > 0 && ref->of > 0, "bad reference");
-  PXST_REQUIRE(st && st->sigma2 && st->scalars, "stats descriptor is NULL");
+  PXST_REQUIRE(st && st->sigma2, "stats descriptor is NULL");
   PXST_REQUIRE(u && di && dj && per_frame && per_pixel && ref_plane && total, "NULL pointer");
   cudaStream_t s = as_stream(stream);
   const int64_t plane = sc->ss * sc->fs;
@@ -188,38 +165,24 @@ extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const 
     PXST_CHECK_CUDA(cudaMemsetAsync(ref_plane, 0, sizeof(double) * n_o, s));
     return PXST_OK;
   }
-  ErrArgs a{*sc, u, di, dj, ref->fm, ref->valid, ref->os, ref->of, ref->n0, ref->m0,
-            st->sigma2};
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
   dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)((rw + kTR - 1) / kTR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
   const int64_t n_ctas = (int64_t)g.x * g.y;
-  Scratch part;
+  Scratch part, acc;
   if (int e = part.alloc(sizeof(double) * (n_ctas + 1) * sc->n_good, s)) return e;
+  if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
   double* ftmp = part.as<double>() + n_ctas * sc->n_good;
-  k_err_pass1<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
+  ErrArgs a{*sc, u, di, dj, ref->fm, ref->valid, ref->os, ref->of, ref->n0, ref->m0,
+            st->sigma2, acc.as<double>(), acc.as<double>() + n_o};
+  k_err_pass<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
   PXST_CHECK_LAUNCH();
   k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_ctas, per_frame,
                                                     ftmp);
   PXST_CHECK_LAUNCH();
   k_err_total<<<1, 1024, 0, s>>>(ftmp, sc->n_good, total);
   PXST_CHECK_LAUNCH();
-  // fixed-point scales need the totals on the host
-  double h[4], tot = 0.0;
-  PXST_CHECK_CUDA(cudaMemcpyAsync(&tot, total, sizeof(double), cudaMemcpyDeviceToHost, s));
-  PXST_CHECK_CUDA(cudaMemcpyAsync(h, st->scalars, sizeof(h), cudaMemcpyDeviceToHost, s));
-  PXST_CHECK_CUDA(cudaStreamSynchronize(s));
-  const double num_scale = pxst_fixed_scale(tot);
-  const double den_scale = pxst_fixed_scale(h[2] * static_cast<double>(sc->n_good));
-  Scratch acc;
-  if (int e = acc.alloc(sizeof(int64_t) * 2 * n_o, s)) return e;
-  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(int64_t) * 2 * n_o, s));
-  int64_t gz = (sc->n_good + 15) / 16;
-  if (gz > 65535) gz = 65535;
-  dim3 g2(g.x, g.y, (unsigned)gz);
-  k_err_splat<<<g2, kThreads, 0, s>>>(a, num_scale, den_scale, acc.as<int64_t>(),
-                                      acc.as<int64_t>() + n_o);
-  PXST_CHECK_LAUNCH();
-  return launch_object_finish(acc.as<int64_t>(), acc.as<int64_t>() + n_o, n_o, num_scale,
-                              den_scale, ref_plane, nullptr, nullptr, nullptr, s);
+  return launch_object_finish(acc.as<double>(), acc.as<double>() + n_o, n_o, ref_plane, nullptr,
+                              nullptr, nullptr, s);
 }

@@ -167,35 +167,26 @@ class DeviceScan:
         shape = (int(math.floor(u0max - dimin)) - n0 + 2, int(math.floor(u1max - djmin)) - m0 + 2)
         return n0, m0, shape
 
-    def fixed_scales(self) -> tuple[float, float]:
-        wmax, iw_mass, n_work, _ = (float(v) for v in self.scalars_host)
-        num = self.lib.pxst_fixed_scale(iw_mass)
-        den = self.lib.pxst_fixed_scale(wmax * wmax * n_work * self.n_good)
-        return num, den
-
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
                      acc: torch.Tensor | None = None) -> torch.Tensor:
-        """Fixed-point num/den accumulators [2, os*of] int64 for a frame range."""
+        """Float64 num/den accumulators [2, os*of] for a range of good frames."""
         os_, of = shape
         if acc is None:
-            acc = torch.zeros((2, os_ * of), dtype=torch.int64, device=self.device)
+            acc = torch.zeros((2, os_ * of), dtype=torch.float64, device=self.device)
         hi = self.n_good if frame_hi is None else frame_hi
-        ns, ds = self.fixed_scales()
         check(self.lib.pxst_object_splat(
             ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0, m0,
-            os_, of, frame_lo, hi, ns, ds, acc[0].data_ptr(), acc[1].data_ptr(), None,
-            stream_ptr()))
+            os_, of, frame_lo, hi, acc[0].data_ptr(), acc[1].data_ptr(), None, stream_ptr()))
         return acc
 
     def object_finish(self, acc, origin, shape) -> DeviceRef:
         os_, of = shape
         n = os_ * of
-        ns, ds = self.fixed_scales()
         i_ref = torch.empty(n, dtype=torch.float64, device=self.device)
         wsum = torch.empty(n, dtype=torch.float64, device=self.device)
         fm = torch.empty(n, dtype=torch.float32, device=self.device)
         valid = torch.empty(n, dtype=torch.uint8, device=self.device)
-        check(self.lib.pxst_object_finish(acc[0].data_ptr(), acc[1].data_ptr(), n, ns, ds,
+        check(self.lib.pxst_object_finish(acc[0].data_ptr(), acc[1].data_ptr(), n,
                                           i_ref.data_ptr(), wsum.data_ptr(), fm.data_ptr(),
                                           valid.data_ptr(), stream_ptr()))
         return DeviceRef(i_ref.view(os_, of), wsum.view(os_, of), fm.view(os_, of),

@@ -31,7 +31,7 @@ def header_symbols():
 
 def test_header_symbols_exported(lib):
     syms = header_symbols()
-    assert len(syms) >= 14, syms
+    assert len(syms) >= 13, syms
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_native.EXPORTED)
@@ -39,15 +39,6 @@ def test_header_symbols_exported(lib):
 
 def test_abi_version(lib):
     assert lib.pxst_abi_version() == _native.ABI_VERSION
-
-
-def test_fixed_scale(lib):
-    # largest power of two with mass*scale <= 2^61
-    for mass in (1.0, 3.0, 1e6, 2.0 ** 40, 123456.789):
-        s = lib.pxst_fixed_scale(mass)
-        assert mass * s <= 2.0 ** 61 < 4 * mass * s
-        assert s == 2.0 ** round(__import__("math").log2(s))
-    assert lib.pxst_fixed_scale(0.0) == 1.0
 
 
 def test_null_arguments_rejected_without_device(lib):
