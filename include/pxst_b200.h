@@ -62,12 +62,14 @@ typedef struct pxst_stats {
 } pxst_stats;
 
 /* Reference image on device: fm = i_ref where valid else 0 (float32),
- * valid = wsum > 0 (data_model.py:186-188). */
+ * valid = wsum > 0 (data_model.py:186-188).  fm64 (nullable) is the same
+ * image in float64; the error maps use it when present. */
 typedef struct pxst_ref {
   const float* fm;        /* [os, of] */
   const uint8_t* valid;   /* [os, of] */
   int64_t os, of;
   int64_t n0, m0;
+  const double* fm64;     /* [os, of] or NULL */
 } pxst_ref;
 
 int pxst_abi_version(void);

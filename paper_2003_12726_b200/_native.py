@@ -34,7 +34,7 @@ class PxstStats(ctypes.Structure):
 
 class PxstRef(ctypes.Structure):
     _fields_ = [("fm", c_void_p), ("valid", c_void_p), ("os", c_int64), ("of", c_int64),
-                ("n0", c_int64), ("m0", c_int64)]
+                ("n0", c_int64), ("m0", c_int64), ("fm64", c_void_p)]
 
 
 _SIGS = {

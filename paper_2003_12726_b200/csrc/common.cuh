@@ -145,4 +145,31 @@ __device__ __forceinline__ bool masked_read(const float* __restrict__ fm,
   return true;
 }
 
+// Float64 variant for the memory-bound error maps (K4), reading a float64
+// masked image: matches the reference's float64 residuals to ~1e-15.
+__device__ __forceinline__ bool masked_read64(const double* __restrict__ fm,
+                                              const uint8_t* __restrict__ valid, int64_t os,
+                                              int64_t of, int i, int j, double fx, double fy,
+                                              double& v) {
+  if (!inside_1d(i, fx, os) || !inside_1d(j, fy, of)) return false;
+  const int r0 = i, c0 = j;
+  const int r1 = min(r0 + 1, static_cast<int>(os - 1));
+  const int c1 = min(c0 + 1, static_cast<int>(of - 1));
+  const double w00 = (1.0 - fx) * (1.0 - fy), w01 = (1.0 - fx) * fy;
+  const double w10 = fx * (1.0 - fy), w11 = fx * fy;
+  const int64_t a00 = (int64_t)r0 * of + c0, a01 = (int64_t)r0 * of + c1;
+  const int64_t a10 = (int64_t)r1 * of + c0, a11 = (int64_t)r1 * of + c1;
+  const double m00 = __ldg(valid + a00), m01 = __ldg(valid + a01);
+  const double m10 = __ldg(valid + a10), m11 = __ldg(valid + a11);
+  // interp.py:70-81 order: den and num summed corner by corner
+  const double den = w00 * m00 + w01 * m01 + w10 * m10 + w11 * m11;
+  if (!(den > 0.0)) return false;
+  const double num = w00 * (m00 != 0.0 ? __ldg(fm + a00) : 0.0) +
+                     w01 * (m01 != 0.0 ? __ldg(fm + a01) : 0.0) +
+                     w10 * (m10 != 0.0 ? __ldg(fm + a10) : 0.0) +
+                     w11 * (m11 != 0.0 ? __ldg(fm + a11) : 0.0);
+  v = num / den;
+  return true;
+}
+
 }  // namespace pxst

@@ -28,6 +28,7 @@ struct ErrArgs {
   const float* fm;
   const uint8_t* valid;
   int64_t os, of, n0, m0;
+  const double* fm64;  // nullable float64 image
   const double* sigma2;
   double* num;   // reference-plane accumulators [os*of]
   double* den;
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pi
   const int64_t plane = a.sc.ss * a.sc.fs;
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
   const float W = live ? a.sc.w32[p] : 0.f;
+  const double W64 = live ? a.sc.w64[p] : 0.0;
   const double s2 = live ? a.sigma2[p] : 1.0;
   const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
   double pix = 0.0;
@@ -62,16 +64,23 @@ __global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pi
         const double y = u1 - a.dj[f] - static_cast<double>(a.m0);
         const float I = __ldg(a.sc.frames + f * plane + p);
         const bool in = x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
-        float v = 0.f;
         bool ok = false;
         Split sx{0, 0.0}, sy{0, 0.0};
+        double r;
         if (in) {
           sx = split(x);
           sy = split(y);
-          ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
         }
-        const float r = ok ? fmaf(-W, v, I) : I - W;                  // recon.py:421
-        const double eps = static_cast<double>(r * r) / s2;           // recon.py:422
+        if (a.fm64) {
+          double v = 0.0;
+          if (in) ok = masked_read64(a.fm64, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
+          r = ok ? static_cast<double>(I) - W64 * v : static_cast<double>(I) - W64;
+        } else {
+          float v = 0.f;
+          if (in) ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
+          r = static_cast<double>(ok ? fmaf(-W, v, I) : I - W);
+        }
+        const double eps = (r * r) / s2;                              // recon.py:421-422
         e[b] = eps;
         pix += eps;
         if (in) {                                                     // recon.py:425
@@ -174,8 +183,9 @@ extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const 
   if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
   PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
   double* ftmp = part.as<double>() + n_ctas * sc->n_good;
-  ErrArgs a{*sc, u, di, dj, ref->fm, ref->valid, ref->os, ref->of, ref->n0, ref->m0,
-            st->sigma2, acc.as<double>(), acc.as<double>() + n_o};
+  ErrArgs a{*sc,        u,          di,          dj,        ref->fm,
+            ref->valid, ref->os,    ref->of,     ref->n0,   ref->m0,
+            ref->fm64,  st->sigma2, acc.as<double>(), acc.as<double>() + n_o};
   k_err_pass<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
   PXST_CHECK_LAUNCH();
   k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_ctas, per_frame,

@@ -49,6 +49,8 @@ def _device() -> torch.device:
 def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
     """Host -> device copy of a contiguous array in the requested dtype."""
     h = np.ascontiguousarray(a, dtype=dtype)
+    if not h.flags.writeable:
+        h = h.copy()
     t = torch.from_numpy(h)
     if t.is_pinned():
         return t.to(device, non_blocking=True)
@@ -78,19 +80,22 @@ class DeviceRef:
     def shape(self) -> tuple[int, int]:
         return tuple(self.fm.shape)
 
+    fm64: torch.Tensor | None = None  # [os, of] f64 masked image (error maps)
+
     def struct(self) -> PxstRef:
         os_, of = self.fm.shape
+        f64 = self.fm64 if self.fm64 is not None else self.i_ref
         return PxstRef(self.fm.data_ptr(), self.valid.data_ptr(), os_, of, int(self.origin[0]),
-                       int(self.origin[1]))
+                       int(self.origin[1]), _ptr(f64))
 
     @classmethod
     def from_host(cls, i_ref, wsum, origin, device) -> "DeviceRef":
         i_ref = np.asarray(i_ref, dtype=np.float64)
         ok = np.asarray(wsum) > 0                      # data_model.py:186-188
-        fm = np.where(ok, i_ref, 0.0).astype(np.float32)
-        return cls(None, None, to_device(fm, np.float32, device),
+        fm64 = np.where(ok, i_ref, 0.0)
+        return cls(None, None, to_device(fm64, np.float32, device),
                    to_device(ok.astype(np.uint8), np.uint8, device),
-                   (int(origin[0]), int(origin[1])))
+                   (int(origin[0]), int(origin[1])), to_device(fm64, np.float64, device))
 
 
 class DeviceScan:
