@@ -1,0 +1,378 @@
+"""Benchmark of the PXST hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+121 frames of 256x512, R=5 (121 trial shifts), one full PXST iteration per
+step = object formation (K1) -> pixel-map grid search + argmin + refinement
+(K2) -> error maps (K4), device-resident, synthetic seeded scan
+(``paper_2003_12726_b200.synth``, stand-in for CXIDB 134-136).
+
+  metric  pixel-map trial evaluations/sec (pixels x shifts x frames) per full
+          PXST iteration; ``value`` = trials of one iteration x steps / time of
+          the whole iterations (K1 + K2 + K4 included), ``ms_per_step`` = the
+          full iteration time.
+  roofline  K2 (the dominant kernel), FP32-bound: 11 FLOP per trial
+          (bilinear 7 + residual 2 + square-accumulate 2) over the
+          K2 launch time measured with CUDA events on its stream.
+  e2e     the same metric through the public drop-in API with host (pinned)
+          buffers: make_reference -> update_pixel_map -> calc_error from
+          numpy inputs, stack upload and result downloads inside the timing.
+  cpu_baseline  the oracle port (numpy restatement of the reference) timed on
+          this host on a bounded row band of the same workload.
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port;
+the reference is pure Python and cannot travel to the GPU box) on the same
+metric: each step is one full iteration restricted to a row band.
+
+Multi-GPU (torchrun, N>1): strong scaling of the same config; frames shard
+K1 (NCCL all-reduce of the object numerator/denominator), detector rows
+shard K2/K4 (all-gather of u rows, all-reduce of per-frame sums and the
+reference-plane accumulators) -- see paper_2003_12726_b200/sharding.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_TRIAL = 11
+METRIC = "pixel-map trial evaluations/sec (full PXST iteration)"
+
+
+def base_config(cfg):
+    """The workload description both arms report (same config, metric, unit)."""
+    return {"workload": cfg.name, "frames": cfg.nx * cfg.ny if cfg.positions == "raster"
+            else cfg.n_frames, "detector": [cfg.n_ss, cfg.n_fs],
+            "shifts": (2 * cfg.half_ss + 1) * (2 * cfg.half_fs + 1),
+            "iteration": "object map + pixel-map search + error maps"
+                         + (" + translations" if cfg.update_translations else "")}
+THEORETICAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 at sm_max_mhz
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def k2_traffic():
+    p = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except Exception:
+                self.out = ""
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port on a row band
+# ---------------------------------------------------------------------------
+def oracle_iteration_band(s, rows, threads):
+    from oracle import pxst_oracle as orc
+    cfg = s.cfg
+    sc = s.scan
+    roi = (rows[0], rows[1], 0, cfg.n_fs)
+    i_ref, wsum, org = orc.make_object_map(sc.frames, sc.good_frames, s.w.w, s.m.mask, s.u0.u,
+                                           s.t0.di, s.t0.dj, roi=roi)
+    u, e = orc.update_pixel_map(sc.frames, sc.good_frames, s.w.w, s.m.mask, i_ref, wsum, org,
+                                s.u0.u, s.t0.di, s.t0.dj, cfg.half_ss, cfg.half_fs,
+                                cfg.subpixel_grid, cfg.refine, roi=roi, threads=threads)
+    orc.calc_error(sc.frames, sc.good_frames, s.w.w, s.m.mask, i_ref, wsum, org, u, s.t0.di,
+                   s.t0.dj, roi=roi)
+
+
+def band_trials(s, rows):
+    W, M = s.w.w, s.m.mask
+    P = int(((M & (W > 0))[rows[0]:rows[1]]).sum())
+    K = (2 * s.cfg.half_ss + 1) * (2 * s.cfg.half_fs + 1)
+    return P * K * int(np.count_nonzero(s.scan.good_frames))
+
+
+def cpu_timing(s, steps, warmup, band_rows):
+    cores = len(os.sched_getaffinity(0))
+    c = s.cfg.n_ss // 2
+    rows = (c - band_rows // 2, c - band_rows // 2 + band_rows)
+    for _ in range(warmup):
+        oracle_iteration_band(s, rows, cores)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle_iteration_band(s, rows, cores)
+    dt = time.perf_counter() - t0
+    trials = band_trials(s, rows) * steps
+    return trials / dt, dt / steps, cores, rows
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2003_12726_b200.synth import CONFIGS, make_scan
+    s = make_scan(args.config)
+    band = 8
+    value, sec, cores, rows = cpu_timing(s, args.steps, args.warmup, band)
+    cfg = CONFIGS[args.config]
+    sample = (f"oracle port (numpy restatement of recon.py) full iteration "
+              f"(make_reference + update_pixel_map threads={cores} + calc_error) on "
+              f"detector rows {rows[0]}:{rows[1]} of {cfg.name}")
+    out = {"impl": "reference", "metric": METRIC, "value": value,
+           "unit": "trials/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, synth.py)",
+           "config": base_config(cfg), "sample_rows": list(rows),
+           "cpu_baseline": {"value": value, "unit": "trials/s", "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "trials/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2003_12726_b200 as pb
+    from paper_2003_12726_b200 import _native, engine
+    from paper_2003_12726_b200.synth import CONFIGS, make_scan
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    s = make_scan(args.config)
+    cfg = s.cfg
+    ds = engine.DeviceScan(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask)
+    u_t = ds.upload_u(s.u0.u)
+    di_t, dj_t = ds.upload_t(s.t0.di, s.t0.dj)
+    K = (2 * cfg.half_ss + 1) * (2 * cfg.half_fs + 1)
+    trials = ds.n_work * K * ds.n_good
+    stream = torch.cuda.current_stream()
+
+    sharded = None
+    if world > 1:
+        from paper_2003_12726_b200.sharding import ShardedIteration
+        sharded = ShardedIteration(ds, rank, world)
+
+    def step(ev=None):
+        if sharded is not None:
+            return sharded.iteration(u_t, di_t, dj_t, cfg, ev)
+        dref = ds.object_map(u_t, di_t, dj_t)
+        if ev:
+            ev[0].record(stream)
+        u_new, err = ds.pixel_map_search(dref, u_t, di_t, dj_t, cfg.half_ss, cfg.half_fs,
+                                         cfg.subpixel_grid, cfg.refine)
+        if ev:
+            ev[1].record(stream)
+        if cfg.update_translations:
+            ds.translation_search(dref, u_new, di_t, dj_t, cfg.t_half_ss, cfg.t_half_fs,
+                                  cfg.t_subpixel_grid)
+        ds.error_maps(dref, u_new, di_t, dj_t)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k2ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (untimed)
+            starts[i].record(stream)
+            step(k2ev[i])
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    k2_ms = [a.elapsed_time(b) for a, b in k2ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, float(np.mean(k2_ms))], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, k2_mean = t.tolist()
+    else:
+        k2_mean = float(np.mean(k2_ms))
+    ms_per_step = total_ms / args.steps
+    value = trials * args.steps / (total_ms * 1e-3)
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    pk = peaks()
+    k2_trials = trials / world if world > 1 else trials
+    achieved = FLOP_PER_TRIAL * k2_trials / (k2_mean * 1e-3) / 1e12
+    traffic = k2_traffic()
+    roofline = {"bound": "fp32", "kernel": "k_pixel_search<11,11>",
+                "achieved": achieved, "peak": THEORETICAL_FP32_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / THEORETICAL_FP32_TFLOPS,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "peak_source": ("theoretical FP32 148 SMs x 128 lanes x 2 x sm_max 1965 MHz "
+                                "(MEASURED_PEAKS.json has no FP32 entry; FFMA2 microbenchmark on "
+                                "this pool: 73.8 TFLOP/s, profiles/microbench_r01.json)"),
+                "work": f"{FLOP_PER_TRIAL} FLOP/trial x {k2_trials} trials per launch",
+                "k2_ms": k2_mean, "k2_trials_per_s": k2_trials / (k2_mean * 1e-3)}
+
+    out = {"metric": METRIC, "value": value, "unit": "trials/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f32 (fp64 coordinates / accumulators where the reference needs them)",
+           "data": "synthetic (seeded, synth.py; stands in for CXIDB 134-136)",
+           "config": base_config(cfg),
+           "workload_detail": {"work_pixels": ds.n_work, "trials_per_iteration": trials,
+                               "l2": "flushed between timed steps (256 MiB write, untimed)",
+                               "parallelism": (f"rows/frames sharded x{world}" if world > 1
+                                               else "single GPU")},
+           "full_iteration_ms": ms_per_step, "gpu_launches": launches,
+           "clocks": clk.summary(), "roofline": roofline}
+
+    if not args.profile and not args.no_e2e and world == 1:
+        out["e2e"] = e2e(s, args, pb, engine, torch, trials)
+    if not args.profile and not args.no_cpu_baseline and world == 1:
+        v, sec, cores, rows = cpu_timing(s, 1, 0, 16)
+        out["cpu_baseline"] = {"value": v, "unit": "trials/s", "cores": cores, "kind": "port",
+                               "sample": f"oracle port full iteration on detector rows "
+                                         f"{rows[0]}:{rows[1]} (update_pixel_map threads="
+                                         f"{cores}), 1 run, {sec:.1f} s"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e(s, args, pb, engine, torch, trials):
+    """Public-API iteration from pinned host buffers, uploads/downloads timed."""
+    pinned = torch.empty(s.scan.frames.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[...] = s.scan.frames
+    from dataclasses import replace
+    scan = replace(s.scan, frames=pinned.numpy())
+    cfg = s.cfg
+    win = pb.SearchWindow(cfg.half_ss, cfg.half_fs, cfg.subpixel_grid)
+    opts = pb.UpdateOptions(quadratic_refinement=cfg.refine)
+
+    def one():
+        engine.SCAN_CACHE.clear()           # every step re-uploads the stack
+        ref = pb.make_reference(scan, s.w, s.m, s.u0, s.t0)
+        u, err = pb.update_pixel_map(scan, s.w, s.m, ref, s.u0, s.t0, win, opts)
+        t = s.t0
+        if cfg.update_translations:
+            t = pb.update_translations(scan, s.w, s.m, ref, u, s.t0,
+                                       pb.SearchWindow(cfg.t_half_ss, cfg.t_half_fs,
+                                                       cfg.t_subpixel_grid))
+        pb.calc_error(scan, s.w, s.m, ref, u, t)
+
+    steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    h0, d0 = engine.TRANSFER["h2d"], engine.TRANSFER["d2h"]
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    h2d = (engine.TRANSFER["h2d"] - h0) // steps
+    d2h = (engine.TRANSFER["d2h"] - d0) // steps
+    engine.SCAN_CACHE.clear()
+    return {"value": trials * steps / dt, "unit": "trials/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": dt / steps * 1e3, "steps": steps,
+            "path": "make_reference -> update_pixel_map -> calc_error (drop-in API, numpy in/out,"
+                    " pinned host frames, device cache cleared each step)"}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

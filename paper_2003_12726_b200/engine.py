@@ -46,15 +46,26 @@ def _device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+# Host<->device byte counters (bench.py's e2e accounting).
+TRANSFER = {"h2d": 0, "d2h": 0}
+
+
 def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
     """Host -> device copy of a contiguous array in the requested dtype."""
     h = np.ascontiguousarray(a, dtype=dtype)
     if not h.flags.writeable:
         h = h.copy()
     t = torch.from_numpy(h)
+    TRANSFER["h2d"] += h.nbytes
     if t.is_pinned():
         return t.to(device, non_blocking=True)
     return t.to(device)
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device -> host copy (synchronising)."""
+    TRANSFER["d2h"] += t.numel() * t.element_size()
+    return t.detach().cpu().numpy()
 
 
 def clip_roi(roi, shape) -> tuple[int, int, int, int]:
@@ -142,7 +153,7 @@ class DeviceScan:
         if not self.empty:
             check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), None,
                                             ctypes.byref(self.c_stats), stream_ptr()))
-            self.scalars_host = self.scalars.cpu().numpy().copy()
+            self.scalars_host = to_host(self.scalars).copy()
         else:
             self.scalars_host = np.array([1.0, 0.0, 0.0, 0.0])
 
@@ -166,7 +177,7 @@ class DeviceScan:
         out = torch.empty(8, dtype=torch.float64, device=self.device)
         check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
                                  dj_t.data_ptr(), out.data_ptr(), stream_ptr()))
-        u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = out.cpu().tolist()
+        u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = to_host(out).tolist()
         n0 = int(math.floor(u0min - dimax))
         m0 = int(math.floor(u1min - djmax))
         shape = (int(math.floor(u0max - dimin)) - n0 + 2, int(math.floor(u1max - djmin)) - m0 + 2)

@@ -31,7 +31,7 @@ from .data_model import (
     ScanData,
     Whitefield,
 )
-from .engine import SCAN_CACHE, DeviceRef, DeviceScan
+from .engine import SCAN_CACHE, DeviceRef, DeviceScan, to_host
 
 # Relative floor applied to per-pixel intensity variances (recon.py:34).
 VAR_EPS_REL = 1e-8
@@ -143,7 +143,7 @@ def _check_options(opts) -> None:
 
 
 def _host(t: torch.Tensor) -> np.ndarray:
-    return t.detach().cpu().numpy()
+    return to_host(t)
 
 
 def _ref_image(dref: DeviceRef, geom) -> ReferenceImage:
