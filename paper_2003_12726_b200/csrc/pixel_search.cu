@@ -1,0 +1,494 @@
+// K2: pixel-map grid search + argmin + paraboloid refinement
+// (recon.py:144-170, 183-207, 221-296; sigma = 0, integrate = False).
+//
+// Pipeline for integer windows (Ka x Kb instantiated):
+//   1. k_tile_geo      per 4x32 pixel tile: bounding box of u over its work
+//                      pixels -> object-window origin and "window fits" flag.
+//   2. k_pix_fast      grid (tiles, frame chunks).  Per frame the tile's object
+//                      window (box BR x BC, shifted by delta_n) is fetched by
+//                      TMA into a 4-deep shared-memory ring (mbarrier full /
+//                      empty pairs), each thread runs the register trial engine
+//                      for its pixel; samples whose patch leaves the grid or
+//                      touches an invalid cell are skipped.  Writes float32
+//                      partial sums partial[chunk][trial][pixel].
+//   3. k_pix_slow      one thread per (pixel, chunk) re-derives the same
+//                      eligibility and adds the exact per-trial contribution of
+//                      every skipped sample (masked renormalised read, (I-W)^2
+//                      fallback): rare, small code, no register window.
+//   4. k_pix_epilogue  one thread per pixel: float64 sum over chunks,
+//                      first-occurrence argmin (numpy order a*Kb + b),
+//                      paraboloid on the normalised 3x3 patch, static-pixel
+//                      rule, writes u_out and the error map.
+// Sub-pixel grids and non-instantiated windows use k_pix_generic (float64,
+// one thread per (pixel, trial)) followed by the same epilogue.
+#include "search_common.cuh"
+#include "tma.cuh"
+
+namespace pxst {
+
+int check_scan(const pxst_scan* sc);
+
+namespace {
+
+constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;
+constexpr int kNB = 4;  // TMA ring depth
+
+struct TileGeo {
+  double umin0, umin1;  // NaN when the tile has no work pixel
+  int use_win;
+  int pad;
+};
+
+struct PixArgs {
+  pxst_scan sc;
+  const double* u;
+  const double* di;
+  const double* dj;
+  const float* fm;
+  const uint8_t* valid;
+  const uint8_t* pv;
+  int64_t os, of, n0, m0;
+  const float* fw;           // nullable frame weights [n_frames, ss, fs]
+  const double* var;         // normaliser [ss*fs]
+  const TileGeo* geo;        // [tiles_y * tiles_x]
+  int tiles_x;
+  int ka, kb;                // window (fast kernels: = template args)
+  int box_r, box_c;          // TMA box (rows, cols)
+  int n_chunks, chunk;       // frame chunking of the good list
+  int64_t nq;                // ROI rectangle pixel count
+  float* partial;            // [n_chunks][ka*kb][nq]
+};
+
+__host__ __device__ inline int box_rows_for(int ka) { return ka + 10; }
+__host__ __device__ inline int box_cols_for(int kb) { return ((kb + 52 + 3) / 4) * 4; }
+
+// ---------------------------------------------------------------------------
+// 1. tile geometry
+// ---------------------------------------------------------------------------
+__global__ void k_tile_geo(PixArgs a, TileGeo* geo) {
+  __shared__ double red[kTR][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
+  const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kTC + lane;
+  const bool inroi = row < a.sc.roi[1] && col < a.sc.roi[3];
+  const int64_t p = inroi ? row * a.sc.fs + col : 0;
+  const bool live = inroi && a.sc.work[p] != 0;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
+  double mn0 = warp_min(live ? u0 : INFINITY), mx0 = warp_max(live ? u0 : -INFINITY);
+  double mn1 = warp_min(live ? u1 : INFINITY), mx1 = warp_max(live ? u1 : -INFINITY);
+  if (lane == 0) { red[warp][0] = mn0; red[warp][1] = mx0; red[warp][2] = mn1; red[warp][3] = mx1; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < kTR; ++w) {
+    mn0 = fmin(red[0][0], red[w][0]); red[0][0] = mn0;
+    mx0 = fmax(red[0][1], red[w][1]); red[0][1] = mx0;
+    mn1 = fmin(red[0][2], red[w][2]); red[0][2] = mn1;
+    mx1 = fmax(red[0][3], red[w][3]); red[0][3] = mx1;
+  }
+  mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
+  TileGeo g;
+  g.pad = 0;
+  if (!(mn0 <= mx0)) {
+    g.umin0 = g.umin1 = NAN;
+    g.use_win = 0;
+  } else {
+    g.umin0 = mn0;
+    g.umin1 = mn1;
+    const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
+    const int wr = clamp_span(floor(mx0 - mn0)) + a.ka + 2;
+    const int wc = clamp_span(floor(mx1 - mn1)) + a.kb + 2;
+    g.use_win = finite && wr <= a.box_r && wc <= a.box_c;
+  }
+  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = g;
+}
+
+// Per-sample geometry shared by the fast and slow kernels (identical float64
+// expressions, so both agree on which samples are "fast").
+struct Sample {
+  int i, j;          // integer base of u - delta - origin
+  double fx, fy;     // fractions
+  int lr, lc;        // patch origin inside the TMA box
+  int wr0, wc0;      // box origin in the object grid
+  bool fast;
+};
+
+__device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g, double u0,
+                                              double u1, double dI, double dJ, float fwv) {
+  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
+  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+  Sample s;
+  const double x = u0 - dI - n0d;                     // recon.py:148
+  const double y = u1 - dJ - m0d;
+  const double xf = floor(x), yf = floor(y);
+  s.fx = x - xf;
+  s.fy = y - yf;
+  const bool finite = fabs(x) < 1e9 && fabs(y) < 1e9;
+  s.i = finite ? static_cast<int>(xf) : -(1 << 30);
+  s.j = finite ? static_cast<int>(yf) : -(1 << 30);
+  s.fast = false;
+  s.wr0 = s.wc0 = s.lr = s.lc = 0;
+  if (g.use_win) {
+    s.wr0 = static_cast<int>(floor(g.umin0 - dI - n0d)) - ra;
+    s.wc0 = static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb;
+    s.lr = s.i - ra - s.wr0;
+    s.lc = s.j - rb - s.wc0;
+    s.fast = fwv >= 0.f && s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of &&
+             a.pv[(int64_t)s.i * a.of + s.j] != 0 && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r &&
+             s.lc >= 0 && s.lc + a.kb + 1 <= a.box_c;
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// 2. fast kernel (TMA ring + register engine)
+// ---------------------------------------------------------------------------
+template <int KA, int KB>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
+  constexpr int RA = (KA - 1) / 2, RB = (KB - 1) / 2;
+  extern __shared__ __align__(128) float ring[];
+  __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
+  if (!(g.umin0 == g.umin0)) return;                  // tile without work pixels
+  const int64_t rr = (int64_t)blockIdx.y * kTR + warp, cc = (int64_t)blockIdx.x * kTC + lane;
+  const int64_t row = a.sc.roi[0] + rr, col = a.sc.roi[2] + cc;
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const bool inroi = row < a.sc.roi[1] && col < a.sc.roi[3];
+  const int64_t p = inroi ? row * a.sc.fs + col : 0;
+  const int64_t q = rr * cw + cc;
+  const bool live = inroi && a.sc.work[p] != 0;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const int64_t k_lo = (int64_t)blockIdx.z * a.chunk;
+  const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+  const int nk = static_cast<int>(k_hi - k_lo);
+  float* out = a.partial + (int64_t)blockIdx.z * KA * KB * a.nq + q;
+
+  float acc[KA][KB];
+#pragma unroll
+  for (int t = 0; t < KA; ++t)
+#pragma unroll
+    for (int s = 0; s < KB; ++s) acc[t][s] = 0.f;
+
+  if (g.use_win && nk > 0) {
+    const int box = a.box_r * a.box_c;
+    const unsigned bytes = static_cast<unsigned>(box * sizeof(float));
+    const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+    auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
+      const int64_t f = a.sc.good[k_lo + jj];
+      const int wr0 = static_cast<int>(floor(g.umin0 - a.di[f] - n0d)) - RA;
+      const int wc0 = static_cast<int>(floor(g.umin1 - a.dj[f] - m0d)) - RB;
+      const int b = jj % kNB;
+      mbar_arrive_expect_tx(&full[b], bytes);
+      tma_load_2d(ring + b * box, &tmap, wc0, wr0, &full[b]);
+    };
+    if (threadIdx.x == 0) {
+      tma_prefetch_desc(&tmap);
+      for (int b = 0; b < kNB; ++b) {
+        mbar_init(&full[b], 1);
+        mbar_init(&empty[b], kThreads);
+      }
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int jj = 0; jj < min(kNB, nk); ++jj) issue(jj);
+
+    const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
+    const float W = live ? a.sc.w32[p] : 0.f;
+    float I_next = live ? __ldg(a.sc.frames + (int64_t)a.sc.good[k_lo] * plane + p) : 0.f;
+    for (int jj = 0; jj < nk; ++jj) {
+      const int64_t f = a.sc.good[k_lo + jj];
+      const int b = jj % kNB;
+      const unsigned ph = (jj / kNB) & 1;
+      const float I = I_next;
+      if (live && jj + 1 < nk) I_next = __ldg(a.sc.frames + (int64_t)a.sc.good[k_lo + jj + 1] * plane + p);
+      float fwv = 1.f;
+      if (live && a.fw) fwv = __ldg(a.fw + f * plane + p);
+      const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
+      mbar_wait(&full[b], ph);
+      if (live && sm.fast) {
+        const float fx = static_cast<float>(sm.fx), fy = static_cast<float>(sm.fy);
+        float sI = I, sW = W;
+        if (a.fw) {
+          const float sq = sqrtf(fwv);
+          sI *= sq;
+          sW *= sq;
+        }
+        engine_fast<KA, KB>(ring + b * box + sm.lr * a.box_c + sm.lc, a.box_c, fx, fy,
+                            sW * (1.f - fx), sW * fx, sI, acc);
+      }
+      mbar_arrive(&empty[b]);
+      if (threadIdx.x == 0 && jj + kNB < nk) {
+        mbar_wait(&empty[b], ph);      // every thread is done with this slot
+        issue(jj + kNB);
+      }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int t = 0; t < KA; ++t)
+#pragma unroll
+      for (int s = 0; s < KB; ++s) out[(int64_t)(t * KB + s) * a.nq] = acc[t][s];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3. slow-sample fix-up (runs after k_pix_fast on the same stream)
+// ---------------------------------------------------------------------------
+__global__ void k_pix_slow(PixArgs a) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= a.nq) return;
+  const int64_t rr = q / cw, cc = q % cw;
+  const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
+  if (!a.sc.work[p]) return;
+  const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const double u0 = a.u[p], u1 = a.u[plane + p];
+  const float W = a.sc.w32[p];
+  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
+  const int nk = a.ka * a.kb;
+  float* out = a.partial + (int64_t)blockIdx.y * nk * a.nq + q;
+  const int64_t k_lo = (int64_t)blockIdx.y * a.chunk;
+  const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+  for (int64_t k = k_lo; k < k_hi; ++k) {
+    const int64_t f = a.sc.good[k];
+    float fwv = 1.f;
+    if (a.fw) fwv = __ldg(a.fw + f * plane + p);
+    const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
+    if (sm.fast) continue;
+    const float I = __ldg(a.sc.frames + f * plane + p);
+    for (int t = 0; t < a.ka; ++t)
+      for (int s = 0; s < a.kb; ++s)
+        out[(int64_t)(t * a.kb + s) * a.nq] +=
+            trial_exact(a.fm, a.valid, a.os, a.of, sm.i - ra + t, sm.j - rb + s, sm.fx, sm.fy, W,
+                        I, fwv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic (sub-pixel / any window): float64, one thread per (pixel, trial)
+// ---------------------------------------------------------------------------
+__global__ void k_pix_generic(PixArgs a, const double* __restrict__ offs_a,
+                              const double* __restrict__ offs_b, double* __restrict__ errs) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (q >= a.nq) return;
+  const int64_t p = (a.sc.roi[0] + q / cw) * a.sc.fs + a.sc.roi[2] + q % cw;
+  if (!a.sc.work[p]) return;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const double u0 = a.u[p], u1 = a.u[plane + p];
+  const double W = a.sc.w64[p];
+  const double oa = offs_a[t / a.kb], ob = offs_b[t % a.kb];
+  double acc = 0.0;
+  for (int64_t k = 0; k < a.sc.n_good; ++k) {
+    const int64_t f = a.sc.good[k];
+    const double I = static_cast<double>(__ldg(a.sc.frames + f * plane + p));
+    const double fwv = a.fw ? static_cast<double>(__ldg(a.fw + f * plane + p)) : 1.0;
+    const double x = (u0 - a.di[f] - a.n0) + oa;      // recon.py:148, 157
+    const double y = (u1 - a.dj[f] - a.m0) + ob;
+    float v = 0.f;
+    bool ok = false;
+    if (fabs(x) < 1e9 && fabs(y) < 1e9) {
+      const Split sx = split(x), sy = split(y);
+      ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
+    }
+    const double r = ok ? I - W * static_cast<double>(v) : I - W;
+    acc += fwv * (r * r);
+  }
+  errs[(int64_t)t * a.nq + q] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// 4. epilogue
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chunks,
+                               const double* __restrict__ offs_a, const double* __restrict__ offs_b,
+                               int refine_ok, double* u_out, double* err_out) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= a.nq) return;
+  const int64_t p = (a.sc.roi[0] + q / cw) * a.sc.fs + a.sc.roi[2] + q % cw;
+  if (!a.sc.work[p]) return;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const int na = a.ka, nb = a.kb, nk = na * nb;
+  const int64_t cstride = (int64_t)nk * a.nq;
+  auto total = [&](int t) {
+    double s = 0.0;
+    for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[c * cstride + (int64_t)t * a.nq + q]);
+    return s;
+  };
+  const double var = a.var[p];                        // recon.py:257-263
+  const bool active = var > 0.0;
+  const double nv = active ? var : 1.0;
+  int best = 0;
+  double bv = total(0) / nv;
+  for (int t = 1; t < nk; ++t) {                      // first occurrence (recon.py:265-269)
+    const double v = total(t) / nv;
+    if (v < bv) { bv = v; best = t; }
+  }
+  const int ia = best / nb, ib = best % nb;
+  double sh_ss = offs_a[ia], sh_fs = offs_b[ib];
+  if (refine_ok && active && ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {   // recon.py:273-287
+    double e[9];
+    for (int d = 0; d < 9; ++d) e[d] = total((ia + d / 3 - 1) * nb + (ib + d % 3 - 1)) / nv;
+    double dss, dfs;
+    paraboloid(e, dss, dfs);
+    sh_ss += dss;
+    sh_fs += dfs;
+  }
+  if (!active) { sh_ss = 0.0; sh_fs = 0.0; }          // recon.py:289-292
+  u_out[p] = a.u[p] + sh_ss;                          // recon.py:294-296
+  u_out[plane + p] = a.u[plane + p] + sh_fs;
+  err_out[p] = active ? bv : 0.0;                     // recon.py:313-315
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+using FastKernel = void (*)(const __grid_constant__ CUtensorMap, PixArgs);
+struct FastEntry { int ka, kb; FastKernel fn; };
+#define PIX(a, b) FastEntry{a, b, k_pix_fast<a, b>}
+const FastEntry kFastTable[] = {
+    PIX(1, 1),  PIX(3, 3),  PIX(5, 5),  PIX(7, 7),  PIX(9, 9),  PIX(11, 11), PIX(13, 13),
+    PIX(1, 3),  PIX(1, 5),  PIX(1, 7),  PIX(1, 9),  PIX(1, 11), PIX(1, 13),  PIX(1, 15),
+    PIX(1, 17), PIX(3, 1),  PIX(5, 1),  PIX(7, 1),  PIX(9, 1),  PIX(11, 1),  PIX(13, 1),
+    PIX(15, 1), PIX(17, 1),
+};
+#undef PIX
+
+FastKernel find_fast(int ka, int kb) {
+  for (const auto& e : kFastTable)
+    if (e.ka == ka && e.kb == kb) return e.fn;
+  return nullptr;
+}
+
+}  // namespace
+}  // namespace pxst
+
+using namespace pxst;
+
+extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
+                                     const pxst_ref* ref, const double* u_in, const double* di,
+                                     const double* dj, int64_t half_ss, int64_t half_fs,
+                                     double subpixel_step, int refine, const float* fw,
+                                     const double* var_fw, double* u_out, double* err_out,
+                                     void* stream) {
+  if (int e = check_scan(sc)) return e;
+  if (int e = check_ref(ref)) return e;
+  PXST_REQUIRE(st && st->var_pm, "stats descriptor is NULL");
+  PXST_REQUIRE(u_in && di && dj && u_out && err_out, "NULL pointer");
+  PXST_REQUIRE(half_ss >= 0 && half_fs >= 0, "search window halves must be >= 0");
+  PXST_REQUIRE(subpixel_step == 0.0 || (subpixel_step > 0.0 && subpixel_step <= 1.0),
+               "subpixel_grid step must be in (0, 1]");
+  PXST_REQUIRE(!fw || var_fw, "frame weights need their normaliser var_fw");
+  cudaStream_t s = as_stream(stream);
+  const int64_t plane = sc->ss * sc->fs;
+  PXST_CHECK_CUDA(cudaMemcpyAsync(u_out, u_in, sizeof(double) * 2 * plane,
+                                  cudaMemcpyDeviceToDevice, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(err_out, 0, sizeof(double) * plane, s));
+  if (sc->n_good == 0) return PXST_OK;
+
+  const std::vector<double> oa = window_offsets(half_ss, subpixel_step);
+  const std::vector<double> ob = window_offsets(half_fs, subpixel_step);
+  const int na = static_cast<int>(oa.size()), nb = static_cast<int>(ob.size());
+  const int nk = na * nb;
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+
+  PixArgs a{};
+  a.sc = *sc;
+  a.u = u_in; a.di = di; a.dj = dj;
+  a.fm = ref->fm; a.valid = ref->valid;
+  a.os = ref->os; a.of = ref->of; a.n0 = ref->n0; a.m0 = ref->m0;
+  a.fw = fw;
+  a.var = fw ? var_fw : st->var_pm;
+  a.ka = na; a.kb = nb;
+  a.nq = cw * rw;
+
+  Scratch offs;
+  if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
+  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.p, oa.data(), sizeof(double) * na,
+                                  cudaMemcpyHostToDevice, s));
+  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.as<double>() + na, ob.data(), sizeof(double) * nb,
+                                  cudaMemcpyHostToDevice, s));
+  const double* d_oa = offs.as<double>();
+  const double* d_ob = d_oa + na;
+  const int refine_ok = refine && subpixel_step == 0.0 && na >= 3 && nb >= 3;   // recon.py:273
+  const unsigned qblocks = (unsigned)((a.nq + 127) / 128);
+
+  FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
+  if (fn) {
+    const int ra = (na - 1) / 2, rb = (nb - 1) / 2;
+    a.box_r = box_rows_for(na);
+    a.box_c = box_cols_for(nb);
+    a.tiles_x = static_cast<int>((cw + kTC - 1) / kTC);
+    const int tiles_y = static_cast<int>((rw + kTR - 1) / kTR);
+    PXST_REQUIRE(tiles_y <= kMaxGridY, "ROI too tall");
+    const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
+    // Frame chunks: enough CTAs for ~6 waves at 2 CTAs/SM, <= 512 frames per
+    // float32 partial sum.
+    int n_chunks = static_cast<int>((6 * 2 * 148 + tiles - 1) / tiles);
+    n_chunks = max(n_chunks, static_cast<int>((sc->n_good + 511) / 512));
+    const int max_chunks = static_cast<int>(sc->n_good / 16 > 1 ? sc->n_good / 16 : 1);
+    n_chunks = n_chunks < max_chunks ? n_chunks : max_chunks;
+    n_chunks = n_chunks > 1 ? n_chunks : 1;
+    a.chunk = static_cast<int>((sc->n_good + n_chunks - 1) / n_chunks);
+    a.n_chunks = static_cast<int>((sc->n_good + a.chunk - 1) / a.chunk);
+
+    Scratch pvbuf, pvtmp, geo, part, fmpad;
+    if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
+    if (int e = make_pv(ref, -ra, ra + 1, -rb, rb + 1, pvbuf.as<uint8_t>(), pvtmp, s)) return e;
+    a.pv = pvbuf.as<uint8_t>();
+    if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
+    a.geo = geo.as<TileGeo>();
+    if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
+    a.partial = part.as<float>();
+    // TMA needs a 16-byte row pitch: pad the object image when of % 4 != 0.
+    const float* tbase = ref->fm;
+    int64_t pitch = ref->of;
+    if (ref->of % 4 != 0 || (reinterpret_cast<uintptr_t>(ref->fm) & 15)) {
+      pitch = (ref->of + 3) / 4 * 4;
+      if (int e = fmpad.alloc(sizeof(float) * pitch * ref->os, s)) return e;
+      PXST_CHECK_CUDA(cudaMemcpy2DAsync(fmpad.p, pitch * sizeof(float), ref->fm,
+                                        ref->of * sizeof(float), ref->of * sizeof(float), ref->os,
+                                        cudaMemcpyDeviceToDevice, s));
+      tbase = fmpad.as<float>();
+    }
+    CUtensorMap tmap;
+    if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
+      return e;
+
+    dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
+    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>());
+    PXST_CHECK_LAUNCH();
+    const size_t smem = sizeof(float) * kNB * a.box_r * a.box_c;
+    PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
+    fn<<<gf, kThreads, smem, s>>>(tmap, a);
+    PXST_CHECK_LAUNCH();
+    dim3 gs(qblocks, (unsigned)a.n_chunks);
+    k_pix_slow<<<gs, 128, 0, s>>>(a);
+    PXST_CHECK_LAUNCH();
+    k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
+                                                  refine_ok, u_out, err_out);
+    PXST_CHECK_LAUNCH();
+    return PXST_OK;
+  }
+  // generic path
+  Scratch errs;
+  if (int e = errs.alloc(sizeof(double) * a.nq * nk, s)) return e;
+  PXST_REQUIRE(nk <= kMaxGridY, "search window too large");
+  dim3 g(qblocks, (unsigned)nk);
+  k_pix_generic<<<g, 128, 0, s>>>(a, d_oa, d_ob, errs.as<double>());
+  PXST_CHECK_LAUNCH();
+  k_pix_epilogue<double><<<qblocks, 128, 0, s>>>(a, errs.as<double>(), 1, d_oa, d_ob, refine_ok,
+                                                 u_out, err_out);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}

@@ -1,0 +1,133 @@
+// Shared pieces of the grid-search kernels (K2 pixel map, K3 translations).
+//
+// Reference: recon.py:144-170 (_candidate_errors), :183-207 (_refine_batch),
+// interp.py:53-85 (masked bilinear read).
+//
+// Trial engine: for integer offsets the fractional part of
+// u - delta - origin is the same for every trial, so one (frame, pixel)
+// sample splits once into an exact integer base (float64 floor) and float32
+// fractions, and the whole Ka x Kb window is evaluated from a single
+// (Ka+1) x (Kb+1) patch of the object.  The patch is walked row by row: each
+// row is interpolated along fs once (h = (1-fy) o_b + fy o_{b+1}) and every
+// trial is
+//     r = I - A h_prev - B h_cur,  acc += r*r        (A = W(1-fx), B = W fx)
+// i.e. 3 FFMA per trial + 2 (Ka+1) Kb / (Ka Kb) per trial for the rows.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace pxst {
+
+// Fast path: the whole patch is valid and inside; `win` points at the patch
+// origin in shared memory (row pitch ld).  acc[t][s] accumulates the trial
+// whose bilinear base cell is (patch row t, patch col s).
+template <int KA, int KB>
+__device__ __forceinline__ void engine_fast(const float* __restrict__ win, int ld, float fx,
+                                            float fy, float A, float B, float I,
+                                            float (&acc)[KA][KB]) {
+  const float gy = 1.f - fy;
+  float hp[KB];
+  {
+    float o[KB + 1];
+#pragma unroll
+    for (int s = 0; s <= KB; ++s) o[s] = win[s];
+#pragma unroll
+    for (int s = 0; s < KB; ++s) hp[s] = fmaf(fy, o[s + 1], gy * o[s]);
+  }
+#pragma unroll
+  for (int t = 0; t < KA; ++t) {
+    const float* rp = win + (t + 1) * ld;
+    float o[KB + 1], hc[KB];
+#pragma unroll
+    for (int s = 0; s <= KB; ++s) o[s] = rp[s];
+#pragma unroll
+    for (int s = 0; s < KB; ++s) hc[s] = fmaf(fy, o[s + 1], gy * o[s]);
+#pragma unroll
+    for (int s = 0; s < KB; ++s) {
+      float r = fmaf(-A, hp[s], I);
+      r = fmaf(-B, hc[s], r);
+      acc[t][s] = fmaf(r, r, acc[t][s]);
+    }
+#pragma unroll
+    for (int s = 0; s < KB; ++s) hp[s] = hc[s];
+  }
+}
+
+// Exact contribution of one sample to one trial whose bilinear base cell is
+// (row, col) with fractions (fx, fy): masked renormalised read from global
+// memory with the inclusive inside test, (I - W)^2 fallback when invalid
+// (recon.py:150, 161), times the frame weight.
+__device__ __forceinline__ float trial_exact(const float* __restrict__ fm,
+                                             const uint8_t* __restrict__ valid, int64_t os,
+                                             int64_t of, int row, int col, double fx, double fy,
+                                             float W, float I, float fwv) {
+  float v;
+  if (masked_read(fm, valid, os, of, row, col, fx, fy, v)) {
+    const float r = fmaf(-W, v, I);
+    return fwv * (r * r);
+  }
+  const float d0 = I - W;
+  return fwv * (d0 * d0);
+}
+
+// Exact slow path for one sample over a register accumulator window (used by
+// the translation kernel, whose accumulators stay in registers).
+template <int KA, int KB>
+__device__ __forceinline__ void engine_slow(const float* __restrict__ fm,
+                                            const uint8_t* __restrict__ valid, int64_t os,
+                                            int64_t of, int pr, int pc, double fx, double fy,
+                                            float W, float I, float fwv, float (&acc)[KA][KB]) {
+#pragma unroll
+  for (int t = 0; t < KA; ++t)
+#pragma unroll
+    for (int s = 0; s < KB; ++s)
+      acc[t][s] += trial_exact(fm, valid, os, of, pr + t, pc + s, fx, fy, W, I, fwv);
+}
+
+// float64 3x3 least-squares paraboloid (recon.py:183-207); e is row-major
+// [ss offset -1,0,1][fs offset -1,0,1].  Offsets clipped to [-1, 1]; (0,0)
+// when the Hessian is not positive definite.
+__device__ __forceinline__ void paraboloid(const double (&e)[9], double& dss, double& dfs) {
+  double s0 = 0, sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const double X = static_cast<double>(q / 3 - 1), Y = static_cast<double>(q % 3 - 1);
+    s0 += e[q];
+    sx += e[q] * X;
+    sy += e[q] * Y;
+    sxx += e[q] * (X * X);
+    syy += e[q] * (Y * Y);
+    sxy += e[q] * (X * Y);
+  }
+  const double b = sx / 6.0, c = sy / 6.0, f = sxy / 4.0;
+  const double d = (-2.0 * s0 + 3.0 * sxx) / 6.0;
+  const double g = (-2.0 * s0 + 3.0 * syy) / 6.0;
+  const double det = 4.0 * d * g - f * f;
+  if (d > 0.0 && det > 0.0) {
+    dss = fmin(fmax((-2.0 * g * b + f * c) / det, -1.0), 1.0);
+    dfs = fmin(fmax((-2.0 * d * c + f * b) / det, -1.0), 1.0);
+  } else {
+    dss = 0.0;
+    dfs = 0.0;
+  }
+}
+
+__device__ __forceinline__ int clamp_span(double v) {
+  return v < 0.0 ? 0 : (v > 4096.0 ? 4096 : static_cast<int>(v));
+}
+
+// Host helpers ---------------------------------------------------------------
+// Patch-valid map: pv[i][j] = every cell of rows [i+lr, i+hr] x cols
+// [j+lc, j+hc] exists and is valid.
+int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Scratch& tmp,
+            cudaStream_t s);
+// Offsets of SearchWindow.offsets (recon.py:51-57).
+std::vector<double> window_offsets(int64_t half, double step);
+// Integer steps per pixel of a sub-pixel grid (0 when 1/step is not integral).
+int steps_per_pixel(double step);
+int check_ref(const pxst_ref* r);
+bool force_generic();
+
+}  // namespace pxst

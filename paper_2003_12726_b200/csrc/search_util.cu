@@ -1,0 +1,103 @@
+// Host/device utilities shared by the search kernels: patch-valid maps,
+// window offsets, TMA descriptor encoding.
+#include <stdlib.h>
+
+#include "search_common.cuh"
+#include "tma.cuh"
+
+namespace pxst {
+namespace {
+
+__global__ void k_pv_rows(const uint8_t* __restrict__ valid, int64_t os, int64_t of, int lc,
+                          int hc, uint8_t* __restrict__ tmp) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < os * of;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / of, j = q % of;
+    uint8_t ok = (j + lc >= 0 && j + hc < of) ? 1 : 0;
+    for (int c = lc; ok && c <= hc; ++c) ok = valid[i * of + j + c];
+    tmp[q] = ok;
+  }
+}
+
+__global__ void k_pv_cols(const uint8_t* __restrict__ tmp, int64_t os, int64_t of, int lr,
+                          int hr, uint8_t* __restrict__ pv) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < os * of;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / of, j = q % of;
+    uint8_t ok = (i + lr >= 0 && i + hr < os) ? 1 : 0;
+    for (int r = lr; ok && r <= hr; ++r) ok = tmp[(i + r) * of + j];
+    pv[q] = ok;
+  }
+}
+
+}  // namespace
+
+int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Scratch& tmp,
+            cudaStream_t s) {
+  const int64_t n = ref->os * ref->of;
+  if (int e = tmp.alloc(n, s)) return e;
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  k_pv_rows<<<(unsigned)b, 256, 0, s>>>(ref->valid, ref->os, ref->of, lc, hc, tmp.as<uint8_t>());
+  PXST_CHECK_LAUNCH();
+  k_pv_cols<<<(unsigned)b, 256, 0, s>>>(tmp.as<uint8_t>(), ref->os, ref->of, lr, hr, pv);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+std::vector<double> window_offsets(int64_t half, double step) {
+  std::vector<double> o;
+  if (step <= 0.0) {
+    for (int64_t k = -half; k <= half; ++k) o.push_back(static_cast<double>(k));
+  } else {
+    const int64_t kh = static_cast<int64_t>(llround(static_cast<double>(half) / step));
+    for (int64_t k = -kh; k <= kh; ++k) o.push_back(step * static_cast<double>(k));
+  }
+  return o;
+}
+
+int steps_per_pixel(double step) {
+  if (step <= 0.0) return 1;
+  const double q = 1.0 / step;
+  const double qr = nearbyint(q);
+  if (qr >= 1.0 && qr <= 16.0 && fabs(q - qr) < 1e-9 && fabs(step * qr - 1.0) < 1e-12)
+    return static_cast<int>(qr);
+  return 0;
+}
+
+int check_ref(const pxst_ref* r) {
+  PXST_REQUIRE(r && r->fm && r->valid && r->os > 0 && r->of > 0, "bad reference image");
+  PXST_REQUIRE(r->os * r->of < (int64_t(1) << 31), "reference image too large");
+  return PXST_OK;
+}
+
+bool force_generic() {
+  const char* v = getenv("PXST_FORCE_GENERIC");
+  return v && v[0] == '1';
+}
+
+int encode_tmap_2d_f32(CUtensorMap* map, const float* base, int64_t rows, int64_t cols,
+                       int64_t pitch_elems, int box_rows, int box_cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return set_error(PXST_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch_elems * 4)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(PXST_ECUDA, "cuTensorMapEncodeTiled failed (%d): rows %lld cols %lld box %dx%d",
+                     static_cast<int>(r), (long long)rows, (long long)cols, box_rows, box_cols);
+  return PXST_OK;
+}
+
+}  // namespace pxst
