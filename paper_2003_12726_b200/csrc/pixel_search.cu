@@ -61,6 +61,11 @@ struct PixArgs {
 
 __host__ __device__ inline int box_rows_for(int ka) { return ka + 10; }
 __host__ __device__ inline int box_cols_for(int kb) { return ((kb + 52 + 3) / 4) * 4; }
+__host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
+// TMA on this stack faults ("illegal instruction") unless the box starts on a
+// 16-byte boundary in the innermost dimension (measured: fp32 column
+// coordinates must be multiples of 4), so window origins are aligned down.
+__host__ __device__ inline int align4_down(int c) { return c - (((c % 4) + 4) % 4); }
 
 // ---------------------------------------------------------------------------
 // 1. tile geometry
@@ -97,7 +102,7 @@ __global__ void k_tile_geo(PixArgs a, TileGeo* geo) {
     g.umin1 = mn1;
     const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
     const int wr = clamp_span(floor(mx0 - mn0)) + a.ka + 2;
-    const int wc = clamp_span(floor(mx1 - mn1)) + a.kb + 2;
+    const int wc = clamp_span(floor(mx1 - mn1)) + a.kb + 2 + 3;   // +3: aligned origin
     g.use_win = finite && wr <= a.box_r && wc <= a.box_c;
   }
   geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = g;
@@ -130,7 +135,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
   if (g.use_win) {
     s.wr0 = static_cast<int>(floor(g.umin0 - dI - n0d)) - ra;
-    s.wc0 = static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb;
+    s.wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb);
     s.lr = s.i - ra - s.wr0;
     s.lc = s.j - rb - s.wc0;
     s.fast = fwv >= 0.f && s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of &&
@@ -147,8 +152,11 @@ template <int KA, int KB>
 __global__ void __launch_bounds__(kThreads, 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
   constexpr int RA = (KA - 1) / 2, RB = (KB - 1) / 2;
-  extern __shared__ __align__(128) float ring[];
+  extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
+  // TMA destinations must be 128-byte aligned: align the base, pad the slots.
+  float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ring_raw) + 127) &
+                                         ~static_cast<uintptr_t>(127));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
@@ -173,13 +181,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int s = 0; s < KB; ++s) acc[t][s] = 0.f;
 
   if (g.use_win && nk > 0) {
-    const int box = a.box_r * a.box_c;
-    const unsigned bytes = static_cast<unsigned>(box * sizeof(float));
+    const int box = slot_floats(a.box_r, a.box_c);      // slot stride (128-byte multiple)
+    const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
     const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
     auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
       const int64_t f = a.sc.good[k_lo + jj];
       const int wr0 = static_cast<int>(floor(g.umin0 - a.di[f] - n0d)) - RA;
-      const int wc0 = static_cast<int>(floor(g.umin1 - a.dj[f] - m0d)) - RB;
+      const int wc0 = align4_down(static_cast<int>(floor(g.umin1 - a.dj[f] - m0d)) - RB);
       const int b = jj % kNB;
       mbar_arrive_expect_tx(&full[b], bytes);
       tma_load_2d(ring + b * box, &tmap, wc0, wr0, &full[b]);
@@ -466,7 +474,7 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
     k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
-    const size_t smem = sizeof(float) * kNB * a.box_r * a.box_c;
+    const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);

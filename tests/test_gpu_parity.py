@@ -180,10 +180,12 @@ def test_cfg1_pixel_map_band(scan1, golden1):
     np.testing.assert_array_equal(uo[:, band[0]:band[1]], g["upm_u"])
     r, c = work_rc(s, band)
     assert_pixel_map(u.u, e, uo, eo, stack, r, c, s.u0.u, True)
-    # the full-frame run agrees with the band run on the band (row independence)
+    # the full-frame run agrees with the band run on the band (row independence;
+    # frame chunking may differ, so to float32 summation order)
     uf, ef = pb.update_pixel_map(s.scan, s.w, s.m, ref, s.u0, s.t0, pb.SearchWindow(5, 5))
-    np.testing.assert_array_equal(uf.u[:, band[0]:band[1]], u.u[:, band[0]:band[1]])
-    np.testing.assert_array_equal(ef[band[0]:band[1]], e[band[0]:band[1]])
+    d = np.abs(uf.u[:, r, c] - u.u[:, r, c]).max(axis=0)
+    assert d[unique_pixels(stack)].max() < PX_TOL
+    np.testing.assert_allclose(ef[band[0]:band[1]], e[band[0]:band[1]], rtol=1e-5, atol=1e-12)
 
 
 def test_cfg1_translation_subset(scan1, golden1):
