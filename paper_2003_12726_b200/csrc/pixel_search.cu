@@ -155,8 +155,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
-  float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(ring_raw) + 127) &
-                                         ~static_cast<uintptr_t>(127));
+  // (Pointer arithmetic on the shared array keeps the address space, so the
+  // engine's reads compile to LDS rather than generic loads.)
+  float* ring = reinterpret_cast<float*>(ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
@@ -244,9 +245,14 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
-// 3. slow-sample fix-up (runs after k_pix_fast on the same stream)
+// 3. slow-sample fix-up (runs after k_pix_fast on the same stream).
+//    k_pix_classify: one thread per (pixel, chunk) re-derives eligibility and
+//    appends (pixel, chunk) pairs that own skipped samples to a list.
+//    k_pix_slow: one warp per listed pair, lanes over trials, frames in
+//    order; each (chunk, trial, pixel) partial is owned by one lane, so the
+//    result does not depend on list order.
 // ---------------------------------------------------------------------------
-__global__ void k_pix_slow(PixArgs a) {
+__global__ void k_pix_classify(PixArgs a, unsigned long long* list, unsigned* list_n) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= a.nq) return;
@@ -256,24 +262,53 @@ __global__ void k_pix_slow(PixArgs a) {
   const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
   const int64_t plane = a.sc.ss * a.sc.fs;
   const double u0 = a.u[p], u1 = a.u[plane + p];
-  const float W = a.sc.w32[p];
-  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
-  const int nk = a.ka * a.kb;
-  float* out = a.partial + (int64_t)blockIdx.y * nk * a.nq + q;
   const int64_t k_lo = (int64_t)blockIdx.y * a.chunk;
   const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
   for (int64_t k = k_lo; k < k_hi; ++k) {
     const int64_t f = a.sc.good[k];
     float fwv = 1.f;
     if (a.fw) fwv = __ldg(a.fw + f * plane + p);
-    const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
-    if (sm.fast) continue;
-    const float I = __ldg(a.sc.frames + f * plane + p);
-    for (int t = 0; t < a.ka; ++t)
-      for (int s = 0; s < a.kb; ++s)
-        out[(int64_t)(t * a.kb + s) * a.nq] +=
-            trial_exact(a.fm, a.valid, a.os, a.of, sm.i - ra + t, sm.j - rb + s, sm.fx, sm.fy, W,
-                        I, fwv);
+    if (!make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast) {
+      const unsigned slot = atomicAdd(list_n, 1u);
+      list[slot] = (static_cast<unsigned long long>(q) << 20) | blockIdx.y;
+      return;
+    }
+  }
+}
+
+__global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ list,
+                           const unsigned* __restrict__ list_n) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned n = *list_n;
+  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
+  const int nk = a.ka * a.kb;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  for (int64_t e = warp0; e < n; e += nwarps) {
+    const unsigned long long ent = list[e];
+    const int64_t q = static_cast<int64_t>(ent >> 20);
+    const int chunk = static_cast<int>(ent & 0xFFFFF);
+    const int64_t rr = q / cw, cc = q % cw;
+    const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
+    const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
+    const double u0 = a.u[p], u1 = a.u[plane + p];
+    const float W = a.sc.w32[p];
+    float* out = a.partial + (int64_t)chunk * nk * a.nq + q;
+    const int64_t k_lo = (int64_t)chunk * a.chunk;
+    const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+    for (int64_t k = k_lo; k < k_hi; ++k) {
+      const int64_t f = a.sc.good[k];
+      float fwv = 1.f;
+      if (a.fw) fwv = __ldg(a.fw + f * plane + p);
+      const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
+      if (sm.fast) continue;                      // warp-uniform
+      const float I = __ldg(a.sc.frames + f * plane + p);
+      for (int t = lane; t < nk; t += 32)
+        out[(int64_t)t * a.nq] += trial_exact(a.fm, a.valid, a.os, a.of, sm.i - ra + t / a.kb,
+                                              sm.j - rb + t % a.kb, sm.fx, sm.fy, W, I, fwv);
+    }
   }
 }
 
@@ -480,8 +515,15 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
     fn<<<gf, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
+    Scratch lst;
+    if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 2), s)) return e;
+    unsigned* list_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
+    unsigned long long* list = lst.as<unsigned long long>() + 1;
+    PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, sizeof(unsigned), s));
     dim3 gs(qblocks, (unsigned)a.n_chunks);
-    k_pix_slow<<<gs, 128, 0, s>>>(a);
+    k_pix_classify<<<gs, 128, 0, s>>>(a, list, list_n);
+    PXST_CHECK_LAUNCH();
+    k_pix_slow<<<148 * 4, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
     k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
                                                   refine_ok, u_out, err_out);
