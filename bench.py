@@ -232,20 +232,31 @@ def run_ours(args, rank, world, local):
         from paper_2003_12726_b200.sharding import ShardedIteration
         sharded = ShardedIteration(ds, rank, world)
 
+    # The config's workload is `cfg.iters` consecutive iterations from the
+    # initial state (config 1: 3 x object -> pixel map -> error); steps walk
+    # that sequence with the state carried over and restart it when done.
+    state = {"it": 0, "u": u_t, "di": di_t, "dj": dj_t}
+
     def step(ev=None):
+        if state["it"] == 0:
+            state.update(u=u_t, di=di_t, dj=dj_t)
+        u, di, dj = state["u"], state["di"], state["dj"]
         if sharded is not None:
-            return sharded.iteration(u_t, di_t, dj_t, cfg, ev)
-        dref = ds.object_map(u_t, di_t, dj_t)
-        if ev:
-            ev[0].record(stream)
-        u_new, err = ds.pixel_map_search(dref, u_t, di_t, dj_t, cfg.half_ss, cfg.half_fs,
-                                         cfg.subpixel_grid, cfg.refine)
-        if ev:
-            ev[1].record(stream)
-        if cfg.update_translations:
-            ds.translation_search(dref, u_new, di_t, dj_t, cfg.t_half_ss, cfg.t_half_fs,
-                                  cfg.t_subpixel_grid)
-        ds.error_maps(dref, u_new, di_t, dj_t)
+            u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev)
+        else:
+            dref = ds.object_map(u, di, dj)
+            if ev:
+                ev[0].record(stream)
+            u_new, err = ds.pixel_map_search(dref, u, di, dj, cfg.half_ss, cfg.half_fs,
+                                             cfg.subpixel_grid, cfg.refine)
+            if ev:
+                ev[1].record(stream)
+            di_new, dj_new = di, dj
+            if cfg.update_translations:
+                di_new, dj_new = ds.translation_search(dref, u_new, di, dj, cfg.t_half_ss,
+                                                       cfg.t_half_fs, cfg.t_subpixel_grid)
+            ds.error_maps(dref, u_new, di_new, dj_new)
+        state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
@@ -307,6 +318,8 @@ def run_ours(args, rank, world, local):
            "config": base_config(cfg),
            "workload_detail": {"work_pixels": ds.n_work, "trials_per_iteration": trials,
                                "l2": "flushed between timed steps (256 MiB write, untimed)",
+                               "sequence": f"steps cycle through the config's {cfg.iters}-iteration "
+                                           "run from the initial (noisy) state, state carried",
                                "parallelism": (f"rows/frames sharded x{world}" if world > 1
                                                else "single GPU")},
            "full_iteration_ms": ms_per_step, "gpu_launches": launches,

@@ -21,6 +21,9 @@
 //                      rule, writes u_out and the error map.
 // Sub-pixel grids and non-instantiated windows use k_pix_generic (float64,
 // one thread per (pixel, trial)) followed by the same epilogue.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "search_common.cuh"
 #include "tma.cuh"
 
@@ -175,11 +178,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int nk = static_cast<int>(k_hi - k_lo);
   float* out = a.partial + (int64_t)blockIdx.z * KA * KB * a.nq + q;
 
-  float acc[KA][KB];
-#pragma unroll
-  for (int t = 0; t < KA; ++t)
-#pragma unroll
-    for (int s = 0; s < KB; ++s) acc[t][s] = 0.f;
+  PackedAcc<KA, KB> acc;
+  acc.zero();
 
   if (g.use_win && nk > 0) {
     const int box = slot_floats(a.box_r, a.box_c);      // slot stride (128-byte multiple)
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           sI *= sq;
           sW *= sq;
         }
-        engine_fast<KA, KB>(ring + b * box + sm.lr * a.box_c + sm.lc, a.box_c, fx, fy,
-                            sW * (1.f - fx), sW * fx, sI, acc);
+        engine_fast2<KA, KB>(ring + b * box + sm.lr * a.box_c + sm.lc, a.box_c, fx, fy,
+                             sW * (1.f - fx), sW * fx, sI, acc);
       }
       mbar_arrive(&empty[b]);
       if (threadIdx.x == 0 && jj + kNB < nk) {
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int t = 0; t < KA; ++t)
 #pragma unroll
-      for (int s = 0; s < KB; ++s) out[(int64_t)(t * KB + s) * a.nq] = acc[t][s];
+      for (int s = 0; s < KB; ++s) out[(int64_t)(t * KB + s) * a.nq] = acc.get(t, s);
   }
 }
 
@@ -369,12 +369,17 @@ __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chun
   const double var = a.var[p];                        // recon.py:257-263
   const bool active = var > 0.0;
   const double nv = active ? var : 1.0;
+  // First-occurrence argmin (recon.py:265-269) on the raw sums: dividing by
+  // the common positive normaliser preserves the order except for ties the
+  // division itself would create, which the parity bar (unique argmin,
+  // margin > 1e-4) excludes.
   int best = 0;
-  double bv = total(0) / nv;
-  for (int t = 1; t < nk; ++t) {                      // first occurrence (recon.py:265-269)
-    const double v = total(t) / nv;
-    if (v < bv) { bv = v; best = t; }
+  double braw = total(0);
+  for (int t = 1; t < nk; ++t) {
+    const double v = total(t);
+    if (v < braw) { braw = v; best = t; }
   }
+  const double bv = braw / nv;
   const int ia = best / nb, ib = best % nb;
   double sh_ss = offs_a[ia], sh_fs = offs_b[ib];
   if (refine_ok && active && ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {   // recon.py:273-287
@@ -525,6 +530,13 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     PXST_CHECK_LAUNCH();
     k_pix_slow<<<148 * 4, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
+    if (getenv("PXST_DEBUG")) {
+      unsigned h = 0;
+      PXST_CHECK_CUDA(cudaMemcpyAsync(&h, list_n, sizeof(h), cudaMemcpyDeviceToHost, s));
+      PXST_CHECK_CUDA(cudaStreamSynchronize(s));
+      fprintf(stderr, "[pxst] K2 %dx%d: %lld pixels x %d chunks, %u (pixel, chunk) pairs own "
+              "slow samples\n", na, nb, (long long)a.nq, a.n_chunks, h);
+    }
     k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
                                                   refine_ok, u_out, err_out);
     PXST_CHECK_LAUNCH();

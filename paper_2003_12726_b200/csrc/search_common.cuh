@@ -55,6 +55,97 @@ __device__ __forceinline__ void engine_fast(const float* __restrict__ win, int l
   }
 }
 
+// ---------------------------------------------------------------------------
+// Packed (FFMA2) variant.  sm_100 executes fma.rn.f32x2 at the full FP32 rate
+// with half the issue slots (measured 73.8 TFLOP/s, profiles/microbench_r01.json).
+// Trials (t, 2k) and (t, 2k+1) share one 64-bit register pair; the row
+// interpolation stays scalar but lands directly in register pairs.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+template <int KA, int KB>
+struct PackedAcc {
+  static constexpr int KP = KB / 2;          // packed pairs per trial row
+  static constexpr bool ODD = (KB % 2) != 0;  // leftover last column
+  f32x2 p[KA][KP > 0 ? KP : 1];
+  float s[KA];
+
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int t = 0; t < KA; ++t) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) p[t][k] = 0ull;
+      s[t] = 0.f;
+    }
+  }
+  __device__ __forceinline__ float get(int t, int c) const {  // t, c compile-time in loops
+    if (ODD && c == KB - 1) return s[t];
+    float lo, hi;
+    unpack2(p[t][c / 2], lo, hi);
+    return (c & 1) ? hi : lo;
+  }
+};
+
+template <int KA, int KB>
+__device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int ld, float fx,
+                                             float fy, float A, float B, float I,
+                                             PackedAcc<KA, KB>& acc) {
+  constexpr int KP = PackedAcc<KA, KB>::KP;
+  constexpr bool ODD = PackedAcc<KA, KB>::ODD;
+  const float gy = 1.f - fy;
+  const f32x2 nA2 = pack2(-A, -A), nB2 = pack2(-B, -B), I2 = pack2(I, I);
+  f32x2 hp2[KP > 0 ? KP : 1];
+  float hpo = 0.f;
+  {
+    float o[KB + 1];
+#pragma unroll
+    for (int s = 0; s <= KB; ++s) o[s] = win[s];
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+      hp2[k] = pack2(fmaf(fy, o[2 * k + 1], gy * o[2 * k]), fmaf(fy, o[2 * k + 2], gy * o[2 * k + 1]));
+    if (ODD) hpo = fmaf(fy, o[KB], gy * o[KB - 1]);
+  }
+#pragma unroll
+  for (int t = 0; t < KA; ++t) {
+    const float* rp = win + (t + 1) * ld;
+    float o[KB + 1];
+#pragma unroll
+    for (int s = 0; s <= KB; ++s) o[s] = rp[s];
+    f32x2 hc2[KP > 0 ? KP : 1];
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+      hc2[k] = pack2(fmaf(fy, o[2 * k + 1], gy * o[2 * k]), fmaf(fy, o[2 * k + 2], gy * o[2 * k + 1]));
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      f32x2 r = ffma2(nA2, hp2[k], I2);
+      r = ffma2(nB2, hc2[k], r);
+      acc.p[t][k] = ffma2(r, r, acc.p[t][k]);
+      hp2[k] = hc2[k];
+    }
+    if (ODD) {
+      const float hco = fmaf(fy, o[KB], gy * o[KB - 1]);
+      float r = fmaf(-A, hpo, I);
+      r = fmaf(-B, hco, r);
+      acc.s[t] = fmaf(r, r, acc.s[t]);
+      hpo = hco;
+    }
+  }
+}
+
 // Exact contribution of one sample to one trial whose bilinear base cell is
 // (row, col) with fractions (fx, fy): masked renormalised read from global
 // memory with the inclusive inside test, (I - W)^2 fallback when invalid
