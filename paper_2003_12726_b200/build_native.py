@@ -17,11 +17,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-BUILD = os.path.join(ROOT, "build", "pxst")
-LIB = os.path.join(HERE, "libpxst_b200.so")
+BUILD = os.environ.get("PXST_BUILD_DIR", os.path.join(ROOT, "build", "pxst"))
+LIB = os.environ.get("PXST_LIB_OUT", os.path.join(HERE, "libpxst_b200.so"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+FLAGS += os.environ.get("PXST_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:

@@ -152,7 +152,10 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
 // 2. fast kernel (TMA ring + register engine)
 // ---------------------------------------------------------------------------
 template <int KA, int KB>
-__global__ void __launch_bounds__(kThreads, 2)
+#ifndef PXST_K2_OCC
+#define PXST_K2_OCC 3
+#endif
+__global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
   constexpr int RA = (KA - 1) / 2, RB = (KB - 1) / 2;
   extern __shared__ __align__(128) unsigned char ring_raw[];
@@ -160,7 +163,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
   // (Pointer arithmetic on the shared array keeps the address space, so the
   // engine's reads compile to LDS rather than generic loads.)
-  float* ring = reinterpret_cast<float*>(ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u));
+  unsigned char* base = ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u);
+  float* ring = reinterpret_cast<float*>(base);
+  const int box = slot_floats(a.box_r, a.box_c);          // slot stride (128-byte multiple)
+  // Per-frame table of the chunk (frame index, di, dj) after the ring.
+  double* t_di = reinterpret_cast<double*>(base + sizeof(float) * kNB * box);
+  double* t_dj = t_di + a.chunk;
+  int* t_f = reinterpret_cast<int*>(t_dj + a.chunk);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
@@ -182,13 +191,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   acc.zero();
 
   if (g.use_win && nk > 0) {
-    const int box = slot_floats(a.box_r, a.box_c);      // slot stride (128-byte multiple)
     const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
     const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+    for (int jj = threadIdx.x; jj < nk; jj += kThreads) {
+      const int f = a.sc.good[k_lo + jj];
+      t_f[jj] = f;
+      t_di[jj] = a.di[f];
+      t_dj[jj] = a.dj[f];
+    }
     auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
-      const int64_t f = a.sc.good[k_lo + jj];
-      const int wr0 = static_cast<int>(floor(g.umin0 - a.di[f] - n0d)) - RA;
-      const int wc0 = align4_down(static_cast<int>(floor(g.umin1 - a.dj[f] - m0d)) - RB);
+      const int wr0 = static_cast<int>(floor(g.umin0 - t_di[jj] - n0d)) - RA;
+      const int wc0 = align4_down(static_cast<int>(floor(g.umin1 - t_dj[jj] - m0d)) - RB);
       const int b = jj % kNB;
       mbar_arrive_expect_tx(&full[b], bytes);
       tma_load_2d(ring + b * box, &tmap, wc0, wr0, &full[b]);
@@ -207,18 +220,25 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
     const float W = live ? a.sc.w32[p] : 0.f;
-    float I_next = live ? __ldg(a.sc.frames + (int64_t)a.sc.good[k_lo] * plane + p) : 0.f;
+    auto sample_of = [&](int jj, float& I, float& fwv) {
+      const int64_t f = t_f[jj];
+      I = live ? __ldg(a.sc.frames + f * plane + p) : 0.f;
+      fwv = (live && a.fw) ? __ldg(a.fw + f * plane + p) : 1.f;
+      return make_sample(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f);
+    };
+    // One-frame-ahead pipeline of the per-sample geometry, stack value and
+    // patch-valid lookup, so their global-load latency hides behind the
+    // current frame's trials.
+    float I_n, fw_n;
+    Sample s_n = sample_of(0, I_n, fw_n);
     for (int jj = 0; jj < nk; ++jj) {
-      const int64_t f = a.sc.good[k_lo + jj];
+      const Sample sm = s_n;
+      const float I = I_n, fwv = fw_n;
+      if (jj + 1 < nk) s_n = sample_of(jj + 1, I_n, fw_n);
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
-      const float I = I_next;
-      if (live && jj + 1 < nk) I_next = __ldg(a.sc.frames + (int64_t)a.sc.good[k_lo + jj + 1] * plane + p);
-      float fwv = 1.f;
-      if (live && a.fw) fwv = __ldg(a.fw + f * plane + p);
-      const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
       mbar_wait(&full[b], ph);
-      if (live && sm.fast) {
+      if (sm.fast) {
         const float fx = static_cast<float>(sm.fx), fy = static_cast<float>(sm.fy);
         float sI = I, sW = W;
         if (a.fw) {
@@ -276,10 +296,42 @@ __global__ void k_pix_classify(PixArgs a, unsigned long long* list, unsigned* li
   }
 }
 
+// Exact trial from a staged patch (same semantics as masked_read): the patch
+// covers object rows [pr0, pr0 + ka] x cols [pc0, pc0 + kb]; cells outside
+// the grid are stored invalid.
+__device__ __forceinline__ float trial_patch(const float* __restrict__ pf,
+                                             const uint8_t* __restrict__ pvld, int ld, int pr0,
+                                             int pc0, int64_t os, int64_t of, int row, int col,
+                                             double fx, double fy, float W, float I, float fwv) {
+  const float d0 = I - W;
+  const float fb = fwv * (d0 * d0);
+  if (!inside_1d(row, fx, os) || !inside_1d(col, fy, of)) return fb;
+  const int r1 = min(row + 1, static_cast<int>(os - 1)), c1 = min(col + 1, static_cast<int>(of - 1));
+  const int a00 = (row - pr0) * ld + (col - pc0), a01 = (row - pr0) * ld + (c1 - pc0);
+  const int a10 = (r1 - pr0) * ld + (col - pc0), a11 = (r1 - pr0) * ld + (c1 - pc0);
+  const bool m00 = pvld[a00], m01 = pvld[a01], m10 = pvld[a10], m11 = pvld[a11];
+  const bool any = m00 || (fy > 0.0 && m01) || (fx > 0.0 && m10) || (fx > 0.0 && fy > 0.0 && m11);
+  if (!any) return fb;
+  const float gx = static_cast<float>(fx), gy = static_cast<float>(fy);
+  const float w00 = (1.f - gx) * (1.f - gy), w01 = (1.f - gx) * gy;
+  const float w10 = gx * (1.f - gy), w11 = gx * gy;
+  float den = 0.f, num = 0.f;
+  if (m00) { den += w00; num = fmaf(w00, pf[a00], num); }
+  if (m01) { den += w01; num = fmaf(w01, pf[a01], num); }
+  if (m10) { den += w10; num = fmaf(w10, pf[a10], num); }
+  if (m11) { den += w11; num = fmaf(w11, pf[a11], num); }
+  const float r = fmaf(-W, num / den, I);
+  return fwv * (r * r);
+}
+
 __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ list,
                            const unsigned* __restrict__ list_n) {
+  extern __shared__ __align__(16) unsigned char slow_sm[];
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int ld = a.kb + 1, pn = (a.ka + 1) * ld;
+  float* pf = reinterpret_cast<float*>(slow_sm) + wib * pn;
+  uint8_t* pvld = slow_sm + sizeof(float) * pn * (blockDim.x >> 5) + wib * pn;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned n = *list_n;
@@ -298,16 +350,38 @@ __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ lis
     float* out = a.partial + (int64_t)chunk * nk * a.nq + q;
     const int64_t k_lo = (int64_t)chunk * a.chunk;
     const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
-    for (int64_t k = k_lo; k < k_hi; ++k) {
-      const int64_t f = a.sc.good[k];
-      float fwv = 1.f;
-      if (a.fw) fwv = __ldg(a.fw + f * plane + p);
-      const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
-      if (sm.fast) continue;                      // warp-uniform
-      const float I = __ldg(a.sc.frames + f * plane + p);
-      for (int t = lane; t < nk; t += 32)
-        out[(int64_t)t * a.nq] += trial_exact(a.fm, a.valid, a.os, a.of, sm.i - ra + t / a.kb,
-                                              sm.j - rb + t % a.kb, sm.fx, sm.fy, W, I, fwv);
+    for (int64_t k0 = k_lo; k0 < k_hi; k0 += 32) {
+      // lane-parallel classification of 32 frames
+      const int64_t kl = k0 + lane;
+      bool slow = false;
+      if (kl < k_hi) {
+        const int64_t f = a.sc.good[kl];
+        const float fwv = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
+        slow = !make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast;
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, slow);
+      while (mask) {
+        const int bsel = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int64_t f = a.sc.good[k0 + bsel];
+        const float fwv = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
+        const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
+        const float I = __ldg(a.sc.frames + f * plane + p);
+        const int pr0 = sm.i - ra, pc0 = sm.j - rb;
+        for (int idx = lane; idx < pn; idx += 32) {
+          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
+          const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
+          const int64_t o = in ? (int64_t)r * a.of + c : 0;
+          pf[idx] = in ? __ldg(a.fm + o) : 0.f;
+          pvld[idx] = in ? __ldg(a.valid + o) : 0;
+        }
+        __syncwarp();
+        for (int t = lane; t < nk; t += 32)
+          out[(int64_t)t * a.nq] += trial_patch(pf, pvld, ld, pr0, pc0, a.os, a.of,
+                                                pr0 + t / a.kb, pc0 + t % a.kb, sm.fx, sm.fy, W,
+                                                I, fwv);
+        __syncwarp();
+      }
     }
   }
 }
@@ -514,7 +588,8 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
     k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
-    const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128;
+    const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
+                        (2 * sizeof(double) + sizeof(int)) * a.chunk;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
@@ -528,7 +603,8 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     dim3 gs(qblocks, (unsigned)a.n_chunks);
     k_pix_classify<<<gs, 128, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
-    k_pix_slow<<<148 * 4, 256, 0, s>>>(a, list, list_n);
+    const size_t slow_smem = (sizeof(float) + 1) * (na + 1) * (nb + 1) * 8;
+    k_pix_slow<<<148 * 4, 256, slow_smem, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;
