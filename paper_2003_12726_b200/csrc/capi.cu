@@ -20,6 +20,19 @@ int set_error(int code, const char* fmt, ...) {
 
 void count_launch(int n) { g_launches += n; }
 
+void retain_pool_memory() {
+  static thread_local int done_mask = 0;   // devices 0..31 configured by this thread
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) return;
+  if (done_mask & (1 << dev)) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_mask |= 1 << dev;
+}
+
 }  // namespace pxst
 
 extern "C" int pxst_abi_version(void) { return PXST_ABI_VERSION; }

@@ -39,6 +39,11 @@ void count_launch(int n = 1);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Keep memory freed with cudaFreeAsync in the device's default pool across
+// synchronisations (the default release threshold of 0 hands it back to the
+// OS at every sync, making the next cudaMallocAsync re-map pages: ms per call).
+void retain_pool_memory();
+
 // Stream-ordered scratch buffer, released on the stream at scope exit.
 struct Scratch {
   void* p = nullptr;
@@ -48,6 +53,7 @@ struct Scratch {
   Scratch& operator=(const Scratch&) = delete;
   int alloc(size_t bytes, cudaStream_t stream) {
     s = stream;
+    retain_pool_memory();
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMallocAsync(&p, bytes, stream);
     if (e != cudaSuccess) {
