@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;
 constexpr int kNB = 4;  // TMA ring depth
+constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
 
 struct TileGeo {
   double umin0, umin1;  // NaN when the tile has no work pixel
@@ -153,7 +154,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
 // ---------------------------------------------------------------------------
 template <int KA, int KB>
 #ifndef PXST_K2_OCC
-#define PXST_K2_OCC 3
+#define PXST_K2_OCC 2
 #endif
 __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
@@ -350,6 +351,9 @@ __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ lis
     float* out = a.partial + (int64_t)chunk * nk * a.nq + q;
     const int64_t k_lo = (int64_t)chunk * a.chunk;
     const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+    float part[kSlowPerLane];          // lane owns trials lane + 32 j
+#pragma unroll
+    for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
     for (int64_t k0 = k_lo; k0 < k_hi; k0 += 32) {
       // lane-parallel classification of 32 frames
       const int64_t kl = k0 + lane;
@@ -376,12 +380,20 @@ __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ lis
           pvld[idx] = in ? __ldg(a.valid + o) : 0;
         }
         __syncwarp();
-        for (int t = lane; t < nk; t += 32)
-          out[(int64_t)t * a.nq] += trial_patch(pf, pvld, ld, pr0, pc0, a.os, a.of,
-                                                pr0 + t / a.kb, pc0 + t % a.kb, sm.fx, sm.fy, W,
-                                                I, fwv);
+#pragma unroll
+        for (int j = 0; j < kSlowPerLane; ++j) {
+          const int t = lane + 32 * j;
+          if (t < nk)
+            part[j] += trial_patch(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
+                                   pc0 + t % a.kb, sm.fx, sm.fy, W, I, fwv);
+        }
         __syncwarp();
       }
+    }
+#pragma unroll
+    for (int j = 0; j < kSlowPerLane; ++j) {
+      const int t = lane + 32 * j;
+      if (t < nk) out[(int64_t)t * a.nq] += part[j];
     }
   }
 }
