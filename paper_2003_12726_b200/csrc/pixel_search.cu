@@ -37,11 +37,6 @@ constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;
 constexpr int kNB = 4;  // TMA ring depth
 constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
 
-struct TileGeo {
-  double umin0, umin1;  // NaN when the tile has no work pixel
-  int use_win;
-  int pad;
-};
 
 struct PixArgs {
   pxst_scan sc;
@@ -61,15 +56,13 @@ struct PixArgs {
   int n_chunks, chunk;       // frame chunking of the good list
   int64_t nq;                // ROI rectangle pixel count
   float* partial;            // [n_chunks][ka*kb][nq]
+  unsigned long long* slow_list;  // (pixel << 20 | chunk) pairs owning skipped samples
+  unsigned* slow_n;
 };
 
 __host__ __device__ inline int box_rows_for(int ka) { return ka + 10; }
 __host__ __device__ inline int box_cols_for(int kb) { return ((kb + 52 + 3) / 4) * 4; }
-__host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
-// TMA on this stack faults ("illegal instruction") unless the box starts on a
-// 16-byte boundary in the innermost dimension (measured: fp32 column
-// coordinates must be multiples of 4), so window origins are aligned down.
-__host__ __device__ inline int align4_down(int c) { return c - (((c % 4) + 4) % 4); }
+
 
 // ---------------------------------------------------------------------------
 // 1. tile geometry
@@ -190,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 
   PackedAcc<KA, KB> acc;
   acc.zero();
+  bool any_slow = live && nk > 0 && !g.use_win;
 
   if (g.use_win && nk > 0) {
     const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
@@ -239,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
       mbar_wait(&full[b], ph);
+      any_slow |= live && !sm.fast;
       if (sm.fast) {
         const float fx = static_cast<float>(sm.fx), fy = static_cast<float>(sm.fy);
         float sI = I, sW = W;
@@ -263,40 +258,19 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 #pragma unroll
       for (int s = 0; s < KB; ++s) out[(int64_t)(t * KB + s) * a.nq] = acc.get(t, s);
   }
+  if (any_slow) {   // hand the skipped samples of this (pixel, chunk) to k_pix_slow
+    const unsigned slot = atomicAdd(a.slow_n, 1u);
+    a.slow_list[slot] = (static_cast<unsigned long long>(q) << 20) | blockIdx.z;
+  }
 }
 
 // ---------------------------------------------------------------------------
 // 3. slow-sample fix-up (runs after k_pix_fast on the same stream).
-//    k_pix_classify: one thread per (pixel, chunk) re-derives eligibility and
-//    appends (pixel, chunk) pairs that own skipped samples to a list.
-//    k_pix_slow: one warp per listed pair, lanes over trials, frames in
+//    k_pix_fast appends (pixel, chunk) pairs that own skipped samples to a
+//    list; k_pix_slow: one warp per listed pair, lanes over trials, frames in
 //    order; each (chunk, trial, pixel) partial is owned by one lane, so the
 //    result does not depend on list order.
 // ---------------------------------------------------------------------------
-__global__ void k_pix_classify(PixArgs a, unsigned long long* list, unsigned* list_n) {
-  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= a.nq) return;
-  const int64_t rr = q / cw, cc = q % cw;
-  const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
-  if (!a.sc.work[p]) return;
-  const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
-  const int64_t plane = a.sc.ss * a.sc.fs;
-  const double u0 = a.u[p], u1 = a.u[plane + p];
-  const int64_t k_lo = (int64_t)blockIdx.y * a.chunk;
-  const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
-  for (int64_t k = k_lo; k < k_hi; ++k) {
-    const int64_t f = a.sc.good[k];
-    float fwv = 1.f;
-    if (a.fw) fwv = __ldg(a.fw + f * plane + p);
-    if (!make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast) {
-      const unsigned slot = atomicAdd(list_n, 1u);
-      list[slot] = (static_cast<unsigned long long>(q) << 20) | blockIdx.y;
-      return;
-    }
-  }
-}
-
 // Exact trial from a staged patch (same semantics as masked_read): the patch
 // covers object rows [pr0, pr0 + ka] x cols [pc0, pc0 + kb]; cells outside
 // the grid are stored invalid.
@@ -604,16 +578,15 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
                         (2 * sizeof(double) + sizeof(int)) * a.chunk;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
-    dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
-    fn<<<gf, kThreads, smem, s>>>(tmap, a);
-    PXST_CHECK_LAUNCH();
     Scratch lst;
     if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 2), s)) return e;
     unsigned* list_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
     unsigned long long* list = lst.as<unsigned long long>() + 1;
     PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, sizeof(unsigned), s));
-    dim3 gs(qblocks, (unsigned)a.n_chunks);
-    k_pix_classify<<<gs, 128, 0, s>>>(a, list, list_n);
+    a.slow_list = list;
+    a.slow_n = list_n;
+    dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
+    fn<<<gf, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
     const size_t slow_smem = (sizeof(float) + 1) * (na + 1) * (nb + 1) * 8;
     k_pix_slow<<<148 * 4, 256, slow_smem, s>>>(a, list, list_n);

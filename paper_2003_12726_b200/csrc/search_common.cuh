@@ -205,6 +205,21 @@ __device__ __forceinline__ void paraboloid(const double (&e)[9], double& dss, do
   }
 }
 
+// Per-tile geometry of the TMA object windows (bounding box of u over the
+// tile's work pixels).
+struct TileGeo {
+  double umin0, umin1;  // NaN when the tile has no work pixel
+  int use_win;          // the tile's footprint fits the TMA box
+  int pad;
+};
+
+__host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
+// TMA on this stack faults ("illegal instruction") unless the box starts on a
+// 16-byte boundary in the innermost dimension (measured: fp32 column
+// coordinates must be multiples of 4; tools/tma_probe4.cu), so window origins
+// are aligned down and the patch offset absorbs the difference.
+__host__ __device__ inline int align4_down(int c) { return c - (((c % 4) + 4) % 4); }
+
 __device__ __forceinline__ int clamp_span(double v) {
   return v < 0.0 ? 0 : (v > 4096.0 ? 4096 : static_cast<int>(v));
 }

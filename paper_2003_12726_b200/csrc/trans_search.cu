@@ -1,18 +1,38 @@
 // K3: per-frame translation grid search (recon.py:336-385).
 //
-// One CTA per (searched frame, band of 16 detector rows): the band's object
-// window for that frame is staged in shared memory (cp.async), threads stride
-// over the band's pixels accumulating the phase group's Ka x Kb trial window
-// in registers (same engine as K2), then a deterministic CTA reduction writes
-// float32 partials[frame][band][trial].  A per-frame epilogue sums the bands
-// in float64 (fixed order), normalises by sum_p (I_n - W)^2, takes the
-// first-occurrence argmin and applies the reference's always-on paraboloid
-// (offset in grid-index units added in pixels).
+// err(n, a, b) = sum over work pixels of the masked-bilinear residual^2 at
+// u - (delta_n + off) - origin (note the minus sign, recon.py:373-374).
 //
-// Sub-pixel grids with integral 1/step (config 4: 0.25 px) decompose into
-// q^2 phase groups, each an integer window of the engine: trial k = q m + rho
-// sits at floor(x - step*rho) - m with the same fractions for every m.
+// Pipeline (integer grids and sub-pixel grids with integral 1/step):
+//   1. k_tile_geo3   per 16x64 pixel tile: u bounding box -> window origin
+//                    and "fits the TMA box" flag.
+//   2. k_trans_fast  grid (bands of 16 rows, searched frames).  The CTA walks
+//                    the band's column tiles; each tile's object window for
+//                    the frame is fetched by TMA into a 4-slot ring; every
+//                    thread (4 pixels per tile) runs the FFMA2 trial engine
+//                    into registers across all tiles; one deterministic CTA
+//                    reduction at the end writes float32
+//                    partial[frame][band][trial].  Samples whose patch leaves
+//                    the grid or touches an invalid cell are skipped and the
+//                    (frame, band) pair is listed.
+//   3. k_trans_slow  one warp per listed (frame, band): re-derives eligibility
+//                    lane-parallel over pixels, stages each skipped sample's
+//                    patch in shared memory, lanes over trials with the exact
+//                    masked read and (I-W)^2 fallback, register accumulation,
+//                    one add per trial into the partial (lane-owned: ordered).
+//   4. k_trans_epilogue per frame: float64 sum over bands (fixed order),
+//                    normalise by sum_p (I_n-W)^2, first-occurrence argmin,
+//                    always-on paraboloid when interior (grid-index units added
+//                    in pixels), write translations.
+// Sub-pixel grids with q = 1/step integral decompose into q^2 phase groups:
+// trial k = q m + rho sits at floor(x - step*rho) - m with fractions common
+// to every m, i.e. an integer window of the same engine (launched per phase).
+// Other grids use k_trans_generic (float64, CTA per (frame, trial)).
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "search_common.cuh"
+#include "tma.cuh"
 
 namespace pxst {
 
@@ -20,36 +40,10 @@ int check_scan(const pxst_scan* sc);
 
 namespace {
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  const int n = ok ? 4 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// Stage the [wr0, wr0+WR) x [wc0, wc0+WC) window of fm into smem (row pitch
-// WC), zero outside the grid.  Warps walk rows, lanes walk columns.
-__device__ __forceinline__ void stage_window(float* dst, const float* __restrict__ fm, int64_t os,
-                                             int64_t of, int wr0, int wc0, int WR, int WC) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = warp; r < WR; r += nw) {
-    const int gr = wr0 + r;
-    const bool rok = gr >= 0 && gr < os;
-    const float* srow = fm + (rok ? (int64_t)gr * of : 0);
-    for (int c = lane; c < WC; c += 32) {
-      const int gc = wc0 + c;
-      const bool ok = rok && gc >= 0 && gc < of;
-      cp_async4(dst + r * WC + c, ok ? srow + gc : fm, ok);
-    }
-  }
-}
-
-constexpr int kTrThreads = 256;
-constexpr int kTrBand = 16;   // detector rows per band
+constexpr int kTR = 16, kTC = 64;           // pixel tile
+constexpr int kThreads = 256;              // 8 warps: warp w -> tile rows 2w, 2w+1
+constexpr int kNB = 4;                      // TMA ring depth
+constexpr int kSlowPerLane = 6;             // ceil(max phase window 13x13 / 32)
 
 struct TransArgs {
   pxst_scan sc;
@@ -58,107 +52,338 @@ struct TransArgs {
   const double* dj;
   const float* fm;
   const uint8_t* valid;
-  const uint8_t* pv;
+  const uint8_t* pv;         // patch-valid map for the union box over phases
   int64_t os, of, n0, m0;
-  const double* band_mm;   // [n_bands][4] min/max u0, min/max u1 over work px
+  const TileGeo* geo;        // [n_bands][n_ct]
+  int n_ct;                  // column tiles per band
   int64_t n_bands;
-  int64_t frame_lo;        // first searched frame (index into good)
+  int64_t frame_lo;          // first searched frame of this launch (index into good)
   // phase group
-  double ph_a, ph_b;       // sub-pixel phase shifts s*rho (0 for integer grids)
-  int mhi_a, mhi_b;        // largest integer step of the phase group
-  int q_a, q_b;            // steps per pixel (1/step)
+  double ph_a, ph_b;         // sub-pixel phase shifts step*rho (0 for integer grids)
+  int mhi_a, mhi_b;          // largest integer step m of the phase group
+  int ka, kb;                // phase window (= template args in the fast kernel)
+  int q_a, q_b;              // steps per pixel (1/step)
   int rho_a, rho_b;
-  int kh_a, kh_b;          // full-grid half counts (offset index = k + kh)
+  int kh_a, kh_b;            // full-grid half counts (offset index = k + kh)
   int na_full, nb_full;
-  float* partial;          // [n_frames_chunk][n_bands][na_full*nb_full]
-  int win_cap;
+  int box_r, box_c;          // TMA box
+  int pv_lr, pv_hr, pv_lc, pv_hc;  // union patch box rows/cols relative to floor(x_rho)
+  float* partial;            // [chunk frames][n_bands][na_full*nb_full]
+  unsigned long long* slow_list;   // (frame_in_chunk << 24 | band) pairs with skipped samples
+  unsigned* slow_n;
 };
 
+// Boxes cover a 16x64 tile's footprint for |du/dx| up to ~1.1 plus noise.
+__host__ __device__ inline int box_rows3(int ka) { return ka + 24; }
+__host__ __device__ inline int box_cols3(int kb) { return ((kb + 76 + 3) / 4) * 4; }
+
+// ---------------------------------------------------------------------------
+// 1. tile geometry (16 x 64 tiles)
+// ---------------------------------------------------------------------------
+__global__ void k_tile_geo3(pxst_scan sc, const double* __restrict__ u, int ka, int kb,
+                            int box_r, int box_c, TileGeo* geo) {
+  __shared__ double red[kThreads / 32][4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t plane = sc.ss * sc.fs;
+  double mn0 = INFINITY, mx0 = -INFINITY, mn1 = INFINITY, mx1 = -INFINITY;
+  for (int e = threadIdx.x; e < kTR * kTC; e += kThreads) {
+    const int64_t row = sc.roi[0] + (int64_t)blockIdx.y * kTR + e / kTC;
+    const int64_t col = sc.roi[2] + (int64_t)blockIdx.x * kTC + e % kTC;
+    if (row >= sc.roi[1] || col >= sc.roi[3]) continue;
+    const int64_t p = row * sc.fs + col;
+    if (!sc.work[p]) continue;
+    mn0 = fmin(mn0, u[p]); mx0 = fmax(mx0, u[p]);
+    mn1 = fmin(mn1, u[plane + p]); mx1 = fmax(mx1, u[plane + p]);
+  }
+  mn0 = warp_min(mn0); mx0 = warp_max(mx0); mn1 = warp_min(mn1); mx1 = warp_max(mx1);
+  if (lane == 0) { red[warp][0] = mn0; red[warp][1] = mx0; red[warp][2] = mn1; red[warp][3] = mx1; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < kThreads / 32; ++w) {
+    mn0 = fmin(red[0][0], red[w][0]); red[0][0] = mn0;
+    mx0 = fmax(red[0][1], red[w][1]); red[0][1] = mx0;
+    mn1 = fmin(red[0][2], red[w][2]); red[0][2] = mn1;
+    mx1 = fmax(red[0][3], red[w][3]); red[0][3] = mx1;
+  }
+  mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
+  TileGeo g;
+  g.pad = 0;
+  if (!(mn0 <= mx0)) {
+    g.umin0 = g.umin1 = NAN;
+    g.use_win = 0;
+  } else {
+    g.umin0 = mn0;
+    g.umin1 = mn1;
+    const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
+    // +1 row/col: the sub-pixel phase shift can move floor() by one.
+    const int wr = clamp_span(floor(mx0 - mn0)) + ka + 3;
+    const int wc = clamp_span(floor(mx1 - mn1)) + kb + 3 + 3;
+    g.use_win = finite && wr <= box_r && wc <= box_c;
+  }
+  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = g;
+}
+
+struct Sample3 {
+  int i, j;
+  double fx, fy;
+  int lr, lc;
+  bool fast;
+};
+
+// Geometry of one (frame, pixel) sample for the current phase, shared by the
+// fast and slow kernels.  x_rho = (u0 - d - n0) - step*rho; trial m sits at
+// floor(x_rho) - m; the engine patch starts at floor(x_rho) - mhi.
+__device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const TileGeo& g, double u0,
+                                                double u1, double dI, double dJ) {
+  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+  Sample3 s;
+  const double x = (u0 - dI - n0d) - a.ph_a;
+  const double y = (u1 - dJ - m0d) - a.ph_b;
+  const double xf = floor(x), yf = floor(y);
+  s.fx = x - xf;
+  s.fy = y - yf;
+  const bool finite = fabs(x) < 1e9 && fabs(y) < 1e9;
+  s.i = finite ? static_cast<int>(xf) : -(1 << 30);
+  s.j = finite ? static_cast<int>(yf) : -(1 << 30);
+  s.fast = false;
+  s.lr = s.lc = 0;
+  if (g.use_win) {
+    const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
+    const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
+    s.lr = s.i - a.mhi_a - wr0;
+    s.lc = s.j - a.mhi_b - wc0;
+    s.fast = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of &&
+             a.pv[(int64_t)s.i * a.of + s.j] != 0 && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r &&
+             s.lc >= 0 && s.lc + a.kb + 1 <= a.box_c;
+  }
+  return s;
+}
+
+// full-grid trial index of phase-local engine trial (t, s)
+__device__ __forceinline__ int full_index(const TransArgs& a, int t, int s) {
+  const int ia = a.q_a * (a.mhi_a - t) + a.rho_a + a.kh_a;
+  const int ib = a.q_b * (a.mhi_b - s) + a.rho_b + a.kh_b;
+  return ia * a.nb_full + ib;
+}
+
+// ---------------------------------------------------------------------------
+// 2. fast kernel
+// ---------------------------------------------------------------------------
 template <int KA, int KB>
-__global__ void __launch_bounds__(kTrThreads, (KA * KB <= 81) ? 2 : 1) k_trans_partial(TransArgs a) {
-  extern __shared__ float win[];
-  __shared__ float red[kTrThreads / 32][KA * KB];
+__global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
+    k_trans_fast(const __grid_constant__ CUtensorMap tmap, TransArgs a) {
+  extern __shared__ __align__(128) unsigned char ring_raw[];
+  __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
+  __shared__ float red[kThreads / 32][KA * KB];
+  unsigned char* base = ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u);
+  float* ring = reinterpret_cast<float*>(base);
+  const int box = slot_floats(a.box_r, a.box_c);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int band = blockIdx.x;
-  const int64_t kk = blockIdx.y;                       // frame within the chunk
+  const int64_t kk = blockIdx.y;                     // frame within this launch's chunk
   const int64_t f = a.sc.good[a.frame_lo + kk];
-  const int64_t r_lo = a.sc.roi[0] + (int64_t)band * kTrBand;
-  const int64_t r_hi = min(a.sc.roi[1], r_lo + kTrBand);
-  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  const int64_t nq = (r_hi - r_lo) * cw;
+  const double dI = a.di[f], dJ = a.dj[f];
   const int64_t plane = a.sc.ss * a.sc.fs;
-  const double mn0 = a.band_mm[4 * band], mx0 = a.band_mm[4 * band + 1];
-  const double mn1 = a.band_mm[4 * band + 2], mx1 = a.band_mm[4 * band + 3];
+  const float* frame = a.sc.frames + f * plane;
+  const TileGeo* grow = a.geo + (int64_t)band * a.n_ct;
+  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+  const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
 
-  float acc[KA][KB];
-#pragma unroll
-  for (int t = 0; t < KA; ++t)
-#pragma unroll
-    for (int s = 0; s < KB; ++s) acc[t][s] = 0.f;
+  PackedAcc<KA, KB> acc;
+  acc.zero();
+  bool any_slow = false;
 
-  if (mn0 <= mx0) {
-    // x_rho = (u0 - di - n0) - s*rho; trial m -> base row floor(x_rho) - m,
-    // engine row t <-> m = mhi - t (recon.py:373-374 sign convention).
-    const double xs = a.di[f] + static_cast<double>(a.n0) + a.ph_a;
-    const double ys = a.dj[f] + static_cast<double>(a.m0) + a.ph_b;
-    const int WR = clamp_span(floor(mx0 - mn0)) + KA + 2;
-    const int WC = clamp_span(floor(mx1 - mn1)) + KB + 2;
-    const bool use_win = WR * WC <= a.win_cap && fabs(mn0) < 1e9 && fabs(mn1) < 1e9;
-    const int wr0 = use_win ? static_cast<int>(floor(mn0 - xs)) - a.mhi_a : 0;
-    const int wc0 = use_win ? static_cast<int>(floor(mn1 - ys)) - a.mhi_b : 0;
-    if (use_win) stage_window(win, a.fm, a.os, a.of, wr0, wc0, WR, WC);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    const float* frame = a.sc.frames + f * plane;
-    for (int64_t q = threadIdx.x; q < nq; q += kTrThreads) {
-      const int64_t p = (r_lo + q / cw) * a.sc.fs + a.sc.roi[2] + q % cw;
-      if (!a.sc.work[p]) continue;
-      const double x = (a.u[p] - a.di[f] - static_cast<double>(a.n0)) - a.ph_a;
-      const double y = (a.u[plane + p] - a.dj[f] - static_cast<double>(a.m0)) - a.ph_b;
-      const double xf = floor(x), yf = floor(y);
-      const double fxd = x - xf, fyd = y - yf;
-      const bool finite = fabs(x) < 1e9 && fabs(y) < 1e9;
-      const int i = finite ? static_cast<int>(xf) : -(1 << 30);
-      const int j = finite ? static_cast<int>(yf) : -(1 << 30);
-      const float I = __ldg(frame + p);
-      const float W = a.sc.w32[p];
-      const int pr = i - a.mhi_a, pc = j - a.mhi_b;
-      bool fast = use_win && i >= 0 && i < a.os && j >= 0 && j < a.of &&
-                  a.pv[(int64_t)i * a.of + j] != 0;
-      const int lr = pr - wr0, lc = pc - wc0;
-      fast = fast && lr >= 0 && lr + KA + 1 <= WR && lc >= 0 && lc + KB + 1 <= WC;
-      if (fast) {
-        const float fx = static_cast<float>(fxd), fy = static_cast<float>(fyd);
-        engine_fast<KA, KB>(win + lr * WC + lc, WC, fx, fy, W * (1.f - fx), W * fx, I, acc);
-      } else {
-        engine_slow<KA, KB>(a.fm, a.valid, a.os, a.of, pr, pc, fxd, fyd, W, I, 1.f, acc);
-      }
+  auto issue = [&](int ct) {
+    const TileGeo g = grow[ct];
+    const int b = ct % kNB;
+    if (g.use_win) {
+      const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
+      const int wc0 =
+          align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
+      mbar_arrive_expect_tx(&full[b], bytes);
+      tma_load_2d(ring + b * box, &tmap, wc0, wr0, &full[b]);
+    } else {
+      mbar_arrive(&full[b]);           // nothing to fetch: complete the phase directly
+    }
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmap);
+    for (int b = 0; b < kNB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kThreads);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int ct = 0; ct < min(kNB, a.n_ct); ++ct) issue(ct);
+
+  for (int ct = 0; ct < a.n_ct; ++ct) {
+    const int b = ct % kNB;
+    const unsigned ph = (ct / kNB) & 1;
+    const TileGeo g = grow[ct];
+    // this thread's 4 pixels of the tile: rows 2w, 2w+1; cols lane, lane+32
+    // compact per-sample state (5 registers each) to keep the window in registers
+    float I[4], W[4], fx[4], fy[4];
+    int off[4];                        // patch origin offset in the slot, -1 = not fast
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t row = a.sc.roi[0] + (int64_t)band * kTR + 2 * warp + (e >> 1);
+      const int64_t col = a.sc.roi[2] + (int64_t)ct * kTC + lane + 32 * (e & 1);
+      const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
+      const int64_t p = in ? row * a.sc.fs + col : 0;
+      const bool live = in && a.sc.work[p] != 0;
+      I[e] = live ? __ldg(frame + p) : 0.f;
+      W[e] = live ? a.sc.w32[p] : 0.f;
+      const Sample3 sm =
+          make_sample3(a, g, live ? a.u[p] : 0.0, live ? a.u[plane + p] : 0.0, dI, dJ);
+      fx[e] = static_cast<float>(sm.fx);
+      fy[e] = static_cast<float>(sm.fy);
+      off[e] = (live && sm.fast) ? sm.lr * a.box_c + sm.lc : -1;
+      any_slow |= live && !sm.fast;
+    }
+    mbar_wait(&full[b], ph);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (off[e] >= 0)
+        engine_fast2<KA, KB>(ring + b * box + off[e], a.box_c, fx[e], fy[e],
+                             W[e] * (1.f - fx[e]), W[e] * fx[e], I[e], acc);
+    }
+    mbar_arrive(&empty[b]);
+    if (threadIdx.x == 0 && ct + kNB < a.n_ct) {
+      mbar_wait(&empty[b], ph);
+      issue(ct + kNB);
     }
   }
-  // Deterministic CTA reduction: warp shuffles, then fixed-order sum of warps.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // deterministic CTA reduction: warp shuffles, then a fixed-order sum of warps
 #pragma unroll
   for (int t = 0; t < KA; ++t)
 #pragma unroll
     for (int s = 0; s < KB; ++s) {
-      const float v = warp_sumf(acc[t][s]);
+      const float v = warp_sumf(acc.get(t, s));
       if (lane == 0) red[warp][t * KB + s] = v;
     }
-  __syncthreads();
+  const int any = __syncthreads_or(any_slow ? 1 : 0);
   const int nk = a.na_full * a.nb_full;
   float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
-  for (int e = threadIdx.x; e < KA * KB; e += kTrThreads) {
+  for (int e = threadIdx.x; e < KA * KB; e += kThreads) {
     float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < kTrThreads / 32; ++w) v += red[w][e];
-    const int t = e / KB, s = e % KB;
-    const int ia = a.q_a * (a.mhi_a - t) + a.rho_a + a.kh_a;
-    const int ib = a.q_b * (a.mhi_b - s) + a.rho_b + a.kh_b;
-    out[ia * a.nb_full + ib] = v;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[w][e];
+    out[full_index(a, e / KB, e % KB)] = v;
+  }
+  if (any && threadIdx.x == 0) {
+    const unsigned slot = atomicAdd(a.slow_n, 1u);
+    a.slow_list[slot] = (static_cast<unsigned long long>(kk) << 24) | static_cast<unsigned>(band);
   }
 }
 
-// Generic K3: one CTA per (searched frame, full-grid trial), float64.
+// ---------------------------------------------------------------------------
+// 3. slow fix-up: warp per listed (frame, band)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float trial_patch3(const float* __restrict__ pf,
+                                              const uint8_t* __restrict__ pvld, int ld, int pr0,
+                                              int pc0, int64_t os, int64_t of, int row, int col,
+                                              double fx, double fy, float W, float I) {
+  const float d0 = I - W;
+  const float fb = d0 * d0;
+  if (!inside_1d(row, fx, os) || !inside_1d(col, fy, of)) return fb;
+  const int r1 = min(row + 1, static_cast<int>(os - 1)), c1 = min(col + 1, static_cast<int>(of - 1));
+  const int a00 = (row - pr0) * ld + (col - pc0), a01 = (row - pr0) * ld + (c1 - pc0);
+  const int a10 = (r1 - pr0) * ld + (col - pc0), a11 = (r1 - pr0) * ld + (c1 - pc0);
+  const bool m00 = pvld[a00], m01 = pvld[a01], m10 = pvld[a10], m11 = pvld[a11];
+  const bool any = m00 || (fy > 0.0 && m01) || (fx > 0.0 && m10) || (fx > 0.0 && fy > 0.0 && m11);
+  if (!any) return fb;
+  const float gx = static_cast<float>(fx), gy = static_cast<float>(fy);
+  const float w00 = (1.f - gx) * (1.f - gy), w01 = (1.f - gx) * gy;
+  const float w10 = gx * (1.f - gy), w11 = gx * gy;
+  float den = 0.f, num = 0.f;
+  if (m00) { den += w00; num = fmaf(w00, pf[a00], num); }
+  if (m01) { den += w01; num = fmaf(w01, pf[a01], num); }
+  if (m10) { den += w10; num = fmaf(w10, pf[a10], num); }
+  if (m11) { den += w11; num = fmaf(w11, pf[a11], num); }
+  const float r = fmaf(-W, num / den, I);
+  return r * r;
+}
+
+__global__ void k_trans_slow(TransArgs a) {
+  extern __shared__ __align__(16) unsigned char slow_sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int ld = a.kb + 1, pn = (a.ka + 1) * ld;
+  float* pf = reinterpret_cast<float*>(slow_sm) + wib * pn;
+  uint8_t* pvld = slow_sm + sizeof(float) * pn * (blockDim.x >> 5) + wib * pn;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned n = *a.slow_n;
+  const int nk_ph = a.ka * a.kb, nk = a.na_full * a.nb_full;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  for (int64_t e = warp0; e < n; e += nwarps) {
+    const unsigned long long ent = a.slow_list[e];
+    const int64_t kk = static_cast<int64_t>(ent >> 24);
+    const int band = static_cast<int>(ent & 0xFFFFFF);
+    const int64_t f = a.sc.good[a.frame_lo + kk];
+    const double dI = a.di[f], dJ = a.dj[f];
+    const float* frame = a.sc.frames + f * plane;
+    const int64_t r_lo = a.sc.roi[0] + (int64_t)band * kTR;
+    const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
+    const int64_t npx = (r_hi - r_lo) * cw;
+    float part[kSlowPerLane];
+#pragma unroll
+    for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
+    for (int64_t q0 = 0; q0 < npx; q0 += 32) {
+      const int64_t ql = q0 + lane;
+      bool slow = false;
+      int64_t p = 0;
+      if (ql < npx) {
+        const int64_t rr = ql / cw, cc = ql % cw;
+        p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
+        if (a.sc.work[p]) {
+          const TileGeo g = a.geo[(int64_t)band * a.n_ct + cc / kTC];
+          slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
+        }
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, slow);
+      while (mask) {
+        const int bsel = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int64_t ps = __shfl_sync(0xffffffffu, p, bsel);
+        const int64_t cc = (q0 + bsel) % cw;
+        const TileGeo g = a.geo[(int64_t)band * a.n_ct + cc / kTC];
+        const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
+        const float I = __ldg(frame + ps), W = a.sc.w32[ps];
+        const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
+        for (int idx = lane; idx < pn; idx += 32) {
+          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
+          const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
+          const int64_t o = in ? (int64_t)r * a.of + c : 0;
+          pf[idx] = in ? __ldg(a.fm + o) : 0.f;
+          pvld[idx] = in ? __ldg(a.valid + o) : 0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kSlowPerLane; ++j) {
+          const int t = lane + 32 * j;
+          if (t < nk_ph)
+            part[j] += trial_patch3(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
+                                    pc0 + t % a.kb, sm.fx, sm.fy, W, I);
+        }
+        __syncwarp();
+      }
+    }
+    float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
+#pragma unroll
+    for (int j = 0; j < kSlowPerLane; ++j) {
+      const int t = lane + 32 * j;
+      if (t < nk_ph) out[full_index(a, t / a.kb, t % a.kb)] += part[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic (any grid): one CTA per (searched frame, full-grid trial), float64
+// ---------------------------------------------------------------------------
 __global__ void k_trans_generic(TransArgs a, const double* __restrict__ offs_a,
                                 const double* __restrict__ offs_b, double* __restrict__ errs) {
   __shared__ double sh[32];
@@ -197,9 +422,9 @@ __global__ void k_trans_generic(TransArgs a, const double* __restrict__ offs_a,
   }
 }
 
-// Per-frame epilogue: sum partials over bands (fixed order, float64),
-// normalise, first-occurrence argmin, paraboloid when interior (always, in
-// grid-index units added as pixels: recon.py:380-384), write translations.
+// ---------------------------------------------------------------------------
+// 4. per-frame epilogue
+// ---------------------------------------------------------------------------
 template <class T>
 __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_norm,
                                  const T* __restrict__ part, int64_t n_bands, int64_t frame_lo,
@@ -247,7 +472,7 @@ __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_
   if (idx == 0x7fffffff) idx = 0;   // all NaN/inf: numpy would pick the first
   const int ia = idx / nb, ib = idx % nb;
   double da = 0.0, db = 0.0;
-  if (ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {
+  if (ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {       // recon.py:381-382
     double q[9];
     for (int d = 0; d < 9; ++d) q[d] = e[(ia + d / 3 - 1) * nb + (ib + d % 3 - 1)];
     paraboloid(q, da, db);
@@ -256,50 +481,20 @@ __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_
   dj_out[f] = dj[f] + offs_b[ib] + db;
 }
 
-// band bbox of u over work pixels
-__global__ void k_band_mm(pxst_scan sc, const double* __restrict__ u, int band_rows,
-                          double* out) {
-  const int band = blockIdx.x;
-  const int64_t r_lo = sc.roi[0] + (int64_t)band * band_rows;
-  const int64_t r_hi = min(sc.roi[1], r_lo + band_rows);
-  const int64_t cw = sc.roi[3] - sc.roi[2];
-  const int64_t plane = sc.ss * sc.fs;
-  double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
-  for (int64_t q = threadIdx.x; q < (r_hi - r_lo) * cw; q += blockDim.x) {
-    const int64_t p = (r_lo + q / cw) * sc.fs + sc.roi[2] + q % cw;
-    if (!sc.work[p]) continue;
-    a0 = fmin(a0, u[p]); b0 = fmax(b0, u[p]);
-    a1 = fmin(a1, u[plane + p]); b1 = fmax(b1, u[plane + p]);
-  }
-  __shared__ double sh[4][32];
-  a0 = warp_min(a0); b0 = warp_max(b0); a1 = warp_min(a1); b1 = warp_max(b1);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) { sh[0][warp] = a0; sh[1][warp] = b0; sh[2][warp] = a1; sh[3][warp] = b1; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      a0 = fmin(a0, sh[0][w]); b0 = fmax(b0, sh[1][w]);
-      a1 = fmin(a1, sh[2][w]); b1 = fmax(b1, sh[3][w]);
-    }
-    out[4 * band] = sh[0][0] < a0 ? sh[0][0] : a0;
-    out[4 * band + 1] = sh[1][0] > b0 ? sh[1][0] : b0;
-    out[4 * band + 2] = sh[2][0] < a1 ? sh[2][0] : a1;
-    out[4 * band + 3] = sh[3][0] > b1 ? sh[3][0] : b1;
-  }
-}
-
-// ----------------------------------------------------------------------------
-using TrKernel = void (*)(TransArgs);
-struct TrEntry { int ka, kb; TrKernel fn; };
-#define TR(a, b) TrEntry{a, b, k_trans_partial<a, b>}
-const TrEntry kTrTable[] = {
+// ---------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------
+using FastKernel = void (*)(const __grid_constant__ CUtensorMap, TransArgs);
+struct FastEntry { int ka, kb; FastKernel fn; };
+#define TR(a, b) FastEntry{a, b, k_trans_fast<a, b>}
+const FastEntry kTable[] = {
     TR(1, 1), TR(3, 3), TR(5, 5), TR(7, 7), TR(9, 9), TR(11, 11), TR(13, 13),
-    TR(8, 8), TR(8, 9), TR(9, 8), TR(9, 9),
+    TR(8, 8), TR(8, 9), TR(9, 8),
 };
 #undef TR
 
-TrKernel find_tr(int ka, int kb) {
-  for (const auto& e : kTrTable)
+FastKernel find_fast(int ka, int kb) {
+  for (const auto& e : kTable)
     if (e.ka == ka && e.kb == kb) return e.fn;
   return nullptr;
 }
@@ -353,21 +548,20 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
   const int qa = steps_per_pixel(subpixel_step), qb = qa;
   bool fast = qa > 0 && !force_generic();
   const int kha = (na - 1) / 2, khb = (nb - 1) / 2;
-  struct Phase { int rho_a, rho_b, mlo_a, mhi_a, mlo_b, mhi_b; TrKernel fn; };
+  struct Phase { int rho_a, rho_b, mlo_a, mhi_a, mlo_b, mhi_b; FastKernel fn; };
   std::vector<Phase> phases;
   if (fast) {
+    auto mrange = [](int q, int rho, int kh, int& lo, int& hi) {   // k = q*m + rho in [-kh, kh]
+      lo = static_cast<int>(ceil((-kh - rho) / static_cast<double>(q)));
+      hi = static_cast<int>(floor((kh - rho) / static_cast<double>(q)));
+    };
     for (int ra_ = 0; ra_ < qa && fast; ++ra_)
       for (int rb_ = 0; rb_ < qb && fast; ++rb_) {
-        // k = q*m + rho in [-kh, kh]
-        auto mrange = [](int q, int rho, int kh, int& lo, int& hi) {
-          lo = static_cast<int>(ceil((-kh - rho) / static_cast<double>(q)));
-          hi = static_cast<int>(floor((kh - rho) / static_cast<double>(q)));
-        };
         Phase ph{ra_, rb_, 0, 0, 0, 0, nullptr};
         mrange(qa, ra_, kha, ph.mlo_a, ph.mhi_a);
         mrange(qb, rb_, khb, ph.mlo_b, ph.mhi_b);
         if (ph.mhi_a < ph.mlo_a || ph.mhi_b < ph.mlo_b) continue;
-        ph.fn = find_tr(ph.mhi_a - ph.mlo_a + 1, ph.mhi_b - ph.mlo_b + 1);
+        ph.fn = find_fast(ph.mhi_a - ph.mlo_a + 1, ph.mhi_b - ph.mlo_b + 1);
         if (!ph.fn) fast = false;
         phases.push_back(ph);
       }
@@ -375,53 +569,91 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
 
   const int64_t n_search = frame_hi - frame_lo;
   if (fast) {
-    const int64_t n_bands = (rw + kTrBand - 1) / kTrBand;
-    Scratch mm, pvbuf, pvtmp;
-    if (int e = mm.alloc(sizeof(double) * 4 * n_bands, s)) return e;
-    k_band_mm<<<(unsigned)n_bands, 256, 0, s>>>(*sc, u, kTrBand, mm.as<double>());
-    PXST_CHECK_LAUNCH();
-    // union patch box over phases, relative to floor(x_rho): rows
-    // [-max mhi, -min mlo + 1]
-    int mhi_a = -1 << 20, mlo_a = 1 << 20, mhi_b = -1 << 20, mlo_b = 1 << 20;
+    int max_ka = 0, max_kb = 0, mhi_a = -1 << 20, mlo_a = 1 << 20, mhi_b = -1 << 20,
+        mlo_b = 1 << 20;
     for (const auto& ph : phases) {
+      max_ka = max(max_ka, ph.mhi_a - ph.mlo_a + 1);
+      max_kb = max(max_kb, ph.mhi_b - ph.mlo_b + 1);
       mhi_a = max(mhi_a, ph.mhi_a); mlo_a = min(mlo_a, ph.mlo_a);
       mhi_b = max(mhi_b, ph.mhi_b); mlo_b = min(mlo_b, ph.mlo_b);
     }
+    a.box_r = box_rows3(max_ka);
+    a.box_c = box_cols3(max_kb);
+    a.n_ct = static_cast<int>((cw + kTC - 1) / kTC);
+    a.n_bands = (rw + kTR - 1) / kTR;
+    PXST_REQUIRE(a.n_bands <= kMaxGridY, "ROI too tall");
+    a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
+
+    Scratch geo, pvbuf, pvtmp, fmpad, lst;
+    if (int e = geo.alloc(sizeof(TileGeo) * a.n_bands * a.n_ct, s)) return e;
+    a.geo = geo.as<TileGeo>();
+    k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
+        *sc, u, max_ka, max_kb, a.box_r, a.box_c, geo.as<TileGeo>());
+    PXST_CHECK_LAUNCH();
+    // union patch box over phases, relative to floor(x_rho): rows
+    // [-max mhi, -min mlo + 1]
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
     if (int e = make_pv(ref, -mhi_a, -mlo_a + 1, -mhi_b, -mlo_b + 1, pvbuf.as<uint8_t>(), pvtmp,
                         s))
       return e;
     a.pv = pvbuf.as<uint8_t>();
-    a.band_mm = mm.as<double>();
-    a.n_bands = n_bands;
-    a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
-    // window: band footprint (~0.8 x 16 rows) x full width, capped at 96 KB
-    a.win_cap = 96 * 1024 / 4;
-    const size_t smem = sizeof(float) * a.win_cap;
-    // frame chunks so the partial buffer stays <= 256 MB
-    int64_t chunk = (256ll << 20) / (4 * n_bands * nk);
-    if (chunk < 1) chunk = 1;
-    if (chunk > kMaxGridY) chunk = kMaxGridY;
-    Scratch part;
-    if (int e = part.alloc(sizeof(float) * min(chunk, n_search) * n_bands * nk, s)) return e;
-    a.partial = part.as<float>();
+    // TMA descriptor (16-byte row pitch)
+    const float* tbase = ref->fm;
+    int64_t pitch = ref->of;
+    if (ref->of % 4 != 0 || (reinterpret_cast<uintptr_t>(ref->fm) & 15)) {
+      pitch = (ref->of + 3) / 4 * 4;
+      if (int e = fmpad.alloc(sizeof(float) * pitch * ref->os, s)) return e;
+      PXST_CHECK_CUDA(cudaMemcpy2DAsync(fmpad.p, pitch * sizeof(float), ref->fm,
+                                        ref->of * sizeof(float), ref->of * sizeof(float), ref->os,
+                                        cudaMemcpyDeviceToDevice, s));
+      tbase = fmpad.as<float>();
+    }
+    CUtensorMap tmap;
+    if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
+      return e;
+    const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128;
     for (const auto& ph : phases)
       PXST_CHECK_CUDA(cudaFuncSetAttribute(ph.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
+    // frame chunks so the partial buffer stays <= 256 MB
+    int64_t chunk = (256ll << 20) / (4 * a.n_bands * nk);
+    chunk = chunk < kMaxGridY ? chunk : kMaxGridY;
+    chunk = chunk > 1 ? chunk : 1;
+    Scratch part;
+    const int64_t cmax = min(chunk, n_search);
+    if (int e = part.alloc(sizeof(float) * cmax * a.n_bands * nk, s)) return e;
+    if (int e = lst.alloc(sizeof(unsigned long long) * (cmax * a.n_bands + 2), s)) return e;
+    a.partial = part.as<float>();
+    a.slow_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
+    a.slow_list = lst.as<unsigned long long>() + 1;
+    const size_t slow_smem = (sizeof(float) + 1) * (max_ka + 1) * (max_kb + 1) * 8;
     for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
       const int64_t c1 = min(frame_hi, c0 + chunk);
       a.frame_lo = c0;
       for (const auto& ph : phases) {
         a.rho_a = ph.rho_a; a.rho_b = ph.rho_b;
         a.mhi_a = ph.mhi_a; a.mhi_b = ph.mhi_b;
+        a.ka = ph.mhi_a - ph.mlo_a + 1;
+        a.kb = ph.mhi_b - ph.mlo_b + 1;
         a.ph_a = subpixel_step > 0.0 ? subpixel_step * ph.rho_a : 0.0;
         a.ph_b = subpixel_step > 0.0 ? subpixel_step * ph.rho_b : 0.0;
-        dim3 g((unsigned)n_bands, (unsigned)(c1 - c0));
-        ph.fn<<<g, kTrThreads, smem, s>>>(a);
+        PXST_CHECK_CUDA(cudaMemsetAsync(a.slow_n, 0, sizeof(unsigned), s));
+        dim3 g((unsigned)a.n_bands, (unsigned)(c1 - c0));
+        ph.fn<<<g, kThreads, smem, s>>>(tmap, a);
         PXST_CHECK_LAUNCH();
+        k_trans_slow<<<148 * 4, 256, slow_smem, s>>>(a);
+        PXST_CHECK_LAUNCH();
+        if (getenv("PXST_DEBUG")) {
+          unsigned h = 0;
+          PXST_CHECK_CUDA(cudaMemcpyAsync(&h, a.slow_n, sizeof(h), cudaMemcpyDeviceToHost, s));
+          PXST_CHECK_CUDA(cudaStreamSynchronize(s));
+          fprintf(stderr, "[pxst] K3 phase (%d,%d) %dx%d: %lld frames x %lld bands, %u slow "
+                  "(frame, band) pairs\n", ph.rho_a, ph.rho_b, a.ka, a.kb,
+                  (long long)(c1 - c0), (long long)a.n_bands, h);
+        }
       }
       k_trans_epilogue<float><<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
-          *sc, st->frame_norm, part.as<float>(), n_bands, c0, na, nb, d_oa, d_ob, di, dj,
+          *sc, st->frame_norm, part.as<float>(), a.n_bands, c0, na, nb, d_oa, d_ob, di, dj,
           di_out, dj_out, err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
       PXST_CHECK_LAUNCH();
     }
@@ -429,8 +661,8 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
   }
   // generic path
   int64_t chunk = (256ll << 20) / (8 * (int64_t)nk);
-  if (chunk < 1) chunk = 1;
-  if (chunk > kMaxGridY) chunk = kMaxGridY;
+  chunk = chunk < kMaxGridY ? chunk : kMaxGridY;
+  chunk = chunk > 1 ? chunk : 1;
   Scratch errs;
   if (int e = errs.alloc(sizeof(double) * min(chunk, n_search) * nk, s)) return e;
   for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
