@@ -130,6 +130,28 @@ def test_cfg0_translations(scan0, golden0):
     assert np.abs(T2.dj - golden0["uts_dj"]).max() < PX_TOL
 
 
+@pytest.mark.parametrize("half,step", [(3, None), (4, 0.25)])
+def test_cfg0_translation_windows(scan0, golden0, half, step):
+    """The config-3 (+-3 integer) and config-4 (+-4 at 0.25 px: 16 phase groups
+    9x9/9x8/8x9/8x8) translation searches against the oracle, incl. the
+    always-on refinement quirk."""
+    s = scan0
+    ref = ref_from(golden0)
+    U = pb.PixelMap(golden0["upm_u"])
+    good = np.zeros(s.scan.n_frames, bool)
+    good[[0, 7, 12, 24]] = True                       # frame subset keeps the oracle fast
+    sc = replace(s.scan, good_frames=good)
+    T = pb.update_translations(sc, s.w, s.m, ref, U, s.t0, pb.SearchWindow(half, half, step))
+    di, dj, errs = orc.update_translations(sc.frames, good, s.w.w, s.m.mask, ref.i_ref, ref.wsum,
+                                           ref.origin, U.u, s.t0.di, s.t0.dj, half, half, step,
+                                           return_errors=True)
+    for fr, e in errs.items():
+        flat = np.sort(e.ravel())
+        if (flat[1] - flat[0]) > MARGIN * abs(flat[0]):   # unique argmin
+            assert abs(T.di[fr] - di[fr]) < PX_TOL and abs(T.dj[fr] - dj[fr]) < PX_TOL, fr
+    np.testing.assert_array_equal(T.di[~good], s.t0.di[~good])
+
+
 def test_cfg0_error_maps(scan0, golden0):
     s = scan0
     ref = ref_from(golden0)
