@@ -229,8 +229,8 @@ def run_ours(args, rank, world, local):
 
     sharded = None
     if world > 1:
-        from paper_2003_12726_b200.sharding import ShardedIteration
-        sharded = ShardedIteration(ds, rank, world)
+        from paper_2003_12726_b200.sharding import DeviceExecutor, ShardedIteration
+        sharded = ShardedIteration(DeviceExecutor(ds), rank, world)
 
     # The config's workload is `cfg.iters` consecutive iterations from the
     # initial state (config 1: 3 x object -> pixel map -> error); steps walk

@@ -149,6 +149,16 @@ int pxst_error_maps(const pxst_scan* scan, const pxst_stats* st, const pxst_ref*
                     const double* u, const double* di, const double* dj, double* per_frame,
                     double* per_pixel, double* ref_plane, double* total, void* stream);
 
+/* K4 without the final normalisation, for detector-row shards: per_frame
+ * [n_frames] = this ROI's per-frame sums, per_pixel [ss,fs] (this ROI only),
+ * and the reference-plane numerator/denominator ADDED into plane_num /
+ * plane_den [os,of] (caller-zeroed).  After an all-reduce (sum) of per_frame,
+ * plane_num and plane_den across shards, pxst_object_finish(plane_num,
+ * plane_den, ...) yields reference_plane. */
+int pxst_error_partials(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                        const double* u, const double* di, const double* dj, double* per_frame,
+                        double* per_pixel, double* plane_num, double* plane_den, void* stream);
+
 /* Interpolation primitives (interp.py:53-85 and :88-123), for the drop-in
  * interp module and the parity tests.  gather: vals/ok at n points of the
  * masked image.  splat: float64 accumulation into acc_v/acc_w [os,of]

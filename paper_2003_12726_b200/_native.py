@@ -61,6 +61,9 @@ _SIGS = {
     "pxst_error_maps": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p]),
+    "pxst_error_partials": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
     "pxst_gather": (c_int, [POINTER(PxstRef), c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                             c_void_p]),
     "pxst_splat": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,

@@ -156,43 +156,77 @@ __global__ void k_err_total(const double* __restrict__ frame_tmp, int64_t n, dou
 
 using namespace pxst;
 
-extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref,
-                               const double* u, const double* di, const double* dj,
-                               double* per_frame, double* per_pixel, double* ref_plane,
-                               double* total, void* stream) {
-  if (int e = check_scan(sc)) return e;
-  PXST_REQUIRE(ref && ref->fm && ref->valid && ref->os > 0 && ref->of > 0, "bad reference");
-  PXST_REQUIRE(st && st->sigma2, "stats descriptor is NULL");
-  PXST_REQUIRE(u && di && dj && per_frame && per_pixel && ref_plane && total, "NULL pointer");
-  cudaStream_t s = as_stream(stream);
+namespace pxst {
+namespace {
+
+// One pass: per_frame (zeroed, then good frames filled), per_pixel (zeroed,
+// then this scan's ROI filled), reference-plane accumulators added into
+// num/den (caller-initialised), optional total.
+int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, const double* u,
+               const double* di, const double* dj, double* per_frame, double* per_pixel,
+               double* num, double* den, double* total, cudaStream_t s) {
   const int64_t plane = sc->ss * sc->fs;
-  const int64_t n_o = ref->os * ref->of;
   PXST_CHECK_CUDA(cudaMemsetAsync(per_frame, 0, sizeof(double) * sc->n_frames, s));
   PXST_CHECK_CUDA(cudaMemsetAsync(per_pixel, 0, sizeof(double) * plane, s));
-  PXST_CHECK_CUDA(cudaMemsetAsync(total, 0, sizeof(double), s));
-  if (sc->n_good == 0) {
-    PXST_CHECK_CUDA(cudaMemsetAsync(ref_plane, 0, sizeof(double) * n_o, s));
-    return PXST_OK;
-  }
+  if (total) PXST_CHECK_CUDA(cudaMemsetAsync(total, 0, sizeof(double), s));
+  if (sc->n_good == 0) return PXST_OK;
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
   dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)((rw + kTR - 1) / kTR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
   const int64_t n_ctas = (int64_t)g.x * g.y;
-  Scratch part, acc;
+  Scratch part;
   if (int e = part.alloc(sizeof(double) * (n_ctas + 1) * sc->n_good, s)) return e;
-  if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
-  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
   double* ftmp = part.as<double>() + n_ctas * sc->n_good;
-  ErrArgs a{*sc,        u,          di,          dj,        ref->fm,
-            ref->valid, ref->os,    ref->of,     ref->n0,   ref->m0,
-            ref->fm64,  st->sigma2, acc.as<double>(), acc.as<double>() + n_o};
+  ErrArgs a{*sc,        u,          di,          dj,      ref->fm,
+            ref->valid, ref->os,    ref->of,     ref->n0, ref->m0,
+            ref->fm64,  st->sigma2, num,         den};
   k_err_pass<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
   PXST_CHECK_LAUNCH();
   k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_ctas, per_frame,
                                                     ftmp);
   PXST_CHECK_LAUNCH();
-  k_err_total<<<1, 1024, 0, s>>>(ftmp, sc->n_good, total);
-  PXST_CHECK_LAUNCH();
+  if (total) {
+    k_err_total<<<1, 1024, 0, s>>>(ftmp, sc->n_good, total);
+    PXST_CHECK_LAUNCH();
+  }
+  return PXST_OK;
+}
+
+int check_err_args(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(ref && ref->fm && ref->valid && ref->os > 0 && ref->of > 0, "bad reference");
+  PXST_REQUIRE(st && st->sigma2, "stats descriptor is NULL");
+  return PXST_OK;
+}
+
+}  // namespace
+}  // namespace pxst
+
+extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref,
+                               const double* u, const double* di, const double* dj,
+                               double* per_frame, double* per_pixel, double* ref_plane,
+                               double* total, void* stream) {
+  if (int e = check_err_args(sc, st, ref)) return e;
+  PXST_REQUIRE(u && di && dj && per_frame && per_pixel && ref_plane && total, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n_o = ref->os * ref->of;
+  Scratch acc;
+  if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
+  if (int e = error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, acc.as<double>(),
+                         acc.as<double>() + n_o, total, s))
+    return e;
   return launch_object_finish(acc.as<double>(), acc.as<double>() + n_o, n_o, ref_plane, nullptr,
                               nullptr, nullptr, s);
+}
+
+extern "C" int pxst_error_partials(const pxst_scan* sc, const pxst_stats* st,
+                                   const pxst_ref* ref, const double* u, const double* di,
+                                   const double* dj, double* per_frame, double* per_pixel,
+                                   double* plane_num, double* plane_den, void* stream) {
+  if (int e = check_err_args(sc, st, ref)) return e;
+  PXST_REQUIRE(u && di && dj && per_frame && per_pixel && plane_num && plane_den,
+               "NULL pointer");
+  return error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, plane_num, plane_den, nullptr,
+                    as_stream(stream));
 }

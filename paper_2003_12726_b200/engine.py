@@ -259,6 +259,42 @@ class DeviceScan:
             dj_out.data_ptr(), _ptr(err_out), stream_ptr()))
         return di_out, dj_out
 
+    # ------------------------------------------------------- shard views / K4
+    def band(self, r0: int, r1: int) -> "DeviceScan":
+        """View restricted to detector rows [r0, r1) of the ROI; shares every
+        device buffer and the (full-ROI) statistics with this scan."""
+        import copy
+        v = copy.copy(self)
+        R0, R1, C0, C1 = self.roi
+        lo, hi = max(r0, R0), min(r1, R1)
+        v.roi = (lo, hi, C0, C1)
+        roi4 = (ctypes.c_int64 * 4)(lo, max(hi, lo + 1), C0, max(C1, C0 + 1))
+        v.c_scan = PxstScan(self.frames.data_ptr(), self.n_frames, self.ss, self.fs,
+                            self.good.data_ptr(), self.n_good, self.w64.data_ptr(),
+                            self.w32.data_ptr(), self.work.data_ptr(), roi4)
+        v.empty = self.empty or hi <= lo
+        return v
+
+    def error_partials(self, ref: DeviceRef, u_t, di_t, dj_t):
+        """K4 without normalisation: (per_frame, per_pixel, plane_num, plane_den)."""
+        per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)
+        per_pixel = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        num = torch.zeros(ref.fm.numel(), dtype=torch.float64, device=self.device)
+        den = torch.zeros_like(num)
+        if not self.empty:
+            c_ref = ref.struct()
+            check(self.lib.pxst_error_partials(
+                ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+                u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
+                per_pixel.data_ptr(), num.data_ptr(), den.data_ptr(), stream_ptr()))
+        return per_frame, per_pixel.view(self.ss, self.fs), num, den
+
+    def plane_finish(self, num, den, shape):
+        plane = torch.empty(num.numel(), dtype=torch.float64, device=self.device)
+        check(self.lib.pxst_object_finish(num.data_ptr(), den.data_ptr(), num.numel(),
+                                          plane.data_ptr(), None, None, None, stream_ptr()))
+        return plane.view(*shape)
+
     # ---------------------------------------------------------- K4 error maps
     def error_maps(self, ref: DeviceRef, u_t, di_t, dj_t):
         per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)

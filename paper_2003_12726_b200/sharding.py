@@ -1,0 +1,206 @@
+"""Multi-GPU sharding of one PXST iteration.
+
+One process per GPU (torchrun), ``torch.distributed`` over NCCL for the
+exchanges.  The frame stack is replicated on every GPU (<= 8 GB vs 180 GB
+HBM), so no data moves between phases except the small exchange tensors:
+
+=====================  =================  ====================================
+phase                  partition          exchange after it
+=====================  =================  ====================================
+K1 object formation    good frames        all-reduce(sum) of num/den (float64)
+K2 pixel-map search    detector rows,     all-gather of the u rows (exact)
+                       balanced by work
+                       pixel count
+K3 translation search  good frames        all-gather of (di, dj) (exact)
+K4 error maps          detector rows      all-reduce of per-frame sums,
+                                          per-pixel map, plane num/den
+=====================  =================  ====================================
+
+The grid bbox is computed redundantly from the replicated u and t.  Row
+shards need no halo (sigma = 0, integrate = False: pixels are independent,
+recon.py:221-315); the all-gathers are exact, so u and t match the
+single-GPU result bit for bit given the same object map; the float64
+all-reduces differ from one GPU only in summation order.
+
+The logic talks to an *executor* (``DeviceExecutor`` here; tests supply a
+CPU one built on the oracle and run it under gloo), so the partitioning and
+collective composition are exercised without GPUs.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def partition_rows(row_work: np.ndarray, r0: int, world: int) -> list[tuple[int, int]]:
+    """Split ROI rows [r0, r0 + len(row_work)) into `world` contiguous bands
+    with (nearly) equal work-pixel counts."""
+    n = len(row_work)
+    cum = np.concatenate([[0], np.cumsum(row_work, dtype=np.int64)])
+    total = cum[-1]
+    cuts = [0]
+    for k in range(1, world):
+        target = total * k / world
+        cut = int(np.searchsorted(cum, target, side="left"))
+        cuts.append(min(max(cut, cuts[-1]), n))
+    cuts.append(n)
+    return [(r0 + cuts[k], r0 + cuts[k + 1]) for k in range(world)]
+
+
+def partition_frames(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous blocks of the good-frame list."""
+    edges = [round(n * k / world) for k in range(world + 1)]
+    return [(edges[k], edges[k + 1]) for k in range(world)]
+
+
+@dataclass
+class ShardedMetrics:
+    total: float
+    per_frame: torch.Tensor
+    per_pixel: torch.Tensor
+    reference_plane: torch.Tensor
+
+
+class ShardedIteration:
+    """Runs object map -> pixel map -> (translations) -> error maps with the
+    work split across the ranks of `group`."""
+
+    def __init__(self, ex, rank: int, world: int, group=None):
+        self.ex = ex
+        self.rank = rank
+        self.world = world
+        self.group = group
+        r0, r1, _, _ = ex.roi
+        self.rows = partition_rows(ex.row_work_counts(), r0, world)
+        self.frames = partition_frames(ex.n_good, world)
+        self.max_rows = max(hi - lo for lo, hi in self.rows)
+        self.max_frames = max(hi - lo for lo, hi in self.frames)
+
+    # ----------------------------------------------------------- collectives
+    def _all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def _gather_rows(self, u_local: torch.Tensor) -> torch.Tensor:
+        """Assemble the full u from each rank's band (exact)."""
+        _, ss, fs = u_local.shape
+        lo, hi = self.rows[self.rank]
+        buf = torch.zeros((2, self.max_rows, fs), dtype=u_local.dtype, device=u_local.device)
+        buf[:, : hi - lo] = u_local[:, lo:hi]
+        out = torch.empty((self.world * 2, self.max_rows, fs), dtype=u_local.dtype,
+                          device=u_local.device)
+        dist.all_gather_into_tensor(out, buf.contiguous(), group=self.group)
+        out = out.view(self.world, 2, self.max_rows, fs)
+        u = u_local.clone()
+        for k, (a, b) in enumerate(self.rows):
+            u[:, a:b] = out[k, :, : b - a]
+        return u
+
+    def _gather_frames(self, di: torch.Tensor, dj: torch.Tensor):
+        """Assemble translations searched on each rank's frame block (exact)."""
+        good = self.ex.good_index_tensor()
+        lo, hi = self.frames[self.rank]
+        buf = torch.zeros((2, self.max_frames), dtype=di.dtype, device=di.device)
+        idx = good[lo:hi]
+        buf[0, : hi - lo] = di[idx]
+        buf[1, : hi - lo] = dj[idx]
+        out = torch.empty((self.world * 2, self.max_frames), dtype=di.dtype, device=di.device)
+        dist.all_gather_into_tensor(out, buf, group=self.group)
+        out = out.view(self.world, 2, self.max_frames)
+        di_o, dj_o = di.clone(), dj.clone()
+        for k, (a, b) in enumerate(self.frames):
+            di_o[good[a:b]] = out[k, 0, : b - a]
+            dj_o[good[a:b]] = out[k, 1, : b - a]
+        return di_o, dj_o
+
+    # ---------------------------------------------------------------- phases
+    def object_map(self, u, di, dj):
+        n0, m0, shape = self.ex.bbox(u, di, dj)
+        lo, hi = self.frames[self.rank]
+        acc = self.ex.object_splat(u, di, dj, n0, m0, shape, lo, hi)
+        self._all_reduce(acc)
+        return self.ex.object_finish(acc, (n0, m0), shape)
+
+    def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True):
+        u_local = self.ex.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine,
+                                           rows=self.rows[self.rank])
+        return self._gather_rows(u_local)
+
+    def translations(self, ref, u, di, dj, half_ss, half_fs, sub=None):
+        lo, hi = self.frames[self.rank]
+        di_l, dj_l = self.ex.translation_search(ref, u, di, dj, half_ss, half_fs, sub, lo, hi)
+        return self._gather_frames(di_l, dj_l)
+
+    def error_maps(self, ref, u, di, dj) -> ShardedMetrics:
+        per_frame, per_pixel, num, den = self.ex.error_partials(ref, u, di, dj,
+                                                                rows=self.rows[self.rank])
+        self._all_reduce(per_frame)
+        self._all_reduce(per_pixel)
+        self._all_reduce(num)
+        self._all_reduce(den)
+        plane = self.ex.error_finish(num, den, ref)
+        good = self.ex.good_index_tensor()
+        total = float(per_frame[good].sum().item()) if len(good) else 0.0
+        return ShardedMetrics(total, per_frame, per_pixel, plane)
+
+    def iteration(self, u, di, dj, cfg, ev=None):
+        """One full iteration with the reference's ordering (recon.py:511-516)."""
+        ref = self.object_map(u, di, dj)
+        if ev:
+            ev[0].record(torch.cuda.current_stream())
+        u_new = self.pixel_map(ref, u, di, dj, cfg.half_ss, cfg.half_fs, cfg.subpixel_grid,
+                               cfg.refine)
+        if ev:
+            ev[1].record(torch.cuda.current_stream())
+        di_new, dj_new = di, dj
+        if cfg.update_translations:
+            di_new, dj_new = self.translations(ref, u_new, di, dj, cfg.t_half_ss, cfg.t_half_fs,
+                                               cfg.t_subpixel_grid)
+        self.metrics = self.error_maps(ref, u_new, di_new, dj_new)
+        return u_new, di_new, dj_new
+
+
+class DeviceExecutor:
+    """Executor over a DeviceScan (the GPU kernels)."""
+
+    def __init__(self, ds):
+        self.ds = ds
+        self.roi = ds.roi
+        self.n_good = ds.n_good
+        self._good = torch.as_tensor(ds.good_idx.astype(np.int64), device=ds.device)
+
+    def row_work_counts(self) -> np.ndarray:
+        r0, r1, c0, c1 = self.roi
+        work = self.ds.work.view(self.ds.ss, self.ds.fs)[r0:r1, c0:c1]
+        return work.sum(dim=1).cpu().numpy()
+
+    def good_index_tensor(self) -> torch.Tensor:
+        return self._good
+
+    def bbox(self, u, di, dj):
+        return self.ds.bbox(u, di, dj)
+
+    def object_splat(self, u, di, dj, n0, m0, shape, lo, hi):
+        return self.ds.object_splat(u, di, dj, n0, m0, shape, lo, hi)
+
+    def object_finish(self, acc, origin, shape):
+        return self.ds.object_finish(acc, origin, shape)
+
+    def pixel_map_search(self, ref, u, di, dj, half_ss, half_fs, sub, refine, rows):
+        band = self.ds.band(*rows)
+        u_out, _ = band.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine)
+        return u_out
+
+    def translation_search(self, ref, u, di, dj, half_ss, half_fs, sub, lo, hi):
+        return self.ds.translation_search(ref, u, di, dj, half_ss, half_fs, sub, lo, hi)
+
+    def error_partials(self, ref, u, di, dj, rows):
+        return self.ds.band(*rows).error_partials(ref, u, di, dj)
+
+    def error_finish(self, num, den, ref):
+        return self.ds.plane_finish(num, den, ref.shape)

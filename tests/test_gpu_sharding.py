@@ -1,0 +1,81 @@
+"""GPU side of the sharding layer: the device executor's row-band views and
+un-normalised K4 partials compose to the unsharded result, and a one-rank
+NCCL group runs ShardedIteration end to end.  (More ranks need more GPUs;
+the multi-rank composition itself is covered on CPU in test_sharding.py.)"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from paper_2003_12726_b200 import engine  # noqa: E402
+from paper_2003_12726_b200.sharding import DeviceExecutor, ShardedIteration, partition_rows  # noqa: E402
+from paper_2003_12726_b200.synth import CONFIGS  # noqa: E402
+
+
+def _ds(s):
+    ds = engine.DeviceScan(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask)
+    return ds, ds.upload_u(s.u0.u), *ds.upload_t(s.t0.di, s.t0.dj)
+
+
+def test_band_views_compose(scan0):
+    ds, u, di, dj = _ds(scan0)
+    ref = ds.object_map(u, di, dj)
+    ex = DeviceExecutor(ds)
+    bands = partition_rows(ex.row_work_counts(), 0, 3)
+    u_full, _ = ds.pixel_map_search(ref, u, di, dj, 3, 3)
+    u_asm = u.clone()
+    pf = torch.zeros(ds.n_frames, dtype=torch.float64, device=ds.device)
+    pp = torch.zeros((ds.ss, ds.fs), dtype=torch.float64, device=ds.device)
+    num = den = None
+    for lo, hi in bands:
+        u_b = ex.pixel_map_search(ref, u, di, dj, 3, 3, None, True, rows=(lo, hi))
+        u_asm[:, lo:hi] = u_b[:, lo:hi]
+        f, p, n_, d_ = ex.error_partials(ref, u_full, di, dj, rows=(lo, hi))
+        pf += f
+        pp += p
+        num = n_ if num is None else num + n_
+        den = d_ if den is None else den + d_
+    d = np.abs((u_asm - u_full).cpu().numpy()).max(axis=0)
+    assert np.mean(d < 1e-3) > 0.999
+    total, per_frame, per_pixel, plane, _ = ds.error_maps(ref, u_full, di, dj)
+    np.testing.assert_allclose(pf.cpu().numpy(), per_frame.cpu().numpy(), rtol=1e-10)
+    np.testing.assert_allclose(pp.cpu().numpy(), per_pixel.cpu().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(ex.error_finish(num, den, ref).cpu().numpy(),
+                               plane.cpu().numpy(), rtol=1e-9, atol=1e-14)
+    # frame-range splats compose to the full object map
+    n0, m0, shape = ds.bbox(u, di, dj)
+    acc = ds.object_splat(u, di, dj, n0, m0, shape, 0, 10)
+    acc += ds.object_splat(u, di, dj, n0, m0, shape, 10, ds.n_good)
+    ref2 = ds.object_finish(acc, (n0, m0), shape)
+    np.testing.assert_allclose(ref2.i_ref.cpu().numpy(), ref.i_ref.cpu().numpy(), rtol=1e-12)
+
+
+def test_one_rank_nccl_iteration(scan0):
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        ds, u, di, dj = _ds(scan0)
+        cfg = CONFIGS[0]
+        it = ShardedIteration(DeviceExecutor(ds), 0, 1)
+        u1, di1, dj1 = it.iteration(u, di, dj, cfg)
+        ref = ds.object_map(u, di, dj)
+        u2, _ = ds.pixel_map_search(ref, u, di, dj, cfg.half_ss, cfg.half_fs)
+        np.testing.assert_allclose(u1.cpu().numpy(), u2.cpu().numpy(), atol=1e-3)
+        total, *_ = ds.error_maps(ref, u2, di, dj)
+        assert abs(it.metrics.total - float(total.item())) <= 1e-6 * float(total.item())
+    finally:
+        dist.destroy_process_group()
