@@ -260,17 +260,21 @@ def run_ours(args, rank, world, local):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k2ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(args.steps)]
-    launches0 = _native.launch_count()
+    # nvidia-smi samples every 100 ms: the sampler starts before the warm-up and
+    # keeps running through an untimed continuation of the same steps (>= 1 s)
+    # so the clock record covers the timed region's load.
     with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        launches0 = _native.launch_count()
         torch.cuda.synchronize()
         for i in range(args.steps):
             flush.zero_()                       # L2 flush between timed steps (untimed)
@@ -278,7 +282,12 @@ def run_ours(args, rank, world, local):
             step(k2ev[i])
             ends[i].record(stream)
         torch.cuda.synchronize()
-    launches = _native.launch_count() - launches0
+        launches = _native.launch_count() - launches0
+        if not args.profile:
+            t_end = time.perf_counter() + 1.0
+            while time.perf_counter() < t_end:
+                step()
+            torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     k2_ms = [a.elapsed_time(b) for a, b in k2ev]
     total_ms = float(sum(step_ms))
