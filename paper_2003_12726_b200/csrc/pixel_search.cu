@@ -126,7 +126,10 @@ struct Sample {
   double fx, fy;     // fractions
   int lr, lc;        // patch origin inside the TMA box
   int wr0, wc0;      // box origin in the object grid
-  bool fast;
+  bool pre;          // every fast-path condition except the patch-valid lookup
+  uint8_t pvb;       // patch-valid byte (loaded unconditionally, consumed late so
+                     // the one-frame-ahead pipeline hides its latency)
+  __device__ __forceinline__ bool fast() const { return pre && pvb != 0; }
 };
 
 __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g, double u0,
@@ -142,16 +145,18 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   const bool finite = fabs(x) < 1e9 && fabs(y) < 1e9;
   s.i = finite ? static_cast<int>(xf) : -(1 << 30);
   s.j = finite ? static_cast<int>(yf) : -(1 << 30);
-  s.fast = false;
+  s.pre = false;
+  s.pvb = 0;
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
   if (g.use_win) {
     s.wr0 = static_cast<int>(floor(g.umin0 - dI - n0d)) - ra;
     s.wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb);
     s.lr = s.i - ra - s.wr0;
     s.lc = s.j - rb - s.wc0;
-    s.fast = fwv >= 0.f && s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of &&
-             a.pv[(int64_t)s.i * a.of + s.j] != 0 && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r &&
-             s.lc >= 0 && s.lc + a.kb + 1 <= a.box_c;
+    const bool in = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of;
+    s.pre = fwv >= 0.f && in && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r && s.lc >= 0 &&
+            s.lc + a.kb + 1 <= a.box_c;
+    s.pvb = __ldg(a.pv + (in ? (int64_t)s.i * a.of + s.j : 0));
   }
   return s;
 }
@@ -247,8 +252,9 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
       mbar_wait(&full[b], ph);
-      any_slow |= live && !sm.fast;
-      if (sm.fast) {
+      const bool fast = sm.fast();
+      any_slow |= live && !fast;
+      if (fast) {
         const float fx = static_cast<float>(sm.fx), fy = static_cast<float>(sm.fy);
         float sI = I, sW = W;
         if (a.fw) {
@@ -349,7 +355,7 @@ __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ lis
       if (kl < k_hi) {
         const int64_t f = a.sc.good[kl];
         const float fwv = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
-        slow = !make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast;
+        slow = !make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast();
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
       while (mask) {
