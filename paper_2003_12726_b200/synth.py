@@ -60,6 +60,7 @@ class ScanConfig:
     t_half_fs: int = 0
     t_subpixel_grid: float | None = None
     margin: int = 8
+    update_pixel_map: bool = True
 
 
 CONFIGS = {
@@ -77,7 +78,8 @@ CONFIGS = {
     4: ScanConfig("cfg4-4000x512x512", 512, 512, "uniform", n_frames=4000, field=200.0,
                   obj_sigma=2.0, obj_contrast=0.3, u_law="cubic", u_noise=0.0, t_noise=1.5,
                   t_noise_kind="normal", half_ss=0, half_fs=0, iters=1,
-                  update_translations=True, t_half_ss=4, t_half_fs=4, t_subpixel_grid=0.25),
+                  update_translations=True, t_half_ss=4, t_half_fs=4, t_subpixel_grid=0.25,
+                  update_pixel_map=False),
 }
 
 # Top-hat whitefield (config 2): plateau over the central 80% of each axis,
@@ -191,6 +193,70 @@ def _scan_record(frames, n):
                     y_pixel_size=1e-5, basis_vectors=np.tile(np.array([[1e-5, 0, 0], [0, 1e-5, 0]]),
                                                              (n, 1, 1)),
                     translations=np.zeros((n, 3)), good_frames=np.ones(n, dtype=bool))
+
+
+def make_scan_device(cfg_id: int | ScanConfig, device, seed: int | None = None,
+                     frame_chunk: int = 64):
+    """Configs 3-4 scale: same recipe, frames rendered and Poisson-sampled on
+    `device` with a seeded torch.Generator (the numpy draws for positions,
+    object, mask and initial state keep the documented order).  Returns
+    ``(SyntheticScan with scan.frames=None, frames_dev [N,SS,FS] float32)``."""
+    import torch
+    cfg = CONFIGS[cfg_id] if isinstance(cfg_id, int) else cfg_id
+    seed = (cfg_id if isinstance(cfg_id, int) else 0) if seed is None else seed
+    rng = np.random.default_rng(seed)
+    di, dj = positions(cfg, rng)
+    u_true = true_pixel_map(cfg)
+    n0, m0, oshape = object_grid(u_true, di, dj, cfg.margin)
+    obj = np.clip(1.0 + cfg.obj_contrast * _smooth_noise(oshape, cfg.obj_sigma, rng), 0.05, None)
+    mask = rng.random((cfg.n_ss, cfg.n_fs)) >= cfg.bad_frac
+    wf = whitefield(cfg)
+    n = di.size
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed) + 1000)
+    tex = torch.as_tensor(obj, device=device)
+    u0 = torch.as_tensor(u_true[0], device=device)
+    u1 = torch.as_tensor(u_true[1], device=device)
+    W = torch.as_tensor(wf, device=device)
+    frames = torch.empty((n, cfg.n_ss, cfg.n_fs), dtype=torch.float32, device=device)
+    of = oshape[1]
+    flat = tex.reshape(-1)
+    for k0 in range(0, n, frame_chunk):
+        k1 = min(n, k0 + frame_chunk)
+        dI = torch.as_tensor(di[k0:k1], device=device)[:, None, None]
+        dJ = torch.as_tensor(dj[k0:k1], device=device)[:, None, None]
+        x = u0[None] - dI - n0
+        y = u1[None] - dJ - m0
+        r0 = torch.floor(x)
+        c0 = torch.floor(y)
+        tx, ty = x - r0, y - c0
+        r0 = r0.long()
+        c0 = c0.long()
+        if int(r0.min()) < 0 or int(c0.min()) < 0 or int(r0.max()) + 1 >= oshape[0] or \
+                int(c0.max()) + 1 >= of:
+            raise ValueError("sample displacement exceeds the object extent")
+        i00 = r0 * of + c0
+        v = ((1 - tx) * (1 - ty) * flat[i00] + (1 - tx) * ty * flat[i00 + 1]
+             + tx * (1 - ty) * flat[i00 + of] + tx * ty * flat[i00 + of + 1])
+        frames[k0:k1] = torch.poisson(W[None] * v, generator=gen).float()
+    u_init = u_true.copy()
+    if cfg.u_noise > 0:
+        noise = rng.uniform(-cfg.u_noise, cfg.u_noise, size=u_true.shape)
+        if cfg.u_law == "fs_only":
+            noise[0] = 0.0
+        u_init = u_true + noise
+    di0, dj0 = di.copy(), dj.copy()
+    if cfg.t_noise_kind == "uniform":
+        tn = rng.uniform(-cfg.t_noise, cfg.t_noise, size=(2, n))
+        di0, dj0 = di + tn[0], dj + tn[1]
+    elif cfg.t_noise_kind == "normal":
+        tn = rng.normal(0.0, cfg.t_noise, size=(2, n))
+        di0, dj0 = di + tn[0], dj + tn[1]
+    rec = _scan_record(None, n)
+    s = SyntheticScan(cfg=cfg, scan=rec, w=Whitefield(wf), m=PixelMask(mask), u0=PixelMap(u_init),
+                      t0=PixelTranslations(di0, dj0), u_true=u_true, di_true=di, dj_true=dj,
+                      obj=obj, obj_origin=(n0, m0))
+    return s, frames
 
 
 def make_scan(cfg_id: int | ScanConfig, seed: int | None = None) -> SyntheticScan:
