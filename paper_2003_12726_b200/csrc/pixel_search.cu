@@ -103,21 +103,13 @@ __global__ void k_tile_geo(PixArgs a, TileGeo* geo) {
     mx1 = fmax(red[0][3], red[w][3]); red[0][3] = mx1;
   }
   mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
-  TileGeo g;
-  g.pad = 0;
-  if (!(mn0 <= mx0)) {
-    g.umin0 = g.umin1 = NAN;
-    g.use_win = 0;
-  } else {
-    g.umin0 = mn0;
-    g.umin1 = mn1;
-    const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
-    const int wr = clamp_span(floor(mx0 - mn0)) + a.ka + 2;
-    const int wc = clamp_span(floor(mx1 - mn1)) + a.kb + 2 + 3;   // +3: aligned origin
-    g.use_win = finite && wr <= a.box_r && wc <= a.box_c;
-  }
-  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = g;
+  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_tile_geo(mn0, mx0, mn1, mx1);
 }
+
+// window rows / cols a tile needs beyond its u span: the (Ka+1) x (Kb+1)
+// patch, one row/col of floor() slack, and 3 columns of box-origin alignment.
+__host__ __device__ inline int need_rows2(int ka) { return ka + 2; }
+__host__ __device__ inline int need_cols2(int kb) { return kb + 5; }
 
 // Per-sample geometry shared by the fast and slow kernels (identical float64
 // expressions, so both agree on which samples are "fast").
@@ -148,7 +140,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   s.pre = false;
   s.pvb = 0;
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
-  if (g.use_win) {
+  if (tile_fits(g, need_rows2(a.ka), need_cols2(a.kb), a.box_r, a.box_c)) {
     s.wr0 = static_cast<int>(floor(g.umin0 - dI - n0d)) - ra;
     s.wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb);
     s.lr = s.i - ra - s.wr0;
@@ -202,9 +194,10 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 
   PackedAcc<KA, KB> acc;
   acc.zero();
-  bool any_slow = live && nk > 0 && !g.use_win;
+  const bool fits = tile_fits(g, need_rows2(KA), need_cols2(KB), a.box_r, a.box_c);
+  bool any_slow = live && nk > 0 && !fits;
 
-  if (g.use_win && nk > 0) {
+  if (fits && nk > 0) {
     const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
     const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
     for (int jj = threadIdx.x; jj < nk; jj += kThreads) {
@@ -587,13 +580,22 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
                                         cudaMemcpyDeviceToDevice, s));
       tbase = fmpad.as<float>();
     }
-    CUtensorMap tmap;
-    if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
-      return e;
-
     dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
     k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
+    // Size the TMA box from the largest tile footprint (|du/dx| reaches ~1.8
+    // at the edges of the config-3 map), capped at 24 KB per ring slot; tiles
+    // beyond the cap take the exact path.
+    int span[2];
+    if (int e = tile_span_max(geo.as<TileGeo>(), tiles, span, s)) return e;
+    a.box_r = max(a.box_r, span[0] + need_rows2(na));
+    a.box_c = max(a.box_c, span[1] + need_cols2(nb));
+    a.box_c = (a.box_c + 23) / 32 * 32 + 8;            // pitch = 8 (mod 32)
+    if (a.box_c > 256) a.box_c = 232;
+    while (a.box_r > 16 && a.box_r * a.box_c * 4 > 24 * 1024) --a.box_r;
+    CUtensorMap tmap;
+    if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
+      return e;
     const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
                         (2 * sizeof(double) + sizeof(int)) * a.chunk;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -209,9 +209,38 @@ __device__ __forceinline__ void paraboloid(const double (&e)[9], double& dss, do
 // tile's work pixels).
 struct TileGeo {
   double umin0, umin1;  // NaN when the tile has no work pixel
-  int use_win;          // the tile's footprint fits the TMA box
-  int pad;
+  int span_r, span_c;   // floor(max u - min u) per axis over the tile's work pixels
+                        // (clamped to 4096; -1 when not finite)
 };
+
+// The tile's object window fits a TMA box of box_r x box_c when its span plus
+// the patch extent (need_r/need_c: window rows/cols beyond the span, incl.
+// floor() slack and the 4-column alignment of the box origin) fit.
+__host__ __device__ inline bool tile_fits(const TileGeo& g, int need_r, int need_c, int box_r,
+                                          int box_c) {
+  return g.span_r >= 0 && g.span_c >= 0 && g.span_r + need_r <= box_r &&
+         g.span_c + need_c <= box_c;
+}
+
+// Per-tile geometry -> TileGeo (device helper used by the tile kernels).
+__device__ __forceinline__ TileGeo make_tile_geo(double mn0, double mx0, double mn1, double mx1) {
+  TileGeo g;
+  if (!(mn0 <= mx0)) {
+    g.umin0 = g.umin1 = NAN;
+    g.span_r = g.span_c = -1;
+    return g;
+  }
+  g.umin0 = mn0;
+  g.umin1 = mn1;
+  const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
+  const double sr = floor(mx0 - mn0), sc = floor(mx1 - mn1);
+  g.span_r = finite ? (sr > 4096.0 ? 4096 : static_cast<int>(sr)) : -1;
+  g.span_c = finite ? (sc > 4096.0 ? 4096 : static_cast<int>(sc)) : -1;
+  return g;
+}
+
+// Host: largest spans over tiles with work pixels -> out[2] (synchronises).
+int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s);
 
 __host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
 // TMA on this stack faults ("illegal instruction") unless the box starts on a

@@ -30,7 +30,41 @@ __global__ void k_pv_cols(const uint8_t* __restrict__ tmp, int64_t os, int64_t o
   }
 }
 
+__global__ void k_span_max(const TileGeo* __restrict__ geo, int64_t n, int* out) {
+  __shared__ int sr[32], sc[32];
+  int mr = -1, mc = -1;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    mr = max(mr, geo[k].span_r);
+    mc = max(mc, geo[k].span_c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mr = max(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sr[w] = mr; sc[w] = mc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) { mr = max(mr, sr[i]); mc = max(mc, sc[i]); }
+    mr = max(mr, sr[0]);
+    mc = max(mc, sc[0]);
+    out[0] = mr;
+    out[1] = mc;
+  }
+}
+
 }  // namespace
+
+int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s) {
+  Scratch d;
+  if (int e = d.alloc(2 * sizeof(int), s)) return e;
+  k_span_max<<<1, 1024, 0, s>>>(geo, n, d.as<int>());
+  PXST_CHECK_LAUNCH();
+  PXST_CHECK_CUDA(cudaMemcpyAsync(out, d.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  PXST_CHECK_CUDA(cudaStreamSynchronize(s));
+  return PXST_OK;
+}
 
 int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Scratch& tmp,
             cudaStream_t s) {

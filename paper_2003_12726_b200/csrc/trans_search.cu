@@ -71,6 +71,7 @@ struct TransArgs {
   float* partial;            // [chunk frames][n_bands][na_full*nb_full]
   unsigned long long* slow_list;   // (frame_in_chunk << 24 | band) pairs with skipped samples
   unsigned* slow_n;
+  unsigned long long* dbg;         // nullable debug counters (PXST_DEBUG)
 };
 
 // Boxes cover a 16x64 tile's footprint for |du/dx| up to ~1.1 plus noise.
@@ -106,22 +107,13 @@ __global__ void k_tile_geo3(pxst_scan sc, const double* __restrict__ u, int ka, 
     mx1 = fmax(red[0][3], red[w][3]); red[0][3] = mx1;
   }
   mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
-  TileGeo g;
-  g.pad = 0;
-  if (!(mn0 <= mx0)) {
-    g.umin0 = g.umin1 = NAN;
-    g.use_win = 0;
-  } else {
-    g.umin0 = mn0;
-    g.umin1 = mn1;
-    const bool finite = fabs(mn0) < 1e9 && fabs(mx0) < 1e9 && fabs(mn1) < 1e9 && fabs(mx1) < 1e9;
-    // +1 row/col: the sub-pixel phase shift can move floor() by one.
-    const int wr = clamp_span(floor(mx0 - mn0)) + ka + 3;
-    const int wc = clamp_span(floor(mx1 - mn1)) + kb + 3 + 3;
-    g.use_win = finite && wr <= box_r && wc <= box_c;
-  }
-  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = g;
+  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_tile_geo(mn0, mx0, mn1, mx1);
 }
+
+// Window rows / cols beyond the tile's u span: the patch, one of floor()
+// slack, one for the sub-pixel phase shift, and 3 columns of box alignment.
+__host__ __device__ inline int need_rows3(int ka) { return ka + 3; }
+__host__ __device__ inline int need_cols3(int kb) { return kb + 6; }
 
 struct Sample3 {
   int i, j;
@@ -147,7 +139,7 @@ __device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const TileGe
   s.j = finite ? static_cast<int>(yf) : -(1 << 30);
   s.fast = false;
   s.lr = s.lc = 0;
-  if (g.use_win) {
+  if (tile_fits(g, need_rows3(a.ka), need_cols3(a.kb), a.box_r, a.box_c)) {
     const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
     const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
     s.lr = s.i - a.mhi_a - wr0;
@@ -192,12 +184,12 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
 
   PackedAcc<KA, KB> acc;
   acc.zero();
-  bool any_slow = false;
+  __shared__ unsigned tmask[2];    // column tiles (< 64) holding skipped samples
 
   auto issue = [&](int ct) {
     const TileGeo g = grow[ct];
     const int b = ct % kNB;
-    if (g.use_win) {
+    if (tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c)) {
       const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
       const int wc0 =
           align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
@@ -214,12 +206,14 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
       mbar_init(&empty[b], kThreads);
     }
     mbar_fence_init();
+    tmask[0] = tmask[1] = 0u;
   }
   __syncthreads();
   if (threadIdx.x == 0)
     for (int ct = 0; ct < min(kNB, a.n_ct); ++ct) issue(ct);
 
   for (int ct = 0; ct < a.n_ct; ++ct) {
+    bool tile_slow = false;
     const int b = ct % kNB;
     const unsigned ph = (ct / kNB) & 1;
     const TileGeo g = grow[ct];
@@ -241,7 +235,22 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
       fx[e] = static_cast<float>(sm.fx);
       fy[e] = static_cast<float>(sm.fy);
       off[e] = (live && sm.fast) ? sm.lr * a.box_c + sm.lc : -1;
-      any_slow |= live && !sm.fast;
+      tile_slow |= live && !sm.fast;
+      if (a.dbg && live) {   // [samples, !fits, !in-grid, !pv, !box]
+        atomicAdd(a.dbg, 1ull);
+        if (!sm.fast) {
+          const bool in = sm.i >= 0 && sm.i < a.os && sm.j >= 0 && sm.j < a.of;
+          if (!tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c))
+            atomicAdd(a.dbg + 1, 1ull);
+          else if (!in) atomicAdd(a.dbg + 2, 1ull);
+          else if (!a.pv[(int64_t)sm.i * a.of + sm.j]) atomicAdd(a.dbg + 3, 1ull);
+          else atomicAdd(a.dbg + 4, 1ull);
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, tile_slow) && lane == 0) {
+      const int bit = ct < 64 ? ct : 63;            // tiles >= 63 share the last bit
+      atomicOr(&tmask[bit >> 5], 1u << (bit & 31));
     }
     mbar_wait(&full[b], ph);
 #pragma unroll
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
       const float v = warp_sumf(acc.get(t, s));
       if (lane == 0) red[warp][t * KB + s] = v;
     }
-  const int any = __syncthreads_or(any_slow ? 1 : 0);
+  __syncthreads();
   const int nk = a.na_full * a.nb_full;
   float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
   for (int e = threadIdx.x; e < KA * KB; e += kThreads) {
@@ -273,9 +282,13 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
     for (int w = 0; w < kThreads / 32; ++w) v += red[w][e];
     out[full_index(a, e / KB, e % KB)] = v;
   }
-  if (any && threadIdx.x == 0) {
+  const unsigned long long mask =
+      (static_cast<unsigned long long>(tmask[1]) << 32) | static_cast<unsigned long long>(tmask[0]);
+  if (mask && threadIdx.x == 0) {   // hand the flagged tiles of (frame, band) to k_trans_slow
     const unsigned slot = atomicAdd(a.slow_n, 1u);
-    a.slow_list[slot] = (static_cast<unsigned long long>(kk) << 24) | static_cast<unsigned>(band);
+    a.slow_list[2 * slot] =
+        (static_cast<unsigned long long>(kk) << 24) | static_cast<unsigned>(band);
+    a.slow_list[2 * slot + 1] = mask;
   }
 }
 
@@ -320,7 +333,8 @@ __global__ void k_trans_slow(TransArgs a) {
   const int64_t plane = a.sc.ss * a.sc.fs;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   for (int64_t e = warp0; e < n; e += nwarps) {
-    const unsigned long long ent = a.slow_list[e];
+    const unsigned long long ent = a.slow_list[2 * e];
+    const unsigned long long tiles = a.slow_list[2 * e + 1];
     const int64_t kk = static_cast<int64_t>(ent >> 24);
     const int band = static_cast<int>(ent & 0xFFFFFF);
     const int64_t f = a.sc.good[a.frame_lo + kk];
@@ -328,29 +342,29 @@ __global__ void k_trans_slow(TransArgs a) {
     const float* frame = a.sc.frames + f * plane;
     const int64_t r_lo = a.sc.roi[0] + (int64_t)band * kTR;
     const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
-    const int64_t npx = (r_hi - r_lo) * cw;
     float part[kSlowPerLane];
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
-    for (int64_t q0 = 0; q0 < npx; q0 += 32) {
+    for (int ct = 0; ct < a.n_ct; ++ct) {
+     if (!((tiles >> (ct < 64 ? ct : 63)) & 1ull)) continue;   // only flagged tiles
+     const TileGeo g = a.geo[(int64_t)band * a.n_ct + ct];
+     const int64_t c_lo = (int64_t)ct * kTC;
+     const int64_t c_hi = min(cw, c_lo + kTC);
+     const int64_t npx = (r_hi - r_lo) * (c_hi - c_lo);
+     for (int64_t q0 = 0; q0 < npx; q0 += 32) {
       const int64_t ql = q0 + lane;
       bool slow = false;
       int64_t p = 0;
       if (ql < npx) {
-        const int64_t rr = ql / cw, cc = ql % cw;
+        const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
         p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
-        if (a.sc.work[p]) {
-          const TileGeo g = a.geo[(int64_t)band * a.n_ct + cc / kTC];
-          slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
-        }
+        if (a.sc.work[p]) slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
         const int64_t ps = __shfl_sync(0xffffffffu, p, bsel);
-        const int64_t cc = (q0 + bsel) % cw;
-        const TileGeo g = a.geo[(int64_t)band * a.n_ct + cc / kTC];
         const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
         const float I = __ldg(frame + ps), W = a.sc.w32[ps];
         const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
@@ -371,6 +385,7 @@ __global__ void k_trans_slow(TransArgs a) {
         }
         __syncwarp();
       }
+     }
     }
     float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
 #pragma unroll
@@ -590,6 +605,15 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
         *sc, u, max_ka, max_kb, a.box_r, a.box_c, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
+    // Box from the largest tile footprint, <= 256 columns and <= 40 KB per
+    // slot; tiles beyond the cap take the exact path.
+    int span[2];
+    if (int e = tile_span_max(geo.as<TileGeo>(), a.n_bands * a.n_ct, span, s)) return e;
+    a.box_r = max(a.box_r, span[0] + need_rows3(max_ka));
+    a.box_c = max(a.box_c, span[1] + need_cols3(max_kb));
+    a.box_c = (a.box_c + 3) / 4 * 4;
+    if (a.box_c > 256) a.box_c = 256;
+    while (a.box_r > 16 && a.box_r * a.box_c * 4 > 40 * 1024) --a.box_r;
     // union patch box over phases, relative to floor(x_rho): rows
     // [-max mhi, -min mlo + 1]
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
@@ -622,10 +646,16 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     Scratch part;
     const int64_t cmax = min(chunk, n_search);
     if (int e = part.alloc(sizeof(float) * cmax * a.n_bands * nk, s)) return e;
-    if (int e = lst.alloc(sizeof(unsigned long long) * (cmax * a.n_bands + 2), s)) return e;
+    if (int e = lst.alloc(sizeof(unsigned long long) * (2 * cmax * a.n_bands + 2), s)) return e;
     a.partial = part.as<float>();
     a.slow_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
     a.slow_list = lst.as<unsigned long long>() + 1;
+    Scratch dbg;
+    if (getenv("PXST_DEBUG")) {
+      if (int e = dbg.alloc(sizeof(unsigned long long) * 8, s)) return e;
+      PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(unsigned long long) * 8, s));
+      a.dbg = dbg.as<unsigned long long>();
+    }
     const size_t slow_smem = (sizeof(float) + 1) * (max_ka + 1) * (max_kb + 1) * 8;
     for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
       const int64_t c1 = min(frame_hi, c0 + chunk);
@@ -643,13 +673,17 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
         PXST_CHECK_LAUNCH();
         k_trans_slow<<<148 * 4, 256, slow_smem, s>>>(a);
         PXST_CHECK_LAUNCH();
-        if (getenv("PXST_DEBUG")) {
+        if (a.dbg) {
           unsigned h = 0;
+          unsigned long long d[5];
           PXST_CHECK_CUDA(cudaMemcpyAsync(&h, a.slow_n, sizeof(h), cudaMemcpyDeviceToHost, s));
+          PXST_CHECK_CUDA(cudaMemcpyAsync(d, a.dbg, sizeof(d), cudaMemcpyDeviceToHost, s));
           PXST_CHECK_CUDA(cudaStreamSynchronize(s));
           fprintf(stderr, "[pxst] K3 phase (%d,%d) %dx%d: %lld frames x %lld bands, %u slow "
-                  "(frame, band) pairs\n", ph.rho_a, ph.rho_b, a.ka, a.kb,
-                  (long long)(c1 - c0), (long long)a.n_bands, h);
+                  "(frame, band) pairs; samples %llu, slow: no-window %llu, outside %llu, "
+                  "patch-invalid %llu, box %llu\n", ph.rho_a, ph.rho_b, a.ka, a.kb,
+                  (long long)(c1 - c0), (long long)a.n_bands, h, d[0], d[1], d[2], d[3], d[4]);
+          PXST_CHECK_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(d), s));
         }
       }
       k_trans_epilogue<float><<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
