@@ -4,30 +4,30 @@
 // u - (delta_n + off) - origin (note the minus sign, recon.py:373-374).
 //
 // Pipeline (integer grids and sub-pixel grids with integral 1/step):
-//   1. k_tile_geo3   per 16x64 pixel tile: u bounding box -> window origin
-//                    and "fits the TMA box" flag.
-//   2. k_trans_fast  grid (bands of 16 rows, searched frames).  The CTA walks
-//                    the band's column tiles; each tile's object window for
-//                    the frame is fetched by TMA into a 4-slot ring; every
-//                    thread (4 pixels per tile) runs the FFMA2 trial engine
-//                    into registers across all tiles; one deterministic CTA
-//                    reduction at the end writes float32
-//                    partial[frame][band][trial].  Samples whose patch leaves
-//                    the grid or touches an invalid cell are skipped and the
-//                    (frame, band) pair is listed.
-//   3. k_trans_slow  one warp per listed (frame, band): re-derives eligibility
-//                    lane-parallel over pixels, stages each skipped sample's
-//                    patch in shared memory, lanes over trials with the exact
-//                    masked read and (I-W)^2 fallback, register accumulation,
-//                    one add per trial into the partial (lane-owned: ordered).
-//   4. k_trans_epilogue per frame: float64 sum over bands (fixed order),
-//                    normalise by sum_p (I_n-W)^2, first-occurrence argmin,
-//                    always-on paraboloid when interior (grid-index units added
-//                    in pixels), write translations.
+//   1. k_tile_geo3   per 16x64 pixel tile: u bounding box and span; the host
+//                    sizes the TMA box from the largest span.
+//   2. k_trans_fast  one CTA per searched frame walks every tile of the ROI:
+//                    each tile's object window for the frame is fetched by TMA
+//                    into a 4-slot ring (mbarrier full/empty), every thread
+//                    (4 pixels per tile) runs the FFMA2 trial engine into
+//                    registers across all tiles, one deterministic CTA
+//                    reduction (float64) writes partial[frame][trial].  Samples
+//                    whose patch leaves the grid or touches an invalid cell are
+//                    skipped; their tiles are flagged in a per-frame bitmap and
+//                    the frame is listed.
+//   3. k_trans_slow  one warp per listed frame: re-derives eligibility over the
+//                    flagged tiles' pixels lane-parallel, stages each skipped
+//                    sample's patch in shared memory, lanes over trials with the
+//                    exact masked read and (I-W)^2 fallback, register
+//                    accumulation, one add per trial into the frame's partial
+//                    (single owner: ordered, deterministic).
+//   4. k_trans_epilogue per frame: normalise by sum_p (I_n-W)^2,
+//                    first-occurrence argmin, always-on paraboloid when interior
+//                    (grid-index units added in pixels).
 // Sub-pixel grids with q = 1/step integral decompose into q^2 phase groups:
 // trial k = q m + rho sits at floor(x - step*rho) - m with fractions common
-// to every m, i.e. an integer window of the same engine (launched per phase).
-// Other grids use k_trans_generic (float64, CTA per (frame, trial)).
+// to every m, i.e. an integer window of the same engine (one launch per
+// phase).  Other grids use k_trans_generic (float64, CTA per (frame, trial)).
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -57,6 +57,7 @@ struct TransArgs {
   const TileGeo* geo;        // [n_bands][n_ct]
   int n_ct;                  // column tiles per band
   int64_t n_bands;
+  int64_t n_tiles;           // n_bands * n_ct
   int64_t frame_lo;          // first searched frame of this launch (index into good)
   // phase group
   double ph_a, ph_b;         // sub-pixel phase shifts step*rho (0 for integer grids)
@@ -67,22 +68,26 @@ struct TransArgs {
   int kh_a, kh_b;            // full-grid half counts (offset index = k + kh)
   int na_full, nb_full;
   int box_r, box_c;          // TMA box
-  int pv_lr, pv_hr, pv_lc, pv_hc;  // union patch box rows/cols relative to floor(x_rho)
-  float* partial;            // [chunk frames][n_bands][na_full*nb_full]
-  unsigned long long* slow_list;   // (frame_in_chunk << 24 | band) pairs with skipped samples
+  double* partial;           // [chunk frames][na_full*nb_full]
+  unsigned long long* tilebits;    // [chunk frames][words] flagged tiles
+  int tile_words;
+  unsigned* slow_list;       // frames (within the chunk) with flagged tiles
   unsigned* slow_n;
-  unsigned long long* dbg;         // nullable debug counters (PXST_DEBUG)
+  unsigned long long* dbg;   // nullable debug counters (PXST_DEBUG)
 };
 
-// Boxes cover a 16x64 tile's footprint for |du/dx| up to ~1.1 plus noise.
+// Boxes cover a 16x64 tile's footprint; the host grows them from the measured spans.
 __host__ __device__ inline int box_rows3(int ka) { return ka + 24; }
 __host__ __device__ inline int box_cols3(int kb) { return ((kb + 76 + 3) / 4) * 4; }
+// Window rows / cols beyond the tile's u span: the patch, one of floor()
+// slack, one for the sub-pixel phase shift, and 3 columns of box alignment.
+__host__ __device__ inline int need_rows3(int ka) { return ka + 3; }
+__host__ __device__ inline int need_cols3(int kb) { return kb + 6; }
 
 // ---------------------------------------------------------------------------
 // 1. tile geometry (16 x 64 tiles)
 // ---------------------------------------------------------------------------
-__global__ void k_tile_geo3(pxst_scan sc, const double* __restrict__ u, int ka, int kb,
-                            int box_r, int box_c, TileGeo* geo) {
+__global__ void k_tile_geo3(pxst_scan sc, const double* __restrict__ u, TileGeo* geo) {
   __shared__ double red[kThreads / 32][4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t plane = sc.ss * sc.fs;
@@ -109,11 +114,6 @@ __global__ void k_tile_geo3(pxst_scan sc, const double* __restrict__ u, int ka, 
   mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
   geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_tile_geo(mn0, mx0, mn1, mx1);
 }
-
-// Window rows / cols beyond the tile's u span: the patch, one of floor()
-// slack, one for the sub-pixel phase shift, and 3 columns of box alignment.
-__host__ __device__ inline int need_rows3(int ka) { return ka + 3; }
-__host__ __device__ inline int need_cols3(int kb) { return kb + 6; }
 
 struct Sample3 {
   int i, j;
@@ -159,36 +159,35 @@ __device__ __forceinline__ int full_index(const TransArgs& a, int t, int s) {
 }
 
 // ---------------------------------------------------------------------------
-// 2. fast kernel
+// 2. fast kernel: one CTA per searched frame
 // ---------------------------------------------------------------------------
 template <int KA, int KB>
 __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
     k_trans_fast(const __grid_constant__ CUtensorMap tmap, TransArgs a) {
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
-  __shared__ float red[kThreads / 32][KA * KB];
+  __shared__ double red[kThreads / 32][KA * KB];
+  __shared__ int any_flag;
   unsigned char* base = ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u);
   float* ring = reinterpret_cast<float*>(base);
   const int box = slot_floats(a.box_r, a.box_c);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int band = blockIdx.x;
-  const int64_t kk = blockIdx.y;                     // frame within this launch's chunk
+  const int64_t kk = blockIdx.x;                     // frame within this launch's chunk
   const int64_t f = a.sc.good[a.frame_lo + kk];
   const double dI = a.di[f], dJ = a.dj[f];
   const int64_t plane = a.sc.ss * a.sc.fs;
   const float* frame = a.sc.frames + f * plane;
-  const TileGeo* grow = a.geo + (int64_t)band * a.n_ct;
   const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
   const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
+  unsigned long long* bits = a.tilebits + kk * a.tile_words;
 
   PackedAcc<KA, KB> acc;
   acc.zero();
-  __shared__ unsigned tmask[2];    // column tiles (< 64) holding skipped samples
 
-  auto issue = [&](int ct) {
-    const TileGeo g = grow[ct];
-    const int b = ct % kNB;
+  auto issue = [&](int64_t it) {
+    const TileGeo g = a.geo[it];
+    const int b = static_cast<int>(it % kNB);
     if (tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c)) {
       const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
       const int wc0 =
@@ -206,24 +205,25 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
       mbar_init(&empty[b], kThreads);
     }
     mbar_fence_init();
-    tmask[0] = tmask[1] = 0u;
+    any_flag = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0)
-    for (int ct = 0; ct < min(kNB, a.n_ct); ++ct) issue(ct);
+    for (int64_t it = 0; it < (a.n_tiles < kNB ? a.n_tiles : kNB); ++it) issue(it);
 
-  for (int ct = 0; ct < a.n_ct; ++ct) {
-    bool tile_slow = false;
-    const int b = ct % kNB;
-    const unsigned ph = (ct / kNB) & 1;
-    const TileGeo g = grow[ct];
+  for (int64_t it = 0; it < a.n_tiles; ++it) {
+    const int b = static_cast<int>(it % kNB);
+    const unsigned ph = static_cast<unsigned>((it / kNB) & 1);
+    const int64_t band = it / a.n_ct;
+    const int ct = static_cast<int>(it % a.n_ct);
+    const TileGeo g = a.geo[it];
     // this thread's 4 pixels of the tile: rows 2w, 2w+1; cols lane, lane+32
-    // compact per-sample state (5 registers each) to keep the window in registers
     float I[4], W[4], fx[4], fy[4];
     int off[4];                        // patch origin offset in the slot, -1 = not fast
+    bool tile_slow = false;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int64_t row = a.sc.roi[0] + (int64_t)band * kTR + 2 * warp + (e >> 1);
+      const int64_t row = a.sc.roi[0] + band * kTR + 2 * warp + (e >> 1);
       const int64_t col = a.sc.roi[2] + (int64_t)ct * kTC + lane + 32 * (e & 1);
       const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
       const int64_t p = in ? row * a.sc.fs + col : 0;
@@ -239,18 +239,18 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
       if (a.dbg && live) {   // [samples, !fits, !in-grid, !pv, !box]
         atomicAdd(a.dbg, 1ull);
         if (!sm.fast) {
-          const bool in = sm.i >= 0 && sm.i < a.os && sm.j >= 0 && sm.j < a.of;
+          const bool ing = sm.i >= 0 && sm.i < a.os && sm.j >= 0 && sm.j < a.of;
           if (!tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c))
             atomicAdd(a.dbg + 1, 1ull);
-          else if (!in) atomicAdd(a.dbg + 2, 1ull);
+          else if (!ing) atomicAdd(a.dbg + 2, 1ull);
           else if (!a.pv[(int64_t)sm.i * a.of + sm.j]) atomicAdd(a.dbg + 3, 1ull);
           else atomicAdd(a.dbg + 4, 1ull);
         }
       }
     }
     if (__any_sync(0xffffffffu, tile_slow) && lane == 0) {
-      const int bit = ct < 64 ? ct : 63;            // tiles >= 63 share the last bit
-      atomicOr(&tmask[bit >> 5], 1u << (bit & 31));
+      atomicOr(&bits[it >> 6], 1ull << (it & 63));
+      any_flag = 1;
     }
     mbar_wait(&full[b], ph);
 #pragma unroll
@@ -260,40 +260,36 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
                              W[e] * (1.f - fx[e]), W[e] * fx[e], I[e], acc);
     }
     mbar_arrive(&empty[b]);
-    if (threadIdx.x == 0 && ct + kNB < a.n_ct) {
+    if (threadIdx.x == 0 && it + kNB < a.n_tiles) {
       mbar_wait(&empty[b], ph);
-      issue(ct + kNB);
+      issue(it + kNB);
     }
   }
-  // deterministic CTA reduction: warp shuffles, then a fixed-order sum of warps
+  // deterministic CTA reduction: float32 warp shuffles, then a fixed-order
+  // float64 sum of the warps
 #pragma unroll
   for (int t = 0; t < KA; ++t)
 #pragma unroll
     for (int s = 0; s < KB; ++s) {
       const float v = warp_sumf(acc.get(t, s));
-      if (lane == 0) red[warp][t * KB + s] = v;
+      if (lane == 0) red[warp][t * KB + s] = static_cast<double>(v);
     }
   __syncthreads();
-  const int nk = a.na_full * a.nb_full;
-  float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
+  double* out = a.partial + kk * (int64_t)(a.na_full * a.nb_full);
   for (int e = threadIdx.x; e < KA * KB; e += kThreads) {
-    float v = 0.f;
+    double v = 0.0;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) v += red[w][e];
     out[full_index(a, e / KB, e % KB)] = v;
   }
-  const unsigned long long mask =
-      (static_cast<unsigned long long>(tmask[1]) << 32) | static_cast<unsigned long long>(tmask[0]);
-  if (mask && threadIdx.x == 0) {   // hand the flagged tiles of (frame, band) to k_trans_slow
+  if (any_flag && threadIdx.x == 0) {   // hand the flagged tiles to k_trans_slow
     const unsigned slot = atomicAdd(a.slow_n, 1u);
-    a.slow_list[2 * slot] =
-        (static_cast<unsigned long long>(kk) << 24) | static_cast<unsigned>(band);
-    a.slow_list[2 * slot + 1] = mask;
+    a.slow_list[slot] = static_cast<unsigned>(kk);
   }
 }
 
 // ---------------------------------------------------------------------------
-// 3. slow fix-up: warp per listed (frame, band)
+// 3. slow fix-up: warp per listed frame
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float trial_patch3(const float* __restrict__ pf,
                                               const uint8_t* __restrict__ pvld, int ld, int pr0,
@@ -333,65 +329,65 @@ __global__ void k_trans_slow(TransArgs a) {
   const int64_t plane = a.sc.ss * a.sc.fs;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   for (int64_t e = warp0; e < n; e += nwarps) {
-    const unsigned long long ent = a.slow_list[2 * e];
-    const unsigned long long tiles = a.slow_list[2 * e + 1];
-    const int64_t kk = static_cast<int64_t>(ent >> 24);
-    const int band = static_cast<int>(ent & 0xFFFFFF);
+    const int64_t kk = a.slow_list[e];
     const int64_t f = a.sc.good[a.frame_lo + kk];
     const double dI = a.di[f], dJ = a.dj[f];
     const float* frame = a.sc.frames + f * plane;
-    const int64_t r_lo = a.sc.roi[0] + (int64_t)band * kTR;
-    const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
+    const unsigned long long* bits = a.tilebits + kk * a.tile_words;
     float part[kSlowPerLane];
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
-    for (int ct = 0; ct < a.n_ct; ++ct) {
-     if (!((tiles >> (ct < 64 ? ct : 63)) & 1ull)) continue;   // only flagged tiles
-     const TileGeo g = a.geo[(int64_t)band * a.n_ct + ct];
-     const int64_t c_lo = (int64_t)ct * kTC;
-     const int64_t c_hi = min(cw, c_lo + kTC);
-     const int64_t npx = (r_hi - r_lo) * (c_hi - c_lo);
-     for (int64_t q0 = 0; q0 < npx; q0 += 32) {
-      const int64_t ql = q0 + lane;
-      bool slow = false;
-      int64_t p = 0;
-      if (ql < npx) {
-        const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
-        p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
-        if (a.sc.work[p]) slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
-      }
-      unsigned mask = __ballot_sync(0xffffffffu, slow);
-      while (mask) {
-        const int bsel = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int64_t ps = __shfl_sync(0xffffffffu, p, bsel);
-        const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
-        const float I = __ldg(frame + ps), W = a.sc.w32[ps];
-        const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
-        for (int idx = lane; idx < pn; idx += 32) {
-          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
-          const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
-          const int64_t o = in ? (int64_t)r * a.of + c : 0;
-          pf[idx] = in ? __ldg(a.fm + o) : 0.f;
-          pvld[idx] = in ? __ldg(a.valid + o) : 0;
+    for (int64_t it = 0; it < a.n_tiles; ++it) {
+      if (!((bits[it >> 6] >> (it & 63)) & 1ull)) continue;     // only flagged tiles
+      const int64_t band = it / a.n_ct;
+      const int ct = static_cast<int>(it % a.n_ct);
+      const TileGeo g = a.geo[it];
+      const int64_t r_lo = a.sc.roi[0] + band * kTR;
+      const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
+      const int64_t c_lo = (int64_t)ct * kTC;
+      const int64_t c_hi = min(cw, c_lo + kTC);
+      const int64_t npx = (r_hi - r_lo) * (c_hi - c_lo);
+      for (int64_t q0 = 0; q0 < npx; q0 += 32) {
+        const int64_t ql = q0 + lane;
+        bool slow = false;
+        int64_t p = 0;
+        if (ql < npx) {
+          const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
+          p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
+          if (a.sc.work[p]) slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
         }
-        __syncwarp();
+        unsigned mask = __ballot_sync(0xffffffffu, slow);
+        while (mask) {
+          const int bsel = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int64_t ps = __shfl_sync(0xffffffffu, p, bsel);
+          const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
+          const float I = __ldg(frame + ps), W = a.sc.w32[ps];
+          const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
+          for (int idx = lane; idx < pn; idx += 32) {
+            const int r = pr0 + idx / ld, c = pc0 + idx % ld;
+            const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
+            const int64_t o = in ? (int64_t)r * a.of + c : 0;
+            pf[idx] = in ? __ldg(a.fm + o) : 0.f;
+            pvld[idx] = in ? __ldg(a.valid + o) : 0;
+          }
+          __syncwarp();
 #pragma unroll
-        for (int j = 0; j < kSlowPerLane; ++j) {
-          const int t = lane + 32 * j;
-          if (t < nk_ph)
-            part[j] += trial_patch3(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
-                                    pc0 + t % a.kb, sm.fx, sm.fy, W, I);
+          for (int j = 0; j < kSlowPerLane; ++j) {
+            const int t = lane + 32 * j;
+            if (t < nk_ph)
+              part[j] += trial_patch3(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
+                                      pc0 + t % a.kb, sm.fx, sm.fy, W, I);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
-     }
     }
-    float* out = a.partial + (kk * a.n_bands + band) * (int64_t)nk;
+    double* out = a.partial + kk * (int64_t)nk;
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) {
       const int t = lane + 32 * j;
-      if (t < nk_ph) out[full_index(a, t / a.kb, t % a.kb)] += part[j];
+      if (t < nk_ph) out[full_index(a, t / a.kb, t % a.kb)] += static_cast<double>(part[j]);
     }
   }
 }
@@ -440,10 +436,9 @@ __global__ void k_trans_generic(TransArgs a, const double* __restrict__ offs_a,
 // ---------------------------------------------------------------------------
 // 4. per-frame epilogue
 // ---------------------------------------------------------------------------
-template <class T>
 __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_norm,
-                                 const T* __restrict__ part, int64_t n_bands, int64_t frame_lo,
-                                 int na, int nb, const double* __restrict__ offs_a,
+                                 const double* __restrict__ part, int64_t frame_lo, int na,
+                                 int nb, const double* __restrict__ offs_a,
                                  const double* __restrict__ offs_b, const double* di,
                                  const double* dj, double* di_out, double* dj_out,
                                  double* err_out) {
@@ -455,12 +450,8 @@ __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_
   const int64_t f = sc.good[k];
   const double norm = frame_norm[k];
   const int nk = na * nb;
-  const T* pp = part + kk * n_bands * nk;
-  for (int t = threadIdx.x; t < nk; t += blockDim.x) {
-    double s = 0.0;
-    for (int64_t b = 0; b < n_bands; ++b) s += static_cast<double>(pp[b * nk + t]);
-    e[t] = norm > 0.0 ? s / norm : s;
-  }
+  const double* pp = part + kk * nk;
+  for (int t = threadIdx.x; t < nk; t += blockDim.x) e[t] = norm > 0.0 ? pp[t] / norm : pp[t];
   __syncthreads();
   if (err_out)
     for (int t = threadIdx.x; t < nk; t += blockDim.x) err_out[kk * nk + t] = e[t];
@@ -583,6 +574,15 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
   }
 
   const int64_t n_search = frame_hi - frame_lo;
+  // frame chunks so the partial buffer stays <= 256 MB
+  int64_t chunk = (256ll << 20) / (8 * (int64_t)nk);
+  chunk = chunk < kMaxGridY ? chunk : kMaxGridY;
+  chunk = chunk > 1 ? chunk : 1;
+  const int64_t cmax = min(chunk, n_search);
+  Scratch part;
+  if (int e = part.alloc(sizeof(double) * cmax * nk, s)) return e;
+  a.partial = part.as<double>();
+
   if (fast) {
     int max_ka = 0, max_kb = 0, mhi_a = -1 << 20, mlo_a = 1 << 20, mhi_b = -1 << 20,
         mlo_b = 1 << 20;
@@ -596,19 +596,21 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     a.box_c = box_cols3(max_kb);
     a.n_ct = static_cast<int>((cw + kTC - 1) / kTC);
     a.n_bands = (rw + kTR - 1) / kTR;
+    a.n_tiles = a.n_bands * a.n_ct;
     PXST_REQUIRE(a.n_bands <= kMaxGridY, "ROI too tall");
     a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
+    a.tile_words = static_cast<int>((a.n_tiles + 63) / 64);
 
-    Scratch geo, pvbuf, pvtmp, fmpad, lst;
-    if (int e = geo.alloc(sizeof(TileGeo) * a.n_bands * a.n_ct, s)) return e;
+    Scratch geo, pvbuf, pvtmp, fmpad, lst, tb;
+    if (int e = geo.alloc(sizeof(TileGeo) * a.n_tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
-        *sc, u, max_ka, max_kb, a.box_r, a.box_c, geo.as<TileGeo>());
+        *sc, u, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
     // Box from the largest tile footprint, <= 256 columns and <= 40 KB per
     // slot; tiles beyond the cap take the exact path.
     int span[2];
-    if (int e = tile_span_max(geo.as<TileGeo>(), a.n_bands * a.n_ct, span, s)) return e;
+    if (int e = tile_span_max(geo.as<TileGeo>(), a.n_tiles, span, s)) return e;
     a.box_r = max(a.box_r, span[0] + need_rows3(max_ka));
     a.box_c = max(a.box_c, span[1] + need_cols3(max_kb));
     a.box_c = (a.box_c + 3) / 4 * 4;
@@ -639,17 +641,12 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     for (const auto& ph : phases)
       PXST_CHECK_CUDA(cudaFuncSetAttribute(ph.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(smem)));
-    // frame chunks so the partial buffer stays <= 256 MB
-    int64_t chunk = (256ll << 20) / (4 * a.n_bands * nk);
-    chunk = chunk < kMaxGridY ? chunk : kMaxGridY;
-    chunk = chunk > 1 ? chunk : 1;
-    Scratch part;
-    const int64_t cmax = min(chunk, n_search);
-    if (int e = part.alloc(sizeof(float) * cmax * a.n_bands * nk, s)) return e;
-    if (int e = lst.alloc(sizeof(unsigned long long) * (2 * cmax * a.n_bands + 2), s)) return e;
-    a.partial = part.as<float>();
-    a.slow_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
-    a.slow_list = lst.as<unsigned long long>() + 1;
+    if (int e = lst.alloc(sizeof(unsigned) * (cmax + 2), s)) return e;
+    a.slow_n = lst.as<unsigned>();
+    a.slow_list = lst.as<unsigned>() + 1;
+    const size_t tb_bytes = sizeof(unsigned long long) * cmax * a.tile_words;
+    if (int e = tb.alloc(tb_bytes, s)) return e;
+    a.tilebits = tb.as<unsigned long long>();
     Scratch dbg;
     if (getenv("PXST_DEBUG")) {
       if (int e = dbg.alloc(sizeof(unsigned long long) * 8, s)) return e;
@@ -668,8 +665,8 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
         a.ph_a = subpixel_step > 0.0 ? subpixel_step * ph.rho_a : 0.0;
         a.ph_b = subpixel_step > 0.0 ? subpixel_step * ph.rho_b : 0.0;
         PXST_CHECK_CUDA(cudaMemsetAsync(a.slow_n, 0, sizeof(unsigned), s));
-        dim3 g((unsigned)a.n_bands, (unsigned)(c1 - c0));
-        ph.fn<<<g, kThreads, smem, s>>>(tmap, a);
+        PXST_CHECK_CUDA(cudaMemsetAsync(a.tilebits, 0, tb_bytes, s));
+        ph.fn<<<(unsigned)(c1 - c0), kThreads, smem, s>>>(tmap, a);
         PXST_CHECK_LAUNCH();
         k_trans_slow<<<148 * 4, 256, slow_smem, s>>>(a);
         PXST_CHECK_LAUNCH();
@@ -679,35 +676,31 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
           PXST_CHECK_CUDA(cudaMemcpyAsync(&h, a.slow_n, sizeof(h), cudaMemcpyDeviceToHost, s));
           PXST_CHECK_CUDA(cudaMemcpyAsync(d, a.dbg, sizeof(d), cudaMemcpyDeviceToHost, s));
           PXST_CHECK_CUDA(cudaStreamSynchronize(s));
-          fprintf(stderr, "[pxst] K3 phase (%d,%d) %dx%d: %lld frames x %lld bands, %u slow "
-                  "(frame, band) pairs; samples %llu, slow: no-window %llu, outside %llu, "
+          fprintf(stderr, "[pxst] K3 phase (%d,%d) %dx%d: %lld frames, %lld tiles, box %dx%d, "
+                  "%u frames with slow tiles; samples %llu, slow: no-fit %llu, outside %llu, "
                   "patch-invalid %llu, box %llu\n", ph.rho_a, ph.rho_b, a.ka, a.kb,
-                  (long long)(c1 - c0), (long long)a.n_bands, h, d[0], d[1], d[2], d[3], d[4]);
+                  (long long)(c1 - c0), (long long)a.n_tiles, a.box_r, a.box_c, h, d[0], d[1],
+                  d[2], d[3], d[4]);
           PXST_CHECK_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(d), s));
         }
       }
-      k_trans_epilogue<float><<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
-          *sc, st->frame_norm, part.as<float>(), a.n_bands, c0, na, nb, d_oa, d_ob, di, dj,
-          di_out, dj_out, err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
+      k_trans_epilogue<<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
+          *sc, st->frame_norm, part.as<double>(), c0, na, nb, d_oa, d_ob, di, dj, di_out,
+          dj_out, err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
       PXST_CHECK_LAUNCH();
     }
     return PXST_OK;
   }
   // generic path
-  int64_t chunk = (256ll << 20) / (8 * (int64_t)nk);
-  chunk = chunk < kMaxGridY ? chunk : kMaxGridY;
-  chunk = chunk > 1 ? chunk : 1;
-  Scratch errs;
-  if (int e = errs.alloc(sizeof(double) * min(chunk, n_search) * nk, s)) return e;
   for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
     const int64_t c1 = min(frame_hi, c0 + chunk);
     a.frame_lo = c0;
     dim3 g((unsigned)nk, (unsigned)(c1 - c0));
-    k_trans_generic<<<g, 256, 0, s>>>(a, d_oa, d_ob, errs.as<double>());
+    k_trans_generic<<<g, 256, 0, s>>>(a, d_oa, d_ob, part.as<double>());
     PXST_CHECK_LAUNCH();
-    k_trans_epilogue<double><<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
-        *sc, st->frame_norm, errs.as<double>(), 1, c0, na, nb, d_oa, d_ob, di, dj, di_out,
-        dj_out, err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
+    k_trans_epilogue<<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
+        *sc, st->frame_norm, part.as<double>(), c0, na, nb, d_oa, d_ob, di, dj, di_out, dj_out,
+        err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
     PXST_CHECK_LAUNCH();
   }
   return PXST_OK;
