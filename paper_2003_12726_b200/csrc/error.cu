@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kTR = 8, kTC = 32, kThreads = kTR * kTC;
 constexpr int kFB = 8;  // frames per reduction batch
+constexpr int kLB = 4;  // frames per load batch (loads issued before the batch's REDs)
 
 struct ErrArgs {
   pxst_scan sc;
@@ -35,7 +36,7 @@ struct ErrArgs {
 };
 
 // Per-pixel sums, per-(frame, CTA) partials, reference-plane splat.
-__global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pixel,
+__global__ void __launch_bounds__(kThreads, 2) k_err_pass(ErrArgs a, double* per_pixel,
                                                        double* part, int64_t n_ctas) {
   __shared__ double red[kThreads / 32][kFB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -47,57 +48,88 @@ __global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pi
   const bool live = inroi && a.sc.work[p] != 0;
   const int64_t plane = a.sc.ss * a.sc.fs;
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
-  const float W = live ? a.sc.w32[p] : 0.f;
   const double W64 = live ? a.sc.w64[p] : 0.0;
   const double s2 = live ? a.sigma2[p] : 1.0;
   const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
+  __shared__ double t_di[kFB], t_dj[kFB];
+  __shared__ int64_t t_off[kFB];
   double pix = 0.0;
   for (int64_t k0 = 0; k0 < a.sc.n_good; k0 += kFB) {
+    if (threadIdx.x < kFB && k0 + threadIdx.x < a.sc.n_good) {
+      const int64_t f = a.sc.good[k0 + threadIdx.x];
+      t_di[threadIdx.x] = a.di[f];
+      t_dj[threadIdx.x] = a.dj[f];
+      t_off[threadIdx.x] = f * plane;
+    }
+    __syncthreads();   // also orders the previous batch's red[] reads before reuse
     double e[kFB];
 #pragma unroll
-    for (int b = 0; b < kFB; ++b) {
-      const int64_t k = k0 + b;
-      e[b] = 0.0;
-      if (live && k < a.sc.n_good) {
-        const int64_t f = a.sc.good[k];
-        const double x = u0 - a.di[f] - static_cast<double>(a.n0);   // recon.py:418
-        const double y = u1 - a.dj[f] - static_cast<double>(a.m0);
-        const float I = __ldg(a.sc.frames + f * plane + p);
-        const bool in = x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
-        bool ok = false;
-        Split sx{0, 0.0}, sy{0, 0.0};
-        double r;
-        if (in) {
-          sx = split(x);
-          sy = split(y);
-        }
-        if (a.fm64) {
-          double v = 0.0;
-          if (in) ok = masked_read64(a.fm64, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
-          r = ok ? static_cast<double>(I) - W64 * v : static_cast<double>(I) - W64;
-        } else {
-          float v = 0.f;
-          if (in) ok = masked_read(a.fm, a.valid, a.os, a.of, sx.i, sy.i, sx.f, sy.f, v);
-          r = static_cast<double>(ok ? fmaf(-W, v, I) : I - W);
-        }
-        const double eps = (r * r) / s2;                              // recon.py:421-422
-        e[b] = eps;
-        pix += eps;
-        if (in) {                                                     // recon.py:425
-          const int r0 = sx.i, c0 = sy.i;
-          const int r1 = min(r0 + 1, static_cast<int>(a.os - 1));
-          const int c1 = min(c0 + 1, static_cast<int>(a.of - 1));
-          const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
-          const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
-          const int64_t cell[4] = {(int64_t)r0 * a.of + c0, (int64_t)r0 * a.of + c1,
-                                   (int64_t)r1 * a.of + c0, (int64_t)r1 * a.of + c1};
+    for (int h = 0; h < kFB; h += kLB) {
+    // Phase A: every load of the sub-batch is issued before any RED of it
+    // (REDs pin the program order of later loads).
+    float Iv[kLB];
+    bool inb[kLB];
+    double fxb[kLB], fyb[kLB];
+    int64_t a00[kLB];
+    int dc[kLB], dr[kLB];               // corner offsets (clipped at the grid edge)
+    double v4[kLB][4];
+    uint8_t m4[kLB][4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            atomicAdd(a.num + cell[q], eps * cw[q]);
-            atomicAdd(a.den + cell[q], cw[q]);
-          }
+    for (int b = 0; b < kLB; ++b) {
+      const int64_t k = k0 + h + b;
+      const bool act = live && k < a.sc.n_good;
+      const double x = u0 - t_di[h + b] - static_cast<double>(a.n0);   // recon.py:418
+      const double y = u1 - t_dj[h + b] - static_cast<double>(a.m0);
+      inb[b] = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
+      Iv[b] = act ? __ldg(a.sc.frames + t_off[h + b] + p) : 0.f;
+      const Split sx = split(inb[b] ? x : 0.0), sy = split(inb[b] ? y : 0.0);
+      fxb[b] = sx.f;
+      fyb[b] = sy.f;
+      dr[b] = sx.i + 1 < a.os ? static_cast<int>(a.of) : 0;
+      dc[b] = sy.i + 1 < a.of ? 1 : 0;
+      a00[b] = (int64_t)sx.i * a.of + sy.i;
+      const int64_t ad[4] = {a00[b], a00[b] + dc[b], a00[b] + dr[b], a00[b] + dr[b] + dc[b]};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        m4[b][q] = inb[b] ? __ldg(a.valid + ad[q]) : 0;
+        // fm / fm64 are 0 on invalid cells (where(m, f, 0), interp.py:64)
+        v4[b][q] = !inb[b] ? 0.0 : (a.fm64 ? __ldg(a.fm64 + ad[q])
+                                           : static_cast<double>(__ldg(a.fm + ad[q])));
+      }
+    }
+    // Phase B: residuals, sums, reference-plane splat.
+#pragma unroll
+    for (int b = 0; b < kLB; ++b) {
+      e[h + b] = 0.0;
+      const int64_t k = k0 + h + b;
+      if (!(live && k < a.sc.n_good)) continue;
+      const double fx = fxb[b], fy = fyb[b], gx = 1.0 - fx, gy = 1.0 - fy;
+      const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};
+      bool ok = false;
+      double v = 0.0;
+      if (inb[b]) {                                   // interp.py:70-84
+        const double den = cw[0] * m4[b][0] + cw[1] * m4[b][1] + cw[2] * m4[b][2] +
+                           cw[3] * m4[b][3];
+        const double nm = cw[0] * v4[b][0] + cw[1] * v4[b][1] + cw[2] * v4[b][2] +
+                          cw[3] * v4[b][3];
+        ok = den > 0.0;
+        v = ok ? nm / den : 0.0;
+      }
+      const double I = static_cast<double>(Iv[b]);
+      const double r = ok ? I - W64 * v : I - W64;  // recon.py:421
+      const double eps = (r * r) / s2;                // recon.py:422
+      e[h + b] = eps;
+      pix += eps;
+      if (inb[b]) {                                   // recon.py:425
+        const int64_t cell[4] = {a00[b], a00[b] + dc[b], a00[b] + dr[b],
+                                 a00[b] + dr[b] + dc[b]};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          atomicAdd(a.num + cell[q], eps * cw[q]);
+          atomicAdd(a.den + cell[q], cw[q]);
         }
       }
+    }
     }
 #pragma unroll
     for (int b = 0; b < kFB; ++b) {
@@ -111,7 +143,6 @@ __global__ void __launch_bounds__(kThreads) k_err_pass(ErrArgs a, double* per_pi
       for (int w = 0; w < kThreads / 32; ++w) s += red[w][threadIdx.x];
       part[(k0 + threadIdx.x) * n_ctas + cta] = s;
     }
-    __syncthreads();
   }
   if (live) per_pixel[p] = pix;
 }

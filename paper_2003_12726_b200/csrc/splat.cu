@@ -24,29 +24,46 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
                const double* __restrict__ dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
                int64_t frame_lo, int64_t frame_hi, double* __restrict__ num,
                double* __restrict__ den, unsigned long long* __restrict__ n_drop) {
+  // Per-frame scalars of the chunk staged once per block; every stack value
+  // of the chunk is loaded before the first RED, so the loads are one round
+  // trip instead of one per frame (REDs pin the program order of later loads).
+  __shared__ double t_di[kFrameChunk], t_dj[kFrameChunk];
+  __shared__ int64_t t_off[kFrameChunk];
   const int64_t c = sc.roi[2] + blockIdx.x * (int64_t)kTC + threadIdx.x;
   const int64_t r = sc.roi[0] + blockIdx.y;
   const int64_t k_lo = frame_lo + (int64_t)blockIdx.z * kFrameChunk;
   const int64_t k_hi = min(frame_hi, k_lo + kFrameChunk);
+  const int nk = static_cast<int>(k_hi - k_lo);
+  const int64_t plane = sc.ss * sc.fs;
+  if (threadIdx.x < nk) {
+    const int64_t f = sc.good[k_lo + threadIdx.x];
+    t_di[threadIdx.x] = di[f];
+    t_dj[threadIdx.x] = dj[f];
+    t_off[threadIdx.x] = f * plane;
+  }
+  __syncthreads();
   if (c >= sc.roi[3]) return;
   const int64_t p = r * sc.fs + c;
   if (!sc.work[p]) return;
-  const int64_t plane = sc.ss * sc.fs;
   const double u0 = u[p], u1 = u[plane + p];
   const double w = sc.w64[p];
   const double w2 = w * w;                       // recon.py:136
+  float Iv[kFrameChunk];
+#pragma unroll
+  for (int b = 0; b < kFrameChunk; ++b) Iv[b] = b < nk ? __ldg(sc.frames + t_off[b] + p) : 0.f;
   unsigned long long dropped = 0;
-  for (int64_t k = k_lo; k < k_hi; ++k) {
-    const int64_t f = sc.good[k];
-    const double x = u0 - __ldg(di + f) - static_cast<double>(n0);   // recon.py:138
-    const double y = u1 - __ldg(dj + f) - static_cast<double>(m0);
+#pragma unroll
+  for (int b = 0; b < kFrameChunk; ++b) {
+    if (b >= nk) break;
+    const double x = u0 - t_di[b] - static_cast<double>(n0);       // recon.py:138
+    const double y = u1 - t_dj[b] - static_cast<double>(m0);
     if (!(x >= 0.0 && x <= static_cast<double>(os - 1) && y >= 0.0 &&
           y <= static_cast<double>(of - 1))) {   // interp.py:103-107
       ++dropped;
       continue;
     }
     const Split sx = split(x), sy = split(y);
-    const double I = static_cast<double>(__ldg(sc.frames + f * plane + p));
+    const double I = static_cast<double>(Iv[b]);
     const double vw = (I / w) * w2;              // value * weight (interp.py:112)
     const int r0 = sx.i, c0 = sy.i;
     const int r1 = min(r0 + 1, static_cast<int>(os - 1));

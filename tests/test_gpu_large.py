@@ -75,10 +75,7 @@ def test_cfg3_translation_subset_vs_oracle():
     cfg = s.cfg
     di_o, dj_o = ds.translation_search(ref, u, di, dj, cfg.t_half_ss, cfg.t_half_fs)
     pick = [0, 777, 1999]
-    good = np.zeros(s.scan.n_frames, bool)
-    good[pick] = True
-    fr = frames.cpu().numpy() if False else None   # full stack not needed on host
-    sub = np.ascontiguousarray(frames[pick].cpu().numpy())
+    sub = np.ascontiguousarray(frames[pick].cpu().numpy())     # only these frames on host
     sub_good = np.ones(len(pick), bool)
     d_o, j_o, errs = orc.update_translations(sub, sub_good, s.w.w, s.m.mask,
                                              ref.i_ref.cpu().numpy(), ref.wsum.cpu().numpy(),
