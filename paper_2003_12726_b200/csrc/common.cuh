@@ -151,6 +151,43 @@ __device__ __forceinline__ bool masked_read(const float* __restrict__ fm,
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Grouped bilinear splat.  A cell group g(r, c) is a float4 holding
+// (num, den) of cell (r, c) and (num, den) of cell (r+1, c); one sample adds
+// its four corners with two 16-byte `red.global.add.v4.f32` into g(r0, c0)
+// and g(r0, c1).  Corners the reference clips (interp.py:44-45: r1 = r0 at the
+// last row) always carry zero weight (an inside point on the last row has
+// fx = 0), so the grouping is exact.  Groups accumulate in float32 per frame
+// chunk image; k_group_fold sums the images in float64 in a fixed order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_v4(float4* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// value*w_c and weight*w_c at the four corners of cell index `cell` =
+// r0*of + c0 with fractions (fx, fy).
+__device__ __forceinline__ void splat_grouped(float4* img, int64_t cell, double fx, double fy,
+                                              double value_w, double weight) {
+  const double gx = 1.0 - fx, gy = 1.0 - fy;
+  const double w00 = gx * gy, w01 = gx * fy, w10 = fx * gy, w11 = fx * fy;
+  float4* g0 = img + cell;
+  red_v4(g0, static_cast<float>(value_w * w00), static_cast<float>(weight * w00),
+         static_cast<float>(value_w * w10), static_cast<float>(weight * w10));
+  if (fy > 0.0)
+    red_v4(g0 + 1, static_cast<float>(value_w * w01), static_cast<float>(weight * w01),
+           static_cast<float>(value_w * w11), static_cast<float>(weight * w11));
+}
+
+// Host: fold n_img grouped images [n_img][os*of] (float4) into float64
+// num/den [os*of] (added to their contents).
+int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* num, double* den,
+                cudaStream_t s);
+// Number of grouped images for `blocks` frame blocks over n_cells cells;
+// returns frame blocks per image.
+int64_t chunk_images(int64_t blocks, int64_t n_cells, int* n_img);
+
 // Float64 variant for the memory-bound error maps (K4), reading a float64
 // masked image: matches the reference's float64 residuals to ~1e-15.
 __device__ __forceinline__ bool masked_read64(const double* __restrict__ fm,

@@ -5,8 +5,8 @@
 // pixels (deterministic: per-CTA partials, fixed-order final sum), total =
 // sum of per_frame, reference_plane = normalise(splat(eps, weight 1)) where
 // every sample is splatted, invalid ones included, out-of-grid
-// points dropped (interp.py:103-107).  The splat accumulates in float64 with
-// RED.ADD.F64 like K1.
+// points dropped (interp.py:103-107).  The splat goes through float32
+// grouped chunk images and a float64 fold like K1 (splat.cu header).
 #include "common.cuh"
 
 namespace pxst {
@@ -19,7 +19,7 @@ namespace {
 
 constexpr int kTR = 8, kTC = 32, kThreads = kTR * kTC;
 constexpr int kFB = 8;  // frames per reduction batch
-constexpr int kLB = 4;  // frames per load batch (loads issued before the batch's REDs)
+constexpr int kLB = 2;  // frames per load batch (loads issued before the batch's REDs)
 
 struct ErrArgs {
   pxst_scan sc;
@@ -31,8 +31,8 @@ struct ErrArgs {
   int64_t os, of, n0, m0;
   const double* fm64;  // nullable float64 image
   const double* sigma2;
-  double* num;   // reference-plane accumulators [os*of]
-  double* den;
+  float4* img;   // grouped reference-plane images [n_img][os*of]
+  int bpi;       // reduction batches (kFB frames) per image
 };
 
 // Per-pixel sums, per-(frame, CTA) partials, reference-plane splat.
@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_err_pass(ErrArgs a, double* per
       t_off[threadIdx.x] = f * plane;
     }
     __syncthreads();   // also orders the previous batch's red[] reads before reuse
+    float4* img = a.img + (int64_t)((k0 / kFB) / a.bpi) * a.os * a.of;
     double e[kFB];
 #pragma unroll
     for (int h = 0; h < kFB; h += kLB) {
@@ -120,15 +121,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_err_pass(ErrArgs a, double* per
       const double eps = (r * r) / s2;                // recon.py:422
       e[h + b] = eps;
       pix += eps;
-      if (inb[b]) {                                   // recon.py:425
-        const int64_t cell[4] = {a00[b], a00[b] + dc[b], a00[b] + dr[b],
-                                 a00[b] + dr[b] + dc[b]};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          atomicAdd(a.num + cell[q], eps * cw[q]);
-          atomicAdd(a.den + cell[q], cw[q]);
-        }
-      }
+      if (inb[b])                                     // recon.py:425
+        splat_grouped(img, a00[b], fx, fy, eps, 1.0);
     }
     }
 #pragma unroll
@@ -207,10 +201,16 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
   const int64_t n_ctas = (int64_t)g.x * g.y;
   Scratch part;
   if (int e = part.alloc(sizeof(double) * (n_ctas + 1) * sc->n_good, s)) return e;
+  const int64_t n_o = ref->os * ref->of;
+  int n_img;
+  const int64_t bpi = chunk_images((sc->n_good + kFB - 1) / kFB, n_o, &n_img);
+  Scratch img;
+  if (int e = img.alloc(sizeof(float4) * n_o * n_img, s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(img.p, 0, sizeof(float4) * n_o * n_img, s));
   double* ftmp = part.as<double>() + n_ctas * sc->n_good;
   ErrArgs a{*sc,        u,          di,          dj,      ref->fm,
             ref->valid, ref->os,    ref->of,     ref->n0, ref->m0,
-            ref->fm64,  st->sigma2, num,         den};
+            ref->fm64,  st->sigma2, img.as<float4>(), (int)bpi};
   k_err_pass<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
   PXST_CHECK_LAUNCH();
   k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_ctas, per_frame,
@@ -220,7 +220,7 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
     k_err_total<<<1, 1024, 0, s>>>(ftmp, sc->n_good, total);
     PXST_CHECK_LAUNCH();
   }
-  return PXST_OK;
+  return fold_groups(img.as<float4>(), n_img, ref->os, ref->of, num, den, s);
 }
 
 int check_err_args(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref) {

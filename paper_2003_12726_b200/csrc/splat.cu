@@ -2,12 +2,13 @@
 // (interp.py:53-135).
 //
 // The reference accumulates the bilinear splat in float64 with np.bincount
-// (interp.py:114-122).  Here every corner contribution is added in float64
-// with the native RED.ADD.F64 (same throughput as 64-bit integer REDs on
-// B200, measured 187-522 G/s).  Float64 keeps full relative precision even
-// on cells that only receive a corner tail of weight ~1e-9 (an int64
-// fixed-point variant lost 1e-3 there); the price is that the summation
-// order, hence the last ulp, varies run to run.
+// (interp.py:114-122).  The splat is bound by the L2 atomic units, so here a
+// sample's four corners go out as two 16-byte float32 REDs (splat_grouped:
+// 2 RED lane-ops per sample instead of 8 float64 ones) into at most 32
+// float32 images, each covering a contiguous range of frame chunks; a fixed
+// order float64 fold sums the images.  Each float32 sum holds <= N/32 frames
+// of positive terms, so its relative error stays ~1e-7 (the 1e-5 bar of
+// SURVEY 8(c)); the summation order inside an image varies run to run.
 #include "common.cuh"
 
 namespace pxst {
@@ -15,15 +16,19 @@ namespace {
 
 constexpr int kTC = 128;        // threads per block along fs
 constexpr int kFrameChunk = 16; // frames per block (grid.z)
+constexpr int64_t kMaxImages = 32;             // float32 chunk images per splat
+constexpr int64_t kImageBytes = int64_t(1) << 30;
 
 // One thread per work pixel, looping over a chunk of good frames.  Lanes of
 // a warp are consecutive fs pixels, so the corner REDs of a warp land on a
-// few consecutive cells (the cheap, row-coalesced atomic pattern).
+// few consecutive cells (the cheap, row-coalesced atomic pattern).  Each
+// sample issues two 16-byte float32 REDs (splat_grouped) into the chunk image
+// blockIdx.z / blocks_per_img.
 __global__ void __launch_bounds__(kTC)
 k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
                const double* __restrict__ dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-               int64_t frame_lo, int64_t frame_hi, double* __restrict__ num,
-               double* __restrict__ den, unsigned long long* __restrict__ n_drop) {
+               int64_t frame_lo, int64_t frame_hi, float4* __restrict__ img, int blocks_per_img,
+               unsigned long long* __restrict__ n_drop) {
   // Per-frame scalars of the chunk staged once per block; every stack value
   // of the chunk is loaded before the first RED, so the loads are one round
   // trip instead of one per frame (REDs pin the program order of later loads).
@@ -45,6 +50,7 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
   if (c >= sc.roi[3]) return;
   const int64_t p = r * sc.fs + c;
   if (!sc.work[p]) return;
+  float4* out = img + (int64_t)(blockIdx.z / blocks_per_img) * os * of;
   const double u0 = u[p], u1 = u[plane + p];
   const double w = sc.w64[p];
   const double w2 = w * w;                       // recon.py:136
@@ -65,20 +71,33 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
     const Split sx = split(x), sy = split(y);
     const double I = static_cast<double>(Iv[b]);
     const double vw = (I / w) * w2;              // value * weight (interp.py:112)
-    const int r0 = sx.i, c0 = sy.i;
-    const int r1 = min(r0 + 1, static_cast<int>(os - 1));
-    const int c1 = min(c0 + 1, static_cast<int>(of - 1));
-    const double gx = 1.0 - sx.f, gy = 1.0 - sy.f;
-    const double cw[4] = {gx * gy, gx * sy.f, sx.f * gy, sx.f * sy.f};
-    const int64_t cell[4] = {(int64_t)r0 * of + c0, (int64_t)r0 * of + c1,
-                             (int64_t)r1 * of + c0, (int64_t)r1 * of + c1};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      atomicAdd(num + cell[q], vw * cw[q]);
-      atomicAdd(den + cell[q], w2 * cw[q]);
-    }
+    splat_grouped(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2);
   }
   if (n_drop && dropped) atomicAdd(n_drop, dropped);
+}
+
+// Fold grouped float32 chunk images into float64 (num, den), fixed order:
+// cell (r, c) = sum_z g_z(r, c).lo + g_z(r-1, c).hi.
+__global__ void k_group_fold(const float4* __restrict__ img, int n_img, int64_t os, int64_t of,
+                             double* __restrict__ num, double* __restrict__ den) {
+  const int64_t n = os * of;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0, b = 0.0;
+    const bool up = q >= of;
+    for (int z = 0; z < n_img; ++z) {
+      const float4 g = __ldg(img + (int64_t)z * n + q);
+      a += g.x;
+      b += g.y;
+      if (up) {
+        const float4 h = __ldg(img + (int64_t)z * n + q - of);
+        a += h.z;
+        b += h.w;
+      }
+    }
+    num[q] += a;
+    den[q] += b;
+  }
 }
 
 // Normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0.
@@ -157,6 +176,25 @@ int grid_1d(int64_t n, int threads) {
 
 int check_scan(const pxst_scan* sc);
 
+int64_t chunk_images(int64_t blocks, int64_t n_cells, int* n_img) {
+  // <= kMaxImages float32 images (bounds each image's sum to blocks/kMaxImages
+  // frame blocks) and <= kImageBytes of scratch.
+  int64_t cap = kImageBytes / (static_cast<int64_t>(sizeof(float4)) * (n_cells > 0 ? n_cells : 1));
+  if (cap > kMaxImages) cap = kMaxImages;
+  if (cap < 1) cap = 1;
+  const int64_t want = blocks < cap ? blocks : cap;
+  const int64_t bpi = (blocks + want - 1) / want;
+  *n_img = static_cast<int>((blocks + bpi - 1) / bpi);
+  return bpi;
+}
+
+int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* num, double* den,
+                cudaStream_t s) {
+  k_group_fold<<<grid_1d(os * of, 256), 256, 0, s>>>(img, n_img, os, of, num, den);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
 int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
                         const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
                         int64_t frame_lo, int64_t frame_hi, double* num, double* den,
@@ -165,12 +203,18 @@ int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
   if (nk <= 0) return PXST_OK;
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
   PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
-  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)rw,
-         (unsigned)((nk + kFrameChunk - 1) / kFrameChunk));
-  k_object_splat<<<g, kTC, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, num,
-                                   den, n_drop);
+  const int64_t blocks = (nk + kFrameChunk - 1) / kFrameChunk;
+  const int64_t n = os * of;
+  int n_img;
+  const int64_t bpi = chunk_images(blocks, n, &n_img);
+  Scratch acc;
+  if (int e = acc.alloc(sizeof(float4) * n * n_img, s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(float4) * n * n_img, s));
+  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)rw, (unsigned)blocks);
+  k_object_splat<<<g, kTC, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi,
+                                   acc.as<float4>(), (int)bpi, n_drop);
   PXST_CHECK_LAUNCH();
-  return PXST_OK;
+  return fold_groups(acc.as<float4>(), n_img, os, of, num, den, s);
 }
 
 int launch_object_finish(const double* num, const double* den, int64_t n, double* i_ref,

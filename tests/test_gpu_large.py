@@ -98,7 +98,7 @@ def test_cfg3_full_size_properties():
     ref2 = ds.object_finish(acc, (n0, m0), shape)
     ok = ref.valid.bool()
     rel = ((ref2.i_ref - ref.i_ref).abs()[ok] / ref.i_ref.abs()[ok]).max().item()
-    assert rel < 1e-12
+    assert rel < 1e-5                      # float32 chunk images (splat.cu header)
     # the pixel-map search is deterministic (no atomics in K2)
     u1, e1 = ds.pixel_map_search(ref, u, di, dj, cfg.half_ss, cfg.half_fs)
     u2, e2 = ds.pixel_map_search(ref, u, di, dj, cfg.half_ss, cfg.half_fs)

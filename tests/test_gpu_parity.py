@@ -46,7 +46,7 @@ def assert_object_map(ref, i_ref, wsum, origin):
     assert rel.max() < OBJ_RTOL, rel.max()
     np.testing.assert_array_equal(ref.i_ref[~ok], 0.0)
     relw = np.abs(ref.wsum[ok] - wsum[ok]) / wsum[ok]
-    assert relw.max() < 1e-9, relw.max()
+    assert relw.max() < OBJ_RTOL, relw.max()
 
 
 def unique_pixels(stack):
@@ -100,8 +100,9 @@ def test_cfg0_object_map(scan0, golden0):
     ref = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
     assert_object_map(ref, golden0["ref_i"], golden0["ref_w"], golden0["ref_origin"])
     ref2 = pb.make_object_map(s.scan, s.w, s.m, s.u0, s.t0)
-    np.testing.assert_allclose(ref.i_ref, ref2.i_ref, rtol=1e-13)   # f64 atomics: ulp-level
-    np.testing.assert_allclose(ref.wsum, ref2.wsum, rtol=1e-13)
+    # float32 chunk images, unordered REDs: run-to-run differences ~1e-7
+    np.testing.assert_allclose(ref.i_ref, ref2.i_ref, rtol=OBJ_RTOL)
+    np.testing.assert_allclose(ref.wsum, ref2.wsum, rtol=OBJ_RTOL)
 
 
 @pytest.mark.parametrize("refine", [True, False])
@@ -164,7 +165,8 @@ def test_cfg0_error_maps(scan0, golden0):
     np.testing.assert_allclose(M.per_frame, g["ce_per_frame"], rtol=1e-10)
     np.testing.assert_allclose(M.per_pixel, g["ce_per_pixel"], rtol=1e-10, atol=1e-14)
     np.testing.assert_allclose(M.variance, g["ce_var"], rtol=1e-12)
-    np.testing.assert_allclose(M.reference_plane, g["ce_plane"], rtol=1e-9, atol=1e-15)
+    # reference plane: float32 grouped chunk images + float64 fold (error.cu header)
+    np.testing.assert_allclose(M.reference_plane, g["ce_plane"], rtol=1e-5, atol=1e-12)
 
 
 def test_cfg0_main_loop(scan0, golden0):

@@ -49,13 +49,14 @@ def test_band_views_compose(scan0):
     np.testing.assert_allclose(pf.cpu().numpy(), per_frame.cpu().numpy(), rtol=1e-10)
     np.testing.assert_allclose(pp.cpu().numpy(), per_pixel.cpu().numpy(), rtol=1e-12)
     np.testing.assert_allclose(ex.error_finish(num, den, ref).cpu().numpy(),
-                               plane.cpu().numpy(), rtol=1e-9, atol=1e-14)
+                               plane.cpu().numpy(), rtol=1e-5, atol=1e-12)
     # frame-range splats compose to the full object map
     n0, m0, shape = ds.bbox(u, di, dj)
     acc = ds.object_splat(u, di, dj, n0, m0, shape, 0, 10)
     acc += ds.object_splat(u, di, dj, n0, m0, shape, 10, ds.n_good)
     ref2 = ds.object_finish(acc, (n0, m0), shape)
-    np.testing.assert_allclose(ref2.i_ref.cpu().numpy(), ref.i_ref.cpu().numpy(), rtol=1e-12)
+    # float32 chunk images (splat.cu header): agreement to ~1e-7
+    np.testing.assert_allclose(ref2.i_ref.cpu().numpy(), ref.i_ref.cpu().numpy(), rtol=1e-5)
 
 
 def test_one_rank_nccl_iteration(scan0):
