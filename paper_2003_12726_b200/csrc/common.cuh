@@ -71,6 +71,14 @@ struct Scratch {
 
 constexpr int kMaxGridY = 65535;
 
+// Blocks for a grid-stride loop over n items.
+inline int grid_1d(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return static_cast<int>(b);
+}
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------

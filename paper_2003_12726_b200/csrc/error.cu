@@ -17,32 +17,81 @@ int launch_object_finish(const double* num, const double* den, int64_t n, double
 
 namespace {
 
-constexpr int kTR = 8, kTC = 32, kThreads = kTR * kTC;
-constexpr int kFB = 8;  // frames per reduction batch
-constexpr int kLB = 2;  // frames per load batch (loads issued before the batch's REDs)
+constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC, kWarps = kThreads / 32;
+constexpr int kFB = 8;    // frames per reduction batch
+constexpr int kLB = 2;    // frames per load batch (loads issued before the batch's REDs)
+constexpr int kTab = 256; // frames per shared-memory frame table chunk
+#ifndef PXST_K4_OCC
+#define PXST_K4_OCC 6   // resident CTAs per SM (80 registers; 4 measured slower)
+#endif
 
 struct ErrArgs {
   pxst_scan sc;
   const double* u;
   const double* di;
   const double* dj;
-  const float* fm;
-  const uint8_t* valid;
+  const double2* grp;  // grouped reference (k_group_ref), NaN = invalid cell
   int64_t os, of, n0, m0;
-  const double* fm64;  // nullable float64 image
   const double* sigma2;
-  float4* img;   // grouped reference-plane images [n_img][os*of]
-  int bpi;       // reduction batches (kFB frames) per image
+  float4* img;         // grouped reference-plane images [n_img][os*of]
+  int bpi;             // reduction batches (kFB frames) per image
+  int64_t frames_per_z;
 };
 
-// Per-pixel sums, per-(frame, CTA) partials, reference-plane splat.
-__global__ void __launch_bounds__(kThreads, 2) k_err_pass(ErrArgs a, double* per_pixel,
-                                                       double* part, int64_t n_ctas) {
-  __shared__ double red[kThreads / 32][kFB];
+// g[r][c] = (v(r, c), v(r+1, c)) with v = the float64 masked reference where
+// valid and NaN elsewhere (and past the last row): one 16-byte load fetches a
+// bilinear column pair, and the NaN doubles as the validity bit.
+__global__ void k_group_ref(const double* __restrict__ fm64, const float* __restrict__ fm,
+                            const uint8_t* __restrict__ valid, int64_t os, int64_t of,
+                            double2* __restrict__ g) {
+  const int64_t n = os * of;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    auto v = [&](int64_t i) {
+      return valid[i] ? (fm64 ? fm64[i] : static_cast<double>(fm[i])) : nan;
+    };
+    g[q] = make_double2(v(q), q + of < n ? v(q + of) : nan);
+  }
+}
+
+// Fixed-order butterfly all-reduce of 8 values over a warp: afterwards lane l
+// holds the warp sum of value index ((l>>4)&1)*4 + ((l>>3)&1)*2 + ((l>>2)&1)
+// (9 float64 shuffles instead of 40).
+__device__ __forceinline__ double warp_sum8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const bool hi = lane & 16;
+    const double send = hi ? v[j] : v[j + 4], keep = hi ? v[j + 4] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const bool hi = lane & 8;
+    const double send = hi ? v[j] : v[j + 2], keep = hi ? v[j + 2] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const double send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+// One thread per work pixel over the frame slice blockIdx.z: per-pixel slice
+// sums, per-(frame, warp) partials, reference-plane splat.  No barrier inside
+// the frame loop (the frame table is refreshed every kTab frames).
+__global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, double* pix_part,
+                                                       double* part, int64_t n_warps) {
+  __shared__ double t_di[kTab], t_dj[kTab];
+  __shared__ int64_t t_off[kTab];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
   const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kTC + lane;
-  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t gwarp = ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kWarps + warp;
   const bool inroi = row < a.sc.roi[1] && col < a.sc.roi[3];
   const int64_t p = inroi ? row * a.sc.fs + col : 0;
   const bool live = inroi && a.sc.work[p] != 0;
@@ -51,103 +100,103 @@ __global__ void __launch_bounds__(kThreads, 2) k_err_pass(ErrArgs a, double* per
   const double W64 = live ? a.sc.w64[p] : 0.0;
   const double s2 = live ? a.sigma2[p] : 1.0;
   const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
-  __shared__ double t_di[kFB], t_dj[kFB];
-  __shared__ int64_t t_off[kFB];
+  const int64_t n_o = a.os * a.of;
+  const int64_t k_begin = (int64_t)blockIdx.z * a.frames_per_z;
+  const int64_t k_end = min(a.sc.n_good, k_begin + a.frames_per_z);
   double pix = 0.0;
-  for (int64_t k0 = 0; k0 < a.sc.n_good; k0 += kFB) {
-    if (threadIdx.x < kFB && k0 + threadIdx.x < a.sc.n_good) {
-      const int64_t f = a.sc.good[k0 + threadIdx.x];
-      t_di[threadIdx.x] = a.di[f];
-      t_dj[threadIdx.x] = a.dj[f];
-      t_off[threadIdx.x] = f * plane;
-    }
-    __syncthreads();   // also orders the previous batch's red[] reads before reuse
-    float4* img = a.img + (int64_t)((k0 / kFB) / a.bpi) * a.os * a.of;
-    double e[kFB];
-#pragma unroll
-    for (int h = 0; h < kFB; h += kLB) {
-    // Phase A: every load of the sub-batch is issued before any RED of it
-    // (REDs pin the program order of later loads).
-    float Iv[kLB];
-    bool inb[kLB];
-    double fxb[kLB], fyb[kLB];
-    int64_t a00[kLB];
-    int dc[kLB], dr[kLB];               // corner offsets (clipped at the grid edge)
-    double v4[kLB][4];
-    uint8_t m4[kLB][4];
-#pragma unroll
-    for (int b = 0; b < kLB; ++b) {
-      const int64_t k = k0 + h + b;
-      const bool act = live && k < a.sc.n_good;
-      const double x = u0 - t_di[h + b] - static_cast<double>(a.n0);   // recon.py:418
-      const double y = u1 - t_dj[h + b] - static_cast<double>(a.m0);
-      inb[b] = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
-      Iv[b] = act ? __ldg(a.sc.frames + t_off[h + b] + p) : 0.f;
-      const Split sx = split(inb[b] ? x : 0.0), sy = split(inb[b] ? y : 0.0);
-      fxb[b] = sx.f;
-      fyb[b] = sy.f;
-      dr[b] = sx.i + 1 < a.os ? static_cast<int>(a.of) : 0;
-      dc[b] = sy.i + 1 < a.of ? 1 : 0;
-      a00[b] = (int64_t)sx.i * a.of + sy.i;
-      const int64_t ad[4] = {a00[b], a00[b] + dc[b], a00[b] + dr[b], a00[b] + dr[b] + dc[b]};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        m4[b][q] = inb[b] ? __ldg(a.valid + ad[q]) : 0;
-        // fm / fm64 are 0 on invalid cells (where(m, f, 0), interp.py:64)
-        v4[b][q] = !inb[b] ? 0.0 : (a.fm64 ? __ldg(a.fm64 + ad[q])
-                                           : static_cast<double>(__ldg(a.fm + ad[q])));
-      }
-    }
-    // Phase B: residuals, sums, reference-plane splat.
-#pragma unroll
-    for (int b = 0; b < kLB; ++b) {
-      e[h + b] = 0.0;
-      const int64_t k = k0 + h + b;
-      if (!(live && k < a.sc.n_good)) continue;
-      const double fx = fxb[b], fy = fyb[b], gx = 1.0 - fx, gy = 1.0 - fy;
-      const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};
-      bool ok = false;
-      double v = 0.0;
-      if (inb[b]) {                                   // interp.py:70-84
-        const double den = cw[0] * m4[b][0] + cw[1] * m4[b][1] + cw[2] * m4[b][2] +
-                           cw[3] * m4[b][3];
-        const double nm = cw[0] * v4[b][0] + cw[1] * v4[b][1] + cw[2] * v4[b][2] +
-                          cw[3] * v4[b][3];
-        ok = den > 0.0;
-        v = ok ? nm / den : 0.0;
-      }
-      const double I = static_cast<double>(Iv[b]);
-      const double r = ok ? I - W64 * v : I - W64;  // recon.py:421
-      const double eps = (r * r) / s2;                // recon.py:422
-      e[h + b] = eps;
-      pix += eps;
-      if (inb[b])                                     // recon.py:425
-        splat_grouped(img, a00[b], fx, fy, eps, 1.0);
-    }
-    }
-#pragma unroll
-    for (int b = 0; b < kFB; ++b) {
-      const double v = warp_sum(e[b]);
-      if (lane == 0) red[warp][b] = v;
+  for (int64_t kc = k_begin; kc < k_end; kc += kTab) {
+    const int nt = static_cast<int>(k_end - kc < kTab ? k_end - kc : kTab);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += kThreads) {
+      const int64_t f = a.sc.good[kc + t];
+      t_di[t] = a.di[f];
+      t_dj[t] = a.dj[f];
+      t_off[t] = f * plane;
     }
     __syncthreads();
-    if (threadIdx.x < kFB && k0 + threadIdx.x < a.sc.n_good) {
-      double s = 0.0;
+    for (int b0 = 0; b0 < nt; b0 += kFB) {
+      float4* img = a.img + ((kc + b0) / kFB / a.bpi) * n_o;
+      double e[kFB];
 #pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) s += red[w][threadIdx.x];
-      part[(k0 + threadIdx.x) * n_ctas + cta] = s;
+      for (int h = 0; h < kFB; h += kLB) {
+        // Phase A: every load of the sub-batch is issued before any RED of it.
+        float Iv[kLB];
+        bool inb[kLB];
+        double fxb[kLB], fyb[kLB];
+        int64_t a00[kLB];
+        double2 g0[kLB], g1[kLB];
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+          const int t = b0 + h + b;
+          const bool act = live && t < nt;
+          const double x = u0 - t_di[t] - static_cast<double>(a.n0);   // recon.py:418
+          const double y = u1 - t_dj[t] - static_cast<double>(a.m0);
+          inb[b] = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;
+          Iv[b] = act ? __ldg(a.sc.frames + t_off[t] + p) : 0.f;
+          const Split sx = split(inb[b] ? x : 0.0), sy = split(inb[b] ? y : 0.0);
+          fxb[b] = sx.f;
+          fyb[b] = sy.f;
+          a00[b] = (int64_t)sx.i * a.of + sy.i;
+          const double2 z2 = make_double2(0.0, 0.0);
+          g0[b] = inb[b] ? __ldg(a.grp + a00[b]) : z2;
+          // fy == 0 <=> the reference's clipped column (interp.py:44-45), weight 0
+          g1[b] = inb[b] && sy.f > 0.0 ? __ldg(a.grp + a00[b] + 1) : z2;
+        }
+        // Phase B: residuals, sums, reference-plane splat.
+#pragma unroll
+        for (int b = 0; b < kLB; ++b) {
+          const double fx = fxb[b], fy = fyb[b], gx = 1.0 - fx, gy = 1.0 - fy;
+          const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};
+          // corners 00, 01, 10, 11 (interp.py:70-84 order)
+          const double cv[4] = {g0[b].x, g1[b].x, g0[b].y, g1[b].y};
+          double den = 0.0, nm = 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool m = cv[q] == cv[q];           // NaN = invalid cell
+            den += m ? cw[q] : 0.0;
+            nm += m ? cw[q] * cv[q] : 0.0;
+          }
+          const bool ok = inb[b] && den > 0.0;
+          const double v = ok ? nm / den : 0.0;
+          const double I = static_cast<double>(Iv[b]);
+          const double r = ok ? I - W64 * v : I - W64;  // recon.py:421
+          const double eps = (live && b0 + h + b < nt) ? (r * r) / s2 : 0.0;   // recon.py:422
+          e[h + b] = eps;
+          pix += eps;
+          if (inb[b])                                   // recon.py:425
+            splat_grouped(img, a00[b], fx, fy, eps, 1.0);
+        }
+      }
+      const double sum = warp_sum8(e, lane);
+      const int idx = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      if ((lane & 3) == 0 && b0 + idx < nt) part[(kc + b0 + idx) * n_warps + gwarp] = sum;
     }
   }
-  if (live) per_pixel[p] = pix;
+  if (live) pix_part[(int64_t)blockIdx.z * plane + p] = pix;
 }
 
-// per_frame[good[k]] = sum over CTAs in a fixed order (one block per frame).
-__global__ void k_err_frames(pxst_scan sc, const double* __restrict__ part, int64_t n_ctas,
+// per_pixel[p] = sum over frame slices (fixed order) on work pixels.
+__global__ void k_err_pixels(pxst_scan sc, const double* __restrict__ pix_part, int n_z,
+                             double* per_pixel) {
+  const int64_t cw = sc.roi[3] - sc.roi[2], n = (sc.roi[1] - sc.roi[0]) * cw;
+  const int64_t plane = sc.ss * sc.fs;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = (sc.roi[0] + q / cw) * sc.fs + sc.roi[2] + q % cw;
+    if (!sc.work[p]) continue;
+    double t = 0.0;
+    for (int z = 0; z < n_z; ++z) t += pix_part[z * plane + p];
+    per_pixel[p] = t;
+  }
+}
+
+// per_frame[good[k]] = sum over warps in a fixed order (one block per frame).
+__global__ void k_err_frames(pxst_scan sc, const double* __restrict__ part, int64_t n_warps,
                              double* per_frame, double* frame_tmp) {
   __shared__ double sh[32];
   const int64_t k = blockIdx.x;
   double s = 0.0;
-  for (int64_t c = threadIdx.x; c < n_ctas; c += blockDim.x) s += part[k * n_ctas + c];
+  for (int64_t c = threadIdx.x; c < n_warps; c += blockDim.x) s += part[k * n_warps + c];
   s = warp_sum(s);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) sh[warp] = s;
@@ -198,22 +247,42 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
   dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)((rw + kTR - 1) / kTR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
-  const int64_t n_ctas = (int64_t)g.x * g.y;
+  const int64_t n_warps = (int64_t)g.x * g.y * kWarps;
+  // Frame slices (grid.z): enough threads for ~3 waves of resident CTAs when
+  // the ROI alone cannot fill the GPU (config 1: 131k pixels).
+  int dev = 0, sms = 148, per_sm = 1;
+  PXST_CHECK_CUDA(cudaGetDevice(&dev));
+  PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PXST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_err_pass, kThreads, 0));
+  const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t n_batches = (sc->n_good + kFB - 1) / kFB;
+  int64_t n_z = (3 * resident + (int64_t)g.x * g.y - 1) / ((int64_t)g.x * g.y);
+  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
+  const int64_t fpz = ((n_batches + n_z - 1) / n_z) * kFB;
+  n_z = (sc->n_good + fpz - 1) / fpz;
+  g.z = static_cast<unsigned>(n_z);
   Scratch part;
-  if (int e = part.alloc(sizeof(double) * (n_ctas + 1) * sc->n_good, s)) return e;
+  if (int e = part.alloc(sizeof(double) * ((n_warps + 1) * sc->n_good + n_z * plane), s)) return e;
+  double* ftmp = part.as<double>() + n_warps * sc->n_good;
+  double* pix_part = ftmp + sc->n_good;
   const int64_t n_o = ref->os * ref->of;
   int n_img;
-  const int64_t bpi = chunk_images((sc->n_good + kFB - 1) / kFB, n_o, &n_img);
-  Scratch img;
+  const int64_t bpi = chunk_images(n_batches, n_o, &n_img);
+  Scratch img, grp;
   if (int e = img.alloc(sizeof(float4) * n_o * n_img, s)) return e;
+  if (int e = grp.alloc(sizeof(double2) * n_o, s)) return e;
   PXST_CHECK_CUDA(cudaMemsetAsync(img.p, 0, sizeof(float4) * n_o * n_img, s));
-  double* ftmp = part.as<double>() + n_ctas * sc->n_good;
-  ErrArgs a{*sc,        u,          di,          dj,      ref->fm,
-            ref->valid, ref->os,    ref->of,     ref->n0, ref->m0,
-            ref->fm64,  st->sigma2, img.as<float4>(), (int)bpi};
-  k_err_pass<<<g, kThreads, 0, s>>>(a, per_pixel, part.as<double>(), n_ctas);
+  k_group_ref<<<grid_1d(n_o, 256), 256, 0, s>>>(ref->fm64, ref->fm, ref->valid, ref->os, ref->of,
+                                                grp.as<double2>());
   PXST_CHECK_LAUNCH();
-  k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_ctas, per_frame,
+  ErrArgs a{*sc,     u,       di,         dj,
+            grp.as<double2>(), ref->os, ref->of, ref->n0,
+            ref->m0, st->sigma2, img.as<float4>(), (int)bpi, fpz};
+  k_err_pass<<<g, kThreads, 0, s>>>(a, pix_part, part.as<double>(), n_warps);
+  PXST_CHECK_LAUNCH();
+  k_err_pixels<<<grid_1d(rw * cw, 256), 256, 0, s>>>(*sc, pix_part, (int)n_z, per_pixel);
+  PXST_CHECK_LAUNCH();
+  k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_warps, per_frame,
                                                     ftmp);
   PXST_CHECK_LAUNCH();
   if (total) {

@@ -14,64 +14,72 @@
 namespace pxst {
 namespace {
 
-constexpr int kTC = 128;        // threads per block along fs
-constexpr int kFrameChunk = 16; // frames per block (grid.z)
-constexpr int64_t kMaxImages = 32;             // float32 chunk images per splat
+constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;  // 4 rows x 32 fs pixels
+constexpr int kFB = 8;                 // frames per load batch (loads before REDs)
+constexpr int kTab = 256;              // frames per shared-memory frame table chunk
+constexpr int64_t kMaxImages = 32;     // float32 chunk images per splat
 constexpr int64_t kImageBytes = int64_t(1) << 30;
+#ifndef PXST_K1_OCC
+#define PXST_K1_OCC 8
+#endif
 
-// One thread per work pixel, looping over a chunk of good frames.  Lanes of
-// a warp are consecutive fs pixels, so the corner REDs of a warp land on a
-// few consecutive cells (the cheap, row-coalesced atomic pattern).  Each
-// sample issues two 16-byte float32 REDs (splat_grouped) into the chunk image
-// blockIdx.z / blocks_per_img.
-__global__ void __launch_bounds__(kTC)
+// One thread per work pixel over the frame slice blockIdx.z.  Lanes of a
+// warp are consecutive fs pixels, so the corner REDs of a warp land on a few
+// consecutive cells (the cheap, row-coalesced atomic pattern).  Each sample
+// issues two 16-byte float32 REDs (splat_grouped) into the chunk image of
+// its frame batch; a batch's frame loads are all issued before its REDs.
+__global__ void __launch_bounds__(kThreads, PXST_K1_OCC)
 k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
                const double* __restrict__ dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-               int64_t frame_lo, int64_t frame_hi, float4* __restrict__ img, int blocks_per_img,
-               unsigned long long* __restrict__ n_drop) {
-  // Per-frame scalars of the chunk staged once per block; every stack value
-  // of the chunk is loaded before the first RED, so the loads are one round
-  // trip instead of one per frame (REDs pin the program order of later loads).
-  __shared__ double t_di[kFrameChunk], t_dj[kFrameChunk];
-  __shared__ int64_t t_off[kFrameChunk];
-  const int64_t c = sc.roi[2] + blockIdx.x * (int64_t)kTC + threadIdx.x;
-  const int64_t r = sc.roi[0] + blockIdx.y;
-  const int64_t k_lo = frame_lo + (int64_t)blockIdx.z * kFrameChunk;
-  const int64_t k_hi = min(frame_hi, k_lo + kFrameChunk);
-  const int nk = static_cast<int>(k_hi - k_lo);
+               int64_t frame_lo, int64_t frame_hi, int64_t frames_per_z, float4* __restrict__ img,
+               int bpi, unsigned long long* __restrict__ n_drop) {
+  __shared__ double t_di[kTab], t_dj[kTab];
+  __shared__ int64_t t_off[kTab];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
+  const int64_t c = sc.roi[2] + (int64_t)blockIdx.x * kTC + lane;
+  const bool inroi = r < sc.roi[1] && c < sc.roi[3];
+  const int64_t p = inroi ? r * sc.fs + c : 0;
+  const bool live = inroi && sc.work[p] != 0;
   const int64_t plane = sc.ss * sc.fs;
-  if (threadIdx.x < nk) {
-    const int64_t f = sc.good[k_lo + threadIdx.x];
-    t_di[threadIdx.x] = di[f];
-    t_dj[threadIdx.x] = dj[f];
-    t_off[threadIdx.x] = f * plane;
-  }
-  __syncthreads();
-  if (c >= sc.roi[3]) return;
-  const int64_t p = r * sc.fs + c;
-  if (!sc.work[p]) return;
-  float4* out = img + (int64_t)(blockIdx.z / blocks_per_img) * os * of;
-  const double u0 = u[p], u1 = u[plane + p];
-  const double w = sc.w64[p];
+  const double u0 = live ? u[p] : 0.0, u1 = live ? u[plane + p] : 0.0;
+  const double w = live ? sc.w64[p] : 1.0;
   const double w2 = w * w;                       // recon.py:136
-  float Iv[kFrameChunk];
-#pragma unroll
-  for (int b = 0; b < kFrameChunk; ++b) Iv[b] = b < nk ? __ldg(sc.frames + t_off[b] + p) : 0.f;
+  const double os1 = static_cast<double>(os - 1), of1 = static_cast<double>(of - 1);
+  const int64_t n_o = os * of;
+  const int64_t k_begin = frame_lo + (int64_t)blockIdx.z * frames_per_z;
+  const int64_t k_end = min(frame_hi, k_begin + frames_per_z);
   unsigned long long dropped = 0;
-#pragma unroll
-  for (int b = 0; b < kFrameChunk; ++b) {
-    if (b >= nk) break;
-    const double x = u0 - t_di[b] - static_cast<double>(n0);       // recon.py:138
-    const double y = u1 - t_dj[b] - static_cast<double>(m0);
-    if (!(x >= 0.0 && x <= static_cast<double>(os - 1) && y >= 0.0 &&
-          y <= static_cast<double>(of - 1))) {   // interp.py:103-107
-      ++dropped;
-      continue;
+  for (int64_t kc = k_begin; kc < k_end; kc += kTab) {
+    const int nt = static_cast<int>(k_end - kc < kTab ? k_end - kc : kTab);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += kThreads) {
+      const int64_t f = sc.good[kc + t];
+      t_di[t] = di[f];
+      t_dj[t] = dj[f];
+      t_off[t] = f * plane;
     }
-    const Split sx = split(x), sy = split(y);
-    const double I = static_cast<double>(Iv[b]);
-    const double vw = (I / w) * w2;              // value * weight (interp.py:112)
-    splat_grouped(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2);
+    __syncthreads();
+    if (!live) continue;
+    for (int b0 = 0; b0 < nt; b0 += kFB) {
+      float4* out = img + ((kc - frame_lo + b0) / kFB / bpi) * n_o;
+      float Iv[kFB];
+#pragma unroll
+      for (int b = 0; b < kFB; ++b) Iv[b] = b0 + b < nt ? __ldg(sc.frames + t_off[b0 + b] + p) : 0.f;
+#pragma unroll
+      for (int b = 0; b < kFB; ++b) {
+        if (b0 + b >= nt) break;
+        const double x = u0 - t_di[b0 + b] - static_cast<double>(n0);   // recon.py:138
+        const double y = u1 - t_dj[b0 + b] - static_cast<double>(m0);
+        if (!(x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1)) {         // interp.py:103-107
+          ++dropped;
+          continue;
+        }
+        const Split sx = split(x), sy = split(y);
+        const double vw = (static_cast<double>(Iv[b]) / w) * w2;    // value*weight (interp.py:112)
+        splat_grouped(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2);
+      }
+    }
   }
   if (n_drop && dropped) atomicAdd(n_drop, dropped);
 }
@@ -165,13 +173,6 @@ __global__ void k_splat_f64(double* acc_v, double* acc_w, int64_t os, int64_t of
   if (dropped) atomicAdd(n_drop, dropped);
 }
 
-int grid_1d(int64_t n, int threads) {
-  int64_t b = (n + threads - 1) / threads;
-  if (b < 1) b = 1;
-  if (b > 148 * 16) b = 148 * 16;
-  return static_cast<int>(b);
-}
-
 }  // namespace
 
 int check_scan(const pxst_scan* sc);
@@ -202,17 +203,28 @@ int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
   const int64_t nk = frame_hi - frame_lo;
   if (nk <= 0) return PXST_OK;
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
-  PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
-  const int64_t blocks = (nk + kFrameChunk - 1) / kFrameChunk;
+  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)((rw + kTR - 1) / kTR));
+  PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
+  // Frame slices (grid.z) so the launch holds ~3 waves of resident CTAs.
+  int dev = 0, sms = 148, per_sm = 1;
+  PXST_CHECK_CUDA(cudaGetDevice(&dev));
+  PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PXST_CHECK_CUDA(
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_object_splat, kThreads, 0));
+  const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t n_batches = (nk + kFB - 1) / kFB;
+  int64_t n_z = (3 * resident + (int64_t)g.x * g.y - 1) / ((int64_t)g.x * g.y);
+  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
+  const int64_t fpz = ((n_batches + n_z - 1) / n_z) * kFB;
+  g.z = static_cast<unsigned>((nk + fpz - 1) / fpz);
   const int64_t n = os * of;
   int n_img;
-  const int64_t bpi = chunk_images(blocks, n, &n_img);
+  const int64_t bpi = chunk_images(n_batches, n, &n_img);
   Scratch acc;
   if (int e = acc.alloc(sizeof(float4) * n * n_img, s)) return e;
   PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(float4) * n * n_img, s));
-  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)rw, (unsigned)blocks);
-  k_object_splat<<<g, kTC, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi,
-                                   acc.as<float4>(), (int)bpi, n_drop);
+  k_object_splat<<<g, kThreads, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, fpz,
+                                        acc.as<float4>(), (int)bpi, n_drop);
   PXST_CHECK_LAUNCH();
   return fold_groups(acc.as<float4>(), n_img, os, of, num, den, s);
 }
