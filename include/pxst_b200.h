@@ -170,6 +170,40 @@ int pxst_splat(double* acc_v, double* acc_w, int64_t os, int64_t of, const doubl
                const double* y, const double* value, const double* weight, int64_t n,
                int64_t* n_dropped, void* stream);
 
+/* ---- pixel-map regularisation (recon.py:298-311) ---- */
+
+/* Mask-aware Gaussian regularisation of the displacement, in place on
+ * u [2, ss, fs] (recon.py:210-218 applied at :300-304): per component
+ * d = u - identity, num = G(d*M), den = G(M) with G = scipy
+ * gaussian_filter(sigma, mode="nearest", truncate 4) (axis 0 then axis 1),
+ * u = identity + (M && den > 0 ? num/den : d).  support [ss, fs] is M. */
+int pxst_smooth_displacement(double* u, const uint8_t* support, int64_t ss, int64_t fs,
+                             double sigma, void* stream);
+
+typedef struct pxst_cg_info {
+  int64_t iterations;   /* CG iterations run                                   */
+  double residual;      /* best relative residual |r| / |b|                     */
+  int converged;        /* residual <= tol                                     */
+} pxst_cg_info;
+
+/* Least-squares potential of a gradient field on a mask
+ * (integration.py:61-118): plain conjugate gradients on the masked Poisson
+ * normal operator with the anchor term at the first mask pixel (row-major),
+ * stopped at |r|/|b| <= tol or maxiter (maxiter <= 0: 20*ss*fs); the best
+ * iterate is returned shifted to phi[anchor] = 0.  gx, gy, phi [ss, fs]
+ * float64 (device); info (host, nullable) is written after a stream sync.
+ * Returns PXST_EINVAL if the mask is empty (the reference's ValueError). */
+int pxst_integrate_gradient(const double* gx, const double* gy, const uint8_t* mask,
+                            int64_t ss, int64_t fs, double tol, int64_t maxiter, double* phi,
+                            pxst_cg_info* info, void* stream);
+
+/* Irrotational projection of the displacement, in place on u [2, ss, fs]
+ * (integration.py:121-134 applied at recon.py:305-311): fits phi to
+ * (u0 - i, u1 - j) on the support and sets u = identity + grad(phi) there
+ * (forward differences, last row/column backward). */
+int pxst_project_irrotational(double* u, const uint8_t* support, int64_t ss, int64_t fs,
+                              double tol, int64_t maxiter, pxst_cg_info* info, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

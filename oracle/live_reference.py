@@ -4,7 +4,7 @@ Works only where ``/root/reference`` exists (the build container), never on
 the GPU box.  ``pxst/__init__.py:10`` imports ``cxi_io`` which needs h5py
 (``cxi_io.py:18``); h5py is not installed and the hot path never touches it,
 so an empty stub module is registered first.  Used to pin the oracle
-(``tests/test_oracle_pins.py``) and to write golden vectors
+(``tests/test_oracle_golden.py``) and to write golden vectors
 (``tests/golden/make_golden.py``).
 """
 

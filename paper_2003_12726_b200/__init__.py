@@ -9,7 +9,7 @@ dataclasses and float64 arrays in and out.  Kernels live in
 buffers, streams and ``torch.distributed`` only.
 """
 
-from . import data_model
+from . import data_model, integration
 from .data_model import (
     ErrorMetrics,
     Geometry,

@@ -37,6 +37,10 @@ class PxstRef(ctypes.Structure):
                 ("n0", c_int64), ("m0", c_int64), ("fm64", c_void_p)]
 
 
+class PxstCgInfo(ctypes.Structure):
+    _fields_ = [("iterations", c_int64), ("residual", c_double), ("converged", c_int)]
+
+
 _SIGS = {
     "pxst_abi_version": (c_int, []),
     "pxst_last_error": (c_char_p, []),
@@ -68,6 +72,12 @@ _SIGS = {
                             c_void_p]),
     "pxst_splat": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                            c_void_p, c_int64, POINTER(c_int64), c_void_p]),
+    "pxst_smooth_displacement": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                         c_void_p]),
+    "pxst_integrate_gradient": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                        c_int64, c_void_p, POINTER(PxstCgInfo), c_void_p]),
+    "pxst_project_irrotational": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                          c_int64, POINTER(PxstCgInfo), c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -11,10 +11,12 @@
 //                      for its pixel; samples whose patch leaves the grid or
 //                      touches an invalid cell are skipped.  Writes float32
 //                      partial sums partial[chunk][trial][pixel].
-//   3. k_pix_slow      one thread per (pixel, chunk) re-derives the same
-//                      eligibility and adds the exact per-trial contribution of
-//                      every skipped sample (masked renormalised read, (I-W)^2
-//                      fallback): rare, small code, no register window.
+//   3. k_pix_slow      one warp per listed (pixel, chunk): lanes classify 32
+//                      frames at a time with the same eligibility test, then
+//                      every skipped sample's patch is staged in shared memory
+//                      (the next one's loads in flight meanwhile) and lanes add
+//                      the exact per-trial contribution (masked renormalised
+//                      read, (I-W)^2 fallback) of the trials they own.
 //   4. k_pix_epilogue  one thread per pixel: float64 sum over chunks,
 //                      first-occurrence argmin (numpy order a*Kb + b),
 //                      paraboloid on the normalised 3x3 patch, static-pixel
@@ -43,6 +45,7 @@ __device__ __forceinline__ int tile_dr(int tid) { return ((tid >> 5) >> 1) * 4 +
 __device__ __forceinline__ int tile_dc(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
 constexpr int kNB = 4;  // TMA ring depth
 constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
+constexpr int kPatchPerLane = 7; // ceil(max patch 14x14 / 32)
 
 
 struct PixArgs {
@@ -312,8 +315,9 @@ __device__ __forceinline__ float trial_patch(const float* __restrict__ pf,
   return fwv * (r * r);
 }
 
-__global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ list,
-                           const unsigned* __restrict__ list_n) {
+__global__ void __launch_bounds__(256) k_pix_slow(PixArgs a,
+                                                 const unsigned long long* __restrict__ list,
+                                                 const unsigned* __restrict__ list_n) {
   extern __shared__ __align__(16) unsigned char slow_sm[];
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -342,39 +346,65 @@ __global__ void k_pix_slow(PixArgs a, const unsigned long long* __restrict__ lis
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
     for (int64_t k0 = k_lo; k0 < k_hi; k0 += 32) {
-      // lane-parallel classification of 32 frames
+      // lane-parallel classification of 32 frames; each lane keeps its
+      // frame's sample and stack value for the broadcast below
       const int64_t kl = k0 + lane;
       bool slow = false;
+      Sample sl{};
+      float Il = 0.f, fwl = 1.f;
       if (kl < k_hi) {
         const int64_t f = a.sc.good[kl];
-        const float fwv = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
-        slow = !make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv).fast();
+        fwl = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
+        sl = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwl);
+        slow = !sl.fast();
+        if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
+      // Patch of the next slow frame held in registers: its loads are in
+      // flight while the current frame's trials run.
+      float rf[kPatchPerLane];
+      uint8_t rv[kPatchPerLane];
+      auto load_patch = [&](int bsel) {
+        const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - ra;
+        const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - rb;
+#pragma unroll
+        for (int m = 0; m < kPatchPerLane; ++m) {
+          const int idx = lane + 32 * m;
+          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
+          const bool in = idx < pn && r >= 0 && r < a.os && c >= 0 && c < a.of;
+          const int64_t o = in ? (int64_t)r * a.of + c : 0;
+          rf[m] = in ? __ldg(a.fm + o) : 0.f;
+          rv[m] = in ? __ldg(a.valid + o) : 0;
+        }
+      };
+      if (mask) load_patch(__ffs(mask) - 1);
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
-        const int64_t f = a.sc.good[k0 + bsel];
-        const float fwv = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
-        const Sample sm = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwv);
-        const float I = __ldg(a.sc.frames + f * plane + p);
-        const int pr0 = sm.i - ra, pc0 = sm.j - rb;
-        for (int idx = lane; idx < pn; idx += 32) {
-          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
-          const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
-          const int64_t o = in ? (int64_t)r * a.of + c : 0;
-          pf[idx] = in ? __ldg(a.fm + o) : 0.f;
-          pvld[idx] = in ? __ldg(a.valid + o) : 0;
+        __syncwarp();                  // previous frame's trials are done with the patch
+#pragma unroll
+        for (int m = 0; m < kPatchPerLane; ++m) {
+          const int idx = lane + 32 * m;
+          if (idx < pn) {
+            pf[idx] = rf[m];
+            pvld[idx] = rv[m];
+          }
         }
         __syncwarp();
+        if (mask) load_patch(__ffs(mask) - 1);
+        const double fx = __shfl_sync(0xffffffffu, sl.fx, bsel);
+        const double fy = __shfl_sync(0xffffffffu, sl.fy, bsel);
+        const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - ra;
+        const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - rb;
+        const float I = __shfl_sync(0xffffffffu, Il, bsel);
+        const float fwv = __shfl_sync(0xffffffffu, fwl, bsel);
 #pragma unroll
         for (int j = 0; j < kSlowPerLane; ++j) {
           const int t = lane + 32 * j;
           if (t < nk)
             part[j] += trial_patch(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
-                                   pc0 + t % a.kb, sm.fx, sm.fy, W, I, fwv);
+                                   pc0 + t % a.kb, fx, fy, W, I, fwv);
         }
-        __syncwarp();
       }
     }
 #pragma unroll
@@ -446,11 +476,23 @@ __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chun
   // the common positive normaliser preserves the order except for ties the
   // division itself would create, which the parity bar (unique argmin,
   // margin > 1e-4) excludes.
+  // Eight trials per step with their loads independent (the sum over chunks
+  // keeps the order of total()).
   int best = 0;
-  double braw = total(0);
-  for (int t = 1; t < nk; ++t) {
-    const double v = total(t);
-    if (v < braw) { braw = v; best = t; }
+  double braw = 0.0;
+  for (int t0 = 0; t0 < nk; t0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      const T* pc = part + c * cstride + q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (t0 + j < nk) v[j] += static_cast<double>(pc[(int64_t)(t0 + j) * a.nq]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (t0 + j < nk && (t0 + j == 0 || v[j] < braw)) { braw = v[j]; best = t0 + j; }
   }
   const double bv = braw / nv;
   const int ia = best / nb, ib = best % nb;

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import PxstRef, PxstScan, PxstStats, check, stream_ptr
+from ._native import PxstCgInfo, PxstRef, PxstScan, PxstStats, check, stream_ptr
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -309,6 +309,32 @@ class DeviceScan:
                 per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), stream_ptr()))
         return (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
                 self.sigma2.view(self.ss, self.fs))
+
+    # ------------------------------------- 8(f) pixel-map regularisation
+    def smooth_displacement(self, u_t, sigma: float):
+        """Mask-aware Gaussian regularisation of u_t in place (recon.py:300-304);
+        the support is the work set."""
+        if sigma > 0:
+            check(self.lib.pxst_smooth_displacement(u_t.data_ptr(), self.work.data_ptr(),
+                                                    self.ss, self.fs, float(sigma),
+                                                    stream_ptr()))
+        return u_t
+
+    def project_irrotational(self, u_t, tol: float = 1e-12, maxiter: int | None = None):
+        """Irrotational projection of u_t in place (recon.py:305-311)."""
+        info = PxstCgInfo()
+        check(self.lib.pxst_project_irrotational(u_t.data_ptr(), self.work.data_ptr(), self.ss,
+                                                 self.fs, float(tol), int(maxiter or 0),
+                                                 ctypes.byref(info), stream_ptr()))
+        return info
+
+    def regularise(self, u_t, opts):
+        """The optional stages of recon.update_pixel_map, in its order."""
+        if getattr(opts, "sigma", 0.0) > 0:
+            self.smooth_displacement(u_t, opts.sigma)
+        if getattr(opts, "integrate", False):
+            self.project_irrotational(u_t)
+        return u_t
 
 
 # ---------------------------------------------------------------------------

@@ -7,9 +7,9 @@ fallback: without the library or a CUDA device every call raises.
 
 Scope: ``make_reference`` (alias ``make_object_map``),
 ``update_pixel_map``, ``update_translations``, ``calc_error``,
-``run_main_loop`` and the option types.  ``UpdateOptions.sigma > 0`` and
-``integrate=True`` (section 8(f) rows 1-2, "next") raise
-``NotImplementedError`` rather than silently differing.
+``run_main_loop`` and the option types, including the optional pixel-map
+stages ``UpdateOptions.sigma > 0`` (mask-aware Gaussian regularisation) and
+``integrate=True`` (irrotational projection), section 8(f) rows 1-2.
 """
 
 from __future__ import annotations
@@ -84,11 +84,7 @@ class IterationSettings:
 
 
 def default_schedule(max_iters: int) -> list[IterationSettings]:
-    """The reference's coarse-to-fine defaults (recon.py:451-468).
-
-    Note: they enable ``sigma`` and ``integrate``, which this build does not
-    implement yet (NotImplementedError at the first pixel-map update).
-    """
+    """The reference's coarse-to-fine defaults (recon.py:451-468)."""
     sigmas = [5.0, 3.0] + [1.0] * max(0, max_iters - 2)
     out = []
     for i in range(max_iters):
@@ -131,17 +127,6 @@ def _device_ref(ref, ds: DeviceScan) -> DeviceRef:
     return DeviceRef.from_host(ref.i_ref, ref.wsum, ref.origin, ds.device)
 
 
-def _check_options(opts) -> None:
-    if getattr(opts, "sigma", 0.0) and opts.sigma > 0:
-        raise NotImplementedError(
-            "UpdateOptions.sigma > 0 (mask-aware Gaussian regularisation, recon.py:210-218) "
-            "is a SURVEY 8(f) 'next' row, not built yet")
-    if getattr(opts, "integrate", False):
-        raise NotImplementedError(
-            "UpdateOptions.integrate=True (irrotational projection, integration.py:121-134) "
-            "is a SURVEY 8(f) 'next' row, not built yet")
-
-
 def _host(t: torch.Tensor) -> np.ndarray:
     return to_host(t)
 
@@ -181,7 +166,6 @@ def update_pixel_map(scan: ScanData, w: Whitefield, m: PixelMask, ref: Reference
     ``threads`` is accepted for signature compatibility; results never
     depend on it (recon.py:163-169).  Returns ``(PixelMap, err_map)``.
     """
-    _check_options(opts)
     ds = SCAN_CACHE.get(scan, w, m, roi)
     u_t = ds.upload_u(u.u)
     di_t, dj_t = ds.upload_t(t.di, t.dj)
@@ -195,6 +179,7 @@ def update_pixel_map(scan: ScanData, w: Whitefield, m: PixelMask, ref: Reference
     dref = _device_ref(ref, ds)
     u_out, err = ds.pixel_map_search(dref, u_t, di_t, dj_t, win.half_ss, win.half_fs,
                                      win.subpixel_grid, opts.quadratic_refinement, fw_t)
+    ds.regularise(u_out, opts)                           # recon.py:298-311
     return PixelMap(_host(u_out)), _host(err)
 
 
@@ -261,8 +246,6 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         schedule = default_schedule(max_iters)
     if len(schedule) < max_iters:
         schedule = list(schedule) + [schedule[-1]] * (max_iters - len(schedule))
-    for st in schedule[:max_iters]:
-        _check_options(st.options)
     ds = SCAN_CACHE.get(scan, w, m, roi)
     if ds.empty:
         raise ValueError("make_reference: empty good pixel/frame set")
@@ -278,6 +261,7 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         u_t, _ = ds.pixel_map_search(dref, u_t, di_t, dj_t, st.window.half_ss,
                                      st.window.half_fs, st.window.subpixel_grid,
                                      st.options.quadratic_refinement)
+        ds.regularise(u_t, st.options)
         if st.update_translations:
             tw = st.translation_window
             di_t, dj_t = ds.translation_search(dref, u_t, di_t, dj_t, tw.half_ss, tw.half_fs,

@@ -126,10 +126,17 @@ class ShardedIteration:
         self._all_reduce(acc)
         return self.ex.object_finish(acc, (n0, m0), shape)
 
-    def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True):
+    def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True, opts=None):
         u_local = self.ex.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine,
                                            rows=self.rows[self.rank])
-        return self._gather_rows(u_local)
+        u_full = self._gather_rows(u_local)
+        # sigma smoothing / irrotational projection (recon.py:298-311) couple all
+        # pixels; they are small [SS, FS] planes, so every rank runs them on the
+        # gathered map (deterministic kernels: the ranks stay identical)
+        if opts is not None and (getattr(opts, "sigma", 0.0) > 0 or
+                                 getattr(opts, "integrate", False)):
+            u_full = self.ex.regularise(u_full, opts)
+        return u_full
 
     def translations(self, ref, u, di, dj, half_ss, half_fs, sub=None):
         lo, hi = self.frames[self.rank]
@@ -154,7 +161,7 @@ class ShardedIteration:
         if ev:
             ev[0].record(torch.cuda.current_stream())
         u_new = self.pixel_map(ref, u, di, dj, cfg.half_ss, cfg.half_fs, cfg.subpixel_grid,
-                               cfg.refine)
+                               cfg.refine, opts=cfg)
         if ev:
             ev[1].record(torch.cuda.current_stream())
         di_new, dj_new = di, dj
@@ -204,3 +211,6 @@ class DeviceExecutor:
 
     def error_finish(self, num, den, ref):
         return self.ds.plane_finish(num, den, ref.shape)
+
+    def regularise(self, u, opts):
+        return self.ds.regularise(u, opts)

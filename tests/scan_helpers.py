@@ -124,6 +124,11 @@ class OracleExecutor:
         return (torch.as_tensor(per_frame), torch.as_tensor(per_pixel),
                 torch.as_tensor(acc_v.ravel()), torch.as_tensor(acc_w.ravel()))
 
+    def regularise(self, u, opts):
+        return torch.as_tensor(orc.regularise_map(u.numpy(), self.work.astype(bool),
+                                                  getattr(opts, "sigma", 0.0),
+                                                  getattr(opts, "integrate", False)))
+
     def error_finish(self, num, den, ref):
         plane, _ = orc.ratio_where_weighted(num.numpy().reshape(ref.shape),
                                             den.numpy().reshape(ref.shape))

@@ -360,9 +360,11 @@ def test_empty_work_set_raises():
         pb.SearchWindow(-1, 2)
     with pytest.raises(ValueError):
         pb.SearchWindow(1, 1, subpixel_grid=2.0)
-    with pytest.raises(NotImplementedError):
-        pb.update_pixel_map(sc, w, m, pb.make_reference(sc, w, m, u, t), u, t,
-                            pb.SearchWindow(1, 1), pb.UpdateOptions(sigma=1.0))
+    # integrate on an empty support: the reference's integrate_gradient ValueError
+    ref = pb.make_reference(sc, w, m, u, t)
+    with pytest.raises(ValueError):
+        pb.update_pixel_map(sc, w, pb.PixelMask(np.zeros_like(m.mask)), ref, u, t,
+                            pb.SearchWindow(1, 1), pb.UpdateOptions(integrate=True))
 
 
 def test_frame_weights():

@@ -128,3 +128,54 @@ def test_window_offsets_semantics():
         orc.window_offsets(-1)
     with pytest.raises(ValueError):
         orc.window_offsets(1, 1.5)
+
+
+# ---------------------------------------------------------------------------
+# pixel-map regularisation rows, golden reg0.npz
+# ---------------------------------------------------------------------------
+def _support_ident(s):
+    support = s.m.mask & (s.w.w > 0)
+    ss, fs = support.shape
+    ident = np.stack(np.meshgrid(np.arange(ss, dtype=np.float64),
+                                 np.arange(fs, dtype=np.float64), indexing="ij"))
+    return support, ident
+
+
+def test_smooth_displacement_pinned(scan0, golden_reg):
+    support, ident = _support_ident(scan0)
+    for c in range(2):
+        np.testing.assert_array_equal(
+            orc.smooth_displacement(scan0.u0.u[c] - ident[c], support, 2.5), golden_reg[f"sm_{c}"])
+
+
+def test_integrate_gradient_pinned(golden_reg):
+    g = golden_reg
+    phi, conv, res, it = orc.integrate_gradient(g["ig_gx"], g["ig_gy"], g["ig_mask"])
+    assert it == int(g["ig_iters"]) and conv == bool(g["ig_conv"])
+    assert res == float(g["ig_res"])
+    np.testing.assert_array_equal(phi, g["ig_phi"])
+    with pytest.raises(ValueError):
+        orc.integrate_gradient(g["ig_gx"], g["ig_gy"], np.zeros_like(g["ig_mask"]))
+
+
+@pytest.mark.parametrize("tag,sigma,integrate", [("s", 2.0, False), ("i", 0.0, True),
+                                                 ("si", 1.5, True)])
+def test_regularised_pixel_map_pinned(scan0, golden0, golden_reg, tag, sigma, integrate):
+    s = scan0
+    u, e = orc.update_pixel_map(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask,
+                                *_ref0(golden0), s.u0.u, s.t0.di, s.t0.dj, 3, 3,
+                                sigma=sigma, integrate=integrate)
+    np.testing.assert_array_equal(u, golden_reg[f"upm_{tag}_u"])
+    np.testing.assert_array_equal(e, golden_reg[f"upm_{tag}_err"])
+
+
+def test_default_schedule_loop_pinned(scan0, golden_reg):
+    from conftest import default_schedule_dicts
+    s = scan0
+    u, ref, di, dj, hist = orc.run_main_loop(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask,
+                                             s.u0.u, s.t0.di, s.t0.dj, default_schedule_dicts(3),
+                                             3, tol=-np.inf)
+    np.testing.assert_array_equal(u, golden_reg["loop_u"])
+    np.testing.assert_array_equal(di, golden_reg["loop_di"])
+    np.testing.assert_array_equal(dj, golden_reg["loop_dj"])
+    np.testing.assert_array_equal(np.array(hist), golden_reg["loop_hist"])

@@ -32,6 +32,8 @@ class Cfg:
     t_half_ss: int = 1
     t_half_fs: int = 1
     t_subpixel_grid: float | None = None
+    sigma: float = 0.0
+    integrate: bool = False
 
 
 def test_partition_rows_balanced():
@@ -53,7 +55,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, cfg):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -65,7 +67,7 @@ def _worker(rank, world, port, out):
         ex = OracleExecutor(sc.frames, good, w.w, m.mask)
         it = ShardedIteration(ex, rank, world)
         u_n, di_n, dj_n = it.iteration(torch.as_tensor(u.u), torch.as_tensor(t.di),
-                                       torch.as_tensor(t.dj), Cfg())
+                                       torch.as_tensor(t.dj), cfg)
         if rank == 0:
             out.update(u=u_n.numpy(), di=di_n.numpy(), dj=dj_n.numpy(),
                        total=it.metrics.total, per_frame=it.metrics.per_frame.numpy(),
@@ -75,23 +77,25 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_rank_iteration_matches_unsharded():
+@pytest.mark.parametrize("cfg", [Cfg(), Cfg(sigma=1.0, integrate=True)],
+                         ids=["plain", "regularised"])
+def test_two_rank_iteration_matches_unsharded(cfg):
     import sys
     sys.path.insert(0, os.path.dirname(__file__))
     from scan_helpers import tiny_scan
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, cfg), nprocs=world, join=True)
     assert len(out["rows"]) == 2 and out["rows"][0][1] == out["rows"][1][0]
 
     sc, w, m, u, t = tiny_scan(seed=21, n=7, ss=20, fs=24)
     good = np.ones(7, bool)
     good[3] = False
-    cfg = Cfg()
     ref = orc.make_object_map(sc.frames, good, w.w, m.mask, u.u, t.di, t.dj)
     u1, _, stack = orc.update_pixel_map(sc.frames, good, w.w, m.mask, *ref, u.u, t.di, t.dj,
-                                        cfg.half_ss, cfg.half_fs, return_stack=True)
+                                        cfg.half_ss, cfg.half_fs, return_stack=True,
+                                        sigma=cfg.sigma, integrate=cfg.integrate)
     di1, dj1 = orc.update_translations(sc.frames, good, w.w, m.mask, *ref, u1, t.di, t.dj,
                                        cfg.t_half_ss, cfg.t_half_fs)
     d = orc.calc_error(sc.frames, good, w.w, m.mask, *ref, u1, di1, dj1)
@@ -100,6 +104,9 @@ def test_two_rank_iteration_matches_unsharded():
     P = stack.shape[-1]
     part = np.partition(stack.reshape(-1, P), 1, axis=0)
     uniq = ((part[1] - part[0]) > 1e-9 * np.abs(part[0])).reshape(w.w.shape)
+    if cfg.sigma > 0 or cfg.integrate:      # coupling stages: every argmin must agree
+        assert uniq.all()
+        uniq = np.ones_like(uniq)
     np.testing.assert_allclose(out["u"][:, uniq], u1[:, uniq], rtol=0, atol=1e-9)
     np.testing.assert_allclose(out["di"], di1, atol=1e-9)
     np.testing.assert_allclose(out["dj"], dj1, atol=1e-9)
