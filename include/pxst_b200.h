@@ -176,7 +176,9 @@ int pxst_splat(double* acc_v, double* acc_w, int64_t os, int64_t of, const doubl
  * u [2, ss, fs] (recon.py:210-218 applied at :300-304): per component
  * d = u - identity, num = G(d*M), den = G(M) with G = scipy
  * gaussian_filter(sigma, mode="nearest", truncate 4) (axis 0 then axis 1),
- * u = identity + (M && den > 0 ? num/den : d).  support [ss, fs] is M. */
+ * u = identity + (M && den > 0 ? num/den : d).  support [ss, fs] is M.
+ * The filter taps are computed on the host exactly as scipy does and copied
+ * to the device; the call synchronises the stream before returning. */
 int pxst_smooth_displacement(double* u, const uint8_t* support, int64_t ss, int64_t fs,
                              double sigma, void* stream);
 
@@ -203,6 +205,22 @@ int pxst_integrate_gradient(const double* gx, const double* gy, const uint8_t* m
  * (forward differences, last row/column backward). */
 int pxst_project_irrotational(double* u, const uint8_t* support, int64_t ss, int64_t fs,
                               double tol, int64_t maxiter, pxst_cg_info* info, void* stream);
+
+/* ---- split-half uncertainty (analysis.py:306-361) ---- */
+
+/* The counter-based sample split of split_half_recon (analysis.py:294-303,
+ * :326-328): for every flat stack index k in [0, n_frames*ss*fs),
+ * bit(k) = SplitMix64-finaliser(k + seed * 0x9E3779B97F4A7C15) & 1 and
+ * fw[k] = bit (half 0, "A") or 1 - bit (half 1, "B"), float32, device;
+ * fw must be 16-byte aligned.  fw is the frame-weight input of
+ * pxst_stack_stats / pxst_pixel_map_search. */
+int pxst_split_weights(uint64_t seed, int64_t n_frames, int64_t ss, int64_t fs, int half,
+                       float* fw, void* stream);
+
+/* counts_a[p] = sum over good frames of bit(good[k]*ss*fs + p): the half-A
+ * sample count per pixel (analysis.py:333-334); half B has n_good - counts_a. */
+int pxst_split_counts(uint64_t seed, const int32_t* good, int64_t n_good, int64_t ss, int64_t fs,
+                      int32_t* counts_a, void* stream);
 
 #ifdef __cplusplus
 }

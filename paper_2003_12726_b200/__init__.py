@@ -9,7 +9,7 @@ dataclasses and float64 arrays in and out.  Kernels live in
 buffers, streams and ``torch.distributed`` only.
 """
 
-from . import data_model, integration
+from . import analysis, data_model, geometry, integration
 from .data_model import (
     ErrorMetrics,
     Geometry,

@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint8, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint8, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PXST_LIB", os.path.join(HERE, "libpxst_b200.so"))
@@ -78,6 +78,10 @@ _SIGS = {
                                         c_int64, c_void_p, POINTER(PxstCgInfo), c_void_p]),
     "pxst_project_irrotational": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double,
                                           c_int64, POINTER(PxstCgInfo), c_void_p]),
+    "pxst_split_weights": (c_int, [c_uint64, c_int64, c_int64, c_int64, c_int, c_void_p,
+                                   c_void_p]),
+    "pxst_split_counts": (c_int, [c_uint64, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                  c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -12,7 +12,13 @@ Writes ``reg0.npz`` (config-0 scan of ``paper_2003_12726_b200.synth``):
 * ``upm_s*`` / ``upm_i*`` / ``upm_si*``: ``update_pixel_map`` with
   sigma=2, with integrate=True, and with both (sigma=1.5);
 * ``loop_*``: ``run_main_loop`` with ``default_schedule(3)`` (sigma 5, 3, 1,
-  integrate, translations from iteration 2), history and final state.
+  integrate, translations from iteration 2), history and final state;
+* ``sh_*``: ``analysis.split_half_recon`` (window +-2, seed 3) maps,
+  histograms and sigma; ``shb_*``: the raw split bits of the first 4096
+  flat indices for seeds 0 and 12345;
+* ``fd_*``: ``geometry.fit_defocus_registration`` on the config-0 scan with
+  physical translations of a true z1 = 0.05 m (7-point grid, and a 3x3
+  astigmatic grid).
 """
 
 from __future__ import annotations
@@ -30,9 +36,21 @@ from oracle import live_reference  # noqa: E402
 from paper_2003_12726_b200.synth import make_scan  # noqa: E402
 
 
+def defocus_scan(s, z1=0.05):
+    """The config-0 scan with translations [m] whose projection at focus
+    distance z1 gives the scan's pixel translations."""
+    from dataclasses import replace
+    sc, t = s.scan, s.t0
+    mag = (z1 + sc.distance) / z1
+    tr = np.stack([t.di * sc.x_pixel_size / mag, t.dj * sc.y_pixel_size / mag,
+                   np.zeros_like(t.di)], axis=1)
+    return replace(sc, translations=tr)
+
+
 def main():
     live_reference.load()
-    from pxst import integration, recon
+    from dataclasses import replace
+    from pxst import analysis, geometry, integration, recon
     s = make_scan(0)
     sc, w, m, u, t = s.scan, s.w, s.m, s.u0, s.t0
     out = {}
@@ -65,6 +83,19 @@ def main():
                             tol=-np.inf)
     out.update(loop_u=L.pixel_map.u, loop_di=L.translations.di, loop_dj=L.translations.dj,
                loop_hist=np.array([h.total for h in L.history]))
+    S = analysis.split_half_recon(sc, w, m, R, u, t, recon.SearchWindow(2, 2), seed=3)
+    out.update(sh_ua=S.map_a.u, sh_ub=S.map_b.u, sh_hss=S.hist_ss, sh_hfs=S.hist_fs,
+               sh_sigma=np.array(S.sigma))
+    for sd in (0, 12345):
+        out[f"shb_{sd}"] = analysis._splitmix(sd, np.arange(4096, dtype=np.uint64))
+    sc2 = defocus_scan(s)
+    grid = 0.05 * np.array([0.8, 0.9, 0.95, 1.0, 1.05, 1.1, 1.25])
+    F = geometry.fit_defocus_registration(sc2, w, m, grid)
+    out.update(fd_grid=grid, fd_contrast=F.contrast, fd_z1=np.array([F.z1_ss, F.z1_fs]))
+    F2 = geometry.fit_defocus_registration(sc2, w, m, 0.05 * np.array([0.9, 1.0, 1.1]),
+                                           astigmatic=True)
+    out.update(fd2_contrast=F2.contrast, fd2_cands=F2.candidates,
+               fd2_z1=np.array([F2.z1_ss, F2.z1_fs]))
     np.savez_compressed(os.path.join(HERE, "reg0.npz"), **out)
     print("wrote reg0.npz:", {k: np.shape(v) for k, v in out.items()})
 

@@ -86,3 +86,71 @@ def test_default_schedule_main_loop(scan0, golden_reg):
     np.testing.assert_allclose(hist[:2], golden_reg["loop_hist"][:2], rtol=1e-6)
     np.testing.assert_allclose(hist, golden_reg["loop_hist"], rtol=1e-2)
     assert np.isfinite(L.pixel_map.u).all()
+
+
+# ---------------------------------------------------------------------------
+# split-half uncertainty
+# ---------------------------------------------------------------------------
+def test_split_weights_bits_vs_golden(golden_reg):
+    from paper_2003_12726_b200 import _native
+    lib = _native.lib()
+    for sd in (0, 12345):
+        fw = torch.empty(4096 + 3, dtype=torch.float32, device="cuda")   # ragged tail
+        _native.check(lib.pxst_split_weights(sd, 1, 1, 4099, 0, fw.data_ptr(),
+                                             _native.stream_ptr()))
+        bits = fw.cpu().numpy()[:4096]
+        np.testing.assert_array_equal(bits.astype(bool), golden_reg[f"shb_{sd}"])
+        np.testing.assert_array_equal(fw.cpu().numpy()[4096:],
+                                      orc.split_bits(sd, 4099)[4096:].astype(np.float32))
+        _native.check(lib.pxst_split_weights(sd, 1, 1, 4099, 1, fw.data_ptr(),
+                                             _native.stream_ptr()))
+        np.testing.assert_array_equal(fw.cpu().numpy()[:4096],
+                                      1.0 - golden_reg[f"shb_{sd}"].astype(np.float32))
+
+
+def test_split_half_recon_vs_golden(scan0, golden0, golden_reg):
+    from paper_2003_12726_b200 import analysis
+    s = scan0
+    g = golden_reg
+    ref = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
+    S = analysis.split_half_recon(s.scan, s.w, s.m, ref, s.u0, s.t0, pb.SearchWindow(2, 2),
+                                  seed=3)
+    # pixels whose per-half argmin is unique (margin 1e-4) match to 1e-3 px
+    *_, st_a, st_b = orc.split_half_recon(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask,
+                                          ref.i_ref, ref.wsum, ref.origin, s.u0.u, s.t0.di,
+                                          s.t0.dj, 2, 2, seed=3, return_stacks=True)
+    work = s.m.mask & (s.w.w > 0)
+    for got, want, st in ((S.map_a.u, g["sh_ua"], st_a), (S.map_b.u, g["sh_ub"], st_b)):
+        P = st.shape[-1]
+        part = np.partition(st.reshape(-1, P), 1, axis=0)
+        uniq = (part[1] - part[0]) > 1e-4 * np.abs(part[0])
+        assert uniq.mean() > 0.97
+        d = np.abs(got[:, work] - want[:, work]).max(axis=0)
+        assert d[uniq].max() < PX_TOL, d[uniq].max()
+        np.testing.assert_array_equal(got[:, ~work], want[:, ~work])
+    # histograms move by at most the pixels whose argmin is not unique
+    slack = 2 * int((~uniq).sum()) + 2
+    assert np.abs(S.hist_ss - g["sh_hss"]).sum() <= slack
+    assert np.abs(S.hist_fs - g["sh_hfs"]).sum() <= slack
+    assert abs(S.sigma - float(g["sh_sigma"])) <= 0.05 * float(g["sh_sigma"]) + 1e-3
+
+
+# ---------------------------------------------------------------------------
+# defocus by registration contrast
+# ---------------------------------------------------------------------------
+def test_defocus_registration_vs_golden(scan0, golden_reg):
+    from golden.make_golden_reg import defocus_scan
+    from paper_2003_12726_b200 import geometry
+    g = golden_reg
+    sc = defocus_scan(scan0)
+    F = geometry.fit_defocus_registration(sc, scan0.w, scan0.m, g["fd_grid"])
+    # object maps to ~1e-7 (float32 chunk images): contrast to 1e-5
+    np.testing.assert_allclose(F.contrast, g["fd_contrast"], rtol=1e-5)
+    assert (F.z1_ss, F.z1_fs) == tuple(g["fd_z1"])
+    F2 = geometry.fit_defocus_registration(sc, scan0.w, scan0.m, 0.05 * np.array([0.9, 1.0, 1.1]),
+                                           astigmatic=True)
+    np.testing.assert_array_equal(F2.candidates, g["fd2_cands"])
+    np.testing.assert_allclose(F2.contrast, g["fd2_contrast"], rtol=1e-5)
+    assert (F2.z1_ss, F2.z1_fs) == tuple(g["fd2_z1"])
+    with pytest.raises(ValueError):
+        geometry.fit_defocus_registration(sc, scan0.w, scan0.m, [])

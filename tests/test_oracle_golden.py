@@ -179,3 +179,38 @@ def test_default_schedule_loop_pinned(scan0, golden_reg):
     np.testing.assert_array_equal(di, golden_reg["loop_di"])
     np.testing.assert_array_equal(dj, golden_reg["loop_dj"])
     np.testing.assert_array_equal(np.array(hist), golden_reg["loop_hist"])
+
+
+def test_split_half_pinned(scan0, golden0, golden_reg):
+    g = golden_reg
+    for sd in (0, 12345):
+        np.testing.assert_array_equal(orc.split_bits(sd, 4096), g[f"shb_{sd}"])
+    s = scan0
+    ua, ub, hss, hfs, sig = orc.split_half_recon(s.scan.frames, s.scan.good_frames, s.w.w,
+                                                 s.m.mask, *_ref0(golden0), s.u0.u, s.t0.di,
+                                                 s.t0.dj, 2, 2, seed=3)
+    np.testing.assert_array_equal(ua, g["sh_ua"])
+    np.testing.assert_array_equal(ub, g["sh_ub"])
+    np.testing.assert_array_equal(hss, g["sh_hss"])
+    np.testing.assert_array_equal(hfs, g["sh_hfs"])
+    assert sig == float(g["sh_sigma"])
+
+
+def _defocus_scan(s):
+    from golden.make_golden_reg import defocus_scan
+    return defocus_scan(s)
+
+
+def test_defocus_registration_pinned(scan0, golden_reg):
+    g = golden_reg
+    sc = _defocus_scan(scan0)
+    args = (sc.frames, sc.good_frames, scan0.w.w, scan0.m.mask, sc.distance,
+            (sc.x_pixel_size, sc.y_pixel_size), sc.basis_vectors, sc.translations)
+    best, contrast, _ = orc.fit_defocus_registration(*args, g["fd_grid"])
+    np.testing.assert_array_equal(contrast, g["fd_contrast"])
+    assert best == tuple(g["fd_z1"])
+    best, contrast, cands = orc.fit_defocus_registration(*args, 0.05 * np.array([0.9, 1.0, 1.1]),
+                                                         astigmatic=True)
+    np.testing.assert_array_equal(cands, g["fd2_cands"])
+    np.testing.assert_array_equal(contrast, g["fd2_contrast"])
+    assert best == tuple(g["fd2_z1"])
