@@ -13,10 +13,10 @@
 //                      partial sums partial[chunk][trial][pixel].
 //   3. k_pix_slow      one warp per listed (pixel, chunk): lanes classify 32
 //                      frames at a time with the same eligibility test, then
-//                      every skipped sample's patch is staged in shared memory
-//                      (the next one's loads in flight meanwhile) and lanes add
-//                      the exact per-trial contribution (masked renormalised
-//                      read, (I-W)^2 fallback) of the trials they own.
+//                      for every skipped sample lanes add the exact per-trial
+//                      contribution (masked renormalised read from a
+//                      NaN-encoded reference, (I-W)^2 fallback) of the trials
+//                      they own, in frame order.
 //   4. k_pix_epilogue  one thread per pixel: float64 sum over chunks,
 //                      first-occurrence argmin (numpy order a*Kb + b),
 //                      paraboloid on the normalised 3x3 patch, static-pixel
@@ -45,7 +45,6 @@ __device__ __forceinline__ int tile_dr(int tid) { return ((tid >> 5) >> 1) * 4 +
 __device__ __forceinline__ int tile_dc(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
 constexpr int kNB = 4;  // TMA ring depth
 constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
-constexpr int kPatchPerLane = 7; // ceil(max patch 14x14 / 32)
 
 
 struct PixArgs {
@@ -56,6 +55,7 @@ struct PixArgs {
   const float* fm;
   const uint8_t* valid;
   const uint8_t* pv;
+  const float* fmn;          // NaN-encoded reference (slow fix-up)
   int64_t os, of, n0, m0;
   const float* fw;           // nullable frame weights [n_frames, ss, fs]
   const double* var;         // normaliser [ss*fs]
@@ -287,49 +287,24 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 //    order; each (chunk, trial, pixel) partial is owned by one lane, so the
 //    result does not depend on list order.
 // ---------------------------------------------------------------------------
-// Exact trial from a staged patch (same semantics as masked_read): the patch
-// covers object rows [pr0, pr0 + ka] x cols [pc0, pc0 + kb]; cells outside
-// the grid are stored invalid.
-__device__ __forceinline__ float trial_patch(const float* __restrict__ pf,
-                                             const uint8_t* __restrict__ pvld, int ld, int pr0,
-                                             int pc0, int64_t os, int64_t of, int row, int col,
-                                             double fx, double fy, float W, float I, float fwv) {
-  const float d0 = I - W;
-  const float fb = fwv * (d0 * d0);
-  if (!inside_1d(row, fx, os) || !inside_1d(col, fy, of)) return fb;
-  const int r1 = min(row + 1, static_cast<int>(os - 1)), c1 = min(col + 1, static_cast<int>(of - 1));
-  const int a00 = (row - pr0) * ld + (col - pc0), a01 = (row - pr0) * ld + (c1 - pc0);
-  const int a10 = (r1 - pr0) * ld + (col - pc0), a11 = (r1 - pr0) * ld + (c1 - pc0);
-  const bool m00 = pvld[a00], m01 = pvld[a01], m10 = pvld[a10], m11 = pvld[a11];
-  const bool any = m00 || (fy > 0.0 && m01) || (fx > 0.0 && m10) || (fx > 0.0 && fy > 0.0 && m11);
-  if (!any) return fb;
-  const float gx = static_cast<float>(fx), gy = static_cast<float>(fy);
-  const float w00 = (1.f - gx) * (1.f - gy), w01 = (1.f - gx) * gy;
-  const float w10 = gx * (1.f - gy), w11 = gx * gy;
-  float den = 0.f, num = 0.f;
-  if (m00) { den += w00; num = fmaf(w00, pf[a00], num); }
-  if (m01) { den += w01; num = fmaf(w01, pf[a01], num); }
-  if (m10) { den += w10; num = fmaf(w10, pf[a10], num); }
-  if (m11) { den += w11; num = fmaf(w11, pf[a11], num); }
-  const float r = fmaf(-W, num / den, I);
-  return fwv * (r * r);
-}
-
-__global__ void __launch_bounds__(256) k_pix_slow(PixArgs a,
+__global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
                                                  const unsigned long long* __restrict__ list,
                                                  const unsigned* __restrict__ list_n) {
-  extern __shared__ __align__(16) unsigned char slow_sm[];
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int ld = a.kb + 1, pn = (a.ka + 1) * ld;
-  float* pf = reinterpret_cast<float*>(slow_sm) + wib * pn;
-  uint8_t* pvld = slow_sm + sizeof(float) * pn * (blockDim.x >> 5) + wib * pn;
+  const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned n = *list_n;
   const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
   const int nk = a.ka * a.kb;
   const int64_t plane = a.sc.ss * a.sc.fs;
+  int ta[kSlowPerLane], tb[kSlowPerLane];   // window coordinates of the lane's trials
+#pragma unroll
+  for (int j = 0; j < kSlowPerLane; ++j) {
+    const int t = lane + 32 * j;
+    ta[j] = t / a.kb;
+    tb[j] = t % a.kb;
+  }
   for (int64_t e = warp0; e < n; e += nwarps) {
     const unsigned long long ent = list[e];
     const int64_t q = static_cast<int64_t>(ent >> 20);
@@ -343,8 +318,12 @@ __global__ void __launch_bounds__(256) k_pix_slow(PixArgs a,
     const int64_t k_lo = (int64_t)chunk * a.chunk;
     const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
     float part[kSlowPerLane];          // lane owns trials lane + 32 j
+    float prev[kSlowPerLane];          // the fast kernel's partials, fetched early
 #pragma unroll
-    for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
+    for (int j = 0; j < kSlowPerLane; ++j) {
+      part[j] = 0.f;
+      prev[j] = lane + 32 * j < nk ? out[(int64_t)(lane + 32 * j) * a.nq] : 0.f;
+    }
     for (int64_t k0 = k_lo; k0 < k_hi; k0 += 32) {
       // lane-parallel classification of 32 frames; each lane keeps its
       // frame's sample and stack value for the broadcast below
@@ -360,57 +339,25 @@ __global__ void __launch_bounds__(256) k_pix_slow(PixArgs a,
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
-      // Patch of the next slow frame held in registers: its loads are in
-      // flight while the current frame's trials run.
-      float rf[kPatchPerLane];
-      uint8_t rv[kPatchPerLane];
-      auto load_patch = [&](int bsel) {
-        const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - ra;
-        const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - rb;
-#pragma unroll
-        for (int m = 0; m < kPatchPerLane; ++m) {
-          const int idx = lane + 32 * m;
-          const int r = pr0 + idx / ld, c = pc0 + idx % ld;
-          const bool in = idx < pn && r >= 0 && r < a.os && c >= 0 && c < a.of;
-          const int64_t o = in ? (int64_t)r * a.of + c : 0;
-          rf[m] = in ? __ldg(a.fm + o) : 0.f;
-          rv[m] = in ? __ldg(a.valid + o) : 0;
-        }
-      };
-      if (mask) load_patch(__ffs(mask) - 1);
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
-        __syncwarp();                  // previous frame's trials are done with the patch
-#pragma unroll
-        for (int m = 0; m < kPatchPerLane; ++m) {
-          const int idx = lane + 32 * m;
-          if (idx < pn) {
-            pf[idx] = rf[m];
-            pvld[idx] = rv[m];
-          }
-        }
-        __syncwarp();
-        if (mask) load_patch(__ffs(mask) - 1);
-        const double fx = __shfl_sync(0xffffffffu, sl.fx, bsel);
-        const double fy = __shfl_sync(0xffffffffu, sl.fy, bsel);
         const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - ra;
         const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - rb;
-        const float I = __shfl_sync(0xffffffffu, Il, bsel);
-        const float fwv = __shfl_sync(0xffffffffu, fwl, bsel);
+        const ExactSample es = exact_sample(__shfl_sync(0xffffffffu, sl.fx, bsel),
+                                            __shfl_sync(0xffffffffu, sl.fy, bsel), W,
+                                            __shfl_sync(0xffffffffu, Il, bsel),
+                                            __shfl_sync(0xffffffffu, fwl, bsel));
 #pragma unroll
-        for (int j = 0; j < kSlowPerLane; ++j) {
-          const int t = lane + 32 * j;
-          if (t < nk)
-            part[j] += trial_patch(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
-                                   pc0 + t % a.kb, fx, fy, W, I, fwv);
-        }
+        for (int j = 0; j < kSlowPerLane; ++j)
+          if (lane + 32 * j < nk)
+            part[j] += trial_global(a.fmn, a.os, a.of, pr0 + ta[j], pc0 + tb[j], es);
       }
     }
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) {
       const int t = lane + 32 * j;
-      if (t < nk) out[(int64_t)t * a.nq] += part[j];
+      if (t < nk) out[(int64_t)t * a.nq] = prev[j] + part[j];
     }
   }
 }
@@ -603,8 +550,11 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     a.chunk = static_cast<int>((sc->n_good + n_chunks - 1) / n_chunks);
     a.n_chunks = static_cast<int>((sc->n_good + a.chunk - 1) / a.chunk);
 
-    Scratch pvbuf, pvtmp, geo, part, fmpad;
+    Scratch pvbuf, pvtmp, geo, part, fmpad, fmn;
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
+    if (int e = fmn.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
+    if (int e = make_nan_ref(ref, fmn.as<float>(), s)) return e;
+    a.fmn = fmn.as<float>();
     if (int e = make_pv(ref, -ra, ra + 1, -rb, rb + 1, pvbuf.as<uint8_t>(), pvtmp, s)) return e;
     a.pv = pvbuf.as<uint8_t>();
     if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
@@ -652,8 +602,7 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
     fn<<<gf, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
-    const size_t slow_smem = (sizeof(float) + 1) * (na + 1) * (nb + 1) * 8;
-    k_pix_slow<<<148 * 4, 256, slow_smem, s>>>(a, list, list_n);
+    k_pix_slow<<<148 * 6, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;

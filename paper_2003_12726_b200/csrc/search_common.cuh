@@ -146,6 +146,109 @@ __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact trials on a staged patch (the slow fix-up kernels).  The patch holds
+// the float32 reference at rows pr0.. and cols pc0.. with NaN on invalid or
+// out-of-grid cells, so one shared-memory load gives value and validity.
+// Everything that is constant over a sample's trials (integer shifts keep
+// its fractions) is hoisted into ExactSample; a trial then costs four loads
+// and the masked renormalisation of masked_read, in the same float32
+// operation order.
+// ---------------------------------------------------------------------------
+struct ExactSample {
+  float w00, w01, w10, w11;   // bilinear weights (masked_read's float32 formulas)
+  bool fxp, fyp;              // fx > 0, fy > 0 decided on the float64 fractions
+  float I, W, fwv, fb;        // fb = fwv (I - W)^2, the invalid-trial fallback
+};
+
+__device__ __forceinline__ ExactSample exact_sample(double fx, double fy, float W, float I,
+                                                    float fwv) {
+  ExactSample e;
+  const float gx = static_cast<float>(fx), gy = static_cast<float>(fy);
+  e.w00 = (1.f - gx) * (1.f - gy);
+  e.w01 = (1.f - gx) * gy;
+  e.w10 = gx * (1.f - gy);
+  e.w11 = gx * gy;
+  e.fxp = fx > 0.0;
+  e.fyp = fy > 0.0;
+  e.I = I;
+  e.W = W;
+  e.fwv = fwv;
+  const float d0 = I - W;
+  e.fb = fwv * (d0 * d0);
+  return e;
+}
+
+// Trial whose base cell is grid (row, col) = patch (pa, pb): the inclusive
+// inside test of interp.py:67 on integers plus the per-sample flags, then
+// the renormalised bilinear read of interp.py:70-84 (clipped corners carry
+// zero weight and are skipped, which also skips their NaN).
+__device__ __forceinline__ float trial_staged(const float* __restrict__ pf, int ld, int pa,
+                                              int pb, int row, int col, int64_t os, int64_t of,
+                                              const ExactSample& e) {
+  const bool rin = (row >= 0 && row < os - 1) || (row == os - 1 && !e.fxp);
+  const bool cin = (col >= 0 && col < of - 1) || (col == of - 1 && !e.fyp);
+  if (!(rin && cin)) return e.fb;
+  const float* p = pf + pa * ld + pb;
+  const float v00 = p[0], v01 = p[1], v10 = p[ld], v11 = p[ld + 1];
+  const bool m00 = v00 == v00;
+  const bool m01 = e.fyp && v01 == v01;
+  const bool m10 = e.fxp && v10 == v10;
+  const bool m11 = e.fxp && e.fyp && v11 == v11;
+  if (!(m00 || m01 || m10 || m11)) return e.fb;
+  float den = 0.f, num = 0.f;
+  if (m00) { den += e.w00; num = fmaf(e.w00, v00, num); }
+  if (m01) { den += e.w01; num = fmaf(e.w01, v01, num); }
+  if (m10) { den += e.w10; num = fmaf(e.w10, v10, num); }
+  if (m11) { den += e.w11; num = fmaf(e.w11, v11, num); }
+  const float r = fmaf(-e.W, num / den, e.I);
+  return e.fwv * (r * r);
+}
+
+// Same trial read straight from a NaN-encoded copy of the reference in
+// global memory (make_nan_ref): four independent L1/L2 loads, no staging.
+// Corners past the last row/column are clamped onto the grid; they carry
+// zero weight and are excluded by the fx/fy flags.
+__device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int64_t os,
+                                              int64_t of, int row, int col,
+                                              const ExactSample& e) {
+  const bool rin = (row >= 0 && row < os - 1) || (row == os - 1 && !e.fxp);
+  const bool cin = (col >= 0 && col < of - 1) || (col == of - 1 && !e.fyp);
+  if (!(rin && cin)) return e.fb;
+  const int r1 = row + 1 < os ? row + 1 : row, c1 = col + 1 < of ? col + 1 : col;
+  const float* p0 = fmn + (int64_t)row * of;
+  const float* p1 = fmn + (int64_t)r1 * of;
+  const float v00 = __ldg(p0 + col), v01 = __ldg(p0 + c1);
+  const float v10 = __ldg(p1 + col), v11 = __ldg(p1 + c1);
+  const bool m00 = v00 == v00;
+  const bool m01 = e.fyp && v01 == v01;
+  const bool m10 = e.fxp && v10 == v10;
+  const bool m11 = e.fxp && e.fyp && v11 == v11;
+  if (!(m00 || m01 || m10 || m11)) return e.fb;
+  float den = 0.f, num = 0.f;
+  if (m00) { den += e.w00; num = fmaf(e.w00, v00, num); }
+  if (m01) { den += e.w01; num = fmaf(e.w01, v01, num); }
+  if (m10) { den += e.w10; num = fmaf(e.w10, v10, num); }
+  if (m11) { den += e.w11; num = fmaf(e.w11, v11, num); }
+  const float r = fmaf(-e.W, num / den, e.I);
+  return e.fwv * (r * r);
+}
+
+// float32 reference with NaN on invalid cells, [os*of] (for trial_global).
+int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s);
+
+// Patch cell value for staging: the float32 reference, NaN where invalid or
+// outside the grid.
+__device__ __forceinline__ float staged_cell(const float* __restrict__ fm,
+                                             const uint8_t* __restrict__ valid, int64_t os,
+                                             int64_t of, int r, int c) {
+  const bool in = r >= 0 && r < os && c >= 0 && c < of;
+  const int64_t o = in ? (int64_t)r * of + c : 0;
+  const uint8_t ok = __ldg(valid + o);      // both loads issued together
+  const float v = __ldg(fm + o);
+  return (in && ok) ? v : __int_as_float(0x7fc00000);
+}
+
 // Exact contribution of one sample to one trial whose bilinear base cell is
 // (row, col) with fractions (fx, fy): masked renormalised read from global
 // memory with the inclusive inside test, (I - W)^2 fallback when invalid

@@ -79,6 +79,20 @@ int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Sc
   return PXST_OK;
 }
 
+__global__ void k_nan_ref(const float* __restrict__ fm, const uint8_t* __restrict__ valid,
+                          int64_t n, float* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = valid[q] ? fm[q] : __int_as_float(0x7fc00000);
+}
+
+int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s) {
+  const int64_t n = ref->os * ref->of;
+  k_nan_ref<<<grid_1d(n, 256), 256, 0, s>>>(ref->fm, ref->valid, n, out);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
 std::vector<double> window_offsets(int64_t half, double step) {
   std::vector<double> o;
   if (step <= 0.0) {

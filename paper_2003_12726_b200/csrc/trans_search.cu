@@ -291,41 +291,22 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
 // ---------------------------------------------------------------------------
 // 3. slow fix-up: warp per listed frame
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ float trial_patch3(const float* __restrict__ pf,
-                                              const uint8_t* __restrict__ pvld, int ld, int pr0,
-                                              int pc0, int64_t os, int64_t of, int row, int col,
-                                              double fx, double fy, float W, float I) {
-  const float d0 = I - W;
-  const float fb = d0 * d0;
-  if (!inside_1d(row, fx, os) || !inside_1d(col, fy, of)) return fb;
-  const int r1 = min(row + 1, static_cast<int>(os - 1)), c1 = min(col + 1, static_cast<int>(of - 1));
-  const int a00 = (row - pr0) * ld + (col - pc0), a01 = (row - pr0) * ld + (c1 - pc0);
-  const int a10 = (r1 - pr0) * ld + (col - pc0), a11 = (r1 - pr0) * ld + (c1 - pc0);
-  const bool m00 = pvld[a00], m01 = pvld[a01], m10 = pvld[a10], m11 = pvld[a11];
-  const bool any = m00 || (fy > 0.0 && m01) || (fx > 0.0 && m10) || (fx > 0.0 && fy > 0.0 && m11);
-  if (!any) return fb;
-  const float gx = static_cast<float>(fx), gy = static_cast<float>(fy);
-  const float w00 = (1.f - gx) * (1.f - gy), w01 = (1.f - gx) * gy;
-  const float w10 = gx * (1.f - gy), w11 = gx * gy;
-  float den = 0.f, num = 0.f;
-  if (m00) { den += w00; num = fmaf(w00, pf[a00], num); }
-  if (m01) { den += w01; num = fmaf(w01, pf[a01], num); }
-  if (m10) { den += w10; num = fmaf(w10, pf[a10], num); }
-  if (m11) { den += w11; num = fmaf(w11, pf[a11], num); }
-  const float r = fmaf(-W, num / den, I);
-  return r * r;
-}
-
 __global__ void k_trans_slow(TransArgs a) {
   extern __shared__ __align__(16) unsigned char slow_sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int ld = a.kb + 1, pn = (a.ka + 1) * ld;
   float* pf = reinterpret_cast<float*>(slow_sm) + wib * pn;
-  uint8_t* pvld = slow_sm + sizeof(float) * pn * (blockDim.x >> 5) + wib * pn;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned n = *a.slow_n;
   const int nk_ph = a.ka * a.kb, nk = a.na_full * a.nb_full;
+  int ta[kSlowPerLane], tb[kSlowPerLane];   // patch coordinates of the lane's trials
+#pragma unroll
+  for (int j = 0; j < kSlowPerLane; ++j) {
+    const int t = lane + 32 * j;
+    ta[j] = t / a.kb;
+    tb[j] = t % a.kb;
+  }
   const int64_t plane = a.sc.ss * a.sc.fs;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   for (int64_t e = warp0; e < n; e += nwarps) {
@@ -364,21 +345,15 @@ __global__ void k_trans_slow(TransArgs a) {
           const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
           const float I = __ldg(frame + ps), W = a.sc.w32[ps];
           const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
-          for (int idx = lane; idx < pn; idx += 32) {
-            const int r = pr0 + idx / ld, c = pc0 + idx % ld;
-            const bool in = r >= 0 && r < a.os && c >= 0 && c < a.of;
-            const int64_t o = in ? (int64_t)r * a.of + c : 0;
-            pf[idx] = in ? __ldg(a.fm + o) : 0.f;
-            pvld[idx] = in ? __ldg(a.valid + o) : 0;
-          }
+          for (int idx = lane; idx < pn; idx += 32)
+            pf[idx] = staged_cell(a.fm, a.valid, a.os, a.of, pr0 + idx / ld, pc0 + idx % ld);
           __syncwarp();
+          const ExactSample es = exact_sample(sm.fx, sm.fy, W, I, 1.f);
 #pragma unroll
-          for (int j = 0; j < kSlowPerLane; ++j) {
-            const int t = lane + 32 * j;
-            if (t < nk_ph)
-              part[j] += trial_patch3(pf, pvld, ld, pr0, pc0, a.os, a.of, pr0 + t / a.kb,
-                                      pc0 + t % a.kb, sm.fx, sm.fy, W, I);
-          }
+          for (int j = 0; j < kSlowPerLane; ++j)
+            if (lane + 32 * j < nk_ph)
+              part[j] += trial_staged(pf, ld, ta[j], tb[j], pr0 + ta[j], pc0 + tb[j], a.os,
+                                      a.of, es);
           __syncwarp();
         }
       }
@@ -653,7 +628,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
       PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(unsigned long long) * 8, s));
       a.dbg = dbg.as<unsigned long long>();
     }
-    const size_t slow_smem = (sizeof(float) + 1) * (max_ka + 1) * (max_kb + 1) * 8;
+    const size_t slow_smem = sizeof(float) * (max_ka + 1) * (max_kb + 1) * 8;
     for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
       const int64_t c1 = min(frame_hi, c0 + chunk);
       a.frame_lo = c0;
