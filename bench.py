@@ -250,18 +250,22 @@ def run_ours(args, rank, world, local):
 
     def step(ev=None):
         if state["it"] == 0:
-            state.update(u=u_t, di=di_t, dj=dj_t)
+            state.update(u=u_t, di=di_t, dj=dj_t, geom=None)
         u, di, dj = state["u"], state["di"], state["dj"]
+        nxt = None
         if sharded is not None:
             u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev)
         else:
-            dref = ds.object_map(u, di, dj)
+            # the iteration's grid bbox and K2 tile spans were fetched on a side
+            # stream while the previous iteration's error maps ran
+            geom = state["geom"] or ds.geometry_async(u, di, dj)
+            dref = ds.object_map(u, di, dj, geom=geom)
             u_new = u
             if cfg.update_pixel_map:
                 if ev:
                     ev[0].record(stream)
                 u_new, err = ds.pixel_map_search(dref, u, di, dj, cfg.half_ss, cfg.half_fs,
-                                                 cfg.subpixel_grid, cfg.refine)
+                                                 cfg.subpixel_grid, cfg.refine, geom=geom)
                 if ev:
                     ev[1].record(stream)
             di_new, dj_new = di, dj
@@ -272,8 +276,10 @@ def run_ours(args, rank, world, local):
                                                        cfg.t_half_fs, cfg.t_subpixel_grid)
                 if ev and not cfg.update_pixel_map:
                     ev[1].record(stream)
+            nxt = ds.geometry_async(u_new, di_new, dj_new)
             ds.error_maps(dref, u_new, di_new, dj_new)
-        state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new)
+        state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new,
+                     geom=nxt)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 

@@ -128,6 +128,24 @@ int pxst_pixel_map_search(const pxst_scan* scan, const pxst_stats* st, const pxs
                           const float* fw, const double* var_fw, double* u_out,
                           double* err_out, void* stream);
 
+/* Same, with the TMA window sizing hint span_hint (host int32[2]) taken from
+ * pxst_tile_spans on the same u instead of a device->host read inside the
+ * call: with the hint the call never synchronises the stream.  A hint that
+ * does not match u costs speed only (tiles whose window does not fit the
+ * box take the exact path).  span_hint = NULL behaves as
+ * pxst_pixel_map_search. */
+int pxst_pixel_map_search_ex(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                             const double* u_in, const double* di, const double* dj,
+                             int64_t half_ss, int64_t half_fs, double subpixel_step, int refine,
+                             const float* fw, const double* var_fw, double* u_out,
+                             double* err_out, const int32_t* span_hint, void* stream);
+
+/* Largest per-tile extent of u over the K2 pixel tiles (rows, cols; device
+ * int32[2]), the window sizing input of pxst_pixel_map_search_ex.  Depends
+ * on u only, so it can be computed (and copied to the host) ahead of time,
+ * e.g. on a side stream while the error maps run. */
+int pxst_tile_spans(const pxst_scan* scan, const double* u, int32_t* spans, void* stream);
+
 /* K3 per-frame translation grid search (recon.py:336-385), including the
  * reference's quirks: offsets enter as u - (d + off) and the paraboloid
  * offset (grid-index units) is added in pixels whenever the argmin is

@@ -58,6 +58,11 @@ _SIGS = {
     "pxst_pixel_map_search": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                       c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
                                       c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_pixel_map_search_ex": (c_int, [POINTER(PxstScan), POINTER(PxstStats),
+                                         POINTER(PxstRef), c_void_p, c_void_p, c_void_p, c_int64,
+                                         c_int64, c_double, c_int, c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p]),
+    "pxst_tile_spans": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p]),
     "pxst_translation_search": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                         c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                         c_double, c_int64, c_int64, c_void_p, c_void_p,

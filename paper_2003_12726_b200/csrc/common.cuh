@@ -192,9 +192,9 @@ __device__ __forceinline__ void splat_grouped(float4* img, int64_t cell, double 
 // num/den [os*of] (added to their contents).
 int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* num, double* den,
                 cudaStream_t s);
-// Number of grouped images for `blocks` frame blocks over n_cells cells;
-// returns frame blocks per image.
-int64_t chunk_images(int64_t blocks, int64_t n_cells, int* n_img);
+// Number of grouped images for `blocks` frame blocks of frames_per_block
+// frames over n_cells cells; returns frame blocks per image.
+int64_t chunk_images(int64_t blocks, int64_t frames_per_block, int64_t n_cells, int* n_img);
 
 // Float64 variant for the memory-bound error maps (K4), reading a float64
 // masked image: matches the reference's float64 residuals to ~1e-15.

@@ -267,7 +267,7 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
   double* pix_part = ftmp + sc->n_good;
   const int64_t n_o = ref->os * ref->of;
   int n_img;
-  const int64_t bpi = chunk_images(n_batches, n_o, &n_img);
+  const int64_t bpi = chunk_images(n_batches, kFB, n_o, &n_img);
   Scratch img, grp;
   if (int e = img.alloc(sizeof(float4) * n_o * n_img, s)) return e;
   if (int e = grp.alloc(sizeof(double2) * n_o, s)) return e;

@@ -483,12 +483,12 @@ FastKernel find_fast(int ka, int kb) {
 
 using namespace pxst;
 
-extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
-                                     const pxst_ref* ref, const double* u_in, const double* di,
-                                     const double* dj, int64_t half_ss, int64_t half_fs,
-                                     double subpixel_step, int refine, const float* fw,
-                                     const double* var_fw, double* u_out, double* err_out,
-                                     void* stream) {
+namespace {
+int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref,
+                     const double* u_in, const double* di, const double* dj, int64_t half_ss,
+                     int64_t half_fs, double subpixel_step, int refine, const float* fw,
+                     const double* var_fw, double* u_out, double* err_out,
+                     const int32_t* span_hint, void* stream) {
   if (int e = check_scan(sc)) return e;
   if (int e = check_ref(ref)) return e;
   PXST_REQUIRE(st && st->var_pm, "stats descriptor is NULL");
@@ -579,7 +579,12 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
     // at the edges of the config-3 map), capped at 24 KB per ring slot; tiles
     // beyond the cap take the exact path.
     int span[2];
-    if (int e = tile_span_max(geo.as<TileGeo>(), tiles, span, s)) return e;
+    if (span_hint) {             // from pxst_tile_spans; a stale hint only costs speed
+      span[0] = span_hint[0];
+      span[1] = span_hint[1];
+    } else if (int e = tile_span_max(geo.as<TileGeo>(), tiles, span, s)) {
+      return e;
+    }
     a.box_r = max(a.box_r, span[0] + need_rows2(na));
     a.box_c = max(a.box_c, span[1] + need_cols2(nb));
     a.box_c = (a.box_c + 23) / 32 * 32 + 8;            // pitch = 8 (mod 32)
@@ -627,4 +632,46 @@ extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
                                                  u_out, err_out);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
+}
+}  // namespace
+
+extern "C" int pxst_pixel_map_search(const pxst_scan* sc, const pxst_stats* st,
+                                     const pxst_ref* ref, const double* u_in, const double* di,
+                                     const double* dj, int64_t half_ss, int64_t half_fs,
+                                     double subpixel_step, int refine, const float* fw,
+                                     const double* var_fw, double* u_out, double* err_out,
+                                     void* stream) {
+  return pixel_map_search(sc, st, ref, u_in, di, dj, half_ss, half_fs, subpixel_step, refine, fw,
+                          var_fw, u_out, err_out, nullptr, stream);
+}
+
+extern "C" int pxst_pixel_map_search_ex(const pxst_scan* sc, const pxst_stats* st,
+                                        const pxst_ref* ref, const double* u_in,
+                                        const double* di, const double* dj, int64_t half_ss,
+                                        int64_t half_fs, double subpixel_step, int refine,
+                                        const float* fw, const double* var_fw, double* u_out,
+                                        double* err_out, const int32_t* span_hint,
+                                        void* stream) {
+  return pixel_map_search(sc, st, ref, u_in, di, dj, half_ss, half_fs, subpixel_step, refine, fw,
+                          var_fw, u_out, err_out, span_hint, stream);
+}
+
+extern "C" int pxst_tile_spans(const pxst_scan* sc, const double* u, int32_t* spans,
+                               void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(u && spans, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  PixArgs a{};
+  a.sc = *sc;
+  a.u = u;
+  a.tiles_x = static_cast<int>((cw + kTC - 1) / kTC);
+  const int tiles_y = static_cast<int>((rw + kTR - 1) / kTR);
+  PXST_REQUIRE(tiles_y <= kMaxGridY, "ROI too tall");
+  const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
+  Scratch geo;
+  if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
+  k_tile_geo<<<dim3((unsigned)a.tiles_x, (unsigned)tiles_y), kThreads, 0, s>>>(a, geo.as<TileGeo>());
+  PXST_CHECK_LAUNCH();
+  return tile_span_max_dev(geo.as<TileGeo>(), tiles, spans, s);
 }

@@ -56,6 +56,12 @@ __global__ void k_span_max(const TileGeo* __restrict__ geo, int64_t n, int* out)
 
 }  // namespace
 
+int tile_span_max_dev(const TileGeo* geo, int64_t n, int* out_dev, cudaStream_t s) {
+  k_span_max<<<1, 1024, 0, s>>>(geo, n, out_dev);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
 int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s) {
   Scratch d;
   if (int e = d.alloc(2 * sizeof(int), s)) return e;

@@ -5,10 +5,11 @@
 // (interp.py:114-122).  The splat is bound by the L2 atomic units, so here a
 // sample's four corners go out as two 16-byte float32 REDs (splat_grouped:
 // 2 RED lane-ops per sample instead of 8 float64 ones) into at most 32
-// float32 images, each covering a contiguous range of frame chunks; a fixed
-// order float64 fold sums the images.  Each float32 sum holds <= N/32 frames
-// of positive terms, so its relative error stays ~1e-7 (the 1e-5 bar of
-// SURVEY 8(c)); the summation order inside an image varies run to run.
+// float32 images, each covering a contiguous range of >= 24 frames (and
+// <= N/32 frames for long stacks); a fixed-order float64 fold sums the
+// images.  An image sums positive terms of a few dozen frames, so its
+// relative error stays ~1e-7-1e-6 (the 1e-5 bar of SURVEY 8(c)); the
+// summation order inside an image varies run to run.
 #include "common.cuh"
 
 namespace pxst {
@@ -18,6 +19,7 @@ constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;  // 4 rows x 32 fs pixels
 constexpr int kFB = 8;                 // frames per load batch (loads before REDs)
 constexpr int kTab = 256;              // frames per shared-memory frame table chunk
 constexpr int64_t kMaxImages = 32;     // float32 chunk images per splat
+constexpr int64_t kMinImageFrames = 24;  // frames summed per image, at least
 constexpr int64_t kImageBytes = int64_t(1) << 30;
 #ifndef PXST_K1_OCC
 #define PXST_K1_OCC 8
@@ -177,14 +179,16 @@ __global__ void k_splat_f64(double* acc_v, double* acc_w, int64_t os, int64_t of
 
 int check_scan(const pxst_scan* sc);
 
-int64_t chunk_images(int64_t blocks, int64_t n_cells, int* n_img) {
-  // <= kMaxImages float32 images (bounds each image's sum to blocks/kMaxImages
-  // frame blocks) and <= kImageBytes of scratch.
+int64_t chunk_images(int64_t blocks, int64_t frames_per_block, int64_t n_cells, int* n_img) {
+  // An image sums >= kMinImageFrames frames (fewer images: less zeroing and
+  // folding traffic) and, for long stacks, <= blocks / kMaxImages blocks;
+  // the scratch stays <= kImageBytes.
   int64_t cap = kImageBytes / (static_cast<int64_t>(sizeof(float4)) * (n_cells > 0 ? n_cells : 1));
   if (cap > kMaxImages) cap = kMaxImages;
   if (cap < 1) cap = 1;
-  const int64_t want = blocks < cap ? blocks : cap;
-  const int64_t bpi = (blocks + want - 1) / want;
+  int64_t bpi = (blocks + cap - 1) / cap;
+  const int64_t min_bpi = (kMinImageFrames + frames_per_block - 1) / frames_per_block;
+  if (bpi < min_bpi) bpi = min_bpi;
   *n_img = static_cast<int>((blocks + bpi - 1) / bpi);
   return bpi;
 }
@@ -219,7 +223,7 @@ int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
   g.z = static_cast<unsigned>((nk + fpz - 1) / fpz);
   const int64_t n = os * of;
   int n_img;
-  const int64_t bpi = chunk_images(n_batches, n, &n_img);
+  const int64_t bpi = chunk_images(n_batches, kFB, n, &n_img);
   Scratch acc;
   if (int e = acc.alloc(sizeof(float4) * n * n_img, s)) return e;
   PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(float4) * n * n_img, s));

@@ -109,6 +109,31 @@ class DeviceRef:
                    (int(origin[0]), int(origin[1])), to_device(fm64, np.float64, device))
 
 
+def _grid_rule(b) -> tuple[int, int, tuple[int, int]]:
+    """Object-grid origin and shape from the bbox values (recon.py:126-132)."""
+    u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = b
+    n0 = int(math.floor(u0min - dimax))
+    m0 = int(math.floor(u1min - djmax))
+    return n0, m0, (int(math.floor(u0max - dimin)) - n0 + 2,
+                    int(math.floor(u1max - djmin)) - m0 + 2)
+
+
+class GeometryFuture:
+    """Result of DeviceScan.geometry_async (pinned host values + event)."""
+
+    def __init__(self, host8, host2, event):
+        self._host8, self._host2, self._event = host8, host2, event
+
+    def bbox(self) -> tuple[int, int, tuple[int, int]]:
+        self._event.synchronize()
+        return _grid_rule(self._host8.tolist())
+
+    def spans_ptr(self) -> int:
+        """Host address of K2's span hint (int32[2]), valid after the event."""
+        self._event.synchronize()
+        return self._host2.data_ptr()
+
+
 class DeviceScan:
     """One scan + whitefield + mask + ROI resident on the current CUDA device."""
 
@@ -143,6 +168,7 @@ class DeviceScan:
                                self.good.data_ptr(), self.n_good, self.w64.data_ptr(),
                                self.w32.data_ptr(), self.work.data_ptr(), roi4)
         self.empty = self.n_work == 0 or self.n_good == 0 or r1 <= r0 or c1 <= c0
+        self._side = None            # side stream of geometry_async
         plane = self.ss * self.fs
         self.var_pm = torch.zeros(plane, dtype=torch.float64, device=dev)
         self.sigma2 = torch.zeros(plane, dtype=torch.float64, device=dev)
@@ -177,11 +203,39 @@ class DeviceScan:
         out = torch.empty(8, dtype=torch.float64, device=self.device)
         check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
                                  dj_t.data_ptr(), out.data_ptr(), stream_ptr()))
-        u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = to_host(out).tolist()
-        n0 = int(math.floor(u0min - dimax))
-        m0 = int(math.floor(u1min - djmax))
-        shape = (int(math.floor(u0max - dimin)) - n0 + 2, int(math.floor(u1max - djmin)) - m0 + 2)
-        return n0, m0, shape
+        return _grid_rule(to_host(out).tolist())
+
+    def geometry_async(self, u_t, di_t, dj_t) -> "GeometryFuture":
+        """Start the host-side geometry of an iteration on a side stream: the
+        object-grid bbox (recon.py:126-132) and K2's tile spans of u.  The
+        main stream is not blocked; reading the future waits only for these
+        two small reductions, so an iteration loop can fetch the next
+        iteration's geometry while the current error maps run."""
+        main = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        side = self._side
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
+        host8 = torch.empty(8, dtype=torch.float64, pin_memory=True)
+        host2 = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        with torch.cuda.stream(side):
+            dev8 = torch.empty(8, dtype=torch.float64, device=self.device)
+            dev2 = torch.empty(2, dtype=torch.int32, device=self.device)
+            sp = stream_ptr(side)
+            check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
+                                     dj_t.data_ptr(), dev8.data_ptr(), sp))
+            check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
+                                           dev2.data_ptr(), sp))
+            host8.copy_(dev8, non_blocking=True)
+            host2.copy_(dev2, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(side)
+        for t in (u_t, di_t, dj_t):
+            t.record_stream(side)
+        TRANSFER["d2h"] += 8 * 8 + 2 * 4
+        return GeometryFuture(host8, host2, done)
 
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
                      acc: torch.Tensor | None = None) -> torch.Tensor:
@@ -208,10 +262,10 @@ class DeviceScan:
         return DeviceRef(i_ref.view(os_, of), wsum.view(os_, of), fm.view(os_, of),
                          valid.view(os_, of), (int(origin[0]), int(origin[1])))
 
-    def object_map(self, u_t, di_t, dj_t) -> DeviceRef:
+    def object_map(self, u_t, di_t, dj_t, geom: "GeometryFuture | None" = None) -> DeviceRef:
         if self.empty:
             raise ValueError("make_reference: empty good pixel/frame set")  # recon.py:116-117
-        n0, m0, shape = self.bbox(u_t, di_t, dj_t)
+        n0, m0, shape = geom.bbox() if geom is not None else self.bbox(u_t, di_t, dj_t)
         acc = self.object_splat(u_t, di_t, dj_t, n0, m0, shape)
         return self.object_finish(acc, (n0, m0), shape)
 
@@ -227,7 +281,8 @@ class DeviceScan:
         return var_fw
 
     def pixel_map_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
-                         subpixel_grid=None, refine=True, fw_t=None):
+                         subpixel_grid=None, refine=True, fw_t=None,
+                         geom: "GeometryFuture | None" = None):
         u_out = torch.empty_like(u_t)
         err = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
         if self.empty:
@@ -236,11 +291,12 @@ class DeviceScan:
             return u_out, err.view(self.ss, self.fs)
         var_fw = self.frame_weight_stats(fw_t) if fw_t is not None else None
         c_ref = ref.struct()
-        check(self.lib.pxst_pixel_map_search(
+        hint = geom.spans_ptr() if geom is not None else None
+        check(self.lib.pxst_pixel_map_search_ex(
             ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
             u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), int(half_ss), int(half_fs),
             float(subpixel_grid or 0.0), int(bool(refine)), _ptr(fw_t), _ptr(var_fw),
-            u_out.data_ptr(), err.data_ptr(), stream_ptr()))
+            u_out.data_ptr(), err.data_ptr(), hint, stream_ptr()))
         return u_out, err.view(self.ss, self.fs)
 
     # ------------------------------------------------------- K3 translations
@@ -297,10 +353,13 @@ class DeviceScan:
 
     # ---------------------------------------------------------- K4 error maps
     def error_maps(self, ref: DeviceRef, u_t, di_t, dj_t):
-        per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)
-        per_pixel = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
-        plane = torch.zeros(ref.fm.numel(), dtype=torch.float64, device=self.device)
-        total = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # pxst_error_maps zeroes per_frame / per_pixel / total and writes every
+        # plane cell itself
+        alloc = torch.zeros if self.empty else torch.empty
+        per_frame = alloc(self.n_frames, dtype=torch.float64, device=self.device)
+        per_pixel = alloc(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        plane = alloc(ref.fm.numel(), dtype=torch.float64, device=self.device)
+        total = alloc(1, dtype=torch.float64, device=self.device)
         if not self.empty:
             c_ref = ref.struct()
             check(self.lib.pxst_error_maps(

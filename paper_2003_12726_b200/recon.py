@@ -251,21 +251,25 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         raise ValueError("make_reference: empty good pixel/frame set")
     u_t = ds.upload_u(u.u)
     di_t, dj_t = ds.upload_t(t.di, t.dj)
-    dref = ds.object_map(u_t, di_t, dj_t)
+    gfut = ds.geometry_async(u_t, di_t, dj_t)
+    dref = ds.object_map(u_t, di_t, dj_t, geom=gfut)
     history = [_metrics(*ds.error_maps(dref, u_t, di_t, dj_t))]
     if progress_cb:
         progress_cb(0.0, f"initial error {history[0].total:.6g}")
     for i in range(max_iters):
         st = schedule[i]
-        dref = ds.object_map(u_t, di_t, dj_t)
+        # make_reference(u, t) of this iteration is the initial one (i = 0) or
+        # comes from the same (u, t) as the previous error maps
+        dref = ds.object_map(u_t, di_t, dj_t, geom=gfut)
         u_t, _ = ds.pixel_map_search(dref, u_t, di_t, dj_t, st.window.half_ss,
                                      st.window.half_fs, st.window.subpixel_grid,
-                                     st.options.quadratic_refinement)
+                                     st.options.quadratic_refinement, geom=gfut)
         ds.regularise(u_t, st.options)
         if st.update_translations:
             tw = st.translation_window
             di_t, dj_t = ds.translation_search(dref, u_t, di_t, dj_t, tw.half_ss, tw.half_fs,
                                                tw.subpixel_grid)
+        gfut = ds.geometry_async(u_t, di_t, dj_t)       # next iteration's, overlaps K4
         history.append(_metrics(*ds.error_maps(dref, u_t, di_t, dj_t)))
         if progress_cb:
             progress_cb((i + 1) / max_iters, f"iter {i + 1} error {history[-1].total:.6g}")
