@@ -64,8 +64,21 @@ def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     """Device -> host copy (synchronising)."""
-    TRANSFER["d2h"] += t.numel() * t.element_size()
-    return t.detach().cpu().numpy()
+    return to_host_many(t)[0]
+
+
+def to_host_many(*ts: torch.Tensor) -> list[np.ndarray]:
+    """Device -> host copies of several tensors through pinned buffers, one
+    stream synchronisation for all of them."""
+    outs = []
+    for t in ts:
+        TRANSFER["d2h"] += t.numel() * t.element_size()
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t.detach(), non_blocking=True)
+        outs.append(h)
+    if ts:
+        torch.cuda.current_stream(ts[0].device).synchronize()
+    return [h.numpy() for h in outs]
 
 
 def clip_roi(roi, shape) -> tuple[int, int, int, int]:
@@ -405,8 +418,7 @@ class _ScanCache:
     The reference treats its dataclasses as immutable value objects
     (data_model.py:13: "construct once, then share read-only"); the cache
     relies on that: an array mutated in place after a call must be passed as
-    a new array, or the cache cleared with :func:`clear_cache`.  W, mask and
-    good_frames (small) are additionally checked by content.
+    a new array, or the cache cleared with :func:`clear_cache`.
     """
 
     def __init__(self, max_entries: int = 2):
@@ -420,15 +432,20 @@ class _ScanCache:
         return (id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str, a.strides)
 
     @staticmethod
-    def _digest(a):
-        a = np.ascontiguousarray(a)
-        return hash(a.tobytes())
+    def _ref(a):
+        try:
+            return weakref.ref(a)
+        except TypeError:
+            return lambda: a
 
     def get(self, scan, w, m, roi) -> DeviceScan:
         frames = scan.frames
-        key = (self._ident(frames), self._digest(scan.good_frames), self._digest(w.w),
-               self._digest(m.mask), None if roi is None else clip_roi(roi, scan.shape))
+        arrays = (frames, scan.good_frames, w.w, m.mask)
+        key = tuple(self._ident(a) for a in arrays) + (
+            None if roi is None else clip_roi(roi, scan.shape),)
         if self.enabled:
+            # every keyed array is held by a weak reference: an identity match
+            # with all of them alive cannot be a recycled address
             for k, refs, ds in self.entries:
                 if k == key and all(r() is not None for r in refs):
                     return ds
@@ -441,12 +458,7 @@ class _ScanCache:
                     break
         ds = DeviceScan(frames, scan.good_frames, w.w, m.mask, roi, frames_dev=frames_dev)
         if self.enabled:
-            refs = []
-            try:
-                refs.append(weakref.ref(frames))
-            except TypeError:
-                refs.append(lambda: frames)
-            self.entries.append((key, refs, ds))
+            self.entries.append((key, [self._ref(a) for a in arrays], ds))
             del self.entries[:-self.max_entries]
         return ds
 

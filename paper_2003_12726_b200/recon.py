@@ -31,7 +31,7 @@ from .data_model import (
     ScanData,
     Whitefield,
 )
-from .engine import SCAN_CACHE, DeviceRef, DeviceScan, to_host
+from .engine import SCAN_CACHE, DeviceRef, DeviceScan, to_host, to_host_many
 
 # Relative floor applied to per-pixel intensity variances (recon.py:34).
 VAR_EPS_REL = 1e-8
@@ -133,7 +133,8 @@ def _host(t: torch.Tensor) -> np.ndarray:
 
 def _ref_image(dref: DeviceRef, geom) -> ReferenceImage:
     du, dv = (geom.du, geom.dv) if geom is not None else (1.0, 1.0)
-    out = ReferenceImage(i_ref=_host(dref.i_ref), wsum=_host(dref.wsum),
+    i_ref, wsum = to_host_many(dref.i_ref, dref.wsum)
+    out = ReferenceImage(i_ref=i_ref, wsum=wsum,
                          origin=(int(dref.origin[0]), int(dref.origin[1])), du=du, dv=dv)
     _remember(out, dref)
     return out
@@ -180,7 +181,8 @@ def update_pixel_map(scan: ScanData, w: Whitefield, m: PixelMask, ref: Reference
     u_out, err = ds.pixel_map_search(dref, u_t, di_t, dj_t, win.half_ss, win.half_fs,
                                      win.subpixel_grid, opts.quadratic_refinement, fw_t)
     ds.regularise(u_out, opts)                           # recon.py:298-311
-    return PixelMap(_host(u_out)), _host(err)
+    u_h, err_h = to_host_many(u_out, err)
+    return PixelMap(u_h), err_h
 
 
 def update_translations(scan: ScanData, w: Whitefield, m: PixelMask, ref: ReferenceImage,
@@ -193,13 +195,14 @@ def update_translations(scan: ScanData, w: Whitefield, m: PixelMask, ref: Refere
     dref = _device_ref(ref, ds)
     di_o, dj_o = ds.translation_search(dref, u_t, di_t, dj_t, win.half_ss, win.half_fs,
                                        win.subpixel_grid)
-    return PixelTranslations(di=_host(di_o), dj=_host(dj_o))
+    di_h, dj_h = to_host_many(di_o, dj_o)
+    return PixelTranslations(di=di_h, dj=dj_h)
 
 
 def _metrics(total, per_frame, per_pixel, plane, variance) -> ErrorMetrics:
-    return ErrorMetrics(total=float(total.item()), per_frame=_host(per_frame),
-                        per_pixel=_host(per_pixel), reference_plane=_host(plane),
-                        variance=_host(variance).copy())
+    t, pf, pp, pl, var = to_host_many(total, per_frame, per_pixel, plane, variance)
+    return ErrorMetrics(total=float(t[0]), per_frame=pf, per_pixel=pp, reference_plane=pl,
+                        variance=var)
 
 
 def calc_error(scan: ScanData, w: Whitefield, m: PixelMask, ref: ReferenceImage, u: PixelMap,
