@@ -250,16 +250,17 @@ def run_ours(args, rank, world, local):
 
     def step(ev=None):
         if state["it"] == 0:
-            state.update(u=u_t, di=di_t, dj=dj_t, geom=None)
+            state.update(u=u_t, di=di_t, dj=dj_t, geom=None, dref=None)
         u, di, dj = state["u"], state["di"], state["dj"]
-        nxt = None
+        nxt = nref = None
         if sharded is not None:
             u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev)
         else:
             # the iteration's grid bbox and K2 tile spans were fetched on a side
-            # stream while the previous iteration's error maps ran
+            # stream while the previous iteration's error maps ran, and its
+            # object was formed in the same pass over the stack as those maps
             geom = state["geom"] or ds.geometry_async(u, di, dj)
-            dref = ds.object_map(u, di, dj, geom=geom)
+            dref = state["dref"].resolve() if state["dref"] else ds.object_map(u, di, dj, geom=geom)
             u_new = u
             if cfg.update_pixel_map:
                 if ev:
@@ -277,9 +278,12 @@ def run_ours(args, rank, world, local):
                 if ev and not cfg.update_pixel_map:
                     ev[1].record(stream)
             nxt = ds.geometry_async(u_new, di_new, dj_new)
-            ds.error_maps(dref, u_new, di_new, dj_new)
+            if state["it"] + 1 < cfg.iters:        # the sequence continues: fuse K4 + next K1
+                _, nref = ds.error_maps_and_next_object(dref, u_new, di_new, dj_new, nxt)
+            else:
+                ds.error_maps(dref, u_new, di_new, dj_new)
         state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new,
-                     geom=nxt)
+                     geom=nxt, dref=nref)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 

@@ -167,6 +167,27 @@ int pxst_error_maps(const pxst_scan* scan, const pxst_stats* st, const pxst_ref*
                     const double* u, const double* di, const double* dj, double* per_frame,
                     double* per_pixel, double* ref_plane, double* total, void* stream);
 
+/* K4 fused with the NEXT iteration's K1 splat: calc_error(ref, u, t) and
+ * make_reference(u, t) read the same samples at the same positions
+ * u - delta (recon.py:511-516 calls them back to back), so one pass over the
+ * stack produces the error maps of `ref` and adds the next object's
+ * numerator / denominator into num / den as pxst_object_splat would.  The
+ * next grid (n0, m0, os, of) is read from DEVICE memory `grid` (e.g. written
+ * by pxst_bbox + pxst_grid_rule on a side stream), so the call never waits
+ * for the host; num / den hold `capacity` cells (the grid is laid out densely
+ * in the first os*of) and a grid with os*of > capacity is not splatted -- the
+ * caller, who learns the grid later, then forms the object separately.
+ * Finish the next object with pxst_object_finish. */
+int pxst_error_maps_splat(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                          const double* u, const double* di, const double* dj,
+                          double* per_frame, double* per_pixel, double* ref_plane, double* total,
+                          const int64_t* grid, int64_t capacity, double* num, double* den,
+                          void* stream);
+
+/* Grid rule of recon.py:126-132 on the device: grid[4] = (n0, m0, os, of)
+ * from the 8 bbox values of pxst_bbox (both device pointers). */
+int pxst_grid_rule(const double* bbox, int64_t* grid, void* stream);
+
 /* K4 without the final normalisation, for detector-row shards: per_frame
  * [n_frames] = this ROI's per-frame sums, per_pixel [ss,fs] (this ROI only),
  * and the reference-plane numerator/denominator ADDED into plane_num /

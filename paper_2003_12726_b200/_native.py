@@ -70,6 +70,11 @@ _SIGS = {
     "pxst_error_maps": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p]),
+    "pxst_error_maps_splat": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                      c_void_p]),
+    "pxst_grid_rule": (c_int, [c_void_p, c_void_p, c_void_p]),
     "pxst_error_partials": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p]),

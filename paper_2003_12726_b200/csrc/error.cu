@@ -36,6 +36,13 @@ struct ErrArgs {
   float4* img;         // grouped reference-plane images [n_img][os*of]
   int bpi;             // reduction batches (kFB frames) per image
   int64_t frames_per_z;
+  // fused next-object splat (pxst_error_maps_splat): K1 of the next
+  // iteration reads the same samples at the same positions u - delta,
+  // relative to its own grid, read from device memory (n0, m0, os, of)
+  float4* img_b;       // grouped object images [n_img_b][cap_b], NULL = not fused
+  int bpi_b;
+  const int64_t* grid_b;
+  int64_t cap_b;       // cells per image; a grid with os*of > cap_b is not splatted
 };
 
 // g[r][c] = (v(r, c), v(r+1, c)) with v = the float64 masked reference where
@@ -84,6 +91,7 @@ __device__ __forceinline__ double warp_sum8(double (&v)[8], int lane) {
 // One thread per work pixel over the frame slice blockIdx.z: per-pixel slice
 // sums, per-(frame, warp) partials, reference-plane splat.  No barrier inside
 // the frame loop (the frame table is refreshed every kTab frames).
+template <bool FUSE>
 __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, double* pix_part,
                                                        double* part, int64_t n_warps) {
   __shared__ double t_di[kTab], t_dj[kTab];
@@ -99,6 +107,16 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
   const double W64 = live ? a.sc.w64[p] : 0.0;
   const double s2 = live ? a.sigma2[p] : 1.0;
+  const double W2 = W64 * W64;                               // recon.py:136
+  int64_t n0b = 0, m0b = 0, osb = 1, ofb = 1;
+  if (FUSE) {
+    n0b = a.grid_b[0];
+    m0b = a.grid_b[1];
+    osb = a.grid_b[2];
+    ofb = a.grid_b[3];
+  }
+  const bool splat_b = FUSE && osb > 0 && ofb > 0 && osb * ofb <= a.cap_b;
+  const double osb1 = static_cast<double>(osb - 1), ofb1 = static_cast<double>(ofb - 1);
   const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
   const int64_t n_o = a.os * a.of;
   const int64_t k_begin = (int64_t)blockIdx.z * a.frames_per_z;
@@ -116,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
     __syncthreads();
     for (int b0 = 0; b0 < nt; b0 += kFB) {
       float4* img = a.img + ((kc + b0) / kFB / a.bpi) * n_o;
+      float4* img_b = FUSE ? a.img_b + ((kc + b0) / kFB / a.bpi_b) * a.cap_b : nullptr;
       double e[kFB];
 #pragma unroll
       for (int h = 0; h < kFB; h += kLB) {
@@ -165,6 +184,15 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
           pix += eps;
           if (inb[b])                                   // recon.py:425
             splat_grouped(img, a00[b], fx, fy, eps, 1.0);
+          if (FUSE && splat_b && live && b0 + h + b < nt) {   // next K1 (recon.py:135-138)
+            const int t = b0 + h + b;
+            const double xb = u0 - t_di[t] - static_cast<double>(n0b);
+            const double yb = u1 - t_dj[t] - static_cast<double>(m0b);
+            if (xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1) {   // interp.py:103-107
+              const Split sx = split(xb), sy = split(yb);
+              splat_grouped(img_b, (int64_t)sx.i * ofb + sy.i, sx.f, sy.f, (I / W64) * W2, W2);
+            }
+          }
         }
       }
       const double sum = warp_sum8(e, lane);
@@ -236,9 +264,56 @@ namespace {
 // One pass: per_frame (zeroed, then good frames filled), per_pixel (zeroed,
 // then this scan's ROI filled), reference-plane accumulators added into
 // num/den (caller-initialised), optional total.
+// The next iteration's object grid for the fused splat (its num/den are
+// added into, like pxst_object_splat).
+struct NextObject {
+  const int64_t* grid;   // device (n0, m0, os, of)
+  int64_t capacity;      // cells of num / den and of each image
+  double* num;
+  double* den;
+};
+
+// Grid rule of recon.py:126-132 on device: grid = (n0, m0, os, of) from the
+// bbox values of pxst_bbox.
+__global__ void k_grid_rule(const double* __restrict__ b, int64_t* __restrict__ grid) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int64_t n0 = static_cast<int64_t>(floor(b[0] - b[5]));
+    const int64_t m0 = static_cast<int64_t>(floor(b[2] - b[7]));
+    grid[0] = n0;
+    grid[1] = m0;
+    grid[2] = static_cast<int64_t>(floor(b[1] - b[4])) - n0 + 2;
+    grid[3] = static_cast<int64_t>(floor(b[3] - b[6])) - m0 + 2;
+  }
+}
+
+// Fold of grouped images whose grid lives in device memory (image stride cap).
+__global__ void k_group_fold_dev(const float4* __restrict__ img, int n_img, int64_t cap,
+                                 const int64_t* __restrict__ grid, double* __restrict__ num,
+                                 double* __restrict__ den) {
+  const int64_t os = grid[2], of = grid[3], n = os * of;
+  if (!(os > 0 && of > 0 && n <= cap)) return;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double x = 0.0, y = 0.0;
+    const bool up = q >= of;
+    for (int z = 0; z < n_img; ++z) {
+      const float4 g = __ldg(img + (int64_t)z * cap + q);
+      x += g.x;
+      y += g.y;
+      if (up) {
+        const float4 h = __ldg(img + (int64_t)z * cap + q - of);
+        x += h.z;
+        y += h.w;
+      }
+    }
+    num[q] += x;
+    den[q] += y;
+  }
+}
+
 int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, const double* u,
                const double* di, const double* dj, double* per_frame, double* per_pixel,
-               double* num, double* den, double* total, cudaStream_t s) {
+               double* num, double* den, double* total, const NextObject* nx, cudaStream_t s) {
   const int64_t plane = sc->ss * sc->fs;
   PXST_CHECK_CUDA(cudaMemsetAsync(per_frame, 0, sizeof(double) * sc->n_frames, s));
   PXST_CHECK_CUDA(cudaMemsetAsync(per_pixel, 0, sizeof(double) * plane, s));
@@ -253,7 +328,8 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
   int dev = 0, sms = 148, per_sm = 1;
   PXST_CHECK_CUDA(cudaGetDevice(&dev));
   PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  PXST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_err_pass, kThreads, 0));
+  PXST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, nx ? k_err_pass<true> : k_err_pass<false>, kThreads, 0));
   const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
   const int64_t n_batches = (sc->n_good + kFB - 1) / kFB;
   int64_t n_z = (3 * resident + (int64_t)g.x * g.y - 1) / ((int64_t)g.x * g.y);
@@ -275,11 +351,40 @@ int error_pass(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref, c
   k_group_ref<<<grid_1d(n_o, 256), 256, 0, s>>>(ref->fm64, ref->fm, ref->valid, ref->os, ref->of,
                                                 grp.as<double2>());
   PXST_CHECK_LAUNCH();
-  ErrArgs a{*sc,     u,       di,         dj,
-            grp.as<double2>(), ref->os, ref->of, ref->n0,
-            ref->m0, st->sigma2, img.as<float4>(), (int)bpi, fpz};
-  k_err_pass<<<g, kThreads, 0, s>>>(a, pix_part, part.as<double>(), n_warps);
+  ErrArgs a{};
+  a.sc = *sc;
+  a.u = u;
+  a.di = di;
+  a.dj = dj;
+  a.grp = grp.as<double2>();
+  a.os = ref->os;
+  a.of = ref->of;
+  a.n0 = ref->n0;
+  a.m0 = ref->m0;
+  a.sigma2 = st->sigma2;
+  a.img = img.as<float4>();
+  a.bpi = static_cast<int>(bpi);
+  a.frames_per_z = fpz;
+  Scratch img_b;
+  int n_img_b = 0;
+  if (nx) {
+    const int64_t n_b = nx->capacity;
+    a.bpi_b = static_cast<int>(chunk_images(n_batches, kFB, n_b, &n_img_b));
+    if (int e = img_b.alloc(sizeof(float4) * n_b * n_img_b, s)) return e;
+    PXST_CHECK_CUDA(cudaMemsetAsync(img_b.p, 0, sizeof(float4) * n_b * n_img_b, s));
+    a.img_b = img_b.as<float4>();
+    a.grid_b = nx->grid;
+    a.cap_b = n_b;
+    k_err_pass<true><<<g, kThreads, 0, s>>>(a, pix_part, part.as<double>(), n_warps);
+  } else {
+    k_err_pass<false><<<g, kThreads, 0, s>>>(a, pix_part, part.as<double>(), n_warps);
+  }
   PXST_CHECK_LAUNCH();
+  if (nx) {
+    k_group_fold_dev<<<grid_1d(nx->capacity, 256), 256, 0, s>>>(
+        img_b.as<float4>(), n_img_b, nx->capacity, nx->grid, nx->num, nx->den);
+    PXST_CHECK_LAUNCH();
+  }
   k_err_pixels<<<grid_1d(rw * cw, 256), 256, 0, s>>>(*sc, pix_part, (int)n_z, per_pixel);
   PXST_CHECK_LAUNCH();
   k_err_frames<<<(unsigned)sc->n_good, 256, 0, s>>>(*sc, part.as<double>(), n_warps, per_frame,
@@ -314,7 +419,7 @@ extern "C" int pxst_error_maps(const pxst_scan* sc, const pxst_stats* st, const 
   if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
   PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
   if (int e = error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, acc.as<double>(),
-                         acc.as<double>() + n_o, total, s))
+                         acc.as<double>() + n_o, total, nullptr, s))
     return e;
   return launch_object_finish(acc.as<double>(), acc.as<double>() + n_o, n_o, ref_plane, nullptr,
                               nullptr, nullptr, s);
@@ -328,5 +433,35 @@ extern "C" int pxst_error_partials(const pxst_scan* sc, const pxst_stats* st,
   PXST_REQUIRE(u && di && dj && per_frame && per_pixel && plane_num && plane_den,
                "NULL pointer");
   return error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, plane_num, plane_den, nullptr,
-                    as_stream(stream));
+                    nullptr, as_stream(stream));
+}
+
+extern "C" int pxst_grid_rule(const double* bbox, int64_t* grid, void* stream) {
+  PXST_REQUIRE(bbox && grid, "NULL pointer");
+  k_grid_rule<<<1, 32, 0, as_stream(stream)>>>(bbox, grid);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+extern "C" int pxst_error_maps_splat(const pxst_scan* sc, const pxst_stats* st,
+                                     const pxst_ref* ref, const double* u, const double* di,
+                                     const double* dj, double* per_frame, double* per_pixel,
+                                     double* ref_plane, double* total, const int64_t* grid,
+                                     int64_t capacity, double* num, double* den, void* stream) {
+  if (int e = check_err_args(sc, st, ref)) return e;
+  PXST_REQUIRE(u && di && dj && per_frame && per_pixel && ref_plane && total && grid && num &&
+                   den,
+               "NULL pointer");
+  PXST_REQUIRE(capacity > 0 && capacity < (int64_t(1) << 40), "bad capacity");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n_o = ref->os * ref->of;
+  Scratch acc;
+  if (int e = acc.alloc(sizeof(double) * 2 * n_o, s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2 * n_o, s));
+  const NextObject nx{grid, capacity, num, den};
+  if (int e = error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, acc.as<double>(),
+                         acc.as<double>() + n_o, total, &nx, s))
+    return e;
+  return launch_object_finish(acc.as<double>(), acc.as<double>() + n_o, n_o, ref_plane, nullptr,
+                              nullptr, nullptr, s);
 }

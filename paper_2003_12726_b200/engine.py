@@ -132,10 +132,17 @@ def _grid_rule(b) -> tuple[int, int, tuple[int, int]]:
 
 
 class GeometryFuture:
-    """Result of DeviceScan.geometry_async (pinned host values + event)."""
+    """Result of DeviceScan.geometry_async (pinned host values + event; the
+    grid (n0, m0, os, of) also stays on the device for kernels that read it
+    without a host round trip)."""
 
-    def __init__(self, host8, host2, event):
+    def __init__(self, host8, host2, event, grid_dev):
         self._host8, self._host2, self._event = host8, host2, event
+        self.grid_dev = grid_dev
+
+    def gpu_wait(self, stream=None):
+        """Make `stream` (default: current) wait for the geometry on the GPU."""
+        (stream or torch.cuda.current_stream()).wait_event(self._event)
 
     def bbox(self) -> tuple[int, int, tuple[int, int]]:
         self._event.synchronize()
@@ -145,6 +152,22 @@ class GeometryFuture:
         """Host address of K2's span hint (int32[2]), valid after the event."""
         self._event.synchronize()
         return self._host2.data_ptr()
+
+
+class PendingObject:
+    """Next-iteration object accumulated by error_maps_and_next_object;
+    resolve() finishes it once the grid is known on the host (normally long
+    after the fact), or forms it afresh if the grid outgrew the capacity."""
+
+    def __init__(self, ds, acc, cap, geom, inputs):
+        self.ds, self.acc, self.cap, self.geom, self.inputs = ds, acc, cap, geom, inputs
+
+    def resolve(self) -> DeviceRef:
+        n0, m0, shape = self.geom.bbox()
+        n = shape[0] * shape[1]
+        if n > self.cap:
+            return self.ds.object_map(*self.inputs, geom=self.geom)
+        return self.ds.object_finish(self.acc[:, :n], (n0, m0), shape)
 
 
 class DeviceScan:
@@ -236,9 +259,11 @@ class DeviceScan:
         with torch.cuda.stream(side):
             dev8 = torch.empty(8, dtype=torch.float64, device=self.device)
             dev2 = torch.empty(2, dtype=torch.int32, device=self.device)
+            grid = torch.empty(4, dtype=torch.int64, device=self.device)
             sp = stream_ptr(side)
             check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
                                      dj_t.data_ptr(), dev8.data_ptr(), sp))
+            check(self.lib.pxst_grid_rule(dev8.data_ptr(), grid.data_ptr(), sp))
             check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
                                            dev2.data_ptr(), sp))
             host8.copy_(dev8, non_blocking=True)
@@ -248,7 +273,7 @@ class DeviceScan:
         for t in (u_t, di_t, dj_t):
             t.record_stream(side)
         TRANSFER["d2h"] += 8 * 8 + 2 * 4
-        return GeometryFuture(host8, host2, done)
+        return GeometryFuture(host8, host2, done, grid)
 
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
                      acc: torch.Tensor | None = None) -> torch.Tensor:
@@ -381,6 +406,31 @@ class DeviceScan:
                 per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), stream_ptr()))
         return (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
                 self.sigma2.view(self.ss, self.fs))
+
+    def error_maps_and_next_object(self, ref: DeviceRef, u_t, di_t, dj_t,
+                                   geom: "GeometryFuture", margin: int = 32):
+        """K4 of (ref, u, t) fused with the next iteration's object formation
+        on (u, t) (recon.py:511-516), without any host wait: the next grid is
+        read on the device from `geom` (= geometry_async(u, di, dj)), and the
+        accumulators are sized from the current grid plus `margin` cells per
+        side.  Returns the error-map tensors and a PendingObject."""
+        os_, of = ref.shape
+        cap = (os_ + 2 * margin) * (of + 2 * margin)
+        acc = torch.zeros((2, cap), dtype=torch.float64, device=self.device)
+        per_frame = torch.empty(self.n_frames, dtype=torch.float64, device=self.device)
+        per_pixel = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
+        plane = torch.empty(ref.fm.numel(), dtype=torch.float64, device=self.device)
+        total = torch.empty(1, dtype=torch.float64, device=self.device)
+        geom.gpu_wait()
+        c_ref = ref.struct()
+        check(self.lib.pxst_error_maps_splat(
+            ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+            u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
+            per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), geom.grid_dev.data_ptr(),
+            cap, acc[0].data_ptr(), acc[1].data_ptr(), stream_ptr()))
+        metrics = (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
+                   self.sigma2.view(self.ss, self.fs))
+        return metrics, PendingObject(self, acc, cap, geom, (u_t, di_t, dj_t))
 
     # ------------------------------------- 8(f) pixel-map regularisation
     def smooth_displacement(self, u_t, sigma: float):

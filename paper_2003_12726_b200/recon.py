@@ -259,11 +259,15 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
     history = [_metrics(*ds.error_maps(dref, u_t, di_t, dj_t))]
     if progress_cb:
         progress_cb(0.0, f"initial error {history[0].total:.6g}")
+    # make_reference(u, t) at the top of every iteration sees the (u, t) of the
+    # error maps just before it (recon.py:504-516): iteration 0 reuses the
+    # initial object, later ones get it from the same pass over the stack as
+    # those error maps (pxst_error_maps_splat)
+    nref = None
     for i in range(max_iters):
         st = schedule[i]
-        # make_reference(u, t) of this iteration is the initial one (i = 0) or
-        # comes from the same (u, t) as the previous error maps
-        dref = ds.object_map(u_t, di_t, dj_t, geom=gfut)
+        if nref is not None:
+            dref = nref.resolve()
         u_t, _ = ds.pixel_map_search(dref, u_t, di_t, dj_t, st.window.half_ss,
                                      st.window.half_fs, st.window.subpixel_grid,
                                      st.options.quadratic_refinement, geom=gfut)
@@ -273,7 +277,11 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
             di_t, dj_t = ds.translation_search(dref, u_t, di_t, dj_t, tw.half_ss, tw.half_fs,
                                                tw.subpixel_grid)
         gfut = ds.geometry_async(u_t, di_t, dj_t)       # next iteration's, overlaps K4
-        history.append(_metrics(*ds.error_maps(dref, u_t, di_t, dj_t)))
+        if i + 1 < max_iters:
+            metrics, nref = ds.error_maps_and_next_object(dref, u_t, di_t, dj_t, gfut)
+        else:
+            metrics = ds.error_maps(dref, u_t, di_t, dj_t)
+        history.append(_metrics(*metrics))
         if progress_cb:
             progress_cb((i + 1) / max_iters, f"iter {i + 1} error {history[-1].total:.6g}")
         prev, curr = history[-2].total, history[-1].total
