@@ -82,9 +82,27 @@ class ShardedIteration:
         self.max_frames = max(hi - lo for lo, hi in self.frames)
 
     # ----------------------------------------------------------- collectives
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        """gloo groups over device tensors (multi-rank tests on one GPU) go
+        through host copies; NCCL takes device tensors directly."""
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def _all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        if self._host_staged(t):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return t
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
+
+    def _all_gather(self, out: torch.Tensor, buf: torch.Tensor) -> None:
+        if self._host_staged(buf):
+            h = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(h, buf.cpu(), group=self.group)
+            out.copy_(h)
+            return
+        dist.all_gather_into_tensor(out, buf, group=self.group)
 
     def _gather_rows(self, u_local: torch.Tensor) -> torch.Tensor:
         """Assemble the full u from each rank's band (exact)."""
@@ -94,7 +112,7 @@ class ShardedIteration:
         buf[:, : hi - lo] = u_local[:, lo:hi]
         out = torch.empty((self.world * 2, self.max_rows, fs), dtype=u_local.dtype,
                           device=u_local.device)
-        dist.all_gather_into_tensor(out, buf.contiguous(), group=self.group)
+        self._all_gather(out, buf.contiguous())
         out = out.view(self.world, 2, self.max_rows, fs)
         u = u_local.clone()
         for k, (a, b) in enumerate(self.rows):
@@ -110,7 +128,7 @@ class ShardedIteration:
         buf[0, : hi - lo] = di[idx]
         buf[1, : hi - lo] = dj[idx]
         out = torch.empty((self.world * 2, self.max_frames), dtype=di.dtype, device=di.device)
-        dist.all_gather_into_tensor(out, buf, group=self.group)
+        self._all_gather(out, buf)
         out = out.view(self.world, 2, self.max_frames)
         di_o, dj_o = di.clone(), dj.clone()
         for k, (a, b) in enumerate(self.frames):
