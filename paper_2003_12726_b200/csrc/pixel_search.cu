@@ -68,6 +68,7 @@ struct PixArgs {
   float* partial;            // [n_chunks][ka*kb][nq]
   unsigned long long* slow_list;  // (pixel << 20 | chunk) pairs owning skipped samples
   unsigned* slow_n;
+  unsigned long long* dbg;   // PXST_DEBUG: skipped-sample count (nullable)
 };
 
 // Box: 8 tile rows (|du/dx| up to ~1.2 plus noise) + window; columns: 16
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
+      if (a.dbg && lane == 0) atomicAdd(a.dbg, (unsigned long long)__popc(mask));
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -522,10 +524,8 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
 
   Scratch offs;
   if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
-  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.p, oa.data(), sizeof(double) * na,
-                                  cudaMemcpyHostToDevice, s));
-  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.as<double>() + na, ob.data(), sizeof(double) * nb,
-                                  cudaMemcpyHostToDevice, s));
+  if (int e = fill_offsets(offs.as<double>(), na, subpixel_step, s)) return e;
+  if (int e = fill_offsets(offs.as<double>() + na, nb, subpixel_step, s)) return e;
   const double* d_oa = offs.as<double>();
   const double* d_ob = d_oa + na;
   const int refine_ok = refine && subpixel_step == 0.0 && na >= 3 && nb >= 3;   // recon.py:273
@@ -604,6 +604,12 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, sizeof(unsigned), s));
     a.slow_list = list;
     a.slow_n = list_n;
+    Scratch dbg;
+    if (getenv("PXST_DEBUG")) {
+      if (int e = dbg.alloc(sizeof(unsigned long long), s)) return e;
+      PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(unsigned long long), s));
+      a.dbg = dbg.as<unsigned long long>();
+    }
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
     fn<<<gf, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
@@ -611,10 +617,12 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;
+      unsigned long long hs = 0;
       PXST_CHECK_CUDA(cudaMemcpyAsync(&h, list_n, sizeof(h), cudaMemcpyDeviceToHost, s));
+      PXST_CHECK_CUDA(cudaMemcpyAsync(&hs, a.dbg, sizeof(hs), cudaMemcpyDeviceToHost, s));
       PXST_CHECK_CUDA(cudaStreamSynchronize(s));
       fprintf(stderr, "[pxst] K2 %dx%d: %lld pixels x %d chunks, %u (pixel, chunk) pairs own "
-              "slow samples\n", na, nb, (long long)a.nq, a.n_chunks, h);
+              "%llu slow samples\n", na, nb, (long long)a.nq, a.n_chunks, h, hs);
     }
     k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
                                                   refine_ok, u_out, err_out);

@@ -345,6 +345,9 @@ __device__ __forceinline__ TileGeo make_tile_geo(double mn0, double mx0, double 
 // Host: largest spans over tiles with work pixels -> out[2] (synchronises).
 // Same reduction left on the device: out_dev[2] (no synchronisation).
 int tile_span_max_dev(const TileGeo* geo, int64_t n, int* out_dev, cudaStream_t s);
+// out[i] = window_offsets(half, step)[i] for the n = 2 kh + 1 offsets, written
+// on the device (no host copy).
+int fill_offsets(double* out, int n, double step, cudaStream_t s);
 int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s);
 
 __host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }

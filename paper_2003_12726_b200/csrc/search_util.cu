@@ -99,6 +99,22 @@ int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s) {
   return PXST_OK;
 }
 
+__global__ void k_fill_offsets(double* __restrict__ out, int n, int64_t kh, double step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double k = static_cast<double>(static_cast<int64_t>(i) - kh);
+    out[i] = step > 0.0 ? step * k : k;          // window_offsets, on the device
+  }
+}
+
+int fill_offsets(double* out, int n, double step, cudaStream_t s) {
+  // A device fill instead of a pageable host->device copy, which would
+  // synchronise the stream before it starts.
+  k_fill_offsets<<<(n + 127) / 128, 128, 0, s>>>(out, n, (n - 1) / 2, step);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
 std::vector<double> window_offsets(int64_t half, double step) {
   std::vector<double> o;
   if (step <= 0.0) {

@@ -511,10 +511,8 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
 
   Scratch offs;
   if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
-  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.p, oa.data(), sizeof(double) * na,
-                                  cudaMemcpyHostToDevice, s));
-  PXST_CHECK_CUDA(cudaMemcpyAsync(offs.as<double>() + na, ob.data(), sizeof(double) * nb,
-                                  cudaMemcpyHostToDevice, s));
+  if (int e = fill_offsets(offs.as<double>(), na, subpixel_step, s)) return e;
+  if (int e = fill_offsets(offs.as<double>() + na, nb, subpixel_step, s)) return e;
   const double* d_oa = offs.as<double>();
   const double* d_ob = d_oa + na;
 
