@@ -228,22 +228,27 @@ typedef struct pxst_cg_info {
 } pxst_cg_info;
 
 /* Least-squares potential of a gradient field on a mask
- * (integration.py:61-118): plain conjugate gradients on the masked Poisson
- * normal operator with the anchor term at the first mask pixel (row-major),
- * stopped at |r|/|b| <= tol or maxiter (maxiter <= 0: 20*ss*fs); the best
- * iterate is returned shifted to phi[anchor] = 0.  gx, gy, phi [ss, fs]
- * float64 (device); info (host, nullable) is written after a stream sync.
- * Returns PXST_EINVAL if the mask is empty (the reference's ValueError). */
+ * (integration.py:61-118): conjugate gradients on the masked Poisson normal
+ * operator with the anchor term at the first mask pixel (row-major), stopped
+ * at |r|/|b| <= tol or maxiter (maxiter <= 0: 20*ss*fs); the best iterate is
+ * returned shifted to phi[anchor] = 0.  solver 0 = plain CG (the
+ * reference's iteration); solver 1 = the same CG preconditioned by an
+ * aggregation-multigrid V-cycle (same operator, stopping rule and gauge;
+ * converges to the same potential in far fewer iterations).  gx, gy, phi
+ * [ss, fs] float64 (device); info (host, nullable) is written after a stream
+ * sync.  Returns PXST_EINVAL if the mask is empty (the reference's
+ * ValueError). */
 int pxst_integrate_gradient(const double* gx, const double* gy, const uint8_t* mask,
-                            int64_t ss, int64_t fs, double tol, int64_t maxiter, double* phi,
-                            pxst_cg_info* info, void* stream);
+                            int64_t ss, int64_t fs, double tol, int64_t maxiter, int solver,
+                            double* phi, pxst_cg_info* info, void* stream);
 
 /* Irrotational projection of the displacement, in place on u [2, ss, fs]
  * (integration.py:121-134 applied at recon.py:305-311): fits phi to
  * (u0 - i, u1 - j) on the support and sets u = identity + grad(phi) there
  * (forward differences, last row/column backward). */
 int pxst_project_irrotational(double* u, const uint8_t* support, int64_t ss, int64_t fs,
-                              double tol, int64_t maxiter, pxst_cg_info* info, void* stream);
+                              double tol, int64_t maxiter, int solver, pxst_cg_info* info,
+                              void* stream);
 
 /* ---- split-half uncertainty (analysis.py:306-361) ---- */
 

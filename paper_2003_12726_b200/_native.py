@@ -85,9 +85,10 @@ _SIGS = {
     "pxst_smooth_displacement": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double,
                                          c_void_p]),
     "pxst_integrate_gradient": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
-                                        c_int64, c_void_p, POINTER(PxstCgInfo), c_void_p]),
+                                        c_int64, c_int, c_void_p, POINTER(PxstCgInfo),
+                                        c_void_p]),
     "pxst_project_irrotational": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double,
-                                          c_int64, POINTER(PxstCgInfo), c_void_p]),
+                                          c_int64, c_int, POINTER(PxstCgInfo), c_void_p]),
     "pxst_split_weights": (c_int, [c_uint64, c_int64, c_int64, c_int64, c_int, c_void_p,
                                    c_void_p]),
     "pxst_split_counts": (c_int, [c_uint64, c_void_p, c_int64, c_int64, c_int64, c_void_p,

@@ -122,6 +122,9 @@ class DeviceRef:
                    (int(origin[0]), int(origin[1])), to_device(fm64, np.float64, device))
 
 
+_SOLVERS = {"cg": 0, "mgcg": 1}
+
+
 def _grid_rule(b) -> tuple[int, int, tuple[int, int]]:
     """Object-grid origin and shape from the bbox values (recon.py:126-132)."""
     u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = b
@@ -205,6 +208,7 @@ class DeviceScan:
                                self.w32.data_ptr(), self.work.data_ptr(), roi4)
         self.empty = self.n_work == 0 or self.n_good == 0 or r1 <= r0 or c1 <= c0
         self._side = None            # side stream of geometry_async
+        self._support_components = None   # project_irrotational's solver choice
         plane = self.ss * self.fs
         self.var_pm = torch.zeros(plane, dtype=torch.float64, device=dev)
         self.sigma2 = torch.zeros(plane, dtype=torch.float64, device=dev)
@@ -442,12 +446,22 @@ class DeviceScan:
                                                     stream_ptr()))
         return u_t
 
-    def project_irrotational(self, u_t, tol: float = 1e-12, maxiter: int | None = None):
-        """Irrotational projection of u_t in place (recon.py:305-311)."""
+    def project_irrotational(self, u_t, tol: float = 1e-12, maxiter: int | None = None,
+                             solver: str = "auto"):
+        """Irrotational projection of u_t in place (recon.py:305-311), converged
+        to the reference's tolerance: "mgcg" = multigrid-preconditioned CG,
+        "cg" = the reference's plain CG, "auto" (default) = "mgcg" when the
+        support has one linked component (integration.linked_components)."""
+        if solver == "auto":
+            if self._support_components is None:
+                from .integration import linked_components
+                self._support_components = linked_components(self.work.cpu().numpy())
+            solver = "mgcg" if self._support_components <= 1 else "cg"
         info = PxstCgInfo()
         check(self.lib.pxst_project_irrotational(u_t.data_ptr(), self.work.data_ptr(), self.ss,
                                                  self.fs, float(tol), int(maxiter or 0),
-                                                 ctypes.byref(info), stream_ptr()))
+                                                 _SOLVERS[solver], ctypes.byref(info),
+                                                 stream_ptr()))
         return info
 
     def regularise(self, u_t, opts):

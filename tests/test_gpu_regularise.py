@@ -154,3 +154,36 @@ def test_defocus_registration_vs_golden(scan0, golden_reg):
     assert (F2.z1_ss, F2.z1_fs) == tuple(g["fd2_z1"])
     with pytest.raises(ValueError):
         geometry.fit_defocus_registration(sc, scan0.w, scan0.m, [])
+
+
+def test_mg_preconditioned_cg_vs_golden(golden_reg):
+    """The multigrid-preconditioned CG converges to the reference's potential
+    under the same stopping rule, in a few dozen iterations."""
+    g = golden_reg
+    res = integration.integrate_gradient(g["ig_gx"], g["ig_gy"], g["ig_mask"], solver="mgcg")
+    assert res.converged and res.residual <= 1e-12
+    assert res.iterations < 0.25 * int(g["ig_iters"]), res.iterations
+    scale = np.abs(g["ig_phi"]).max()
+    np.testing.assert_allclose(res.phi, g["ig_phi"], rtol=0, atol=1e-9 * scale)
+    # a hole-riddled but connected mask: same potential
+    rng = np.random.default_rng(3)
+    mask = rng.random((70, 90)) > 0.1
+    gx, gy = rng.normal(size=(2, 70, 90))
+    assert integration.linked_components(mask) == 1
+    a = integration.integrate_gradient(gx, gy, mask, solver="cg")
+    b = integration.integrate_gradient(gx, gy, mask, solver="auto")
+    assert a.converged and b.converged and b.iterations < a.iterations // 4
+    np.testing.assert_allclose(b.phi, a.phi, rtol=0, atol=1e-8 * np.abs(a.phi).max())
+    # two linked components: "mgcg" may move the anchor-free one by a constant,
+    # "auto" falls back to plain CG and reproduces it
+    mask2 = mask.copy()
+    mask2[:, 45] = False
+    assert integration.linked_components(mask2) == 2
+    c = integration.integrate_gradient(gx, gy, mask2, solver="cg")
+    d = integration.integrate_gradient(gx, gy, mask2, solver="auto")
+    np.testing.assert_array_equal(d.phi, c.phi)
+    e = integration.integrate_gradient(gx, gy, mask2, solver="mgcg")
+    np.testing.assert_allclose(np.gradient(e.phi - c.phi)[0][:, :44], 0, atol=1e-7)
+    assert e.converged
+    with pytest.raises(ValueError):
+        integration.integrate_gradient(gx, gy, mask, solver="lu")
