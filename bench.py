@@ -213,11 +213,19 @@ def run_ours(args, rank, world, local):
     from paper_2003_12726_b200 import _native, engine
     from paper_2003_12726_b200.synth import CONFIGS, make_scan
 
+    # PXST_BENCH_BACKEND=gloo with PXST_BENCH_ONE_GPU=1 runs the N-rank code path
+    # on a single device (functional check only: host-staged collectives)
+    if os.environ.get("PXST_BENCH_ONE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("PXST_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     host_data = args.config <= 1
     if host_data:
         s = make_scan(args.config)
@@ -254,7 +262,8 @@ def run_ours(args, rank, world, local):
         u, di, dj = state["u"], state["di"], state["dj"]
         nxt = nref = None
         if sharded is not None:
-            u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev)
+            u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev, geom=state["geom"])
+            nxt = sharded.next_geom
         else:
             # the iteration's grid bbox and K2 tile spans were fetched on a side
             # stream while the previous iteration's error maps ran, and its

@@ -43,7 +43,10 @@ namespace {
 constexpr int kTR = 8, kTC = 16, kThreads = kTR * kTC;
 __device__ __forceinline__ int tile_dr(int tid) { return ((tid >> 5) >> 1) * 4 + ((tid & 31) >> 3); }
 __device__ __forceinline__ int tile_dc(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
-constexpr int kNB = 4;  // TMA ring depth
+#ifndef PXST_K2_RING
+#define PXST_K2_RING 4
+#endif
+constexpr int kNB = PXST_K2_RING;  // TMA ring depth
 constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
 
 

@@ -60,10 +60,14 @@ def partition_frames(n: int, world: int) -> list[tuple[int, int]]:
 
 @dataclass
 class ShardedMetrics:
-    total: float
+    total_t: torch.Tensor          # [1] sum of per_frame over good frames (no host sync)
     per_frame: torch.Tensor
     per_pixel: torch.Tensor
     reference_plane: torch.Tensor
+
+    @property
+    def total(self) -> float:
+        return float(self.total_t.item())
 
 
 class ShardedIteration:
@@ -137,16 +141,17 @@ class ShardedIteration:
         return di_o, dj_o
 
     # ---------------------------------------------------------------- phases
-    def object_map(self, u, di, dj):
-        n0, m0, shape = self.ex.bbox(u, di, dj)
+    def object_map(self, u, di, dj, geom=None):
+        n0, m0, shape = geom.bbox() if geom is not None else self.ex.bbox(u, di, dj)
         lo, hi = self.frames[self.rank]
         acc = self.ex.object_splat(u, di, dj, n0, m0, shape, lo, hi)
         self._all_reduce(acc)
         return self.ex.object_finish(acc, (n0, m0), shape)
 
-    def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True, opts=None):
+    def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True, opts=None,
+                  geom=None):
         u_local = self.ex.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine,
-                                           rows=self.rows[self.rank])
+                                           rows=self.rows[self.rank], geom=geom)
         u_full = self._gather_rows(u_local)
         # sigma smoothing / irrotational projection (recon.py:298-311) couple all
         # pixels; they are small [SS, FS] planes, so every rank runs them on the
@@ -170,22 +175,26 @@ class ShardedIteration:
         self._all_reduce(den)
         plane = self.ex.error_finish(num, den, ref)
         good = self.ex.good_index_tensor()
-        total = float(per_frame[good].sum().item()) if len(good) else 0.0
+        total = per_frame[good].sum().reshape(1) if len(good) else per_frame.new_zeros(1)
         return ShardedMetrics(total, per_frame, per_pixel, plane)
 
-    def iteration(self, u, di, dj, cfg, ev=None):
-        """One full iteration with the reference's ordering (recon.py:511-516)."""
-        ref = self.object_map(u, di, dj)
+    def iteration(self, u, di, dj, cfg, ev=None, geom=None):
+        """One full iteration with the reference's ordering (recon.py:511-516).
+        `geom` = this iteration's geometry future (GeometryFuture, optional);
+        the next one is left in self.next_geom (computed on every rank from
+        the gathered u and translations, overlapping the error maps)."""
+        ref = self.object_map(u, di, dj, geom)
         if ev:
             ev[0].record(torch.cuda.current_stream())
         u_new = self.pixel_map(ref, u, di, dj, cfg.half_ss, cfg.half_fs, cfg.subpixel_grid,
-                               cfg.refine, opts=cfg)
+                               cfg.refine, opts=cfg, geom=geom)
         if ev:
             ev[1].record(torch.cuda.current_stream())
         di_new, dj_new = di, dj
         if cfg.update_translations:
             di_new, dj_new = self.translations(ref, u_new, di, dj, cfg.t_half_ss, cfg.t_half_fs,
                                                cfg.t_subpixel_grid)
+        self.next_geom = self.ex.geometry_async(u_new, di_new, dj_new)
         self.metrics = self.error_maps(ref, u_new, di_new, dj_new)
         return u_new, di_new, dj_new
 
@@ -216,10 +225,14 @@ class DeviceExecutor:
     def object_finish(self, acc, origin, shape):
         return self.ds.object_finish(acc, origin, shape)
 
-    def pixel_map_search(self, ref, u, di, dj, half_ss, half_fs, sub, refine, rows):
+    def pixel_map_search(self, ref, u, di, dj, half_ss, half_fs, sub, refine, rows, geom=None):
         band = self.ds.band(*rows)
-        u_out, _ = band.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine)
+        u_out, _ = band.pixel_map_search(ref, u, di, dj, half_ss, half_fs, sub, refine,
+                                         geom=geom)
         return u_out
+
+    def geometry_async(self, u, di, dj):
+        return self.ds.geometry_async(u, di, dj)
 
     def translation_search(self, ref, u, di, dj, half_ss, half_fs, sub, lo, hi):
         return self.ds.translation_search(ref, u, di, dj, half_ss, half_fs, sub, lo, hi)

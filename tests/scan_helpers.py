@@ -83,7 +83,10 @@ class OracleExecutor:
         i_ref, _ = orc.ratio_where_weighted(a[0].reshape(shape), a[1].reshape(shape))
         return OracleRef(i_ref, a[1].reshape(shape).copy(), tuple(origin))
 
-    def pixel_map_search(self, ref, u, di, dj, half_ss, half_fs, sub, refine, rows):
+    def geometry_async(self, u, di, dj):
+        return None                     # host executor: object_map falls back to bbox()
+
+    def pixel_map_search(self, ref, u, di, dj, half_ss, half_fs, sub, refine, rows, geom=None):
         roi = (rows[0], rows[1], self.roi[2], self.roi[3])
         if rows[1] <= rows[0]:
             return u.clone()
