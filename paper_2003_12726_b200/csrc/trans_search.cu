@@ -162,7 +162,10 @@ __device__ __forceinline__ int full_index(const TransArgs& a, int t, int s) {
 // 2. fast kernel: one CTA per searched frame
 // ---------------------------------------------------------------------------
 template <int KA, int KB>
-__global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
+#ifndef PXST_K3_OCC2_BELOW
+#define PXST_K3_OCC2_BELOW 72
+#endif
+__global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC2_BELOW) ? 2 : 1)
     k_trans_fast(const __grid_constant__ CUtensorMap tmap, TransArgs a) {
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
@@ -211,27 +214,55 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < 72) ? 2 : 1)
   if (threadIdx.x == 0)
     for (int64_t it = 0; it < (a.n_tiles < kNB ? a.n_tiles : kNB); ++it) issue(it);
 
+  // One-tile-ahead pipeline of the per-pixel inputs (work flag, stack value,
+  // W, u): their global loads for tile it+1 are in flight while tile it runs.
+  struct Raw3 {
+    float I[4], W[4];
+    double u0[4], u1[4];
+    bool live[4];
+  };
+  auto load_raw = [&](int64_t it, Raw3& R) {
+    const int64_t band = it / a.n_ct;
+    const int ct = static_cast<int>(it % a.n_ct);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {   // this thread's 4 pixels: rows 2w, 2w+1; cols lane, lane+32
+      const int64_t row = a.sc.roi[0] + band * kTR + 2 * warp + (e >> 1);
+      const int64_t col = a.sc.roi[2] + (int64_t)ct * kTC + lane + 32 * (e & 1);
+      const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
+      const int64_t p = in ? row * a.sc.fs + col : 0;
+      R.live[e] = in && a.sc.work[p] != 0;
+      R.I[e] = __ldg(frame + p);
+      R.W[e] = a.sc.w32[p];
+      R.u0[e] = a.u[p];
+      R.u1[e] = a.u[plane + p];
+    }
+  };
+  // (The 2-CTA kernels, capped at 128 registers, have no room for the second
+  // set and load in place.)
+  constexpr bool kPipe = !(KA * KB < PXST_K3_OCC2_BELOW);
+  Raw3 nxt;
+  if (kPipe) load_raw(0, nxt);
+
   for (int64_t it = 0; it < a.n_tiles; ++it) {
     const int b = static_cast<int>(it % kNB);
     const unsigned ph = static_cast<unsigned>((it / kNB) & 1);
-    const int64_t band = it / a.n_ct;
-    const int ct = static_cast<int>(it % a.n_ct);
     const TileGeo g = a.geo[it];
-    // this thread's 4 pixels of the tile: rows 2w, 2w+1; cols lane, lane+32
+    Raw3 cur;
+    if (kPipe) {
+      cur = nxt;
+      if (it + 1 < a.n_tiles) load_raw(it + 1, nxt);
+    } else {
+      load_raw(it, cur);
+    }
     float I[4], W[4], fx[4], fy[4];
     int off[4];                        // patch origin offset in the slot, -1 = not fast
     bool tile_slow = false;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int64_t row = a.sc.roi[0] + band * kTR + 2 * warp + (e >> 1);
-      const int64_t col = a.sc.roi[2] + (int64_t)ct * kTC + lane + 32 * (e & 1);
-      const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
-      const int64_t p = in ? row * a.sc.fs + col : 0;
-      const bool live = in && a.sc.work[p] != 0;
-      I[e] = live ? __ldg(frame + p) : 0.f;
-      W[e] = live ? a.sc.w32[p] : 0.f;
-      const Sample3 sm =
-          make_sample3(a, g, live ? a.u[p] : 0.0, live ? a.u[plane + p] : 0.0, dI, dJ);
+      const bool live = cur.live[e];
+      I[e] = live ? cur.I[e] : 0.f;
+      W[e] = live ? cur.W[e] : 0.f;
+      const Sample3 sm = make_sample3(a, g, live ? cur.u0[e] : 0.0, live ? cur.u1[e] : 0.0, dI, dJ);
       fx[e] = static_cast<float>(sm.fx);
       fy[e] = static_cast<float>(sm.fy);
       off[e] = (live && sm.fast) ? sm.lr * a.box_c + sm.lc : -1;
