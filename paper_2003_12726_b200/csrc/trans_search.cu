@@ -53,6 +53,7 @@ struct TransArgs {
   const float* fm;
   const uint8_t* valid;
   const uint8_t* pv;         // patch-valid map for the union box over phases
+  const float* fmn;          // NaN-encoded reference (slow fix-up)
   int64_t os, of, n0, m0;
   const TileGeo* geo;        // [n_bands][n_ct]
   int n_ct;                  // column tiles per band
@@ -323,10 +324,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC2_BELOW) ? 2 :
 // 3. slow fix-up: warp per listed frame
 // ---------------------------------------------------------------------------
 __global__ void k_trans_slow(TransArgs a) {
-  extern __shared__ __align__(16) unsigned char slow_sm[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int ld = a.kb + 1, pn = (a.ka + 1) * ld;
-  float* pf = reinterpret_cast<float*>(slow_sm) + wib * pn;
+  const int lane = threadIdx.x & 31;
   const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned n = *a.slow_n;
@@ -360,32 +358,38 @@ __global__ void k_trans_slow(TransArgs a) {
       const int64_t c_hi = min(cw, c_lo + kTC);
       const int64_t npx = (r_hi - r_lo) * (c_hi - c_lo);
       for (int64_t q0 = 0; q0 < npx; q0 += 32) {
+        // lane-parallel classification of 32 pixels; each lane keeps its
+        // sample and inputs for the broadcast below
         const int64_t ql = q0 + lane;
         bool slow = false;
-        int64_t p = 0;
+        Sample3 sl{};
+        float Il = 0.f, Wl = 0.f;
         if (ql < npx) {
           const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
-          p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
-          if (a.sc.work[p]) slow = !make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ).fast;
+          const int64_t p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
+          if (a.sc.work[p]) {
+            sl = make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ);
+            slow = !sl.fast;
+            if (slow) {
+              Il = __ldg(frame + p);
+              Wl = a.sc.w32[p];
+            }
+          }
         }
         unsigned mask = __ballot_sync(0xffffffffu, slow);
         while (mask) {
           const int bsel = __ffs(mask) - 1;
           mask &= mask - 1;
-          const int64_t ps = __shfl_sync(0xffffffffu, p, bsel);
-          const Sample3 sm = make_sample3(a, g, a.u[ps], a.u[plane + ps], dI, dJ);
-          const float I = __ldg(frame + ps), W = a.sc.w32[ps];
-          const int pr0 = sm.i - a.mhi_a, pc0 = sm.j - a.mhi_b;
-          for (int idx = lane; idx < pn; idx += 32)
-            pf[idx] = staged_cell(a.fm, a.valid, a.os, a.of, pr0 + idx / ld, pc0 + idx % ld);
-          __syncwarp();
-          const ExactSample es = exact_sample(sm.fx, sm.fy, W, I, 1.f);
+          const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - a.mhi_a;
+          const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - a.mhi_b;
+          const ExactSample es = exact_sample(__shfl_sync(0xffffffffu, sl.fx, bsel),
+                                              __shfl_sync(0xffffffffu, sl.fy, bsel),
+                                              __shfl_sync(0xffffffffu, Wl, bsel),
+                                              __shfl_sync(0xffffffffu, Il, bsel), 1.f);
 #pragma unroll
           for (int j = 0; j < kSlowPerLane; ++j)
             if (lane + 32 * j < nk_ph)
-              part[j] += trial_staged(pf, ld, ta[j], tb[j], pr0 + ta[j], pc0 + tb[j], a.os,
-                                      a.of, es);
-          __syncwarp();
+              part[j] += trial_global(a.fmn, a.os, a.of, pr0 + ta[j], pc0 + tb[j], es);
         }
       }
     }
@@ -605,7 +609,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
     a.tile_words = static_cast<int>((a.n_tiles + 63) / 64);
 
-    Scratch geo, pvbuf, pvtmp, fmpad, lst, tb;
+    Scratch geo, pvbuf, fmnbuf, pvtmp, fmpad, lst, tb;
     if (int e = geo.alloc(sizeof(TileGeo) * a.n_tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
@@ -627,6 +631,9 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
                         s))
       return e;
     a.pv = pvbuf.as<uint8_t>();
+    if (int e = fmnbuf.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
+    if (int e = make_nan_ref(ref, fmnbuf.as<float>(), s)) return e;
+    a.fmn = fmnbuf.as<float>();
     // TMA descriptor (16-byte row pitch)
     const float* tbase = ref->fm;
     int64_t pitch = ref->of;
@@ -657,7 +664,6 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
       PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(unsigned long long) * 8, s));
       a.dbg = dbg.as<unsigned long long>();
     }
-    const size_t slow_smem = sizeof(float) * (max_ka + 1) * (max_kb + 1) * 8;
     for (int64_t c0 = frame_lo; c0 < frame_hi; c0 += chunk) {
       const int64_t c1 = min(frame_hi, c0 + chunk);
       a.frame_lo = c0;
@@ -672,7 +678,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
         PXST_CHECK_CUDA(cudaMemsetAsync(a.tilebits, 0, tb_bytes, s));
         ph.fn<<<(unsigned)(c1 - c0), kThreads, smem, s>>>(tmap, a);
         PXST_CHECK_LAUNCH();
-        k_trans_slow<<<148 * 4, 256, slow_smem, s>>>(a);
+        k_trans_slow<<<148 * 4, 256, 0, s>>>(a);
         PXST_CHECK_LAUNCH();
         if (a.dbg) {
           unsigned h = 0;
