@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
   const double W64 = live ? a.sc.w64[p] : 0.0;
   const double s2 = live ? a.sigma2[p] : 1.0;
   const double W2 = W64 * W64;                               // recon.py:136
+  const double inv_s2 = live ? 1.0 / s2 : 0.0;               // one division per pixel
+  const double inv_W = live ? 1.0 / W64 : 0.0;
   int64_t n0b = 0, m0b = 0, osb = 1, ofb = 1;
   if (FUSE) {
     n0b = a.grid_b[0];
@@ -169,17 +171,21 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
           // corners 00, 01, 10, 11 (interp.py:70-84 order)
           const double cv[4] = {g0[b].x, g1[b].x, g0[b].y, g1[b].y};
           double den = 0.0, nm = 0.0;
+          bool all = true;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const bool m = cv[q] == cv[q];           // NaN = invalid cell
-            den += m ? cw[q] : 0.0;
-            nm += m ? cw[q] * cv[q] : 0.0;
+            all = all && m;
+            den = fma(cw[q], m ? 1.0 : 0.0, den);    // cw * {0, 1} is exact: = den + cw m
+            nm = fma(cw[q], m ? cv[q] : 0.0, nm);
           }
           const bool ok = inb[b] && den > 0.0;
-          const double v = ok ? nm / den : 0.0;
+          // all four corners valid: den = 1 to a few ulp, and 1/den = 2 - den to
+          // ~1e-31 -- no division on the common path
+          const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
           const double I = static_cast<double>(Iv[b]);
           const double r = ok ? I - W64 * v : I - W64;  // recon.py:421
-          const double eps = (live && b0 + h + b < nt) ? (r * r) / s2 : 0.0;   // recon.py:422
+          const double eps = (live && b0 + h + b < nt) ? (r * r) * inv_s2 : 0.0;   // recon.py:422
           e[h + b] = eps;
           pix += eps;
           if (inb[b])                                   // recon.py:425
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
             const double yb = u1 - t_dj[t] - static_cast<double>(m0b);
             if (xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1) {   // interp.py:103-107
               const Split sx = split(xb), sy = split(yb);
-              splat_grouped(img_b, (int64_t)sx.i * ofb + sy.i, sx.f, sy.f, (I / W64) * W2, W2);
+              splat_grouped(img_b, (int64_t)sx.i * ofb + sy.i, sx.f, sy.f, (I * inv_W) * W2, W2);
             }
           }
         }

@@ -47,6 +47,7 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
   const double u0 = live ? u[p] : 0.0, u1 = live ? u[plane + p] : 0.0;
   const double w = live ? sc.w64[p] : 1.0;
   const double w2 = w * w;                       // recon.py:136
+  const double inv_w = 1.0 / w;                  // value = I / W (interp.py:112), <= 1 ulp
   const double os1 = static_cast<double>(os - 1), of1 = static_cast<double>(of - 1);
   const int64_t n_o = os * of;
   const int64_t k_begin = frame_lo + (int64_t)blockIdx.z * frames_per_z;
@@ -78,7 +79,7 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
           continue;
         }
         const Split sx = split(x), sy = split(y);
-        const double vw = (static_cast<double>(Iv[b]) / w) * w2;    // value*weight (interp.py:112)
+        const double vw = (static_cast<double>(Iv[b]) * inv_w) * w2;   // value*weight (interp.py:112)
         splat_grouped(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2);
       }
     }
