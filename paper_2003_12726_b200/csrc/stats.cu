@@ -109,28 +109,69 @@ __global__ void k_pixel_stats(pxst_scan sc, const float* __restrict__ fw,
 }
 
 // Per-frame normaliser and |I|W mass: one block per good frame.
-__global__ void k_frame_stats(pxst_scan sc, double* frame_norm, double* frame_iw,
-                              double* frame_i) {
+// Per-frame sums over the ROI's work pixels, split over gridDim.y slices of
+// rows (enough blocks to fill the GPU; one block per frame left most SMs
+// idle), partial[k * slices + slice]; k_frame_final adds the slices in order.
+__global__ void k_frame_stats(pxst_scan sc, double* part_norm, double* part_iw,
+                              double* part_i) {
   __shared__ double sh[32];
   const int64_t k = blockIdx.x;
+  const int slices = gridDim.y, sl = blockIdx.y;
   const int64_t f = sc.good[k];
   const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
-  const int64_t n = rw * cw;
+  const int64_t r_lo = sc.roi[0] + rw * sl / slices, r_hi = sc.roi[0] + rw * (sl + 1) / slices;
   const float* fr = sc.frames + f * sc.ss * sc.fs;
   double acc = 0.0, iw = 0.0, ia = 0.0;
-  for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
-    const int64_t p = (sc.roi[0] + q / cw) * sc.fs + sc.roi[2] + q % cw;
-    if (!sc.work[p]) continue;
-    const double I = static_cast<double>(__ldg(fr + p));
-    const double d = I - sc.w64[p];
-    acc += d * d;
-    iw += fabs(I) * sc.w64[p];
-    ia += fabs(I);
-  }
+  constexpr int kR = 4;                          // rows in flight per thread
+  for (int64_t r0 = r_lo; r0 < r_hi; r0 += kR)
+    for (int64_t c = threadIdx.x; c < cw; c += blockDim.x) {
+      float I32[kR];
+      double w[kR];
+      bool m[kR];
+#pragma unroll
+      for (int j = 0; j < kR; ++j) {             // all loads first
+        const bool in = r0 + j < r_hi;
+        const int64_t p = (in ? r0 + j : r0) * sc.fs + sc.roi[2] + c;
+        I32[j] = __ldg(fr + p);
+        w[j] = sc.w64[p];
+        m[j] = in && sc.work[p];
+      }
+#pragma unroll
+      for (int j = 0; j < kR; ++j)
+        if (m[j]) {
+          const double I = static_cast<double>(I32[j]);
+          const double d = I - w[j];
+          acc += d * d;
+          iw += fabs(I) * w[j];
+          ia += fabs(I);
+        }
+    }
   acc = block_reduce(acc, Sum(), sh);
   iw = block_reduce(iw, Sum(), sh);
   ia = block_reduce(ia, Sum(), sh);
-  if (threadIdx.x == 0) { frame_norm[k] = acc; frame_iw[k] = iw; frame_i[k] = ia; }
+  if (threadIdx.x == 0) {
+    part_norm[k * slices + sl] = acc;
+    part_iw[k * slices + sl] = iw;
+    part_i[k * slices + sl] = ia;
+  }
+}
+
+__global__ void k_frame_final(const double* __restrict__ part_norm,
+                              const double* __restrict__ part_iw, const double* __restrict__ part_i,
+                              int64_t n_good, int slices, double* frame_norm, double* frame_iw,
+                              double* frame_i) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_good;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int j = 0; j < slices; ++j) {
+      a += part_norm[k * slices + j];
+      b += part_iw[k * slices + j];
+      c += part_i[k * slices + j];
+    }
+    frame_norm[k] = a;
+    frame_iw[k] = b;
+    frame_i[k] = c;
+  }
 }
 
 __global__ void k_sum_final(const double* a, const double* b, int64_t n, double* out_a,
@@ -242,7 +283,19 @@ extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst
   PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
   k_pixel_stats<<<g, 128, 0, s>>>(*sc, fw, st->scalars, st->var_pm, st->sigma2);
   PXST_CHECK_LAUNCH();
-  k_frame_stats<<<(unsigned)sc->n_good, 512, 0, s>>>(*sc, st->frame_norm, fiw, fi);
+  const int64_t rows = sc->roi[1] - sc->roi[0];
+  int64_t slices = (4 * 148 + sc->n_good - 1) / sc->n_good;
+  slices = slices < 1 ? 1 : (slices > rows ? rows : slices);
+  if (slices > 64) slices = 64;
+  Scratch fpart;
+  if (int e = fpart.alloc(sizeof(double) * 3 * slices * sc->n_good, s)) return e;
+  double* pn = fpart.as<double>();
+  k_frame_stats<<<dim3((unsigned)sc->n_good, (unsigned)slices), 256, 0, s>>>(
+      *sc, pn, pn + slices * sc->n_good, pn + 2 * slices * sc->n_good);
+  PXST_CHECK_LAUNCH();
+  k_frame_final<<<grid_1d(sc->n_good, 128), 128, 0, s>>>(
+      pn, pn + slices * sc->n_good, pn + 2 * slices * sc->n_good, sc->n_good, (int)slices,
+      st->frame_norm, fiw, fi);
   PXST_CHECK_LAUNCH();
   k_sum_final<<<1, 1024, 0, s>>>(fiw, fi, sc->n_good, st->scalars + 1, st->scalars + 3);
   PXST_CHECK_LAUNCH();
