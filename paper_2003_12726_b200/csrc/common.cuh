@@ -103,15 +103,6 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// Round-to-nearest conversion of a non-negative or signed double to int64
-// fixed point.
-__device__ __forceinline__ long long to_fixed(double v) { return __double2ll_rn(v); }
-
-__device__ __forceinline__ void red_add(int64_t* p, long long v) {
-  if (v != 0)
-    atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
-}
-
 // Split coordinate: x = i + f with integer i = floor(x) and f in [0,1)
 // (interp.py:39-42).  Computed in float64 exactly as the reference does.
 struct Split {
@@ -195,32 +186,5 @@ int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* nu
 // Number of grouped images for `blocks` frame blocks of frames_per_block
 // frames over n_cells cells; returns frame blocks per image.
 int64_t chunk_images(int64_t blocks, int64_t frames_per_block, int64_t n_cells, int* n_img);
-
-// Float64 variant for the memory-bound error maps (K4), reading a float64
-// masked image: matches the reference's float64 residuals to ~1e-15.
-__device__ __forceinline__ bool masked_read64(const double* __restrict__ fm,
-                                              const uint8_t* __restrict__ valid, int64_t os,
-                                              int64_t of, int i, int j, double fx, double fy,
-                                              double& v) {
-  if (!inside_1d(i, fx, os) || !inside_1d(j, fy, of)) return false;
-  const int r0 = i, c0 = j;
-  const int r1 = min(r0 + 1, static_cast<int>(os - 1));
-  const int c1 = min(c0 + 1, static_cast<int>(of - 1));
-  const double w00 = (1.0 - fx) * (1.0 - fy), w01 = (1.0 - fx) * fy;
-  const double w10 = fx * (1.0 - fy), w11 = fx * fy;
-  const int64_t a00 = (int64_t)r0 * of + c0, a01 = (int64_t)r0 * of + c1;
-  const int64_t a10 = (int64_t)r1 * of + c0, a11 = (int64_t)r1 * of + c1;
-  const double m00 = __ldg(valid + a00), m01 = __ldg(valid + a01);
-  const double m10 = __ldg(valid + a10), m11 = __ldg(valid + a11);
-  // interp.py:70-81 order: den and num summed corner by corner
-  const double den = w00 * m00 + w01 * m01 + w10 * m10 + w11 * m11;
-  if (!(den > 0.0)) return false;
-  const double num = w00 * (m00 != 0.0 ? __ldg(fm + a00) : 0.0) +
-                     w01 * (m01 != 0.0 ? __ldg(fm + a01) : 0.0) +
-                     w10 * (m10 != 0.0 ? __ldg(fm + a10) : 0.0) +
-                     w11 * (m11 != 0.0 ? __ldg(fm + a11) : 0.0);
-  v = num / den;
-  return true;
-}
 
 }  // namespace pxst

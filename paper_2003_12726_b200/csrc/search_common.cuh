@@ -20,41 +20,6 @@
 
 namespace pxst {
 
-// Fast path: the whole patch is valid and inside; `win` points at the patch
-// origin in shared memory (row pitch ld).  acc[t][s] accumulates the trial
-// whose bilinear base cell is (patch row t, patch col s).
-template <int KA, int KB>
-__device__ __forceinline__ void engine_fast(const float* __restrict__ win, int ld, float fx,
-                                            float fy, float A, float B, float I,
-                                            float (&acc)[KA][KB]) {
-  const float gy = 1.f - fy;
-  float hp[KB];
-  {
-    float o[KB + 1];
-#pragma unroll
-    for (int s = 0; s <= KB; ++s) o[s] = win[s];
-#pragma unroll
-    for (int s = 0; s < KB; ++s) hp[s] = fmaf(fy, o[s + 1], gy * o[s]);
-  }
-#pragma unroll
-  for (int t = 0; t < KA; ++t) {
-    const float* rp = win + (t + 1) * ld;
-    float o[KB + 1], hc[KB];
-#pragma unroll
-    for (int s = 0; s <= KB; ++s) o[s] = rp[s];
-#pragma unroll
-    for (int s = 0; s < KB; ++s) hc[s] = fmaf(fy, o[s + 1], gy * o[s]);
-#pragma unroll
-    for (int s = 0; s < KB; ++s) {
-      float r = fmaf(-A, hp[s], I);
-      r = fmaf(-B, hc[s], r);
-      acc[t][s] = fmaf(r, r, acc[t][s]);
-    }
-#pragma unroll
-    for (int s = 0; s < KB; ++s) hp[s] = hc[s];
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Packed (FFMA2) variant.  sm_100 executes fma.rn.f32x2 at the full FP32 rate
 // with half the issue slots (measured 73.8 TFLOP/s, profiles/microbench_r01.json).
@@ -147,13 +112,12 @@ __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int 
 }
 
 // ---------------------------------------------------------------------------
-// Exact trials on a staged patch (the slow fix-up kernels).  The patch holds
-// the float32 reference at rows pr0.. and cols pc0.. with NaN on invalid or
-// out-of-grid cells, so one shared-memory load gives value and validity.
-// Everything that is constant over a sample's trials (integer shifts keep
-// its fractions) is hoisted into ExactSample; a trial then costs four loads
-// and the masked renormalisation of masked_read, in the same float32
-// operation order.
+// Exact trials (the slow fix-up kernels), read from a float32 copy of the
+// reference with NaN on invalid cells (make_nan_ref), so one load gives value
+// and validity.  Everything that is constant over a sample's trials (integer
+// shifts keep its fractions) is hoisted into ExactSample; a trial then costs
+// four loads and the masked renormalisation of masked_read, in the same
+// float32 operation order.
 // ---------------------------------------------------------------------------
 struct ExactSample {
   float w00, w01, w10, w11;   // bilinear weights (masked_read's float32 formulas)
@@ -177,32 +141,6 @@ __device__ __forceinline__ ExactSample exact_sample(double fx, double fy, float 
   const float d0 = I - W;
   e.fb = fwv * (d0 * d0);
   return e;
-}
-
-// Trial whose base cell is grid (row, col) = patch (pa, pb): the inclusive
-// inside test of interp.py:67 on integers plus the per-sample flags, then
-// the renormalised bilinear read of interp.py:70-84 (clipped corners carry
-// zero weight and are skipped, which also skips their NaN).
-__device__ __forceinline__ float trial_staged(const float* __restrict__ pf, int ld, int pa,
-                                              int pb, int row, int col, int64_t os, int64_t of,
-                                              const ExactSample& e) {
-  const bool rin = (row >= 0 && row < os - 1) || (row == os - 1 && !e.fxp);
-  const bool cin = (col >= 0 && col < of - 1) || (col == of - 1 && !e.fyp);
-  if (!(rin && cin)) return e.fb;
-  const float* p = pf + pa * ld + pb;
-  const float v00 = p[0], v01 = p[1], v10 = p[ld], v11 = p[ld + 1];
-  const bool m00 = v00 == v00;
-  const bool m01 = e.fyp && v01 == v01;
-  const bool m10 = e.fxp && v10 == v10;
-  const bool m11 = e.fxp && e.fyp && v11 == v11;
-  if (!(m00 || m01 || m10 || m11)) return e.fb;
-  float den = 0.f, num = 0.f;
-  if (m00) { den += e.w00; num = fmaf(e.w00, v00, num); }
-  if (m01) { den += e.w01; num = fmaf(e.w01, v01, num); }
-  if (m10) { den += e.w10; num = fmaf(e.w10, v10, num); }
-  if (m11) { den += e.w11; num = fmaf(e.w11, v11, num); }
-  const float r = fmaf(-e.W, num / den, e.I);
-  return e.fwv * (r * r);
 }
 
 // Same trial read straight from a NaN-encoded copy of the reference in
@@ -237,48 +175,7 @@ __device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int
 // float32 reference with NaN on invalid cells, [os*of] (for trial_global).
 int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s);
 
-// Patch cell value for staging: the float32 reference, NaN where invalid or
-// outside the grid.
-__device__ __forceinline__ float staged_cell(const float* __restrict__ fm,
-                                             const uint8_t* __restrict__ valid, int64_t os,
-                                             int64_t of, int r, int c) {
-  const bool in = r >= 0 && r < os && c >= 0 && c < of;
-  const int64_t o = in ? (int64_t)r * of + c : 0;
-  const uint8_t ok = __ldg(valid + o);      // both loads issued together
-  const float v = __ldg(fm + o);
-  return (in && ok) ? v : __int_as_float(0x7fc00000);
-}
 
-// Exact contribution of one sample to one trial whose bilinear base cell is
-// (row, col) with fractions (fx, fy): masked renormalised read from global
-// memory with the inclusive inside test, (I - W)^2 fallback when invalid
-// (recon.py:150, 161), times the frame weight.
-__device__ __forceinline__ float trial_exact(const float* __restrict__ fm,
-                                             const uint8_t* __restrict__ valid, int64_t os,
-                                             int64_t of, int row, int col, double fx, double fy,
-                                             float W, float I, float fwv) {
-  float v;
-  if (masked_read(fm, valid, os, of, row, col, fx, fy, v)) {
-    const float r = fmaf(-W, v, I);
-    return fwv * (r * r);
-  }
-  const float d0 = I - W;
-  return fwv * (d0 * d0);
-}
-
-// Exact slow path for one sample over a register accumulator window (used by
-// the translation kernel, whose accumulators stay in registers).
-template <int KA, int KB>
-__device__ __forceinline__ void engine_slow(const float* __restrict__ fm,
-                                            const uint8_t* __restrict__ valid, int64_t os,
-                                            int64_t of, int pr, int pc, double fx, double fy,
-                                            float W, float I, float fwv, float (&acc)[KA][KB]) {
-#pragma unroll
-  for (int t = 0; t < KA; ++t)
-#pragma unroll
-    for (int s = 0; s < KB; ++s)
-      acc[t][s] += trial_exact(fm, valid, os, of, pr + t, pc + s, fx, fy, W, I, fwv);
-}
 
 // float64 3x3 least-squares paraboloid (recon.py:183-207); e is row-major
 // [ss offset -1,0,1][fs offset -1,0,1].  Offsets clipped to [-1, 1]; (0,0)
@@ -343,12 +240,12 @@ __device__ __forceinline__ TileGeo make_tile_geo(double mn0, double mx0, double 
 }
 
 // Host: largest spans over tiles with work pixels -> out[2] (synchronises).
+int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s);
 // Same reduction left on the device: out_dev[2] (no synchronisation).
 int tile_span_max_dev(const TileGeo* geo, int64_t n, int* out_dev, cudaStream_t s);
 // out[i] = window_offsets(half, step)[i] for the n = 2 kh + 1 offsets, written
 // on the device (no host copy).
 int fill_offsets(double* out, int n, double step, cudaStream_t s);
-int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s);
 
 __host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
 // TMA on this stack faults ("illegal instruction") unless the box starts on a
