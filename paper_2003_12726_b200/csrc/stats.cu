@@ -232,7 +232,7 @@ __global__ void k_bbox_final(pxst_scan sc, const double* part, int nb, const dou
 
 int partial_blocks(const pxst_scan* sc) {
   const int64_t n = (sc->roi[1] - sc->roi[0]) * (sc->roi[3] - sc->roi[2]);
-  int64_t nb = (n + kThreads * 8 - 1) / (kThreads * 8);
+  int64_t nb = (n + kThreads * 2 - 1) / (kThreads * 2);   // latency-bound: many short blocks
   if (nb < 1) nb = 1;
   if (nb > 1184) nb = 1184;  // 8 x 148 SMs
   return static_cast<int>(nb);

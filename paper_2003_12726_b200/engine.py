@@ -139,13 +139,15 @@ class GeometryFuture:
     grid (n0, m0, os, of) also stays on the device for kernels that read it
     without a host round trip)."""
 
-    def __init__(self, host8, host2, event, grid_dev):
+    def __init__(self, host8, host2, event, grid_dev, grid_event):
         self._host8, self._host2, self._event = host8, host2, event
         self.grid_dev = grid_dev
+        self._grid_event = grid_event
 
     def gpu_wait(self, stream=None):
-        """Make `stream` (default: current) wait for the geometry on the GPU."""
-        (stream or torch.cuda.current_stream()).wait_event(self._event)
+        """Make `stream` (default: current) wait on the GPU for grid_dev (the
+        tile spans and host copies behind it are not waited for)."""
+        (stream or torch.cuda.current_stream()).wait_event(self._grid_event)
 
     def bbox(self) -> tuple[int, int, tuple[int, int]]:
         self._event.synchronize()
@@ -268,16 +270,18 @@ class DeviceScan:
             check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
                                      dj_t.data_ptr(), dev8.data_ptr(), sp))
             check(self.lib.pxst_grid_rule(dev8.data_ptr(), grid.data_ptr(), sp))
+            grid_ready = torch.cuda.Event()      # what device-side consumers wait for
+            grid_ready.record(side)
+            host8.copy_(dev8, non_blocking=True)
             check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
                                            dev2.data_ptr(), sp))
-            host8.copy_(dev8, non_blocking=True)
             host2.copy_(dev2, non_blocking=True)
             done = torch.cuda.Event()
             done.record(side)
         for t in (u_t, di_t, dj_t):
             t.record_stream(side)
         TRANSFER["d2h"] += 8 * 8 + 2 * 4
-        return GeometryFuture(host8, host2, done, grid)
+        return GeometryFuture(host8, host2, done, grid, grid_ready)
 
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
                      acc: torch.Tensor | None = None) -> torch.Tensor:
