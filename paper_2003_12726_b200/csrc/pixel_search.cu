@@ -126,16 +126,32 @@ struct Sample {
   int lr, lc;        // patch origin inside the TMA box
   int wr0, wc0;      // box origin in the object grid
   bool pre;          // every fast-path condition except the patch-valid lookup
+                     // and the frame-weight sign
   uint8_t pvb;       // patch-valid byte (loaded unconditionally, consumed late so
                      // the one-frame-ahead pipeline hides its latency)
-  __device__ __forceinline__ bool fast() const { return pre && pvb != 0; }
+  float fwv;         // frame weight (< 0: not live); also consumed late
+  __device__ __forceinline__ bool fast() const { return pre && pvb != 0 && fwv >= 0.f; }
 };
 
+// Object-window origin (box row, 16-byte aligned box column) of a tile for
+// the frame at (dI, dJ): the same for every thread of the tile, so the fast
+// kernel computes it once per frame in its shared frame table.
+__device__ __forceinline__ void window_origin(const PixArgs& a, const TileGeo& g, double dI,
+                                              double dJ, int& wr0, int& wc0) {
+  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
+  wr0 = static_cast<int>(floor(g.umin0 - dI - static_cast<double>(a.n0))) - ra;
+  wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - static_cast<double>(a.m0))) - rb);
+}
+
+// fwv is only stored (checked by fast()), so a frame-weight load issued for
+// the next frame is not waited on here.
 __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g, double u0,
-                                              double u1, double dI, double dJ, float fwv) {
+                                              double u1, double dI, double dJ, float fwv,
+                                              int wr0, int wc0) {
   const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
   const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
   Sample s;
+  s.fwv = fwv;
   const double x = u0 - dI - n0d;                     // recon.py:148
   const double y = u1 - dJ - m0d;
   const double xf = floor(x), yf = floor(y);
@@ -148,12 +164,12 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   s.pvb = 0;
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
   if (tile_fits(g, need_rows2(a.ka), need_cols2(a.kb), a.box_r, a.box_c)) {
-    s.wr0 = static_cast<int>(floor(g.umin0 - dI - n0d)) - ra;
-    s.wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - m0d)) - rb);
+    s.wr0 = wr0;
+    s.wc0 = wc0;
     s.lr = s.i - ra - s.wr0;
     s.lc = s.j - rb - s.wc0;
     const bool in = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of;
-    s.pre = fwv >= 0.f && in && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r && s.lc >= 0 &&
+    s.pre = in && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r && s.lc >= 0 &&
             s.lc + a.kb + 1 <= a.box_c;
     s.pvb = __ldg(a.pv + (in ? (int64_t)s.i * a.of + s.j : 0));
   }
@@ -169,7 +185,6 @@ template <int KA, int KB>
 #endif
 __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
-  constexpr int RA = (KA - 1) / 2, RB = (KB - 1) / 2;
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
@@ -182,6 +197,8 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
   double* t_di = reinterpret_cast<double*>(base + sizeof(float) * kNB * box);
   double* t_dj = t_di + a.chunk;
   int* t_f = reinterpret_cast<int*>(t_dj + a.chunk);
+  int* t_wr = t_f + a.chunk;                         // window origin per frame
+  int* t_wc = t_wr + a.chunk;
 
   const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
   if (!(g.umin0 == g.umin0)) return;                  // tile without work pixels
@@ -206,19 +223,18 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 
   if (fits && nk > 0) {
     const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
-    const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
     for (int jj = threadIdx.x; jj < nk; jj += kThreads) {
       const int f = a.sc.good[k_lo + jj];
+      const double dI = a.di[f], dJ = a.dj[f];
       t_f[jj] = f;
-      t_di[jj] = a.di[f];
-      t_dj[jj] = a.dj[f];
+      t_di[jj] = dI;
+      t_dj[jj] = dJ;
+      window_origin(a, g, dI, dJ, t_wr[jj], t_wc[jj]);
     }
     auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
-      const int wr0 = static_cast<int>(floor(g.umin0 - t_di[jj] - n0d)) - RA;
-      const int wc0 = align4_down(static_cast<int>(floor(g.umin1 - t_dj[jj] - m0d)) - RB);
       const int b = jj % kNB;
       mbar_arrive_expect_tx(&full[b], bytes);
-      tma_load_2d(ring + b * box, &tmap, wc0, wr0, &full[b]);
+      tma_load_2d(ring + b * box, &tmap, t_wc[jj], t_wr[jj], &full[b]);
     };
     if (threadIdx.x == 0) {
       tma_prefetch_desc(&tmap);
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       const int64_t f = t_f[jj];
       I = live ? __ldg(a.sc.frames + f * plane + p) : 0.f;
       fwv = (live && a.fw) ? __ldg(a.fw + f * plane + p) : 1.f;
-      return make_sample(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f);
+      return make_sample(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f, t_wr[jj], t_wc[jj]);
     };
     // One-frame-ahead pipeline of the per-sample geometry, stack value and
     // patch-valid lookup, so their global-load latency hides behind the
@@ -338,7 +354,10 @@ __global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
       if (kl < k_hi) {
         const int64_t f = a.sc.good[kl];
         fwl = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
-        sl = make_sample(a, g, u0, u1, a.di[f], a.dj[f], fwl);
+        const double dI = a.di[f], dJ = a.dj[f];
+        int wr0, wc0;
+        window_origin(a, g, dI, dJ, wr0, wc0);
+        sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
         slow = !sl.fast();
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
@@ -597,7 +616,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
       return e;
     const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
-                        (2 * sizeof(double) + sizeof(int)) * a.chunk;
+                        (2 * sizeof(double) + 3 * sizeof(int)) * a.chunk;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     Scratch lst;

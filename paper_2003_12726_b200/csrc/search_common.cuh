@@ -21,10 +21,23 @@
 namespace pxst {
 
 // ---------------------------------------------------------------------------
-// Packed (FFMA2) variant.  sm_100 executes fma.rn.f32x2 at the full FP32 rate
+// Packed (FFMA2) engine.  sm_100 executes fma.rn.f32x2 at the full FP32 rate
 // with half the issue slots (measured 73.8 TFLOP/s, profiles/microbench_r01.json).
-// Trials (t, 2k) and (t, 2k+1) share one 64-bit register pair; the row
-// interpolation stays scalar but lands directly in register pairs.
+//
+// Two changes to the plain engine above cut its FP32 work per trial from
+// ~5.2 to ~4.1 lane operations and its issue slots by a third:
+//  * Row interpolation in one FMA.  h = gy o_b + fy o_{b+1} (gy = 1 - fy) is
+//    carried as h' = o_b + rho o_{b+1} with rho = fy / gy and the factor gy
+//    folded into the trial weights (A' = A gy, B' = B gy), so every trial is
+//    still r = I - A' h'_prev - B' h'_cur = I - A h_prev - B h_cur.  fy is
+//    kept <= 1 - 2^-24, so gy > 0; the relative rounding of A' h' matches
+//    that of A h (h' is one fused rounding, the gy scale one more).
+//  * Trial columns paired at a distance H = ceil(KB / 2): the register pair k
+//    holds trials (t, k) and (t, k + H).  The patch row then packs as
+//    Q_k = (o_k, o_{k+H}) with every value in exactly one register, and the
+//    row's h' pairs are one FFMA2 each, h'_(k, k+H) = Q_k + rho Q_{k+1}
+//    (the plain (2k, 2k+1) pairing needs the misaligned pair (o_{2k+1},
+//    o_{2k+2})).
 // ---------------------------------------------------------------------------
 typedef unsigned long long f32x2;
 
@@ -44,24 +57,49 @@ __device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
 
 template <int KA, int KB>
 struct PackedAcc {
-  static constexpr int KP = KB / 2;          // packed pairs per trial row
-  static constexpr bool ODD = (KB % 2) != 0;  // leftover last column
-  f32x2 p[KA][KP > 0 ? KP : 1];
+  static constexpr int H = (KB + 1) / 2;      // pair distance
+  static constexpr int NP = KB / 2;           // register pairs per trial row
+  static constexpr bool ODD = (KB % 2) != 0;  // single column NP (= H - 1)
+  f32x2 p[KA][NP > 0 ? NP : 1];
   float s[KA];
 
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int t = 0; t < KA; ++t) {
 #pragma unroll
-      for (int k = 0; k < KP; ++k) p[t][k] = 0ull;
+      for (int k = 0; k < NP; ++k) p[t][k] = 0ull;
       s[t] = 0.f;
     }
   }
   __device__ __forceinline__ float get(int t, int c) const {  // t, c compile-time in loops
-    if (ODD && c == KB - 1) return s[t];
+    if (ODD && c == NP) return s[t];
     float lo, hi;
-    unpack2(p[t][c / 2], lo, hi);
-    return (c & 1) ? hi : lo;
+    unpack2(p[t][c < NP ? c : c - H], lo, hi);
+    return c < NP ? lo : hi;
+  }
+};
+
+// One patch row: o_0 .. o_KB packed as Q_k = (o_k, o_{k+H}) (+ o_KB alone when
+// KB is even), and its h' values in the accumulator layout.
+template <int KB>
+struct PatchRow {
+  static constexpr int H = (KB + 1) / 2, NP = KB / 2;
+  static constexpr bool ODD = (KB % 2) != 0;
+  f32x2 h[NP > 0 ? NP : 1];
+  float hs;
+
+  __device__ __forceinline__ void load(const float* __restrict__ rp, float rho) {
+    float o[KB + 1];
+#pragma unroll
+    for (int c = 0; c <= KB; ++c) o[c] = rp[c];
+    f32x2 q[H + 1];
+#pragma unroll
+    for (int k = 0; k < H; ++k) q[k] = pack2(o[k], o[k + H]);
+    if (!ODD) q[H] = pack2(o[H], o[KB]);            // (o_H, o_2H) for the last pair
+    const f32x2 rho2 = pack2(rho, rho);
+#pragma unroll
+    for (int k = 0; k < NP; ++k) h[k] = ffma2(rho2, q[k + 1], q[k]);
+    hs = ODD ? fmaf(rho, o[H], o[H - 1]) : 0.f;
   }
 };
 
@@ -69,45 +107,30 @@ template <int KA, int KB>
 __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int ld, float fx,
                                              float fy, float A, float B, float I,
                                              PackedAcc<KA, KB>& acc) {
-  constexpr int KP = PackedAcc<KA, KB>::KP;
+  constexpr int NP = PackedAcc<KA, KB>::NP;
   constexpr bool ODD = PackedAcc<KA, KB>::ODD;
+  fy = fminf(fy, 0x1.fffffep-1f);
   const float gy = 1.f - fy;
-  const f32x2 nA2 = pack2(-A, -A), nB2 = pack2(-B, -B), I2 = pack2(I, I);
-  f32x2 hp2[KP > 0 ? KP : 1];
-  float hpo = 0.f;
-  {
-    float o[KB + 1];
-#pragma unroll
-    for (int s = 0; s <= KB; ++s) o[s] = win[s];
-#pragma unroll
-    for (int k = 0; k < KP; ++k)
-      hp2[k] = pack2(fmaf(fy, o[2 * k + 1], gy * o[2 * k]), fmaf(fy, o[2 * k + 2], gy * o[2 * k + 1]));
-    if (ODD) hpo = fmaf(fy, o[KB], gy * o[KB - 1]);
-  }
+  const float rho = fy / gy;
+  const float Ap = A * gy, Bp = B * gy;
+  const f32x2 nA2 = pack2(-Ap, -Ap), nB2 = pack2(-Bp, -Bp), I2 = pack2(I, I);
+  PatchRow<KB> prev, cur;
+  prev.load(win, rho);
 #pragma unroll
   for (int t = 0; t < KA; ++t) {
-    const float* rp = win + (t + 1) * ld;
-    float o[KB + 1];
+    cur.load(win + (t + 1) * ld, rho);
 #pragma unroll
-    for (int s = 0; s <= KB; ++s) o[s] = rp[s];
-    f32x2 hc2[KP > 0 ? KP : 1];
-#pragma unroll
-    for (int k = 0; k < KP; ++k)
-      hc2[k] = pack2(fmaf(fy, o[2 * k + 1], gy * o[2 * k]), fmaf(fy, o[2 * k + 2], gy * o[2 * k + 1]));
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-      f32x2 r = ffma2(nA2, hp2[k], I2);
-      r = ffma2(nB2, hc2[k], r);
+    for (int k = 0; k < NP; ++k) {
+      f32x2 r = ffma2(nA2, prev.h[k], I2);
+      r = ffma2(nB2, cur.h[k], r);
       acc.p[t][k] = ffma2(r, r, acc.p[t][k]);
-      hp2[k] = hc2[k];
     }
     if (ODD) {
-      const float hco = fmaf(fy, o[KB], gy * o[KB - 1]);
-      float r = fmaf(-A, hpo, I);
-      r = fmaf(-B, hco, r);
+      float r = fmaf(-Ap, prev.hs, I);
+      r = fmaf(-Bp, cur.hs, r);
       acc.s[t] = fmaf(r, r, acc.s[t]);
-      hpo = hco;
     }
+    prev = cur;
   }
 }
 
