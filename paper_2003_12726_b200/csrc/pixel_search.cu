@@ -145,6 +145,7 @@ __device__ __forceinline__ void window_origin(const PixArgs& a, const TileGeo& g
 
 // fwv is only stored (checked by fast()), so a frame-weight load issued for
 // the next frame is not waited on here.
+template <bool kKnownFit = false>
 __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g, double u0,
                                               double u1, double dI, double dJ, float fwv,
                                               int wr0, int wc0) {
@@ -163,7 +164,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   s.pre = false;
   s.pvb = 0;
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
-  if (tile_fits(g, need_rows2(a.ka), need_cols2(a.kb), a.box_r, a.box_c)) {
+  if (kKnownFit || tile_fits(g, need_rows2(a.ka), need_cols2(a.kb), a.box_r, a.box_c)) {
     s.wr0 = wr0;
     s.wc0 = wc0;
     s.lr = s.i - ra - s.wr0;
@@ -171,7 +172,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
     const bool in = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of;
     s.pre = in && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r && s.lc >= 0 &&
             s.lc + a.kb + 1 <= a.box_c;
-    s.pvb = __ldg(a.pv + (in ? (int64_t)s.i * a.of + s.j : 0));
+    s.pvb = __ldg(a.pv + (in ? s.i * static_cast<int>(a.of) + s.j : 0));   // os * of < 2^31
   }
   return s;
 }
@@ -196,8 +197,8 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
   // Per-frame table of the chunk (frame index, di, dj) after the ring.
   double* t_di = reinterpret_cast<double*>(base + sizeof(float) * kNB * box);
   double* t_dj = t_di + a.chunk;
-  int* t_f = reinterpret_cast<int*>(t_dj + a.chunk);
-  int* t_wr = t_f + a.chunk;                         // window origin per frame
+  int64_t* t_off = reinterpret_cast<int64_t*>(t_dj + a.chunk);   // frame offset f * plane
+  int* t_wr = reinterpret_cast<int*>(t_off + a.chunk);           // window origin per frame
   int* t_wc = t_wr + a.chunk;
 
   const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     for (int jj = threadIdx.x; jj < nk; jj += kThreads) {
       const int f = a.sc.good[k_lo + jj];
       const double dI = a.di[f], dJ = a.dj[f];
-      t_f[jj] = f;
+      t_off[jj] = f * plane;
       t_di[jj] = dI;
       t_dj[jj] = dJ;
       window_origin(a, g, dI, dJ, t_wr[jj], t_wc[jj]);
@@ -251,41 +252,55 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
     const float W = live ? a.sc.w32[p] : 0.f;
     auto sample_of = [&](int jj, float& I, float& fwv) {
-      const int64_t f = t_f[jj];
-      I = live ? __ldg(a.sc.frames + f * plane + p) : 0.f;
-      fwv = (live && a.fw) ? __ldg(a.fw + f * plane + p) : 1.f;
-      return make_sample(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f, t_wr[jj], t_wc[jj]);
+      const int64_t off = t_off[jj];
+      I = live ? __ldg(a.sc.frames + off + p) : 0.f;
+      fwv = (live && a.fw) ? __ldg(a.fw + off + p) : 1.f;
+      return make_sample<true>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f, t_wr[jj],
+                               t_wc[jj]);
     };
     // One-frame-ahead pipeline of the per-sample geometry, stack value and
-    // patch-valid lookup, so their global-load latency hides behind the
-    // current frame's trials.
+    // patch-valid lookup.  The loop body after the ring wait is one basic
+    // block (samples that are not fast run the engine with zero weights on
+    // the slot origin), so the compiler interleaves the next sample's float64
+    // geometry and loads with this frame's trials.
     float I_n, fw_n;
     Sample s_n = sample_of(0, I_n, fw_n);
+    int issued = min(kNB, nk);     // thread 0: frames [0, issued) are in flight or done
     for (int jj = 0; jj < nk; ++jj) {
       const Sample sm = s_n;
       const float I = I_n, fwv = fw_n;
-      if (jj + 1 < nk) s_n = sample_of(jj + 1, I_n, fw_n);
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
+      if (threadIdx.x == 0) {
+        // Refill freed slots without waiting for the slowest warp: frame k
+        // reuses the slot of frame k - kNB; block only when this thread
+        // itself needs frame jj next.
+        while (issued < nk && issued < jj + kNB) {
+          const int k = issued;
+          const unsigned eph = ((k / kNB) - 1) & 1;
+          if (k > jj) {
+            if (!mbar_test(&empty[k % kNB], eph)) break;
+          } else {
+            mbar_wait(&empty[k % kNB], eph);
+          }
+          issue(k);
+          ++issued;
+        }
+      }
       mbar_wait(&full[b], ph);
       const bool fast = sm.fast();
       any_slow |= live && !fast;
-      if (fast) {
-        const float fx = static_cast<float>(sm.fx), fy = static_cast<float>(sm.fy);
-        float sI = I, sW = W;
-        if (a.fw) {
-          const float sq = sqrtf(fwv);
-          sI *= sq;
-          sW *= sq;
-        }
-        engine_fast2<KA, KB>(ring + b * box + sm.lr * a.box_c + sm.lc, a.box_c, fx, fy,
-                             sW * (1.f - fx), sW * fx, sI, acc);
-      }
+      const float fx = fast ? static_cast<float>(sm.fx) : 0.f;
+      const float fy = fast ? static_cast<float>(sm.fy) : 0.f;
+      float sq = sqrt_approx(fmaxf(fwv, 0.f));     // unconditional: no branch in the block
+      sq = fwv == 1.f ? 1.f : sq;
+      sq = fast ? sq : 0.f;
+      const float sI = I * sq, sW = W * sq;
+      const int off = fast ? sm.lr * a.box_c + sm.lc : 0;
+      s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
+      engine_fast2<KA, KB>(ring + b * box + off, a.box_c, fx, fy, sW * (1.f - fx), sW * fx, sI,
+                           acc);
       mbar_arrive(&empty[b]);
-      if (threadIdx.x == 0 && jj + kNB < nk) {
-        mbar_wait(&empty[b], ph);      // every thread is done with this slot
-        issue(jj + kNB);
-      }
     }
   }
   if (live) {
@@ -555,6 +570,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
 
   FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
   if (fn) {
+    PXST_REQUIRE(ref->os * ref->of < (int64_t(1) << 31), "reference image too large");
     const int ra = (na - 1) / 2, rb = (nb - 1) / 2;
     a.box_r = box_rows_for(na);
     a.box_c = box_cols_for(nb);
@@ -616,7 +632,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
       return e;
     const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
-                        (2 * sizeof(double) + 3 * sizeof(int)) * a.chunk;
+                        (3 * sizeof(double) + 2 * sizeof(int)) * a.chunk;
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     Scratch lst;
