@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 //    order; each (chunk, trial, pixel) partial is owned by one lane, so the
 //    result does not depend on list order.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
+__global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                                                  const unsigned long long* __restrict__ list,
                                                  const unsigned* __restrict__ list_n) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
@@ -377,7 +377,18 @@ __global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
-      if (a.dbg && lane == 0) atomicAdd(a.dbg, (unsigned long long)__popc(mask));
+      if (a.dbg) {   // skipped samples by reason: off grid, outside the box, patch invalid
+        const bool in = sl.i >= 0 && sl.i < a.os && sl.j >= 0 && sl.j < a.of;
+        const bool inbox = sl.lr >= 0 && sl.lr + a.ka + 1 <= a.box_r && sl.lc >= 0 &&
+                           sl.lc + a.kb + 1 <= a.box_c;
+        const unsigned m1 = __ballot_sync(0xffffffffu, slow && !in);
+        const unsigned m2 = __ballot_sync(0xffffffffu, slow && in && !inbox);
+        if (lane == 0) {
+          atomicAdd(a.dbg, (unsigned long long)__popc(mask));
+          atomicAdd(a.dbg + 1, (unsigned long long)__popc(m1));
+          atomicAdd(a.dbg + 2, (unsigned long long)__popc(m2));
+        }
+      }
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -390,7 +401,8 @@ __global__ void __launch_bounds__(256, 3) k_pix_slow(PixArgs a,
 #pragma unroll
         for (int j = 0; j < kSlowPerLane; ++j)
           if (lane + 32 * j < nk)
-            part[j] += trial_global(a.fmn, a.os, a.of, pr0 + ta[j], pc0 + tb[j], es);
+            part[j] += trial_global(a.fmn, static_cast<int>(a.os), static_cast<int>(a.of),
+                                    pr0 + ta[j], pc0 + tb[j], es);
       }
     }
 #pragma unroll
@@ -570,7 +582,6 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
 
   FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
   if (fn) {
-    PXST_REQUIRE(ref->os * ref->of < (int64_t(1) << 31), "reference image too large");
     const int ra = (na - 1) / 2, rb = (nb - 1) / 2;
     a.box_r = box_rows_for(na);
     a.box_c = box_cols_for(nb);
@@ -644,8 +655,8 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.slow_n = list_n;
     Scratch dbg;
     if (getenv("PXST_DEBUG")) {
-      if (int e = dbg.alloc(sizeof(unsigned long long), s)) return e;
-      PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(unsigned long long), s));
+      if (int e = dbg.alloc(3 * sizeof(unsigned long long), s)) return e;
+      PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, 3 * sizeof(unsigned long long), s));
       a.dbg = dbg.as<unsigned long long>();
     }
     dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
@@ -655,12 +666,14 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;
-      unsigned long long hs = 0;
+      unsigned long long hs[3] = {0, 0, 0};
       PXST_CHECK_CUDA(cudaMemcpyAsync(&h, list_n, sizeof(h), cudaMemcpyDeviceToHost, s));
-      PXST_CHECK_CUDA(cudaMemcpyAsync(&hs, a.dbg, sizeof(hs), cudaMemcpyDeviceToHost, s));
+      PXST_CHECK_CUDA(cudaMemcpyAsync(hs, a.dbg, sizeof(hs), cudaMemcpyDeviceToHost, s));
       PXST_CHECK_CUDA(cudaStreamSynchronize(s));
       fprintf(stderr, "[pxst] K2 %dx%d: %lld pixels x %d chunks, %u (pixel, chunk) pairs own "
-              "%llu slow samples\n", na, nb, (long long)a.nq, a.n_chunks, h, hs);
+              "%llu slow samples (%llu off grid, %llu outside the %dx%d box, rest patch "
+              "invalid)\n", na, nb, (long long)a.nq, a.n_chunks, h, hs[0], hs[1], hs[2],
+              a.box_r, a.box_c);
     }
     k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
                                                   refine_ok, u_out, err_out);

@@ -176,31 +176,35 @@ __device__ __forceinline__ ExactSample exact_sample(double fx, double fy, float 
 
 // Same trial read straight from a NaN-encoded copy of the reference in
 // global memory (make_nan_ref): four independent L1/L2 loads, no staging.
-// Corners past the last row/column are clamped onto the grid; they carry
-// zero weight and are excluded by the fx/fy flags.
-__device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int64_t os,
-                                              int64_t of, int row, int col,
-                                              const ExactSample& e) {
+// Branch-free, 32-bit cell indices (callers guarantee os * of < 2^31): the
+// four loads always go to clamped in-grid cells and the reference's rules
+// are applied by selects.  Corners past the last row/column carry zero
+// weight and are excluded by the fx/fy flags; a base outside the grid (or a
+// weighted corner past its edge) gives the (I - W)^2 fallback.
+__device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int os, int of,
+                                              int row, int col, const ExactSample& e) {
   const bool rin = (row >= 0 && row < os - 1) || (row == os - 1 && !e.fxp);
   const bool cin = (col >= 0 && col < of - 1) || (col == of - 1 && !e.fyp);
-  if (!(rin && cin)) return e.fb;
-  const int r1 = row + 1 < os ? row + 1 : row, c1 = col + 1 < of ? col + 1 : col;
-  const float* p0 = fmn + (int64_t)row * of;
-  const float* p1 = fmn + (int64_t)r1 * of;
-  const float v00 = __ldg(p0 + col), v01 = __ldg(p0 + c1);
-  const float v10 = __ldg(p1 + col), v11 = __ldg(p1 + c1);
+  const int r0 = min(max(row, 0), os - 1), c0 = min(max(col, 0), of - 1);
+  const int dr = r0 + 1 < os ? of : 0, dc = c0 + 1 < of ? 1 : 0;
+  const float* p0 = fmn + (r0 * of + c0);
+  const float v00 = __ldg(p0), v01 = __ldg(p0 + dc);
+  const float v10 = __ldg(p0 + dr), v11 = __ldg(p0 + dr + dc);
   const bool m00 = v00 == v00;
   const bool m01 = e.fyp && v01 == v01;
   const bool m10 = e.fxp && v10 == v10;
   const bool m11 = e.fxp && e.fyp && v11 == v11;
-  if (!(m00 || m01 || m10 || m11)) return e.fb;
-  float den = 0.f, num = 0.f;
-  if (m00) { den += e.w00; num = fmaf(e.w00, v00, num); }
-  if (m01) { den += e.w01; num = fmaf(e.w01, v01, num); }
-  if (m10) { den += e.w10; num = fmaf(e.w10, v10, num); }
-  if (m11) { den += e.w11; num = fmaf(e.w11, v11, num); }
-  const float r = fmaf(-e.W, num / den, e.I);
-  return e.fwv * (r * r);
+  float den = m00 ? e.w00 : 0.f;
+  float num = m00 ? e.w00 * v00 : 0.f;
+  den += m01 ? e.w01 : 0.f;
+  num = fmaf(m01 ? e.w01 : 0.f, m01 ? v01 : 0.f, num);
+  den += m10 ? e.w10 : 0.f;
+  num = fmaf(m10 ? e.w10 : 0.f, m10 ? v10 : 0.f, num);
+  den += m11 ? e.w11 : 0.f;
+  num = fmaf(m11 ? e.w11 : 0.f, m11 ? v11 : 0.f, num);
+  const float r = fmaf(-e.W, __fdividef(num, den), e.I);
+  const bool ok = rin && cin && (m00 || m01 || m10 || m11);
+  return ok ? e.fwv * (r * r) : e.fb;
 }
 
 // float32 reference with NaN on invalid cells, [os*of] (for trial_global).

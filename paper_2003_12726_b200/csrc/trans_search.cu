@@ -389,7 +389,8 @@ __global__ void k_trans_slow(TransArgs a) {
 #pragma unroll
           for (int j = 0; j < kSlowPerLane; ++j)
             if (lane + 32 * j < nk_ph)
-              part[j] += trial_global(a.fmn, a.os, a.of, pr0 + ta[j], pc0 + tb[j], es);
+              part[j] += trial_global(a.fmn, static_cast<int>(a.os),
+                                      static_cast<int>(a.of), pr0 + ta[j], pc0 + tb[j], es);
         }
       }
     }
