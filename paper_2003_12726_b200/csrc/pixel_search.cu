@@ -23,6 +23,7 @@
 //                      rule, writes u_out and the error map.
 // Sub-pixel grids and non-instantiated windows use k_pix_generic (float64,
 // one thread per (pixel, trial)) followed by the same epilogue.
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -66,8 +67,15 @@ struct PixArgs {
   int tiles_x;
   int ka, kb;                // window (fast kernels: = template args)
   int box_r, box_c;          // TMA box (rows, cols)
-  int n_chunks, chunk;       // frame chunking of the good list
+  int n_chunks, chunk;       // frame chunking of the good list (split tiles)
+  int tbl;                   // frame-table capacity of a fast CTA
+  int64_t n_full;            // work units [0, n_full) are whole tiles over all frames
   int64_t nq;                // ROI rectangle pixel count
+  const double* offs_a;      // window offsets (device)
+  const double* offs_b;
+  int refine_ok;
+  double* u_out;
+  double* err_out;
   float* partial;            // [n_chunks][ka*kb][nq]
   unsigned long long* slow_list;  // (pixel << 20 | chunk) pairs owning skipped samples
   unsigned* slow_n;
@@ -83,6 +91,70 @@ __host__ __device__ inline int box_cols_for(int kb) {
   return c - 32 >= kb + 36 ? c - 32 : c;
 }
 constexpr int kWarps = kThreads / 32;
+
+// Work units of k_pix_fast (1-D grid): units [0, n_full) are whole tiles over
+// all frames, finished in the kernel (argmin + paraboloid, no partial sums);
+// the remaining tiles are split into n_chunks frame chunks each, one unit per
+// (tile, chunk), so the last partial wave still fills the machine.  Slow-list
+// entries and partial slots name a chunk; kAllFrames = a whole-tile unit
+// (partial slot 0).
+constexpr unsigned kAllFrames = 0xFFFFFu;
+
+__device__ __forceinline__ void unit_of(const PixArgs& a, int64_t unit, int64_t& tile,
+                                        unsigned& chunk) {
+  if (unit < a.n_full) {
+    tile = unit;
+    chunk = kAllFrames;
+  } else {
+    const int64_t v = unit - a.n_full;
+    tile = a.n_full + v / a.n_chunks;
+    chunk = static_cast<unsigned>(v % a.n_chunks);
+  }
+}
+
+__device__ __forceinline__ void chunk_frames(const PixArgs& a, unsigned chunk, int64_t& k_lo,
+                                             int64_t& k_hi, int64_t& slot) {
+  if (chunk == kAllFrames) {
+    k_lo = 0;
+    k_hi = a.sc.n_good;
+    slot = 0;
+  } else {
+    k_lo = (int64_t)chunk * a.chunk;
+    k_hi = min(a.sc.n_good, k_lo + a.chunk);
+    slot = chunk;
+  }
+}
+
+// Argmin / paraboloid / static-pixel rule for one pixel (recon.py:257-296,
+// 313-315) from its raw trial sums (total(t), t in numpy order a * Kb + b).
+// First-occurrence argmin on the raw sums: dividing by the common positive
+// normaliser preserves the order except for ties the division itself would
+// create, which the parity bar (unique argmin, margin > 1e-4) excludes.
+template <class Total>
+__device__ __forceinline__ void finish_pixel(const PixArgs& a, int64_t p, int best, double braw,
+                                             double u0, double u1, double var, double off_a,
+                                             double off_b, Total total) {
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const int na = a.ka, nb = a.kb;
+  const bool active = var > 0.0;                      // recon.py:257-263
+  const double nv = active ? var : 1.0;
+  const double bv = braw / nv;
+  const int ia = best / nb, ib = best % nb;
+  double sh_ss = off_a, sh_fs = off_b;
+  if (a.refine_ok && active && ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {   // recon.py:273-287
+    double e[9];
+#pragma unroll
+    for (int d = 0; d < 9; ++d) e[d] = total((ia + d / 3 - 1) * nb + (ib + d % 3 - 1)) / nv;
+    double dss, dfs;
+    paraboloid(e, dss, dfs);
+    sh_ss += dss;
+    sh_fs += dfs;
+  }
+  if (!active) { sh_ss = 0.0; sh_fs = 0.0; }          // recon.py:289-292
+  a.u_out[p] = u0 + sh_ss;                            // recon.py:294-296
+  a.u_out[plane + p] = u1 + sh_fs;
+  a.err_out[p] = active ? bv : 0.0;                   // recon.py:313-315
+}
 
 
 // ---------------------------------------------------------------------------
@@ -196,15 +268,19 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
   const int box = slot_floats(a.box_r, a.box_c);          // slot stride (128-byte multiple)
   // Per-frame table of the chunk (frame index, di, dj) after the ring.
   double* t_di = reinterpret_cast<double*>(base + sizeof(float) * kNB * box);
-  double* t_dj = t_di + a.chunk;
-  int64_t* t_off = reinterpret_cast<int64_t*>(t_dj + a.chunk);   // frame offset f * plane
-  int* t_wr = reinterpret_cast<int*>(t_off + a.chunk);           // window origin per frame
-  int* t_wc = t_wr + a.chunk;
+  double* t_dj = t_di + a.tbl;
+  int64_t* t_off = reinterpret_cast<int64_t*>(t_dj + a.tbl);     // frame offset f * plane
+  int* t_wr = reinterpret_cast<int*>(t_off + a.tbl);             // window origin per frame
+  int* t_wc = t_wr + a.tbl;
 
-  const TileGeo g = a.geo[(int64_t)blockIdx.y * a.tiles_x + blockIdx.x];
+  int64_t tile;
+  unsigned chunk;
+  unit_of(a, blockIdx.x, tile, chunk);
+  const int64_t ty = tile / a.tiles_x, tx = tile % a.tiles_x;
+  const TileGeo g = a.geo[tile];
   if (!(g.umin0 == g.umin0)) return;                  // tile without work pixels
-  const int64_t rr = (int64_t)blockIdx.y * kTR + tile_dr(threadIdx.x);
-  const int64_t cc = (int64_t)blockIdx.x * kTC + tile_dc(threadIdx.x);
+  const int64_t rr = ty * kTR + tile_dr(threadIdx.x);
+  const int64_t cc = tx * kTC + tile_dc(threadIdx.x);
   const int64_t row = a.sc.roi[0] + rr, col = a.sc.roi[2] + cc;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const bool inroi = row < a.sc.roi[1] && col < a.sc.roi[3];
@@ -212,16 +288,18 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
   const int64_t q = rr * cw + cc;
   const bool live = inroi && a.sc.work[p] != 0;
   const int64_t plane = a.sc.ss * a.sc.fs;
-  const int64_t k_lo = (int64_t)blockIdx.z * a.chunk;
-  const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+  int64_t k_lo, k_hi, pslot;
+  chunk_frames(a, chunk, k_lo, k_hi, pslot);
   const int nk = static_cast<int>(k_hi - k_lo);
-  float* out = a.partial + (int64_t)blockIdx.z * KA * KB * a.nq + q;
+  float* out = a.partial + pslot * KA * KB * a.nq + q;
 
   PackedAcc<KA, KB> acc;
   acc.zero();
   const bool fits = tile_fits(g, need_rows2(KA), need_cols2(KB), a.box_r, a.box_c);
   bool any_slow = live && nk > 0 && !fits;
 
+  const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
+  const double var_p = (live && chunk == kAllFrames) ? a.var[p] : 0.0;   // used after the loop
   if (fits && nk > 0) {
     const unsigned bytes = static_cast<unsigned>(a.box_r * a.box_c * sizeof(float));
     for (int jj = threadIdx.x; jj < nk; jj += kThreads) {
@@ -249,7 +327,6 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     if (threadIdx.x == 0)
       for (int jj = 0; jj < min(kNB, nk); ++jj) issue(jj);
 
-    const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
     const float W = live ? a.sc.w32[p] : 0.f;
     auto sample_of = [&](int jj, float& I, float& fwv) {
       const int64_t off = t_off[jj];
@@ -303,7 +380,33 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       mbar_arrive(&empty[b]);
     }
   }
-  if (live) {
+  bool finished = false;
+  if (chunk == kAllFrames) {
+    // Whole-tile unit: finish every pixel without skipped samples here (the
+    // others are finished by k_pix_slow after their fix-up).  The
+    // trial sums go to this thread's column of the (now idle) ring so the
+    // 3x3 refinement patch can be indexed.
+    __syncthreads();                               // no thread reads the ring any more
+    float* st = ring + threadIdx.x;
+    int best = 0;
+    float bsum = 0.f;
+#pragma unroll
+    for (int t = 0; t < KA; ++t)
+#pragma unroll
+      for (int s = 0; s < KB; ++s) {
+        const float v = acc.get(t, s);
+        st[(t * KB + s) * kThreads] = v;
+        if (t * KB + s == 0 || v < bsum) { bsum = v; best = t * KB + s; }
+      }
+    finished = live && !any_slow;
+    if (finished) {   // integer window: offsets are index - half (window_offsets)
+      constexpr int RA = (KA - 1) / 2, RB = (KB - 1) / 2;
+      finish_pixel(a, p, best, static_cast<double>(bsum), u0, u1, var_p,
+                   static_cast<double>(best / KB - RA), static_cast<double>(best % KB - RB),
+                   [&](int t) { return static_cast<double>(st[t * kThreads]); });
+    }
+  }
+  if (live && !finished) {
 #pragma unroll
     for (int t = 0; t < KA; ++t)
 #pragma unroll
@@ -311,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
   }
   if (any_slow) {   // hand the skipped samples of this (pixel, chunk) to k_pix_slow
     const unsigned slot = atomicAdd(a.slow_n, 1u);
-    a.slow_list[slot] = (static_cast<unsigned long long>(q) << 20) | blockIdx.z;
+    a.slow_list[slot] = (static_cast<unsigned long long>(q) << 20) | chunk;
   }
 }
 
@@ -343,15 +446,15 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
   for (int64_t e = warp0; e < n; e += nwarps) {
     const unsigned long long ent = list[e];
     const int64_t q = static_cast<int64_t>(ent >> 20);
-    const int chunk = static_cast<int>(ent & 0xFFFFF);
+    const unsigned chunk = static_cast<unsigned>(ent & 0xFFFFF);
     const int64_t rr = q / cw, cc = q % cw;
     const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
     const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
     const double u0 = a.u[p], u1 = a.u[plane + p];
     const float W = a.sc.w32[p];
-    float* out = a.partial + (int64_t)chunk * nk * a.nq + q;
-    const int64_t k_lo = (int64_t)chunk * a.chunk;
-    const int64_t k_hi = min(a.sc.n_good, k_lo + a.chunk);
+    int64_t k_lo, k_hi, pslot;
+    chunk_frames(a, chunk, k_lo, k_hi, pslot);
+    float* out = a.partial + pslot * nk * a.nq + q;
     float part[kSlowPerLane];          // lane owns trials lane + 32 j
     float prev[kSlowPerLane];          // the fast kernel's partials, fetched early
 #pragma unroll
@@ -405,11 +508,39 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                                     pr0 + ta[j], pc0 + tb[j], es);
       }
     }
+    float tot[kSlowPerLane];
+#pragma unroll
+    for (int j = 0; j < kSlowPerLane; ++j) tot[j] = prev[j] + part[j];
+    if (chunk != kAllFrames) {
+#pragma unroll
+      for (int j = 0; j < kSlowPerLane; ++j) {
+        const int t = lane + 32 * j;
+        if (t < nk) out[(int64_t)t * a.nq] = tot[j];
+      }
+      continue;
+    }
+    // Whole-tile pixel: every frame is in, finish it here.  Warp first-
+    // occurrence argmin (smaller sum, ties to the smaller trial index).
+    int best = -1;
+    float bsum = 0.f;
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) {
       const int t = lane + 32 * j;
-      if (t < nk) out[(int64_t)t * a.nq] = prev[j] + part[j];
+      if (t < nk && (best < 0 || tot[j] < bsum)) { bsum = tot[j]; best = t; }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bsum, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+      if (ob >= 0 && (best < 0 || ov < bsum || (ov == bsum && ob < best))) { bsum = ov; best = ob; }
+    }
+    finish_pixel(a, p, best, static_cast<double>(bsum), u0, u1, a.var[p],
+                 a.offs_a[best / a.kb], a.offs_b[best % a.kb], [&](int t) {
+                   float v = tot[0];
+#pragma unroll
+                   for (int j = 1; j < kSlowPerLane; ++j) v = (t >> 5) == j ? tot[j] : v;
+                   return static_cast<double>(__shfl_sync(0xffffffffu, v, t & 31));
+                 });
   }
 }
 
@@ -450,63 +581,72 @@ __global__ void k_pix_generic(PixArgs a, const double* __restrict__ offs_a,
 // ---------------------------------------------------------------------------
 // 4. epilogue
 // ---------------------------------------------------------------------------
+// Eight lanes per pixel: lane k sums trials k, k + 8, ... over the chunks
+// (all loads independent), then a first-occurrence argmin across the group
+// (smaller sum, ties to the smaller trial index = numpy's order).
+constexpr int kEpiLanes = 8;
+
+// Pixels: linear over the ROI (generic path, tiles_x == 0), or the pixels of
+// the split tiles [n_full, tiles) of the fast path (whole-tile pixels are
+// finished by k_pix_fast / k_pix_slow).
 template <class T>
-__global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chunks,
-                               const double* __restrict__ offs_a, const double* __restrict__ offs_b,
-                               int refine_ok, double* u_out, double* err_out) {
+__global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chunks) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= a.nq) return;
-  const int64_t p = (a.sc.roi[0] + q / cw) * a.sc.fs + a.sc.roi[2] + q % cw;
+  const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kEpiLanes;
+  const int sub = threadIdx.x % kEpiLanes;
+  const unsigned gmask = 0xFFu << ((threadIdx.x & 31) & ~(kEpiLanes - 1));
+  int64_t rr, cc;
+  if (a.tiles_x > 0) {
+    const int64_t tile = a.n_full + gi / kThreads;
+    const int loc = static_cast<int>(gi % kThreads);
+    rr = (tile / a.tiles_x) * kTR + tile_dr(loc);
+    cc = (tile % a.tiles_x) * kTC + tile_dc(loc);
+    if (rr >= a.sc.roi[1] - a.sc.roi[0] || cc >= cw) return;
+  } else {
+    if (gi >= a.nq) return;
+    rr = gi / cw;
+    cc = gi % cw;
+  }
+  const int64_t q = rr * cw + cc;
+  const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
   if (!a.sc.work[p]) return;
-  const int64_t plane = a.sc.ss * a.sc.fs;
-  const int na = a.ka, nb = a.kb, nk = na * nb;
+  const int nk = a.ka * a.kb;
   const int64_t cstride = (int64_t)nk * a.nq;
   auto total = [&](int t) {
     double s = 0.0;
     for (int c = 0; c < n_chunks; ++c) s += static_cast<double>(part[c * cstride + (int64_t)t * a.nq + q]);
     return s;
   };
-  const double var = a.var[p];                        // recon.py:257-263
-  const bool active = var > 0.0;
-  const double nv = active ? var : 1.0;
-  // First-occurrence argmin (recon.py:265-269) on the raw sums: dividing by
-  // the common positive normaliser preserves the order except for ties the
-  // division itself would create, which the parity bar (unique argmin,
-  // margin > 1e-4) excludes.
-  // Eight trials per step with their loads independent (the sum over chunks
-  // keeps the order of total()).
-  int best = 0;
+  int best = -1;
   double braw = 0.0;
-  for (int t0 = 0; t0 < nk; t0 += 8) {
+  for (int t0 = 0; t0 < nk; t0 += 8 * kEpiLanes) {
     double v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = 0.0;
     for (int c = 0; c < n_chunks; ++c) {
       const T* pc = part + c * cstride + q;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (t0 + j < nk) v[j] += static_cast<double>(pc[(int64_t)(t0 + j) * a.nq]);
+      for (int j = 0; j < 8; ++j) {
+        const int t = t0 + sub + j * kEpiLanes;
+        if (t < nk) v[j] += static_cast<double>(pc[(int64_t)t * a.nq]);
+      }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (t0 + j < nk && (t0 + j == 0 || v[j] < braw)) { braw = v[j]; best = t0 + j; }
+    for (int j = 0; j < 8; ++j) {
+      const int t = t0 + sub + j * kEpiLanes;
+      if (t < nk && (best < 0 || v[j] < braw)) { braw = v[j]; best = t; }
+    }
   }
-  const double bv = braw / nv;
-  const int ia = best / nb, ib = best % nb;
-  double sh_ss = offs_a[ia], sh_fs = offs_b[ib];
-  if (refine_ok && active && ia > 0 && ia < na - 1 && ib > 0 && ib < nb - 1) {   // recon.py:273-287
-    double e[9];
-    for (int d = 0; d < 9; ++d) e[d] = total((ia + d / 3 - 1) * nb + (ib + d % 3 - 1)) / nv;
-    double dss, dfs;
-    paraboloid(e, dss, dfs);
-    sh_ss += dss;
-    sh_fs += dfs;
+#pragma unroll
+  for (int o = kEpiLanes / 2; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(gmask, braw, o, kEpiLanes);
+    const int ob = __shfl_xor_sync(gmask, best, o, kEpiLanes);
+    if (ob >= 0 && (best < 0 || ov < braw || (ov == braw && ob < best))) { braw = ov; best = ob; }
   }
-  if (!active) { sh_ss = 0.0; sh_fs = 0.0; }          // recon.py:289-292
-  u_out[p] = a.u[p] + sh_ss;                          // recon.py:294-296
-  u_out[plane + p] = a.u[plane + p] + sh_fs;
-  err_out[p] = active ? bv : 0.0;                     // recon.py:313-315
+  if (sub != 0) return;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  finish_pixel(a, p, best, braw, a.u[p], a.u[plane + p], a.var[p], a.offs_a[best / a.kb],
+               a.offs_b[best % a.kb], total);
 }
 
 // ---------------------------------------------------------------------------
@@ -577,7 +717,11 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   if (int e = fill_offsets(offs.as<double>() + na, nb, subpixel_step, s)) return e;
   const double* d_oa = offs.as<double>();
   const double* d_ob = d_oa + na;
-  const int refine_ok = refine && subpixel_step == 0.0 && na >= 3 && nb >= 3;   // recon.py:273
+  a.offs_a = d_oa;
+  a.offs_b = d_ob;
+  a.refine_ok = refine && subpixel_step == 0.0 && na >= 3 && nb >= 3;   // recon.py:273
+  a.u_out = u_out;
+  a.err_out = err_out;
   const unsigned qblocks = (unsigned)((a.nq + 127) / 128);
 
   FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
@@ -589,15 +733,6 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     const int tiles_y = static_cast<int>((rw + kTR - 1) / kTR);
     PXST_REQUIRE(tiles_y <= kMaxGridY, "ROI too tall");
     const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
-    // Frame chunks: enough CTAs for ~6 waves at 2 CTAs/SM, <= 512 frames per
-    // float32 partial sum.
-    int n_chunks = static_cast<int>((6 * 2 * 148 + tiles - 1) / tiles);
-    n_chunks = max(n_chunks, static_cast<int>((sc->n_good + 511) / 512));
-    const int max_chunks = static_cast<int>(sc->n_good / 16 > 1 ? sc->n_good / 16 : 1);
-    n_chunks = n_chunks < max_chunks ? n_chunks : max_chunks;
-    n_chunks = n_chunks > 1 ? n_chunks : 1;
-    a.chunk = static_cast<int>((sc->n_good + n_chunks - 1) / n_chunks);
-    a.n_chunks = static_cast<int>((sc->n_good + a.chunk - 1) / a.chunk);
 
     Scratch pvbuf, pvtmp, geo, part, fmpad, fmn;
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
@@ -608,8 +743,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.pv = pvbuf.as<uint8_t>();
     if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
-    if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
-    a.partial = part.as<float>();
+
     // TMA needs a 16-byte row pitch: pad the object image when of % 4 != 0.
     const float* tbase = ref->fm;
     int64_t pitch = ref->of;
@@ -642,10 +776,47 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     CUtensorMap tmap;
     if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
       return e;
-    const size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
-                        (3 * sizeof(double) + 2 * sizeof(int)) * a.chunk;
+    // Work units.  Resident CTAs S = 2 per SM.  With <= 512 good frames (one
+    // float32 partial holds them) the first floor(tiles / S) full waves are
+    // whole tiles finished in the kernel; the remaining R tiles are split into
+    // ~S / R frame chunks so the last wave is full.  More frames: every tile
+    // is split (<= 512 frames per float32 partial, ~6 waves).
+    int sms = 148;
+    {
+      int dev = 0;
+      PXST_CHECK_CUDA(cudaGetDevice(&dev));
+      PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t slots = 2 * static_cast<int64_t>(sms);
+    const int max_chunks = static_cast<int>(sc->n_good / 16 > 1 ? sc->n_good / 16 : 1);
+    int n_chunks;
+    a.n_full = 0;
+    if (sc->n_good <= 512 && tiles >= slots && !getenv("PXST_K2_NO_FUSE")) {
+      a.n_full = tiles / slots * slots;
+      const int64_t rest = tiles - a.n_full;
+      int64_t c = rest > 0 ? slots / rest : 1;
+      c = c < 1 ? 1 : c;
+      c = c > max_chunks ? max_chunks : c;
+      n_chunks = static_cast<int>(c);
+    } else {
+      n_chunks = static_cast<int>((6 * slots + tiles - 1) / tiles);
+      n_chunks = max(n_chunks, static_cast<int>((sc->n_good + 511) / 512));
+      n_chunks = n_chunks < max_chunks ? n_chunks : max_chunks;
+      n_chunks = n_chunks > 1 ? n_chunks : 1;
+    }
+    a.chunk = static_cast<int>((sc->n_good + n_chunks - 1) / n_chunks);
+    a.n_chunks = static_cast<int>((sc->n_good + a.chunk - 1) / a.chunk);
+    a.tbl = a.n_full > 0 ? static_cast<int>(sc->n_good) : a.chunk;
+    const int64_t units = a.n_full + (tiles - a.n_full) * a.n_chunks;
+    size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
+                  (3 * sizeof(double) + 2 * sizeof(int)) * a.tbl;
+    if (a.n_full > 0)      // whole-tile units stage their trial sums in the ring
+      smem = std::max(smem, sizeof(float) * nk * kThreads + 128 +
+                                (3 * sizeof(double) + 2 * sizeof(int)) * a.tbl);
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
+    if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
+    a.partial = part.as<float>();
     Scratch lst;
     if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 2), s)) return e;
     unsigned* list_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
@@ -659,8 +830,8 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
       PXST_CHECK_CUDA(cudaMemsetAsync(dbg.p, 0, 3 * sizeof(unsigned long long), s));
       a.dbg = dbg.as<unsigned long long>();
     }
-    dim3 gf((unsigned)a.tiles_x, (unsigned)tiles_y, (unsigned)a.n_chunks);
-    fn<<<gf, kThreads, smem, s>>>(tmap, a);
+    PXST_REQUIRE(units < (int64_t(1) << 31), "ROI too large");
+    fn<<<(unsigned)units, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
     k_pix_slow<<<148 * 6, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
@@ -675,8 +846,12 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
               "invalid)\n", na, nb, (long long)a.nq, a.n_chunks, h, hs[0], hs[1], hs[2],
               a.box_r, a.box_c);
     }
-    k_pix_epilogue<float><<<qblocks, 128, 0, s>>>(a, part.as<float>(), a.n_chunks, d_oa, d_ob,
-                                                  refine_ok, u_out, err_out);
+    const int64_t split_px = (tiles - a.n_full) * kThreads;
+    if (split_px > 0) {
+      k_pix_epilogue<float><<<(unsigned)((split_px * kEpiLanes + 127) / 128), 128, 0, s>>>(
+          a, part.as<float>(), a.n_chunks);
+      PXST_CHECK_LAUNCH();
+    }
     PXST_CHECK_LAUNCH();
     return PXST_OK;
   }
@@ -687,8 +862,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   dim3 g(qblocks, (unsigned)nk);
   k_pix_generic<<<g, 128, 0, s>>>(a, d_oa, d_ob, errs.as<double>());
   PXST_CHECK_LAUNCH();
-  k_pix_epilogue<double><<<qblocks, 128, 0, s>>>(a, errs.as<double>(), 1, d_oa, d_ob, refine_ok,
-                                                 u_out, err_out);
+  k_pix_epilogue<double><<<qblocks * kEpiLanes, 128, 0, s>>>(a, errs.as<double>(), 1);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }
