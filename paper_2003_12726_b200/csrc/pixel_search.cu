@@ -427,12 +427,12 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                                                  const unsigned long long* __restrict__ list,
-                                                 const unsigned* __restrict__ list_n) {
+                                                 unsigned* __restrict__ list_n) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const unsigned n = *list_n;
+  const unsigned n = list_n[0];
+  unsigned* next = list_n + 1;       // work counter: entries are fetched dynamically per warp
+                                     // (their cost ranges from 1 to all frames)
   const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
   const int nk = a.ka * a.kb;
   const int64_t plane = a.sc.ss * a.sc.fs;
@@ -443,7 +443,11 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
     ta[j] = t / a.kb;
     tb[j] = t % a.kb;
   }
-  for (int64_t e = warp0; e < n; e += nwarps) {
+  for (;;) {
+    unsigned e = 0;
+    if (lane == 0) e = atomicAdd(next, 1u);
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (e >= n) break;
     const unsigned long long ent = list[e];
     const int64_t q = static_cast<int64_t>(ent >> 20);
     const unsigned chunk = static_cast<unsigned>(ent & 0xFFFFF);
@@ -821,7 +825,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 2), s)) return e;
     unsigned* list_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
     unsigned long long* list = lst.as<unsigned long long>() + 1;
-    PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, sizeof(unsigned), s));
+    PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, 2 * sizeof(unsigned), s));
     a.slow_list = list;
     a.slow_n = list_n;
     Scratch dbg;
@@ -833,7 +837,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_REQUIRE(units < (int64_t(1) << 31), "ROI too large");
     fn<<<(unsigned)units, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
-    k_pix_slow<<<148 * 6, 256, 0, s>>>(a, list, list_n);
+    k_pix_slow<<<2 * sms, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;
