@@ -717,8 +717,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
 
   Scratch offs;
   if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
-  if (int e = fill_offsets(offs.as<double>(), na, subpixel_step, s)) return e;
-  if (int e = fill_offsets(offs.as<double>() + na, nb, subpixel_step, s)) return e;
+  if (int e = fill_offsets(offs.as<double>(), na, nb, subpixel_step, s)) return e;
   const double* d_oa = offs.as<double>();
   const double* d_ob = d_oa + na;
   a.offs_a = d_oa;
@@ -738,12 +737,12 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_REQUIRE(tiles_y <= kMaxGridY, "ROI too tall");
     const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
 
-    Scratch pvbuf, pvtmp, geo, part, fmpad, fmn;
+    Scratch pvbuf, geo, part, fmpad, fmn;
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
     if (int e = fmn.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
-    if (int e = make_nan_ref(ref, fmn.as<float>(), s)) return e;
     a.fmn = fmn.as<float>();
-    if (int e = make_pv(ref, -ra, ra + 1, -rb, rb + 1, pvbuf.as<uint8_t>(), pvtmp, s)) return e;
+    if (int e = make_pv(ref, -ra, ra + 1, -rb, rb + 1, pvbuf.as<uint8_t>(), fmn.as<float>(), s))
+      return e;
     a.pv = pvbuf.as<uint8_t>();
     if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
     a.geo = geo.as<TileGeo>();

@@ -278,9 +278,9 @@ __device__ __forceinline__ TileGeo make_tile_geo(double mn0, double mx0, double 
 int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s);
 // Same reduction left on the device: out_dev[2] (no synchronisation).
 int tile_span_max_dev(const TileGeo* geo, int64_t n, int* out_dev, cudaStream_t s);
-// out[i] = window_offsets(half, step)[i] for the n = 2 kh + 1 offsets, written
-// on the device (no host copy).
-int fill_offsets(double* out, int n, double step, cudaStream_t s);
+// out = window_offsets of the na-point window then of the nb-point window
+// (n = 2 kh + 1 points each), written on the device (no host copy).
+int fill_offsets(double* out, int na, int nb, double step, cudaStream_t s);
 
 __host__ __device__ inline int slot_floats(int br, int bc) { return (br * bc + 31) / 32 * 32; }
 // TMA on this stack faults ("illegal instruction") unless the box starts on a
@@ -295,8 +295,9 @@ __device__ __forceinline__ int clamp_span(double v) {
 
 // Host helpers ---------------------------------------------------------------
 // Patch-valid map: pv[i][j] = every cell of rows [i+lr, i+hr] x cols
-// [j+lc, j+hc] exists and is valid.
-int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Scratch& tmp,
+// [j+lc, j+hc] exists and is valid; with fmn != NULL also the NaN-encoded
+// reference (make_nan_ref) in the same launch.
+int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, float* fmn,
             cudaStream_t s);
 // Offsets of SearchWindow.offsets (recon.py:51-57).
 std::vector<double> window_offsets(int64_t half, double step);

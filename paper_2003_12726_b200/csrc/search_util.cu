@@ -8,25 +8,39 @@
 namespace pxst {
 namespace {
 
-__global__ void k_pv_rows(const uint8_t* __restrict__ valid, int64_t os, int64_t of, int lc,
-                          int hc, uint8_t* __restrict__ tmp) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < os * of;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q / of, j = q % of;
-    uint8_t ok = (j + lc >= 0 && j + hc < of) ? 1 : 0;
-    for (int c = lc; ok && c <= hc; ++c) ok = valid[i * of + j + c];
-    tmp[q] = ok;
-  }
-}
+// Patch-valid map pv[i][j] = every cell of rows [i+lr, i+hr] x cols
+// [j+lc, j+hc] exists and is valid, as a separable AND over a 32 x 32 output
+// tile with its halo staged in shared memory (one launch); optionally also
+// the NaN-encoded float32 reference of the tile's cells (make_nan_ref).
+constexpr int kPvT = 32, kPvMaxHalo = 64;
 
-__global__ void k_pv_cols(const uint8_t* __restrict__ tmp, int64_t os, int64_t of, int lr,
-                          int hr, uint8_t* __restrict__ pv) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < os * of;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q / of, j = q % of;
-    uint8_t ok = (i + lr >= 0 && i + hr < os) ? 1 : 0;
-    for (int r = lr; ok && r <= hr; ++r) ok = tmp[(i + r) * of + j];
-    pv[q] = ok;
+__global__ void __launch_bounds__(256) k_pv_tile(const uint8_t* __restrict__ valid,
+                                                 const float* __restrict__ fm, int os, int of,
+                                                 int lr, int hr, int lc, int hc,
+                                                 uint8_t* __restrict__ pv, float* __restrict__ fmn) {
+  __shared__ uint8_t v[kPvT + kPvMaxHalo][kPvT + kPvMaxHalo];
+  __shared__ uint8_t rowok[kPvT + kPvMaxHalo][kPvT];
+  const int i0 = blockIdx.y * kPvT, j0 = blockIdx.x * kPvT;
+  const int th = kPvT + hr - lr, tw = kPvT + hc - lc;
+  for (int k = threadIdx.x; k < th * tw; k += blockDim.x) {
+    const int r = i0 + lr + k / tw, c = j0 + lc + k % tw;
+    v[k / tw][k % tw] = (r >= 0 && r < os && c >= 0 && c < of) ? valid[r * of + c] : 0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < th * kPvT; k += blockDim.x) {
+    const int rr = k / kPvT, cc = k % kPvT;
+    uint8_t ok = 1;
+    for (int d = 0; d <= hc - lc; ++d) ok &= v[rr][cc + d];
+    rowok[rr][cc] = ok;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kPvT * kPvT; k += blockDim.x) {
+    const int rr = k / kPvT, cc = k % kPvT, i = i0 + rr, j = j0 + cc;
+    if (i >= os || j >= of) continue;
+    uint8_t ok = 1;
+    for (int d = 0; d <= hr - lr; ++d) ok &= rowok[rr + d][cc];
+    pv[i * of + j] = ok;
+    if (fmn) fmn[i * of + j] = valid[i * of + j] ? fm[i * of + j] : __int_as_float(0x7fc00000);
   }
 }
 
@@ -72,15 +86,14 @@ int tile_span_max(const TileGeo* geo, int64_t n, int* out, cudaStream_t s) {
   return PXST_OK;
 }
 
-int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, Scratch& tmp,
+int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, float* fmn,
             cudaStream_t s) {
-  const int64_t n = ref->os * ref->of;
-  if (int e = tmp.alloc(n, s)) return e;
-  int64_t b = (n + 255) / 256;
-  if (b > 148 * 16) b = 148 * 16;
-  k_pv_rows<<<(unsigned)b, 256, 0, s>>>(ref->valid, ref->os, ref->of, lc, hc, tmp.as<uint8_t>());
-  PXST_CHECK_LAUNCH();
-  k_pv_cols<<<(unsigned)b, 256, 0, s>>>(tmp.as<uint8_t>(), ref->os, ref->of, lr, hr, pv);
+  PXST_REQUIRE(lr <= hr && lc <= hc && hr - lr <= kPvMaxHalo && hc - lc <= kPvMaxHalo,
+               "patch extent too large");
+  dim3 g((unsigned)((ref->of + kPvT - 1) / kPvT), (unsigned)((ref->os + kPvT - 1) / kPvT));
+  PXST_REQUIRE(g.y <= kMaxGridY, "reference image too tall");
+  k_pv_tile<<<g, 256, 0, s>>>(ref->valid, ref->fm, static_cast<int>(ref->os),
+                              static_cast<int>(ref->of), lr, hr, lc, hc, pv, fmn);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }
@@ -99,18 +112,19 @@ int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s) {
   return PXST_OK;
 }
 
-__global__ void k_fill_offsets(double* __restrict__ out, int n, int64_t kh, double step) {
+__global__ void k_fill_offsets(double* __restrict__ out, int na, int nb, double step) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const double k = static_cast<double>(static_cast<int64_t>(i) - kh);
+  if (i < na + nb) {
+    const int n = i < na ? na : nb, k0 = i < na ? i : i - na;
+    const double k = static_cast<double>(k0 - (n - 1) / 2);
     out[i] = step > 0.0 ? step * k : k;          // window_offsets, on the device
   }
 }
 
-int fill_offsets(double* out, int n, double step, cudaStream_t s) {
+int fill_offsets(double* out, int na, int nb, double step, cudaStream_t s) {
   // A device fill instead of a pageable host->device copy, which would
   // synchronise the stream before it starts.
-  k_fill_offsets<<<(n + 127) / 128, 128, 0, s>>>(out, n, (n - 1) / 2, step);
+  k_fill_offsets<<<(na + nb + 127) / 128, 128, 0, s>>>(out, na, nb, step);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }

@@ -547,8 +547,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
 
   Scratch offs;
   if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
-  if (int e = fill_offsets(offs.as<double>(), na, subpixel_step, s)) return e;
-  if (int e = fill_offsets(offs.as<double>() + na, nb, subpixel_step, s)) return e;
+  if (int e = fill_offsets(offs.as<double>(), na, nb, subpixel_step, s)) return e;
   const double* d_oa = offs.as<double>();
   const double* d_ob = d_oa + na;
 
@@ -610,7 +609,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
     a.tile_words = static_cast<int>((a.n_tiles + 63) / 64);
 
-    Scratch geo, pvbuf, fmnbuf, pvtmp, fmpad, lst, tb;
+    Scratch geo, pvbuf, fmnbuf, fmpad, lst, tb;
     if (int e = geo.alloc(sizeof(TileGeo) * a.n_tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
@@ -628,12 +627,11 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     // union patch box over phases, relative to floor(x_rho): rows
     // [-max mhi, -min mlo + 1]
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
-    if (int e = make_pv(ref, -mhi_a, -mlo_a + 1, -mhi_b, -mlo_b + 1, pvbuf.as<uint8_t>(), pvtmp,
-                        s))
+    if (int e = fmnbuf.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
+    if (int e = make_pv(ref, -mhi_a, -mlo_a + 1, -mhi_b, -mlo_b + 1, pvbuf.as<uint8_t>(),
+                        fmnbuf.as<float>(), s))
       return e;
     a.pv = pvbuf.as<uint8_t>();
-    if (int e = fmnbuf.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
-    if (int e = make_nan_ref(ref, fmnbuf.as<float>(), s)) return e;
     a.fmn = fmnbuf.as<float>();
     // TMA descriptor (16-byte row pitch)
     const float* tbase = ref->fm;
