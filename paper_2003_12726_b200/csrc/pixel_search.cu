@@ -340,10 +340,15 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     // block (samples that are not fast run the engine with zero weights on
     // the slot origin), so the compiler interleaves the next sample's float64
     // geometry and loads with this frame's trials.
-    float I_n, fw_n;
-    Sample s_n = sample_of(0, I_n, fw_n);
+    // (Windows above 11 x 11 compute the sample in place: the 169 accumulators
+    // of 13 x 13 leave no registers for a second sample.)
+    constexpr bool kAhead = KA * KB <= 121;
+    float I_n = 0.f, fw_n = 0.f;
+    Sample s_n{};
+    if (kAhead) s_n = sample_of(0, I_n, fw_n);
     int issued = min(kNB, nk);     // thread 0: frames [0, issued) are in flight or done
     for (int jj = 0; jj < nk; ++jj) {
+      if (!kAhead) s_n = sample_of(jj, I_n, fw_n);
       const Sample sm = s_n;
       const float I = I_n, fwv = fw_n;
       const int b = jj % kNB;
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       sq = fast ? sq : 0.f;
       const float sI = I * sq, sW = W * sq;
       const int off = fast ? sm.lr * a.box_c + sm.lc : 0;
-      s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
+      if (kAhead) s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
       engine_fast2<KA, KB>(ring + b * box + off, a.box_c, fx, fy, sW * (1.f - fx), sW * fx, sI,
                            acc);
       mbar_arrive(&empty[b]);
