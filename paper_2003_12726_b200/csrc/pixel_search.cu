@@ -342,7 +342,10 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     // geometry and loads with this frame's trials.
     // (Windows above 11 x 11 compute the sample in place: the 169 accumulators
     // of 13 x 13 leave no registers for a second sample.)
-    constexpr bool kAhead = KA * KB <= 121;
+#ifndef PXST_K2_AHEAD_MAX
+#define PXST_K2_AHEAD_MAX 121
+#endif
+    constexpr bool kAhead = KA * KB <= PXST_K2_AHEAD_MAX;
     float I_n = 0.f, fw_n = 0.f;
     Sample s_n{};
     if (kAhead) s_n = sample_of(0, I_n, fw_n);
