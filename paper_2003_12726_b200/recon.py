@@ -150,8 +150,8 @@ def make_reference(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
     ds = SCAN_CACHE.get(scan, w, m, roi)
     if ds.empty:
         raise ValueError("make_reference: empty good pixel/frame set")
-    u_t = ds.upload_u(u.u)
-    di_t, dj_t = ds.upload_t(t.di, t.dj)
+    u_t = ds.upload_u(u.u, cache=True)
+    di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
     return _ref_image(ds.object_map(u_t, di_t, dj_t), geom)
 
 
@@ -168,8 +168,8 @@ def update_pixel_map(scan: ScanData, w: Whitefield, m: PixelMask, ref: Reference
     depend on it (recon.py:163-169).  Returns ``(PixelMap, err_map)``.
     """
     ds = SCAN_CACHE.get(scan, w, m, roi)
-    u_t = ds.upload_u(u.u)
-    di_t, dj_t = ds.upload_t(t.di, t.dj)
+    u_t = ds.upload_u(u.u, cache=True)
+    di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
     fw_t = None
     if frame_weights is not None:
         fw = np.asarray(frame_weights)
@@ -182,6 +182,7 @@ def update_pixel_map(scan: ScanData, w: Whitefield, m: PixelMask, ref: Reference
                                      win.subpixel_grid, opts.quadratic_refinement, fw_t)
     ds.regularise(u_out, opts)                           # recon.py:298-311
     u_h, err_h = to_host_many(u_out, err)
+    ds.remember((u_h,), u_out)     # a later call on the returned map reuses u_out
     return PixelMap(u_h), err_h
 
 
@@ -190,12 +191,13 @@ def update_translations(scan: ScanData, w: Whitefield, m: PixelMask, ref: Refere
                         roi: Roi | None = None) -> PixelTranslations:
     """Per-frame translation grid search (recon.py:336-385) on the GPU (K3)."""
     ds = SCAN_CACHE.get(scan, w, m, roi)
-    u_t = ds.upload_u(u.u)
-    di_t, dj_t = ds.upload_t(t.di, t.dj)
+    u_t = ds.upload_u(u.u, cache=True)
+    di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
     dref = _device_ref(ref, ds)
     di_o, dj_o = ds.translation_search(dref, u_t, di_t, dj_t, win.half_ss, win.half_fs,
                                        win.subpixel_grid)
     di_h, dj_h = to_host_many(di_o, dj_o)
+    ds.remember((di_h, dj_h), (di_o, dj_o))
     return PixelTranslations(di=di_h, dj=dj_h)
 
 
@@ -209,8 +211,8 @@ def calc_error(scan: ScanData, w: Whitefield, m: PixelMask, ref: ReferenceImage,
                t: PixelTranslations, roi: Roi | None = None) -> ErrorMetrics:
     """Error decomposition (recon.py:388-438) on the GPU (K4)."""
     ds = SCAN_CACHE.get(scan, w, m, roi)
-    u_t = ds.upload_u(u.u)
-    di_t, dj_t = ds.upload_t(t.di, t.dj)
+    u_t = ds.upload_u(u.u, cache=True)
+    di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
     dref = _device_ref(ref, ds)
     return _metrics(*ds.error_maps(dref, u_t, di_t, dj_t))
 
@@ -252,8 +254,8 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
     ds = SCAN_CACHE.get(scan, w, m, roi)
     if ds.empty:
         raise ValueError("make_reference: empty good pixel/frame set")
-    u_t = ds.upload_u(u.u)
-    di_t, dj_t = ds.upload_t(t.di, t.dj)
+    u_t = ds.upload_u(u.u, cache=True)
+    di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
     gfut = ds.geometry_async(u_t, di_t, dj_t)
     dref = ds.object_map(u_t, di_t, dj_t, geom=gfut)
     history = [_metrics(*ds.error_maps(dref, u_t, di_t, dj_t))]
