@@ -190,14 +190,15 @@ __global__ void __launch_bounds__(kThreads, PXST_K4_OCC) k_err_pass(ErrArgs a, d
           pix += eps;
           if (inb[b])                                   // recon.py:425
             splat_grouped(img, a00[b], fx, fy, eps, 1.0);
-          if (FUSE && splat_b && live && b0 + h + b < nt) {   // next K1 (recon.py:135-138)
-            const int t = b0 + h + b;
+          if (FUSE) {                                   // next K1 (recon.py:135-138)
+            const int t = b0 + h + b < nt ? b0 + h + b : 0;
             const double xb = u0 - t_di[t] - static_cast<double>(n0b);
             const double yb = u1 - t_dj[t] - static_cast<double>(m0b);
-            if (xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1) {   // interp.py:103-107
-              const Split sx = split(xb), sy = split(yb);
+            const bool in_b = splat_b && live && b0 + h + b < nt && xb >= 0.0 && xb <= osb1 &&
+                              yb >= 0.0 && yb <= ofb1;   // interp.py:103-107
+            const Split sx = split(in_b ? xb : 0.0), sy = split(in_b ? yb : 0.0);
+            if (in_b)
               splat_grouped(img_b, (int64_t)sx.i * ofb + sy.i, sx.f, sy.f, (I * inv_W) * W2, W2);
-            }
           }
         }
       }

@@ -63,24 +63,25 @@ k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restr
       t_off[t] = f * plane;
     }
     __syncthreads();
-    if (!live) continue;
+    // every lane runs the loop (the splat is warp-cooperative); lanes
+    // without a work pixel splat nothing
     for (int b0 = 0; b0 < nt; b0 += kFB) {
       float4* out = img + ((kc - frame_lo + b0) / kFB / bpi) * n_o;
       float Iv[kFB];
 #pragma unroll
-      for (int b = 0; b < kFB; ++b) Iv[b] = b0 + b < nt ? __ldg(sc.frames + t_off[b0 + b] + p) : 0.f;
+      for (int b = 0; b < kFB; ++b)
+        Iv[b] = (live && b0 + b < nt) ? __ldg(sc.frames + t_off[b0 + b] + p) : 0.f;
 #pragma unroll
       for (int b = 0; b < kFB; ++b) {
         if (b0 + b >= nt) break;
         const double x = u0 - t_di[b0 + b] - static_cast<double>(n0);   // recon.py:138
         const double y = u1 - t_dj[b0 + b] - static_cast<double>(m0);
-        if (!(x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1)) {         // interp.py:103-107
-          ++dropped;
-          continue;
-        }
-        const Split sx = split(x), sy = split(y);
+        const bool in = x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;   // interp.py:103-107
+        dropped += (live && !in) ? 1 : 0;
+        const bool act = live && in;
+        const Split sx = split(act ? x : 0.0), sy = split(act ? y : 0.0);
         const double vw = (static_cast<double>(Iv[b]) * inv_w) * w2;   // value*weight (interp.py:112)
-        splat_grouped(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2);
+        splat_grouped_warp(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2, act);
       }
     }
   }
