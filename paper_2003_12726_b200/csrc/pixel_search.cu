@@ -356,7 +356,10 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       const float I = I_n, fwv = fw_n;
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
-      if (threadIdx.x == 0) {
+#ifndef PXST_K2_PRODUCER
+#define PXST_K2_PRODUCER 1
+#endif
+      if (PXST_K2_PRODUCER == 1 && threadIdx.x == 0) {
         // Refill freed slots without waiting for the slowest warp: frame k
         // reuses the slot of frame k - kNB; block only when this thread
         // itself needs frame jj next.
@@ -386,6 +389,10 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       engine_fast2<KA, KB>(ring + b * box + off, a.box_c, fx, fy, sW * (1.f - fx), sW * fx, sI,
                            acc);
       mbar_arrive(&empty[b]);
+      if (PXST_K2_PRODUCER == 0 && threadIdx.x == 0 && jj + kNB < nk) {
+        mbar_wait(&empty[b], ph);      // every thread is done with this slot
+        issue(jj + kNB);
+      }
     }
   }
   bool finished = false;
