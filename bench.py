@@ -225,9 +225,7 @@ def one_time_costs(ds, s, host_data, engine, torch):
     else:
         a.record(st)
         b.record(st)
-    check = engine._native.check
-    check(ds.lib.pxst_stack_stats(engine.ctypes.byref(ds.c_scan), None,
-                                  engine.ctypes.byref(ds.c_stats), engine._native.stream_ptr()))
+    ds.ready()                         # K0 (pxst_stack_stats), once per scan
     c.record(st)
     torch.cuda.synchronize()
     if host_data:

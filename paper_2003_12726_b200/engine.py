@@ -51,15 +51,22 @@ TRANSFER = {"h2d": 0, "d2h": 0}
 
 
 def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
-    """Host -> device copy of a contiguous array in the requested dtype."""
+    """Host -> device copy of a contiguous array in the requested dtype.
+
+    Never blocks the host on the device: a pageable array is staged through
+    a pinned buffer from torch's caching host allocator (which keeps the
+    block until the copy has run), then copied asynchronously like a pinned
+    one.  (A pageable cudaMemcpy would wait for everything queued before it,
+    e.g. a stack upload.)"""
     h = np.ascontiguousarray(a, dtype=dtype)
-    if not h.flags.writeable:
-        h = h.copy()
-    t = torch.from_numpy(h)
     TRANSFER["h2d"] += h.nbytes
-    if t.is_pinned():
-        return t.to(device, non_blocking=True)
-    return t.to(device)
+    if h.flags.writeable:
+        t = torch.from_numpy(h)
+        if t.is_pinned():
+            return t.to(device, non_blocking=True)
+    pin = torch.empty(h.shape, dtype=torch.from_numpy(h[:0].copy()).dtype, pin_memory=True)
+    np.copyto(pin.numpy(), h)
+    return pin.to(device, non_blocking=True)
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
@@ -190,20 +197,25 @@ class DeviceScan:
         r0, r1, c0, c1 = self.roi
         W = np.asarray(W)
         mask = np.asarray(mask)
+        self.good_idx = np.flatnonzero(np.asarray(good_frames)).astype(np.int32)
+        self.n_good = int(self.good_idx.size)
+        dev = self.device
+        # frames uploads still in flight: [(good_lo, good_hi, event)] on a copy
+        # stream (pinned host stacks; shared with band views through the dict)
+        self._upload = {"chunks": [], "waited": True, "stats": False}
+        self._uploads: list = []     # identity cache of pixel maps / translations
+        if frames_dev is None:
+            frames_dev = self._upload_frames(frames, dev)
+        self.frames = frames_dev
         work = np.zeros((self.ss, self.fs), dtype=np.uint8)
         if r1 > r0 and c1 > c0:
             work[r0:r1, c0:c1] = (mask[r0:r1, c0:c1] & (W[r0:r1, c0:c1] > 0)) != 0
         self.n_work = int(work.sum())
-        self.good_idx = np.flatnonzero(np.asarray(good_frames)).astype(np.int32)
-        self.n_good = int(self.good_idx.size)
-        dev = self.device
-        if frames_dev is None:
-            frames_dev = to_device(frames, np.float32, dev)
-        self.frames = frames_dev
         self.good = to_device(self.good_idx if self.n_good else np.zeros(1, np.int32), np.int32, dev)
         self.w64 = to_device(W, np.float64, dev)
         self.w32 = self.w64.to(torch.float32)
         self.work = to_device(work, np.uint8, dev)
+        self._work_host = work.astype(bool)
         roi4 = (ctypes.c_int64 * 4)(r0, max(r1, r0 + 1), c0, max(c1, c0 + 1))
         self.c_scan = PxstScan(self.frames.data_ptr(), self.n_frames, self.ss, self.fs,
                                self.good.data_ptr(), self.n_good, self.w64.data_ptr(),
@@ -218,17 +230,90 @@ class DeviceScan:
         self.scalars = torch.zeros(4, dtype=torch.float64, device=dev)
         self.c_stats = PxstStats(self.var_pm.data_ptr(), self.sigma2.data_ptr(),
                                  self.frame_norm.data_ptr(), self.scalars.data_ptr())
-        if not self.empty:
-            check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), None,
-                                            ctypes.byref(self.c_stats), stream_ptr()))
-        self._uploads: list = []     # identity cache of pixel maps / translations
+        # K0 (pxst_stack_stats) runs when a kernel first needs the stack
+        # statistics (ready()); object formation does not, so make_reference
+        # overlaps the stack upload instead of waiting behind K0.
+        self._upload["stats"] = self.empty
 
     @property
     def scalars_host(self) -> np.ndarray:
         """K0 scalars on the host (synchronises; not needed by the hot path)."""
         if self.empty:
             return np.array([1.0, 0.0, 0.0, 0.0])
+        self.ready()
         return to_host(self.scalars).copy()
+
+    # ------------------------------------------------- stack upload / K0
+    _UPLOAD_CHUNKS = 4
+
+    def _upload_frames(self, frames, dev):
+        """Stack to HBM.  A pinned host stack is copied in frame chunks on a
+        copy stream (one event per chunk), so object formation can splat the
+        chunks that have landed while the rest is in flight; every other
+        consumer waits for the whole stack (ready())."""
+        h = np.ascontiguousarray(frames, dtype=np.float32)
+        t = torch.from_numpy(h) if h.flags.writeable else None
+        if t is None or not t.is_pinned() or self.n_good == 0:
+            return to_device(frames, np.float32, dev)
+        out = torch.empty(t.shape, dtype=torch.float32, device=dev)
+        copy = torch.cuda.Stream(dev)
+        copy.wait_stream(torch.cuda.current_stream(dev))
+        good = self.good_idx
+        n = self._UPLOAD_CHUNKS
+        bounds = [int(good[min(len(good) - 1, (len(good) * c) // n)]) for c in range(n)]
+        bounds = sorted(set([0] + bounds[1:])) + [self.n_frames]
+        spans = [(f0, f1) for f0, f1 in zip(bounds[:-1], bounds[1:]) if f1 > f0]
+        chunks = []
+
+        def issue(span_list):
+            with torch.cuda.stream(copy):
+                for f0, f1 in span_list:
+                    out[f0:f1].copy_(t[f0:f1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                    g0, g1 = np.searchsorted(good, [f0, f1])
+                    chunks.append((int(g0), int(g1), ev))
+
+        issue(spans)
+        TRANSFER["h2d"] += h.nbytes
+        out.record_stream(copy)
+        self._upload.update(chunks=chunks, waited=False, host=t)
+        return out
+
+    def ready(self) -> "DeviceScan":
+        """Make the current stream wait for the whole stack and run K0 once."""
+        up = self._upload
+        if not up["waited"]:
+            st = torch.cuda.current_stream(self.device)
+            for _, _, ev in up["chunks"]:
+                st.wait_event(ev)
+            up.update(waited=True, host=None)
+        if not up["stats"]:
+            up["stats"] = True
+            check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), None,
+                                            ctypes.byref(self.c_stats), stream_ptr()))
+        return self
+
+    def host_bbox(self, u, di, dj):
+        """Grid rule (recon.py:126-132) from host arrays, in the device
+        kernel's arithmetic (exact min/max over work pixels and good frames,
+        NaN ignored); None when it does not apply (non-finite values).
+        make_reference uses it while the stack upload holds the copy engine
+        (inputs of a device bbox would queue behind the stack)."""
+        w = self._work_host
+        u = np.asarray(u, dtype=np.float64)
+        g = self.good_idx
+        di = np.asarray(di, dtype=np.float64)[g]
+        dj = np.asarray(dj, dtype=np.float64)[g]
+        vals = [np.fmin.reduce(u[0], axis=None, where=w, initial=np.inf),
+                np.fmax.reduce(u[0], axis=None, where=w, initial=-np.inf),
+                np.fmin.reduce(u[1], axis=None, where=w, initial=np.inf),
+                np.fmax.reduce(u[1], axis=None, where=w, initial=-np.inf),
+                np.fmin.reduce(di), np.fmax.reduce(di), np.fmin.reduce(dj), np.fmax.reduce(dj)]
+        vals = [float(v) for v in vals]
+        if not all(math.isfinite(v) for v in vals):
+            return None
+        return _grid_rule(vals)
 
     # ------------------------------------------------------------------ utils
     def _cached(self, arrays, make):
@@ -321,9 +406,21 @@ class DeviceScan:
         if acc is None:
             acc = torch.zeros((2, os_ * of), dtype=torch.float64, device=self.device)
         hi = self.n_good if frame_hi is None else frame_hi
-        check(self.lib.pxst_object_splat(
-            ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0, m0,
-            os_, of, frame_lo, hi, acc[0].data_ptr(), acc[1].data_ptr(), None, stream_ptr()))
+        up = self._upload
+        if up["waited"]:
+            ranges = [(frame_lo, hi)]
+        else:     # splat the chunks of the stack upload as they land
+            st = torch.cuda.current_stream(self.device)
+            ranges = []
+            for g0, g1, ev in up["chunks"]:
+                a, b = max(g0, frame_lo), min(g1, hi)
+                if a < b:
+                    st.wait_event(ev)
+                    ranges.append((a, b))
+        for a, b in ranges:
+            check(self.lib.pxst_object_splat(
+                ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0,
+                m0, os_, of, a, b, acc[0].data_ptr(), acc[1].data_ptr(), None, stream_ptr()))
         return acc
 
     def object_finish(self, acc, origin, shape) -> DeviceRef:
@@ -339,15 +436,26 @@ class DeviceScan:
         return DeviceRef(i_ref.view(os_, of), wsum.view(os_, of), fm.view(os_, of),
                          valid.view(os_, of), (int(origin[0]), int(origin[1])))
 
-    def object_map(self, u_t, di_t, dj_t, geom: "GeometryFuture | None" = None) -> DeviceRef:
+    def object_map(self, u_t, di_t, dj_t, geom: "GeometryFuture | None" = None,
+                   host=None) -> DeviceRef:
+        """host = the (u, di, dj) host arrays of this state, if the caller has
+        them and the stack upload is still in flight: the grid is then derived
+        on the host (host_bbox)."""
         if self.empty:
             raise ValueError("make_reference: empty good pixel/frame set")  # recon.py:116-117
-        n0, m0, shape = geom.bbox() if geom is not None else self.bbox(u_t, di_t, dj_t)
+        hb = None
+        if geom is None and host is not None and not self._upload["waited"]:
+            hb = self.host_bbox(*host)
+        if hb is not None:
+            n0, m0, shape = hb
+        else:
+            n0, m0, shape = geom.bbox() if geom is not None else self.bbox(u_t, di_t, dj_t)
         acc = self.object_splat(u_t, di_t, dj_t, n0, m0, shape)
         return self.object_finish(acc, (n0, m0), shape)
 
     # ---------------------------------------------------------- K2 pixel map
     def frame_weight_stats(self, fw_t: torch.Tensor) -> torch.Tensor:
+        self.ready()
         var_fw = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
         tmp_s2 = torch.zeros_like(var_fw)
         fn = torch.zeros_like(self.frame_norm)
@@ -360,6 +468,7 @@ class DeviceScan:
     def pixel_map_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                          subpixel_grid=None, refine=True, fw_t=None,
                          geom: "GeometryFuture | None" = None):
+        self.ready()
         u_out = torch.empty_like(u_t)
         err = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
         if self.empty:
@@ -379,6 +488,7 @@ class DeviceScan:
     # ------------------------------------------------------- K3 translations
     def translation_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                            subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None):
+        self.ready()
         di_out = di_t.clone()
         dj_out = dj_t.clone()
         if self.empty:
@@ -397,6 +507,7 @@ class DeviceScan:
         """View restricted to detector rows [r0, r1) of the ROI; shares every
         device buffer and the (full-ROI) statistics with this scan."""
         import copy
+        self.ready()
         v = copy.copy(self)
         R0, R1, C0, C1 = self.roi
         lo, hi = max(r0, R0), min(r1, R1)
@@ -410,6 +521,7 @@ class DeviceScan:
 
     def error_partials(self, ref: DeviceRef, u_t, di_t, dj_t):
         """K4 without normalisation: (per_frame, per_pixel, plane_num, plane_den)."""
+        self.ready()
         per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)
         per_pixel = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
         num = torch.zeros(ref.fm.numel(), dtype=torch.float64, device=self.device)
@@ -430,6 +542,7 @@ class DeviceScan:
 
     # ---------------------------------------------------------- K4 error maps
     def error_maps(self, ref: DeviceRef, u_t, di_t, dj_t):
+        self.ready()
         # pxst_error_maps zeroes per_frame / per_pixel / total and writes every
         # plane cell itself
         alloc = torch.zeros if self.empty else torch.empty
@@ -453,6 +566,7 @@ class DeviceScan:
         read on the device from `geom` (= geometry_async(u, di, dj)), and the
         accumulators are sized from the current grid plus `margin` cells per
         side.  Returns the error-map tensors and a PendingObject."""
+        self.ready()
         os_, of = ref.shape
         cap = (os_ + 2 * margin) * (of + 2 * margin)
         acc = torch.zeros((2, cap), dtype=torch.float64, device=self.device)

@@ -152,7 +152,7 @@ def make_reference(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         raise ValueError("make_reference: empty good pixel/frame set")
     u_t = ds.upload_u(u.u, cache=True)
     di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
-    return _ref_image(ds.object_map(u_t, di_t, dj_t), geom)
+    return _ref_image(ds.object_map(u_t, di_t, dj_t, host=(u.u, t.di, t.dj)), geom)
 
 
 make_object_map = make_reference
