@@ -225,7 +225,7 @@ def one_time_costs(ds, s, host_data, engine, torch):
     else:
         a.record(st)
         b.record(st)
-    ds.ready()                         # K0 (pxst_stack_stats), once per scan
+    ds.ready(frame_stats=True)         # K0 (pxst_stack_stats, both parts), once per scan
     c.record(st)
     torch.cuda.synchronize()
     if host_data:

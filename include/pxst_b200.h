@@ -85,6 +85,14 @@ int64_t pxst_launch_count(void);
 int pxst_stack_stats(const pxst_scan* scan, const float* fw, const pxst_stats* st,
                      void* stream);
 
+/* The same statistics in two independent parts: PXST_STATS_PIXEL = max W,
+ * var_pm, sigma2 (what K2 and K4 read); PXST_STATS_FRAME = frame_norm and
+ * the |I| sums (what K3 reads).  pxst_stack_stats = both. */
+#define PXST_STATS_PIXEL 1
+#define PXST_STATS_FRAME 2
+int pxst_stack_stats_parts(const pxst_scan* scan, const float* fw, const pxst_stats* st,
+                           int parts, void* stream);
+
 /* Bounding box of u over work pixels and of (di, dj) over good frames:
  * out[8] (device, float64) = min u0, max u0, min u1, max u1, min di, max di,
  * min dj, max dj.  Feeds the grid rule of recon.py:126-132. */

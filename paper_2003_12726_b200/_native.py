@@ -46,6 +46,8 @@ _SIGS = {
     "pxst_last_error": (c_char_p, []),
     "pxst_launch_count": (c_int64, []),
     "pxst_stack_stats": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_void_p]),
+    "pxst_stack_stats_parts": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_int,
+                                       c_void_p]),
     "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pxst_object_splat": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
                                   c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,

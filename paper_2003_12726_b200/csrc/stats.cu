@@ -257,23 +257,18 @@ int check_scan(const pxst_scan* sc) {
 
 using namespace pxst;
 
-extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst_stats* st,
-                                void* stream) {
-  if (int e = check_scan(sc)) return e;
-  PXST_REQUIRE(st && st->var_pm && st->sigma2 && st->frame_norm && st->scalars,
-               "stats descriptor has a NULL pointer");
-  PXST_REQUIRE(sc->n_good > 0, "no good frames");
-  cudaStream_t s = as_stream(stream);
+namespace {
+
+// K0 per-pixel part: max W (scalars[0], scalars[2]), var_pm, sigma2.
+int pixel_part(const pxst_scan* sc, const float* fw, const pxst_stats* st, cudaStream_t s) {
   const int64_t plane = sc->ss * sc->fs;
   PXST_CHECK_CUDA(cudaMemsetAsync(st->var_pm, 0, sizeof(double) * plane, s));
   PXST_CHECK_CUDA(cudaMemsetAsync(st->sigma2, 0, sizeof(double) * plane, s));
   const int nb = partial_blocks(sc);
   Scratch part;
-  if (int e = part.alloc(sizeof(double) * (2 * nb + 3 * sc->n_good), s)) return e;
+  if (int e = part.alloc(sizeof(double) * 2 * nb, s)) return e;
   double* pm = part.as<double>();
   double* pc = pm + nb;
-  double* fiw = pc + nb;
-  double* fi = fiw + sc->n_good;
   k_wmax_partial<<<nb, kThreads, 0, s>>>(*sc, pm, pc);
   PXST_CHECK_LAUNCH();
   k_wmax_final<<<1, 1024, 0, s>>>(pm, pc, nb, st->scalars);
@@ -283,13 +278,20 @@ extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst
   PXST_REQUIRE(rw <= kMaxGridY, "ROI too tall");
   k_pixel_stats<<<g, 128, 0, s>>>(*sc, fw, st->scalars, st->var_pm, st->sigma2);
   PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+// K0 per-frame part: frame_norm, scalars[1], scalars[3].
+int frame_part(const pxst_scan* sc, const pxst_stats* st, cudaStream_t s) {
   const int64_t rows = sc->roi[1] - sc->roi[0];
   int64_t slices = (4 * 148 + sc->n_good - 1) / sc->n_good;
   slices = slices < 1 ? 1 : (slices > rows ? rows : slices);
   if (slices > 64) slices = 64;
   Scratch fpart;
-  if (int e = fpart.alloc(sizeof(double) * 3 * slices * sc->n_good, s)) return e;
+  if (int e = fpart.alloc(sizeof(double) * (3 * slices + 2) * sc->n_good, s)) return e;
   double* pn = fpart.as<double>();
+  double* fiw = pn + 3 * slices * sc->n_good;
+  double* fi = fiw + sc->n_good;
   k_frame_stats<<<dim3((unsigned)sc->n_good, (unsigned)slices), 256, 0, s>>>(
       *sc, pn, pn + slices * sc->n_good, pn + 2 * slices * sc->n_good);
   PXST_CHECK_LAUNCH();
@@ -300,6 +302,28 @@ extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst
   k_sum_final<<<1, 1024, 0, s>>>(fiw, fi, sc->n_good, st->scalars + 1, st->scalars + 3);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
+}
+
+}  // namespace
+
+extern "C" int pxst_stack_stats_parts(const pxst_scan* sc, const float* fw,
+                                      const pxst_stats* st, int parts, void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(st && st->var_pm && st->sigma2 && st->frame_norm && st->scalars,
+               "stats descriptor has a NULL pointer");
+  PXST_REQUIRE(sc->n_good > 0, "no good frames");
+  PXST_REQUIRE(parts >= 1 && parts <= 3, "parts must be PXST_STATS_PIXEL and/or _FRAME");
+  cudaStream_t s = as_stream(stream);
+  if (parts & PXST_STATS_PIXEL)
+    if (int e = pixel_part(sc, fw, st, s)) return e;
+  if (parts & PXST_STATS_FRAME)
+    if (int e = frame_part(sc, st, s)) return e;
+  return PXST_OK;
+}
+
+extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst_stats* st,
+                                void* stream) {
+  return pxst_stack_stats_parts(sc, fw, st, PXST_STATS_PIXEL | PXST_STATS_FRAME, stream);
 }
 
 extern "C" int pxst_bbox(const pxst_scan* sc, const double* u, const double* di,

@@ -202,7 +202,7 @@ class DeviceScan:
         dev = self.device
         # frames uploads still in flight: [(good_lo, good_hi, event)] on a copy
         # stream (pinned host stacks; shared with band views through the dict)
-        self._upload = {"chunks": [], "waited": True, "stats": False}
+        self._upload = {"chunks": [], "waited": True, "stats": 0}   # stats: K0 parts run
         self._uploads: list = []     # identity cache of pixel maps / translations
         if frames_dev is None:
             frames_dev = self._upload_frames(frames, dev)
@@ -233,14 +233,14 @@ class DeviceScan:
         # K0 (pxst_stack_stats) runs when a kernel first needs the stack
         # statistics (ready()); object formation does not, so make_reference
         # overlaps the stack upload instead of waiting behind K0.
-        self._upload["stats"] = self.empty
+        self._upload["stats"] = 3 if self.empty else 0
 
     @property
     def scalars_host(self) -> np.ndarray:
         """K0 scalars on the host (synchronises; not needed by the hot path)."""
         if self.empty:
             return np.array([1.0, 0.0, 0.0, 0.0])
-        self.ready()
+        self.ready(frame_stats=True)
         return to_host(self.scalars).copy()
 
     # ------------------------------------------------- stack upload / K0
@@ -280,18 +280,22 @@ class DeviceScan:
         self._upload.update(chunks=chunks, waited=False, host=t)
         return out
 
-    def ready(self) -> "DeviceScan":
-        """Make the current stream wait for the whole stack and run K0 once."""
+    def ready(self, frame_stats: bool = False) -> "DeviceScan":
+        """Make the current stream wait for the whole stack and run the K0
+        parts not yet run: the per-pixel part always (K2, K4), the per-frame
+        part (frame_norm) only for K3."""
         up = self._upload
         if not up["waited"]:
             st = torch.cuda.current_stream(self.device)
             for _, _, ev in up["chunks"]:
                 st.wait_event(ev)
             up.update(waited=True, host=None)
-        if not up["stats"]:
-            up["stats"] = True
-            check(self.lib.pxst_stack_stats(ctypes.byref(self.c_scan), None,
-                                            ctypes.byref(self.c_stats), stream_ptr()))
+        parts = (0 if up["stats"] & 1 else 1) | (2 if frame_stats and not up["stats"] & 2 else 0)
+        if parts:
+            up["stats"] |= parts
+            check(self.lib.pxst_stack_stats_parts(ctypes.byref(self.c_scan), None,
+                                                  ctypes.byref(self.c_stats), parts,
+                                                  stream_ptr()))
         return self
 
     def host_bbox(self, u, di, dj):
@@ -488,7 +492,7 @@ class DeviceScan:
     # ------------------------------------------------------- K3 translations
     def translation_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                            subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None):
-        self.ready()
+        self.ready(frame_stats=True)
         di_out = di_t.clone()
         dj_out = dj_t.clone()
         if self.empty:
