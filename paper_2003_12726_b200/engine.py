@@ -244,7 +244,8 @@ class DeviceScan:
         return to_host(self.scalars).copy()
 
     # ------------------------------------------------- stack upload / K0
-    _UPLOAD_CHUNKS = 4
+    _UPLOAD_CHUNKS = 1     # (object formation's other inputs queue behind the stack on
+                           # the copy engine, so splitting its splat bought nothing)
 
     def _upload_frames(self, frames, dev):
         """Stack to HBM.  A pinned host stack is copied in frame chunks on a
@@ -304,15 +305,23 @@ class DeviceScan:
         NaN ignored); None when it does not apply (non-finite values).
         make_reference uses it while the stack upload holds the copy engine
         (inputs of a device bbox would queue behind the stack)."""
-        w = self._work_host
+        w = self._work_host.ravel()
         u = np.asarray(u, dtype=np.float64)
         g = self.good_idx
         di = np.asarray(di, dtype=np.float64)[g]
         dj = np.asarray(dj, dtype=np.float64)[g]
-        vals = [np.fmin.reduce(u[0], axis=None, where=w, initial=np.inf),
-                np.fmax.reduce(u[0], axis=None, where=w, initial=-np.inf),
-                np.fmin.reduce(u[1], axis=None, where=w, initial=np.inf),
-                np.fmax.reduce(u[1], axis=None, where=w, initial=-np.inf),
+
+        def ext(plane, lo):
+            # unmasked extremum first: when a work pixel attains it, it is the
+            # masked one too (nearly every pixel is a work pixel)
+            flat = plane.ravel()
+            k = int(np.argmin(flat) if lo else np.argmax(flat))
+            if w[k]:
+                return flat[k]
+            red = np.fmin.reduce if lo else np.fmax.reduce
+            return red(plane, axis=None, where=self._work_host, initial=np.inf if lo else -np.inf)
+
+        vals = [ext(u[0], True), ext(u[0], False), ext(u[1], True), ext(u[1], False),
                 np.fmin.reduce(di), np.fmax.reduce(di), np.fmin.reduce(dj), np.fmax.reduce(dj)]
         vals = [float(v) for v in vals]
         if not all(math.isfinite(v) for v in vals):
