@@ -160,7 +160,9 @@ __device__ __forceinline__ void finish_pixel(const PixArgs& a, int64_t p, int be
 // ---------------------------------------------------------------------------
 // 1. tile geometry
 // ---------------------------------------------------------------------------
-__global__ void k_tile_geo(PixArgs a, TileGeo* geo) {
+// With init_out, every ROI pixel also gets u_out = u, err_out = 0 (the
+// search's finishers then overwrite the work pixels).
+__global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out) {
   __shared__ double red[kWarps][4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + tile_dr(threadIdx.x);
@@ -169,6 +171,11 @@ __global__ void k_tile_geo(PixArgs a, TileGeo* geo) {
   const int64_t p = inroi ? row * a.sc.fs + col : 0;
   const bool live = inroi && a.sc.work[p] != 0;
   const int64_t plane = a.sc.ss * a.sc.fs;
+  if (init_out && inroi) {
+    a.u_out[p] = a.u[p];
+    a.u_out[plane + p] = a.u[plane + p];
+    a.err_out[p] = 0.0;
+  }
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
   double mn0 = warp_min(live ? u0 : INFINITY), mx0 = warp_max(live ? u0 : -INFINITY);
   double mn1 = warp_min(live ? u1 : INFINITY), mx1 = warp_max(live ? u1 : -INFINITY);
@@ -709,9 +716,19 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   PXST_REQUIRE(!fw || var_fw, "frame weights need their normaliser var_fw");
   cudaStream_t s = as_stream(stream);
   const int64_t plane = sc->ss * sc->fs;
-  PXST_CHECK_CUDA(cudaMemcpyAsync(u_out, u_in, sizeof(double) * 2 * plane,
-                                  cudaMemcpyDeviceToDevice, s));
-  PXST_CHECK_CUDA(cudaMemsetAsync(err_out, 0, sizeof(double) * plane, s));
+  // u_out = u_in, err_out = 0 outside the work set: done by k_tile_geo for the
+  // ROI on the fast path when the ROI is the whole detector, else here
+  const bool full_roi = sc->roi[0] == 0 && sc->roi[1] == sc->ss && sc->roi[2] == 0 &&
+                        sc->roi[3] == sc->fs;
+  const bool fast_init = full_roi && sc->n_good > 0 && subpixel_step == 0.0 &&
+                         !force_generic() &&
+                         find_fast(static_cast<int>(2 * half_ss + 1),
+                                   static_cast<int>(2 * half_fs + 1)) != nullptr;
+  if (!fast_init) {
+    PXST_CHECK_CUDA(cudaMemcpyAsync(u_out, u_in, sizeof(double) * 2 * plane,
+                                    cudaMemcpyDeviceToDevice, s));
+    PXST_CHECK_CUDA(cudaMemsetAsync(err_out, 0, sizeof(double) * plane, s));
+  }
   if (sc->n_good == 0) return PXST_OK;
 
   const std::vector<double> oa = window_offsets(half_ss, subpixel_step);
@@ -774,7 +791,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
       tbase = fmpad.as<float>();
     }
     dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
-    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>());
+    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>(), fast_init ? 1 : 0);
     PXST_CHECK_LAUNCH();
     // Size the TMA box from the largest tile footprint (|du/dx| reaches ~1.8
     // at the edges of the config-3 map), capped at 24 KB per ring slot; tiles
@@ -922,7 +939,8 @@ extern "C" int pxst_tile_spans(const pxst_scan* sc, const double* u, int32_t* sp
   const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
   Scratch geo;
   if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
-  k_tile_geo<<<dim3((unsigned)a.tiles_x, (unsigned)tiles_y), kThreads, 0, s>>>(a, geo.as<TileGeo>());
+  k_tile_geo<<<dim3((unsigned)a.tiles_x, (unsigned)tiles_y), kThreads, 0, s>>>(a, geo.as<TileGeo>(),
+                                                                             0);
   PXST_CHECK_LAUNCH();
   return tile_span_max_dev(geo.as<TileGeo>(), tiles, spans, s);
 }

@@ -12,33 +12,35 @@ namespace {
 // [j+lc, j+hc] exists and is valid, as a separable AND over a 32 x 32 output
 // tile with its halo staged in shared memory (one launch); optionally also
 // the NaN-encoded float32 reference of the tile's cells (make_nan_ref).
-constexpr int kPvT = 32, kPvMaxHalo = 64;
+constexpr int kPvC = 32, kPvR = 16, kPvMaxHalo = 64;   // output tile: 16 rows x 32 cols
 
 __global__ void __launch_bounds__(256) k_pv_tile(const uint8_t* __restrict__ valid,
                                                  const float* __restrict__ fm, int os, int of,
                                                  int lr, int hr, int lc, int hc,
                                                  uint8_t* __restrict__ pv, float* __restrict__ fmn) {
-  __shared__ uint8_t v[kPvT + kPvMaxHalo][kPvT + kPvMaxHalo];
-  __shared__ uint8_t rowok[kPvT + kPvMaxHalo][kPvT];
-  const int i0 = blockIdx.y * kPvT, j0 = blockIdx.x * kPvT;
-  const int th = kPvT + hr - lr, tw = kPvT + hc - lc;
-  for (int k = threadIdx.x; k < th * tw; k += blockDim.x) {
-    const int r = i0 + lr + k / tw, c = j0 + lc + k % tw;
-    v[k / tw][k % tw] = (r >= 0 && r < os && c >= 0 && c < of) ? valid[r * of + c] : 0;
-  }
+  __shared__ uint8_t v[kPvR + kPvMaxHalo][kPvC + kPvMaxHalo];
+  __shared__ uint8_t rowok[kPvR + kPvMaxHalo][kPvC];
+  const int tx = threadIdx.x, ty = threadIdx.y;          // 32 x 8 threads
+  const int i0 = blockIdx.y * kPvR, j0 = blockIdx.x * kPvC;
+  const int th = kPvR + hr - lr, tw = kPvC + hc - lc;
+  for (int rr = ty; rr < th; rr += 8)
+    for (int cc = tx; cc < tw; cc += 32) {
+      const int r = i0 + lr + rr, c = j0 + lc + cc;
+      v[rr][cc] = (r >= 0 && r < os && c >= 0 && c < of) ? valid[r * of + c] : 0;
+    }
   __syncthreads();
-  for (int k = threadIdx.x; k < th * kPvT; k += blockDim.x) {
-    const int rr = k / kPvT, cc = k % kPvT;
+  for (int rr = ty; rr < th; rr += 8) {
     uint8_t ok = 1;
-    for (int d = 0; d <= hc - lc; ++d) ok &= v[rr][cc + d];
-    rowok[rr][cc] = ok;
+    for (int d = 0; d <= hc - lc; ++d) ok &= v[rr][tx + d];
+    rowok[rr][tx] = ok;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kPvT * kPvT; k += blockDim.x) {
-    const int rr = k / kPvT, cc = k % kPvT, i = i0 + rr, j = j0 + cc;
+  const int j = j0 + tx;
+  for (int rr = ty; rr < kPvR; rr += 8) {
+    const int i = i0 + rr;
     if (i >= os || j >= of) continue;
     uint8_t ok = 1;
-    for (int d = 0; d <= hr - lr; ++d) ok &= rowok[rr + d][cc];
+    for (int d = 0; d <= hr - lr; ++d) ok &= rowok[rr + d][tx];
     pv[i * of + j] = ok;
     if (fmn) fmn[i * of + j] = valid[i * of + j] ? fm[i * of + j] : __int_as_float(0x7fc00000);
   }
@@ -90,9 +92,9 @@ int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, fl
             cudaStream_t s) {
   PXST_REQUIRE(lr <= hr && lc <= hc && hr - lr <= kPvMaxHalo && hc - lc <= kPvMaxHalo,
                "patch extent too large");
-  dim3 g((unsigned)((ref->of + kPvT - 1) / kPvT), (unsigned)((ref->os + kPvT - 1) / kPvT));
+  dim3 g((unsigned)((ref->of + kPvC - 1) / kPvC), (unsigned)((ref->os + kPvR - 1) / kPvR));
   PXST_REQUIRE(g.y <= kMaxGridY, "reference image too tall");
-  k_pv_tile<<<g, 256, 0, s>>>(ref->valid, ref->fm, static_cast<int>(ref->os),
+  k_pv_tile<<<g, dim3(32, 8), 0, s>>>(ref->valid, ref->fm, static_cast<int>(ref->os),
                               static_cast<int>(ref->of), lr, hr, lc, hc, pv, fmn);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
