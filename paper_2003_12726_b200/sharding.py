@@ -169,10 +169,13 @@ class ShardedIteration:
     def error_maps(self, ref, u, di, dj) -> ShardedMetrics:
         per_frame, per_pixel, num, den = self.ex.error_partials(ref, u, di, dj,
                                                                 rows=self.rows[self.rank])
-        self._all_reduce(per_frame)
-        self._all_reduce(per_pixel)
-        self._all_reduce(num)
-        self._all_reduce(den)
+        # one all-reduce for the four partial sums (launch latency, not
+        # bandwidth, dominates collectives of a few MB over NVSwitch)
+        parts = (per_frame, per_pixel, num, den)
+        flat = torch.cat([t.reshape(-1) for t in parts])
+        self._all_reduce(flat)
+        views = torch.split(flat, [t.numel() for t in parts])
+        per_frame, per_pixel, num, den = (v.view(t.shape) for v, t in zip(views, parts))
         plane = self.ex.error_finish(num, den, ref)
         good = self.ex.good_index_tensor()
         total = per_frame[good].sum().reshape(1) if len(good) else per_frame.new_zeros(1)
