@@ -212,6 +212,31 @@ def test_cfg1_pixel_map_band(scan1, golden1):
     np.testing.assert_allclose(ef[band[0]:band[1]], e[band[0]:band[1]], rtol=1e-5, atol=1e-12)
 
 
+@pytest.mark.parametrize("band", [(0, 8), (248, 256)])
+@pytest.mark.parametrize("refine", [False, True])
+def test_cfg1_full_frame_work_units(scan1, golden1, band, refine):
+    """The full-frame config-1 search (whole-tile units finished inside
+    k_pix_fast or, for pixels with skipped samples, inside k_pix_slow; the last
+    partial wave's tiles frame-split through the epilogue) against the oracle
+    on the top rows (whole-tile units, grid-edge slow samples) and the bottom
+    rows (frame-split units)."""
+    s = scan1
+    ref = ref_from(golden1)
+    u, e = pb.update_pixel_map(s.scan, s.w, s.m, ref, s.u0, s.t0, pb.SearchWindow(5, 5),
+                               pb.UpdateOptions(quadratic_refinement=refine))
+    roi = (band[0], band[1], 0, s.w.w.shape[1])
+    uo, eo, stack = oracle_pixel_map(s, ref, s.u0.u, s.t0.di, s.t0.dj, (5, 5), refine, roi)
+    r, c = work_rc(s, roi)
+    uniq = unique_pixels(stack)
+    assert uniq.mean() > 0.97, uniq.mean()
+    gu, ou = u.u[:, r, c], uo[:, r, c]
+    if not refine:
+        np.testing.assert_array_equal(gu[:, uniq], ou[:, uniq])
+    assert np.abs(gu - ou).max(axis=0)[uniq].max() < PX_TOL
+    eg, eo_ = e[r, c][uniq], eo[r, c][uniq]
+    assert np.max(np.abs(eg - eo_) / np.maximum(np.abs(eo_), 1e-12)) < 1e-4
+
+
 def test_cfg1_translation_subset(scan1, golden1):
     s = scan1
     g = golden1
