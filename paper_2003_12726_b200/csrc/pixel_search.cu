@@ -48,7 +48,6 @@ __device__ __forceinline__ int tile_dc(int tid) { return ((tid >> 5) & 1) * 8 + 
 #define PXST_K2_RING 4
 #endif
 constexpr int kNB = PXST_K2_RING;  // TMA ring depth
-constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
 
 
 struct PixArgs {
@@ -443,10 +442,178 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
 // ---------------------------------------------------------------------------
 // 3. slow-sample fix-up (runs after k_pix_fast on the same stream).
 //    k_pix_fast appends (pixel, chunk) pairs that own skipped samples to a
-//    list; k_pix_slow: one warp per listed pair, lanes over trials, frames in
-//    order; each (chunk, trial, pixel) partial is owned by one lane, so the
-//    result does not depend on list order.
+//    list; k_pix_slow: one warp per listed pair (fetched dynamically: an
+//    entry's cost ranges from one to all frames).  Lanes classify 32 frames
+//    at a time with the fast kernel's eligibility test.  Windows of up to 3
+//    rows (k_pix_slow_rows; larger ones: k_pix_slow, lanes over trials) then
+//    evaluate the skipped samples by "row lanes": lane l works on sample slot l / Ka and
+//    owns trial row l % Ka, loading that row's two patch rows once (Kb + 1
+//    cells each, NaN-encoded reference, off-grid cells marked) and evaluating
+//    its Kb trials exactly from registers (trial_patch: the reference's masked
+//    renormalised read and (I-W)^2 fallback).  32 / Ka samples are in flight
+//    per warp; each slot's partial sums are added in a fixed slot order, so
+//    the result does not depend on the list order or on timing.
 // ---------------------------------------------------------------------------
+constexpr int kRowMax = 17;        // widest fast-path window row (1 x 17)
+
+__device__ __forceinline__ float slow_cell(const float* __restrict__ fmn, int os, int of, int r,
+                                           int c) {
+  return (r >= 0 && r < os && c >= 0 && c < of) ? __ldg(fmn + (r * of + c))
+                                                : __uint_as_float(kOffGrid);
+}
+
+__global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
+                                                      const unsigned long long* __restrict__ list,
+                                                      unsigned* __restrict__ list_n) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
+  const int lane = threadIdx.x & 31;
+  const unsigned n = list_n[0];
+  unsigned* next = list_n + 1;       // work counter
+  const int ka = a.ka, kb = a.kb;
+  const int ra = (ka - 1) / 2, rb = (kb - 1) / 2;
+  const int nk = ka * kb;
+  const int nslot = 32 / ka;         // samples in flight per warp
+  const int slot = lane / ka, trow = lane % ka;
+  const bool lane_on = slot < nslot;
+  const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  for (;;) {
+    unsigned e = 0;
+    if (lane == 0) e = atomicAdd(next, 1u);
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (e >= n) break;
+    const unsigned long long ent = list[e];
+    const int64_t q = static_cast<int64_t>(ent >> 20);
+    const unsigned chunk = static_cast<unsigned>(ent & 0xFFFFF);
+    const int64_t rr = q / cw, cc = q % cw;
+    const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
+    const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
+    const double u0 = a.u[p], u1 = a.u[plane + p];
+    const float W = a.sc.w32[p];
+    int64_t k_lo, k_hi, pslot;
+    chunk_frames(a, chunk, k_lo, k_hi, pslot);
+    float* out = a.partial + pslot * nk * a.nq + q;
+    float acc[kRowMax];              // this lane's trial row, its slot's samples
+    float prev[kRowMax];             // slot 0: the fast kernel's partials of the row
+#pragma unroll
+    for (int c = 0; c < kRowMax; ++c) {
+      acc[c] = 0.f;
+      prev[c] = (slot == 0 && c < kb) ? out[(int64_t)(trow * kb + c) * a.nq] : 0.f;
+    }
+    for (int64_t k0 = k_lo; k0 < k_hi; k0 += 32) {
+      // lane-parallel classification of 32 frames; each lane keeps its
+      // frame's sample and stack value for the row lanes below
+      const int64_t kl = k0 + lane;
+      bool slow = false;
+      Sample sl{};
+      float Il = 0.f, fwl = 1.f;
+      if (kl < k_hi) {
+        const int64_t f = a.sc.good[kl];
+        fwl = a.fw ? __ldg(a.fw + f * plane + p) : 1.f;
+        const double dI = a.di[f], dJ = a.dj[f];
+        int wr0, wc0;
+        window_origin(a, g, dI, dJ, wr0, wc0);
+        sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
+        slow = !sl.fast();
+        if (slow) Il = __ldg(a.sc.frames + f * plane + p);
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, slow);
+      if (a.dbg) {   // skipped samples by reason: off grid, outside the box, patch invalid
+        const bool in = sl.i >= 0 && sl.i < a.os && sl.j >= 0 && sl.j < a.of;
+        const bool inbox = sl.lr >= 0 && sl.lr + a.ka + 1 <= a.box_r && sl.lc >= 0 &&
+                           sl.lc + a.kb + 1 <= a.box_c;
+        const unsigned m1 = __ballot_sync(0xffffffffu, slow && !in);
+        const unsigned m2 = __ballot_sync(0xffffffffu, slow && in && !inbox);
+        if (lane == 0) {
+          atomicAdd(a.dbg, (unsigned long long)__popc(mask));
+          atomicAdd(a.dbg + 1, (unsigned long long)__popc(m1));
+          atomicAdd(a.dbg + 2, (unsigned long long)__popc(m2));
+        }
+      }
+      while (mask) {
+        // slot s takes the (s+1)-th lowest set bit: samples stay in frame
+        // order within a slot
+        const int cnt = __popc(mask);
+        const int bsel = (lane_on && slot < cnt) ? static_cast<int>(__fns(mask, 0, slot + 1)) : -1;
+        const int src = bsel >= 0 ? bsel : 0;
+        const int si = __shfl_sync(0xffffffffu, sl.i, src);
+        const int sj = __shfl_sync(0xffffffffu, sl.j, src);
+        const double sfx = __shfl_sync(0xffffffffu, sl.fx, src);
+        const double sfy = __shfl_sync(0xffffffffu, sl.fy, src);
+        const float sI = __shfl_sync(0xffffffffu, Il, src);
+        const float sfw = __shfl_sync(0xffffffffu, fwl, src);
+        if (cnt <= nslot) {
+          mask = 0u;
+        } else {
+          const unsigned last = __fns(mask, 0, nslot);      // bit of the last slot's sample
+          mask &= ~((2u << last) - 1u);
+        }
+        if (bsel >= 0) {
+          const ExactSample es = exact_sample(sfx, sfy, W, sI, sfw);
+          const int pr = si - ra + trow, pc = sj - rb;
+          float r0[kRowMax + 1], r1[kRowMax + 1];
+#pragma unroll
+          for (int c = 0; c <= kRowMax; ++c) {
+            r0[c] = c <= kb ? slow_cell(a.fmn, os, of, pr, pc + c) : 0.f;
+            r1[c] = c <= kb ? slow_cell(a.fmn, os, of, pr + 1, pc + c) : 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < kRowMax; ++c)
+            if (c < kb) acc[c] += trial_patch(r0[c], r0[c + 1], r1[c], r1[c + 1], es);
+        }
+      }
+    }
+    // slot partials into slot 0, fixed order
+    for (int s = 1; s < nslot; ++s) {
+#pragma unroll
+      for (int c = 0; c < kRowMax; ++c) {
+        const float v = __shfl_sync(0xffffffffu, acc[c], (s * ka + trow) & 31);
+        if (slot == 0) acc[c] += v;
+      }
+    }
+    float tot[kRowMax];
+#pragma unroll
+    for (int c = 0; c < kRowMax; ++c) tot[c] = prev[c] + acc[c];
+    if (chunk != kAllFrames) {
+      if (slot == 0) {
+#pragma unroll
+        for (int c = 0; c < kRowMax; ++c)
+          if (c < kb) out[(int64_t)(trow * kb + c) * a.nq] = tot[c];
+      }
+      continue;
+    }
+    // Whole-tile pixel: every frame is in, finish it here.  Warp first-
+    // occurrence argmin (smaller sum, ties to the smaller trial index).
+    int best = -1;
+    float bsum = 0.f;
+    if (slot == 0) {
+#pragma unroll
+      for (int c = 0; c < kRowMax; ++c)
+        if (c < kb && (best < 0 || tot[c] < bsum)) { bsum = tot[c]; best = trow * kb + c; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bsum, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+      if (ob >= 0 && (best < 0 || ov < bsum || (ov == bsum && ob < best))) { bsum = ov; best = ob; }
+    }
+    finish_pixel(a, p, best, static_cast<double>(bsum), u0, u1, a.var[p],
+                 a.offs_a[best / kb], a.offs_b[best % kb], [&](int t) {
+                   const int c = t % kb;
+                   float v = tot[0];
+#pragma unroll
+                   for (int j = 1; j < kRowMax; ++j) v = c == j ? tot[j] : v;
+                   return static_cast<double>(__shfl_sync(0xffffffffu, v, t / kb));
+                 });
+  }
+}
+
+// Lane-per-trial variant for windows of 5 rows and more (row lanes would
+// leave a third of the warp idle and serialise each lane's Kb trials): lanes
+// own trials lane + 32 j and read each trial's corners straight from the
+// NaN-encoded reference (trial_global), in frame order.
+constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
+
 __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                                                  const unsigned long long* __restrict__ list,
                                                  unsigned* __restrict__ list_n) {
@@ -868,7 +1035,10 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_REQUIRE(units < (int64_t(1) << 31), "ROI too large");
     fn<<<(unsigned)units, kThreads, smem, s>>>(tmap, a);
     PXST_CHECK_LAUNCH();
-    k_pix_slow<<<2 * sms, 256, 0, s>>>(a, list, list_n);
+    if (na <= 3)          // 1 x N / 3 x N windows: >= 10 samples in flight per warp
+      k_pix_slow_rows<<<2 * sms, 256, 0, s>>>(a, list, list_n);
+    else
+      k_pix_slow<<<2 * sms, 256, 0, s>>>(a, list, list_n);
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;

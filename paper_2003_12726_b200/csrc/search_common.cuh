@@ -207,6 +207,33 @@ __device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int
   return ok ? e.fwv * (r * r) : e.fb;
 }
 
+// Same trial from four corner values in registers (off-grid cells carry
+// kOffGrid, a NaN with its own payload, so one value gives position, validity
+// and value).  Equal to trial_global: the reference's bounds rule (row in
+// [0, os-1), or os-1 with zero row weight; likewise for columns) is "base
+// corner on the grid and every corner with nonzero weight on the grid".
+constexpr unsigned kOffGrid = 0xffc0beefu;
+__device__ __forceinline__ bool on_grid(float v) { return __float_as_uint(v) != kOffGrid; }
+
+__device__ __forceinline__ float trial_patch(float v00, float v01, float v10, float v11,
+                                             const ExactSample& e) {
+  const bool in = on_grid(v00) && (!e.fxp || on_grid(v10)) && (!e.fyp || on_grid(v01));
+  const bool m00 = v00 == v00;
+  const bool m01 = e.fyp && v01 == v01;
+  const bool m10 = e.fxp && v10 == v10;
+  const bool m11 = e.fxp && e.fyp && v11 == v11;
+  float den = m00 ? e.w00 : 0.f;
+  float num = m00 ? e.w00 * v00 : 0.f;
+  den += m01 ? e.w01 : 0.f;
+  num = fmaf(m01 ? e.w01 : 0.f, m01 ? v01 : 0.f, num);
+  den += m10 ? e.w10 : 0.f;
+  num = fmaf(m10 ? e.w10 : 0.f, m10 ? v10 : 0.f, num);
+  den += m11 ? e.w11 : 0.f;
+  num = fmaf(m11 ? e.w11 : 0.f, m11 ? v11 : 0.f, num);
+  const float r = fmaf(-e.W, __fdividef(num, den), e.I);
+  return (in && (m00 || m01 || m10 || m11)) ? e.fwv * (r * r) : e.fb;
+}
+
 // float32 reference with NaN on invalid cells, [os*of] (for trial_global).
 int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s);
 
