@@ -164,7 +164,8 @@ __device__ __forceinline__ int full_index(const TransArgs& a, int t, int s) {
 // ---------------------------------------------------------------------------
 template <int KA, int KB>
 #ifndef PXST_K3_OCC2_BELOW
-#define PXST_K3_OCC2_BELOW 72
+#define PXST_K3_OCC2_BELOW 82   // up to 9 x 9 at 2 CTAs/SM: the 128-register cap spills a few
+                                  // values but the doubled warps win (config 4: -11 %)
 #endif
 __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC2_BELOW) ? 2 : 1)
     k_trans_fast(const __grid_constant__ CUtensorMap tmap, TransArgs a) {
