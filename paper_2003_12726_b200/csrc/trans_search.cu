@@ -167,7 +167,12 @@ template <int KA, int KB>
 #define PXST_K3_OCC2_BELOW 82   // up to 9 x 9 at 2 CTAs/SM: the 128-register cap spills a few
                                   // values but the doubled warps win (config 4: -11 %)
 #endif
-__global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC2_BELOW) ? 2 : 1)
+#ifndef PXST_K3_OCC3_BELOW
+#define PXST_K3_OCC3_BELOW 0
+#endif
+__global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
+                                            : (KA * KB < PXST_K3_OCC2_BELOW) ? 2
+                                                                             : 1)
     k_trans_fast(const __grid_constant__ CUtensorMap tmap, TransArgs a) {
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
