@@ -258,12 +258,16 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
 // ---------------------------------------------------------------------------
 // 2. fast kernel (TMA ring + register engine)
 // ---------------------------------------------------------------------------
-template <int KA, int KB>
+// BC > 0: the TMA box width (window row pitch in the ring) is the compile-time
+// constant BC (= a.box_c), so the engine's patch rows are immediate LDS
+// offsets from one base register.
+template <int KA, int KB, int BC = 0>
 #ifndef PXST_K2_OCC
 #define PXST_K2_OCC 2
 #endif
 __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
+  const int ldw = BC > 0 ? BC : a.box_c;
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
@@ -390,9 +394,9 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       sq = fwv == 1.f ? 1.f : sq;
       sq = fast ? sq : 0.f;
       const float sI = I * sq, sW = W * sq;
-      const int off = fast ? sm.lr * a.box_c + sm.lc : 0;
+      const int off = fast ? sm.lr * ldw + sm.lc : 0;
       if (kAhead) s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
-      engine_fast2<KA, KB>(ring + b * box + off, a.box_c, fx, fy, sW * (1.f - fx), sW * fx, sI,
+      engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
                            acc);
       mbar_arrive(&empty[b]);
       if (PXST_K2_PRODUCER == 0 && threadIdx.x == 0 && jj + kNB < nk) {
@@ -846,19 +850,21 @@ __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chun
 // dispatch
 // ---------------------------------------------------------------------------
 using FastKernel = void (*)(const __grid_constant__ CUtensorMap, PixArgs);
-struct FastEntry { int ka, kb; FastKernel fn; };
-#define PIX(a, b) FastEntry{a, b, k_pix_fast<a, b>}
+struct FastEntry { int ka, kb; FastKernel fn; FastKernel fn72; };   // fn72: box_c == 72
+#define PIX(a, b) FastEntry{a, b, k_pix_fast<a, b>, nullptr}
+#define PIX72(a, b) FastEntry{a, b, k_pix_fast<a, b>, k_pix_fast<a, b, 72>}
 const FastEntry kFastTable[] = {
-    PIX(1, 1),  PIX(3, 3),  PIX(5, 5),  PIX(7, 7),  PIX(9, 9),  PIX(11, 11), PIX(13, 13),
+    PIX(1, 1),  PIX(3, 3),  PIX(5, 5),  PIX(7, 7),  PIX(9, 9),  PIX72(11, 11), PIX72(13, 13),
     PIX(1, 3),  PIX(1, 5),  PIX(1, 7),  PIX(1, 9),  PIX(1, 11), PIX(1, 13),  PIX(1, 15),
     PIX(1, 17), PIX(3, 1),  PIX(5, 1),  PIX(7, 1),  PIX(9, 1),  PIX(11, 1),  PIX(13, 1),
     PIX(15, 1), PIX(17, 1),
 };
 #undef PIX
+#undef PIX72
 
-FastKernel find_fast(int ka, int kb) {
+FastKernel find_fast(int ka, int kb, int box_c = 0) {
   for (const auto& e : kFastTable)
-    if (e.ka == ka && e.kb == kb) return e.fn;
+    if (e.ka == ka && e.kb == kb) return (box_c == 72 && e.fn72) ? e.fn72 : e.fn;
   return nullptr;
 }
 
@@ -975,6 +981,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.box_c = (a.box_c + 23) / 32 * 32 + 8;            // pitch = 8 (mod 32)
     if (a.box_c > 256) a.box_c = 232;
     while (a.box_r > 16 && a.box_r * a.box_c * 4 > 24 * 1024) --a.box_r;
+    fn = find_fast(na, nb, a.box_c);                     // compile-time row pitch if 72
     CUtensorMap tmap;
     if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
       return e;
