@@ -260,7 +260,8 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
 // ---------------------------------------------------------------------------
 // BC > 0: the TMA box width (window row pitch in the ring) is the compile-time
 // constant BC (= a.box_c), so the engine's patch rows are immediate LDS
-// offsets from one base register.
+// offsets from one base register; these variants are also specialised for
+// calls without frame weights (the host picks them only then).
 template <int KA, int KB, int BC = 0>
 #ifndef PXST_K2_OCC
 #define PXST_K2_OCC 2
@@ -268,6 +269,7 @@ template <int KA, int KB, int BC = 0>
 __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
   const int ldw = BC > 0 ? BC : a.box_c;
+  const float* const fwp = BC > 0 ? nullptr : a.fw;
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
@@ -341,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
     auto sample_of = [&](int jj, float& I, float& fwv) {
       const int64_t off = t_off[jj];
       I = live ? __ldg(a.sc.frames + off + p) : 0.f;
-      fwv = (live && a.fw) ? __ldg(a.fw + off + p) : 1.f;
+      fwv = (live && fwp) ? __ldg(fwp + off + p) : 1.f;
       return make_sample<true>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f, t_wr[jj],
                                t_wc[jj]);
     };
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       any_slow |= live && !fast;
       const float fx = fast ? static_cast<float>(sm.fx) : 0.f;
       const float fy = fast ? static_cast<float>(sm.fy) : 0.f;
-      float sq = sqrt_approx(fmaxf(fwv, 0.f));     // unconditional: no branch in the block
+      float sq = BC > 0 ? 1.f : sqrt_approx(fmaxf(fwv, 0.f));   // no branch in the block
       sq = fwv == 1.f ? 1.f : sq;
       sq = fast ? sq : 0.f;
       const float sI = I * sq, sW = W * sq;
@@ -981,7 +983,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.box_c = (a.box_c + 23) / 32 * 32 + 8;            // pitch = 8 (mod 32)
     if (a.box_c > 256) a.box_c = 232;
     while (a.box_r > 16 && a.box_r * a.box_c * 4 > 24 * 1024) --a.box_r;
-    fn = find_fast(na, nb, a.box_c);                     // compile-time row pitch if 72
+    fn = find_fast(na, nb, fw ? 0 : a.box_c);            // compile-time row pitch if 72
     CUtensorMap tmap;
     if (int e = encode_tmap_2d_f32(&tmap, tbase, ref->os, ref->of, pitch, a.box_r, a.box_c))
       return e;
