@@ -223,11 +223,15 @@ __device__ __forceinline__ void window_origin(const PixArgs& a, const TileGeo& g
 
 // fwv is only stored (checked by fast()), so a frame-weight load issued for
 // the next frame is not waited on here.
-template <bool kKnownFit = false>
+// KA_/KB_/BC_ > 0: the window and box width as compile-time constants (the
+// fast kernels); the same tests as with the runtime values.
+template <bool kKnownFit = false, int KA_ = 0, int KB_ = 0, int BC_ = 0>
 __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g, double u0,
                                               double u1, double dI, double dJ, float fwv,
                                               int wr0, int wc0) {
-  const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
+  const int ka = KA_ > 0 ? KA_ : a.ka, kb = KB_ > 0 ? KB_ : a.kb;
+  const int box_c = BC_ > 0 ? BC_ : a.box_c;
+  const int ra = (ka - 1) / 2, rb = (kb - 1) / 2;
   const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
   Sample s;
   s.fwv = fwv;
@@ -242,15 +246,19 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
   s.pre = false;
   s.pvb = 0;
   s.wr0 = s.wc0 = s.lr = s.lc = 0;
-  if (kKnownFit || tile_fits(g, need_rows2(a.ka), need_cols2(a.kb), a.box_r, a.box_c)) {
+  if (kKnownFit || tile_fits(g, need_rows2(ka), need_cols2(kb), a.box_r, box_c)) {
     s.wr0 = wr0;
     s.wc0 = wc0;
     s.lr = s.i - ra - s.wr0;
     s.lc = s.j - rb - s.wc0;
-    const bool in = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of;
-    s.pre = in && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r && s.lc >= 0 &&
-            s.lc + a.kb + 1 <= a.box_c;
-    s.pvb = __ldg(a.pv + (in ? s.i * static_cast<int>(a.of) + s.j : 0));   // os * of < 2^31
+    // 0 <= v < n as one unsigned compare (os * of < 2^31, check_ref; the box
+    // holds the patch: box_r >= ka + 2, box_c >= kb + 2)
+    const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
+    const bool in = static_cast<unsigned>(s.i) < static_cast<unsigned>(os) &&
+                    static_cast<unsigned>(s.j) < static_cast<unsigned>(of);
+    s.pre = in && static_cast<unsigned>(s.lr) <= static_cast<unsigned>(a.box_r - ka - 1) &&
+            static_cast<unsigned>(s.lc) <= static_cast<unsigned>(box_c - kb - 1);
+    s.pvb = __ldg(a.pv + (in ? s.i * of + s.j : 0));
   }
   return s;
 }
@@ -344,8 +352,8 @@ __global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
       const int64_t off = t_off[jj];
       I = live ? __ldg(a.sc.frames + off + p) : 0.f;
       fwv = (live && fwp) ? __ldg(fwp + off + p) : 1.f;
-      return make_sample<true>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f, t_wr[jj],
-                               t_wc[jj]);
+      return make_sample<true, KA, KB, BC>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f,
+                                           t_wr[jj], t_wc[jj]);
     };
     // One-frame-ahead pipeline of the per-sample geometry, stack value and
     // patch-valid lookup.  The loop body after the ring wait is one basic

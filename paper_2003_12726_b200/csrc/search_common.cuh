@@ -28,7 +28,7 @@ namespace pxst {
 // ~5.2 to ~4.1 lane operations and its issue slots by a third:
 //  * Row interpolation in one FMA.  h = gy o_b + fy o_{b+1} (gy = 1 - fy) is
 //    carried as h' = o_b + rho o_{b+1} with rho = fy / gy (MUFU reciprocal,
-//    ~2 ulp: it scales the o_{b+1} term only) and the factor gy
+//    ~1 ulp: it scales the o_{b+1} term only) and the factor gy
 //    folded into the trial weights (A' = A gy, B' = B gy), so every trial is
 //    still r = I - A' h'_prev - B' h'_cur = I - A h_prev - B h_cur.  fy is
 //    kept <= 1 - 2^-24, so gy > 0; the relative rounding of A' h' matches
@@ -54,6 +54,13 @@ __device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
   f32x2 d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
+}
+
+// MUFU reciprocal, flush-to-zero (~1 ulp).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // MUFU square root (frame weights of the split-half path).
@@ -119,7 +126,7 @@ __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int 
   constexpr bool ODD = PackedAcc<KA, KB>::ODD;
   fy = fminf(fy, 0x1.fffffep-1f);
   const float gy = 1.f - fy;
-  const float rho = __fdividef(fy, gy);   // gy in [2^-24, 1]
+  const float rho = fy * rcp_approx(gy);   // gy in [2^-24, 1]: no denormal path needed
   const float Ap = A * gy, Bp = B * gy;
   const f32x2 nA2 = pack2(-Ap, -Ap), nB2 = pack2(-Bp, -Bp), I2 = pack2(I, I);
   PatchRow<KB> prev, cur;
