@@ -151,7 +151,7 @@ __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int 
 
 // ---------------------------------------------------------------------------
 // Exact trials (the slow fix-up kernels), read from a float32 copy of the
-// reference with NaN on invalid cells (make_nan_ref), so one load gives value
+// reference with NaN on invalid cells (make_pv's fmn), so one load gives value
 // and validity.  Everything that is constant over a sample's trials (integer
 // shifts keep its fractions) is hoisted into ExactSample; a trial then costs
 // four loads and the masked renormalisation of masked_read, in the same
@@ -182,7 +182,7 @@ __device__ __forceinline__ ExactSample exact_sample(double fx, double fy, float 
 }
 
 // Same trial read straight from a NaN-encoded copy of the reference in
-// global memory (make_nan_ref): four independent L1/L2 loads, no staging.
+// global memory (make_pv's fmn): four independent L1/L2 loads, no staging.
 // Branch-free, 32-bit cell indices (callers guarantee os * of < 2^31): the
 // four loads always go to clamped in-grid cells and the reference's rules
 // are applied by selects.  Corners past the last row/column carry zero
@@ -241,8 +241,6 @@ __device__ __forceinline__ float trial_patch(float v00, float v01, float v10, fl
   return (in && (m00 || m01 || m10 || m11)) ? e.fwv * (r * r) : e.fb;
 }
 
-// float32 reference with NaN on invalid cells, [os*of] (for trial_global).
-int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s);
 
 
 
@@ -330,7 +328,7 @@ __device__ __forceinline__ int clamp_span(double v) {
 // Host helpers ---------------------------------------------------------------
 // Patch-valid map: pv[i][j] = every cell of rows [i+lr, i+hr] x cols
 // [j+lc, j+hc] exists and is valid; with fmn != NULL also the NaN-encoded
-// reference (make_nan_ref) in the same launch.
+// reference (NaN on invalid cells, read by the exact fix-ups) in the same launch.
 int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, float* fmn,
             cudaStream_t s);
 // Offsets of SearchWindow.offsets (recon.py:51-57).

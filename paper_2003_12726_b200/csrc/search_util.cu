@@ -11,7 +11,7 @@ namespace {
 // Patch-valid map pv[i][j] = every cell of rows [i+lr, i+hr] x cols
 // [j+lc, j+hc] exists and is valid, as a separable AND over a 32 x 32 output
 // tile with its halo staged in shared memory (one launch); optionally also
-// the NaN-encoded float32 reference of the tile's cells (make_nan_ref).
+// the NaN-encoded float32 reference of the tile's cells (fmn).
 constexpr int kPvC = 32, kPvR = 16, kPvMaxHalo = 64;   // output tile: 16 rows x 32 cols
 
 __global__ void __launch_bounds__(256) k_pv_tile(const uint8_t* __restrict__ valid,
@@ -96,20 +96,6 @@ int make_pv(const pxst_ref* ref, int lr, int hr, int lc, int hc, uint8_t* pv, fl
   PXST_REQUIRE(g.y <= kMaxGridY, "reference image too tall");
   k_pv_tile<<<g, dim3(32, 8), 0, s>>>(ref->valid, ref->fm, static_cast<int>(ref->os),
                               static_cast<int>(ref->of), lr, hr, lc, hc, pv, fmn);
-  PXST_CHECK_LAUNCH();
-  return PXST_OK;
-}
-
-__global__ void k_nan_ref(const float* __restrict__ fm, const uint8_t* __restrict__ valid,
-                          int64_t n, float* __restrict__ out) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x)
-    out[q] = valid[q] ? fm[q] : __int_as_float(0x7fc00000);
-}
-
-int make_nan_ref(const pxst_ref* ref, float* out, cudaStream_t s) {
-  const int64_t n = ref->os * ref->of;
-  k_nan_ref<<<grid_1d(n, 256), 256, 0, s>>>(ref->fm, ref->valid, n, out);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }
