@@ -41,7 +41,11 @@ namespace {
 // window pitch = 8 (mod 32) this cuts shared-memory bank conflicts on noisy
 // maps from 2.16x (warp = one 32-pixel row) to ~1.6x and to 1.0x on smooth
 // maps (model of the access pattern, confirmed by ncu).
-constexpr int kTR = 8, kTC = 16, kThreads = kTR * kTC;
+#ifndef PXST_K2_TILE_ROWS
+#define PXST_K2_TILE_ROWS 8
+#endif
+constexpr int kTR = PXST_K2_TILE_ROWS, kTC = 16, kThreads = kTR * kTC;
+constexpr int kCtaPerSm = kThreads <= 128 ? 2 : 1;   // fast-kernel CTAs resident per SM
 __device__ __forceinline__ int tile_dr(int tid) { return ((tid >> 5) >> 1) * 4 + ((tid & 31) >> 3); }
 __device__ __forceinline__ int tile_dc(int tid) { return ((tid >> 5) & 1) * 8 + (tid & 7); }
 #ifndef PXST_K2_RING
@@ -271,10 +275,7 @@ __device__ __forceinline__ Sample make_sample(const PixArgs& a, const TileGeo& g
 // offsets from one base register; these variants are also specialised for
 // calls without frame weights (the host picks them only then).
 template <int KA, int KB, int BC = 0>
-#ifndef PXST_K2_OCC
-#define PXST_K2_OCC 2
-#endif
-__global__ void __launch_bounds__(kThreads, (KA * KB <= 121) ? PXST_K2_OCC : 2)
+__global__ void __launch_bounds__(kThreads, kCtaPerSm)
     k_pix_fast(const __grid_constant__ CUtensorMap tmap, PixArgs a) {
   const int ldw = BC > 0 ? BC : a.box_c;
   const float* const fwp = BC > 0 ? nullptr : a.fw;
@@ -1008,7 +1009,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
       PXST_CHECK_CUDA(cudaGetDevice(&dev));
       PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    const int64_t slots = 2 * static_cast<int64_t>(sms);
+    const int64_t slots = kCtaPerSm * static_cast<int64_t>(sms);
     const int max_chunks = static_cast<int>(sc->n_good / 16 > 1 ? sc->n_good / 16 : 1);
     int n_chunks;
     a.n_full = 0;
