@@ -2,25 +2,31 @@
 // (recon.py:144-170, 183-207, 221-296; sigma = 0, integrate = False).
 //
 // Pipeline for integer windows (Ka x Kb instantiated):
-//   1. k_tile_geo      per 4x32 pixel tile: bounding box of u over its work
-//                      pixels -> object-window origin and "window fits" flag.
-//   2. k_pix_fast      grid (tiles, frame chunks).  Per frame the tile's object
-//                      window (box BR x BC, shifted by delta_n) is fetched by
-//                      TMA into a 4-deep shared-memory ring (mbarrier full /
-//                      empty pairs), each thread runs the register trial engine
-//                      for its pixel; samples whose patch leaves the grid or
-//                      touches an invalid cell are skipped.  Writes float32
-//                      partial sums partial[chunk][trial][pixel].
-//   3. k_pix_slow      one warp per listed (pixel, chunk): lanes classify 32
+//   1. k_tile_geo      per 8x16 pixel tile: bounding box of u over its work
+//                      pixels -> object-window origin and "window fits" flag
+//                      (and u_out = u, err = 0 on the ROI when it is the
+//                      whole detector).
+//   2. k_pix_fast      1-D grid of work units: whole tiles over all frames
+//                      (<= 512 good frames: the first full waves) and
+//                      (tile, frame chunk) units for the rest.  Per frame the
+//                      tile's object window (box BR x BC, shifted by delta_n)
+//                      is fetched by TMA into a 4-deep shared-memory ring
+//                      (mbarrier full / empty pairs), each thread runs the
+//                      register trial engine for its pixel; samples whose
+//                      patch leaves the grid or touches an invalid cell are
+//                      skipped and listed.  Whole-tile units finish their
+//                      pixels in the kernel (argmin, paraboloid); chunk units
+//                      write float32 partial[chunk][trial][pixel].
+//   3. k_pix_slow(_rows) one warp per listed (pixel, chunk): lanes classify 32
 //                      frames at a time with the same eligibility test, then
-//                      for every skipped sample lanes add the exact per-trial
-//                      contribution (masked renormalised read from a
-//                      NaN-encoded reference, (I-W)^2 fallback) of the trials
-//                      they own, in frame order.
-//   4. k_pix_epilogue  one thread per pixel: float64 sum over chunks,
-//                      first-occurrence argmin (numpy order a*Kb + b),
-//                      paraboloid on the normalised 3x3 patch, static-pixel
-//                      rule, writes u_out and the error map.
+//                      add every skipped sample's exact per-trial contribution
+//                      (masked renormalised read from a NaN-encoded reference,
+//                      (I-W)^2 fallback), in frame order; whole-tile pixels
+//                      are finished there.
+//   4. k_pix_epilogue  pixels of the chunked tiles, eight lanes per pixel:
+//                      float64 sum over chunks, first-occurrence argmin (numpy
+//                      order a*Kb + b), paraboloid on the normalised 3x3
+//                      patch, static-pixel rule, u_out and the error map.
 // Sub-pixel grids and non-instantiated windows use k_pix_generic (float64,
 // one thread per (pixel, trial)) followed by the same epilogue.
 #include <algorithm>
