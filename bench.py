@@ -346,10 +346,21 @@ def run_ours(args, rank, world, local):
         # untimed burn-in (~0.3 s of steps) ahead of the W warm-up steps: on a
         # fresh box the first timed step otherwise measured up to 2.7 ms
         # (K2 alone; steady state 0.59) in the first process
-        t_burn = time.perf_counter() + (0.0 if args.profile else 0.3)
-        while time.perf_counter() < t_burn:
+        # The step count is the same on every rank (the sharded step runs
+        # collectives): ~0.3 s worth, from one measured step, max over ranks.
+        n_burn = 0
+        if not args.profile:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             step()
             torch.cuda.synchronize()
+            n_burn = min(300, max(1, int(0.3 / max(time.perf_counter() - t0, 1e-4))))
+            if world > 1:
+                nb = torch.tensor([n_burn], device=dev)
+                torch.distributed.all_reduce(nb, op=torch.distributed.ReduceOp.MAX)
+                n_burn = int(nb.item())
+        for _ in range(n_burn):
+            step()
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
