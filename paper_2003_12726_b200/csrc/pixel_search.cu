@@ -633,9 +633,14 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
 // leave a third of the warp idle and serialise each lane's Kb trials): lanes
 // own trials lane + 32 j and read each trial's corners straight from the
 // NaN-encoded reference (trial_global), in frame order.
-constexpr int kSlowPerLane = 6;  // ceil(max fast-path window 13x13 / 32)
+// NJ = trials per lane, ceil(Ka Kb / 32) (<= 6 for the fast-path windows):
+// sized per window so 11x11 (NJ = 4) fits three blocks per SM.
 
-__global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
+#ifndef PXST_K2_SLOW_OCC
+#define PXST_K2_SLOW_OCC 3
+#endif
+template <int NJ>
+__global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slow(PixArgs a,
                                                  const unsigned long long* __restrict__ list,
                                                  unsigned* __restrict__ list_n) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
@@ -646,9 +651,9 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
   const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
   const int nk = a.ka * a.kb;
   const int64_t plane = a.sc.ss * a.sc.fs;
-  int ta[kSlowPerLane], tb[kSlowPerLane];   // window coordinates of the lane's trials
+  int ta[NJ], tb[NJ];   // window coordinates of the lane's trials
 #pragma unroll
-  for (int j = 0; j < kSlowPerLane; ++j) {
+  for (int j = 0; j < NJ; ++j) {
     const int t = lane + 32 * j;
     ta[j] = t / a.kb;
     tb[j] = t % a.kb;
@@ -669,10 +674,10 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
     int64_t k_lo, k_hi, pslot;
     chunk_frames(a, chunk, k_lo, k_hi, pslot);
     float* out = a.partial + pslot * nk * a.nq + q;
-    float part[kSlowPerLane];          // lane owns trials lane + 32 j
-    float prev[kSlowPerLane];          // the fast kernel's partials, fetched early
+    float part[NJ];          // lane owns trials lane + 32 j
+    float prev[NJ];          // the fast kernel's partials, fetched early
 #pragma unroll
-    for (int j = 0; j < kSlowPerLane; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       part[j] = 0.f;
       prev[j] = lane + 32 * j < nk ? out[(int64_t)(lane + 32 * j) * a.nq] : 0.f;
     }
@@ -716,18 +721,18 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                                             __shfl_sync(0xffffffffu, Il, bsel),
                                             __shfl_sync(0xffffffffu, fwl, bsel));
 #pragma unroll
-        for (int j = 0; j < kSlowPerLane; ++j)
+        for (int j = 0; j < NJ; ++j)
           if (lane + 32 * j < nk)
             part[j] += trial_global(a.fmn, static_cast<int>(a.os), static_cast<int>(a.of),
                                     pr0 + ta[j], pc0 + tb[j], es);
       }
     }
-    float tot[kSlowPerLane];
+    float tot[NJ];
 #pragma unroll
-    for (int j = 0; j < kSlowPerLane; ++j) tot[j] = prev[j] + part[j];
+    for (int j = 0; j < NJ; ++j) tot[j] = prev[j] + part[j];
     if (chunk != kAllFrames) {
 #pragma unroll
-      for (int j = 0; j < kSlowPerLane; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         const int t = lane + 32 * j;
         if (t < nk) out[(int64_t)t * a.nq] = tot[j];
       }
@@ -738,7 +743,7 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
     int best = -1;
     float bsum = 0.f;
 #pragma unroll
-    for (int j = 0; j < kSlowPerLane; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int t = lane + 32 * j;
       if (t < nk && (best < 0 || tot[j] < bsum)) { bsum = tot[j]; best = t; }
     }
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow(PixArgs a,
                  a.offs_a[best / a.kb], a.offs_b[best % a.kb], [&](int t) {
                    float v = tot[0];
 #pragma unroll
-                   for (int j = 1; j < kSlowPerLane; ++j) v = (t >> 5) == j ? tot[j] : v;
+                   for (int j = 1; j < NJ; ++j) v = (t >> 5) == j ? tot[j] : v;
                    return static_cast<double>(__shfl_sync(0xffffffffu, v, t & 31));
                  });
   }
@@ -1064,7 +1069,17 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (na <= 3)          // 1 x N / 3 x N windows: >= 10 samples in flight per warp
       k_pix_slow_rows<<<2 * sms, 256, 0, s>>>(a, list, list_n);
     else
-      k_pix_slow<<<2 * sms, 256, 0, s>>>(a, list, list_n);
+    {
+      const int nj = (nk + 31) / 32;
+      switch (nj) {
+        case 1: k_pix_slow<1><<<PXST_K2_SLOW_OCC * sms, 256, 0, s>>>(a, list, list_n); break;
+        case 2: k_pix_slow<2><<<PXST_K2_SLOW_OCC * sms, 256, 0, s>>>(a, list, list_n); break;
+        case 3: k_pix_slow<3><<<PXST_K2_SLOW_OCC * sms, 256, 0, s>>>(a, list, list_n); break;
+        case 4: k_pix_slow<4><<<PXST_K2_SLOW_OCC * sms, 256, 0, s>>>(a, list, list_n); break;
+        case 5: k_pix_slow<5><<<2 * sms, 256, 0, s>>>(a, list, list_n); break;
+        default: k_pix_slow<6><<<2 * sms, 256, 0, s>>>(a, list, list_n); break;
+      }
+    }
     PXST_CHECK_LAUNCH();
     if (getenv("PXST_DEBUG")) {
       unsigned h = 0;
