@@ -329,10 +329,13 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
 // ---------------------------------------------------------------------------
 // 3. slow fix-up: warp per listed frame
 // ---------------------------------------------------------------------------
-__global__ void k_trans_slow(TransArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// One block per listed frame: its 8 warps take the frame's flagged tiles in
+// turn (a warp per frame left the launch waiting on the frame with the most
+// flagged tiles), then the warps' partial sums are added in warp order.
+constexpr int kSlowWarps = 8;
+__global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
+  __shared__ float red[kSlowWarps][kSlowPerLane * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned n = *a.slow_n;
   const int nk_ph = a.ka * a.kb, nk = a.na_full * a.nb_full;
   int ta[kSlowPerLane], tb[kSlowPerLane];   // patch coordinates of the lane's trials
@@ -344,7 +347,7 @@ __global__ void k_trans_slow(TransArgs a) {
   }
   const int64_t plane = a.sc.ss * a.sc.fs;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
-  for (int64_t e = warp0; e < n; e += nwarps) {
+  for (int64_t e = blockIdx.x; e < n; e += gridDim.x) {
     const int64_t kk = a.slow_list[e];
     const int64_t f = a.sc.good[a.frame_lo + kk];
     const double dI = a.di[f], dJ = a.dj[f];
@@ -353,8 +356,10 @@ __global__ void k_trans_slow(TransArgs a) {
     float part[kSlowPerLane];
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
+    int flagged = 0;
     for (int64_t it = 0; it < a.n_tiles; ++it) {
       if (!((bits[it >> 6] >> (it & 63)) & 1ull)) continue;     // only flagged tiles
+      if ((flagged++ % kSlowWarps) != warp) continue;           // this warp's share
       const int64_t band = it / a.n_ct;
       const int ct = static_cast<int>(it % a.n_ct);
       const TileGeo g = a.geo[it];
@@ -400,12 +405,20 @@ __global__ void k_trans_slow(TransArgs a) {
         }
       }
     }
-    double* out = a.partial + kk * (int64_t)nk;
 #pragma unroll
-    for (int j = 0; j < kSlowPerLane; ++j) {
-      const int t = lane + 32 * j;
-      if (t < nk_ph) out[full_index(a, t / a.kb, t % a.kb)] += static_cast<double>(part[j]);
+    for (int j = 0; j < kSlowPerLane; ++j) red[warp][lane + 32 * j] = part[j];
+    __syncthreads();
+    if (warp == 0) {
+      double* out = a.partial + kk * (int64_t)nk;
+#pragma unroll
+      for (int j = 0; j < kSlowPerLane; ++j) {
+        const int t = lane + 32 * j;
+        float v = red[0][t];
+        for (int w = 1; w < kSlowWarps; ++w) v += red[w][t];
+        if (t < nk_ph) out[full_index(a, t / a.kb, t % a.kb)] += static_cast<double>(v);
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -683,7 +696,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
         PXST_CHECK_CUDA(cudaMemsetAsync(a.tilebits, 0, tb_bytes, s));
         ph.fn<<<(unsigned)(c1 - c0), kThreads, smem, s>>>(tmap, a);
         PXST_CHECK_LAUNCH();
-        k_trans_slow<<<148 * 4, 256, 0, s>>>(a);
+        k_trans_slow<<<148 * 4, 32 * kSlowWarps, 0, s>>>(a);
         PXST_CHECK_LAUNCH();
         if (a.dbg) {
           unsigned h = 0;
