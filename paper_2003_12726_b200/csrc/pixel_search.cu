@@ -800,20 +800,22 @@ __global__ void k_pix_generic(PixArgs a, const double* __restrict__ offs_a,
 // ---------------------------------------------------------------------------
 // 4. epilogue
 // ---------------------------------------------------------------------------
-// Eight lanes per pixel: lane k sums trials k, k + 8, ... over the chunks
-// (all loads independent), then a first-occurrence argmin across the group
-// (smaller sum, ties to the smaller trial index = numpy's order).
-constexpr int kEpiLanes = 8;
+// kEpiLanes lanes per pixel: lane k sums trials k, k + kEpiLanes, ... over
+// the chunks (all loads independent), then a first-occurrence argmin across
+// the group (smaller sum, ties to the smaller trial index = numpy's order).
+// 4 lanes measured best when only the tail tiles are chunked (config 1: 8
+// lanes 20.9 us, 4 lanes 16.0, 2 lanes 21.6), 2 when every tile is (config 3:
+// 8 lanes 1.85 ms, 4 lanes 1.54, 2 lanes 0.91: better coalesced trial loads).
 
 // Pixels: linear over the ROI (generic path, tiles_x == 0), or the pixels of
 // the split tiles [n_full, tiles) of the fast path (whole-tile pixels are
 // finished by k_pix_fast / k_pix_slow).
-template <class T>
+template <class T, int kEpiLanes>
 __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chunks) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kEpiLanes;
   const int sub = threadIdx.x % kEpiLanes;
-  const unsigned gmask = 0xFFu << ((threadIdx.x & 31) & ~(kEpiLanes - 1));
+  const unsigned gmask = ((1u << kEpiLanes) - 1u) << ((threadIdx.x & 31) & ~(kEpiLanes - 1));
   int64_t rr, cc;
   if (a.tiles_x > 0) {
     const int64_t tile = a.n_full + gi / kThreads;
@@ -1094,8 +1096,12 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     }
     const int64_t split_px = (tiles - a.n_full) * kThreads;
     if (split_px > 0) {
-      k_pix_epilogue<float><<<(unsigned)((split_px * kEpiLanes + 127) / 128), 128, 0, s>>>(
-          a, part.as<float>(), a.n_chunks);
+      if (a.n_full > 0)
+        k_pix_epilogue<float, 4><<<(unsigned)((split_px * 4 + 127) / 128), 128, 0, s>>>(
+            a, part.as<float>(), a.n_chunks);
+      else
+        k_pix_epilogue<float, 2><<<(unsigned)((split_px * 2 + 127) / 128), 128, 0, s>>>(
+            a, part.as<float>(), a.n_chunks);
       PXST_CHECK_LAUNCH();
     }
     PXST_CHECK_LAUNCH();
@@ -1108,7 +1114,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   dim3 g(qblocks, (unsigned)nk);
   k_pix_generic<<<g, 128, 0, s>>>(a, d_oa, d_ob, errs.as<double>());
   PXST_CHECK_LAUNCH();
-  k_pix_epilogue<double><<<qblocks * kEpiLanes, 128, 0, s>>>(a, errs.as<double>(), 1);
+  k_pix_epilogue<double, 2><<<qblocks * 2, 128, 0, s>>>(a, errs.as<double>(), 1);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }
