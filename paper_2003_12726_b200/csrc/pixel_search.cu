@@ -134,6 +134,12 @@ __device__ __forceinline__ void chunk_frames(const PixArgs& a, unsigned chunk, i
   }
 }
 
+// Window offset i of an n-point window (recon.py:51-57): from the device
+// array when one is given (sub-pixel grids), else the integer offset i - half.
+__device__ __forceinline__ double win_off(const double* offs, int i, int n) {
+  return offs ? offs[i] : static_cast<double>(i - (n - 1) / 2);
+}
+
 // Argmin / paraboloid / static-pixel rule for one pixel (recon.py:257-296,
 // 313-315) from its raw trial sums (total(t), t in numpy order a * Kb + b).
 // First-occurrence argmin on the raw sums: dividing by the common positive
@@ -171,7 +177,8 @@ __device__ __forceinline__ void finish_pixel(const PixArgs& a, int64_t p, int be
 // ---------------------------------------------------------------------------
 // With init_out, every ROI pixel also gets u_out = u, err_out = 0 (the
 // search's finishers then overwrite the work pixels).
-__global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out) {
+__global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out, unsigned* zero2 = nullptr) {
+  if (zero2 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;
   __shared__ double red[kWarps][4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + tile_dr(threadIdx.x);
@@ -619,7 +626,8 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
       if (ob >= 0 && (best < 0 || ov < bsum || (ov == bsum && ob < best))) { bsum = ov; best = ob; }
     }
     finish_pixel(a, p, best, static_cast<double>(bsum), u0, u1, a.var[p],
-                 a.offs_a[best / kb], a.offs_b[best % kb], [&](int t) {
+                 win_off(a.offs_a, best / kb, a.ka), win_off(a.offs_b, best % kb, a.kb),
+                 [&](int t) {
                    const int c = t % kb;
                    float v = tot[0];
 #pragma unroll
@@ -754,7 +762,8 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
       if (ob >= 0 && (best < 0 || ov < bsum || (ov == bsum && ob < best))) { bsum = ov; best = ob; }
     }
     finish_pixel(a, p, best, static_cast<double>(bsum), u0, u1, a.var[p],
-                 a.offs_a[best / a.kb], a.offs_b[best % a.kb], [&](int t) {
+                 win_off(a.offs_a, best / a.kb, a.ka), win_off(a.offs_b, best % a.kb, a.kb),
+                 [&](int t) {
                    float v = tot[0];
 #pragma unroll
                    for (int j = 1; j < NJ; ++j) v = (t >> 5) == j ? tot[j] : v;
@@ -866,8 +875,8 @@ __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chun
   }
   if (sub != 0) return;
   const int64_t plane = a.sc.ss * a.sc.fs;
-  finish_pixel(a, p, best, braw, a.u[p], a.u[plane + p], a.var[p], a.offs_a[best / a.kb],
-               a.offs_b[best % a.kb], total);
+  finish_pixel(a, p, best, braw, a.u[p], a.u[plane + p], a.var[p],
+               win_off(a.offs_a, best / a.kb, a.ka), win_off(a.offs_b, best % a.kb, a.kb), total);
 }
 
 // ---------------------------------------------------------------------------
@@ -946,11 +955,17 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   a.ka = na; a.kb = nb;
   a.nq = cw * rw;
 
+  FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
+  // window offsets: integer windows (the fast path) compute them inline
   Scratch offs;
-  if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
-  if (int e = fill_offsets(offs.as<double>(), na, nb, subpixel_step, s)) return e;
-  const double* d_oa = offs.as<double>();
-  const double* d_ob = d_oa + na;
+  const double* d_oa = nullptr;
+  const double* d_ob = nullptr;
+  if (!fn) {
+    if (int e = offs.alloc(sizeof(double) * (na + nb), s)) return e;
+    if (int e = fill_offsets(offs.as<double>(), na, nb, subpixel_step, s)) return e;
+    d_oa = offs.as<double>();
+    d_ob = d_oa + na;
+  }
   a.offs_a = d_oa;
   a.offs_b = d_ob;
   a.refine_ok = refine && subpixel_step == 0.0 && na >= 3 && nb >= 3;   // recon.py:273
@@ -958,7 +973,6 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   a.err_out = err_out;
   const unsigned qblocks = (unsigned)((a.nq + 127) / 128);
 
-  FastKernel fn = (subpixel_step == 0.0 && !force_generic()) ? find_fast(na, nb) : nullptr;
   if (fn) {
     const int ra = (na - 1) / 2, rb = (nb - 1) / 2;
     a.box_r = box_rows_for(na);
@@ -989,8 +1003,10 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
                                         cudaMemcpyDeviceToDevice, s));
       tbase = fmpad.as<float>();
     }
+    Scratch cnt;                 // slow-list count and work counter, zeroed by k_tile_geo
+    if (int e = cnt.alloc(2 * sizeof(unsigned), s)) return e;
     dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
-    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>(), fast_init ? 1 : 0);
+    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>(), fast_init ? 1 : 0, cnt.as<unsigned>());
     PXST_CHECK_LAUNCH();
     // Size the TMA box from the largest tile footprint (|du/dx| reaches ~1.8
     // at the edges of the config-3 map), capped at 24 KB per ring slot; tiles
@@ -1053,10 +1069,9 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
     a.partial = part.as<float>();
     Scratch lst;
-    if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 2), s)) return e;
-    unsigned* list_n = reinterpret_cast<unsigned*>(lst.as<unsigned long long>());
-    unsigned long long* list = lst.as<unsigned long long>() + 1;
-    PXST_CHECK_CUDA(cudaMemsetAsync(list_n, 0, 2 * sizeof(unsigned), s));
+    if (int e = lst.alloc(sizeof(unsigned long long) * (a.nq * a.n_chunks + 1), s)) return e;
+    unsigned* list_n = cnt.as<unsigned>();
+    unsigned long long* list = lst.as<unsigned long long>();
     a.slow_list = list;
     a.slow_n = list_n;
     Scratch dbg;
