@@ -481,6 +481,20 @@ class DeviceScan:
     def pixel_map_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                          subpixel_grid=None, refine=True, fw_t=None,
                          geom: "GeometryFuture | None" = None):
+        spans = None
+        if geom is None and not self.empty:
+            # K2 sizes its TMA box from the tile spans of u: queue them (and
+            # their copy to the host) ahead of K0 on this stream, so the host
+            # waits for them while K0 runs instead of synchronising inside the
+            # search call
+            dev2 = torch.empty(2, dtype=torch.int32, device=self.device)
+            spans = torch.empty(2, dtype=torch.int32, pin_memory=True)
+            check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
+                                           dev2.data_ptr(), stream_ptr()))
+            spans.copy_(dev2, non_blocking=True)
+            spans_ready = torch.cuda.Event()
+            spans_ready.record()
+            TRANSFER["d2h"] += 8
         self.ready()
         u_out = torch.empty_like(u_t)
         err = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
@@ -490,7 +504,11 @@ class DeviceScan:
             return u_out, err.view(self.ss, self.fs)
         var_fw = self.frame_weight_stats(fw_t) if fw_t is not None else None
         c_ref = ref.struct()
-        hint = geom.spans_ptr() if geom is not None else None
+        if spans is not None:
+            spans_ready.synchronize()
+            hint = spans.data_ptr()
+        else:
+            hint = geom.spans_ptr()
         check(self.lib.pxst_pixel_map_search_ex(
             ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
             u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), int(half_ss), int(half_fs),
