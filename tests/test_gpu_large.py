@@ -106,3 +106,28 @@ def test_cfg3_full_size_properties():
     # the search never worsens the selected error of a pixel (incumbent is a candidate)
     total, *_ = ds.error_maps(ref, u1, di, dj)
     assert np.isfinite(float(total.item()))
+
+
+def test_cfg4_subpixel_translation_subset_vs_oracle():
+    """Config 4's sub-pixel translation grid (+-4 px at 0.25 px: 33 x 33 = 1089
+    trials, 16 phase groups in K3) on two frames of the 4000, full detector."""
+    s, frames, ds, u, di, dj, ref = _setup(4)
+    cfg = s.cfg
+    assert cfg.t_subpixel_grid == 0.25
+    di_o, dj_o = ds.translation_search(ref, u, di, dj, cfg.t_half_ss, cfg.t_half_fs,
+                                       cfg.t_subpixel_grid)
+    pick = [0, 3999]
+    sub = np.ascontiguousarray(frames[pick].cpu().numpy())
+    d_o, j_o, errs = orc.update_translations(sub, np.ones(len(pick), bool), s.w.w, s.m.mask,
+                                             ref.i_ref.cpu().numpy(), ref.wsum.cpu().numpy(),
+                                             ref.origin, s.u0.u, s.t0.di[pick], s.t0.dj[pick],
+                                             cfg.t_half_ss, cfg.t_half_fs, cfg.t_subpixel_grid,
+                                             return_errors=True)
+    gd, gj = di_o.cpu().numpy()[pick], dj_o.cpu().numpy()[pick]
+    checked = 0
+    for k, e in errs.items():
+        flat = np.sort(e.ravel())
+        if (flat[1] - flat[0]) > 1e-4 * abs(flat[0]):
+            assert abs(gd[k] - d_o[k]) < PX_TOL and abs(gj[k] - j_o[k]) < PX_TOL
+            checked += 1
+    assert checked >= 1
