@@ -1,5 +1,6 @@
 """Parity at the BASELINE's large configs (2: 1000 frames 516x1556, 1-D window
-(0, 8); 3: 2000 frames 1024x1024, R=6 pixel map and +-3 translations).
+(0, 8); 3: 2000 frames 1024x1024, R=6 pixel map and +-3 translations; 4: 4000
+frames 512x512, +-4 px translations at 0.25 px and error maps).
 
 Data are rendered on the device (synth.make_scan_device).  The GPU builds the
 object map; the CPU oracle then recomputes, on a detector row band (pixels are
@@ -131,3 +132,23 @@ def test_cfg4_subpixel_translation_subset_vs_oracle():
             assert abs(gd[k] - d_o[k]) < PX_TOL and abs(gj[k] - j_o[k]) < PX_TOL
             checked += 1
     assert checked >= 1
+
+
+def test_cfg4_error_maps_band_vs_oracle():
+    """Config 4 error maps (4000 frames): the per-pixel sums and the variance
+    of a detector row band against the oracle on that band (pixels are
+    independent, recon.py:416-425); total == sum of per-frame at full size."""
+    s, frames, ds, u, di, dj, ref = _setup(4)
+    total, per_frame, per_pixel, plane, var = ds.error_maps(ref, u, di, dj)
+    r0, r1 = 300, 306
+    fb = np.ascontiguousarray(frames[:, r0:r1].cpu().numpy())
+    M = orc.calc_error(fb, s.scan.good_frames, s.w.w[r0:r1], s.m.mask[r0:r1],
+                       ref.i_ref.cpu().numpy(), ref.wsum.cpu().numpy(), ref.origin,
+                       s.u0.u[:, r0:r1], s.t0.di, s.t0.dj)
+    np.testing.assert_allclose(var[r0:r1].cpu().numpy(), M["variance"], rtol=1e-9)
+    np.testing.assert_allclose(per_pixel[r0:r1].cpu().numpy(), M["per_pixel"], rtol=1e-4,
+                               atol=1e-9)
+    pf = per_frame.cpu().numpy()
+    good = s.scan.good_frames
+    assert abs(float(total.item()) - pf[good].sum()) <= 1e-9 * abs(pf[good].sum())
+    assert np.all(pf[~good] == 0)
