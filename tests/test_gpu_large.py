@@ -134,13 +134,14 @@ def test_cfg4_subpixel_translation_subset_vs_oracle():
     assert checked >= 1
 
 
-def test_cfg4_error_maps_band_vs_oracle():
-    """Config 4 error maps (4000 frames): the per-pixel sums and the variance
-    of a detector row band against the oracle on that band (pixels are
-    independent, recon.py:416-425); total == sum of per-frame at full size."""
-    s, frames, ds, u, di, dj, ref = _setup(4)
+@pytest.mark.parametrize("cfg_id,rows", [(2, (100, 106)), (3, (700, 704)), (4, (300, 306))])
+def test_error_maps_band_vs_oracle(cfg_id, rows):
+    """Error maps at full size: the per-pixel sums and the variance of a
+    detector row band against the oracle on that band (pixels are
+    independent, recon.py:416-425); total == sum of per-frame."""
+    s, frames, ds, u, di, dj, ref = _setup(cfg_id)
     total, per_frame, per_pixel, plane, var = ds.error_maps(ref, u, di, dj)
-    r0, r1 = 300, 306
+    r0, r1 = rows
     fb = np.ascontiguousarray(frames[:, r0:r1].cpu().numpy())
     M = orc.calc_error(fb, s.scan.good_frames, s.w.w[r0:r1], s.m.mask[r0:r1],
                        ref.i_ref.cpu().numpy(), ref.wsum.cpu().numpy(), ref.origin,
