@@ -659,12 +659,15 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
   const int ra = (a.ka - 1) / 2, rb = (a.kb - 1) / 2;
   const int nk = a.ka * a.kb;
   const int64_t plane = a.sc.ss * a.sc.fs;
+  const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
   int ta[NJ], tb[NJ];   // window coordinates of the lane's trials
+  int to[NJ];           // and their cell offsets from the window's corner
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int t = lane + 32 * j;
     ta[j] = t / a.kb;
     tb[j] = t % a.kb;
+    to[j] = ta[j] * of + tb[j];
   }
   for (;;) {
     unsigned e = 0;
@@ -728,11 +731,19 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
                                             __shfl_sync(0xffffffffu, sl.fy, bsel), W,
                                             __shfl_sync(0xffffffffu, Il, bsel),
                                             __shfl_sync(0xffffffffu, fwl, bsel));
+        // warp-uniform: the whole window's 2x2 cells on the grid (the usual
+        // case: skipped samples touch invalid cells, not the grid's edge)
+        if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {
+          const float* w0 = a.fmn + (pr0 * of + pc0);
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          if (lane + 32 * j < nk)
-            part[j] += trial_global(a.fmn, static_cast<int>(a.os), static_cast<int>(a.of),
-                                    pr0 + ta[j], pc0 + tb[j], es);
+          for (int j = 0; j < NJ; ++j)
+            if (lane + 32 * j < nk) part[j] += trial_interior(w0 + to[j], of, es);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (lane + 32 * j < nk)
+              part[j] += trial_global(a.fmn, os, of, pr0 + ta[j], pc0 + tb[j], es);
+        }
       }
     }
     float tot[NJ];

@@ -214,6 +214,28 @@ __device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int
   return ok ? e.fwv * (r * r) : e.fb;
 }
 
+// trial_global for a cell whose 2x2 corners are all on the grid (the caller
+// checked the whole patch): no bounds tests or clamps, identical arithmetic.
+__device__ __forceinline__ float trial_interior(const float* __restrict__ p0, int of,
+                                                const ExactSample& e) {
+  const float v00 = __ldg(p0), v01 = __ldg(p0 + 1);
+  const float v10 = __ldg(p0 + of), v11 = __ldg(p0 + of + 1);
+  const bool m00 = v00 == v00;
+  const bool m01 = e.fyp && v01 == v01;
+  const bool m10 = e.fxp && v10 == v10;
+  const bool m11 = e.fxp && e.fyp && v11 == v11;
+  float den = m00 ? e.w00 : 0.f;
+  float num = m00 ? e.w00 * v00 : 0.f;
+  den += m01 ? e.w01 : 0.f;
+  num = fmaf(m01 ? e.w01 : 0.f, m01 ? v01 : 0.f, num);
+  den += m10 ? e.w10 : 0.f;
+  num = fmaf(m10 ? e.w10 : 0.f, m10 ? v10 : 0.f, num);
+  den += m11 ? e.w11 : 0.f;
+  num = fmaf(m11 ? e.w11 : 0.f, m11 ? v11 : 0.f, num);
+  const float r = fmaf(-e.W, __fdividef(num, den), e.I);
+  return (m00 || m01 || m10 || m11) ? e.fwv * (r * r) : e.fb;
+}
+
 // Same trial from four corner values in registers (off-grid cells carry
 // kOffGrid, a NaN with its own payload, so one value gives position, validity
 // and value).  Equal to trial_global: the reference's bounds rule (row in
