@@ -338,12 +338,15 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned n = *a.slow_n;
   const int nk_ph = a.ka * a.kb, nk = a.na_full * a.nb_full;
+  const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
   int ta[kSlowPerLane], tb[kSlowPerLane];   // patch coordinates of the lane's trials
+  int to[kSlowPerLane];                     // and their cell offsets from the patch corner
 #pragma unroll
   for (int j = 0; j < kSlowPerLane; ++j) {
     const int t = lane + 32 * j;
     ta[j] = t / a.kb;
     tb[j] = t % a.kb;
+    to[j] = ta[j] * of + tb[j];
   }
   const int64_t plane = a.sc.ss * a.sc.fs;
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
@@ -397,11 +400,17 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
                                               __shfl_sync(0xffffffffu, sl.fy, bsel),
                                               __shfl_sync(0xffffffffu, Wl, bsel),
                                               __shfl_sync(0xffffffffu, Il, bsel), 1.f);
+          if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {   // warp-uniform
+            const float* w0 = a.fmn + (pr0 * of + pc0);
 #pragma unroll
-          for (int j = 0; j < kSlowPerLane; ++j)
-            if (lane + 32 * j < nk_ph)
-              part[j] += trial_global(a.fmn, static_cast<int>(a.os),
-                                      static_cast<int>(a.of), pr0 + ta[j], pc0 + tb[j], es);
+            for (int j = 0; j < kSlowPerLane; ++j)
+              if (lane + 32 * j < nk_ph) part[j] += trial_interior(w0 + to[j], of, es);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kSlowPerLane; ++j)
+              if (lane + 32 * j < nk_ph)
+                part[j] += trial_global(a.fmn, os, of, pr0 + ta[j], pc0 + tb[j], es);
+          }
         }
       }
     }
