@@ -254,6 +254,11 @@ def run_ours(args, rank, world, local):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        probe = torch.ones(1, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(probe)                 # communicator up: every rank answered
+        print(f"[bench] rank {rank}: {backend} process group initialised, "
+              f"nranks={dist.get_world_size()}, all_reduce(1)={int(probe.item())}",
+              file=sys.stderr, flush=True)
     host_data = args.config <= 1
     if host_data:
         s = make_scan(args.config)
@@ -491,13 +496,36 @@ def e2e(s, args, pb, engine, torch, trials):
                     " pinned host frames, device cache cleared each step)"}
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch the N ranks (one process per
+    GPU) through torch.distributed.run on this node, same arguments."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    launched = "WORLD_SIZE" in os.environ
     if args.impl == "reference":
-        run_reference(args, rank, world)
-    else:
-        run_ours(args, rank, world, local)
+        # CPU arm: rank 0 alone runs (the other torchrun ranks exit without work)
+        run_reference(args, rank, world if launched else args.gpus)
+        return
+    if not launched and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

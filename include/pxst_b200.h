@@ -77,6 +77,12 @@ const char* pxst_last_error(void);
 /* Number of kernels this thread has launched through the library (for the
  * bench's gpu_launches count). */
 int64_t pxst_launch_count(void);
+/* Return the scratch memory the library keeps in the current device's
+ * default memory pool to the driver (synchronises the device).  The
+ * library raises the pool's release threshold so stream-ordered scratch is
+ * not re-mapped at every synchronisation; this undoes the retention (the
+ * Python shim's clear_cache() calls it). */
+int pxst_release_pool(void);
 
 /* K0: per-scan statistics.  Replaces the fallback/variance/normaliser
  * computations at recon.py:257-260, :367 and :410-412.  `fw` (nullable,

@@ -45,6 +45,7 @@ _SIGS = {
     "pxst_abi_version": (c_int, []),
     "pxst_last_error": (c_char_p, []),
     "pxst_launch_count": (c_int64, []),
+    "pxst_release_pool": (c_int, []),
     "pxst_stack_stats": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_void_p]),
     "pxst_stack_stats_parts": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_int,
                                        c_void_p]),

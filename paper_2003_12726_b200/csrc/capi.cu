@@ -38,3 +38,16 @@ void retain_pool_memory() {
 extern "C" int pxst_abi_version(void) { return PXST_ABI_VERSION; }
 extern "C" const char* pxst_last_error(void) { return pxst::g_err; }
 extern "C" int64_t pxst_launch_count(void) { return pxst::g_launches; }
+
+// Hand the scratch memory the library kept in the current device's default
+// pool back to the driver (the pool otherwise retains it for the process,
+// see retain_pool_memory): waits for the device, then trims to zero bytes.
+extern "C" int pxst_release_pool(void) {
+  int dev = 0;
+  PXST_CHECK_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  PXST_CHECK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  PXST_CHECK_CUDA(cudaDeviceSynchronize());
+  PXST_CHECK_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return PXST_OK;
+}

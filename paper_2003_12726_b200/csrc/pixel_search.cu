@@ -787,10 +787,11 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
 // generic (sub-pixel / any window): float64, one thread per (pixel, trial)
 // ---------------------------------------------------------------------------
 __global__ void k_pix_generic(PixArgs a, const double* __restrict__ offs_a,
-                              const double* __restrict__ offs_b, double* __restrict__ errs) {
+                              const double* __restrict__ offs_b, double* __restrict__ errs,
+                              int t0) {
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2];
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int t = blockIdx.y;
+  const int t = t0 + blockIdx.y;
   if (q >= a.nq) return;
   const int64_t p = (a.sc.roi[0] + q / cw) * a.sc.fs + a.sc.roi[2] + q % cw;
   if (!a.sc.work[p]) return;
@@ -1136,10 +1137,11 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
   // generic path
   Scratch errs;
   if (int e = errs.alloc(sizeof(double) * a.nq * nk, s)) return e;
-  PXST_REQUIRE(nk <= kMaxGridY, "search window too large");
-  dim3 g(qblocks, (unsigned)nk);
-  k_pix_generic<<<g, 128, 0, s>>>(a, d_oa, d_ob, errs.as<double>());
-  PXST_CHECK_LAUNCH();
+  for (int t0 = 0; t0 < nk; t0 += kMaxGridY) {       // grid.y <= 65535 trials per launch
+    dim3 g(qblocks, (unsigned)std::min(nk - t0, kMaxGridY));
+    k_pix_generic<<<g, 128, 0, s>>>(a, d_oa, d_ob, errs.as<double>(), t0);
+    PXST_CHECK_LAUNCH();
+  }
   k_pix_epilogue<double, 2><<<qblocks * 2, 128, 0, s>>>(a, errs.as<double>(), 1);
   PXST_CHECK_LAUNCH();
   return PXST_OK;

@@ -122,7 +122,9 @@ std::vector<double> window_offsets(int64_t half, double step) {
   if (step <= 0.0) {
     for (int64_t k = -half; k <= half; ++k) o.push_back(static_cast<double>(k));
   } else {
-    const int64_t kh = static_cast<int64_t>(llround(static_cast<double>(half) / step));
+    // Python round() (recon.py:55): ties to even, as nearbyint in the default
+    // rounding mode (llround would round 0.5 away from zero)
+    const int64_t kh = static_cast<int64_t>(nearbyint(static_cast<double>(half) / step));
     for (int64_t k = -kh; k <= kh; ++k) o.push_back(step * static_cast<double>(k));
   }
   return o;

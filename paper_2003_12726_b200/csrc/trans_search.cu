@@ -476,12 +476,11 @@ __global__ void k_trans_generic(TransArgs a, const double* __restrict__ offs_a,
 // 4. per-frame epilogue
 // ---------------------------------------------------------------------------
 __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_norm,
-                                 const double* __restrict__ part, int64_t frame_lo, int na,
+                                 double* part, int64_t frame_lo, int na,
                                  int nb, const double* __restrict__ offs_a,
                                  const double* __restrict__ offs_b, const double* di,
                                  const double* dj, double* di_out, double* dj_out,
                                  double* err_out) {
-  extern __shared__ double e[];
   __shared__ double bv[32];
   __shared__ int bi[32];
   const int64_t kk = blockIdx.x;
@@ -489,8 +488,11 @@ __global__ void k_trans_epilogue(pxst_scan sc, const double* __restrict__ frame_
   const int64_t f = sc.good[k];
   const double norm = frame_norm[k];
   const int nk = na * nb;
-  const double* pp = part + kk * nk;
-  for (int t = threadIdx.x; t < nk; t += blockDim.x) e[t] = norm > 0.0 ? pp[t] / norm : pp[t];
+  // normalised in place in the frame's partial row (any window size: no
+  // shared-memory copy of the nk errors)
+  double* e = part + kk * nk;
+  if (norm > 0.0)
+    for (int t = threadIdx.x; t < nk; t += blockDim.x) e[t] = e[t] / norm;
   __syncthreads();
   if (err_out)
     for (int t = threadIdx.x; t < nk; t += blockDim.x) err_out[kk * nk + t] = e[t];
@@ -721,7 +723,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
           PXST_CHECK_CUDA(cudaMemsetAsync(a.dbg, 0, sizeof(d), s));
         }
       }
-      k_trans_epilogue<<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
+      k_trans_epilogue<<<(unsigned)(c1 - c0), 256, 0, s>>>(
           *sc, st->frame_norm, part.as<double>(), c0, na, nb, d_oa, d_ob, di, dj, di_out,
           dj_out, err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
       PXST_CHECK_LAUNCH();
@@ -735,7 +737,7 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     dim3 g((unsigned)nk, (unsigned)(c1 - c0));
     k_trans_generic<<<g, 256, 0, s>>>(a, d_oa, d_ob, part.as<double>());
     PXST_CHECK_LAUNCH();
-    k_trans_epilogue<<<(unsigned)(c1 - c0), 256, sizeof(double) * nk, s>>>(
+    k_trans_epilogue<<<(unsigned)(c1 - c0), 256, 0, s>>>(
         *sc, st->frame_norm, part.as<double>(), c0, na, nb, d_oa, d_ob, di, dj, di_out, dj_out,
         err_out ? err_out + (c0 - frame_lo) * nk : nullptr);
     PXST_CHECK_LAUNCH();

@@ -186,7 +186,7 @@ class DeviceScan:
     """One scan + whitefield + mask + ROI resident on the current CUDA device."""
 
     def __init__(self, frames, good_frames, W, mask, roi=None, device=None,
-                 frames_dev: torch.Tensor | None = None):
+                 frames_dev: torch.Tensor | None = None, frames_upload: dict | None = None):
         self.device = device or _device()
         self.lib = _native.lib()
         frames_shape = tuple(frames_dev.shape) if frames_dev is not None else np.shape(frames)
@@ -203,6 +203,15 @@ class DeviceScan:
         # frames uploads still in flight: [(good_lo, good_hi, event)] on a copy
         # stream (pinned host stacks; shared with band views through the dict)
         self._upload = {"chunks": [], "waited": True, "stats": 0}   # stats: K0 parts run
+        if frames_upload is not None and not frames_upload["waited"]:
+            # a stack shared with another scan whose upload may still be in
+            # flight: wait for the same copy events before any kernel reads it
+            # (the copies run in order on one stream: the last event covers all;
+            # the chunk ranges index the other scan's good frames, so one range
+            # over this scan's good frames replaces them)
+            last = frames_upload["chunks"][-1][2]
+            self._upload.update(chunks=[(0, self.n_good, last)], waited=False,
+                                host=frames_upload.get("host"))
         self._uploads: list = []     # identity cache of pixel maps / translations
         if frames_dev is None:
             frames_dev = self._upload_frames(frames, dev)
@@ -693,14 +702,16 @@ class _ScanCache:
             for k, refs, ds in self.entries:
                 if k == key and all(r() is not None for r in refs):
                     return ds
-        frames_dev = None
+        frames_dev = upload = None
         if self.enabled:
             # reuse an uploaded stack when only W / mask / ROI / good frames differ
+            # (with its upload events: the copy may still be running)
             for k, refs, ds in self.entries:
                 if k[0] == key[0] and refs[0]() is not None:
-                    frames_dev = ds.frames
+                    frames_dev, upload = ds.frames, ds._upload
                     break
-        ds = DeviceScan(frames, scan.good_frames, w.w, m.mask, roi, frames_dev=frames_dev)
+        ds = DeviceScan(frames, scan.good_frames, w.w, m.mask, roi, frames_dev=frames_dev,
+                        frames_upload=upload)
         if self.enabled:
             self.entries.append((key, [self._ref(a) for a in arrays], ds))
             del self.entries[:-self.max_entries]
@@ -714,5 +725,12 @@ SCAN_CACHE = _ScanCache()
 
 
 def clear_cache() -> None:
+    """Drop every cached device scan / reference and return the memory: torch's
+    caching allocator and the scratch the library keeps in the device's
+    default pool (pxst_release_pool)."""
     SCAN_CACHE.clear()
+    from . import recon
+    recon._REF_CACHE.clear()
     torch.cuda.empty_cache()
+    if torch.cuda.is_available():
+        check(_native.lib().pxst_release_pool())

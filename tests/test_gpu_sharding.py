@@ -126,3 +126,23 @@ def test_two_ranks_device_kernels(scan0):
     assert abs(out["total"] - float(total.item())) <= 1e-5 * float(total.item())
     np.testing.assert_allclose(out["per_frame"], per_frame.cpu().numpy(), rtol=1e-5)
     np.testing.assert_allclose(out["plane"], plane.cpu().numpy(), rtol=1e-4, atol=1e-9)
+
+
+def test_bench_spawns_ranks():
+    """`python bench.py --gpus 2` (no torchrun) launches the two ranks itself
+    and reports n_gpus = 2 (one-GPU functional mode: gloo, ranks sharing
+    cuda:0, host-staged collectives)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PXST_BENCH_BACKEND="gloo", PXST_BENCH_ONE_GPU="1")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--config", "0", "--steps", "3", "--warmup", "3", "--profile"],
+                         env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2
+    assert "nranks=2" in out.stderr

@@ -158,13 +158,95 @@ __global__ void k_lds_cyc(float* out, long long* cyc, int iters, int mode) {
     for (int it = 0; it < iters; ++it) {
       const float4* q = p4 + ((it * 64) & 1023);
 #pragma unroll
-      for (int k = 0; k < 4; k += 1) { float4 a = q[k * 128]; s0 += a.x; s1 += a.y; s2 += a.z; s3 += a.w; }
+      for (int k = 0; k < 4; k += 1) { float4 a = p4[(q - p4 + k * 128 + w * 32 + lane) & 2047]; s0 += a.x; s1 += a.y; s2 += a.z; s3 += a.w; }
     }
   }
   __syncthreads();
   long long t1 = clock64();
   out[blockIdx.x * blockDim.x + threadIdx.x] = s0 + s1 + s2 + s3;
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// Shared-memory u32 atomics: each lane adds into its own word (spread = a
+// lane-dependent hash inside a 4096-word window, row = consecutive words).
+__global__ void k_atoms(float* out, int iters, int row) {
+  __shared__ unsigned sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const unsigned h = row ? ((w * 32 + lane + (it * 8 + k) * 256) & 4095)
+                             : (((w * 32 + lane) * 2654435761u + (it * 8 + k) * 40503u) >> 20) & 4095;
+      atomicAdd(&sm[h], lane + (unsigned)k + 3u);
+    }
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sm[threadIdx.x & 4095];
+}
+
+// Shared-memory f32 atomics (compiled as ATOMS.CAS loops or native adds).
+__global__ void k_atoms_f32(float* out, int iters) {
+  __shared__ float sm[4096];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) sm[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&sm[(w * 32 + lane + (it * 8 + k) * 256) & 4095], 1.f);
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sm[threadIdx.x & 4095];
+}
+
+// Shared-memory read-modify-write of float4 cells (LDS.128 + 4 FADD + STS.128).
+__global__ void k_rmw128(float* out, int iters) {
+  __shared__ float4 sm[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = make_float4(0, 0, 0, 0);
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4* mine = sm + (w * 32 & 2047);   // warps own disjoint 32-cell rows
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float4* c = mine + ((lane + it * 8 + k) & 31);
+      float4 v = *c;
+      v.x += 1.f; v.y += 2.f; v.z += 3.f; v.w += 4.f;
+      *c = v;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sm[threadIdx.x & 2047].x;
+}
+
+__global__ void k_match(float* out, int iters) {
+  unsigned acc = 0;
+  const unsigned lane = threadIdx.x & 31;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += __match_any_sync(0xffffffffu, (lane + it + k) >> 1);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+// Global REDs into an L2-resident 4 MB image, lanes on consecutive cells of a
+// row (the splat pattern): v4.f32 (16 B per lane) vs u64 (8 B per lane).
+__global__ void k_red_v4_rows(float4* acc, int n_cells, int iters) {
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    const unsigned h = ((tid >> 5) * 977u + it * 131u) * 32u % (n_cells - 64) + (threadIdx.x & 31);
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(acc + h), "f"(1.f),
+                 "f"(1.f), "f"(1.f), "f"(1.f) : "memory");
+  }
+}
+__global__ void k_red_u64_rows(unsigned long long* acc, int n_cells, int iters) {
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    const unsigned h = ((tid >> 5) * 977u + it * 131u) * 32u % (n_cells - 64) + (threadIdx.x & 31);
+    atomicAdd(acc + h, 1ull);
+  }
 }
 
 int main() {
@@ -230,6 +312,25 @@ int main() {
       double bytes = 1024.0 * it * 64;  // 16 floats per iter per thread
       printf(", \"lds_mode%d_B_per_clk_sm\": %.1f", mode, bytes / mean);
     }
+  }
+  {
+    const int ai = 256;
+    const double ops = lanes * ai * 8;
+    ms = timeit([&] { k_atoms<<<blocks, threads>>>(fout, ai, 0); });
+    printf(", \"atoms_u32_spread_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_atoms<<<blocks, threads>>>(fout, ai, 1); });
+    printf(", \"atoms_u32_row_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_atoms_f32<<<blocks, threads>>>(fout, ai); });
+    printf(", \"atoms_f32_row_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_rmw128<<<blocks, threads>>>(fout, ai); });
+    printf(", \"smem_rmw128_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_match<<<blocks, threads>>>(fout, ai); });
+    printf(", \"match_any_warp_ops_per_clk_sm\": %.3f", ops / 32 / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    const int cells = 1 << 18;   // 4 MB of float4: L2 resident
+    ms = timeit([&] { k_red_v4_rows<<<blocks, threads>>>((float4*)acc, cells, aiters); });
+    printf(", \"redg_v4f32_rows_Gops\": %.1f", lanes * aiters / (ms * 1e-3) / 1e9);
+    ms = timeit([&] { k_red_u64_rows<<<blocks, threads>>>(acc, cells, aiters); });
+    printf(", \"redg_u64_rows_Gops\": %.1f", lanes * aiters / (ms * 1e-3) / 1e9);
   }
   printf("}\n");
   CK(cudaGetLastError());
