@@ -15,13 +15,14 @@
 //                    whose patch leaves the grid or touches an invalid cell are
 //                    skipped; their tiles are flagged in a per-frame bitmap and
 //                    the frame is listed.
-//   3. k_trans_slow  one warp per listed frame: re-derives eligibility over the
-//                    flagged tiles' pixels lane-parallel, stages each skipped
-//                    sample's patch in shared memory, lanes over trials with the
-//                    exact masked read and (I-W)^2 fallback, register
-//                    accumulation, one add per trial into the frame's partial
-//                    (single owner: ordered, deterministic).
-//   4. k_trans_epilogue per frame: normalise by sum_p (I_n-W)^2,
+//   3. k_trans_slow  one block per listed frame: its 8 warps take the frame's
+//                    flagged tiles in turn, re-derive eligibility over each
+//                    tile's pixels lane-parallel and, for every skipped sample,
+//                    evaluate the trials with lanes over trials (exact masked
+//                    read of the NaN-encoded reference, (I-W)^2 fallback) into
+//                    registers; the warps' sums are added in warp order, one
+//                    add per trial into the frame's partial (deterministic).
+//   4. k_trans_epilogue per frame: normalise by sum_p (I_n-W)^2 in place,
 //                    first-occurrence argmin, always-on paraboloid when interior
 //                    (grid-index units added in pixels).
 // Sub-pixel grids with q = 1/step integral decompose into q^2 phase groups:

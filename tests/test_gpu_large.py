@@ -153,3 +153,32 @@ def test_error_maps_band_vs_oracle(cfg_id, rows):
     good = s.scan.good_frames
     assert abs(float(total.item()) - pf[good].sum()) <= 1e-9 * abs(pf[good].sum())
     assert np.all(pf[~good] == 0)
+
+
+@pytest.mark.slow
+def test_cfg2_object_map_full_vs_reference():
+    """Config 2's full object map (1000 frames of 516x1556, numpy-rendered so
+    it is bit-identical to the build container's) against the LIVE
+    reference's make_reference (tests/golden/make_golden_loop.py: ref2.npz,
+    i_ref stored as float32): every valid cell within 1e-5 relative, identical
+    validity and origin (recon.py:99-141)."""
+    import hashlib
+    import paper_2003_12726_b200 as pb
+    from paper_2003_12726_b200.synth import make_scan
+    from conftest import GOLDEN
+    g = dict(np.load(os.path.join(GOLDEN, "ref2.npz")))
+    s = make_scan(2)
+    assert hashlib.sha256(np.ascontiguousarray(s.scan.frames).tobytes()).hexdigest() == \
+        str(g["frames_sha"])
+    ref = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
+    shape = tuple(int(v) for v in g["ref_shape"])
+    assert ref.i_ref.shape == shape
+    assert tuple(ref.origin) == tuple(int(v) for v in g["ref_origin"])
+    valid = np.unpackbits(g["ref_valid"])[:shape[0] * shape[1]].reshape(shape).astype(bool)
+    np.testing.assert_array_equal(ref.wsum > 0, valid)
+    gi = g["ref_i"].astype(np.float64)
+    rel = np.abs(ref.i_ref - gi)[valid] / np.maximum(np.abs(gi[valid]), 1e-30)
+    assert rel.max() < 1e-5, rel.max()
+    # float64 row sums of the reference's own i_ref (no float32 storage loss)
+    np.testing.assert_allclose(ref.i_ref.sum(axis=1), g["ref_i_rowsum"], rtol=1e-6)
+    engine.clear_cache()
