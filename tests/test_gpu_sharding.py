@@ -136,7 +136,10 @@ def test_bench_spawns_ranks():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PXST_BENCH_BACKEND="gloo", PXST_BENCH_ONE_GPU="1")
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR",
+                        "MASTER_PORT", "GROUP_RANK", "ROLE_RANK")}
+    env.update(PXST_BENCH_BACKEND="gloo", PXST_BENCH_ONE_GPU="1")
     out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
                           "--config", "0", "--steps", "3", "--warmup", "3", "--profile"],
                          env=env, capture_output=True, text=True, timeout=600, cwd=root)

@@ -158,7 +158,7 @@ __global__ void k_lds_cyc(float* out, long long* cyc, int iters, int mode) {
     for (int it = 0; it < iters; ++it) {
       const float4* q = p4 + ((it * 64) & 1023);
 #pragma unroll
-      for (int k = 0; k < 4; k += 1) { float4 a = p4[(q - p4 + k * 128 + w * 32 + lane) & 2047]; s0 += a.x; s1 += a.y; s2 += a.z; s3 += a.w; }
+      for (int k = 0; k < 4; k += 1) { float4 a = reinterpret_cast<const float4*>(sm)[((q - p4) + k * 128 + w * 32 + lane) & 2047]; s0 += a.x; s1 += a.y; s2 += a.z; s3 += a.w; }
     }
   }
   __syncthreads();
