@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define PXST_ABI_VERSION 1
+#define PXST_ABI_VERSION 2
 
 /* status codes */
 #define PXST_OK 0
@@ -105,26 +105,57 @@ int pxst_stack_stats_parts(const pxst_scan* scan, const float* fw, const pxst_st
 int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const double* dj,
               double* out, void* stream);
 
+/* Deterministic splat accumulators (K1 object numerator / denominator, K4
+ * reference-plane numerator / denominator).  Every float64 term t of the
+ * reference's bincount (interp.py:113-122) is rounded once to an integer
+ * multiple of a power-of-two quantum q (round to nearest even) and the
+ * integers are summed exactly in int64, so the images do not depend on the
+ * order of the additions, on the kernels' work split or on the number of
+ * GPUs: frame shards all-reduce num/den as int64 (exact) and touched with
+ * max.  quanta (device, float64[2]) = (q_num, q_den), chosen so that
+ * |t| < 2^41 q (pxst_object_quanta / pxst_plane_quanta; ~41 significant
+ * bits relative to the largest possible term).  touched[c] = 1 where a
+ * positive-weight term landed: the reference's wsum > 0 (data_model.py:186). */
+typedef struct pxst_accum {
+  int64_t* num;           /* [cells], units of quanta[0]        */
+  int64_t* den;           /* [cells], units of quanta[1]        */
+  uint8_t* touched;       /* [cells] or NULL                    */
+  const double* quanta;   /* device [2]                         */
+} pxst_accum;
+
+/* max |I| over the whole frame stack (device float64 scalar): the bound the
+ * quanta are derived from.  One pass over the stack; cache it per stack. */
+int pxst_stack_absmax(const pxst_scan* scan, double* out, void* stream);
+
+/* Quanta of the object accumulators: q_num from max|I| max W, q_den from
+ * max W^2 (max W over the ROI's work pixels), with headroom for n_good
+ * frames.  Frame shards must use the same quanta (same scan, same absmax). */
+int pxst_object_quanta(const pxst_scan* scan, const double* absmax, double* quanta,
+                       void* stream);
+
 /* K1 object formation, splat half (recon.py:99-138; interp.py:88-123).
  * Adds, for every good frame in [frame_lo, frame_hi) of scan->good and work
- * pixel, I*W*w_c to num and W^2*w_c to den (float64, [os*of]) at the four
- * bilinear corners of (u0 - di - n0, u1 - dj - m0).  Points outside
- * [0,os-1]x[0,of-1] are dropped whole; their count is added to *n_dropped
- * (device, nullable).  Frame ranges let frame shards accumulate partial
- * images that are summed (all-reduce) before pxst_object_finish. */
+ * pixel, the fixed-point terms of I*W*w_c to acc->num and W^2*w_c to
+ * acc->den ([os*of]) at the four bilinear corners of (u0 - di - n0,
+ * u1 - dj - m0), and marks acc->touched.  Points outside [0,os-1]x[0,of-1]
+ * are dropped whole; their count is added to *n_dropped (device, nullable).
+ * Frame ranges let frame shards accumulate partial images that are summed
+ * (int64 all-reduce) before pxst_object_finish. */
 int pxst_object_splat(const pxst_scan* scan, const double* u, const double* di,
                       const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-                      int64_t frame_lo, int64_t frame_hi, double* num, double* den,
+                      int64_t frame_lo, int64_t frame_hi, const pxst_accum* acc,
                       unsigned long long* n_dropped, void* stream);
 
 /* K1 normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0,
- * wsum = den; also writes the float32 masked image fm and validity flags the
- * search kernels read.  Any of the four outputs may be NULL. */
-int pxst_object_finish(const double* num, const double* den, int64_t n, double* i_ref,
-                       double* wsum, float* fm, uint8_t* valid, void* stream);
+ * wsum = den (in float64 units), valid = touched (or den > 0 without
+ * touched); also writes the float32 masked image fm the search kernels read.
+ * Any of the four outputs may be NULL.  (A touched cell whose whole weight
+ * rounds below one quantum keeps valid = 1 with i_ref = 0 and a tiny wsum.) */
+int pxst_object_finish(const pxst_accum* acc, int64_t n, double* i_ref, double* wsum, float* fm,
+                       uint8_t* valid, void* stream);
 
-/* Convenience: splat + finish over all good frames for a known grid
- * (recon.make_reference after the bbox of pxst_bbox). */
+/* Convenience: absmax + quanta + splat + finish over all good frames for a
+ * known grid (recon.make_reference after the bbox of pxst_bbox). */
 int pxst_object_map(const pxst_scan* scan, const double* u, const double* di, const double* dj,
                     int64_t n0, int64_t m0, int64_t os, int64_t of, double* i_ref, double* wsum,
                     float* fm, uint8_t* valid, void* stream);
@@ -173,30 +204,39 @@ int pxst_translation_search(const pxst_scan* scan, const pxst_stats* st, const p
                             int64_t frame_lo, int64_t frame_hi, double* di_out,
                             double* dj_out, double* err_out, void* stream);
 
+/* Quanta of the reference-plane accumulators (see pxst_accum): q_num from
+ * the bound (max|I| + max W max(1, max|ref|))^2 / min sigma2 on eps, q_den
+ * from 1 (weight 1).  Row shards must share the full scan's quanta. */
+int pxst_plane_quanta(const pxst_scan* scan, const double* absmax, const pxst_stats* st,
+                      const pxst_ref* ref, double* quanta, void* stream);
+
 /* K4 error maps (recon.py:388-438), one pass over the stack: per_frame
  * [n_frames] (0 for frames not good), per_pixel [ss,fs], ref_plane [os,of]
  * (normalised reference-plane projection of the residuals, every work sample
- * splatted with weight 1), total (device scalar). */
+ * splatted with weight 1, in exact fixed point: bit-reproducible), total
+ * (device scalar).  absmax (nullable) = pxst_stack_absmax of the stack;
+ * computed here when NULL. */
 int pxst_error_maps(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
-                    const double* u, const double* di, const double* dj, double* per_frame,
-                    double* per_pixel, double* ref_plane, double* total, void* stream);
+                    const double* u, const double* di, const double* dj, const double* absmax,
+                    double* per_frame, double* per_pixel, double* ref_plane, double* total,
+                    void* stream);
 
 /* K4 fused with the NEXT iteration's K1 splat: calc_error(ref, u, t) and
  * make_reference(u, t) read the same samples at the same positions
  * u - delta (recon.py:511-516 calls them back to back), so one pass over the
  * stack produces the error maps of `ref` and adds the next object's
- * numerator / denominator into num / den as pxst_object_splat would.  The
- * next grid (n0, m0, os, of) is read from DEVICE memory `grid` (e.g. written
- * by pxst_bbox + pxst_grid_rule on a side stream), so the call never waits
- * for the host; num / den hold `capacity` cells (the grid is laid out densely
- * in the first os*of) and a grid with os*of > capacity is not splatted -- the
- * caller, who learns the grid later, then forms the object separately.
- * Finish the next object with pxst_object_finish. */
+ * fixed-point terms into `next` as pxst_object_splat would (next->quanta
+ * from pxst_object_quanta).  The next grid (n0, m0, os, of) is read from
+ * DEVICE memory `grid` (e.g. written by pxst_bbox + pxst_grid_rule on a side
+ * stream), so the call never waits for the host; next holds `capacity` cells
+ * (the grid is laid out densely in the first os*of) and a grid with
+ * os*of > capacity is not splatted -- the caller, who learns the grid later,
+ * then forms the object separately.  Finish it with pxst_object_finish. */
 int pxst_error_maps_splat(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
                           const double* u, const double* di, const double* dj,
-                          double* per_frame, double* per_pixel, double* ref_plane, double* total,
-                          const int64_t* grid, int64_t capacity, double* num, double* den,
-                          void* stream);
+                          const double* absmax, double* per_frame, double* per_pixel,
+                          double* ref_plane, double* total, const int64_t* grid,
+                          int64_t capacity, const pxst_accum* next, void* stream);
 
 /* Grid rule of recon.py:126-132 on the device: grid[4] = (n0, m0, os, of)
  * from the 8 bbox values of pxst_bbox (both device pointers). */
@@ -204,13 +244,14 @@ int pxst_grid_rule(const double* bbox, int64_t* grid, void* stream);
 
 /* K4 without the final normalisation, for detector-row shards: per_frame
  * [n_frames] = this ROI's per-frame sums, per_pixel [ss,fs] (this ROI only),
- * and the reference-plane numerator/denominator ADDED into plane_num /
- * plane_den [os,of] (caller-zeroed).  After an all-reduce (sum) of per_frame,
- * plane_num and plane_den across shards, pxst_object_finish(plane_num,
- * plane_den, ...) yields reference_plane. */
+ * and the reference-plane fixed-point terms ADDED into plane ([os,of],
+ * caller-zeroed, quanta from pxst_plane_quanta of the FULL scan).  After an
+ * all-reduce (sum) of per_frame and of plane->num / plane->den (int64,
+ * exact) across shards, pxst_object_finish(plane, ...) yields
+ * reference_plane. */
 int pxst_error_partials(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
                         const double* u, const double* di, const double* dj, double* per_frame,
-                        double* per_pixel, double* plane_num, double* plane_den, void* stream);
+                        double* per_pixel, const pxst_accum* plane, void* stream);
 
 /* Interpolation primitives (interp.py:53-85 and :88-123), for the drop-in
  * interp module and the parity tests.  gather: vals/ok at n points of the

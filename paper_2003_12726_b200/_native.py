@@ -16,7 +16,7 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int64, c_uint8, c_uint6
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PXST_LIB", os.path.join(HERE, "libpxst_b200.so"))
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 PXST_OK, PXST_EINVAL, PXST_ECUDA, PXST_ENOMEM = 0, 1, 2, 3
 
@@ -37,6 +37,11 @@ class PxstRef(ctypes.Structure):
                 ("n0", c_int64), ("m0", c_int64), ("fm64", c_void_p)]
 
 
+class PxstAccum(ctypes.Structure):
+    _fields_ = [("num", c_void_p), ("den", c_void_p), ("touched", c_void_p),
+                ("quanta", c_void_p)]
+
+
 class PxstCgInfo(ctypes.Structure):
     _fields_ = [("iterations", c_int64), ("residual", c_double), ("converged", c_int)]
 
@@ -50,10 +55,14 @@ _SIGS = {
     "pxst_stack_stats_parts": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_int,
                                        c_void_p]),
     "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_stack_absmax": (c_int, [POINTER(PxstScan), c_void_p, c_void_p]),
+    "pxst_object_quanta": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p]),
+    "pxst_plane_quanta": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats),
+                                  POINTER(PxstRef), c_void_p, c_void_p]),
     "pxst_object_splat": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
-                                  c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
-                                  c_void_p, c_void_p, c_void_p]),
-    "pxst_object_finish": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_int64, c_int64, c_int64, c_int64, c_int64,
+                                  POINTER(PxstAccum), c_void_p, c_void_p]),
+    "pxst_object_finish": (c_int, [POINTER(PxstAccum), c_int64, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p]),
     "pxst_object_map": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
                                 c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
@@ -72,15 +81,15 @@ _SIGS = {
                                         c_void_p, c_void_p]),
     "pxst_error_maps": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                c_void_p, c_void_p]),
+                                c_void_p, c_void_p, c_void_p]),
     "pxst_error_maps_splat": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                      c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_int64, POINTER(PxstAccum),
                                       c_void_p]),
     "pxst_grid_rule": (c_int, [c_void_p, c_void_p, c_void_p]),
     "pxst_error_partials": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
-                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                    c_void_p, c_void_p]),
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    POINTER(PxstAccum), c_void_p]),
     "pxst_gather": (c_int, [POINTER(PxstRef), c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                             c_void_p]),
     "pxst_splat": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,

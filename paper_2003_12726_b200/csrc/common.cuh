@@ -150,81 +150,4 @@ __device__ __forceinline__ bool masked_read(const float* __restrict__ fm,
   return true;
 }
 
-// ---------------------------------------------------------------------------
-// Grouped bilinear splat.  A cell group g(r, c) is a float4 holding
-// (num, den) of cell (r, c) and (num, den) of cell (r+1, c); one sample adds
-// its four corners with two 16-byte `red.global.add.v4.f32` into g(r0, c0)
-// and g(r0, c1).  Corners the reference clips (interp.py:44-45: r1 = r0 at the
-// last row) always carry zero weight (an inside point on the last row has
-// fx = 0), so the grouping is exact.  Groups accumulate in float32 per frame
-// chunk image; k_group_fold sums the images in float64 in a fixed order.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void red_v4(float4* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
-}
-
-// value*w_c and weight*w_c at the four corners of cell index `cell` =
-// r0*of + c0 with fractions (fx, fy).
-__device__ __forceinline__ void splat_grouped(float4* img, int64_t cell, double fx, double fy,
-                                              double value_w, double weight) {
-  const double gx = 1.0 - fx, gy = 1.0 - fy;
-  const double w00 = gx * gy, w01 = gx * fy, w10 = fx * gy, w11 = fx * fy;
-  float4* g0 = img + cell;
-  red_v4(g0, static_cast<float>(value_w * w00), static_cast<float>(weight * w00),
-         static_cast<float>(value_w * w10), static_cast<float>(weight * w10));
-  if (fy > 0.0)
-    red_v4(g0 + 1, static_cast<float>(value_w * w01), static_cast<float>(weight * w01),
-           static_cast<float>(value_w * w11), static_cast<float>(weight * w11));
-}
-
-// Warp-cooperative splat_grouped (every lane of the warp must call it; `act`
-// = this lane has a sample).  Lanes are consecutive detector pixels, so lane
-// i's second group (cell + 1) is usually lane i+1's first group: lane i adds
-// that value to its own and lane i+1 skips its RED.  This removes about a
-// third of the L1 -> L2 RED sectors, which bound the splat kernels (ncu:
-// l1tex__m_l1tex2xbar_req_cycles_active ~75 %).  Sums stay float32 per image
-// with a run-to-run varying order, as before.
-__device__ __forceinline__ void splat_grouped_warp(float4* img, int64_t cell, double fx, double fy,
-                                                   double value_w, double weight, bool act) {
-  const unsigned lane = threadIdx.x & 31u;
-  const double gx = 1.0 - fx, gy = 1.0 - fy;
-  const double w00 = gx * gy, w01 = gx * fy, w10 = fx * gy, w11 = fx * fy;
-  const bool has_b = act && fy > 0.0;
-  float a0 = act ? static_cast<float>(value_w * w00) : 0.f;
-  float a1 = act ? static_cast<float>(weight * w00) : 0.f;
-  float a2 = act ? static_cast<float>(value_w * w10) : 0.f;
-  float a3 = act ? static_cast<float>(weight * w10) : 0.f;
-  float b0 = has_b ? static_cast<float>(value_w * w01) : 0.f;
-  float b1 = has_b ? static_cast<float>(weight * w01) : 0.f;
-  float b2 = has_b ? static_cast<float>(value_w * w11) : 0.f;
-  float b3 = has_b ? static_cast<float>(weight * w11) : 0.f;
-  const long long nxt = __shfl_down_sync(0xffffffffu, static_cast<long long>(cell), 1);
-  const unsigned acts = __ballot_sync(0xffffffffu, act);
-  const bool merge = lane < 31u && act && ((acts >> (lane + 1u)) & 1u) &&
-                     nxt == static_cast<long long>(cell) + 1;
-  const unsigned merges = __ballot_sync(0xffffffffu, merge);
-  const bool absorbed = lane > 0u && ((merges >> (lane - 1u)) & 1u);
-  const float n0 = __shfl_down_sync(0xffffffffu, a0, 1), n1 = __shfl_down_sync(0xffffffffu, a1, 1);
-  const float n2 = __shfl_down_sync(0xffffffffu, a2, 1), n3 = __shfl_down_sync(0xffffffffu, a3, 1);
-  if (merge) {
-    b0 += n0;
-    b1 += n1;
-    b2 += n2;
-    b3 += n3;
-  }
-  float4* g0 = img + cell;
-  if (act && !absorbed) red_v4(g0, a0, a1, a2, a3);
-  if (has_b || merge) red_v4(g0 + 1, b0, b1, b2, b3);
-}
-
-// Host: fold n_img grouped images [n_img][os*of] (float4) into float64
-// num/den [os*of] (added to their contents).
-int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* num, double* den,
-                cudaStream_t s);
-// Number of grouped images for `blocks` frame blocks of frames_per_block
-// frames over n_cells cells; returns frame blocks per image.
-int64_t chunk_images(int64_t blocks, int64_t frames_per_block, int64_t n_cells, int* n_img);
-
 }  // namespace pxst

@@ -1,0 +1,717 @@
+// Deterministic splat pass shared by K1 (object formation, recon.py:99-141)
+// and K4 (error maps, recon.py:388-438): see fixsplat.cuh for the number
+// format.
+//
+// One CTA per 16 x 32 detector tile and frame slice (grid.z).  The CTA walks
+// its frames in batches of 8 and groups consecutive batches into "sessions"
+// whose joint object footprint (the tile's u bounding box shifted by each
+// frame's translation) fits a shared-memory region of RC cells and whose
+// term count per cell stays <= 2047 (bounded by the tile's largest number of
+// pixels reaching one cell in one frame, from a shared-memory histogram of
+// the tile's u).  A session zeroes the region, adds every sample's corner
+// terms with 32-bit shared atomics on (lo, hi) limbs, then adds the region's
+// nonzero cells to the global int64 accumulators (one RED.64 per cell and
+// value instead of two 16-byte REDs per sample and image).  A batch whose
+// footprint alone exceeds the region (a pathological map) adds its terms to
+// the global accumulators directly -- the same integers, so the same result.
+//
+// Modes: 0 = object splat (value I/W, weight W^2: recon.py:135-138);
+// 1 = error maps (masked bilinear read of the reference, eps = r^2/sigma^2,
+// per-pixel / per-frame sums, reference-plane splat of eps with weight 1,
+// recon.py:414-431); 2 = mode 1 fused with the next iteration's object
+// splat (same samples, positions relative to the next grid read from the
+// device, recon.py:504-516).
+#include "fixsplat.cuh"
+
+namespace pxst {
+namespace {
+
+constexpr int kXR = 16, kXC = 32, kXT = 256, kXW = kXT / 32;  // tile, threads, warps
+constexpr int kXB = 8;        // frames per batch
+constexpr int kXTab = 256;    // frames per shared frame-table chunk (multiple of kXB)
+
+template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 2048; };
+template <> struct FixCfg<2> { static constexpr int NV = 4, RC = 1536; };
+
+template <int MODE>
+constexpr size_t fix_smem_bytes() {
+  return sizeof(unsigned) * 2 * FixCfg<MODE>::NV * FixCfg<MODE>::RC + 2 * FixCfg<MODE>::RC;
+}
+
+}  // namespace
+
+struct FixArgs {
+  pxst_scan sc;
+  const double* u;
+  const double* di;
+  const double* dj;
+  int64_t n0, m0, os, of;      // primary grid: the object (mode 0) or the reference (1, 2)
+  int64_t k_lo, k_hi;          // good-frame range of the launch
+  int64_t frames_per_z;        // frames per grid.z slice (multiple of kXB)
+  FixAcc A;                    // mode 0: object; modes 1, 2: reference plane
+  FixAcc B;                    // mode 2: next object
+  const int64_t* grid_b;       // mode 2: device (n0, m0, os, of) of the next object
+  int64_t cap_b;               //   cells of B; a next grid larger than this is not splatted
+  const double2* grp;          // modes 1, 2: grouped float64 reference, NaN = invalid
+  const double* sigma2;
+  double* pix_part;            // [n_z][ss*fs] per-pixel eps sums of each slice
+  double* part;                // [n_good][n_cta] per-frame eps sums of each CTA
+  int64_t n_cta;
+  unsigned long long* n_drop;  // mode 0, nullable: out-of-grid samples
+};
+
+namespace {
+
+__device__ __forceinline__ int ifloor(double x) {
+  return static_cast<int>(fmax(fmin(floor(x), 1e9), -1e9));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
+  constexpr int NV = FixCfg<MODE>::NV, RC = FixCfg<MODE>::RC;
+  constexpr bool ERR = MODE != 0;
+  extern __shared__ __align__(16) unsigned char fx_raw[];
+  unsigned* slo = reinterpret_cast<unsigned*>(fx_raw);              // [NV][RC]
+  int* shi = reinterpret_cast<int*>(slo + NV * RC);                 // [NV][RC]
+  uint8_t* stc = reinterpret_cast<uint8_t*>(shi + NV * RC);         // [2][RC]
+  __shared__ double t_di[kXTab], t_dj[kXTab];
+  __shared__ int64_t t_off[kXTab];
+  __shared__ double s_red[kXW][4];
+  __shared__ double s_fr[kXW][kXB];
+  __shared__ int s_cmax;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t plane = a.sc.ss * a.sc.fs;
+  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
+  const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
+  const int of = static_cast<int>(a.of);
+
+  int64_t p[2];
+  bool live[2];
+  double u0[2], u1[2], Wv[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kXR + 2 * warp + e;
+    const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kXC + lane;
+    const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
+    p[e] = in ? row * a.sc.fs + col : 0;
+    live[e] = in && a.sc.work[p[e]] != 0;
+    u0[e] = live[e] ? a.u[p[e]] : 0.0;
+    u1[e] = live[e] ? a.u[plane + p[e]] : 0.0;
+    Wv[e] = live[e] ? a.sc.w64[p[e]] : 1.0;
+  }
+  // tile bounding box of u over its work pixels
+  double b0 = fmin(live[0] ? u0[0] : INFINITY, live[1] ? u0[1] : INFINITY);
+  double b1 = fmax(live[0] ? u0[0] : -INFINITY, live[1] ? u0[1] : -INFINITY);
+  double b2 = fmin(live[0] ? u1[0] : INFINITY, live[1] ? u1[1] : INFINITY);
+  double b3 = fmax(live[0] ? u1[0] : -INFINITY, live[1] ? u1[1] : -INFINITY);
+  b0 = warp_min(b0); b1 = warp_max(b1); b2 = warp_min(b2); b3 = warp_max(b3);
+  if (lane == 0) { s_red[warp][0] = b0; s_red[warp][1] = b1; s_red[warp][2] = b2; s_red[warp][3] = b3; }
+  __syncthreads();
+  double umin0 = s_red[0][0], umax0 = s_red[0][1], umin1 = s_red[0][2], umax1 = s_red[0][3];
+#pragma unroll
+  for (int w = 1; w < kXW; ++w) {
+    umin0 = fmin(umin0, s_red[w][0]); umax0 = fmax(umax0, s_red[w][1]);
+    umin1 = fmin(umin1, s_red[w][2]); umax1 = fmax(umax1, s_red[w][3]);
+  }
+  const int64_t k_begin = a.k_lo + (int64_t)blockIdx.z * a.frames_per_z;
+  const int64_t k_end = min(a.k_hi, k_begin + a.frames_per_z);
+  if (!(umin0 <= umax0)) {   // no work pixel: only the per-frame partials need writing
+    if (ERR)
+      for (int64_t k = k_begin + threadIdx.x; k < k_end; k += kXT) a.part[k * a.n_cta + cta] = 0.0;
+    return;
+  }
+
+  // Largest number of this tile's pixels whose corners reach one cell in one
+  // frame: a pixel in u-bin b reaches cells b - D + {-1, 0, 1} per axis
+  // (D = the frame's integer shift), so the max over 3 x 3 blocks of the
+  // tile's u-bin histogram bounds it.
+  if (threadIdx.x == 0) s_cmax = 0;
+  const bool fin = fabs(umin0) < 1e9 && fabs(umax0) < 1e9 && fabs(umin1) < 1e9 && fabs(umax1) < 1e9;
+  const int hb0 = fin ? ifloor(umin0) : 0, hb1 = fin ? ifloor(umin1) : 0;
+  const int hh = fin ? ifloor(umax0) - hb0 + 1 : 1 << 20, hw = fin ? ifloor(umax1) - hb1 + 1 : 1 << 20;
+  int cmax;
+  if (hh <= 2 * RC && hw <= 2 * RC && hh * hw <= NV * RC) {
+    for (int i = threadIdx.x; i < hh * hw; i += kXT) slo[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (live[e]) atomicAdd(&slo[(ifloor(u0[e]) - hb0) * hw + (ifloor(u1[e]) - hb1)], 1u);
+    __syncthreads();
+    int m = 0;
+    for (int i = threadIdx.x; i < hh * hw; i += kXT) {
+      const int r = i / hw, c = i % hw;
+      int s = 0;
+      for (int dr = -1; dr <= 1; ++dr)
+        for (int dc = -1; dc <= 1; ++dc) {
+          const int rr = r + dr, cc = c + dc;
+          if (rr >= 0 && rr < hh && cc >= 0 && cc < hw) s += static_cast<int>(slo[rr * hw + cc]);
+        }
+      m = max(m, s);
+    }
+    atomicMax(&s_cmax, m);
+    __syncthreads();
+    cmax = s_cmax;
+  } else {
+    cmax = 2 * kXT;   // every pixel of the tile
+  }
+  // frames per session: whole batches, <= 2047 terms per cell (a map whose
+  // bounding box is not finite takes the direct path throughout)
+  const int max_frames = cmax > 0 ? (kFixMaxTerms / cmax) / kXB * kXB : 1 << 30;
+
+  // accumulator scales
+  const double qa_n = 1.0 / a.A.q[0], qa_d = 1.0 / a.A.q[1];
+  double qb_n = 0.0, qb_d = 0.0;
+  int64_t dn = 0, dm = 0, osb = 1, ofb = 1;
+  bool splat_b = false;
+  if (MODE == 2) {
+    qb_n = 1.0 / a.B.q[0];
+    qb_d = 1.0 / a.B.q[1];
+    dn = a.n0 - a.grid_b[0];
+    dm = a.m0 - a.grid_b[1];
+    osb = a.grid_b[2];
+    ofb = a.grid_b[3];
+    splat_b = osb > 0 && ofb > 0 && osb * ofb <= a.cap_b;
+  }
+  const double osb1 = static_cast<double>(osb - 1), ofb1 = static_cast<double>(ofb - 1);
+  double W2[2], vsc[2], isig[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    W2[e] = Wv[e] * Wv[e];                                    // recon.py:136
+    vsc[e] = live[e] ? W2[e] / Wv[e] : 0.0;                   // (value = I / W) * W^2 per unit I
+    isig[e] = (ERR && live[e]) ? 1.0 / a.sigma2[p[e]] : 0.0;  // recon.py:422
+  }
+  double pix[2] = {0.0, 0.0};
+  unsigned long long dropped = 0;
+
+  for (int64_t kc = k_begin; kc < k_end; kc += kXTab) {
+    const int nt = static_cast<int>(min((int64_t)kXTab, k_end - kc));
+    __syncthreads();
+    for (int t = threadIdx.x; t < nt; t += kXT) {
+      const int64_t f = a.sc.good[kc + t];
+      t_di[t] = a.di[f];
+      t_dj[t] = a.dj[f];
+      t_off[t] = f * plane;
+    }
+    __syncthreads();
+    // footprint of the tile for frame t (primary-grid cells, the +1 row /
+    // column holds the r0 + 1 / c0 + 1 corners)
+    auto foot = [&](int t, int& r0, int& r1, int& c0, int& c1) {
+      r0 = ifloor(umin0 - t_di[t] - n0d);
+      r1 = ifloor(umax0 - t_di[t] - n0d) + 1;
+      c0 = ifloor(umin1 - t_dj[t] - m0d);
+      c1 = ifloor(umax1 - t_dj[t] - m0d) + 1;
+    };
+    for (int s0 = 0; s0 < nt;) {
+      int R0 = 1 << 30, R1 = -(1 << 30), C0 = 1 << 30, C1 = -(1 << 30);
+      auto add_batch = [&](int bb, int& r0, int& r1, int& c0, int& c1) {
+        const int nf = min(kXB, nt - bb);
+        for (int f = 0; f < nf; ++f) {
+          int x0, x1, y0, y1;
+          foot(bb + f, x0, x1, y0, y1);
+          r0 = min(r0, x0); r1 = max(r1, x1); c0 = min(c0, y0); c1 = max(c1, y1);
+        }
+        return nf;
+      };
+      int s1 = s0 + add_batch(s0, R0, R1, C0, C1);
+      const bool region = fin && max_frames > 0 &&
+                          (int64_t)(R1 - R0 + 1) * (C1 - C0 + 1) <= RC;
+      if (region) {
+        while (s1 < nt && s1 - s0 + kXB <= max_frames) {
+          int r0 = R0, r1 = R1, c0 = C0, c1 = C1;
+          const int nf = add_batch(s1, r0, r1, c0, c1);
+          if ((int64_t)(r1 - r0 + 1) * (c1 - c0 + 1) > RC) break;
+          R0 = r0; R1 = r1; C0 = c0; C1 = c1;
+          s1 += nf;
+        }
+      }
+      const int nc = region ? C1 - C0 + 1 : 0;
+      const int ncell = region ? (R1 - R0 + 1) * nc : 0;
+      if (region) {
+        for (int i = threadIdx.x; i < ncell; i += kXT) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            slo[v * RC + i] = 0u;
+            shi[v * RC + i] = 0;
+          }
+          stc[i] = 0;
+          stc[RC + i] = 0;
+        }
+        __syncthreads();
+      }
+      // ---- the session's samples, batch by batch
+      for (int bb = s0; bb < s1; bb += kXB) {
+        const int nf = min(kXB, s1 - bb);
+        float Iv[kXB][2];
+#pragma unroll
+        for (int f = 0; f < kXB; ++f)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            Iv[f][e] = (live[e] && f < nf) ? __ldg(a.sc.frames + t_off[bb + f] + p[e]) : 0.f;
+        double ef[kXB];
+#pragma unroll
+        for (int f = 0; f < kXB; ++f) {
+          ef[f] = 0.0;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool act = live[e] && f < nf;
+            const int t = bb + (f < nf ? f : 0);
+            const double x = act ? u0[e] - t_di[t] - n0d : 0.0;      // recon.py:138, 418
+            const double y = act ? u1[e] - t_dj[t] - m0d : 0.0;
+            const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
+            const double xf = floor(x), yf = floor(y);
+            const double fx = x - xf, fy = y - yf;
+            const int r0 = static_cast<int>(xf), c0 = static_cast<int>(yf);
+            const double gx = 1.0 - fx, gy = 1.0 - fy;
+            const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
+            const bool cok[4] = {true, fy > 0.0, fx > 0.0, fx > 0.0 && fy > 0.0};
+            const double I = static_cast<double>(Iv[f][e]);
+            double sAn, sAd;
+            if (ERR) {
+              double eps = 0.0;
+              if (act) {
+                // masked bilinear read (interp.py:53-85) of the grouped reference:
+                // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
+                const double2 z2 = make_double2(0.0, 0.0);
+                const int64_t a00 = (int64_t)r0 * a.of + c0;
+                const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
+                const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
+                const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
+                double den = 0.0, nm = 0.0;
+                bool all = true;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const bool m = cv[q] == cv[q];
+                  all = all && m;
+                  den = fma(cw[q], m ? 1.0 : 0.0, den);
+                  nm = fma(cw[q], m ? cv[q] : 0.0, nm);
+                }
+                const bool ok = inA && den > 0.0;
+                const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
+                const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
+                eps = (r * r) * isig[e];                                // recon.py:422
+              }
+              pix[e] += eps;
+              ef[f] += eps;
+              sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
+              sAd = qa_d;
+            } else {
+              dropped += (act && !inA) ? 1 : 0;
+              sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
+              sAd = W2[e] * qa_d;
+            }
+            bool inB = false;
+            double sBn = 0.0, sBd = 0.0;
+            if (MODE == 2) {
+              const double xb = x + static_cast<double>(dn), yb = y + static_cast<double>(dm);
+              inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
+              sBn = I * vsc[e] * qb_n;
+              sBd = W2[e] * qb_d;
+            }
+            const int dl[4] = {0, 1, nc, nc + 1};
+            const int dc_[4] = {0, 1, 0, 1}, dr_[4] = {0, 0, 1, 1};
+            const int l = (r0 - R0) * nc + (c0 - C0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const bool okA = inA && cok[q];
+              const bool okB = inB && cok[q];
+              if (!okA && !okB) continue;
+              unsigned lo;
+              int hi;
+              if (region) {
+                const int li = l + dl[q];
+                if (okA) {
+                  fix_limbs(sAn, cw[q], lo, hi);
+                  atomicAdd(&slo[li], lo);
+                  atomicAdd(&shi[li], hi);
+                  fix_limbs(sAd, cw[q], lo, hi);
+                  atomicAdd(&slo[RC + li], lo);
+                  atomicAdd(&shi[RC + li], hi);
+                  if (!ERR) stc[li] = 1;
+                }
+                if (MODE == 2 && okB) {
+                  fix_limbs(sBn, cw[q], lo, hi);
+                  atomicAdd(&slo[2 * RC + li], lo);
+                  atomicAdd(&shi[2 * RC + li], hi);
+                  fix_limbs(sBd, cw[q], lo, hi);
+                  atomicAdd(&slo[3 * RC + li], lo);
+                  atomicAdd(&shi[3 * RC + li], hi);
+                  stc[RC + li] = 1;
+                }
+              } else {     // direct: the same integers straight into the int64 images
+                if (okA) {
+                  const int64_t cell = (int64_t)(r0 + dr_[q]) * a.of + (c0 + dc_[q]);
+                  atomicAdd(reinterpret_cast<unsigned long long*>(a.A.num + cell),
+                            static_cast<unsigned long long>(fix_value(sAn, cw[q])));
+                  atomicAdd(reinterpret_cast<unsigned long long*>(a.A.den + cell),
+                            static_cast<unsigned long long>(fix_value(sAd, cw[q])));
+                  if (!ERR && a.A.touched) a.A.touched[cell] = 1;
+                }
+                if (MODE == 2 && okB) {
+                  const int64_t cell = (int64_t)(r0 + dr_[q] + dn) * ofb + (c0 + dc_[q] + dm);
+                  atomicAdd(reinterpret_cast<unsigned long long*>(a.B.num + cell),
+                            static_cast<unsigned long long>(fix_value(sBn, cw[q])));
+                  atomicAdd(reinterpret_cast<unsigned long long*>(a.B.den + cell),
+                            static_cast<unsigned long long>(fix_value(sBd, cw[q])));
+                  if (a.B.touched) a.B.touched[cell] = 1;
+                }
+              }
+            }
+          }
+        }
+        if (ERR) {   // per-frame sums: warp, then the CTA's warps in a fixed order
+#pragma unroll
+          for (int f = 0; f < kXB; ++f) {
+            const double sum = warp_sum(ef[f]);
+            if (lane == 0) s_fr[warp][f] = sum;
+          }
+          __syncthreads();
+          if (threadIdx.x < nf) {
+            double sum = 0.0;
+#pragma unroll
+            for (int w = 0; w < kXW; ++w) sum += s_fr[w][threadIdx.x];
+            a.part[(kc + bb + threadIdx.x) * a.n_cta + cta] = sum;
+          }
+          __syncthreads();
+        }
+      }
+      // ---- flush the region into the int64 images
+      if (region) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < ncell; i += kXT) {
+          const int r = R0 + i / nc, c = C0 + i % nc;
+          const long long vn = fix_join(slo[i], shi[i]);
+          const long long vd = fix_join(slo[RC + i], shi[RC + i]);
+          if (vn != 0 || vd != 0 || (!ERR && stc[i])) {
+            const int64_t cell = (int64_t)r * of + c;
+            if (vn) atomicAdd(reinterpret_cast<unsigned long long*>(a.A.num + cell),
+                              static_cast<unsigned long long>(vn));
+            if (vd) atomicAdd(reinterpret_cast<unsigned long long*>(a.A.den + cell),
+                              static_cast<unsigned long long>(vd));
+            if (!ERR && stc[i] && a.A.touched) a.A.touched[cell] = 1;
+          }
+          if (MODE == 2) {
+            const long long wn = fix_join(slo[2 * RC + i], shi[2 * RC + i]);
+            const long long wd = fix_join(slo[3 * RC + i], shi[3 * RC + i]);
+            if (wn != 0 || wd != 0 || stc[RC + i]) {
+              const int64_t cell = (int64_t)(r + dn) * ofb + (c + dm);
+              if (wn) atomicAdd(reinterpret_cast<unsigned long long*>(a.B.num + cell),
+                                static_cast<unsigned long long>(wn));
+              if (wd) atomicAdd(reinterpret_cast<unsigned long long*>(a.B.den + cell),
+                                static_cast<unsigned long long>(wd));
+              if (stc[RC + i] && a.B.touched) a.B.touched[cell] = 1;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      s0 = s1;
+    }
+  }
+  if (ERR) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (live[e]) a.pix_part[(int64_t)blockIdx.z * plane + p[e]] = pix[e];
+  }
+  if (!ERR && a.n_drop) {
+    dropped += __shfl_xor_sync(0xffffffffu, dropped, 16);
+    dropped += __shfl_xor_sync(0xffffffffu, dropped, 8);
+    dropped += __shfl_xor_sync(0xffffffffu, dropped, 4);
+    dropped += __shfl_xor_sync(0xffffffffu, dropped, 2);
+    dropped += __shfl_xor_sync(0xffffffffu, dropped, 1);
+    if (lane == 0 && dropped) atomicAdd(a.n_drop, dropped);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scales
+// ---------------------------------------------------------------------------
+// Order-independent max of non-negative doubles (their bit patterns order
+// like the values).
+__device__ __forceinline__ void atomic_max_nonneg(double* p, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(p),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+__device__ __forceinline__ void atomic_min_nonneg(double* p, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(p),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// max |I| over the whole stack (a bound for every sample of every frame set)
+__global__ void k_abs_max(const float* __restrict__ frames, int64_t n, double* out) {
+  float m = 0.f;
+  const int64_t n4 = n / 4;
+  const float4* f4 = reinterpret_cast<const float4*>(frames);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(f4 + i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(__ldg(frames + i)));
+  // NaN / inf samples: an infinite bound (quantum 2^-41 of 1, see fix_quantum)
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, static_cast<double>(m));
+}
+
+// scratch[0] = max W over the work pixels of the ROI, scratch[1] = min
+// sigma2 over them (nullable sigma2), scratch[2] = max |reference| over its
+// valid cells (nullable reference).
+__global__ void k_scale_stats(pxst_scan sc, const double* __restrict__ sigma2,
+                              const double* __restrict__ fm64, const float* __restrict__ fm,
+                              const uint8_t* __restrict__ valid, int64_t n_ref, double* scratch) {
+  const int64_t cw = sc.roi[3] - sc.roi[2], n = (sc.roi[1] - sc.roi[0]) * cw;
+  double wmax = 0.0, smin = INFINITY, rmax = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = (sc.roi[0] + q / cw) * sc.fs + sc.roi[2] + q % cw;
+    if (!sc.work[p]) continue;
+    wmax = fmax(wmax, fabs(sc.w64[p]));
+    if (sigma2) smin = fmin(smin, sigma2[p]);
+  }
+  if (valid)
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_ref;
+         q += (int64_t)gridDim.x * blockDim.x)
+      if (valid[q]) rmax = fmax(rmax, fabs(fm64 ? fm64[q] : static_cast<double>(fm[q])));
+  wmax = warp_max(wmax);
+  smin = warp_min(smin);
+  rmax = warp_max(rmax);
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_nonneg(scratch, wmax);
+    if (sigma2) atomic_min_nonneg(scratch + 1, smin);
+    atomic_max_nonneg(scratch + 2, rmax);
+  }
+}
+
+__global__ void k_scale_init(double* d) {
+  if (threadIdx.x == 0) {
+    d[0] = 0.0;
+    d[1] = INFINITY;
+    d[2] = 0.0;
+  }
+}
+
+// kind 0 (object): q_num from max |I| max W, q_den from max W^2.
+// kind 1 (reference plane): q_num from the eps bound
+// (max|I| + max W max(1, max|ref|))^2 / min sigma2, q_den from 1.
+__global__ void k_quanta(const double* __restrict__ absmax, const double* __restrict__ scratch,
+                         int kind, int k, double* quanta) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double amax = *absmax, wmax = scratch[0];
+  if (kind == 0) {
+    quanta[0] = fix_quantum(amax * wmax, k);
+    quanta[1] = fix_quantum(wmax * wmax, k);
+  } else {
+    const double r = amax + wmax * fmax(1.0, scratch[2]);
+    const double s = scratch[1] > 0.0 && isfinite(scratch[1]) ? scratch[1] : 1.0;
+    quanta[0] = fix_quantum(r * r / s, k);
+    quanta[1] = fix_quantum(1.0, k);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finish
+// ---------------------------------------------------------------------------
+// Normalise (interp.py:126-135): out = num/den where den > 0 else 0.  The
+// object's validity is "a positive-weight term landed" (touched); a cell
+// whose whole weight rounds below one quantum (< 2^-42 of the largest
+// possible term) keeps that validity with value 0 and wsum = q/2^32.
+__global__ void k_fix_finish(const long long* __restrict__ num, const long long* __restrict__ den,
+                             const uint8_t* __restrict__ touched, const double* __restrict__ q,
+                             const int64_t* __restrict__ grid, int64_t n, double* out,
+                             double* wsum, float* fm, uint8_t* valid) {
+  if (grid) {
+    const int64_t gn = grid[2] * grid[3];
+    if (!(grid[2] > 0 && grid[3] > 0)) return;
+    n = gn < n ? gn : n;
+  }
+  const double qn = q[0], qd = q[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const long long d = den[i];
+    const bool pos = d > 0;
+    const bool ok = touched ? (touched[i] != 0) : pos;
+    const double dd = static_cast<double>(d) * qd;
+    const double v = pos ? (static_cast<double>(num[i]) * qn) / dd : 0.0;
+    if (out) out[i] = v;
+    if (wsum) wsum[i] = pos ? dd : (ok ? qd * 0x1p-32 : 0.0);
+    if (fm) fm[i] = ok ? static_cast<float>(v) : 0.f;
+    if (valid) valid[i] = ok ? 1 : 0;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+int check_scan(const pxst_scan* sc);
+
+int launch_abs_max(const pxst_scan* sc, double* out, cudaStream_t s) {
+  PXST_CHECK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+  const int64_t n = sc->n_frames * sc->ss * sc->fs;
+  if (n <= 0) return PXST_OK;
+  k_abs_max<<<148 * 8, 256, 0, s>>>(sc->frames, n, out);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma2,
+                  const pxst_ref* ref, int kind, double* quanta, cudaStream_t s) {
+  Scratch sc3;
+  if (int e = sc3.alloc(3 * sizeof(double), s)) return e;
+  double* d = sc3.as<double>();
+  k_scale_init<<<1, 32, 0, s>>>(d);     // (0, +inf, 0): max W, min sigma2, max |ref|
+  PXST_CHECK_LAUNCH();
+  const int64_t n_ref = ref ? ref->os * ref->of : 0;
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  k_scale_stats<<<grid_1d(std::max(rw * cw, n_ref), 256), 256, 0, s>>>(
+      *sc, kind == 1 ? sigma2 : nullptr, ref ? ref->fm64 : nullptr, ref ? ref->fm : nullptr,
+      ref ? ref->valid : nullptr, n_ref, d);
+  PXST_CHECK_LAUNCH();
+  k_quanta<<<1, 32, 0, s>>>(absmax, d, kind, fix_headroom(sc->n_good), quanta);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+template <int MODE>
+int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
+  const int64_t cw = a.sc.roi[3] - a.sc.roi[2], rw = a.sc.roi[1] - a.sc.roi[0];
+  dim3 g((unsigned)((cw + kXC - 1) / kXC), (unsigned)((rw + kXR - 1) / kXR));
+  PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
+  a.n_cta = (int64_t)g.x * g.y;
+  const int64_t nk = a.k_hi - a.k_lo;
+  constexpr size_t smem = fix_smem_bytes<MODE>();
+  PXST_CHECK_CUDA(cudaFuncSetAttribute(k_fix_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+  // frame slices (grid.z): ~3 waves of resident CTAs when the ROI alone
+  // cannot fill the GPU
+  int dev = 0, sms = 148, per_sm = 1;
+  PXST_CHECK_CUDA(cudaGetDevice(&dev));
+  PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  PXST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<MODE>, kXT,
+                                                                smem));
+  const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t n_batches = (nk + kXB - 1) / kXB;
+  int64_t n_z = (3 * resident + a.n_cta - 1) / a.n_cta;
+  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
+  n_z = n_z < 1 ? 1 : n_z;
+  a.frames_per_z = ((n_batches + n_z - 1) / n_z) * kXB;
+  if (a.frames_per_z < kXB) a.frames_per_z = kXB;
+  n_z = (nk + a.frames_per_z - 1) / a.frames_per_z;
+  if (n_z < 1) n_z = 1;
+  g.z = static_cast<unsigned>(n_z);
+  if (n_z_out) *n_z_out = static_cast<int>(n_z);
+  if (nk <= 0) return PXST_OK;
+  k_fix_pass<MODE><<<g, kXT, smem, s>>>(a);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+// slices the launch would use (the caller sizes pix_part with it)
+int fix_pass_slices(const pxst_scan* sc, int64_t nk, int mode, int64_t* n_cta) {
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  const int64_t ctas = ((cw + kXC - 1) / kXC) * ((rw + kXR - 1) / kXR);
+  if (n_cta) *n_cta = ctas;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = mode == 2 ? fix_smem_bytes<2>() : fix_smem_bytes<0>();
+  if (mode == 2) {
+    cudaFuncSetAttribute(k_fix_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<2>, kXT, smem);
+  } else if (mode == 1) {
+    cudaFuncSetAttribute(k_fix_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<1>, kXT, smem);
+  } else {
+    cudaFuncSetAttribute(k_fix_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<0>, kXT, smem);
+  }
+  const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  const int64_t n_batches = (nk + kXB - 1) / kXB;
+  int64_t n_z = (3 * resident + ctas - 1) / ctas;
+  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
+  n_z = n_z < 1 ? 1 : n_z;
+  int64_t fpz = ((n_batches + n_z - 1) / n_z) * kXB;
+  if (fpz < kXB) fpz = kXB;
+  n_z = (nk + fpz - 1) / fpz;
+  return static_cast<int>(n_z < 1 ? 1 : n_z);
+}
+
+template int launch_fix_pass<0>(FixArgs&, int*, cudaStream_t);
+template int launch_fix_pass<1>(FixArgs&, int*, cudaStream_t);
+template int launch_fix_pass<2>(FixArgs&, int*, cudaStream_t);
+
+int launch_fix_finish(const FixAcc& acc, const int64_t* grid, int64_t n, double* out, double* wsum,
+                      float* fm, uint8_t* valid, cudaStream_t s) {
+  if (n <= 0) return PXST_OK;
+  k_fix_finish<<<grid_1d(n, 256), 256, 0, s>>>(acc.num, acc.den, acc.touched, acc.q, grid, n, out,
+                                               wsum, fm, valid);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
+}  // namespace pxst
+
+namespace pxst {
+
+int launch_object_fix(const pxst_scan* sc, const double* u, const double* di, const double* dj,
+                      int64_t n0, int64_t m0, int64_t os, int64_t of, int64_t frame_lo,
+                      int64_t frame_hi, const FixAcc& acc, unsigned long long* n_drop,
+                      cudaStream_t s) {
+  FixArgs a{};
+  a.sc = *sc;
+  a.u = u;
+  a.di = di;
+  a.dj = dj;
+  a.n0 = n0;
+  a.m0 = m0;
+  a.os = os;
+  a.of = of;
+  a.k_lo = frame_lo;
+  a.k_hi = frame_hi;
+  a.A = acc;
+  a.n_drop = n_drop;
+  return launch_fix_pass<0>(a, nullptr, s);
+}
+
+}  // namespace pxst
+
+namespace pxst {
+
+int launch_error_fix(const pxst_scan* sc, const pxst_ref* ref, const double* u, const double* di,
+                     const double* dj, const double* sigma2, const double2* grp, const FixAcc& plane,
+                     const FixAcc* next, const int64_t* grid_b, int64_t cap_b, double* pix_part,
+                     double* part, int* n_z, int64_t* n_cta, cudaStream_t s) {
+  FixArgs a{};
+  a.sc = *sc;
+  a.u = u;
+  a.di = di;
+  a.dj = dj;
+  a.n0 = ref->n0;
+  a.m0 = ref->m0;
+  a.os = ref->os;
+  a.of = ref->of;
+  a.k_lo = 0;
+  a.k_hi = sc->n_good;
+  a.A = plane;
+  a.grp = grp;
+  a.sigma2 = sigma2;
+  a.pix_part = pix_part;
+  a.part = part;
+  int e;
+  if (next) {
+    a.B = *next;
+    a.grid_b = grid_b;
+    a.cap_b = cap_b;
+    e = launch_fix_pass<2>(a, n_z, s);
+  } else {
+    e = launch_fix_pass<1>(a, n_z, s);
+  }
+  if (n_cta) *n_cta = a.n_cta;
+  return e;
+}
+
+}  // namespace pxst

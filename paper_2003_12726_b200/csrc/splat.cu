@@ -2,132 +2,29 @@
 // (interp.py:53-135).
 //
 // The reference accumulates the bilinear splat in float64 with np.bincount
-// (interp.py:114-122).  The splat is bound by the L2 atomic units, so here a
-// sample's four corners go out as two 16-byte float32 REDs (splat_grouped:
-// 2 RED lane-ops per sample instead of 8 float64 ones) into at most 32
-// float32 images, each covering a contiguous range of >= 24 frames (and
-// <= N/32 frames for long stacks); a fixed-order float64 fold sums the
-// images.  An image sums positive terms of a few dozen frames, so its
-// relative error stays ~1e-7-1e-6 (the 1e-5 bar of SURVEY 8(c)); the
-// summation order inside an image varies run to run.
-#include "common.cuh"
+// (interp.py:114-122).  Here the splat runs through the deterministic
+// fixed-point pass of fixsplat.cu (mode 0): every term I/W * W^2 * w_c and
+// W^2 * w_c is rounded once to a power-of-two quantum and summed exactly in
+// int64, so the object map is bit-identical from run to run, for any frame
+// split and any number of GPUs (the int64 images of frame shards add
+// exactly).
+#include "fixsplat.cuh"
 
 namespace pxst {
+
+struct FixArgs;
+template <int MODE> int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s);
+int launch_abs_max(const pxst_scan* sc, double* out, cudaStream_t s);
+int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma2,
+                  const pxst_ref* ref, int kind, double* quanta, cudaStream_t s);
+int launch_fix_finish(const FixAcc& acc, const int64_t* grid, int64_t n, double* out, double* wsum,
+                      float* fm, uint8_t* valid, cudaStream_t s);
+int launch_object_fix(const pxst_scan* sc, const double* u, const double* di, const double* dj,
+                      int64_t n0, int64_t m0, int64_t os, int64_t of, int64_t frame_lo,
+                      int64_t frame_hi, const FixAcc& acc, unsigned long long* n_drop,
+                      cudaStream_t s);
+
 namespace {
-
-constexpr int kTR = 4, kTC = 32, kThreads = kTR * kTC;  // 4 rows x 32 fs pixels
-constexpr int kFB = 8;                 // frames per load batch (loads before REDs)
-constexpr int kTab = 256;              // frames per shared-memory frame table chunk
-constexpr int64_t kMaxImages = 32;     // float32 chunk images per splat
-constexpr int64_t kMinImageFrames = 24;  // frames summed per image, at least
-constexpr int64_t kImageBytes = int64_t(1) << 30;
-#ifndef PXST_K1_OCC
-#define PXST_K1_OCC 8
-#endif
-
-// One thread per work pixel over the frame slice blockIdx.z.  Lanes of a
-// warp are consecutive fs pixels, so the corner REDs of a warp land on a few
-// consecutive cells (the cheap, row-coalesced atomic pattern).  Each sample
-// issues two 16-byte float32 REDs (splat_grouped) into the chunk image of
-// its frame batch; a batch's frame loads are all issued before its REDs.
-__global__ void __launch_bounds__(kThreads, PXST_K1_OCC)
-k_object_splat(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
-               const double* __restrict__ dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-               int64_t frame_lo, int64_t frame_hi, int64_t frames_per_z, float4* __restrict__ img,
-               int bpi, unsigned long long* __restrict__ n_drop) {
-  __shared__ double t_di[kTab], t_dj[kTab];
-  __shared__ int64_t t_off[kTab];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t r = sc.roi[0] + (int64_t)blockIdx.y * kTR + warp;
-  const int64_t c = sc.roi[2] + (int64_t)blockIdx.x * kTC + lane;
-  const bool inroi = r < sc.roi[1] && c < sc.roi[3];
-  const int64_t p = inroi ? r * sc.fs + c : 0;
-  const bool live = inroi && sc.work[p] != 0;
-  const int64_t plane = sc.ss * sc.fs;
-  const double u0 = live ? u[p] : 0.0, u1 = live ? u[plane + p] : 0.0;
-  const double w = live ? sc.w64[p] : 1.0;
-  const double w2 = w * w;                       // recon.py:136
-  const double inv_w = 1.0 / w;                  // value = I / W (interp.py:112), <= 1 ulp
-  const double os1 = static_cast<double>(os - 1), of1 = static_cast<double>(of - 1);
-  const int64_t n_o = os * of;
-  const int64_t k_begin = frame_lo + (int64_t)blockIdx.z * frames_per_z;
-  const int64_t k_end = min(frame_hi, k_begin + frames_per_z);
-  unsigned long long dropped = 0;
-  for (int64_t kc = k_begin; kc < k_end; kc += kTab) {
-    const int nt = static_cast<int>(k_end - kc < kTab ? k_end - kc : kTab);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nt; t += kThreads) {
-      const int64_t f = sc.good[kc + t];
-      t_di[t] = di[f];
-      t_dj[t] = dj[f];
-      t_off[t] = f * plane;
-    }
-    __syncthreads();
-    // every lane runs the loop (the splat is warp-cooperative); lanes
-    // without a work pixel splat nothing
-    for (int b0 = 0; b0 < nt; b0 += kFB) {
-      float4* out = img + ((kc - frame_lo + b0) / kFB / bpi) * n_o;
-      float Iv[kFB];
-#pragma unroll
-      for (int b = 0; b < kFB; ++b)
-        Iv[b] = (live && b0 + b < nt) ? __ldg(sc.frames + t_off[b0 + b] + p) : 0.f;
-#pragma unroll
-      for (int b = 0; b < kFB; ++b) {
-        if (b0 + b >= nt) break;
-        const double x = u0 - t_di[b0 + b] - static_cast<double>(n0);   // recon.py:138
-        const double y = u1 - t_dj[b0 + b] - static_cast<double>(m0);
-        const bool in = x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;   // interp.py:103-107
-        dropped += (live && !in) ? 1 : 0;
-        const bool act = live && in;
-        const Split sx = split(act ? x : 0.0), sy = split(act ? y : 0.0);
-        const double vw = (static_cast<double>(Iv[b]) * inv_w) * w2;   // value*weight (interp.py:112)
-        splat_grouped_warp(out, (int64_t)sx.i * of + sy.i, sx.f, sy.f, vw, w2, act);
-      }
-    }
-  }
-  if (n_drop && dropped) atomicAdd(n_drop, dropped);
-}
-
-// Fold grouped float32 chunk images into float64 (num, den), fixed order:
-// cell (r, c) = sum_z g_z(r, c).lo + g_z(r-1, c).hi.
-__global__ void k_group_fold(const float4* __restrict__ img, int n_img, int64_t os, int64_t of,
-                             double* __restrict__ num, double* __restrict__ den) {
-  const int64_t n = os * of;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    double a = 0.0, b = 0.0;
-    const bool up = q >= of;
-    for (int z = 0; z < n_img; ++z) {
-      const float4 g = __ldg(img + (int64_t)z * n + q);
-      a += g.x;
-      b += g.y;
-      if (up) {
-        const float4 h = __ldg(img + (int64_t)z * n + q - of);
-        a += h.z;
-        b += h.w;
-      }
-    }
-    num[q] += a;
-    den[q] += b;
-  }
-}
-
-// Normalise (interp.py:126-135): i_ref = num/den where den > 0 else 0.
-__global__ void k_object_finish(const double* __restrict__ num, const double* __restrict__ den,
-                                int64_t n, double* i_ref, double* wsum, float* fm,
-                                uint8_t* valid) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const double vv = num[q];
-    const double ww = den[q];
-    const bool ok = ww > 0.0;
-    const double out = ok ? vv / ww : 0.0;
-    if (i_ref) i_ref[q] = out;
-    if (wsum) wsum[q] = ww;
-    if (fm) fm[q] = static_cast<float>(out);
-    if (valid) valid[q] = ok ? 1 : 0;
-  }
-}
 
 __global__ void k_gather(pxst_ref ref, const double* __restrict__ x, const double* __restrict__ y,
                          int64_t n, double* vals, uint8_t* ok) {
@@ -181,89 +78,53 @@ __global__ void k_splat_f64(double* acc_v, double* acc_w, int64_t os, int64_t of
 
 int check_scan(const pxst_scan* sc);
 
-int64_t chunk_images(int64_t blocks, int64_t frames_per_block, int64_t n_cells, int* n_img) {
-  // An image sums >= kMinImageFrames frames (fewer images: less zeroing and
-  // folding traffic) and, for long stacks, <= blocks / kMaxImages blocks;
-  // the scratch stays <= kImageBytes.
-  int64_t cap = kImageBytes / (static_cast<int64_t>(sizeof(float4)) * (n_cells > 0 ? n_cells : 1));
-  if (cap > kMaxImages) cap = kMaxImages;
-  if (cap < 1) cap = 1;
-  int64_t bpi = (blocks + cap - 1) / cap;
-  const int64_t min_bpi = (kMinImageFrames + frames_per_block - 1) / frames_per_block;
-  if (bpi < min_bpi) bpi = min_bpi;
-  *n_img = static_cast<int>((blocks + bpi - 1) / bpi);
-  return bpi;
-}
-
-int fold_groups(const float4* img, int n_img, int64_t os, int64_t of, double* num, double* den,
-                cudaStream_t s) {
-  k_group_fold<<<grid_1d(os * of, 256), 256, 0, s>>>(img, n_img, os, of, num, den);
-  PXST_CHECK_LAUNCH();
-  return PXST_OK;
-}
-
-int launch_object_splat(const pxst_scan* sc, const double* u, const double* di,
-                        const double* dj, int64_t n0, int64_t m0, int64_t os, int64_t of,
-                        int64_t frame_lo, int64_t frame_hi, double* num, double* den,
-                        unsigned long long* n_drop, cudaStream_t s) {
-  const int64_t nk = frame_hi - frame_lo;
-  if (nk <= 0) return PXST_OK;
-  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
-  dim3 g((unsigned)((cw + kTC - 1) / kTC), (unsigned)((rw + kTR - 1) / kTR));
-  PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
-  // Frame slices (grid.z) so the launch holds ~3 waves of resident CTAs.
-  int dev = 0, sms = 148, per_sm = 1;
-  PXST_CHECK_CUDA(cudaGetDevice(&dev));
-  PXST_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  PXST_CHECK_CUDA(
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_object_splat, kThreads, 0));
-  const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  const int64_t n_batches = (nk + kFB - 1) / kFB;
-  int64_t n_z = (3 * resident + (int64_t)g.x * g.y - 1) / ((int64_t)g.x * g.y);
-  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
-  const int64_t fpz = ((n_batches + n_z - 1) / n_z) * kFB;
-  g.z = static_cast<unsigned>((nk + fpz - 1) / fpz);
-  const int64_t n = os * of;
-  int n_img;
-  const int64_t bpi = chunk_images(n_batches, kFB, n, &n_img);
-  Scratch acc;
-  if (int e = acc.alloc(sizeof(float4) * n * n_img, s)) return e;
-  PXST_CHECK_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(float4) * n * n_img, s));
-  k_object_splat<<<g, kThreads, 0, s>>>(*sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, fpz,
-                                        acc.as<float4>(), (int)bpi, n_drop);
-  PXST_CHECK_LAUNCH();
-  return fold_groups(acc.as<float4>(), n_img, os, of, num, den, s);
-}
-
-int launch_object_finish(const double* num, const double* den, int64_t n, double* i_ref,
-                         double* wsum, float* fm, uint8_t* valid, cudaStream_t s) {
-  k_object_finish<<<grid_1d(n, 256), 256, 0, s>>>(num, den, n, i_ref, wsum, fm, valid);
-  PXST_CHECK_LAUNCH();
-  return PXST_OK;
-}
-
 }  // namespace pxst
 
 using namespace pxst;
 
+static int check_accum(const pxst_accum* acc) {
+  PXST_REQUIRE(acc && acc->num && acc->den && acc->quanta, "bad accumulator");
+  return PXST_OK;
+}
+
+static FixAcc fix_acc(const pxst_accum* acc) {
+  return FixAcc{reinterpret_cast<long long*>(acc->num), reinterpret_cast<long long*>(acc->den),
+                acc->touched, acc->quanta};
+}
+
+extern "C" int pxst_stack_absmax(const pxst_scan* sc, double* out, void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(out, "NULL pointer");
+  return launch_abs_max(sc, out, as_stream(stream));
+}
+
+extern "C" int pxst_object_quanta(const pxst_scan* sc, const double* absmax, double* quanta,
+                                  void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(absmax && quanta, "NULL pointer");
+  return launch_quanta(sc, absmax, nullptr, nullptr, 0, quanta, as_stream(stream));
+}
+
 extern "C" int pxst_object_splat(const pxst_scan* sc, const double* u, const double* di,
                                  const double* dj, int64_t n0, int64_t m0, int64_t os,
-                                 int64_t of, int64_t frame_lo, int64_t frame_hi, double* num,
-                                 double* den, unsigned long long* n_dropped, void* stream) {
+                                 int64_t of, int64_t frame_lo, int64_t frame_hi,
+                                 const pxst_accum* acc, unsigned long long* n_dropped,
+                                 void* stream) {
   if (int e = check_scan(sc)) return e;
-  PXST_REQUIRE(u && di && dj && num && den, "NULL pointer");
+  if (int e = check_accum(acc)) return e;
+  PXST_REQUIRE(u && di && dj, "NULL pointer");
   PXST_REQUIRE(os > 0 && of > 0 && os * of < (int64_t(1) << 40), "bad grid shape");
   PXST_REQUIRE(0 <= frame_lo && frame_lo <= frame_hi && frame_hi <= sc->n_good,
                "bad frame range");
-  return launch_object_splat(sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, num, den,
-                             n_dropped, as_stream(stream));
+  return launch_object_fix(sc, u, di, dj, n0, m0, os, of, frame_lo, frame_hi, fix_acc(acc),
+                           n_dropped, as_stream(stream));
 }
 
-extern "C" int pxst_object_finish(const double* num, const double* den, int64_t n,
-                                  double* i_ref, double* wsum, float* fm, uint8_t* valid,
-                                  void* stream) {
-  PXST_REQUIRE(num && den && n > 0, "bad accumulators");
-  return launch_object_finish(num, den, n, i_ref, wsum, fm, valid, as_stream(stream));
+extern "C" int pxst_object_finish(const pxst_accum* acc, int64_t n, double* i_ref, double* wsum,
+                                  float* fm, uint8_t* valid, void* stream) {
+  if (int e = check_accum(acc)) return e;
+  PXST_REQUIRE(n > 0, "bad accumulator size");
+  return launch_fix_finish(fix_acc(acc), nullptr, n, i_ref, wsum, fm, valid, as_stream(stream));
 }
 
 extern "C" int pxst_object_map(const pxst_scan* sc, const double* u,
@@ -271,17 +132,25 @@ extern "C" int pxst_object_map(const pxst_scan* sc, const double* u,
                                int64_t os, int64_t of, double* i_ref, double* wsum, float* fm,
                                uint8_t* valid, void* stream) {
   if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(u && di && dj, "NULL pointer");
   PXST_REQUIRE(os > 0 && of > 0 && os * of < (int64_t(1) << 40), "bad grid shape");
   cudaStream_t s = as_stream(stream);
   const int64_t n = os * of;
-  Scratch acc;
-  if (int e = acc.alloc(sizeof(double) * 2 * n, s)) return e;
-  double* num = acc.as<double>();
-  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(double) * 2 * n, s));
-  if (int e = launch_object_splat(sc, u, di, dj, n0, m0, os, of, 0, sc->n_good, num, num + n,
-                                  nullptr, s))
+  Scratch buf;
+  if (int e = buf.alloc(sizeof(int64_t) * 2 * n + n + 4 * sizeof(double) + 16, s)) return e;
+  int64_t* num = buf.as<int64_t>();
+  double* q = reinterpret_cast<double*>(num + 2 * n);
+  double* amax = q + 2;
+  uint8_t* touched = reinterpret_cast<uint8_t*>(q + 4);
+  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 2 * n, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(touched, 0, n, s));
+  if (int e = launch_abs_max(sc, amax, s)) return e;
+  if (int e = launch_quanta(sc, amax, nullptr, nullptr, 0, q, s)) return e;
+  const FixAcc acc{reinterpret_cast<long long*>(num), reinterpret_cast<long long*>(num + n),
+                   touched, q};
+  if (int e = launch_object_fix(sc, u, di, dj, n0, m0, os, of, 0, sc->n_good, acc, nullptr, s))
     return e;
-  return launch_object_finish(num, num + n, n, i_ref, wsum, fm, valid, s);
+  return launch_fix_finish(acc, nullptr, n, i_ref, wsum, fm, valid, s);
 }
 
 extern "C" int pxst_gather(const pxst_ref* ref, const double* x, const double* y, int64_t n,

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _native
-from ._native import PxstCgInfo, PxstRef, PxstScan, PxstStats, check, stream_ptr
+from ._native import PxstAccum, PxstCgInfo, PxstRef, PxstScan, PxstStats, check, stream_ptr
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -132,6 +132,26 @@ class DeviceRef:
 _SOLVERS = {"cg": 0, "mgcg": 1}
 
 
+class Accum:
+    """Deterministic splat accumulators on the device (``pxst_accum``): int64
+    numerator / denominator [2, cells] in units of the device quanta
+    (float64[2]) and the touched flags (uint8, optional).  Frame shards add
+    ``data`` exactly (int64 all-reduce) and ``touched`` with max."""
+
+    def __init__(self, cells: int, quanta: torch.Tensor, device, touched: bool = True):
+        self.data = torch.zeros((2, cells), dtype=torch.int64, device=device)
+        self.touched = torch.zeros(cells, dtype=torch.uint8, device=device) if touched else None
+        self.quanta = quanta
+
+    @property
+    def cells(self) -> int:
+        return int(self.data.shape[1])
+
+    def c(self) -> PxstAccum:
+        return PxstAccum(self.data[0].data_ptr(), self.data[1].data_ptr(), _ptr(self.touched),
+                         self.quanta.data_ptr())
+
+
 def _grid_rule(b) -> tuple[int, int, tuple[int, int]]:
     """Object-grid origin and shape from the bbox values (recon.py:126-132)."""
     u0min, u0max, u1min, u1max, dimin, dimax, djmin, djmax = b
@@ -179,7 +199,7 @@ class PendingObject:
         n = shape[0] * shape[1]
         if n > self.cap:
             return self.ds.object_map(*self.inputs, geom=self.geom)
-        return self.ds.object_finish(self.acc[:, :n], (n0, m0), shape)
+        return self.ds.object_finish(self.acc, (n0, m0), shape)
 
 
 class DeviceScan:
@@ -212,6 +232,8 @@ class DeviceScan:
             last = frames_upload["chunks"][-1][2]
             self._upload.update(chunks=[(0, self.n_good, last)], waited=False,
                                 host=frames_upload.get("host"))
+        if frames_upload is not None and frames_upload.get("absmax") is not None:
+            self._upload["absmax"] = frames_upload["absmax"]     # same stack, same bound
         self._uploads: list = []     # identity cache of pixel maps / translations
         if frames_dev is None:
             frames_dev = self._upload_frames(frames, dev)
@@ -230,6 +252,7 @@ class DeviceScan:
                                self.good.data_ptr(), self.n_good, self.w64.data_ptr(),
                                self.w32.data_ptr(), self.work.data_ptr(), roi4)
         self.empty = self.n_work == 0 or self.n_good == 0 or r1 <= r0 or c1 <= c0
+        self.full_c_scan = self.c_scan     # band views keep the full scan's (shared quanta)
         self._side = None            # side stream of geometry_async
         self._support_components = None   # project_irrotational's solver choice
         plane = self.ss * self.fs
@@ -290,16 +313,56 @@ class DeviceScan:
         self._upload.update(chunks=chunks, waited=False, host=t)
         return out
 
-    def ready(self, frame_stats: bool = False) -> "DeviceScan":
-        """Make the current stream wait for the whole stack and run the K0
-        parts not yet run: the per-pixel part always (K2, K4), the per-frame
-        part (frame_norm) only for K3."""
+    def wait_frames(self) -> "DeviceScan":
+        """Make the current stream wait for the whole stack upload."""
         up = self._upload
         if not up["waited"]:
             st = torch.cuda.current_stream(self.device)
             for _, _, ev in up["chunks"]:
                 st.wait_event(ev)
             up.update(waited=True, host=None)
+        return self
+
+    def absmax(self) -> torch.Tensor:
+        """max |I| over the stack (device float64[1], pxst_stack_absmax): the
+        bound the fixed-point splat quanta derive from; once per stack."""
+        up = self._upload
+        if up.get("absmax") is None:
+            self.wait_frames()
+            t = torch.empty(1, dtype=torch.float64, device=self.device)
+            check(self.lib.pxst_stack_absmax(ctypes.byref(self.c_scan), t.data_ptr(), stream_ptr()))
+            up["absmax"] = t
+        return up["absmax"]
+
+    def object_quanta(self) -> torch.Tensor:
+        """Quanta of this scan's object accumulators (device float64[2]); the
+        same for every frame range and band view of the scan."""
+        up = self._upload
+        if up.get("obj_q") is None:
+            q = torch.empty(2, dtype=torch.float64, device=self.device)
+            check(self.lib.pxst_object_quanta(ctypes.byref(self.full_c_scan),
+                                              self.absmax().data_ptr(), q.data_ptr(),
+                                              stream_ptr()))
+            up["obj_q"] = q
+        return up["obj_q"]
+
+    def plane_quanta(self, ref: "DeviceRef") -> torch.Tensor:
+        """Quanta of the reference-plane accumulators of `ref`, from the full
+        scan (row shards must share them)."""
+        self.ready()
+        q = torch.empty(2, dtype=torch.float64, device=self.device)
+        c_ref = ref.struct()
+        check(self.lib.pxst_plane_quanta(ctypes.byref(self.full_c_scan), self.absmax().data_ptr(),
+                                         ctypes.byref(self.c_stats), ctypes.byref(c_ref),
+                                         q.data_ptr(), stream_ptr()))
+        return q
+
+    def ready(self, frame_stats: bool = False) -> "DeviceScan":
+        """Make the current stream wait for the whole stack and run the K0
+        parts not yet run: the per-pixel part always (K2, K4), the per-frame
+        part (frame_norm) only for K3."""
+        up = self._upload
+        self.wait_frames()
         parts = (0 if up["stats"] & 1 else 1) | (2 if frame_stats and not up["stats"] & 2 else 0)
         if parts:
             up["stats"] |= parts
@@ -422,39 +485,31 @@ class DeviceScan:
         return GeometryFuture(host8, host2, done, grid, grid_ready)
 
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
-                     acc: torch.Tensor | None = None) -> torch.Tensor:
-        """Float64 num/den accumulators [2, os*of] for a range of good frames."""
+                     acc: "Accum | None" = None) -> Accum:
+        """Fixed-point object accumulators (Accum, os*of cells) for a range of
+        good frames; added into `acc` when given."""
         os_, of = shape
         if acc is None:
-            acc = torch.zeros((2, os_ * of), dtype=torch.float64, device=self.device)
+            acc = Accum(os_ * of, self.object_quanta(), self.device)
         hi = self.n_good if frame_hi is None else frame_hi
-        up = self._upload
-        if up["waited"]:
-            ranges = [(frame_lo, hi)]
-        else:     # splat the chunks of the stack upload as they land
-            st = torch.cuda.current_stream(self.device)
-            ranges = []
-            for g0, g1, ev in up["chunks"]:
-                a, b = max(g0, frame_lo), min(g1, hi)
-                if a < b:
-                    st.wait_event(ev)
-                    ranges.append((a, b))
-        for a, b in ranges:
-            check(self.lib.pxst_object_splat(
-                ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0,
-                m0, os_, of, a, b, acc[0].data_ptr(), acc[1].data_ptr(), None, stream_ptr()))
+        self.wait_frames()
+        c_acc = acc.c()
+        check(self.lib.pxst_object_splat(
+            ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), n0, m0,
+            os_, of, frame_lo, hi, ctypes.byref(c_acc), None, stream_ptr()))
         return acc
 
-    def object_finish(self, acc, origin, shape) -> DeviceRef:
+    def object_finish(self, acc: Accum, origin, shape) -> DeviceRef:
         os_, of = shape
         n = os_ * of
         i_ref = torch.empty(n, dtype=torch.float64, device=self.device)
         wsum = torch.empty(n, dtype=torch.float64, device=self.device)
         fm = torch.empty(n, dtype=torch.float32, device=self.device)
         valid = torch.empty(n, dtype=torch.uint8, device=self.device)
-        check(self.lib.pxst_object_finish(acc[0].data_ptr(), acc[1].data_ptr(), n,
-                                          i_ref.data_ptr(), wsum.data_ptr(), fm.data_ptr(),
-                                          valid.data_ptr(), stream_ptr()))
+        c_acc = acc.c()
+        check(self.lib.pxst_object_finish(ctypes.byref(c_acc), n, i_ref.data_ptr(),
+                                          wsum.data_ptr(), fm.data_ptr(), valid.data_ptr(),
+                                          stream_ptr()))
         return DeviceRef(i_ref.view(os_, of), wsum.view(os_, of), fm.view(os_, of),
                          valid.view(os_, of), (int(origin[0]), int(origin[1])))
 
@@ -559,25 +614,28 @@ class DeviceScan:
         v.empty = self.empty or hi <= lo
         return v
 
-    def error_partials(self, ref: DeviceRef, u_t, di_t, dj_t):
-        """K4 without normalisation: (per_frame, per_pixel, plane_num, plane_den)."""
+    def error_partials(self, ref: DeviceRef, u_t, di_t, dj_t, quanta=None):
+        """K4 without normalisation: (per_frame, per_pixel, plane Accum) with
+        the full scan's plane quanta (or `quanta`)."""
         self.ready()
         per_frame = torch.zeros(self.n_frames, dtype=torch.float64, device=self.device)
         per_pixel = torch.zeros(self.ss * self.fs, dtype=torch.float64, device=self.device)
-        num = torch.zeros(ref.fm.numel(), dtype=torch.float64, device=self.device)
-        den = torch.zeros_like(num)
+        q = quanta if quanta is not None else self.plane_quanta(ref)
+        acc = Accum(ref.fm.numel(), q, self.device, touched=False)
         if not self.empty:
             c_ref = ref.struct()
+            c_acc = acc.c()
             check(self.lib.pxst_error_partials(
                 ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
                 u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
-                per_pixel.data_ptr(), num.data_ptr(), den.data_ptr(), stream_ptr()))
-        return per_frame, per_pixel.view(self.ss, self.fs), num, den
+                per_pixel.data_ptr(), ctypes.byref(c_acc), stream_ptr()))
+        return per_frame, per_pixel.view(self.ss, self.fs), acc
 
-    def plane_finish(self, num, den, shape):
-        plane = torch.empty(num.numel(), dtype=torch.float64, device=self.device)
-        check(self.lib.pxst_object_finish(num.data_ptr(), den.data_ptr(), num.numel(),
-                                          plane.data_ptr(), None, None, None, stream_ptr()))
+    def plane_finish(self, acc: Accum, shape):
+        plane = torch.empty(acc.cells, dtype=torch.float64, device=self.device)
+        c_acc = acc.c()
+        check(self.lib.pxst_object_finish(ctypes.byref(c_acc), acc.cells, plane.data_ptr(), None,
+                                          None, None, stream_ptr()))
         return plane.view(*shape)
 
     # ---------------------------------------------------------- K4 error maps
@@ -594,8 +652,9 @@ class DeviceScan:
             c_ref = ref.struct()
             check(self.lib.pxst_error_maps(
                 ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
-                u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
-                per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), stream_ptr()))
+                u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), self.absmax().data_ptr(),
+                per_frame.data_ptr(), per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(),
+                stream_ptr()))
         return (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
                 self.sigma2.view(self.ss, self.fs))
 
@@ -609,18 +668,19 @@ class DeviceScan:
         self.ready()
         os_, of = ref.shape
         cap = (os_ + 2 * margin) * (of + 2 * margin)
-        acc = torch.zeros((2, cap), dtype=torch.float64, device=self.device)
+        acc = Accum(cap, self.object_quanta(), self.device)
         per_frame = torch.empty(self.n_frames, dtype=torch.float64, device=self.device)
         per_pixel = torch.empty(self.ss * self.fs, dtype=torch.float64, device=self.device)
         plane = torch.empty(ref.fm.numel(), dtype=torch.float64, device=self.device)
         total = torch.empty(1, dtype=torch.float64, device=self.device)
         geom.gpu_wait()
         c_ref = ref.struct()
+        c_acc = acc.c()
         check(self.lib.pxst_error_maps_splat(
             ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
-            u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), per_frame.data_ptr(),
-            per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(), geom.grid_dev.data_ptr(),
-            cap, acc[0].data_ptr(), acc[1].data_ptr(), stream_ptr()))
+            u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), self.absmax().data_ptr(),
+            per_frame.data_ptr(), per_pixel.data_ptr(), plane.data_ptr(), total.data_ptr(),
+            geom.grid_dev.data_ptr(), cap, ctypes.byref(c_acc), stream_ptr()))
         metrics = (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
                    self.sigma2.view(self.ss, self.fs))
         return metrics, PendingObject(self, acc, cap, geom, (u_t, di_t, dj_t))

@@ -7,20 +7,25 @@ HBM), so no data moves between phases except the small exchange tensors:
 =====================  =================  ====================================
 phase                  partition          exchange after it
 =====================  =================  ====================================
-K1 object formation    good frames        all-reduce(sum) of num/den (float64)
+K1 object formation    good frames        all-reduce(sum) of the int64
+                                          fixed-point num/den (exact), max of
+                                          the touched flags
 K2 pixel-map search    detector rows,     all-gather of the u rows (exact)
                        balanced by work
                        pixel count
 K3 translation search  good frames        all-gather of (di, dj) (exact)
-K4 error maps          detector rows      all-reduce of per-frame sums,
-                                          per-pixel map, plane num/den
+K4 error maps          detector rows      all-reduce of the per-frame sums
+                                          (float64) and of the int64 plane
+                                          num/den (exact); all-gather of the
+                                          per-pixel rows (exact)
 =====================  =================  ====================================
 
 The grid bbox is computed redundantly from the replicated u and t.  Row
 shards need no halo (sigma = 0, integrate = False: pixels are independent,
-recon.py:221-315); the all-gathers are exact, so u and t match the
-single-GPU result bit for bit given the same object map; the float64
-all-reduces differ from one GPU only in summation order.
+recon.py:221-315).  The object map and the reference plane are integer sums
+(fixsplat.cuh), so they are bit-identical for any number of GPUs; the
+all-gathers are exact, so u and t then match the single-GPU result bit for
+bit too; only the per-frame error sums differ, in float64 summation order.
 
 The logic talks to an *executor* (``DeviceExecutor`` here; tests supply a
 CPU one built on the oracle and run it under gloo), so the partitioning and
@@ -91,14 +96,21 @@ class ShardedIteration:
         through host copies; NCCL takes device tensors directly."""
         return t.is_cuda and dist.get_backend(self.group) == "gloo"
 
-    def _all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+    def _all_reduce(self, t: torch.Tensor, op=dist.ReduceOp.SUM) -> torch.Tensor:
         if self._host_staged(t):
             h = t.cpu()
-            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(h, op=op, group=self.group)
             t.copy_(h)
             return t
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        dist.all_reduce(t, op=op, group=self.group)
         return t
+
+    def _all_reduce_acc(self, acc) -> None:
+        """Splat accumulators of the ranks' frame / row shares: int64 sums
+        (exact) and touched flags (max)."""
+        self._all_reduce(acc.data)
+        if getattr(acc, "touched", None) is not None:
+            self._all_reduce(acc.touched, op=dist.ReduceOp.MAX)
 
     def _all_gather(self, out: torch.Tensor, buf: torch.Tensor) -> None:
         if self._host_staged(buf):
@@ -109,15 +121,16 @@ class ShardedIteration:
         dist.all_gather_into_tensor(out, buf, group=self.group)
 
     def _gather_rows(self, u_local: torch.Tensor) -> torch.Tensor:
-        """Assemble the full u from each rank's band (exact)."""
-        _, ss, fs = u_local.shape
+        """Assemble a full [C, SS, FS] plane from each rank's row band (exact);
+        rows outside every band keep u_local's values."""
+        c, ss, fs = u_local.shape
         lo, hi = self.rows[self.rank]
-        buf = torch.zeros((2, self.max_rows, fs), dtype=u_local.dtype, device=u_local.device)
+        buf = torch.zeros((c, self.max_rows, fs), dtype=u_local.dtype, device=u_local.device)
         buf[:, : hi - lo] = u_local[:, lo:hi]
-        out = torch.empty((self.world * 2, self.max_rows, fs), dtype=u_local.dtype,
+        out = torch.empty((self.world * c, self.max_rows, fs), dtype=u_local.dtype,
                           device=u_local.device)
         self._all_gather(out, buf.contiguous())
-        out = out.view(self.world, 2, self.max_rows, fs)
+        out = out.view(self.world, c, self.max_rows, fs)
         u = u_local.clone()
         for k, (a, b) in enumerate(self.rows):
             u[:, a:b] = out[k, :, : b - a]
@@ -145,7 +158,7 @@ class ShardedIteration:
         n0, m0, shape = geom.bbox() if geom is not None else self.ex.bbox(u, di, dj)
         lo, hi = self.frames[self.rank]
         acc = self.ex.object_splat(u, di, dj, n0, m0, shape, lo, hi)
-        self._all_reduce(acc)
+        self._all_reduce_acc(acc)
         return self.ex.object_finish(acc, (n0, m0), shape)
 
     def pixel_map(self, ref, u, di, dj, half_ss, half_fs, sub=None, refine=True, opts=None,
@@ -167,16 +180,14 @@ class ShardedIteration:
         return self._gather_frames(di_l, dj_l)
 
     def error_maps(self, ref, u, di, dj) -> ShardedMetrics:
-        per_frame, per_pixel, num, den = self.ex.error_partials(ref, u, di, dj,
-                                                                rows=self.rows[self.rank])
-        # one all-reduce for the four partial sums (launch latency, not
-        # bandwidth, dominates collectives of a few MB over NVSwitch)
-        parts = (per_frame, per_pixel, num, den)
-        flat = torch.cat([t.reshape(-1) for t in parts])
-        self._all_reduce(flat)
-        views = torch.split(flat, [t.numel() for t in parts])
-        per_frame, per_pixel, num, den = (v.view(t.shape) for v, t in zip(views, parts))
-        plane = self.ex.error_finish(num, den, ref)
+        per_frame, per_pixel, acc = self.ex.error_partials(ref, u, di, dj,
+                                                           rows=self.rows[self.rank])
+        # per-frame sums add; the per-pixel map is row-local (gathered); the
+        # plane accumulators add exactly
+        self._all_reduce(per_frame)
+        per_pixel = self._gather_rows(per_pixel.reshape(1, *per_pixel.shape))[0]
+        self._all_reduce_acc(acc)
+        plane = self.ex.error_finish(acc, ref)
         good = self.ex.good_index_tensor()
         total = per_frame[good].sum().reshape(1) if len(good) else per_frame.new_zeros(1)
         return ShardedMetrics(total, per_frame, per_pixel, plane)
@@ -243,8 +254,8 @@ class DeviceExecutor:
     def error_partials(self, ref, u, di, dj, rows):
         return self.ds.band(*rows).error_partials(ref, u, di, dj)
 
-    def error_finish(self, num, den, ref):
-        return self.ds.plane_finish(num, den, ref.shape)
+    def error_finish(self, acc, ref):
+        return self.ds.plane_finish(acc, ref.shape)
 
     def regularise(self, u, opts):
         return self.ds.regularise(u, opts)

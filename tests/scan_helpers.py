@@ -30,6 +30,15 @@ def tiny_scan(seed=3, n=6, ss=24, fs=28):
         pb.PixelTranslations(di, dj)
 
 
+class HostAcc:
+    """Splat accumulators of the oracle executor (float64 [2, cells], the
+    interface of engine.Accum that ShardedIteration all-reduces)."""
+
+    def __init__(self, data):
+        self.data = data
+        self.touched = None
+
+
 class OracleRef:
     def __init__(self, i_ref, wsum, origin):
         self.i_ref, self.wsum, self.origin = i_ref, wsum, origin
@@ -76,10 +85,10 @@ class OracleExecutor:
             I = self.frames[f][rows, cols].astype(np.float64)
             orc.splat(acc_v, acc_w, u[0][rows, cols] - di[f] - n0, u[1][rows, cols] - dj[f] - m0,
                       I / wf, wf * wf)
-        return torch.as_tensor(np.stack([acc_v.ravel(), acc_w.ravel()]))
+        return HostAcc(torch.as_tensor(np.stack([acc_v.ravel(), acc_w.ravel()])))
 
     def object_finish(self, acc, origin, shape):
-        a = acc.numpy()
+        a = acc.data.numpy()
         i_ref, _ = orc.ratio_where_weighted(a[0].reshape(shape), a[1].reshape(shape))
         return OracleRef(i_ref, a[1].reshape(shape).copy(), tuple(origin))
 
@@ -125,14 +134,14 @@ class OracleExecutor:
             per_pixel[r, c] += eps
             orc.splat(acc_v, acc_w, x, y, eps, 1.0)
         return (torch.as_tensor(per_frame), torch.as_tensor(per_pixel),
-                torch.as_tensor(acc_v.ravel()), torch.as_tensor(acc_w.ravel()))
+                HostAcc(torch.as_tensor(np.stack([acc_v.ravel(), acc_w.ravel()]))))
 
     def regularise(self, u, opts):
         return torch.as_tensor(orc.regularise_map(u.numpy(), self.work.astype(bool),
                                                   getattr(opts, "sigma", 0.0),
                                                   getattr(opts, "integrate", False)))
 
-    def error_finish(self, num, den, ref):
-        plane, _ = orc.ratio_where_weighted(num.numpy().reshape(ref.shape),
-                                            den.numpy().reshape(ref.shape))
+    def error_finish(self, acc, ref):
+        a = acc.data.numpy()
+        plane, _ = orc.ratio_where_weighted(a[0].reshape(ref.shape), a[1].reshape(ref.shape))
         return torch.as_tensor(plane)

@@ -49,8 +49,13 @@ def test_null_arguments_rejected_without_device(lib):
     rc = lib.pxst_translation_search(None, None, None, None, None, None, 1, 1, 0.0, 0, 0, None,
                                      None, None, None)
     assert rc == _native.PXST_EINVAL
-    rc = lib.pxst_error_maps(None, None, None, None, None, None, None, None, None, None, None)
+    rc = lib.pxst_error_maps(None, None, None, None, None, None, None, None, None, None, None,
+                             None)
     assert rc == _native.PXST_EINVAL
+    rc = lib.pxst_object_splat(None, None, None, None, 0, 0, 1, 1, 0, 0, None, None, None)
+    assert rc == _native.PXST_EINVAL
+    rc = lib.pxst_object_finish(None, 1, None, None, None, None, None)
+    assert rc == _native.PXST_EINVAL and b"accumulator" in lib.pxst_last_error()
 
 
 def test_bad_window_rejected(lib):

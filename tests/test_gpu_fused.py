@@ -28,13 +28,13 @@ def test_error_maps_and_next_object(request, scan_name):
     sref = ds.object_map(u1, di, dj)
     np.testing.assert_allclose(pf_f.cpu().numpy(), pf_s.cpu().numpy(), rtol=1e-12)
     np.testing.assert_allclose(pp_f.cpu().numpy(), pp_s.cpu().numpy(), rtol=1e-12)
-    np.testing.assert_allclose(pl_f.cpu().numpy(), pl_s.cpu().numpy(), rtol=1e-5, atol=1e-12)
+    # plane and object are exact fixed-point sums (fixsplat.cuh): the fused
+    # and separate passes agree bit for bit
+    assert torch.equal(pl_f, pl_s)
     assert abs(t_f.item() - t_s.item()) <= 1e-12 * abs(t_s.item())
     assert tuple(nref.origin) == tuple(sref.origin) and nref.shape == sref.shape
     assert torch.equal(nref.valid, sref.valid)
-    ok = sref.valid.bool()
-    rel = ((nref.i_ref - sref.i_ref).abs()[ok] / sref.i_ref.abs()[ok]).max().item()
-    assert rel < 1e-5, rel
+    assert torch.equal(nref.i_ref, sref.i_ref) and torch.equal(nref.wsum, sref.wsum)
     # the geometry future agrees with the synchronous bbox
     assert geom.bbox() == ds.bbox(u1, di, dj)
     n0, m0, (os_, of) = geom.bbox()
@@ -43,6 +43,28 @@ def test_error_maps_and_next_object(request, scan_name):
     (_, _, _, _, _), small = ds.error_maps_and_next_object(ref, u1, di, dj, geom, margin=-20)
     assert small.cap < os_ * of
     alt = small.resolve()
-    ok = alt.valid.bool()
-    rel = ((alt.i_ref - sref.i_ref).abs()[ok] / sref.i_ref.abs()[ok]).max().item()
-    assert rel < 1e-5 and torch.equal(alt.valid, sref.valid)
+    assert torch.equal(alt.i_ref, sref.i_ref) and torch.equal(alt.valid, sref.valid)
+
+
+@pytest.mark.parametrize("scan_name", ["scan0", "scan1"])
+def test_object_map_and_plane_bit_reproducible(request, scan_name):
+    """Two runs of object formation and of the error maps give identical
+    bits (the reference's np.bincount is deterministic, interp.py:114-122;
+    here the terms are summed as exact integers, fixsplat.cuh), and so does a
+    fresh DeviceScan of the same data."""
+    s = request.getfixturevalue(scan_name)
+    outs = []
+    for _ in range(2):
+        ds = engine.DeviceScan(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask)
+        u, (di, dj) = ds.upload_u(s.u0.u), ds.upload_t(s.t0.di, s.t0.dj)
+        runs = []
+        for _ in range(2):
+            ref = ds.object_map(u, di, dj)
+            total, pf, pp, plane, _ = ds.error_maps(ref, u, di, dj)
+            runs.append((ref.i_ref.clone(), ref.wsum.clone(), ref.valid.clone(), plane.clone(),
+                         pf.clone(), pp.clone(), total.clone()))
+        for a, b in zip(*runs):
+            assert torch.equal(a, b)
+        outs.append(runs[0])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)

@@ -34,29 +34,32 @@ def test_band_views_compose(scan0):
     u_asm = u.clone()
     pf = torch.zeros(ds.n_frames, dtype=torch.float64, device=ds.device)
     pp = torch.zeros((ds.ss, ds.fs), dtype=torch.float64, device=ds.device)
-    num = den = None
+    acc = None
     for lo, hi in bands:
         u_b = ex.pixel_map_search(ref, u, di, dj, 3, 3, None, True, rows=(lo, hi))
         u_asm[:, lo:hi] = u_b[:, lo:hi]
-        f, p, n_, d_ = ex.error_partials(ref, u_full, di, dj, rows=(lo, hi))
+        f, p, a_ = ex.error_partials(ref, u_full, di, dj, rows=(lo, hi))
         pf += f
         pp += p
-        num = n_ if num is None else num + n_
-        den = d_ if den is None else den + d_
+        if acc is None:
+            acc = a_
+        else:
+            acc.data += a_.data
     d = np.abs((u_asm - u_full).cpu().numpy()).max(axis=0)
     assert np.mean(d < 1e-3) > 0.999
     total, per_frame, per_pixel, plane, _ = ds.error_maps(ref, u_full, di, dj)
     np.testing.assert_allclose(pf.cpu().numpy(), per_frame.cpu().numpy(), rtol=1e-10)
     np.testing.assert_allclose(pp.cpu().numpy(), per_pixel.cpu().numpy(), rtol=1e-12)
-    np.testing.assert_allclose(ex.error_finish(num, den, ref).cpu().numpy(),
-                               plane.cpu().numpy(), rtol=1e-5, atol=1e-12)
-    # frame-range splats compose to the full object map
+    # fixed-point plane: the row bands' integer sums add up to the full
+    # pass's exactly (fixsplat.cuh)
+    assert torch.equal(ex.error_finish(acc, ref), plane)
+    # frame-range splats compose to the full object map, bit for bit
     n0, m0, shape = ds.bbox(u, di, dj)
     acc = ds.object_splat(u, di, dj, n0, m0, shape, 0, 10)
-    acc += ds.object_splat(u, di, dj, n0, m0, shape, 10, ds.n_good)
+    ds.object_splat(u, di, dj, n0, m0, shape, 10, ds.n_good, acc=acc)
     ref2 = ds.object_finish(acc, (n0, m0), shape)
-    # float32 chunk images (splat.cu header): agreement to ~1e-7
-    np.testing.assert_allclose(ref2.i_ref.cpu().numpy(), ref.i_ref.cpu().numpy(), rtol=1e-5)
+    assert torch.equal(ref2.i_ref, ref.i_ref) and torch.equal(ref2.wsum, ref.wsum)
+    assert torch.equal(ref2.valid, ref.valid)
 
 
 def test_one_rank_nccl_iteration(scan0):
@@ -125,7 +128,11 @@ def test_two_ranks_device_kernels(scan0):
     assert np.mean(d < 1e-3) > 0.999
     assert abs(out["total"] - float(total.item())) <= 1e-5 * float(total.item())
     np.testing.assert_allclose(out["per_frame"], per_frame.cpu().numpy(), rtol=1e-5)
-    np.testing.assert_allclose(out["plane"], plane.cpu().numpy(), rtol=1e-4, atol=1e-9)
+    # (the ranks' row-band searches sum their float32 trials in other frame
+    # chunks than the full-frame search, so u -- and the plane splatted from
+    # it -- may differ in the last bits; for one u the plane splits exactly:
+    # test_band_views_compose)
+    np.testing.assert_allclose(out["plane"], plane.cpu().numpy(), rtol=1e-6, atol=1e-12)
 
 
 def test_bench_spawns_ranks():

@@ -221,6 +221,40 @@ __global__ void k_rmw128(float* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = sm[threadIdx.x & 2047].x;
 }
 
+// Shared-memory u64 atomics (ATOMS.CAST.SPIN.64 loops): lanes on consecutive
+// words (dup = 1) or pairs of lanes on the same word (dup = 2).
+__global__ void k_atoms_u64(float* out, int iters, int dup) {
+  __shared__ unsigned long long sm[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sm[i] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      atomicAdd(&sm[(w * 32 + lane / dup + (it * 8 + k) * 256) & 2047],
+                (unsigned long long)(lane + k + 3));
+  }
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)sm[threadIdx.x & 2047];
+}
+
+// Fixed-point term: DFMA against a magic constant, 64-bit subtract (the
+// conversion cost of one accumulation term).
+__global__ void k_fix_terms(float* out, int iters, double s) {
+  const double magic = 6755399441055744.0;
+  long long acc = 0;
+  double x = threadIdx.x * 1e-3;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double y = fma(x + k, s, magic);
+      acc += __double_as_longlong(y) - 0x4338000000000000ll;
+    }
+    x += 1e-7;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+}
+
 __global__ void k_match(float* out, int iters) {
   unsigned acc = 0;
   const unsigned lane = threadIdx.x & 31;
@@ -322,6 +356,12 @@ int main() {
     printf(", \"atoms_u32_row_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
     ms = timeit([&] { k_atoms_f32<<<blocks, threads>>>(fout, ai); });
     printf(", \"atoms_f32_row_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_atoms_u64<<<blocks, threads>>>(fout, ai, 1); });
+    printf(", \"atoms_u64_cas_row_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_atoms_u64<<<blocks, threads>>>(fout, ai, 2); });
+    printf(", \"atoms_u64_cas_dup2_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
+    ms = timeit([&] { k_fix_terms<<<blocks, threads>>>(fout, ai, 1.2345e3); });
+    printf(", \"fix_terms_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
     ms = timeit([&] { k_rmw128<<<blocks, threads>>>(fout, ai); });
     printf(", \"smem_rmw128_lane_ops_per_clk_sm\": %.2f", ops / (ms * 1e-3) / (clk_khz * 1e3) / sms);
     ms = timeit([&] { k_match<<<blocks, threads>>>(fout, ai); });
