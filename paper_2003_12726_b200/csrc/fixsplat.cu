@@ -197,11 +197,14 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
     __syncthreads();
     // footprint of the tile for frame t (primary-grid cells, the +1 row /
     // column holds the r0 + 1 / c0 + 1 corners)
+    // (mode 2: one more cell on each side -- the next grid's positions are
+    // rounded separately, recon.py:138 order, and may floor one cell over)
+    constexpr int kM = MODE == 2 ? 1 : 0;
     auto foot = [&](int t, int& r0, int& r1, int& c0, int& c1) {
-      r0 = ifloor(umin0 - t_di[t] - n0d);
-      r1 = ifloor(umax0 - t_di[t] - n0d) + 1;
-      c0 = ifloor(umin1 - t_dj[t] - m0d);
-      c1 = ifloor(umax1 - t_dj[t] - m0d) + 1;
+      r0 = ifloor(umin0 - t_di[t] - n0d) - kM;
+      r1 = ifloor(umax0 - t_di[t] - n0d) + 1 + kM;
+      c0 = ifloor(umin1 - t_dj[t] - m0d) - kM;
+      c1 = ifloor(umax1 - t_dj[t] - m0d) + 1 + kM;
     };
     for (int s0 = 0; s0 < nt;) {
       int R0 = 1 << 30, R1 = -(1 << 30), C0 = 1 << 30, C1 = -(1 << 30);
@@ -303,19 +306,35 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
             }
             bool inB = false;
             double sBn = 0.0, sBd = 0.0;
+            double cwb[4] = {0.0, 0.0, 0.0, 0.0};
+            bool cokb[4] = {false, false, false, false};
+            int r0b = 0, c0b = 0;
             if (MODE == 2) {
-              const double xb = x + static_cast<double>(dn), yb = y + static_cast<double>(dm);
+              // the next object's own position, as make_reference computes it
+              // (recon.py:138: u - d - origin), so the terms equal a separate
+              // object formation bit for bit
+              const double xb = act ? u0[e] - t_di[t] - static_cast<double>(a.n0 - dn) : 0.0;
+              const double yb = act ? u1[e] - t_dj[t] - static_cast<double>(a.m0 - dm) : 0.0;
               inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
+              const double xbf = floor(xb), ybf = floor(yb);
+              const double fxb = xb - xbf, fyb = yb - ybf;
+              r0b = static_cast<int>(xbf);
+              c0b = static_cast<int>(ybf);
+              const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
+              cwb[0] = gxb * gyb; cwb[1] = gxb * fyb; cwb[2] = fxb * gyb; cwb[3] = fxb * fyb;
+              cokb[0] = true; cokb[1] = fyb > 0.0; cokb[2] = fxb > 0.0; cokb[3] = fxb > 0.0 && fyb > 0.0;
               sBn = I * vsc[e] * qb_n;
               sBd = W2[e] * qb_d;
             }
             const int dl[4] = {0, 1, nc, nc + 1};
             const int dc_[4] = {0, 1, 0, 1}, dr_[4] = {0, 0, 1, 1};
             const int l = (r0 - R0) * nc + (c0 - C0);
+            // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
+            const int lb = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const bool okA = inA && cok[q];
-              const bool okB = inB && cok[q];
+              const bool okB = inB && cokb[q];
               if (!okA && !okB) continue;
               unsigned lo;
               int hi;
@@ -331,13 +350,14 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
                   if (!ERR) stc[li] = 1;
                 }
                 if (MODE == 2 && okB) {
-                  fix_limbs(sBn, cw[q], lo, hi);
-                  atomicAdd(&slo[2 * RC + li], lo);
-                  atomicAdd(&shi[2 * RC + li], hi);
-                  fix_limbs(sBd, cw[q], lo, hi);
-                  atomicAdd(&slo[3 * RC + li], lo);
-                  atomicAdd(&shi[3 * RC + li], hi);
-                  stc[RC + li] = 1;
+                  const int lib = lb + dl[q];
+                  fix_limbs(sBn, cwb[q], lo, hi);
+                  atomicAdd(&slo[2 * RC + lib], lo);
+                  atomicAdd(&shi[2 * RC + lib], hi);
+                  fix_limbs(sBd, cwb[q], lo, hi);
+                  atomicAdd(&slo[3 * RC + lib], lo);
+                  atomicAdd(&shi[3 * RC + lib], hi);
+                  stc[RC + lib] = 1;
                 }
               } else {     // direct: the same integers straight into the int64 images
                 if (okA) {
@@ -349,11 +369,11 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
                   if (!ERR && a.A.touched) a.A.touched[cell] = 1;
                 }
                 if (MODE == 2 && okB) {
-                  const int64_t cell = (int64_t)(r0 + dr_[q] + dn) * ofb + (c0 + dc_[q] + dm);
+                  const int64_t cell = (int64_t)(r0b + dr_[q]) * ofb + (c0b + dc_[q]);
                   atomicAdd(reinterpret_cast<unsigned long long*>(a.B.num + cell),
-                            static_cast<unsigned long long>(fix_value(sBn, cw[q])));
+                            static_cast<unsigned long long>(fix_value(sBn, cwb[q])));
                   atomicAdd(reinterpret_cast<unsigned long long*>(a.B.den + cell),
-                            static_cast<unsigned long long>(fix_value(sBd, cw[q])));
+                            static_cast<unsigned long long>(fix_value(sBd, cwb[q])));
                   if (a.B.touched) a.B.touched[cell] = 1;
                 }
               }
