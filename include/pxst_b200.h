@@ -114,13 +114,17 @@ int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const do
  * GPUs: frame shards all-reduce num/den as int64 (exact) and touched with
  * max.  quanta (device, float64[2]) = (q_num, q_den), chosen so that
  * |t| < 2^41 q (pxst_object_quanta / pxst_plane_quanta; ~41 significant
- * bits relative to the largest possible term).  touched[c] = 1 where a
- * positive-weight term landed: the reference's wsum > 0 (data_model.py:186). */
+ * bits relative to the largest possible term).  A cell is valid (the
+ * reference's wsum > 0, data_model.py:186) when den + den_fine > 0 or a
+ * tiny-weight term marked it in touched. */
 typedef struct pxst_accum {
-  int64_t* num;           /* [cells], units of quanta[0]        */
-  int64_t* den;           /* [cells], units of quanta[1]        */
-  uint8_t* touched;       /* [cells] or NULL                    */
-  const double* quanta;   /* device [2]                         */
+  int64_t* num;           /* [cells], units of quanta[0]                        */
+  int64_t* den;           /* [cells], units of quanta[1]                        */
+  int64_t* num_fine;      /* [cells], units of quanta[0] * 2^-30: terms whose   */
+  int64_t* den_fine;      /*   bilinear corner weight is < 2^-10 (cells reached */
+                          /*   only by tiny-weight corners keep their precision)*/
+  uint8_t* touched;       /* [cells] or NULL: a tiny-weight term landed         */
+  const double* quanta;   /* device [2]                                         */
 } pxst_accum;
 
 /* max |I| over the whole frame stack (device float64 scalar): the bound the

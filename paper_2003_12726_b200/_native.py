@@ -38,8 +38,8 @@ class PxstRef(ctypes.Structure):
 
 
 class PxstAccum(ctypes.Structure):
-    _fields_ = [("num", c_void_p), ("den", c_void_p), ("touched", c_void_p),
-                ("quanta", c_void_p)]
+    _fields_ = [("num", c_void_p), ("den", c_void_p), ("num_fine", c_void_p),
+                ("den_fine", c_void_p), ("touched", c_void_p), ("quanta", c_void_p)]
 
 
 class PxstCgInfo(ctypes.Structure):

@@ -170,7 +170,8 @@ int check_err_args(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* re
 
 FixAcc fix_acc(const pxst_accum* acc) {
   return FixAcc{reinterpret_cast<long long*>(acc->num), reinterpret_cast<long long*>(acc->den),
-                acc->touched, acc->quanta};
+                reinterpret_cast<long long*>(acc->num_fine),
+                reinterpret_cast<long long*>(acc->den_fine), acc->touched, acc->quanta};
 }
 
 // Plane accumulators + quanta in one scratch block, the error pass, the
@@ -181,18 +182,19 @@ int error_maps_full(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* r
                     const FixAcc* next, const int64_t* grid_b, int64_t cap_b, cudaStream_t s) {
   const int64_t n_o = ref->os * ref->of;
   Scratch acc;
-  if (int e = acc.alloc(sizeof(int64_t) * 2 * n_o + 4 * sizeof(double), s)) return e;
+  if (int e = acc.alloc(sizeof(int64_t) * 4 * n_o + 4 * sizeof(double), s)) return e;
   int64_t* num = acc.as<int64_t>();
-  double* q = reinterpret_cast<double*>(num + 2 * n_o);
+  double* q = reinterpret_cast<double*>(num + 4 * n_o);
   double* amax = q + 2;
-  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 2 * n_o, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 4 * n_o, s));
   if (!absmax) {
     if (int e = launch_abs_max(sc, amax, s)) return e;
     absmax = amax;
   }
   if (int e = launch_quanta(sc, absmax, st->sigma2, ref, 1, q, s)) return e;
   const FixAcc plane{reinterpret_cast<long long*>(num), reinterpret_cast<long long*>(num + n_o),
-                     nullptr, q};
+                     reinterpret_cast<long long*>(num + 2 * n_o),
+                     reinterpret_cast<long long*>(num + 3 * n_o), nullptr, q};
   if (int e = error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, plane, total, next, grid_b,
                          cap_b, s))
     return e;
@@ -225,7 +227,7 @@ extern "C" int pxst_error_partials(const pxst_scan* sc, const pxst_stats* st,
                                    const pxst_accum* plane, void* stream) {
   if (int e = check_err_args(sc, st, ref)) return e;
   PXST_REQUIRE(u && di && dj && per_frame && per_pixel && plane && plane->num && plane->den &&
-                   plane->quanta,
+                   plane->num_fine && plane->den_fine && plane->quanta,
                "NULL pointer");
   return error_pass(sc, st, ref, u, di, dj, per_frame, per_pixel, fix_acc(plane), nullptr,
                     nullptr, nullptr, 0, as_stream(stream));
@@ -246,7 +248,7 @@ extern "C" int pxst_error_maps_splat(const pxst_scan* sc, const pxst_stats* st,
                                      const pxst_accum* next, void* stream) {
   if (int e = check_err_args(sc, st, ref)) return e;
   PXST_REQUIRE(u && di && dj && per_frame && per_pixel && ref_plane && total && grid && next &&
-                   next->num && next->den && next->quanta,
+                   next->num && next->den && next->num_fine && next->den_fine && next->quanta,
                "NULL pointer");
   PXST_REQUIRE(capacity > 0 && capacity < (int64_t(1) << 40), "bad capacity");
   const FixAcc nx = fix_acc(next);

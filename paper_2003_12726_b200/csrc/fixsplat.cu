@@ -30,12 +30,12 @@ constexpr int kXR = 16, kXC = 32, kXT = 256, kXW = kXT / 32;  // tile, threads, 
 constexpr int kXB = 8;        // frames per batch
 constexpr int kXTab = 256;    // frames per shared frame-table chunk (multiple of kXB)
 
-template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 2048; };
-template <> struct FixCfg<2> { static constexpr int NV = 4, RC = 1536; };
+template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 3072; };
+template <> struct FixCfg<2> { static constexpr int NV = 4, RC = 2048; };
 
 template <int MODE>
 constexpr size_t fix_smem_bytes() {
-  return sizeof(unsigned) * 2 * FixCfg<MODE>::NV * FixCfg<MODE>::RC + 2 * FixCfg<MODE>::RC;
+  return sizeof(unsigned) * 2 * FixCfg<MODE>::NV * FixCfg<MODE>::RC;
 }
 
 }  // namespace
@@ -62,8 +62,35 @@ struct FixArgs {
 
 namespace {
 
-__device__ __forceinline__ int ifloor(double x) {
-  return static_cast<int>(fmax(fmin(floor(x), 1e9), -1e9));
+__device__ __forceinline__ void red64(long long* p, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// One term t = scaled * w of an image: coarse corners into the shared region
+// (limbs) or, without a region, into the global int64 image; tiny-weight
+// corners into the fine image (see kFineW).
+struct TermSink {
+  unsigned* lo;       // region limbs of this value (lo, hi = lo + NV*RC) or nullptr
+  int* hi;
+  long long* g;       // global coarse image
+  long long* gf;      // global fine image
+};
+
+__device__ __forceinline__ void add_term(const TermSink& k, bool region, int li, int64_t cell,
+                                         double scaled, double w) {
+  if (w >= kFineW) {
+    if (region) {
+      unsigned lo;
+      int hi;
+      fix_limbs(scaled, w, lo, hi);
+      atomicAdd(k.lo + li, lo);
+      atomicAdd(k.hi + li, hi);
+    } else {
+      red64(k.g + cell, fix_value(scaled, w));
+    }
+  } else if (w > 0.0) {
+    red64(k.gf + cell, fix_value(scaled * 0x1p30, w));
+  }
 }
 
 template <int MODE>
@@ -73,9 +100,9 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   extern __shared__ __align__(16) unsigned char fx_raw[];
   unsigned* slo = reinterpret_cast<unsigned*>(fx_raw);              // [NV][RC]
   int* shi = reinterpret_cast<int*>(slo + NV * RC);                 // [NV][RC]
-  uint8_t* stc = reinterpret_cast<uint8_t*>(shi + NV * RC);         // [2][RC]
   __shared__ double t_di[kXTab], t_dj[kXTab];
   __shared__ int64_t t_off[kXTab];
+  __shared__ int4 t_ft[kXTab];                                      // frame footprints
   __shared__ double s_red[kXW][4];
   __shared__ double s_fr[kXW][kXB];
   __shared__ int s_cmax;
@@ -108,6 +135,7 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   double b3 = fmax(live[0] ? u1[0] : -INFINITY, live[1] ? u1[1] : -INFINITY);
   b0 = warp_min(b0); b1 = warp_max(b1); b2 = warp_min(b2); b3 = warp_max(b3);
   if (lane == 0) { s_red[warp][0] = b0; s_red[warp][1] = b1; s_red[warp][2] = b2; s_red[warp][3] = b3; }
+  if (threadIdx.x == 0) s_cmax = 0;
   __syncthreads();
   double umin0 = s_red[0][0], umax0 = s_red[0][1], umin1 = s_red[0][2], umax1 = s_red[0][3];
 #pragma unroll
@@ -127,28 +155,29 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   // frame: a pixel in u-bin b reaches cells b - D + {-1, 0, 1} per axis
   // (D = the frame's integer shift), so the max over 3 x 3 blocks of the
   // tile's u-bin histogram bounds it.
-  if (threadIdx.x == 0) s_cmax = 0;
   const bool fin = fabs(umin0) < 1e9 && fabs(umax0) < 1e9 && fabs(umin1) < 1e9 && fabs(umax1) < 1e9;
-  const int hb0 = fin ? ifloor(umin0) : 0, hb1 = fin ? ifloor(umin1) : 0;
-  const int hh = fin ? ifloor(umax0) - hb0 + 1 : 1 << 20, hw = fin ? ifloor(umax1) - hb1 + 1 : 1 << 20;
+  const int hb0 = fin ? __double2int_rd(umin0) : 0, hb1 = fin ? __double2int_rd(umin1) : 0;
+  const int hh = fin ? __double2int_rd(umax0) - hb0 + 1 : 1 << 20;
+  const int hw = fin ? __double2int_rd(umax1) - hb1 + 1 : 1 << 20;
   int cmax;
   if (hh <= 2 * RC && hw <= 2 * RC && hh * hw <= NV * RC) {
     for (int i = threadIdx.x; i < hh * hw; i += kXT) slo[i] = 0u;
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 2; ++e)
-      if (live[e]) atomicAdd(&slo[(ifloor(u0[e]) - hb0) * hw + (ifloor(u1[e]) - hb1)], 1u);
+      if (live[e])
+        atomicAdd(&slo[(__double2int_rd(u0[e]) - hb0) * hw + (__double2int_rd(u1[e]) - hb1)], 1u);
     __syncthreads();
     int m = 0;
     for (int i = threadIdx.x; i < hh * hw; i += kXT) {
       const int r = i / hw, c = i % hw;
-      int s = 0;
+      int sum = 0;
       for (int dr = -1; dr <= 1; ++dr)
         for (int dc = -1; dc <= 1; ++dc) {
           const int rr = r + dr, cc = c + dc;
-          if (rr >= 0 && rr < hh && cc >= 0 && cc < hw) s += static_cast<int>(slo[rr * hw + cc]);
+          if (rr >= 0 && rr < hh && cc >= 0 && cc < hw) sum += static_cast<int>(slo[rr * hw + cc]);
         }
-      m = max(m, s);
+      m = max(m, sum);
     }
     atomicMax(&s_cmax, m);
     __syncthreads();
@@ -156,9 +185,9 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   } else {
     cmax = 2 * kXT;   // every pixel of the tile
   }
-  // frames per session: whole batches, <= 2047 terms per cell (a map whose
-  // bounding box is not finite takes the direct path throughout)
-  const int max_frames = cmax > 0 ? (kFixMaxTerms / cmax) / kXB * kXB : 1 << 30;
+  // frames per session: <= 2047 terms per cell (a map whose bounding box is
+  // not finite takes the direct path throughout)
+  const int max_frames = cmax > 0 ? kFixMaxTerms / cmax : 1 << 30;
 
   // accumulator scales
   const double qa_n = 1.0 / a.A.q[0], qa_d = 1.0 / a.A.q[1];
@@ -174,6 +203,7 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
     ofb = a.grid_b[3];
     splat_b = osb > 0 && ofb > 0 && osb * ofb <= a.cap_b;
   }
+  const double n0b = static_cast<double>(a.n0 - dn), m0b = static_cast<double>(a.m0 - dm);
   const double osb1 = static_cast<double>(osb - 1), ofb1 = static_cast<double>(ofb - 1);
   double W2[2], vsc[2], isig[2];
 #pragma unroll
@@ -182,55 +212,53 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
     vsc[e] = live[e] ? W2[e] / Wv[e] : 0.0;                   // (value = I / W) * W^2 per unit I
     isig[e] = (ERR && live[e]) ? 1.0 / a.sigma2[p[e]] : 0.0;  // recon.py:422
   }
+  const TermSink kAn{slo, shi, a.A.num, a.A.num_f};
+  const TermSink kAd{slo + RC, shi + RC, a.A.den, a.A.den_f};
+  const TermSink kBn{slo + 2 * RC, shi + 2 * RC, a.B.num, a.B.num_f};
+  const TermSink kBd{slo + 3 * RC, shi + 3 * RC, a.B.den, a.B.den_f};
   double pix[2] = {0.0, 0.0};
   unsigned long long dropped = 0;
+  // (mode 2: one more cell on each side of a footprint -- the next grid's
+  // positions are rounded separately, recon.py:138 order, and may floor one
+  // cell over)
+  constexpr int kM = MODE == 2 ? 1 : 0;
 
   for (int64_t kc = k_begin; kc < k_end; kc += kXTab) {
     const int nt = static_cast<int>(min((int64_t)kXTab, k_end - kc));
     __syncthreads();
     for (int t = threadIdx.x; t < nt; t += kXT) {
       const int64_t f = a.sc.good[kc + t];
-      t_di[t] = a.di[f];
-      t_dj[t] = a.dj[f];
+      const double dI = a.di[f], dJ = a.dj[f];
+      t_di[t] = dI;
+      t_dj[t] = dJ;
       t_off[t] = f * plane;
+      // the tile's cells for this frame (primary grid; + 1 row / column for
+      // the r0 + 1 / c0 + 1 corners)
+      t_ft[t] = fin ? make_int4(__double2int_rd(umin0 - dI - n0d) - kM,
+                                __double2int_rd(umax0 - dI - n0d) + 1 + kM,
+                                __double2int_rd(umin1 - dJ - m0d) - kM,
+                                __double2int_rd(umax1 - dJ - m0d) + 1 + kM)
+                    : make_int4(0, 1 << 20, 0, 1 << 20);
     }
     __syncthreads();
-    // footprint of the tile for frame t (primary-grid cells, the +1 row /
-    // column holds the r0 + 1 / c0 + 1 corners)
-    // (mode 2: one more cell on each side -- the next grid's positions are
-    // rounded separately, recon.py:138 order, and may floor one cell over)
-    constexpr int kM = MODE == 2 ? 1 : 0;
-    auto foot = [&](int t, int& r0, int& r1, int& c0, int& c1) {
-      r0 = ifloor(umin0 - t_di[t] - n0d) - kM;
-      r1 = ifloor(umax0 - t_di[t] - n0d) + 1 + kM;
-      c0 = ifloor(umin1 - t_dj[t] - m0d) - kM;
-      c1 = ifloor(umax1 - t_dj[t] - m0d) + 1 + kM;
-    };
     for (int s0 = 0; s0 < nt;) {
-      int R0 = 1 << 30, R1 = -(1 << 30), C0 = 1 << 30, C1 = -(1 << 30);
-      auto add_batch = [&](int bb, int& r0, int& r1, int& c0, int& c1) {
-        const int nf = min(kXB, nt - bb);
-        for (int f = 0; f < nf; ++f) {
-          int x0, x1, y0, y1;
-          foot(bb + f, x0, x1, y0, y1);
-          r0 = min(r0, x0); r1 = max(r1, x1); c0 = min(c0, y0); c1 = max(c1, y1);
-        }
-        return nf;
-      };
-      int s1 = s0 + add_batch(s0, R0, R1, C0, C1);
+      // session: consecutive frames whose joint footprint fits the region
+      int4 fb = t_ft[s0];
+      int s1 = s0 + 1;
       const bool region = fin && max_frames > 0 &&
-                          (int64_t)(R1 - R0 + 1) * (C1 - C0 + 1) <= RC;
+                          (int64_t)(fb.y - fb.x + 1) * (fb.w - fb.z + 1) <= RC;
       if (region) {
-        while (s1 < nt && s1 - s0 + kXB <= max_frames) {
-          int r0 = R0, r1 = R1, c0 = C0, c1 = C1;
-          const int nf = add_batch(s1, r0, r1, c0, c1);
-          if ((int64_t)(r1 - r0 + 1) * (c1 - c0 + 1) > RC) break;
-          R0 = r0; R1 = r1; C0 = c0; C1 = c1;
-          s1 += nf;
+        while (s1 < nt && s1 - s0 < max_frames) {
+          const int4 g = t_ft[s1];
+          const int4 u = make_int4(min(fb.x, g.x), max(fb.y, g.y), min(fb.z, g.z), max(fb.w, g.w));
+          if ((int64_t)(u.y - u.x + 1) * (u.w - u.z + 1) > RC) break;
+          fb = u;
+          ++s1;
         }
       }
-      const int nc = region ? C1 - C0 + 1 : 0;
-      const int ncell = region ? (R1 - R0 + 1) * nc : 0;
+      const int R0 = fb.x, C0 = fb.z;
+      const int nc = region ? fb.w - fb.z + 1 : 0;
+      const int ncell = region ? (fb.y - fb.x + 1) * nc : 0;
       if (region) {
         for (int i = threadIdx.x; i < ncell; i += kXT) {
 #pragma unroll
@@ -238,12 +266,10 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
             slo[v * RC + i] = 0u;
             shi[v * RC + i] = 0;
           }
-          stc[i] = 0;
-          stc[RC + i] = 0;
         }
         __syncthreads();
       }
-      // ---- the session's samples, batch by batch
+      // ---- the session's samples, up to kXB frames at a time
       for (int bb = s0; bb < s1; bb += kXB) {
         const int nf = min(kXB, s1 - bb);
         float Iv[kXB][2];
@@ -256,19 +282,19 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
 #pragma unroll
         for (int f = 0; f < kXB; ++f) {
           ef[f] = 0.0;
+          if (f >= nf) continue;
+          const int t = bb + f;
+          const double dI = t_di[t], dJ = t_dj[t];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const bool act = live[e] && f < nf;
-            const int t = bb + (f < nf ? f : 0);
-            const double x = act ? u0[e] - t_di[t] - n0d : 0.0;      // recon.py:138, 418
-            const double y = act ? u1[e] - t_dj[t] - m0d : 0.0;
+            const bool act = live[e];
+            const double x = u0[e] - dI - n0d;                // recon.py:138, 418
+            const double y = u1[e] - dJ - m0d;
             const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
-            const double xf = floor(x), yf = floor(y);
-            const double fx = x - xf, fy = y - yf;
-            const int r0 = static_cast<int>(xf), c0 = static_cast<int>(yf);
+            const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
+            const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
             const double gx = 1.0 - fx, gy = 1.0 - fy;
             const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
-            const bool cok[4] = {true, fy > 0.0, fx > 0.0, fx > 0.0 && fy > 0.0};
             const double I = static_cast<double>(Iv[f][e]);
             double sAn, sAd;
             if (ERR) {
@@ -304,77 +330,41 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
               sAd = W2[e] * qa_d;
             }
-            bool inB = false;
-            double sBn = 0.0, sBd = 0.0;
-            double cwb[4] = {0.0, 0.0, 0.0, 0.0};
-            bool cokb[4] = {false, false, false, false};
-            int r0b = 0, c0b = 0;
+            if (inA) {
+              const int l = (r0 - R0) * nc + (c0 - C0);
+              const int64_t cell = (int64_t)r0 * a.of + c0;
+              const int dl[4] = {0, 1, nc, nc + 1};
+              const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                add_term(kAn, region, l + dl[q], cell + dcell[q], sAn, cw[q]);
+                add_term(kAd, region, l + dl[q], cell + dcell[q], sAd, cw[q]);
+                if (!ERR && cw[q] < kFineW && cw[q] > 0.0 && a.A.touched)
+                  a.A.touched[cell + dcell[q]] = 1;
+              }
+            }
             if (MODE == 2) {
               // the next object's own position, as make_reference computes it
               // (recon.py:138: u - d - origin), so the terms equal a separate
               // object formation bit for bit
-              const double xb = act ? u0[e] - t_di[t] - static_cast<double>(a.n0 - dn) : 0.0;
-              const double yb = act ? u1[e] - t_dj[t] - static_cast<double>(a.m0 - dm) : 0.0;
-              inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
-              const double xbf = floor(xb), ybf = floor(yb);
-              const double fxb = xb - xbf, fyb = yb - ybf;
-              r0b = static_cast<int>(xbf);
-              c0b = static_cast<int>(ybf);
-              const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
-              cwb[0] = gxb * gyb; cwb[1] = gxb * fyb; cwb[2] = fxb * gyb; cwb[3] = fxb * fyb;
-              cokb[0] = true; cokb[1] = fyb > 0.0; cokb[2] = fxb > 0.0; cokb[3] = fxb > 0.0 && fyb > 0.0;
-              sBn = I * vsc[e] * qb_n;
-              sBd = W2[e] * qb_d;
-            }
-            const int dl[4] = {0, 1, nc, nc + 1};
-            const int dc_[4] = {0, 1, 0, 1}, dr_[4] = {0, 0, 1, 1};
-            const int l = (r0 - R0) * nc + (c0 - C0);
-            // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
-            const int lb = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
+              const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
+              const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
+              if (inB) {
+                const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
+                const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
+                const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
+                const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
+                const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
+                // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
+                const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
+                const int64_t cell = (int64_t)r0b * ofb + c0b;
+                const int dl[4] = {0, 1, nc, nc + 1};
+                const int64_t dcell[4] = {0, 1, ofb, ofb + 1};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const bool okA = inA && cok[q];
-              const bool okB = inB && cokb[q];
-              if (!okA && !okB) continue;
-              unsigned lo;
-              int hi;
-              if (region) {
-                const int li = l + dl[q];
-                if (okA) {
-                  fix_limbs(sAn, cw[q], lo, hi);
-                  atomicAdd(&slo[li], lo);
-                  atomicAdd(&shi[li], hi);
-                  fix_limbs(sAd, cw[q], lo, hi);
-                  atomicAdd(&slo[RC + li], lo);
-                  atomicAdd(&shi[RC + li], hi);
-                  if (!ERR) stc[li] = 1;
-                }
-                if (MODE == 2 && okB) {
-                  const int lib = lb + dl[q];
-                  fix_limbs(sBn, cwb[q], lo, hi);
-                  atomicAdd(&slo[2 * RC + lib], lo);
-                  atomicAdd(&shi[2 * RC + lib], hi);
-                  fix_limbs(sBd, cwb[q], lo, hi);
-                  atomicAdd(&slo[3 * RC + lib], lo);
-                  atomicAdd(&shi[3 * RC + lib], hi);
-                  stc[RC + lib] = 1;
-                }
-              } else {     // direct: the same integers straight into the int64 images
-                if (okA) {
-                  const int64_t cell = (int64_t)(r0 + dr_[q]) * a.of + (c0 + dc_[q]);
-                  atomicAdd(reinterpret_cast<unsigned long long*>(a.A.num + cell),
-                            static_cast<unsigned long long>(fix_value(sAn, cw[q])));
-                  atomicAdd(reinterpret_cast<unsigned long long*>(a.A.den + cell),
-                            static_cast<unsigned long long>(fix_value(sAd, cw[q])));
-                  if (!ERR && a.A.touched) a.A.touched[cell] = 1;
-                }
-                if (MODE == 2 && okB) {
-                  const int64_t cell = (int64_t)(r0b + dr_[q]) * ofb + (c0b + dc_[q]);
-                  atomicAdd(reinterpret_cast<unsigned long long*>(a.B.num + cell),
-                            static_cast<unsigned long long>(fix_value(sBn, cwb[q])));
-                  atomicAdd(reinterpret_cast<unsigned long long*>(a.B.den + cell),
-                            static_cast<unsigned long long>(fix_value(sBd, cwb[q])));
-                  if (a.B.touched) a.B.touched[cell] = 1;
+                for (int q = 0; q < 4; ++q) {
+                  add_term(kBn, region, l + dl[q], cell + dcell[q], sBn, cwb[q]);
+                  add_term(kBd, region, l + dl[q], cell + dcell[q], sBd, cwb[q]);
+                  if (cwb[q] < kFineW && cwb[q] > 0.0 && a.B.touched) a.B.touched[cell + dcell[q]] = 1;
                 }
               }
             }
@@ -403,24 +393,18 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
           const int r = R0 + i / nc, c = C0 + i % nc;
           const long long vn = fix_join(slo[i], shi[i]);
           const long long vd = fix_join(slo[RC + i], shi[RC + i]);
-          if (vn != 0 || vd != 0 || (!ERR && stc[i])) {
+          if (vn != 0 || vd != 0) {
             const int64_t cell = (int64_t)r * of + c;
-            if (vn) atomicAdd(reinterpret_cast<unsigned long long*>(a.A.num + cell),
-                              static_cast<unsigned long long>(vn));
-            if (vd) atomicAdd(reinterpret_cast<unsigned long long*>(a.A.den + cell),
-                              static_cast<unsigned long long>(vd));
-            if (!ERR && stc[i] && a.A.touched) a.A.touched[cell] = 1;
+            if (vn) red64(a.A.num + cell, vn);
+            if (vd) red64(a.A.den + cell, vd);
           }
           if (MODE == 2) {
             const long long wn = fix_join(slo[2 * RC + i], shi[2 * RC + i]);
             const long long wd = fix_join(slo[3 * RC + i], shi[3 * RC + i]);
-            if (wn != 0 || wd != 0 || stc[RC + i]) {
+            if (wn != 0 || wd != 0) {
               const int64_t cell = (int64_t)(r + dn) * ofb + (c + dm);
-              if (wn) atomicAdd(reinterpret_cast<unsigned long long*>(a.B.num + cell),
-                                static_cast<unsigned long long>(wn));
-              if (wd) atomicAdd(reinterpret_cast<unsigned long long*>(a.B.den + cell),
-                                static_cast<unsigned long long>(wd));
-              if (stc[RC + i] && a.B.touched) a.B.touched[cell] = 1;
+              if (wn) red64(a.B.num + cell, wn);
+              if (wd) red64(a.B.den + cell, wd);
             }
           }
         }
@@ -534,29 +518,29 @@ __global__ void k_quanta(const double* __restrict__ absmax, const double* __rest
 // ---------------------------------------------------------------------------
 // finish
 // ---------------------------------------------------------------------------
-// Normalise (interp.py:126-135): out = num/den where den > 0 else 0.  The
-// object's validity is "a positive-weight term landed" (touched); a cell
-// whose whole weight rounds below one quantum (< 2^-42 of the largest
-// possible term) keeps that validity with value 0 and wsum = q/2^32.
-__global__ void k_fix_finish(const long long* __restrict__ num, const long long* __restrict__ den,
-                             const uint8_t* __restrict__ touched, const double* __restrict__ q,
-                             const int64_t* __restrict__ grid, int64_t n, double* out,
+// Normalise (interp.py:126-135): out = num/den where den > 0 else 0, with
+// num = num q + num_f q 2^-30 (likewise den).  The object's validity is "a
+// positive-weight term landed": den > 0, or a tiny-weight term marked the
+// cell (touched) -- such a cell whose weight rounds to zero keeps valid = 1
+// with value 0 and wsum = q 2^-62.
+__global__ void k_fix_finish(FixAcc acc, const int64_t* __restrict__ grid, int64_t n, double* out,
                              double* wsum, float* fm, uint8_t* valid) {
   if (grid) {
     const int64_t gn = grid[2] * grid[3];
     if (!(grid[2] > 0 && grid[3] > 0)) return;
     n = gn < n ? gn : n;
   }
-  const double qn = q[0], qd = q[1];
+  const double qn = acc.q[0], qd = acc.q[1];
+  const double qnf = qn * 0x1p-30, qdf = qd * 0x1p-30;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const long long d = den[i];
-    const bool pos = d > 0;
-    const bool ok = touched ? (touched[i] != 0) : pos;
-    const double dd = static_cast<double>(d) * qd;
-    const double v = pos ? (static_cast<double>(num[i]) * qn) / dd : 0.0;
+    const double d = static_cast<double>(acc.den[i]) * qd + static_cast<double>(acc.den_f[i]) * qdf;
+    const double nm = static_cast<double>(acc.num[i]) * qn + static_cast<double>(acc.num_f[i]) * qnf;
+    const bool pos = d > 0.0;
+    const bool ok = pos || (acc.touched && acc.touched[i] != 0);
+    const double v = pos ? nm / d : 0.0;
     if (out) out[i] = v;
-    if (wsum) wsum[i] = pos ? dd : (ok ? qd * 0x1p-32 : 0.0);
+    if (wsum) wsum[i] = pos ? d : (ok ? qd * 0x1p-62 : 0.0);
     if (fm) fm[i] = ok ? static_cast<float>(v) : 0.f;
     if (valid) valid[i] = ok ? 1 : 0;
   }
@@ -667,8 +651,7 @@ template int launch_fix_pass<2>(FixArgs&, int*, cudaStream_t);
 int launch_fix_finish(const FixAcc& acc, const int64_t* grid, int64_t n, double* out, double* wsum,
                       float* fm, uint8_t* valid, cudaStream_t s) {
   if (n <= 0) return PXST_OK;
-  k_fix_finish<<<grid_1d(n, 256), 256, 0, s>>>(acc.num, acc.den, acc.touched, acc.q, grid, n, out,
-                                               wsum, fm, valid);
+  k_fix_finish<<<grid_1d(n, 256), 256, 0, s>>>(acc, grid, n, out, wsum, fm, valid);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
 }

@@ -70,12 +70,24 @@ __host__ __device__ inline int fix_headroom(int64_t n_good) {
   return k;
 }
 
-// Device accumulator pair (num, den) of one image, int64 in units of the
-// quanta q[0] (num) and q[1] (den); touched (nullable) = a term of positive
-// weight landed on the cell (the reference's wsum > 0, data_model.py:186-188).
+// Terms whose bilinear corner weight is below kFineW are summed apart, in
+// units of q * 2^-kFineShift (a single int64 per term: |t| < 2^(41-10+30)):
+// a cell reached only by tiny-weight corners (e.g. the grid's last row,
+// weighted by the fractions of the outermost samples) keeps ~30 more bits.
+// Such corners are rare (a fraction < 2^-10), so they go straight to global
+// memory.
+constexpr double kFineW = 1.0 / 1024.0;
+constexpr int kFineShift = 30;
+
+// Device accumulators of one image, int64: num / den in units of the quanta
+// q[0] / q[1], num_f / den_f in units of q * 2^-kFineShift; touched
+// (nullable) = a tiny-weight term landed (so that a cell whose whole weight
+// rounds to zero stays valid: the reference's wsum > 0, data_model.py:186).
 struct FixAcc {
   long long* num;
   long long* den;
+  long long* num_f;
+  long long* den_f;
   uint8_t* touched;
   const double* q;
 };

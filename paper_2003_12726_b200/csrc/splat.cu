@@ -83,13 +83,15 @@ int check_scan(const pxst_scan* sc);
 using namespace pxst;
 
 static int check_accum(const pxst_accum* acc) {
-  PXST_REQUIRE(acc && acc->num && acc->den && acc->quanta, "bad accumulator");
+  PXST_REQUIRE(acc && acc->num && acc->den && acc->num_fine && acc->den_fine && acc->quanta,
+               "bad accumulator");
   return PXST_OK;
 }
 
 static FixAcc fix_acc(const pxst_accum* acc) {
   return FixAcc{reinterpret_cast<long long*>(acc->num), reinterpret_cast<long long*>(acc->den),
-                acc->touched, acc->quanta};
+                reinterpret_cast<long long*>(acc->num_fine),
+                reinterpret_cast<long long*>(acc->den_fine), acc->touched, acc->quanta};
 }
 
 extern "C" int pxst_stack_absmax(const pxst_scan* sc, double* out, void* stream) {
@@ -137,17 +139,18 @@ extern "C" int pxst_object_map(const pxst_scan* sc, const double* u,
   cudaStream_t s = as_stream(stream);
   const int64_t n = os * of;
   Scratch buf;
-  if (int e = buf.alloc(sizeof(int64_t) * 2 * n + n + 4 * sizeof(double) + 16, s)) return e;
+  if (int e = buf.alloc(sizeof(int64_t) * 4 * n + n + 4 * sizeof(double) + 16, s)) return e;
   int64_t* num = buf.as<int64_t>();
-  double* q = reinterpret_cast<double*>(num + 2 * n);
+  double* q = reinterpret_cast<double*>(num + 4 * n);
   double* amax = q + 2;
   uint8_t* touched = reinterpret_cast<uint8_t*>(q + 4);
-  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 2 * n, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(num, 0, sizeof(int64_t) * 4 * n, s));
   PXST_CHECK_CUDA(cudaMemsetAsync(touched, 0, n, s));
   if (int e = launch_abs_max(sc, amax, s)) return e;
   if (int e = launch_quanta(sc, amax, nullptr, nullptr, 0, q, s)) return e;
   const FixAcc acc{reinterpret_cast<long long*>(num), reinterpret_cast<long long*>(num + n),
-                   touched, q};
+                   reinterpret_cast<long long*>(num + 2 * n),
+                   reinterpret_cast<long long*>(num + 3 * n), touched, q};
   if (int e = launch_object_fix(sc, u, di, dj, n0, m0, os, of, 0, sc->n_good, acc, nullptr, s))
     return e;
   return launch_fix_finish(acc, nullptr, n, i_ref, wsum, fm, valid, s);

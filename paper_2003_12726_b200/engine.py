@@ -134,12 +134,13 @@ _SOLVERS = {"cg": 0, "mgcg": 1}
 
 class Accum:
     """Deterministic splat accumulators on the device (``pxst_accum``): int64
-    numerator / denominator [2, cells] in units of the device quanta
-    (float64[2]) and the touched flags (uint8, optional).  Frame shards add
-    ``data`` exactly (int64 all-reduce) and ``touched`` with max."""
+    [4, cells] = numerator, denominator (units of the device quanta,
+    float64[2]) and their tiny-weight parts (units of quanta * 2^-30), plus
+    the touched flags (uint8, optional).  Frame shards add ``data`` exactly
+    (int64 all-reduce) and ``touched`` with max."""
 
     def __init__(self, cells: int, quanta: torch.Tensor, device, touched: bool = True):
-        self.data = torch.zeros((2, cells), dtype=torch.int64, device=device)
+        self.data = torch.zeros((4, cells), dtype=torch.int64, device=device)
         self.touched = torch.zeros(cells, dtype=torch.uint8, device=device) if touched else None
         self.quanta = quanta
 
@@ -148,8 +149,8 @@ class Accum:
         return int(self.data.shape[1])
 
     def c(self) -> PxstAccum:
-        return PxstAccum(self.data[0].data_ptr(), self.data[1].data_ptr(), _ptr(self.touched),
-                         self.quanta.data_ptr())
+        return PxstAccum(self.data[0].data_ptr(), self.data[1].data_ptr(), self.data[2].data_ptr(),
+                         self.data[3].data_ptr(), _ptr(self.touched), self.quanta.data_ptr())
 
 
 def _grid_rule(b) -> tuple[int, int, tuple[int, int]]:
