@@ -88,8 +88,8 @@ __device__ __forceinline__ void add_term(const TermSink& k, bool region, int li,
     } else {
       red64(k.g + cell, fix_value(scaled, w));
     }
-  } else if (w > 0.0) {
-    red64(k.gf + cell, fix_value(scaled * 0x1p30, w));
+  } else if (w > 0.0) {     // |t| < 2^61 fine quanta: a full-range rounding conversion
+    red64(k.gf + cell, __double2ll_rn(scaled * 0x1p30 * w));
   }
 }
 
