@@ -120,7 +120,7 @@ int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const do
 typedef struct pxst_accum {
   int64_t* num;           /* [cells], units of quanta[0]                        */
   int64_t* den;           /* [cells], units of quanta[1]                        */
-  int64_t* num_fine;      /* [cells], units of quanta[0] * 2^-30: terms whose   */
+  int64_t* num_fine;      /* [cells], units of quanta[0] * 2^-20: terms whose   */
   int64_t* den_fine;      /*   bilinear corner weight is < 2^-10 (cells reached */
                           /*   only by tiny-weight corners keep their precision)*/
   uint8_t* touched;       /* [cells] or NULL: a tiny-weight term landed         */

@@ -21,6 +21,8 @@
 // recon.py:414-431); 2 = mode 1 fused with the next iteration's object
 // splat (same samples, positions relative to the next grid read from the
 // device, recon.py:504-516).
+#include <stdlib.h>
+
 #include "fixsplat.cuh"
 
 namespace pxst {
@@ -30,8 +32,11 @@ constexpr int kXR = 16, kXC = 32, kXT = 256, kXW = kXT / 32;  // tile, threads, 
 constexpr int kXB = 8;        // frames per batch
 constexpr int kXTab = 256;    // frames per shared frame-table chunk (multiple of kXB)
 
+// Region values: mode 0 object num, den; modes 1, 2 plane num, den, plane
+// num fine band (see add_plane_num); mode 2 adds the next object's num, den.
 template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 3072; };
-template <> struct FixCfg<2> { static constexpr int NV = 4, RC = 2048; };
+template <> struct FixCfg<1> { static constexpr int NV = 3, RC = 3072; };
+template <> struct FixCfg<2> { static constexpr int NV = 5, RC = 2048; };
 
 template <int MODE>
 constexpr size_t fix_smem_bytes() {
@@ -58,6 +63,8 @@ struct FixArgs {
   double* part;                // [n_good][n_cta] per-frame eps sums of each CTA
   int64_t n_cta;
   unsigned long long* n_drop;  // mode 0, nullable: out-of-grid samples
+  double fine_w;               // corner weights below go to the fine image (kFineW)
+  int no_region;               // debug: every term straight to global memory
 };
 
 namespace {
@@ -77,8 +84,8 @@ struct TermSink {
 };
 
 __device__ __forceinline__ void add_term(const TermSink& k, bool region, int li, int64_t cell,
-                                         double scaled, double w) {
-  if (w >= kFineW) {
+                                         double scaled, double w, double fine_w) {
+  if (w >= fine_w) {
     if (region) {
       unsigned lo;
       int hi;
@@ -88,8 +95,22 @@ __device__ __forceinline__ void add_term(const TermSink& k, bool region, int li,
     } else {
       red64(k.g + cell, fix_value(scaled, w));
     }
-  } else if (w > 0.0) {     // |t| < 2^61 fine quanta: a full-range rounding conversion
-    red64(k.gf + cell, __double2ll_rn(scaled * 0x1p30 * w));
+  } else if (w > 0.0) {     // |t| < 2^51 fine quanta
+    red64(k.gf + cell, fix_value(scaled * 0x1p20, w));
+  }
+}
+
+// The plane numerator eps * w_c: eps is bounded loosely (pxst_plane_quanta:
+// (max|I| + max W max|ref|)^2 / min sigma^2, often 10^4 x the typical eps),
+// so a term below 2^21 coarse quanta goes to a second band in units of
+// q * 2^-20 (the fine image) and keeps >= 20 significant bits.
+__device__ __forceinline__ void add_plane_num(const TermSink& k, const TermSink& band,
+                                              bool region, int li, int64_t cell, double scaled,
+                                              double w, double fine_w) {
+  if (w >= fine_w && fabs(scaled * w) < 2097152.0) {
+    add_term(band, region, li, cell, scaled * 0x1p20, w, 0.0);   // band's "coarse" = fine image
+  } else {
+    add_term(k, region, li, cell, scaled, w, fine_w);
   }
 }
 
@@ -216,6 +237,8 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   const TermSink kAd{slo + RC, shi + RC, a.A.den, a.A.den_f};
   const TermSink kBn{slo + 2 * RC, shi + 2 * RC, a.B.num, a.B.num_f};
   const TermSink kBd{slo + 3 * RC, shi + 3 * RC, a.B.den, a.B.den_f};
+  constexpr int kBandV = MODE == 2 ? 4 : 2;        // the plane numerator's fine band
+  const TermSink kAnB{slo + kBandV * RC, shi + kBandV * RC, a.A.num_f, nullptr};
   double pix[2] = {0.0, 0.0};
   unsigned long long dropped = 0;
   // (mode 2: one more cell on each side of a footprint -- the next grid's
@@ -245,7 +268,7 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
       // session: consecutive frames whose joint footprint fits the region
       int4 fb = t_ft[s0];
       int s1 = s0 + 1;
-      const bool region = fin && max_frames > 0 &&
+      const bool region = fin && max_frames > 0 && !a.no_region &&
                           (int64_t)(fb.y - fb.x + 1) * (fb.w - fb.z + 1) <= RC;
       if (region) {
         while (s1 < nt && s1 - s0 < max_frames) {
@@ -337,9 +360,12 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                add_term(kAn, region, l + dl[q], cell + dcell[q], sAn, cw[q]);
-                add_term(kAd, region, l + dl[q], cell + dcell[q], sAd, cw[q]);
-                if (!ERR && cw[q] < kFineW && cw[q] > 0.0 && a.A.touched)
+                if (ERR)
+                  add_plane_num(kAn, kAnB, region, l + dl[q], cell + dcell[q], sAn, cw[q], a.fine_w);
+                else
+                  add_term(kAn, region, l + dl[q], cell + dcell[q], sAn, cw[q], a.fine_w);
+                add_term(kAd, region, l + dl[q], cell + dcell[q], sAd, cw[q], a.fine_w);
+                if (!ERR && cw[q] < a.fine_w && cw[q] > 0.0 && a.A.touched)
                   a.A.touched[cell + dcell[q]] = 1;
               }
             }
@@ -362,9 +388,9 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
                 const int64_t dcell[4] = {0, 1, ofb, ofb + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  add_term(kBn, region, l + dl[q], cell + dcell[q], sBn, cwb[q]);
-                  add_term(kBd, region, l + dl[q], cell + dcell[q], sBd, cwb[q]);
-                  if (cwb[q] < kFineW && cwb[q] > 0.0 && a.B.touched) a.B.touched[cell + dcell[q]] = 1;
+                  add_term(kBn, region, l + dl[q], cell + dcell[q], sBn, cwb[q], a.fine_w);
+                  add_term(kBd, region, l + dl[q], cell + dcell[q], sBd, cwb[q], a.fine_w);
+                  if (cwb[q] < a.fine_w && cwb[q] > 0.0 && a.B.touched) a.B.touched[cell + dcell[q]] = 1;
                 }
               }
             }
@@ -397,6 +423,10 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
             const int64_t cell = (int64_t)r * of + c;
             if (vn) red64(a.A.num + cell, vn);
             if (vd) red64(a.A.den + cell, vd);
+          }
+          if (ERR) {
+            const long long vb = fix_join(slo[kBandV * RC + i], shi[kBandV * RC + i]);
+            if (vb) red64(a.A.num_f + (int64_t)r * of + c, vb);
           }
           if (MODE == 2) {
             const long long wn = fix_join(slo[2 * RC + i], shi[2 * RC + i]);
@@ -519,7 +549,7 @@ __global__ void k_quanta(const double* __restrict__ absmax, const double* __rest
 // finish
 // ---------------------------------------------------------------------------
 // Normalise (interp.py:126-135): out = num/den where den > 0 else 0, with
-// num = num q + num_f q 2^-30 (likewise den).  The object's validity is "a
+// num = num q + num_f q 2^-20 (likewise den).  The object's validity is "a
 // positive-weight term landed": den > 0, or a tiny-weight term marked the
 // cell (touched) -- such a cell whose weight rounds to zero keeps valid = 1
 // with value 0 and wsum = q 2^-62.
@@ -531,7 +561,7 @@ __global__ void k_fix_finish(FixAcc acc, const int64_t* __restrict__ grid, int64
     n = gn < n ? gn : n;
   }
   const double qn = acc.q[0], qd = acc.q[1];
-  const double qnf = qn * 0x1p-30, qdf = qd * 0x1p-30;
+  const double qnf = qn * 0x1p-20, qdf = qd * 0x1p-20;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double d = static_cast<double>(acc.den[i]) * qd + static_cast<double>(acc.den_f[i]) * qdf;
@@ -582,6 +612,9 @@ int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma
 
 template <int MODE>
 int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
+  a.fine_w = kFineW;
+  if (const char* v = getenv("PXST_FIX_FINE_W")) a.fine_w = atof(v);
+  if (const char* v = getenv("PXST_FIX_NO_REGION")) a.no_region = v[0] == '1';
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2], rw = a.sc.roi[1] - a.sc.roi[0];
   dim3 g((unsigned)((cw + kXC - 1) / kXC), (unsigned)((rw + kXR - 1) / kXR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
@@ -622,7 +655,7 @@ int fix_pass_slices(const pxst_scan* sc, int64_t nk, int mode, int64_t* n_cta) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = mode == 2 ? fix_smem_bytes<2>() : fix_smem_bytes<0>();
+  const size_t smem = mode == 2 ? fix_smem_bytes<2>() : mode == 1 ? fix_smem_bytes<1>() : fix_smem_bytes<0>();
   if (mode == 2) {
     cudaFuncSetAttribute(k_fix_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<2>, kXT, smem);

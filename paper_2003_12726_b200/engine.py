@@ -135,7 +135,7 @@ _SOLVERS = {"cg": 0, "mgcg": 1}
 class Accum:
     """Deterministic splat accumulators on the device (``pxst_accum``): int64
     [4, cells] = numerator, denominator (units of the device quanta,
-    float64[2]) and their tiny-weight parts (units of quanta * 2^-30), plus
+    float64[2]) and their tiny-weight parts (units of quanta * 2^-20), plus
     the touched flags (uint8, optional).  Frame shards add ``data`` exactly
     (int64 all-reduce) and ``touched`` with max."""
 
