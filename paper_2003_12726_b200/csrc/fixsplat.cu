@@ -23,6 +23,8 @@
 // device, recon.py:504-516).
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "fixsplat.cuh"
 
 namespace pxst {
@@ -33,7 +35,7 @@ constexpr int kXB = 8;        // frames per batch
 constexpr int kXTab = 256;    // frames per shared frame-table chunk (multiple of kXB)
 
 // Region values: mode 0 object num, den; modes 1, 2 plane num, den, plane
-// num fine band (see add_plane_num); mode 2 adds the next object's num, den.
+// num fine band (see plane_band); mode 2 adds the next object's num, den.
 template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 3072; };
 template <> struct FixCfg<1> { static constexpr int NV = 3, RC = 3072; };
 template <> struct FixCfg<2> { static constexpr int NV = 5, RC = 2048; };
@@ -63,8 +65,7 @@ struct FixArgs {
   double* part;                // [n_good][n_cta] per-frame eps sums of each CTA
   int64_t n_cta;
   unsigned long long* n_drop;  // mode 0, nullable: out-of-grid samples
-  double fine_w;               // corner weights below go to the fine image (kFineW)
-  int no_region;               // debug: every term straight to global memory
+  int no_region;               // debug (PXST_FIX_NO_REGION=1): every term straight to global memory
 };
 
 namespace {
@@ -83,35 +84,30 @@ struct TermSink {
   long long* gf;      // global fine image
 };
 
-__device__ __forceinline__ void add_term(const TermSink& k, bool region, int li, int64_t cell,
-                                         double scaled, double w, double fine_w) {
-  if (w >= fine_w) {
-    if (region) {
-      unsigned lo;
-      int hi;
-      fix_limbs(scaled, w, lo, hi);
-      atomicAdd(k.lo + li, lo);
-      atomicAdd(k.hi + li, hi);
-    } else {
-      red64(k.g + cell, fix_value(scaled, w));
-    }
-  } else if (w > 0.0) {     // |t| < 2^51 fine quanta
-    red64(k.gf + cell, fix_value(scaled * 0x1p20, w));
-  }
+// A term into the region's limbs (coarse, corner weight >= kFineW).
+__device__ __forceinline__ void region_term(unsigned* lo_arr, int* hi_arr, int li, double scaled,
+                                            double w) {
+  unsigned lo;
+  int hi;
+  fix_limbs(scaled, w, lo, hi);
+  atomicAdd(lo_arr + li, lo);
+  atomicAdd(hi_arr + li, hi);
+}
+
+// A term straight into the global images (no region; and tiny-weight
+// corners, |t| < 2^51 fine quanta).
+__device__ __forceinline__ void global_term(long long* g, long long* gf, int64_t cell,
+                                            double scaled, double w) {
+  if (w >= kFineW) red64(g + cell, fix_value(scaled, w));
+  else if (w > 0.0) red64(gf + cell, fix_value(scaled * 0x1p20, w));
 }
 
 // The plane numerator eps * w_c: eps is bounded loosely (pxst_plane_quanta:
 // (max|I| + max W max|ref|)^2 / min sigma^2, often 10^4 x the typical eps),
-// so a term below 2^21 coarse quanta goes to a second band in units of
-// q * 2^-20 (the fine image) and keeps >= 20 significant bits.
-__device__ __forceinline__ void add_plane_num(const TermSink& k, const TermSink& band,
-                                              bool region, int li, int64_t cell, double scaled,
-                                              double w, double fine_w) {
-  if (w >= fine_w && fabs(scaled * w) < 2097152.0) {
-    add_term(band, region, li, cell, scaled * 0x1p20, w, 0.0);   // band's "coarse" = fine image
-  } else {
-    add_term(k, region, li, cell, scaled, w, fine_w);
-  }
+// so a coarse-weight term below 2^21 coarse quanta goes to a second band in
+// units of q * 2^-20 (the fine image) and keeps >= 20 significant bits.
+__device__ __forceinline__ bool plane_band(double scaled, double w) {
+  return fabs(scaled * w) < 2097152.0;
 }
 
 template <int MODE>
@@ -292,126 +288,180 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
         }
         __syncthreads();
       }
-      // ---- the session's samples, up to kXB frames at a time
-      for (int bb = s0; bb < s1; bb += kXB) {
-        const int nf = min(kXB, s1 - bb);
-        float Iv[kXB][2];
+      // ---- the session's samples, up to kXB frames at a time (the region /
+      // direct choice is uniform over the session: two compiled bodies)
+      auto session = [&](auto region_c) {
+        constexpr bool REG = decltype(region_c)::value;
+        for (int bb = s0; bb < s1; bb += kXB) {
+          const int nf = min(kXB, s1 - bb);
+          float Iv[kXB][2];
 #pragma unroll
-        for (int f = 0; f < kXB; ++f)
+          for (int f = 0; f < kXB; ++f)
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            Iv[f][e] = (live[e] && f < nf) ? __ldg(a.sc.frames + t_off[bb + f] + p[e]) : 0.f;
-        double ef[kXB];
+            for (int e = 0; e < 2; ++e)
+              Iv[f][e] = (live[e] && f < nf) ? __ldg(a.sc.frames + t_off[bb + f] + p[e]) : 0.f;
+          double ef[kXB];
 #pragma unroll
-        for (int f = 0; f < kXB; ++f) {
-          ef[f] = 0.0;
-          if (f >= nf) continue;
-          const int t = bb + f;
-          const double dI = t_di[t], dJ = t_dj[t];
+          for (int f = 0; f < kXB; ++f) {
+            ef[f] = 0.0;
+            if (f >= nf) continue;
+            const int t = bb + f;
+            const double dI = t_di[t], dJ = t_dj[t];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const bool act = live[e];
-            const double x = u0[e] - dI - n0d;                // recon.py:138, 418
-            const double y = u1[e] - dJ - m0d;
-            const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
-            const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
-            const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
-            const double gx = 1.0 - fx, gy = 1.0 - fy;
-            const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
-            const double I = static_cast<double>(Iv[f][e]);
-            double sAn, sAd;
-            if (ERR) {
-              double eps = 0.0;
-              if (act) {
-                // masked bilinear read (interp.py:53-85) of the grouped reference:
-                // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
-                const double2 z2 = make_double2(0.0, 0.0);
-                const int64_t a00 = (int64_t)r0 * a.of + c0;
-                const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
-                const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
-                const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
-                double den = 0.0, nm = 0.0;
-                bool all = true;
+            for (int e = 0; e < 2; ++e) {
+              const bool act = live[e];
+              const double x = u0[e] - dI - n0d;                // recon.py:138, 418
+              const double y = u1[e] - dJ - m0d;
+              const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
+              const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
+              const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
+              const double gx = 1.0 - fx, gy = 1.0 - fy;
+              const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
+              const double I = static_cast<double>(Iv[f][e]);
+              double sAn, sAd;
+              if (ERR) {
+                double eps = 0.0;
+                if (act) {
+                  // masked bilinear read (interp.py:53-85) of the grouped reference:
+                  // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
+                  const double2 z2 = make_double2(0.0, 0.0);
+                  const int64_t a00 = (int64_t)r0 * a.of + c0;
+                  const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
+                  const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
+                  const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
+                  double den = 0.0, nm = 0.0;
+                  bool all = true;
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const bool m = cv[q] == cv[q];
+                    all = all && m;
+                    den = fma(cw[q], m ? 1.0 : 0.0, den);
+                    nm = fma(cw[q], m ? cv[q] : 0.0, nm);
+                  }
+                  const bool ok = inA && den > 0.0;
+                  const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
+                  const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
+                  eps = (r * r) * isig[e];                                // recon.py:422
+                }
+                pix[e] += eps;
+                ef[f] += eps;
+                sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
+                sAd = qa_d;
+              } else {
+                dropped += (act && !inA) ? 1 : 0;
+                sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
+                sAd = W2[e] * qa_d;
+              }
+              const int64_t cell = (int64_t)r0 * a.of + c0;
+              const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
+              bool tiny = false;             // a corner of weight in (0, kFineW)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) tiny |= inA && cw[q] > 0.0 && cw[q] < kFineW;
+              if (REG) {
+                const int l = (r0 - R0) * nc + (c0 - C0);
+                const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const bool m = cv[q] == cv[q];
-                  all = all && m;
-                  den = fma(cw[q], m ? 1.0 : 0.0, den);
-                  nm = fma(cw[q], m ? cv[q] : 0.0, nm);
+                  if (inA && cw[q] >= kFineW) {
+                    if (ERR) {
+                      const bool band = plane_band(sAn, cw[q]);
+                      region_term(band ? slo + kBandV * RC : slo, band ? shi + kBandV * RC : shi,
+                                  l + dl[q], band ? sAn * 0x1p20 : sAn, cw[q]);
+                    } else {
+                      region_term(slo, shi, l + dl[q], sAn, cw[q]);
+                    }
+                    region_term(slo + RC, shi + RC, l + dl[q], sAd, cw[q]);
+                  }
                 }
-                const bool ok = inA && den > 0.0;
-                const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
-                const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
-                eps = (r * r) * isig[e];                                // recon.py:422
-              }
-              pix[e] += eps;
-              ef[f] += eps;
-              sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
-              sAd = qa_d;
-            } else {
-              dropped += (act && !inA) ? 1 : 0;
-              sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
-              sAd = W2[e] * qa_d;
-            }
-            if (inA) {
-              const int l = (r0 - R0) * nc + (c0 - C0);
-              const int64_t cell = (int64_t)r0 * a.of + c0;
-              const int dl[4] = {0, 1, nc, nc + 1};
-              const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
+                if (tiny) {                  // rare: straight to the fine images
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (ERR)
-                  add_plane_num(kAn, kAnB, region, l + dl[q], cell + dcell[q], sAn, cw[q], a.fine_w);
-                else
-                  add_term(kAn, region, l + dl[q], cell + dcell[q], sAn, cw[q], a.fine_w);
-                add_term(kAd, region, l + dl[q], cell + dcell[q], sAd, cw[q], a.fine_w);
-                if (!ERR && cw[q] < a.fine_w && cw[q] > 0.0 && a.A.touched)
-                  a.A.touched[cell + dcell[q]] = 1;
+                  for (int q = 0; q < 4; ++q)
+                    if (cw[q] > 0.0 && cw[q] < kFineW) {
+                      global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
+                      global_term(a.A.den, a.A.den_f, cell + dcell[q], sAd, cw[q]);
+                      if (!ERR && a.A.touched) a.A.touched[cell + dcell[q]] = 1;
+                    }
+                }
+              } else if (inA) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  if (ERR && cw[q] >= kFineW && plane_band(sAn, cw[q]))
+                    red64(a.A.num_f + cell + dcell[q], fix_value(sAn * 0x1p20, cw[q]));
+                  else
+                    global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
+                  global_term(a.A.den, a.A.den_f, cell + dcell[q], sAd, cw[q]);
+                  if (!ERR && a.A.touched && cw[q] > 0.0 && cw[q] < kFineW)
+                    a.A.touched[cell + dcell[q]] = 1;
+                }
               }
-            }
-            if (MODE == 2) {
-              // the next object's own position, as make_reference computes it
-              // (recon.py:138: u - d - origin), so the terms equal a separate
-              // object formation bit for bit
-              const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
-              const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
-              if (inB) {
+              if (MODE == 2) {
+                // the next object's own position, as make_reference computes it
+                // (recon.py:138: u - d - origin), so the terms equal a separate
+                // object formation bit for bit
+                const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
+                const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
                 const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
                 const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
                 const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
                 const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
                 const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
-                // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
-                const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
-                const int64_t cell = (int64_t)r0b * ofb + c0b;
-                const int dl[4] = {0, 1, nc, nc + 1};
-                const int64_t dcell[4] = {0, 1, ofb, ofb + 1};
+                const int64_t cellb = (int64_t)r0b * ofb + c0b;
+                const int64_t dcb[4] = {0, 1, ofb, ofb + 1};
+                bool tinyb = false;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  add_term(kBn, region, l + dl[q], cell + dcell[q], sBn, cwb[q], a.fine_w);
-                  add_term(kBd, region, l + dl[q], cell + dcell[q], sBd, cwb[q], a.fine_w);
-                  if (cwb[q] < a.fine_w && cwb[q] > 0.0 && a.B.touched) a.B.touched[cell + dcell[q]] = 1;
+                for (int q = 0; q < 4; ++q) tinyb |= inB && cwb[q] > 0.0 && cwb[q] < kFineW;
+                if (REG) {
+                  // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
+                  const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
+                  const int dl[4] = {0, 1, nc, nc + 1};
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    if (inB && cwb[q] >= kFineW) {
+                      region_term(slo + 2 * RC, shi + 2 * RC, l + dl[q], sBn, cwb[q]);
+                      region_term(slo + 3 * RC, shi + 3 * RC, l + dl[q], sBd, cwb[q]);
+                    }
+                  }
+                  if (tinyb) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                      if (cwb[q] > 0.0 && cwb[q] < kFineW) {
+                        global_term(a.B.num, a.B.num_f, cellb + dcb[q], sBn, cwb[q]);
+                        global_term(a.B.den, a.B.den_f, cellb + dcb[q], sBd, cwb[q]);
+                        if (a.B.touched) a.B.touched[cellb + dcb[q]] = 1;
+                      }
+                  }
+                } else if (inB) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    global_term(a.B.num, a.B.num_f, cellb + dcb[q], sBn, cwb[q]);
+                    global_term(a.B.den, a.B.den_f, cellb + dcb[q], sBd, cwb[q]);
+                    if (a.B.touched && cwb[q] > 0.0 && cwb[q] < kFineW) a.B.touched[cellb + dcb[q]] = 1;
+                  }
                 }
               }
             }
           }
-        }
-        if (ERR) {   // per-frame sums: warp, then the CTA's warps in a fixed order
+          if (ERR) {   // per-frame sums: warp, then the CTA's warps in a fixed order
 #pragma unroll
-          for (int f = 0; f < kXB; ++f) {
-            const double sum = warp_sum(ef[f]);
-            if (lane == 0) s_fr[warp][f] = sum;
-          }
-          __syncthreads();
-          if (threadIdx.x < nf) {
-            double sum = 0.0;
+            for (int f = 0; f < kXB; ++f) {
+              const double sum = warp_sum(ef[f]);
+              if (lane == 0) s_fr[warp][f] = sum;
+            }
+            __syncthreads();
+            if (threadIdx.x < nf) {
+              double sum = 0.0;
 #pragma unroll
-            for (int w = 0; w < kXW; ++w) sum += s_fr[w][threadIdx.x];
-            a.part[(kc + bb + threadIdx.x) * a.n_cta + cta] = sum;
+              for (int w = 0; w < kXW; ++w) sum += s_fr[w][threadIdx.x];
+              a.part[(kc + bb + threadIdx.x) * a.n_cta + cta] = sum;
+            }
+            __syncthreads();
           }
-          __syncthreads();
         }
-      }
+      };
+      if (region)
+        session(std::integral_constant<bool, true>{});
+      else
+        session(std::integral_constant<bool, false>{});
       // ---- flush the region into the int64 images
       if (region) {
         __syncthreads();
@@ -612,8 +662,6 @@ int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma
 
 template <int MODE>
 int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
-  a.fine_w = kFineW;
-  if (const char* v = getenv("PXST_FIX_FINE_W")) a.fine_w = atof(v);
   if (const char* v = getenv("PXST_FIX_NO_REGION")) a.no_region = v[0] == '1';
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2], rw = a.sc.roi[1] - a.sc.roi[0];
   dim3 g((unsigned)((cw + kXC - 1) / kXC), (unsigned)((rw + kXR - 1) / kXR));
