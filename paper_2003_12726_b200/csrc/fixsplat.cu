@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
   __shared__ int64_t t_off[kXTab];
   __shared__ int4 t_ft[kXTab];                                      // frame footprints
   __shared__ double s_red[kXW][4];
-  __shared__ double s_fr[kXW][kXB];
+  __shared__ double s_frw[ERR ? kXW : 1][ERR ? kXTab : 1];   // per-frame sums of each warp
   __shared__ int s_cmax;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -288,173 +288,136 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
         }
         __syncthreads();
       }
-      // ---- the session's samples, up to kXB frames at a time (the region /
-      // direct choice is uniform over the session: two compiled bodies)
+      // ---- the session's samples, one frame at a time (the next frame's
+      // stack values in flight); region / direct are two compiled bodies
       auto session = [&](auto region_c) {
         constexpr bool REG = decltype(region_c)::value;
-        for (int bb = s0; bb < s1; bb += kXB) {
-          const int nf = min(kXB, s1 - bb);
-          float Iv[kXB][2];
+        float In[2];
 #pragma unroll
-          for (int f = 0; f < kXB; ++f)
+        for (int e = 0; e < 2; ++e) In[e] = live[e] ? __ldg(a.sc.frames + t_off[s0] + p[e]) : 0.f;
+        for (int t = s0; t < s1; ++t) {
+          const float Ic[2] = {In[0], In[1]};
+          if (t + 1 < s1) {
 #pragma unroll
             for (int e = 0; e < 2; ++e)
-              Iv[f][e] = (live[e] && f < nf) ? __ldg(a.sc.frames + t_off[bb + f] + p[e]) : 0.f;
-          double ef[kXB];
+              In[e] = live[e] ? __ldg(a.sc.frames + t_off[t + 1] + p[e]) : 0.f;
+          }
+          const double dI = t_di[t], dJ = t_dj[t];
+          double ef = 0.0;
 #pragma unroll
-          for (int f = 0; f < kXB; ++f) {
-            ef[f] = 0.0;
-            if (f >= nf) continue;
-            const int t = bb + f;
-            const double dI = t_di[t], dJ = t_dj[t];
+          for (int e = 0; e < 2; ++e) {
+            const bool act = live[e];
+            const double x = u0[e] - dI - n0d;                // recon.py:138, 418
+            const double y = u1[e] - dJ - m0d;
+            const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
+            const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
+            const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
+            const double gx = 1.0 - fx, gy = 1.0 - fy;
+            const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
+            const double I = static_cast<double>(Ic[e]);
+            double sAn, sAd;
+            if (ERR) {
+              double eps = 0.0;
+              if (act) {
+                // masked bilinear read (interp.py:53-85) of the grouped reference:
+                // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
+                const double2 z2 = make_double2(0.0, 0.0);
+                const int64_t a00 = (int64_t)r0 * a.of + c0;
+                const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
+                const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
+                const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
+                double den = 0.0, nm = 0.0;
+                bool all = true;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const bool act = live[e];
-              const double x = u0[e] - dI - n0d;                // recon.py:138, 418
-              const double y = u1[e] - dJ - m0d;
-              const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
-              const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
-              const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
-              const double gx = 1.0 - fx, gy = 1.0 - fy;
-              const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
-              const double I = static_cast<double>(Iv[f][e]);
-              double sAn, sAd;
-              if (ERR) {
-                double eps = 0.0;
-                if (act) {
-                  // masked bilinear read (interp.py:53-85) of the grouped reference:
-                  // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
-                  const double2 z2 = make_double2(0.0, 0.0);
-                  const int64_t a00 = (int64_t)r0 * a.of + c0;
-                  const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
-                  const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
-                  const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
-                  double den = 0.0, nm = 0.0;
-                  bool all = true;
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const bool m = cv[q] == cv[q];
-                    all = all && m;
-                    den = fma(cw[q], m ? 1.0 : 0.0, den);
-                    nm = fma(cw[q], m ? cv[q] : 0.0, nm);
-                  }
-                  const bool ok = inA && den > 0.0;
-                  const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
-                  const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
-                  eps = (r * r) * isig[e];                                // recon.py:422
+                for (int q = 0; q < 4; ++q) {
+                  const bool m = cv[q] == cv[q];
+                  all = all && m;
+                  den = fma(cw[q], m ? 1.0 : 0.0, den);
+                  nm = fma(cw[q], m ? cv[q] : 0.0, nm);
                 }
-                pix[e] += eps;
-                ef[f] += eps;
-                sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
-                sAd = qa_d;
-              } else {
-                dropped += (act && !inA) ? 1 : 0;
-                sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
-                sAd = W2[e] * qa_d;
+                const bool ok = inA && den > 0.0;
+                const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
+                const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
+                eps = (r * r) * isig[e];                                // recon.py:422
               }
+              pix[e] += eps;
+              ef += eps;
+              sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
+              sAd = qa_d;
+            } else {
+              dropped += (act && !inA) ? 1 : 0;
+              sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
+              sAd = W2[e] * qa_d;
+            }
+            // hot path: every corner weight >= kFineW (the others, and the
+            // direct sessions, take the per-corner path below)
+            const bool hot = REG && cw[0] >= kFineW && cw[1] >= kFineW && cw[2] >= kFineW &&
+                             cw[3] >= kFineW;
+            if (inA && hot) {
+              const int l = (r0 - R0) * nc + (c0 - C0);
+              const int dl[4] = {0, 1, nc, nc + 1};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (ERR) {
+                  const bool band = plane_band(sAn, cw[q]);
+                  region_term(band ? slo + kBandV * RC : slo, band ? shi + kBandV * RC : shi,
+                              l + dl[q], band ? sAn * 0x1p20 : sAn, cw[q]);
+                } else {
+                  region_term(slo, shi, l + dl[q], sAn, cw[q]);
+                }
+                region_term(slo + RC, shi + RC, l + dl[q], sAd, cw[q]);
+              }
+            } else if (inA) {
               const int64_t cell = (int64_t)r0 * a.of + c0;
               const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
-              bool tiny = false;             // a corner of weight in (0, kFineW)
 #pragma unroll
-              for (int q = 0; q < 4; ++q) tiny |= inA && cw[q] > 0.0 && cw[q] < kFineW;
-              if (REG) {
-                const int l = (r0 - R0) * nc + (c0 - C0);
+              for (int q = 0; q < 4; ++q) {
+                if (ERR && cw[q] >= kFineW && plane_band(sAn, cw[q]))
+                  red64(a.A.num_f + cell + dcell[q], fix_value(sAn * 0x1p20, cw[q]));
+                else
+                  global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
+                global_term(a.A.den, a.A.den_f, cell + dcell[q], sAd, cw[q]);
+                if (!ERR && a.A.touched && cw[q] > 0.0 && cw[q] < kFineW)
+                  a.A.touched[cell + dcell[q]] = 1;
+              }
+            }
+            if (MODE == 2) {
+              // the next object's own position, as make_reference computes it
+              // (recon.py:138: u - d - origin), so the terms equal a separate
+              // object formation bit for bit
+              const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
+              const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
+              const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
+              const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
+              const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
+              const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
+              const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
+              const bool hotb = REG && cwb[0] >= kFineW && cwb[1] >= kFineW && cwb[2] >= kFineW &&
+                                cwb[3] >= kFineW;
+              if (inB && hotb) {
+                // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
+                const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
                 const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  if (inA && cw[q] >= kFineW) {
-                    if (ERR) {
-                      const bool band = plane_band(sAn, cw[q]);
-                      region_term(band ? slo + kBandV * RC : slo, band ? shi + kBandV * RC : shi,
-                                  l + dl[q], band ? sAn * 0x1p20 : sAn, cw[q]);
-                    } else {
-                      region_term(slo, shi, l + dl[q], sAn, cw[q]);
-                    }
-                    region_term(slo + RC, shi + RC, l + dl[q], sAd, cw[q]);
-                  }
+                  region_term(slo + 2 * RC, shi + 2 * RC, l + dl[q], sBn, cwb[q]);
+                  region_term(slo + 3 * RC, shi + 3 * RC, l + dl[q], sBd, cwb[q]);
                 }
-                if (tiny) {                  // rare: straight to the fine images
-#pragma unroll
-                  for (int q = 0; q < 4; ++q)
-                    if (cw[q] > 0.0 && cw[q] < kFineW) {
-                      global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
-                      global_term(a.A.den, a.A.den_f, cell + dcell[q], sAd, cw[q]);
-                      if (!ERR && a.A.touched) a.A.touched[cell + dcell[q]] = 1;
-                    }
-                }
-              } else if (inA) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  if (ERR && cw[q] >= kFineW && plane_band(sAn, cw[q]))
-                    red64(a.A.num_f + cell + dcell[q], fix_value(sAn * 0x1p20, cw[q]));
-                  else
-                    global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
-                  global_term(a.A.den, a.A.den_f, cell + dcell[q], sAd, cw[q]);
-                  if (!ERR && a.A.touched && cw[q] > 0.0 && cw[q] < kFineW)
-                    a.A.touched[cell + dcell[q]] = 1;
-                }
-              }
-              if (MODE == 2) {
-                // the next object's own position, as make_reference computes it
-                // (recon.py:138: u - d - origin), so the terms equal a separate
-                // object formation bit for bit
-                const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
-                const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
-                const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
-                const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
-                const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
-                const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
-                const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
+              } else if (inB) {
                 const int64_t cellb = (int64_t)r0b * ofb + c0b;
                 const int64_t dcb[4] = {0, 1, ofb, ofb + 1};
-                bool tinyb = false;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) tinyb |= inB && cwb[q] > 0.0 && cwb[q] < kFineW;
-                if (REG) {
-                  // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
-                  const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
-                  const int dl[4] = {0, 1, nc, nc + 1};
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    if (inB && cwb[q] >= kFineW) {
-                      region_term(slo + 2 * RC, shi + 2 * RC, l + dl[q], sBn, cwb[q]);
-                      region_term(slo + 3 * RC, shi + 3 * RC, l + dl[q], sBd, cwb[q]);
-                    }
-                  }
-                  if (tinyb) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                      if (cwb[q] > 0.0 && cwb[q] < kFineW) {
-                        global_term(a.B.num, a.B.num_f, cellb + dcb[q], sBn, cwb[q]);
-                        global_term(a.B.den, a.B.den_f, cellb + dcb[q], sBd, cwb[q]);
-                        if (a.B.touched) a.B.touched[cellb + dcb[q]] = 1;
-                      }
-                  }
-                } else if (inB) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    global_term(a.B.num, a.B.num_f, cellb + dcb[q], sBn, cwb[q]);
-                    global_term(a.B.den, a.B.den_f, cellb + dcb[q], sBd, cwb[q]);
-                    if (a.B.touched && cwb[q] > 0.0 && cwb[q] < kFineW) a.B.touched[cellb + dcb[q]] = 1;
-                  }
+                for (int q = 0; q < 4; ++q) {
+                  global_term(a.B.num, a.B.num_f, cellb + dcb[q], sBn, cwb[q]);
+                  global_term(a.B.den, a.B.den_f, cellb + dcb[q], sBd, cwb[q]);
+                  if (a.B.touched && cwb[q] > 0.0 && cwb[q] < kFineW) a.B.touched[cellb + dcb[q]] = 1;
                 }
               }
             }
           }
-          if (ERR) {   // per-frame sums: warp, then the CTA's warps in a fixed order
-#pragma unroll
-            for (int f = 0; f < kXB; ++f) {
-              const double sum = warp_sum(ef[f]);
-              if (lane == 0) s_fr[warp][f] = sum;
-            }
-            __syncthreads();
-            if (threadIdx.x < nf) {
-              double sum = 0.0;
-#pragma unroll
-              for (int w = 0; w < kXW; ++w) sum += s_fr[w][threadIdx.x];
-              a.part[(kc + bb + threadIdx.x) * a.n_cta + cta] = sum;
-            }
-            __syncthreads();
+          if (ERR) {       // this warp's share of the frame's sum (CTA sum at chunk end)
+            const double sum = warp_sum(ef);
+            if (lane == 0) s_frw[warp][t] = sum;
           }
         }
       };
@@ -491,6 +454,15 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
         __syncthreads();
       }
       s0 = s1;
+    }
+    if (ERR) {   // per-frame sums of the chunk: the CTA's warps in a fixed order
+      __syncthreads();
+      for (int t = threadIdx.x; t < nt; t += kXT) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kXW; ++w) sum += s_frw[w][t];
+        a.part[(kc + t) * a.n_cta + cta] = sum;
+      }
     }
   }
   if (ERR) {
