@@ -349,15 +349,17 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
               sAd = W2[e] * qa_d;
             }
-            // hot path: every corner weight >= kFineW (the others, and the
-            // direct sessions, take the per-corner path below)
-            const bool hot = REG && cw[0] >= kFineW && cw[1] >= kFineW && cw[2] >= kFineW &&
-                             cw[3] >= kFineW;
+            // hot path: every corner weight 0 (nothing to add) or >= kFineW;
+            // the others, and the direct sessions, take the per-corner path
+            const bool hot = REG && (cw[1] == 0.0 || cw[1] >= kFineW) &&
+                             (cw[2] == 0.0 || cw[2] >= kFineW) && (cw[3] == 0.0 || cw[3] >= kFineW) &&
+                             cw[0] >= kFineW;
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
               const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
+                if (q > 0 && cw[q] == 0.0) continue;
                 if (ERR) {
                   const bool band = plane_band(sAn, cw[q]);
                   region_term(band ? slo + kBandV * RC : slo, band ? shi + kBandV * RC : shi,
@@ -392,14 +394,16 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
               const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
               const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
-              const bool hotb = REG && cwb[0] >= kFineW && cwb[1] >= kFineW && cwb[2] >= kFineW &&
-                                cwb[3] >= kFineW;
+              const bool hotb = REG && (cwb[1] == 0.0 || cwb[1] >= kFineW) &&
+                                (cwb[2] == 0.0 || cwb[2] >= kFineW) &&
+                                (cwb[3] == 0.0 || cwb[3] >= kFineW) && cwb[0] >= kFineW;
               if (inB && hotb) {
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
                 const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
                 const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                  if (q > 0 && cwb[q] == 0.0) continue;
                   region_term(slo + 2 * RC, shi + 2 * RC, l + dl[q], sBn, cwb[q]);
                   region_term(slo + 3 * RC, shi + 3 * RC, l + dl[q], sBd, cwb[q]);
                 }

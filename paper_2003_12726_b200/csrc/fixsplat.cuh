@@ -70,13 +70,14 @@ __host__ __device__ inline int fix_headroom(int64_t n_good) {
   return k;
 }
 
-// Terms whose bilinear corner weight is below kFineW are summed apart, in
-// units of q * 2^-kFineShift (a single int64 per term, |t| < 2^(41-10+20) =
-// 2^51 fine quanta, 12 bits of headroom for the cell's sum): a cell reached
-// only by tiny-weight corners (e.g. the grid's last row, weighted by the
-// fractions of the outermost samples) keeps 20 more bits.  Such corners are
-// rare (a fraction ~2^-10), so they go straight to global memory.
-constexpr double kFineW = 1.0 / 1024.0;
+// Terms whose bilinear corner weight is below kFineW = 2^-20 are summed
+// apart, in units of q * 2^-kFineShift (a single int64 per term,
+// |t| < 2^(41-20+20) = 2^41 fine quanta): a cell reached only by tiny-weight
+// corners (e.g. the grid's last row, weighted by the fractions of the
+// outermost samples) keeps 20 more bits; a coarse term of weight >= 2^-20
+// keeps >= 21.  Such corners are rare (~1e-5 of the samples), so they go
+// straight to global memory.
+constexpr double kFineW = 0x1p-20;
 constexpr int kFineShift = 20;
 
 // Device accumulators of one image, int64: num / den in units of the quanta
