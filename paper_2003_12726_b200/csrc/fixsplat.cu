@@ -110,8 +110,11 @@ __device__ __forceinline__ bool plane_band(double scaled, double w) {
   return fabs(scaled * w) < 2097152.0;
 }
 
+#ifndef PXST_FIX_OCC0
+#define PXST_FIX_OCC0 3
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
+__global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass(FixArgs a) {
   constexpr int NV = FixCfg<MODE>::NV, RC = FixCfg<MODE>::RC;
   constexpr bool ERR = MODE != 0;
   extern __shared__ __align__(16) unsigned char fx_raw[];
@@ -297,10 +300,10 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
         for (int e = 0; e < 2; ++e) In[e] = live[e] ? __ldg(a.sc.frames + t_off[s0] + p[e]) : 0.f;
         for (int t = s0; t < s1; ++t) {
           const float Ic[2] = {In[0], In[1]};
-          if (t + 1 < s1) {
+          {
+            const int64_t off = t_off[t + 1 < s1 ? t + 1 : t];
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
-              In[e] = live[e] ? __ldg(a.sc.frames + t_off[t + 1] + p[e]) : 0.f;
+            for (int e = 0; e < 2; ++e) In[e] = live[e] ? __ldg(a.sc.frames + off + p[e]) : 0.f;
           }
           const double dI = t_di[t], dJ = t_dj[t];
           double ef = 0.0;
@@ -345,15 +348,16 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
               sAd = qa_d;
             } else {
-              dropped += (act && !inA) ? 1 : 0;
+              if (a.n_drop) dropped += (act && !inA) ? 1 : 0;
               sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
               sAd = W2[e] * qa_d;
             }
             // hot path: every corner weight 0 (nothing to add) or >= kFineW;
             // the others, and the direct sessions, take the per-corner path
-            const bool hot = REG && (cw[1] == 0.0 || cw[1] >= kFineW) &&
-                             (cw[2] == 0.0 || cw[2] >= kFineW) && (cw[3] == 0.0 || cw[3] >= kFineW) &&
-                             cw[0] >= kFineW;
+            // (smallest nonzero corner weight = min(fx, 1-fx) min(fy, 1-fy)
+            // over the axes with a nonzero fraction)
+            const bool hot = REG && (fx > 0.0 ? fmin(fx, gx) : 1.0) * (fy > 0.0 ? fmin(fy, gy) : 1.0) >=
+                                        kFineW;
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
               const int dl[4] = {0, 1, nc, nc + 1};
@@ -394,9 +398,8 @@ __global__ void __launch_bounds__(kXT, 2) k_fix_pass(FixArgs a) {
               const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
               const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
               const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
-              const bool hotb = REG && (cwb[1] == 0.0 || cwb[1] >= kFineW) &&
-                                (cwb[2] == 0.0 || cwb[2] >= kFineW) &&
-                                (cwb[3] == 0.0 || cwb[3] >= kFineW) && cwb[0] >= kFineW;
+              const bool hotb = REG && (fxb > 0.0 ? fmin(fxb, gxb) : 1.0) *
+                                               (fyb > 0.0 ? fmin(fyb, gyb) : 1.0) >= kFineW;
               if (inB && hotb) {
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
                 const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
