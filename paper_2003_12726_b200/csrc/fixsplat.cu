@@ -84,14 +84,15 @@ struct TermSink {
   long long* gf;      // global fine image
 };
 
-// A term into the region's limbs (coarse, corner weight >= kFineW).
-__device__ __forceinline__ void region_term(unsigned* lo_arr, int* hi_arr, int li, double scaled,
-                                            double w) {
+// A term into the region's limbs (coarse, corner weight >= kFineW): lo at
+// slo[idx], hi at slo[idx + HI] (HI = NV * RC words, an immediate offset).
+template <int HI>
+__device__ __forceinline__ void region_term(unsigned* slo, int idx, double scaled, double w) {
   unsigned lo;
   int hi;
   fix_limbs(scaled, w, lo, hi);
-  atomicAdd(lo_arr + li, lo);
-  atomicAdd(hi_arr + li, hi);
+  atomicAdd(slo + idx, lo);
+  atomicAdd(reinterpret_cast<int*>(slo) + idx + HI, hi);
 }
 
 // A term straight into the global images (no region; and tiny-weight
@@ -361,17 +362,18 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
               const int dl[4] = {0, 1, nc, nc + 1};
+              const double sAnb = sAn * 0x1p20;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 if (q > 0 && cw[q] == 0.0) continue;
                 if (ERR) {
                   const bool band = plane_band(sAn, cw[q]);
-                  region_term(band ? slo + kBandV * RC : slo, band ? shi + kBandV * RC : shi,
-                              l + dl[q], band ? sAn * 0x1p20 : sAn, cw[q]);
+                  region_term<NV * RC>(slo, l + dl[q] + (band ? kBandV * RC : 0), band ? sAnb : sAn,
+                                       cw[q]);
                 } else {
-                  region_term(slo, shi, l + dl[q], sAn, cw[q]);
+                  region_term<NV * RC>(slo, l + dl[q], sAn, cw[q]);
                 }
-                region_term(slo + RC, shi + RC, l + dl[q], sAd, cw[q]);
+                region_term<NV * RC>(slo, l + dl[q] + RC, sAd, cw[q]);
               }
             } else if (inA) {
               const int64_t cell = (int64_t)r0 * a.of + c0;
@@ -407,8 +409,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   if (q > 0 && cwb[q] == 0.0) continue;
-                  region_term(slo + 2 * RC, shi + 2 * RC, l + dl[q], sBn, cwb[q]);
-                  region_term(slo + 3 * RC, shi + 3 * RC, l + dl[q], sBd, cwb[q]);
+                  region_term<NV * RC>(slo, l + dl[q] + 2 * RC, sBn, cwb[q]);
+                  region_term<NV * RC>(slo, l + dl[q] + 3 * RC, sBd, cwb[q]);
                 }
               } else if (inB) {
                 const int64_t cellb = (int64_t)r0b * ofb + c0b;
@@ -515,8 +517,14 @@ __global__ void k_abs_max(const float* __restrict__ frames, int64_t n, double* o
        i += (int64_t)gridDim.x * blockDim.x)
     m = fmaxf(m, fabsf(__ldg(frames + i)));
   // NaN / inf samples: an infinite bound (quantum 2^-41 of 1, see fix_quantum)
+  __shared__ float red[32];
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, static_cast<double>(m));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = fmaxf(m, red[k]);
+    atomic_max_nonneg(out, static_cast<double>(m));
+  }
 }
 
 // scratch[0] = max W over the work pixels of the ROI, scratch[1] = min
@@ -538,10 +546,19 @@ __global__ void k_scale_stats(pxst_scan sc, const double* __restrict__ sigma2,
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_ref;
          q += (int64_t)gridDim.x * blockDim.x)
       if (valid[q]) rmax = fmax(rmax, fabs(fm64 ? fm64[q] : static_cast<double>(fm[q])));
+  __shared__ double red[3][32];
   wmax = warp_max(wmax);
   smin = warp_min(smin);
   rmax = warp_max(rmax);
-  if ((threadIdx.x & 31) == 0) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { red[0][w] = wmax; red[1][w] = smin; red[2][w] = rmax; }
+  __syncthreads();
+  if (threadIdx.x == 0) {   // one atomic per block (many per address serialise in L2)
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      wmax = fmax(wmax, red[0][k]);
+      smin = fmin(smin, red[1][k]);
+      rmax = fmax(rmax, red[2][k]);
+    }
     atomic_max_nonneg(scratch, wmax);
     if (sigma2) atomic_min_nonneg(scratch + 1, smin);
     atomic_max_nonneg(scratch + 2, rmax);
@@ -630,7 +647,7 @@ int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma
   PXST_CHECK_LAUNCH();
   const int64_t n_ref = ref ? ref->os * ref->of : 0;
   const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
-  k_scale_stats<<<grid_1d(std::max(rw * cw, n_ref), 256), 256, 0, s>>>(
+  k_scale_stats<<<std::min(grid_1d(std::max(rw * cw, n_ref), 256), 2 * 148), 256, 0, s>>>(
       *sc, kind == 1 ? sigma2 : nullptr, ref ? ref->fm64 : nullptr, ref ? ref->fm : nullptr,
       ref ? ref->valid : nullptr, n_ref, d);
   PXST_CHECK_LAUNCH();
