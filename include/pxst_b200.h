@@ -127,6 +127,9 @@ typedef struct pxst_accum {
   const double* quanta;   /* device [2]                                         */
 } pxst_accum;
 
+/* Zero `cells` cells of every array of an accumulator (cudaMemsetAsync). */
+int pxst_accum_zero(const pxst_accum* acc, int64_t cells, void* stream);
+
 /* max |I| over the whole frame stack (device float64 scalar): the bound the
  * quanta are derived from.  One pass over the stack; cache it per stack. */
 int pxst_stack_absmax(const pxst_scan* scan, double* out, void* stream);

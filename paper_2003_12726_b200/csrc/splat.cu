@@ -122,6 +122,19 @@ extern "C" int pxst_object_splat(const pxst_scan* sc, const double* u, const dou
                            n_dropped, as_stream(stream));
 }
 
+extern "C" int pxst_accum_zero(const pxst_accum* acc, int64_t cells, void* stream) {
+  if (int e = check_accum(acc)) return e;
+  PXST_REQUIRE(cells >= 0, "bad accumulator size");
+  cudaStream_t s = as_stream(stream);
+  const size_t b = sizeof(int64_t) * cells;
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc->num, 0, b, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc->den, 0, b, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc->num_fine, 0, b, s));
+  PXST_CHECK_CUDA(cudaMemsetAsync(acc->den_fine, 0, b, s));
+  if (acc->touched) PXST_CHECK_CUDA(cudaMemsetAsync(acc->touched, 0, cells, s));
+  return PXST_OK;
+}
+
 extern "C" int pxst_object_finish(const pxst_accum* acc, int64_t n, double* i_ref, double* wsum,
                                   float* fm, uint8_t* valid, void* stream) {
   if (int e = check_accum(acc)) return e;

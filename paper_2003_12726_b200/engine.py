@@ -140,9 +140,11 @@ class Accum:
     (int64 all-reduce) and ``touched`` with max."""
 
     def __init__(self, cells: int, quanta: torch.Tensor, device, touched: bool = True):
-        self.data = torch.zeros((4, cells), dtype=torch.int64, device=device)
-        self.touched = torch.zeros(cells, dtype=torch.uint8, device=device) if touched else None
+        self.data = torch.empty((4, cells), dtype=torch.int64, device=device)
+        self.touched = torch.empty(cells, dtype=torch.uint8, device=device) if touched else None
         self.quanta = quanta
+        c = self.c()
+        check(_native.lib().pxst_accum_zero(ctypes.byref(c), cells, stream_ptr()))
 
     @property
     def cells(self) -> int:
