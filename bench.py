@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
+    ap.add_argument("--extras", default="2,3",
+                    help="larger configs also measured in the same run (comma list, '' = none)")
     return ap.parse_args()
 
 
@@ -87,10 +89,13 @@ def peaks():
         return {}
 
 
-def k2_traffic():
-    p = os.path.join(ROOT, "profiles", "k2_traffic.json")
+def kernel_traffic(workload: str):
+    """DRAM bytes per launch of the workload's dominant kernel from the ncu
+    --set full capture recorded for that workload (profiles/traffic.json,
+    keyed by workload name; None when no capture of this workload exists)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p))
+        return json.load(open(p)).get(workload)
     except Exception:
         return None
 
@@ -235,6 +240,129 @@ def one_time_costs(ds, s, host_data, engine, torch):
     return out
 
 
+class Sequence:
+    """The config's workload: `cfg.iters` consecutive iterations from the
+    initial state (config 1: 3 x object -> pixel map -> error); steps walk
+    that sequence with the state carried over and restart it when done.
+    ev = (start, end) events around the pixel-map search (K2), or around the
+    translation search (K3) when the config has no pixel-map update;
+    ev3 = events around K3 when both run."""
+
+    def __init__(self, ds, cfg, u_t, di_t, dj_t, stream, sharded=None):
+        self.ds, self.cfg, self.stream, self.sharded = ds, cfg, stream, sharded
+        self.init = (u_t, di_t, dj_t)
+        self.state = {"it": 0, "u": u_t, "di": di_t, "dj": dj_t, "geom": None, "dref": None}
+
+    def step(self, ev=None, ev3=None):
+        ds, cfg, stream, sharded, state = self.ds, self.cfg, self.stream, self.sharded, self.state
+        u_t, di_t, dj_t = self.init
+        if state["it"] == 0:
+            # (single GPU: state["geom"] is already the initial state's,
+            # prefetched by the last iteration of the previous pass)
+            state.update(u=u_t, di=di_t, dj=dj_t, dref=None)
+            if sharded is not None:
+                state.update(geom=None)
+        u, di, dj = state["u"], state["di"], state["dj"]
+        nxt = nref = None
+        if sharded is not None:
+            u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev, geom=state["geom"])
+            nxt = sharded.next_geom
+        else:
+            # the iteration's grid bbox and K2 tile spans were fetched on a side
+            # stream while the previous iteration's error maps ran, and its
+            # object was formed in the same pass over the stack as those maps
+            geom = state["geom"] or ds.geometry_async(u, di, dj)
+            dref = state["dref"].resolve() if state["dref"] else ds.object_map(u, di, dj, geom=geom)
+            u_new = u
+            if cfg.update_pixel_map:
+                if ev:
+                    ev[0].record(stream)
+                u_new, err = ds.pixel_map_search(dref, u, di, dj, cfg.half_ss, cfg.half_fs,
+                                                 cfg.subpixel_grid, cfg.refine, geom=geom)
+                if ev:
+                    ev[1].record(stream)
+            di_new, dj_new = di, dj
+            if cfg.update_translations:
+                k3 = ev if (ev and not cfg.update_pixel_map) else ev3
+                if k3:
+                    k3[0].record(stream)
+                di_new, dj_new = ds.translation_search(dref, u_new, di, dj, cfg.t_half_ss,
+                                                       cfg.t_half_fs, cfg.t_subpixel_grid)
+                if k3:
+                    k3[1].record(stream)
+            if state["it"] + 1 < cfg.iters:        # the sequence continues: fuse K4 + next K1
+                nxt = ds.geometry_async(u_new, di_new, dj_new)
+                _, nref = ds.error_maps_and_next_object(dref, u_new, di_new, dj_new, nxt)
+            else:
+                # the next step restarts the sequence from the initial state:
+                # fetch that state's geometry now, behind these error maps, as
+                # every other iteration's is (no host wait at the restart)
+                nxt = ds.geometry_async(u_t, di_t, dj_t)
+                ds.error_maps(dref, u_new, di_new, dj_new)
+        state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new,
+                     geom=nxt, dref=nref)
+
+
+def k3_trials(pb, ds, cfg):
+    w = pb.SearchWindow(cfg.t_half_ss, cfg.t_half_fs, cfg.t_subpixel_grid)
+    return ds.n_work * len(w.offsets(0)) * len(w.offsets(1)) * ds.n_good
+
+
+def extra_config(cfg_id, dev, steps=4, warmup=3):
+    """A larger BASELINE config measured in the same process as the headline
+    (device-resident stack rendered on the GPU, the config's own iteration
+    sequence, device-timed with CUDA events; its 3-8 GB stack is larger than
+    L2, so no flush is needed).  Reports ms per full iteration and the K2
+    (and K3) trial rates and FP32 fractions (11 FLOP per trial)."""
+    import torch
+    import paper_2003_12726_b200 as pb
+    from paper_2003_12726_b200 import engine
+    from paper_2003_12726_b200.synth import make_scan_device
+    t0 = time.perf_counter()
+    s, frames_dev = make_scan_device(cfg_id, dev)
+    ds = engine.DeviceScan(None, s.scan.good_frames, s.w.w, s.m.mask, frames_dev=frames_dev)
+    cfg = s.cfg
+    u_t = ds.upload_u(s.u0.u)
+    di_t, dj_t = ds.upload_t(s.t0.di, s.t0.dj)
+    ds.ready(frame_stats=cfg.update_translations)
+    ds.absmax()
+    stream = torch.cuda.current_stream()
+    seq = Sequence(ds, cfg, u_t, di_t, dj_t, stream)
+    for _ in range(warmup):
+        seq.step()
+    mk = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
+    st, en = [mk() for _ in range(steps)], [mk() for _ in range(steps)]
+    k2 = [(mk(), mk()) for _ in range(steps)]
+    k3 = [(mk(), mk()) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i in range(steps):
+        st[i].record(stream)
+        seq.step(k2[i] if cfg.update_pixel_map else None,
+                 k3[i] if cfg.update_translations else None)
+        en[i].record(stream)
+    torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in zip(st, en)]
+    out = {"workload": cfg.name, "iterations_timed": steps,
+           "ms_per_iteration": float(np.mean(ms)), "step_ms": [round(x, 3) for x in ms],
+           "setup_s": round(time.perf_counter() - t0, 1)}
+    if cfg.update_pixel_map:
+        trials = ds.n_work * (2 * cfg.half_ss + 1) * (2 * cfg.half_fs + 1) * ds.n_good
+        k2ms = float(np.mean([a.elapsed_time(b) for a, b in k2]))
+        tf = FLOP_PER_TRIAL * trials / (k2ms * 1e-3) / 1e12
+        out.update(pixel_map_trials_per_iteration=trials,
+                   trials_per_s=trials / (out["ms_per_iteration"] * 1e-3),
+                   k2_ms=k2ms, k2_tflops=tf, k2_frac=tf / THEORETICAL_FP32_TFLOPS)
+    if cfg.update_translations:
+        tt = k3_trials(pb, ds, cfg)
+        k3ms = float(np.mean([a.elapsed_time(b) for a, b in k3]))
+        tf = FLOP_PER_TRIAL * tt / (k3ms * 1e-3) / 1e12
+        out.update(translation_trials_per_iteration=tt, k3_ms=k3ms, k3_tflops=tf,
+                   k3_frac=tf / THEORETICAL_FP32_TFLOPS)
+    del seq, ds, frames_dev
+    engine.clear_cache()
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2003_12726_b200 as pb
@@ -285,56 +413,8 @@ def run_ours(args, rank, world, local):
         from paper_2003_12726_b200.sharding import DeviceExecutor, ShardedIteration
         sharded = ShardedIteration(DeviceExecutor(ds), rank, world)
 
-    # The config's workload is `cfg.iters` consecutive iterations from the
-    # initial state (config 1: 3 x object -> pixel map -> error); steps walk
-    # that sequence with the state carried over and restart it when done.
-    state = {"it": 0, "u": u_t, "di": di_t, "dj": dj_t, "geom": None, "dref": None}
-
-    def step(ev=None):
-        if state["it"] == 0:
-            # (single GPU: state["geom"] is already the initial state's,
-            # prefetched by the last iteration of the previous pass)
-            state.update(u=u_t, di=di_t, dj=dj_t, dref=None)
-            if sharded is not None:
-                state.update(geom=None)
-        u, di, dj = state["u"], state["di"], state["dj"]
-        nxt = nref = None
-        if sharded is not None:
-            u_new, di_new, dj_new = sharded.iteration(u, di, dj, cfg, ev, geom=state["geom"])
-            nxt = sharded.next_geom
-        else:
-            # the iteration's grid bbox and K2 tile spans were fetched on a side
-            # stream while the previous iteration's error maps ran, and its
-            # object was formed in the same pass over the stack as those maps
-            geom = state["geom"] or ds.geometry_async(u, di, dj)
-            dref = state["dref"].resolve() if state["dref"] else ds.object_map(u, di, dj, geom=geom)
-            u_new = u
-            if cfg.update_pixel_map:
-                if ev:
-                    ev[0].record(stream)
-                u_new, err = ds.pixel_map_search(dref, u, di, dj, cfg.half_ss, cfg.half_fs,
-                                                 cfg.subpixel_grid, cfg.refine, geom=geom)
-                if ev:
-                    ev[1].record(stream)
-            di_new, dj_new = di, dj
-            if cfg.update_translations:
-                if ev and not cfg.update_pixel_map:
-                    ev[0].record(stream)
-                di_new, dj_new = ds.translation_search(dref, u_new, di, dj, cfg.t_half_ss,
-                                                       cfg.t_half_fs, cfg.t_subpixel_grid)
-                if ev and not cfg.update_pixel_map:
-                    ev[1].record(stream)
-            if state["it"] + 1 < cfg.iters:        # the sequence continues: fuse K4 + next K1
-                nxt = ds.geometry_async(u_new, di_new, dj_new)
-                _, nref = ds.error_maps_and_next_object(dref, u_new, di_new, dj_new, nxt)
-            else:
-                # the next step restarts the sequence from the initial state:
-                # fetch that state's geometry now, behind these error maps, as
-                # every other iteration's is (no host wait at the restart)
-                nxt = ds.geometry_async(u_t, di_t, dj_t)
-                ds.error_maps(dref, u_new, di_new, dj_new)
-        state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new,
-                     geom=nxt, dref=nref)
+    seq = Sequence(ds, cfg, u_t, di_t, dj_t, stream, sharded)
+    step = seq.step
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
@@ -410,13 +490,15 @@ def run_ours(args, rank, world, local):
     pk = peaks()
     k2_trials = trials / world if world > 1 else trials
     achieved = FLOP_PER_TRIAL * k2_trials / (k2_mean * 1e-3) / 1e12
-    traffic = k2_traffic()
+    traffic = kernel_traffic(cfg.name)
     kname = (f"k_pix_fast<{2 * cfg.half_ss + 1},{2 * cfg.half_fs + 1}> (+slow, epilogue)"
              if cfg.update_pixel_map else "k_trans_fast phase groups (+slow, epilogue)")
     roofline = {"bound": "fp32", "kernel": kname,
                 "achieved": achieved, "peak": THEORETICAL_FP32_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / THEORETICAL_FP32_TFLOPS,
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_source": traffic.get("source") if traffic else
+                "no ncu capture of this workload in profiles/traffic.json",
                 "peak_source": ("theoretical FP32 148 SMs x 128 lanes x 2 x sm_max 1965 MHz "
                                 "(MEASURED_PEAKS.json has no FP32 entry; FFMA2 microbenchmark on "
                                 "this pool: 73.8 TFLOP/s, profiles/microbench_r01.json)"),
@@ -445,6 +527,15 @@ def run_ours(args, rank, world, local):
 
     if not args.profile and not args.no_e2e and world == 1 and host_data:
         out["e2e"] = e2e(s, args, pb, engine, torch, trials)
+    if not args.profile and world == 1 and args.extras:
+        # the larger configs, measured in this same run (builder-run numbers
+        # alone were not driver-observed)
+        out["extra_configs"] = {}
+        for cid in (int(c) for c in args.extras.split(",") if c.strip()):
+            try:
+                out["extra_configs"][f"cfg{cid}"] = extra_config(cid, dev)
+            except Exception as exc:       # reported, never fatal to the headline line
+                out["extra_configs"][f"cfg{cid}"] = {"error": repr(exc)[:300]}
     if not args.profile and not args.no_cpu_baseline and world == 1 and host_data:
         v, sec, cores, rows = cpu_timing(s, 1, 0, 16)
         out["cpu_baseline"] = {"value": v, "unit": "trials/s", "cores": cores, "kind": "port",

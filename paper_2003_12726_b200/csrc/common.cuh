@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <stdio.h>
 
 #include "pxst_b200.h"
 
@@ -38,6 +39,24 @@ void count_launch(int n = 1);
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Device-side bounds / invariant checks, compiled in with -DPXST_CHECKED
+// (tools/checked_run.sh: the checked library runs the GPU tests; this pool
+// has compute-sanitizer closed).  A failure prints the condition and traps.
+#ifdef PXST_CHECKED
+#define PXST_DCHECK(cond)                                                           \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("PXST_DCHECK failed: %s at %s:%d (block %d,%d,%d thread %d)\n", #cond, \
+             __FILE__, __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);   \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define PXST_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 // Keep memory freed with cudaFreeAsync in the device's default pool across
 // synchronisations (the default release threshold of 0 hands it back to the

@@ -88,6 +88,7 @@ struct TermSink {
 // slo[idx], hi at slo[idx + HI] (HI = NV * RC words, an immediate offset).
 template <int HI>
 __device__ __forceinline__ void region_term(unsigned* slo, int idx, double scaled, double w) {
+  PXST_DCHECK(idx >= 0 && idx < HI);
   unsigned lo;
   int hi;
   fix_limbs(scaled, w, lo, hi);
@@ -99,6 +100,7 @@ __device__ __forceinline__ void region_term(unsigned* slo, int idx, double scale
 // corners, |t| < 2^51 fine quanta).
 __device__ __forceinline__ void global_term(long long* g, long long* gf, int64_t cell,
                                             double scaled, double w) {
+  PXST_DCHECK(cell >= 0);
   if (w >= kFineW) red64(g + cell, fix_value(scaled, w));
   else if (w > 0.0) red64(gf + cell, fix_value(scaled * 0x1p20, w));
 }
@@ -361,6 +363,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
                                         kFineW;
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
+              PXST_DCHECK(r0 >= R0 && c0 >= C0 && l >= 0 && l + nc + 1 < ncell);
               const int dl[4] = {0, 1, nc, nc + 1};
               const double sAnb = sAn * 0x1p20;
 #pragma unroll
@@ -405,6 +408,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
               if (inB && hotb) {
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
                 const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
+                PXST_DCHECK(l >= 0 && l + nc + 1 < ncell);
                 const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -442,6 +446,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
           const long long vn = fix_join(slo[i], shi[i]);
           const long long vd = fix_join(slo[RC + i], shi[RC + i]);
           if (vn != 0 || vd != 0) {
+            PXST_DCHECK(r >= 0 && r < a.os && c >= 0 && c < a.of);
             const int64_t cell = (int64_t)r * of + c;
             if (vn) red64(a.A.num + cell, vn);
             if (vd) red64(a.A.den + cell, vd);
@@ -454,6 +459,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
             const long long wn = fix_join(slo[2 * RC + i], shi[2 * RC + i]);
             const long long wd = fix_join(slo[3 * RC + i], shi[3 * RC + i]);
             if (wn != 0 || wd != 0) {
+              PXST_DCHECK(r + dn >= 0 && r + dn < osb && c + dm >= 0 && c + dm < ofb);
               const int64_t cell = (int64_t)(r + dn) * ofb + (c + dm);
               if (wn) red64(a.B.num + cell, wn);
               if (wd) red64(a.B.den + cell, wd);

@@ -419,6 +419,8 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       sq = fast ? sq : 0.f;
       const float sI = I * sq, sW = W * sq;
       const int off = fast ? sm.lr * ldw + sm.lc : 0;
+      PXST_DCHECK(!fast || (sm.lr >= 0 && sm.lr + KA + 1 <= a.box_r && sm.lc >= 0 &&
+                            sm.lc + KB + 1 <= a.box_c));
       if (kAhead) s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
       engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
                            acc);

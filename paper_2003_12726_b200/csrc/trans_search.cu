@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
     mbar_wait(&full[b], ph);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+      PXST_DCHECK(off[e] < 0 || off[e] + KA * a.box_c + KB + a.box_c + 1 < box);
       if (off[e] >= 0)
         engine_fast2<KA, KB>(ring + b * box + off[e], a.box_c, fx[e], fy[e],
                              W[e] * (1.f - fx[e]), W[e] * fx[e], I[e], acc);
