@@ -260,6 +260,15 @@ int pxst_error_partials(const pxst_scan* scan, const pxst_stats* st, const pxst_
                         const double* u, const double* di, const double* dj, double* per_frame,
                         double* per_pixel, const pxst_accum* plane, void* stream);
 
+/* Elementwise reductions of the single-process multi-GPU path (device
+ * pointers on the stream's device; `src` is a peer's accumulator copied
+ * over NVLink): dst += src (int64: the exact fixed-point images; float64: the
+ * per-frame error sums, added by every device in the same peer order) and
+ * dst |= src (touched flags). */
+int pxst_add_i64(int64_t* dst, const int64_t* src, int64_t n, void* stream);
+int pxst_add_f64(double* dst, const double* src, int64_t n, void* stream);
+int pxst_or_u8(uint8_t* dst, const uint8_t* src, int64_t n, void* stream);
+
 /* Interpolation primitives (interp.py:53-85 and :88-123), for the drop-in
  * interp module and the parity tests.  gather: vals/ok at n points of the
  * masked image.  splat: float64 accumulation into acc_v/acc_w [os,of]

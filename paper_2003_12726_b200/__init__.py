@@ -22,6 +22,7 @@ from .data_model import (
     Whitefield,
 )
 from .engine import clear_cache
+from .multigpu import Devices
 from .recon import (
     IterationSettings,
     LoopResult,

@@ -56,6 +56,9 @@ _SIGS = {
                                        c_void_p]),
     "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pxst_accum_zero": (c_int, [POINTER(PxstAccum), c_int64, c_void_p]),
+    "pxst_add_i64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "pxst_add_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "pxst_or_u8": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "pxst_stack_absmax": (c_int, [POINTER(PxstScan), c_void_p, c_void_p]),
     "pxst_object_quanta": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p]),
     "pxst_plane_quanta": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats),

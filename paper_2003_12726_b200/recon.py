@@ -240,17 +240,28 @@ def quadratic_subpixel_refine(err3x3: np.ndarray) -> tuple[float, float]:
 def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
                   t: PixelTranslations, roi: Roi | None = None, geom: Geometry | None = None,
                   schedule: list[IterationSettings] | None = None, max_iters: int = 10,
-                  tol: float = 1e-3, threads: int = 1, progress_cb=None) -> LoopResult:
+                  tol: float = 1e-3, threads: int = 1, progress_cb=None,
+                  devices=None) -> LoopResult:
     """Device-resident main loop with the reference's ordering (recon.py:479-522).
 
     u, translations and the reference stay on the GPU between steps; per
     iteration the host only reads the grid shape (bbox) and the error
     metrics (which the history records, as the reference does).
+
+    ``devices`` (extension, default None = the current GPU): a
+    ``multigpu.Devices`` (or list of device ids); the iteration then runs on
+    all of them from this one process (frames shard object formation and
+    translations, detector rows the pixel map and error maps).
     """
     if schedule is None:
         schedule = default_schedule(max_iters)
     if len(schedule) < max_iters:
         schedule = list(schedule) + [schedule[-1]] * (max_iters - len(schedule))
+    if devices is not None:
+        from .multigpu import Devices
+        devs = devices if isinstance(devices, Devices) else Devices(devices)
+        return _run_main_loop_multi(scan, w, m, u, t, roi, geom, schedule, max_iters, tol,
+                                    progress_cb, devs)
     ds = SCAN_CACHE.get(scan, w, m, roi)
     if ds.empty:
         raise ValueError("make_reference: empty good pixel/frame set")
@@ -291,3 +302,36 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
             break
     return LoopResult(pixel_map=PixelMap(_host(u_t)), reference=_ref_image(dref, geom),
                       translations=PixelTranslations(_host(di_t), _host(dj_t)), history=history)
+
+
+def _run_main_loop_multi(scan, w, m, u, t, roi, geom, schedule, max_iters, tol, progress_cb,
+                         devs) -> LoopResult:
+    """run_main_loop over several GPUs of this process (multigpu.MultiScan)."""
+    from .multigpu import MultiScan
+    ms = MultiScan(scan, w, m, roi, devs)
+    if ms.empty:
+        raise ValueError("make_reference: empty good pixel/frame set")
+    us, dis, djs = ms.upload(u.u, t.di, t.dj)
+    refs = ms.object_map(us, dis, djs)
+    history = [_metrics(*ms.error_maps(refs, us, dis, djs)[0])]
+    if progress_cb:
+        progress_cb(0.0, f"initial error {history[0].total:.6g}")
+    for i in range(max_iters):
+        st = schedule[i]
+        refs = ms.object_map(us, dis, djs)
+        us = ms.pixel_map(refs, us, dis, djs, st.window.half_ss, st.window.half_fs,
+                          st.window.subpixel_grid, st.options.quadratic_refinement,
+                          opts=st.options)
+        if st.update_translations:
+            tw = st.translation_window
+            dis, djs = ms.translations(refs, us, dis, djs, tw.half_ss, tw.half_fs,
+                                       tw.subpixel_grid)
+        history.append(_metrics(*ms.error_maps(refs, us, dis, djs)[0]))
+        if progress_cb:
+            progress_cb((i + 1) / max_iters, f"iter {i + 1} error {history[-1].total:.6g}")
+        prev, curr = history[-2].total, history[-1].total
+        if prev > 0 and (prev - curr) / prev < tol:
+            break
+    return LoopResult(pixel_map=PixelMap(_host(us[0])), reference=_ref_image(refs[0], geom),
+                      translations=PixelTranslations(_host(dis[0]), _host(djs[0])),
+                      history=history)
