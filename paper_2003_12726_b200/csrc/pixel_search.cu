@@ -226,14 +226,6 @@ struct Sample {
                      // the one-frame-ahead pipeline hides its latency)
   float fwv;         // frame weight (< 0: not live); also consumed late
   __device__ __forceinline__ bool fast() const { return pre && pvb != 0 && fwv >= 0.f; }
-  // The fast kernel runs its engine on every sample whose patch sits in the
-  // box (eng): a patch touching an invalid cell (pvb == 0) reads that cell
-  // as 0 (the masked image; TMA zero-fills off-grid cells), so only the
-  // trials whose corners touch it come out wrong, and the fix-up adds
-  // (exact - engine) for those trials alone (corr).  Samples not eng take
-  // the exact path for every trial.
-  __device__ __forceinline__ bool eng() const { return pre && fwv >= 0.f; }
-  __device__ __forceinline__ bool corr() const { return eng() && pvb == 0; }
 };
 
 // Object-window origin (box row, 16-byte aligned box column) of a tile for
@@ -418,8 +410,8 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
         }
       }
       mbar_wait(&full[b], ph);
-      const bool fast = sm.eng();
-      any_slow |= live && !sm.fast();
+      const bool fast = sm.fast();
+      any_slow |= live && !fast;
       const float fx = fast ? static_cast<float>(sm.fx) : 0.f;
       const float fy = fast ? static_cast<float>(sm.fy) : 0.f;
       float sq = BC > 0 ? 1.f : sqrt_approx(fmaxf(fwv, 0.f));   // no branch in the block
@@ -568,7 +560,6 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
           atomicAdd(a.dbg + 2, (unsigned long long)__popc(m2));
         }
       }
-      const unsigned cmask = __ballot_sync(0xffffffffu, slow && sl.corr());
       while (mask) {
         // slot s takes the (s+1)-th lowest set bit: samples stay in frame
         // order within a slot
@@ -589,7 +580,6 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
         }
         if (bsel >= 0) {
           const ExactSample es = exact_sample(sfx, sfy, W, sI, sfw);
-          const bool corr = (cmask >> bsel) & 1u;   // engine already added it (Sample::corr)
           const int pr = si - ra + trow, pc = sj - rb;
           float r0[kRowMax + 1], r1[kRowMax + 1];
 #pragma unroll
@@ -599,9 +589,7 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
           }
 #pragma unroll
           for (int c = 0; c < kRowMax; ++c)
-            if (c < kb)
-              acc[c] += corr ? trial_patch_correction(r0[c], r0[c + 1], r1[c], r1[c + 1], es)
-                             : trial_patch(r0[c], r0[c + 1], r1[c], r1[c + 1], es);
+            if (c < kb) acc[c] += trial_patch(r0[c], r0[c + 1], r1[c], r1[c + 1], es);
         }
       }
     }
@@ -736,26 +724,18 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
           atomicAdd(a.dbg + 2, (unsigned long long)__popc(m2));
         }
       }
-      const unsigned cmask = __ballot_sync(0xffffffffu, slow && sl.corr());
       while (mask) {
         const int bsel = __ffs(mask) - 1;
         mask &= mask - 1;
-        const bool corr = (cmask >> bsel) & 1u;          // warp-uniform
         const int pr0 = __shfl_sync(0xffffffffu, sl.i, bsel) - ra;
         const int pc0 = __shfl_sync(0xffffffffu, sl.j, bsel) - rb;
         const ExactSample es = exact_sample(__shfl_sync(0xffffffffu, sl.fx, bsel),
                                             __shfl_sync(0xffffffffu, sl.fy, bsel), W,
                                             __shfl_sync(0xffffffffu, Il, bsel),
                                             __shfl_sync(0xffffffffu, fwl, bsel));
-        if (corr) {
-          // the engine already added this sample with invalid / off-grid
-          // cells read as 0: correct the trials that touch one
-#pragma unroll
-          for (int j = 0; j < NJ; ++j)
-            if (lane + 32 * j < nk)
-              part[j] += trial_correction(a.fmn, os, of, pr0 + ta[j], pc0 + tb[j], es);
-        } else if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {
-          // warp-uniform: the whole window's 2x2 cells on the grid
+        // warp-uniform: the whole window's 2x2 cells on the grid (the usual
+        // case: skipped samples touch invalid cells, not the grid's edge)
+        if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {
           const float* w0 = a.fmn + (pr0 * of + pc0);
 #pragma unroll
           for (int j = 0; j < NJ; ++j)

@@ -214,55 +214,6 @@ __device__ __forceinline__ float trial_global(const float* __restrict__ fmn, int
   return ok ? e.fwv * (r * r) : e.fb;
 }
 
-// For a sample the fast engine already added with invalid and off-grid
-// cells read as 0: (exact trial) - (engine trial) when one of the trial's
-// weighted corners is invalid or off the grid, else 0 (the engine's value
-// stands).  The engine's value is recomputed as fwv (I - W sum_c w_c o_c)^2
-// with o_c = 0 on such corners (to float32 rounding of the engine's
-// factored form).
-__device__ __forceinline__ float trial_correction(const float* __restrict__ fmn, int os, int of,
-                                                  int row, int col, const ExactSample& e) {
-  const bool rin = (row >= 0 && row < os - 1) || (row == os - 1 && !e.fxp);
-  const bool cin = (col >= 0 && col < of - 1) || (col == of - 1 && !e.fyp);
-  const bool r1in = row + 1 >= 0 && row + 1 < os, c1in = col + 1 >= 0 && col + 1 < of;
-  const bool r0in = row >= 0 && row < os, c0in = col >= 0 && col < of;
-  const int r0 = min(max(row, 0), os - 1), c0 = min(max(col, 0), of - 1);
-  const int dr = r0 + 1 < os ? of : 0, dc = c0 + 1 < of ? 1 : 0;
-  const float* p0 = fmn + (r0 * of + c0);
-  const float v00 = __ldg(p0), v01 = __ldg(p0 + dc);
-  const float v10 = __ldg(p0 + dr), v11 = __ldg(p0 + dr + dc);
-  // a corner is "good" when on the grid and valid
-  const bool g00 = r0in && c0in && v00 == v00;
-  const bool g01 = r0in && c1in && v01 == v01;
-  const bool g10 = r1in && c0in && v10 == v10;
-  const bool g11 = r1in && c1in && v11 == v11;
-  const bool affected = !g00 || (e.fyp && !g01) || (e.fxp && !g10) || (e.fxp && e.fyp && !g11);
-  if (!affected) return 0.f;
-  // exact (trial_global's rules)
-  const bool m00 = g00;
-  const bool m01 = e.fyp && g01;
-  const bool m10 = e.fxp && g10;
-  const bool m11 = e.fxp && e.fyp && g11;
-  float den = m00 ? e.w00 : 0.f;
-  float num = m00 ? e.w00 * v00 : 0.f;
-  den += m01 ? e.w01 : 0.f;
-  num = fmaf(m01 ? e.w01 : 0.f, m01 ? v01 : 0.f, num);
-  den += m10 ? e.w10 : 0.f;
-  num = fmaf(m10 ? e.w10 : 0.f, m10 ? v10 : 0.f, num);
-  den += m11 ? e.w11 : 0.f;
-  num = fmaf(m11 ? e.w11 : 0.f, m11 ? v11 : 0.f, num);
-  const float rx = fmaf(-e.W, __fdividef(num, den), e.I);
-  const bool ok = rin && cin && (m00 || m01 || m10 || m11);
-  const float exact = ok ? e.fwv * (rx * rx) : e.fb;
-  // the engine's: every corner weighted, invalid / off-grid ones as 0
-  float vf = g00 ? e.w00 * v00 : 0.f;
-  vf = fmaf(e.w01, g01 ? v01 : 0.f, vf);
-  vf = fmaf(e.w10, g10 ? v10 : 0.f, vf);
-  vf = fmaf(e.w11, g11 ? v11 : 0.f, vf);
-  const float rf = fmaf(-e.W, vf, e.I);
-  return exact - e.fwv * (rf * rf);
-}
-
 // trial_global for a cell whose 2x2 corners are all on the grid (the caller
 // checked the whole patch): no bounds tests or clamps, identical arithmetic.
 __device__ __forceinline__ float trial_interior(const float* __restrict__ p0, int of,
@@ -314,23 +265,6 @@ __device__ __forceinline__ float trial_patch(float v00, float v01, float v10, fl
 
 
 
-
-// trial_correction from four corner values in registers (NaN-encoded, the
-// off-grid marker kOffGrid is a NaN too): (exact - engine) when a weighted
-// corner is invalid or off the grid, else 0.
-__device__ __forceinline__ float trial_patch_correction(float v00, float v01, float v10, float v11,
-                                                        const ExactSample& e) {
-  const bool g00 = v00 == v00, g01 = v01 == v01, g10 = v10 == v10, g11 = v11 == v11;
-  const bool affected = !g00 || (e.fyp && !g01) || (e.fxp && !g10) || (e.fxp && e.fyp && !g11);
-  if (!affected) return 0.f;
-  const float exact = trial_patch(v00, v01, v10, v11, e);
-  float vf = g00 ? e.w00 * v00 : 0.f;
-  vf = fmaf(e.w01, g01 ? v01 : 0.f, vf);
-  vf = fmaf(e.w10, g10 ? v10 : 0.f, vf);
-  vf = fmaf(e.w11, g11 ? v11 : 0.f, vf);
-  const float rf = fmaf(-e.W, vf, e.I);
-  return exact - e.fwv * (rf * rf);
-}
 
 // float64 3x3 least-squares paraboloid (recon.py:183-207); e is row-major
 // [ss offset -1,0,1][fs offset -1,0,1].  Offsets clipped to [-1, 1]; (0,0)
