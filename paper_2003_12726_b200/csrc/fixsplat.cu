@@ -367,8 +367,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
               const int dl[4] = {0, 1, nc, nc + 1};
               const double sAnb = sAn * 0x1p20;
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (q > 0 && cw[q] == 0.0) continue;
+              for (int q = 0; q < 4; ++q) {   // (a zero-weight corner adds 0: no branch)
                 if (ERR) {
                   const bool band = plane_band(sAn, cw[q]);
                   region_term<NV * RC>(slo, l + dl[q] + (band ? kBandV * RC : 0), band ? sAnb : sAn,
@@ -412,7 +411,6 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass
                 const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  if (q > 0 && cwb[q] == 0.0) continue;
                   region_term<NV * RC>(slo, l + dl[q] + 2 * RC, sBn, cwb[q]);
                   region_term<NV * RC>(slo, l + dl[q] + 3 * RC, sBd, cwb[q]);
                 }
