@@ -32,13 +32,25 @@ namespace {
 
 constexpr int kXR = 16, kXC = 32, kXT = 256, kXW = kXT / 32;  // tile, threads, warps
 constexpr int kXB = 8;        // frames per batch
-constexpr int kXTab = 256;    // frames per shared frame-table chunk (multiple of kXB)
+#ifndef PXST_FIX_TAB
+#define PXST_FIX_TAB 128
+#endif
+constexpr int kXTab = PXST_FIX_TAB;   // frames per shared frame-table chunk (multiple of kXB)
 
 // Region values: mode 0 object num, den; modes 1, 2 plane num, den, plane
 // num fine band (see plane_band); mode 2 adds the next object's num, den.
+#ifndef PXST_FIX_RC1
+#define PXST_FIX_RC1 2048
+#endif
+#ifndef PXST_FIX_RC2
+#define PXST_FIX_RC2 1280
+#endif
+#ifndef PXST_FIX_OCC12
+#define PXST_FIX_OCC12 3
+#endif
 template <int MODE> struct FixCfg { static constexpr int NV = 2, RC = 3072; };
-template <> struct FixCfg<1> { static constexpr int NV = 3, RC = 3072; };
-template <> struct FixCfg<2> { static constexpr int NV = 5, RC = 2048; };
+template <> struct FixCfg<1> { static constexpr int NV = 3, RC = PXST_FIX_RC1; };
+template <> struct FixCfg<2> { static constexpr int NV = 5, RC = PXST_FIX_RC2; };
 
 template <int MODE>
 constexpr size_t fix_smem_bytes() {
@@ -117,7 +129,7 @@ __device__ __forceinline__ bool plane_band(double scaled, double w) {
 #define PXST_FIX_OCC0 3
 #endif
 template <int MODE>
-__global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : 2) k_fix_pass(FixArgs a) {
+__global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC12) k_fix_pass(FixArgs a) {
   constexpr int NV = FixCfg<MODE>::NV, RC = FixCfg<MODE>::RC;
   constexpr bool ERR = MODE != 0;
   extern __shared__ __align__(16) unsigned char fx_raw[];
