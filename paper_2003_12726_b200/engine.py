@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import math
 import weakref
+import zlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -410,8 +411,9 @@ class DeviceScan:
         drop-in API uploads a pixel map / translation set once, and a map it
         returned is found again on the device (see remember)."""
         key = tuple(_ScanCache._ident(a) for a in arrays)
-        for k, refs, val in self._uploads:
-            if k == key and all(r() is not None for r in refs):
+        fps = tuple(_ScanCache._fp(a) for a in arrays)
+        for k, refs, val, fp in self._uploads:
+            if k == key and fp == fps and all(r() is not None for r in refs):
                 return val
         val = make()
         self.remember(arrays, val)
@@ -419,7 +421,9 @@ class DeviceScan:
 
     def remember(self, arrays, val) -> None:
         key = tuple(_ScanCache._ident(a) for a in arrays)
-        self._uploads.append((key, [_ScanCache._ref(a) for a in arrays], val))
+        fps = tuple(_ScanCache._fp(a) for a in arrays)
+        self._uploads = [e for e in self._uploads if e[0] != key]
+        self._uploads.append((key, [_ScanCache._ref(a) for a in arrays], val, fps))
         del self._uploads[:-8]
 
     def upload_u(self, u, cache: bool = False) -> torch.Tensor:
@@ -748,6 +752,19 @@ class _ScanCache:
         return (id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str, a.strides)
 
     @staticmethod
+    def _fp(a) -> int:
+        """Content fingerprint: CRC-32 of <= 4097 evenly strided elements
+        (tens of microseconds even for a config-3 stack).  An array mutated in
+        place between calls is caught when a sampled element changed; the
+        caches then re-upload instead of returning stale device data."""
+        flat = np.asarray(a).reshape(-1)
+        if flat.size == 0:
+            return 0
+        step = max(1, flat.size // 4096)
+        sample = np.concatenate([flat[::step], flat[-1:]])
+        return zlib.crc32(np.ascontiguousarray(sample).view(np.uint8))
+
+    @staticmethod
     def _ref(a):
         try:
             return weakref.ref(a)
@@ -759,24 +776,28 @@ class _ScanCache:
         arrays = (frames, scan.good_frames, w.w, m.mask)
         key = tuple(self._ident(a) for a in arrays) + (
             None if roi is None else clip_roi(roi, scan.shape),)
+        fps = tuple(self._fp(a) for a in arrays)
         if self.enabled:
             # every keyed array is held by a weak reference: an identity match
-            # with all of them alive cannot be a recycled address
-            for k, refs, ds in self.entries:
+            # with all of them alive cannot be a recycled address; the content
+            # fingerprints catch arrays mutated in place since
+            self.entries = [e for e in self.entries
+                            if not (e[0] == key and e[3] != fps)]
+            for k, refs, ds, fp in self.entries:
                 if k == key and all(r() is not None for r in refs):
                     return ds
         frames_dev = upload = None
         if self.enabled:
             # reuse an uploaded stack when only W / mask / ROI / good frames differ
             # (with its upload events: the copy may still be running)
-            for k, refs, ds in self.entries:
-                if k[0] == key[0] and refs[0]() is not None:
+            for k, refs, ds, fp in self.entries:
+                if k[0] == key[0] and refs[0]() is not None and fp[0] == fps[0]:
                     frames_dev, upload = ds.frames, ds._upload
                     break
         ds = DeviceScan(frames, scan.good_frames, w.w, m.mask, roi, frames_dev=frames_dev,
                         frames_upload=upload)
         if self.enabled:
-            self.entries.append((key, [self._ref(a) for a in arrays], ds))
+            self.entries.append((key, [self._ref(a) for a in arrays], ds, fps))
             del self.entries[:-self.max_entries]
         return ds
 

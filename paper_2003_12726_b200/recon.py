@@ -31,7 +31,7 @@ from .data_model import (
     ScanData,
     Whitefield,
 )
-from .engine import SCAN_CACHE, DeviceRef, DeviceScan, to_host, to_host_many
+from .engine import SCAN_CACHE, DeviceRef, DeviceScan, _ScanCache, to_host, to_host_many
 
 # Relative floor applied to per-pixel intensity variances (recon.py:34).
 VAR_EPS_REL = 1e-8
@@ -108,21 +108,23 @@ class LoopResult:
 # device reference-image cache: ReferenceImages produced here keep their
 # device copy, so a make_reference -> update_pixel_map chain never re-uploads.
 # ---------------------------------------------------------------------------
-_REF_CACHE: dict[int, tuple[weakref.ref, weakref.ref, DeviceRef]] = {}
+_REF_CACHE: dict[int, tuple] = {}
 
 
 def _remember(ref: ReferenceImage, dref: DeviceRef) -> None:
-    for k in [k for k, (a, b, _) in _REF_CACHE.items() if a() is None or b() is None]:
+    for k in [k for k, (a, b, _, _) in _REF_CACHE.items() if a() is None or b() is None]:
         del _REF_CACHE[k]
-    _REF_CACHE[id(ref.i_ref)] = (weakref.ref(ref.i_ref), weakref.ref(ref.wsum), dref)
+    fp = (_ScanCache._fp(ref.i_ref), _ScanCache._fp(ref.wsum))
+    _REF_CACHE[id(ref.i_ref)] = (weakref.ref(ref.i_ref), weakref.ref(ref.wsum), dref, fp)
 
 
 def _device_ref(ref, ds: DeviceScan) -> DeviceRef:
     hit = _REF_CACHE.get(id(ref.i_ref))
     if hit is not None:
-        a, b, dref = hit
+        a, b, dref, fp = hit
         if a() is ref.i_ref and b() is ref.wsum and tuple(dref.origin) == tuple(ref.origin) \
-                and dref.fm.device == ds.device:
+                and dref.fm.device == ds.device \
+                and fp == (_ScanCache._fp(ref.i_ref), _ScanCache._fp(ref.wsum)):
             return dref
     return DeviceRef.from_host(ref.i_ref, ref.wsum, ref.origin, ds.device)
 

@@ -132,3 +132,27 @@ def test_pixel_map_never_worse_than_incumbent(half):
     _, e1 = pb.update_pixel_map(sc, w, m, ref, u, t, pb.SearchWindow(half, half))
     # equal where the incumbent wins, up to the engines' float32 sum order
     assert np.all(e1 <= e0 * (1 + 1e-5) + 1e-12)
+
+
+def test_in_place_mutation_detected(scan0):
+    """The device caches are keyed by array identity (value-object convention,
+    data_model.py:13) plus a sampled content fingerprint: an input mutated in
+    place between calls is re-uploaded, never served stale."""
+    import copy
+    s = copy.deepcopy(scan0)
+    ref1 = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
+    s.scan.frames[3] *= 1.5                      # same array object, new content
+    ref2 = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
+    pb.clear_cache()
+    ref3 = pb.make_reference(s.scan, s.w, s.m, s.u0, s.t0)
+    assert not np.array_equal(ref1.i_ref, ref2.i_ref)
+    np.testing.assert_array_equal(ref2.i_ref, ref3.i_ref)
+    u = pb.PixelMap(s.u0.u.copy())
+    win = pb.SearchWindow(2, 2)
+    a, _ = pb.update_pixel_map(s.scan, s.w, s.m, ref3, u, s.t0, win)
+    u.u[0] += 0.25                               # mutate the pixel map in place
+    b, _ = pb.update_pixel_map(s.scan, s.w, s.m, ref3, u, s.t0, win)
+    pb.clear_cache()
+    c, _ = pb.update_pixel_map(s.scan, s.w, s.m, ref3, u, s.t0, win)
+    np.testing.assert_array_equal(b.u, c.u)
+    assert not np.array_equal(a.u, b.u)
