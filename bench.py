@@ -286,8 +286,10 @@ class Sequence:
                 k3 = ev if (ev and not cfg.update_pixel_map) else ev3
                 if k3:
                     k3[0].record(stream)
+                grow = 2 * (max(cfg.half_ss, cfg.half_fs) + 1) if cfg.update_pixel_map else 0
                 di_new, dj_new = ds.translation_search(dref, u_new, di, dj, cfg.t_half_ss,
-                                                       cfg.t_half_fs, cfg.t_subpixel_grid)
+                                                       cfg.t_half_fs, cfg.t_subpixel_grid,
+                                                       span_hint=geom.spans3_hint(grow))
                 if k3:
                     k3[1].record(stream)
             if state["it"] + 1 < cfg.iters:        # the sequence continues: fuse K4 + next K1

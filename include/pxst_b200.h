@@ -211,6 +211,20 @@ int pxst_translation_search(const pxst_scan* scan, const pxst_stats* st, const p
                             int64_t frame_lo, int64_t frame_hi, double* di_out,
                             double* dj_out, double* err_out, void* stream);
 
+/* Same, with K3's TMA box sized from span_hint (host int32[2], from
+ * pxst_tile_spans3 of this u or a bound of it) instead of a device->host
+ * read inside the call; a hint that does not match u costs speed only. */
+int pxst_translation_search_ex(const pxst_scan* scan, const pxst_stats* st, const pxst_ref* ref,
+                               const double* u, const double* di, const double* dj,
+                               int64_t half_ss, int64_t half_fs, double subpixel_step,
+                               int64_t frame_lo, int64_t frame_hi, double* di_out,
+                               double* dj_out, double* err_out, const int32_t* span_hint,
+                               void* stream);
+
+/* Largest row / column extent of u over K3's 16x64-pixel tiles (device
+ * int32[2], no host wait): the span hint of pxst_translation_search_ex. */
+int pxst_tile_spans3(const pxst_scan* scan, const double* u, int32_t* spans, void* stream);
+
 /* Quanta of the reference-plane accumulators (see pxst_accum): q_num from
  * the bound (max|I| + max W max(1, max|ref|))^2 / min sigma2 on eps, q_den
  * from 1 (weight 1).  Row shards must share the full scan's quanta. */

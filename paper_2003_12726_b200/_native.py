@@ -83,6 +83,11 @@ _SIGS = {
                                         c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                         c_double, c_int64, c_int64, c_void_p, c_void_p,
                                         c_void_p, c_void_p]),
+    "pxst_translation_search_ex": (c_int, [POINTER(PxstScan), POINTER(PxstStats),
+                                           POINTER(PxstRef), c_void_p, c_void_p, c_void_p,
+                                           c_int64, c_int64, c_double, c_int64, c_int64,
+                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_tile_spans3": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p]),
     "pxst_error_maps": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p]),

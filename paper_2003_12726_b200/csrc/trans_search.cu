@@ -553,12 +553,58 @@ FastKernel find_fast(int ka, int kb) {
 
 using namespace pxst;
 
+namespace {
+int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref,
+                       const double* u, const double* di, const double* dj, int64_t half_ss,
+                       int64_t half_fs, double subpixel_step, int64_t frame_lo, int64_t frame_hi,
+                       double* di_out, double* dj_out, double* err_out, const int32_t* span_hint,
+                       void* stream);
+}
+
 extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st,
                                        const pxst_ref* ref, const double* u, const double* di,
                                        const double* dj, int64_t half_ss, int64_t half_fs,
                                        double subpixel_step, int64_t frame_lo, int64_t frame_hi,
                                        double* di_out, double* dj_out, double* err_out,
                                        void* stream) {
+  return translation_search(sc, st, ref, u, di, dj, half_ss, half_fs, subpixel_step, frame_lo,
+                            frame_hi, di_out, dj_out, err_out, nullptr, stream);
+}
+
+extern "C" int pxst_translation_search_ex(const pxst_scan* sc, const pxst_stats* st,
+                                          const pxst_ref* ref, const double* u, const double* di,
+                                          const double* dj, int64_t half_ss, int64_t half_fs,
+                                          double subpixel_step, int64_t frame_lo,
+                                          int64_t frame_hi, double* di_out, double* dj_out,
+                                          double* err_out, const int32_t* span_hint,
+                                          void* stream) {
+  return translation_search(sc, st, ref, u, di, dj, half_ss, half_fs, subpixel_step, frame_lo,
+                            frame_hi, di_out, dj_out, err_out, span_hint, stream);
+}
+
+extern "C" int pxst_tile_spans3(const pxst_scan* sc, const double* u, int32_t* spans,
+                                void* stream) {
+  if (int e = check_scan(sc)) return e;
+  PXST_REQUIRE(u && spans, "NULL pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
+  const int n_ct = static_cast<int>((cw + kTC - 1) / kTC);
+  const int64_t n_bands = (rw + kTR - 1) / kTR;
+  PXST_REQUIRE(n_bands <= kMaxGridY, "ROI too tall");
+  Scratch geo;
+  if (int e = geo.alloc(sizeof(TileGeo) * n_ct * n_bands, s)) return e;
+  k_tile_geo3<<<dim3((unsigned)n_ct, (unsigned)n_bands), kThreads, 0, s>>>(*sc, u,
+                                                                            geo.as<TileGeo>());
+  PXST_CHECK_LAUNCH();
+  return tile_span_max_dev(geo.as<TileGeo>(), (int64_t)n_ct * n_bands, spans, s);
+}
+
+namespace {
+int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* ref,
+                       const double* u, const double* di, const double* dj, int64_t half_ss,
+                       int64_t half_fs, double subpixel_step, int64_t frame_lo, int64_t frame_hi,
+                       double* di_out, double* dj_out, double* err_out, const int32_t* span_hint,
+                       void* stream) {
   if (int e = check_scan(sc)) return e;
   if (int e = check_ref(ref)) return e;
   PXST_REQUIRE(st && st->frame_norm, "stats descriptor is NULL");
@@ -650,7 +696,12 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
     // Box from the largest tile footprint, <= 256 columns and <= 40 KB per
     // slot; tiles beyond the cap take the exact path.
     int span[2];
-    if (int e = tile_span_max(geo.as<TileGeo>(), a.n_tiles, span, s)) return e;
+    if (span_hint) {             // from pxst_tile_spans3; a stale hint only costs speed
+      span[0] = span_hint[0];
+      span[1] = span_hint[1];
+    } else if (int e = tile_span_max(geo.as<TileGeo>(), a.n_tiles, span, s)) {
+      return e;
+    }
     a.box_r = max(a.box_r, span[0] + need_rows3(max_ka));
     a.box_c = max(a.box_c, span[1] + need_cols3(max_kb));
     a.box_c = (a.box_c + 3) / 4 * 4;
@@ -746,3 +797,4 @@ extern "C" int pxst_translation_search(const pxst_scan* sc, const pxst_stats* st
   }
   return PXST_OK;
 }
+}  // namespace

@@ -189,6 +189,15 @@ class GeometryFuture:
         self._event.synchronize()
         return self._host2.data_ptr()
 
+    def spans3_hint(self, grow: int = 0):
+        """K3's span hint (host int32[2]) of this geometry's u, widened by
+        `grow` rows / columns (a bound for a map moved by <= grow / 2 px)."""
+        self._event.synchronize()
+        h = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        h[0] = int(self._host2[2]) + grow
+        h[1] = int(self._host2[3]) + grow
+        return h
+
 
 class PendingObject:
     """Next-iteration object accumulated by error_maps_and_next_object;
@@ -469,10 +478,10 @@ class DeviceScan:
         ready.record(main)
         side.wait_event(ready)
         host8 = torch.empty(8, dtype=torch.float64, pin_memory=True)
-        host2 = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        host2 = torch.empty(4, dtype=torch.int32, pin_memory=True)
         with torch.cuda.stream(side):
             dev8 = torch.empty(8, dtype=torch.float64, device=self.device)
-            dev2 = torch.empty(2, dtype=torch.int32, device=self.device)
+            dev2 = torch.empty(4, dtype=torch.int32, device=self.device)
             grid = torch.empty(4, dtype=torch.int64, device=self.device)
             sp = stream_ptr(side)
             check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
@@ -483,12 +492,14 @@ class DeviceScan:
             host8.copy_(dev8, non_blocking=True)
             check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
                                            dev2.data_ptr(), sp))
+            check(self.lib.pxst_tile_spans3(ctypes.byref(self.c_scan), u_t.data_ptr(),
+                                            dev2[2:].data_ptr(), sp))
             host2.copy_(dev2, non_blocking=True)
             done = torch.cuda.Event()
             done.record(side)
         for t in (u_t, di_t, dj_t):
             t.record_stream(side)
-        TRANSFER["d2h"] += 8 * 8 + 2 * 4
+        TRANSFER["d2h"] += 8 * 8 + 4 * 4
         return GeometryFuture(host8, host2, done, grid, grid_ready)
 
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
@@ -589,7 +600,10 @@ class DeviceScan:
 
     # ------------------------------------------------------- K3 translations
     def translation_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
-                           subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None):
+                           subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None,
+                           span_hint=None):
+        """span_hint: GeometryFuture.spans3_hint(...) (host int32[2]) or None
+        (the call then reads K3's tile spans from the device, a stream sync)."""
         self.ready(frame_stats=True)
         di_out = di_t.clone()
         dj_out = dj_t.clone()
@@ -597,11 +611,11 @@ class DeviceScan:
             return di_out, dj_out
         hi = self.n_good if frame_hi is None else frame_hi
         c_ref = ref.struct()
-        check(self.lib.pxst_translation_search(
+        check(self.lib.pxst_translation_search_ex(
             ctypes.byref(self.c_scan), ctypes.byref(self.c_stats), ctypes.byref(c_ref),
             u_t.data_ptr(), di_t.data_ptr(), dj_t.data_ptr(), int(half_ss), int(half_fs),
             float(subpixel_grid or 0.0), int(frame_lo), int(hi), di_out.data_ptr(),
-            dj_out.data_ptr(), _ptr(err_out), stream_ptr()))
+            dj_out.data_ptr(), _ptr(err_out), _ptr(span_hint), stream_ptr()))
         return di_out, dj_out
 
     # ------------------------------------------------------- shard views / K4

@@ -289,8 +289,12 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         ds.regularise(u_t, st.options)
         if st.update_translations:
             tw = st.translation_window
+            # K3's TMA box from this iteration's geometry (u before the pixel-map
+            # update, which moves a pixel by <= half + 1 px): no stream sync
+            grow = 2 * (max(st.window.half_ss, st.window.half_fs) + 1)
             di_t, dj_t = ds.translation_search(dref, u_t, di_t, dj_t, tw.half_ss, tw.half_fs,
-                                               tw.subpixel_grid)
+                                               tw.subpixel_grid,
+                                               span_hint=gfut.spans3_hint(grow))
         gfut = ds.geometry_async(u_t, di_t, dj_t)       # next iteration's, overlaps K4
         if i + 1 < max_iters:
             metrics, nref = ds.error_maps_and_next_object(dref, u_t, di_t, dj_t, gfut)
