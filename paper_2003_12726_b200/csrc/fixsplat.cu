@@ -373,6 +373,10 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
             // over the axes with a nonzero fraction)
             const bool hot = REG && (fx > 0.0 ? fmin(fx, gx) : 1.0) * (fy > 0.0 ? fmin(fy, gy) : 1.0) >=
                                         kFineW;
+            // warp-uniform: skip the r0+1 / c0+1 corners when no lane weights
+            // them (config 2: u_ss = x, every fx = 0)
+            const bool need_r1 = __any_sync(0xffffffffu, inA && hot && fx > 0.0);
+            const bool need_c1 = __any_sync(0xffffffffu, inA && hot && fy > 0.0);
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
               PXST_DCHECK(r0 >= R0 && c0 >= C0 && l >= 0 && l + nc + 1 < ncell);
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               const double sAnb = sAn * 0x1p20;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {   // (a zero-weight corner adds 0: no branch)
+                if (((q & 2) && !need_r1) || ((q & 1) && !need_c1)) continue;
                 if (ERR) {
                   const bool band = plane_band(sAn, cw[q]);
                   region_term<NV * RC>(slo, l + dl[q] + (band ? kBandV * RC : 0), band ? sAnb : sAn,
@@ -416,6 +421,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
               const bool hotb = REG && (fxb > 0.0 ? fmin(fxb, gxb) : 1.0) *
                                                (fyb > 0.0 ? fmin(fyb, gyb) : 1.0) >= kFineW;
+              const bool need_r1b = __any_sync(0xffffffffu, inB && hotb && fxb > 0.0);
+              const bool need_c1b = __any_sync(0xffffffffu, inB && hotb && fyb > 0.0);
               if (inB && hotb) {
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
                 const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
@@ -423,6 +430,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
                 const int dl[4] = {0, 1, nc, nc + 1};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                  if (((q & 2) && !need_r1b) || ((q & 1) && !need_c1b)) continue;
                   region_term<NV * RC>(slo, l + dl[q] + 2 * RC, sBn, cwb[q]);
                   region_term<NV * RC>(slo, l + dl[q] + 3 * RC, sBd, cwb[q]);
                 }

@@ -422,8 +422,12 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       PXST_DCHECK(!fast || (sm.lr >= 0 && sm.lr + KA + 1 <= a.box_r && sm.lc >= 0 &&
                             sm.lc + KB + 1 <= a.box_c));
       if (kAhead) s_n = sample_of(jj + 1 < nk ? jj + 1 : jj, I_n, fw_n);
-      engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
-                           acc);
+      if (KA == 1 && __all_sync(0xffffffffu, fx == 0.f))   // warp-uniform (config 2)
+        engine_row1<KB>(ring + b * box + off, fy, sW, sI,
+                        reinterpret_cast<PackedAcc<1, KB>&>(acc));
+      else
+        engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
+                             acc);
       mbar_arrive(&empty[b]);
       if (PXST_K2_PRODUCER == 0 && threadIdx.x == 0 && jj + kNB < nk) {
         mbar_wait(&empty[b], ph);      // every thread is done with this slot

@@ -149,6 +149,33 @@ __device__ __forceinline__ void engine_fast2(const float* __restrict__ win, int 
   }
 }
 
+// One-row engine for KA == 1 windows when the sample's ss fraction is 0:
+// the r0 + 1 corners carry zero weight (B = 0), so the second patch row and
+// its half of each trial drop out (config 2: u_ss = x and no ss scan, every
+// fx = 0).  Same values as engine_fast2 with B = 0.
+template <int KB>
+__device__ __forceinline__ void engine_row1(const float* __restrict__ win, float fy, float A,
+                                            float I, PackedAcc<1, KB>& acc) {
+  constexpr int NP = PackedAcc<1, KB>::NP;
+  constexpr bool ODD = PackedAcc<1, KB>::ODD;
+  fy = fminf(fy, 0x1.fffffep-1f);
+  const float gy = 1.f - fy;
+  const float rho = fy * rcp_approx(gy);
+  const float Ap = A * gy;
+  const f32x2 nA2 = pack2(-Ap, -Ap), I2 = pack2(I, I);
+  PatchRow<KB> row;
+  row.load(win, rho);
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const f32x2 r = ffma2(nA2, row.h[k], I2);
+    acc.p[0][k] = ffma2(r, r, acc.p[0][k]);
+  }
+  if (ODD) {
+    const float r = fmaf(-Ap, row.hs, I);
+    acc.s[0] = fmaf(r, r, acc.s[0]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Exact trials (the slow fix-up kernels), read from a float32 copy of the
 // reference with NaN on invalid cells (make_pv's fmn), so one load gives value
