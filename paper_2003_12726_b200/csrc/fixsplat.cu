@@ -98,6 +98,16 @@ struct TermSink {
 
 // A term into the region's limbs (coarse, corner weight >= kFineW): lo at
 // slo[idx], hi at slo[idx + HI] (HI = NV * RC words, an immediate offset).
+// Every nonzero corner weight >= kFineW: the smallest nonzero one is
+// min(fx, 1-fx) min(fy, 1-fy) over the axes with a nonzero fraction
+// (float32 classification; exact fractions 0 stay 0).
+__device__ __forceinline__ bool small_corner_ok(double fx, double fy) {
+  const float x = static_cast<float>(fx), y = static_cast<float>(fy);
+  const float mx = x > 0.f ? fminf(x, 1.f - x) : 1.f;
+  const float my = y > 0.f ? fminf(y, 1.f - y) : 1.f;
+  return mx * my >= static_cast<float>(kFineW) * 1.0001f;
+}
+
 template <int HI>
 __device__ __forceinline__ void region_term(unsigned* slo, int idx, double scaled, double w) {
   PXST_DCHECK(idx >= 0 && idx < HI);
@@ -141,6 +151,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   __shared__ double s_red[kXW][4];
   __shared__ double s_frw[ERR ? kXW : 1][ERR ? kXTab : 1];   // per-frame sums of each warp
   __shared__ int s_cmax;
+  __shared__ int4 s_sess[2];   // session footprint (R0, R1, C0, C1), (end frame, region)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
@@ -254,7 +265,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   constexpr int kBandV = MODE == 2 ? 4 : 2;        // the plane numerator's fine band
   const TermSink kAnB{slo + kBandV * RC, shi + kBandV * RC, a.A.num_f, nullptr};
   double pix[2] = {0.0, 0.0};
-  unsigned long long dropped = 0;
+  unsigned dropped = 0;
+  const bool count_drop = !ERR && a.n_drop != nullptr;
   // (mode 2: one more cell on each side of a footprint -- the next grid's
   // positions are rounded separately, recon.py:138 order, and may floor one
   // cell over)
@@ -280,19 +292,29 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
     __syncthreads();
     for (int s0 = 0; s0 < nt;) {
       // session: consecutive frames whose joint footprint fits the region
-      int4 fb = t_ft[s0];
-      int s1 = s0 + 1;
-      const bool region = fin && max_frames > 0 && !a.no_region &&
-                          (int64_t)(fb.y - fb.x + 1) * (fb.w - fb.z + 1) <= RC;
-      if (region) {
-        while (s1 < nt && s1 - s0 < max_frames) {
-          const int4 g = t_ft[s1];
-          const int4 u = make_int4(min(fb.x, g.x), max(fb.y, g.y), min(fb.z, g.z), max(fb.w, g.w));
-          if ((int64_t)(u.y - u.x + 1) * (u.w - u.z + 1) > RC) break;
-          fb = u;
-          ++s1;
+      // (formed by thread 0, broadcast through shared memory)
+      if (threadIdx.x == 0) {
+        int4 fb = t_ft[s0];
+        int s1 = s0 + 1;
+        const bool reg = fin && max_frames > 0 && !a.no_region &&
+                         (int64_t)(fb.y - fb.x + 1) * (fb.w - fb.z + 1) <= RC;
+        if (reg) {
+          while (s1 < nt && s1 - s0 < max_frames) {
+            const int4 g = t_ft[s1];
+            const int4 u = make_int4(min(fb.x, g.x), max(fb.y, g.y), min(fb.z, g.z),
+                                     max(fb.w, g.w));
+            if ((int64_t)(u.y - u.x + 1) * (u.w - u.z + 1) > RC) break;
+            fb = u;
+            ++s1;
+          }
         }
+        s_sess[0] = fb;
+        s_sess[1] = make_int4(s1, reg ? 1 : 0, 0, 0);
       }
+      __syncthreads();
+      const int4 fb = s_sess[0];
+      const int s1 = s_sess[1].x;
+      const bool region = s_sess[1].y != 0;
       const int R0 = fb.x, C0 = fb.z;
       const int nc = region ? fb.w - fb.z + 1 : 0;
       const int ncell = region ? (fb.y - fb.x + 1) * nc : 0;
@@ -363,7 +385,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
               sAd = qa_d;
             } else {
-              if (a.n_drop) dropped += (act && !inA) ? 1 : 0;
+              dropped += (count_drop && act && !inA) ? 1u : 0u;
               sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
               sAd = W2[e] * qa_d;
             }
@@ -371,8 +393,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
             // the others, and the direct sessions, take the per-corner path
             // (smallest nonzero corner weight = min(fx, 1-fx) min(fy, 1-fy)
             // over the axes with a nonzero fraction)
-            const bool hot = REG && (fx > 0.0 ? fmin(fx, gx) : 1.0) * (fy > 0.0 ? fmin(fy, gy) : 1.0) >=
-                                        kFineW;
+            // (classified in float32: only the routing depends on it)
+            const bool hot = REG && small_corner_ok(fx, fy);
             // warp-uniform: skip the r0+1 / c0+1 corners when no lane weights
             // them (config 2: u_ss = x, every fx = 0)
             const bool need_r1 = __any_sync(0xffffffffu, inA && hot && fx > 0.0);
@@ -419,8 +441,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
               const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
               const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
-              const bool hotb = REG && (fxb > 0.0 ? fmin(fxb, gxb) : 1.0) *
-                                               (fyb > 0.0 ? fmin(fyb, gyb) : 1.0) >= kFineW;
+              const bool hotb = REG && small_corner_ok(fxb, fyb);
               const bool need_r1b = __any_sync(0xffffffffu, inB && hotb && fxb > 0.0);
               const bool need_c1b = __any_sync(0xffffffffu, inB && hotb && fyb > 0.0);
               if (inB && hotb) {
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
     dropped += __shfl_xor_sync(0xffffffffu, dropped, 4);
     dropped += __shfl_xor_sync(0xffffffffu, dropped, 2);
     dropped += __shfl_xor_sync(0xffffffffu, dropped, 1);
-    if (lane == 0 && dropped) atomicAdd(a.n_drop, dropped);
+    if (lane == 0 && dropped) atomicAdd(a.n_drop, static_cast<unsigned long long>(dropped));
   }
 }
 
