@@ -46,7 +46,10 @@ def _unique(stack, margin=1e-4):
     return (part[1] - part[0]) > margin * np.abs(part[0])
 
 
-@pytest.mark.parametrize("cfg_id,rows", [(2, (250, 258)), (3, (500, 506))])
+@pytest.mark.parametrize("cfg_id,rows", [
+    (2, (250, 258)), (3, (500, 506)),
+    pytest.param(3, (240, 272), marks=pytest.mark.slow),   # 32 rows: two K2 tile rows
+])
 def test_pixel_map_band_vs_oracle(cfg_id, rows):
     s, frames, ds, u, di, dj, ref = _setup(cfg_id)
     cfg = s.cfg
@@ -71,11 +74,15 @@ def test_pixel_map_band_vs_oracle(cfg_id, rows):
     np.testing.assert_allclose(eg, eo[rr, cc][uniq], rtol=1e-4)
 
 
-def test_cfg3_translation_subset_vs_oracle():
+@pytest.mark.parametrize("pick", [
+    [0, 777, 1999],
+    pytest.param([0, 1, 49, 50, 313, 499, 500, 777, 1000, 1234, 1499, 1500, 1750, 1949, 1998,
+                  1999], marks=pytest.mark.slow),    # 16 frames: raster edges and interior
+])
+def test_cfg3_translation_subset_vs_oracle(pick):
     s, frames, ds, u, di, dj, ref = _setup(3)
     cfg = s.cfg
     di_o, dj_o = ds.translation_search(ref, u, di, dj, cfg.t_half_ss, cfg.t_half_fs)
-    pick = [0, 777, 1999]
     sub = np.ascontiguousarray(frames[pick].cpu().numpy())     # only these frames on host
     sub_good = np.ones(len(pick), bool)
     d_o, j_o, errs = orc.update_translations(sub, sub_good, s.w.w, s.m.mask,
