@@ -127,24 +127,7 @@ struct Sample3 {
 // Geometry of one (frame, pixel) sample for the current phase, shared by the
 // fast and slow kernels.  x_rho = (u0 - d - n0) - step*rho; trial m sits at
 // floor(x_rho) - m; the engine patch starts at floor(x_rho) - mhi.
-// Box origin (row, 16-byte aligned column) of a tile for the frame at
-// (dI, dJ) and the current phase: the same for every sample of the tile.
-struct Origin3 {
-  int wr0, wc0;
-  bool fits;
-};
-__device__ __forceinline__ Origin3 tile_origin3(const TransArgs& a, const TileGeo& g, double dI,
-                                                double dJ) {
-  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
-  Origin3 o;
-  o.fits = tile_fits(g, need_rows3(a.ka), need_cols3(a.kb), a.box_r, a.box_c);
-  o.wr0 = o.fits ? static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a : 0;
-  o.wc0 = o.fits ? align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b)
-                 : 0;
-  return o;
-}
-
-__device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const Origin3& o, double u0,
+__device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const TileGeo& g, double u0,
                                                 double u1, double dI, double dJ) {
   const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
   Sample3 s;
@@ -158,9 +141,11 @@ __device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const Origin
   s.j = finite ? static_cast<int>(yf) : -(1 << 30);
   s.fast = false;
   s.lr = s.lc = 0;
-  if (o.fits) {
-    s.lr = s.i - a.mhi_a - o.wr0;
-    s.lc = s.j - a.mhi_b - o.wc0;
+  if (tile_fits(g, need_rows3(a.ka), need_cols3(a.kb), a.box_r, a.box_c)) {
+    const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
+    const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
+    s.lr = s.i - a.mhi_a - wr0;
+    s.lc = s.j - a.mhi_b - wc0;
     s.fast = s.i >= 0 && s.i < a.os && s.j >= 0 && s.j < a.of &&
              a.pv[(int64_t)s.i * a.of + s.j] != 0 && s.lr >= 0 && s.lr + a.ka + 1 <= a.box_r &&
              s.lc >= 0 && s.lc + a.kb + 1 <= a.box_c;
@@ -270,7 +255,6 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
     const int b = static_cast<int>(it % kNB);
     const unsigned ph = static_cast<unsigned>((it / kNB) & 1);
     const TileGeo g = a.geo[it];
-    const Origin3 org = tile_origin3(a, g, dI, dJ);    // once per tile, not per sample
     Raw3 cur;
     if (kPipe) {
       cur = nxt;
@@ -286,8 +270,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
       const bool live = cur.live[e];
       I[e] = live ? cur.I[e] : 0.f;
       W[e] = live ? cur.W[e] : 0.f;
-      const Sample3 sm = make_sample3(a, org, live ? cur.u0[e] : 0.0, live ? cur.u1[e] : 0.0, dI,
-                                      dJ);
+      const Sample3 sm = make_sample3(a, g, live ? cur.u0[e] : 0.0, live ? cur.u1[e] : 0.0, dI, dJ);
       fx[e] = static_cast<float>(sm.fx);
       fy[e] = static_cast<float>(sm.fy);
       off[e] = (live && sm.fast) ? sm.lr * a.box_c + sm.lc : -1;
@@ -385,7 +368,6 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
       const int64_t band = it / a.n_ct;
       const int ct = static_cast<int>(it % a.n_ct);
       const TileGeo g = a.geo[it];
-      const Origin3 org = tile_origin3(a, g, dI, dJ);
       const int64_t r_lo = a.sc.roi[0] + band * kTR;
       const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
       const int64_t c_lo = (int64_t)ct * kTC;
@@ -402,7 +384,7 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
           const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
           const int64_t p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
           if (a.sc.work[p]) {
-            sl = make_sample3(a, org, a.u[p], a.u[plane + p], dI, dJ);
+            sl = make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ);
             slow = !sl.fast;
             if (slow) {
               Il = __ldg(frame + p);
