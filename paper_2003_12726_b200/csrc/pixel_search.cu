@@ -238,6 +238,78 @@ __device__ __forceinline__ void window_origin(const PixArgs& a, const TileGeo& g
   wc0 = align4_down(static_cast<int>(floor(g.umin1 - dJ - static_cast<double>(a.m0))) - rb);
 }
 
+// Sample geometry from precomputed splits (what the fast kernel and the
+// fast / slow classification use): u = iu + fu per pixel (once per thread)
+// and d + origin = id + fd per frame (once per CTA, in the frame table), so
+// x = u - d - origin = (iu - id) + (fu - fd) costs one float32 subtract and a
+// carry instead of the float64 split.  The base may differ from the float64
+// floor by one where x is within ~1e-7 of an integer; the trial positions
+// x + a, and so the bilinear values (continuous there: these samples' patches
+// are valid and on the grid, or they go to the fix-up, which re-derives the
+// exact float64 split), are the same.
+struct USplit {
+  int i0, i1;
+  float f0, f1;
+  bool ok;
+};
+__device__ __forceinline__ USplit split_u(double u0, double u1) {
+  USplit s;
+  s.ok = fabs(u0) < 1e9 && fabs(u1) < 1e9;
+  const double a = s.ok ? floor(u0) : 0.0, b = s.ok ? floor(u1) : 0.0;
+  s.i0 = static_cast<int>(a);
+  s.i1 = static_cast<int>(b);
+  s.f0 = s.ok ? static_cast<float>(u0 - a) : 0.f;
+  s.f1 = s.ok ? static_cast<float>(u1 - b) : 0.f;
+  return s;
+}
+// frame split packed as int4 (i0, i1, bits of f0, bits of f1) of d + origin
+__device__ __forceinline__ int4 split_d(double dI, double dJ, int64_t n0, int64_t m0) {
+  const double x = dI + static_cast<double>(n0), y = dJ + static_cast<double>(m0);
+  const bool ok = fabs(x) < 1e9 && fabs(y) < 1e9;
+  const double a = ok ? floor(x) : 0.0, b = ok ? floor(y) : 0.0;
+  return make_int4(ok ? static_cast<int>(a) : (1 << 30), static_cast<int>(b),
+                   __float_as_int(ok ? static_cast<float>(x - a) : 0.f),
+                   __float_as_int(ok ? static_cast<float>(y - b) : 0.f));
+}
+
+template <bool kKnownFit = false, int KA_ = 0, int KB_ = 0, int BC_ = 0>
+__device__ __forceinline__ Sample make_sample_split(const PixArgs& a, const TileGeo& g,
+                                                    const USplit& us, int4 ds, float fwv,
+                                                    int wr0, int wc0) {
+  const int ka = KA_ > 0 ? KA_ : a.ka, kb = KB_ > 0 ? KB_ : a.kb;
+  const int box_c = BC_ > 0 ? BC_ : a.box_c;
+  const int ra = (ka - 1) / 2, rb = (kb - 1) / 2;
+  Sample s;
+  s.fwv = fwv;
+  float dx = us.f0 - __int_as_float(ds.z), dy = us.f1 - __int_as_float(ds.w);
+  int i = us.i0 - ds.x, j = us.i1 - ds.y;
+  if (dx < 0.f) { dx += 1.f; --i; }
+  if (dy < 0.f) { dy += 1.f; --j; }
+  if (dx >= 1.f) { dx = 0.f; ++i; }
+  if (dy >= 1.f) { dy = 0.f; ++j; }
+  s.fx = dx;
+  s.fy = dy;
+  const bool finite = us.ok && ds.x != (1 << 30);
+  s.i = finite ? i : -(1 << 30);
+  s.j = finite ? j : -(1 << 30);
+  s.pre = false;
+  s.pvb = 0;
+  s.wr0 = s.wc0 = s.lr = s.lc = 0;
+  if (kKnownFit || tile_fits(g, need_rows2(ka), need_cols2(kb), a.box_r, box_c)) {
+    s.wr0 = wr0;
+    s.wc0 = wc0;
+    s.lr = s.i - ra - s.wr0;
+    s.lc = s.j - rb - s.wc0;
+    const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
+    const bool in = static_cast<unsigned>(s.i) < static_cast<unsigned>(os) &&
+                    static_cast<unsigned>(s.j) < static_cast<unsigned>(of);
+    s.pre = in && static_cast<unsigned>(s.lr) <= static_cast<unsigned>(a.box_r - ka - 1) &&
+            static_cast<unsigned>(s.lc) <= static_cast<unsigned>(box_c - kb - 1);
+    s.pvb = __ldg(a.pv + (in ? s.i * of + s.j : 0));
+  }
+  return s;
+}
+
 // fwv is only stored (checked by fast()), so a frame-weight load issued for
 // the next frame is not waited on here.
 // KA_/KB_/BC_ > 0: the window and box width as compile-time constants (the
@@ -300,10 +372,10 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
   unsigned char* base = ring_raw + ((128u - (smem_addr(ring_raw) & 127u)) & 127u);
   float* ring = reinterpret_cast<float*>(base);
   const int box = slot_floats(a.box_r, a.box_c);          // slot stride (128-byte multiple)
-  // Per-frame table of the chunk (frame index, di, dj) after the ring.
-  double* t_di = reinterpret_cast<double*>(base + sizeof(float) * kNB * box);
-  double* t_dj = t_di + a.tbl;
-  int64_t* t_off = reinterpret_cast<int64_t*>(t_dj + a.tbl);     // frame offset f * plane
+  // Per-frame table of the chunk after the ring: the split of d + origin
+  // (int4), the frame's stack offset, the window origin.
+  int4* t_ds = reinterpret_cast<int4*>(base + sizeof(float) * kNB * box);
+  int64_t* t_off = reinterpret_cast<int64_t*>(t_ds + a.tbl);     // frame offset f * plane
   int* t_wr = reinterpret_cast<int*>(t_off + a.tbl);             // window origin per frame
   int* t_wc = t_wr + a.tbl;
 
@@ -340,8 +412,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       const int f = a.sc.good[k_lo + jj];
       const double dI = a.di[f], dJ = a.dj[f];
       t_off[jj] = f * plane;
-      t_di[jj] = dI;
-      t_dj[jj] = dJ;
+      t_ds[jj] = split_d(dI, dJ, a.n0, a.m0);
       window_origin(a, g, dI, dJ, t_wr[jj], t_wc[jj]);
     }
     auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
@@ -362,12 +433,13 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       for (int jj = 0; jj < min(kNB, nk); ++jj) issue(jj);
 
     const float W = live ? a.sc.w32[p] : 0.f;
+    const USplit us = split_u(u0, u1);
     auto sample_of = [&](int jj, float& I, float& fwv) {
       const int64_t off = t_off[jj];
       I = live ? __ldg(a.sc.frames + off + p) : 0.f;
       fwv = (live && fwp) ? __ldg(fwp + off + p) : 1.f;
-      return make_sample<true, KA, KB, BC>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f,
-                                           t_wr[jj], t_wc[jj]);
+      return make_sample_split<true, KA, KB, BC>(a, g, us, t_ds[jj], live ? fwv : -1.f,
+                                                 t_wr[jj], t_wc[jj]);
     };
     // One-frame-ahead pipeline of the per-sample geometry, stack value and
     // patch-valid lookup.  The loop body after the ring wait is one basic
@@ -523,6 +595,7 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
     const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
     const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
     const double u0 = a.u[p], u1 = a.u[plane + p];
+    const USplit us = split_u(u0, u1);
     const float W = a.sc.w32[p];
     int64_t k_lo, k_hi, pslot;
     chunk_frames(a, chunk, k_lo, k_hi, pslot);
@@ -547,8 +620,10 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
         const double dI = a.di[f], dJ = a.dj[f];
         int wr0, wc0;
         window_origin(a, g, dI, dJ, wr0, wc0);
+        // classified exactly as the fast kernel did (split geometry); the
+        // exact trials use the float64 split of the reference
+        slow = !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast();
         sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
-        slow = !sl.fast();
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
@@ -687,6 +762,7 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
     const int64_t p = (a.sc.roi[0] + rr) * a.sc.fs + a.sc.roi[2] + cc;
     const TileGeo g = a.geo[(rr / kTR) * a.tiles_x + cc / kTC];
     const double u0 = a.u[p], u1 = a.u[plane + p];
+    const USplit us = split_u(u0, u1);
     const float W = a.sc.w32[p];
     int64_t k_lo, k_hi, pslot;
     chunk_frames(a, chunk, k_lo, k_hi, pslot);
@@ -711,8 +787,10 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
         const double dI = a.di[f], dJ = a.dj[f];
         int wr0, wc0;
         window_origin(a, g, dI, dJ, wr0, wc0);
+        // classified exactly as the fast kernel did (split geometry); the
+        // exact trials use the float64 split of the reference
+        slow = !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast();
         sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
-        slow = !sl.fast();
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
@@ -1078,10 +1156,10 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.tbl = a.n_full > 0 ? static_cast<int>(sc->n_good) : a.chunk;
     const int64_t units = a.n_full + (tiles - a.n_full) * a.n_chunks;
     size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
-                  (3 * sizeof(double) + 2 * sizeof(int)) * a.tbl;
+                  (sizeof(int4) + sizeof(int64_t) + 2 * sizeof(int)) * a.tbl;
     if (a.n_full > 0)      // whole-tile units stage their trial sums in the ring
       smem = std::max(smem, sizeof(float) * nk * kThreads + 128 +
-                                (3 * sizeof(double) + 2 * sizeof(int)) * a.tbl);
+                                (sizeof(int4) + sizeof(int64_t) + 2 * sizeof(int)) * a.tbl);
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
