@@ -373,9 +373,12 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
   float* ring = reinterpret_cast<float*>(base);
   const int box = slot_floats(a.box_r, a.box_c);          // slot stride (128-byte multiple)
   // Per-frame table of the chunk after the ring: the split of d + origin
-  // (int4), the frame's stack offset, the window origin.
+  // (int4, one-row windows) or (di, dj), the frame's stack offset, the window
+  // origin.
   int4* t_ds = reinterpret_cast<int4*>(base + sizeof(float) * kNB * box);
-  int64_t* t_off = reinterpret_cast<int64_t*>(t_ds + a.tbl);     // frame offset f * plane
+  double* t_di = reinterpret_cast<double*>(t_ds + a.tbl);
+  double* t_dj = t_di + a.tbl;
+  int64_t* t_off = reinterpret_cast<int64_t*>(t_dj + a.tbl);     // frame offset f * plane
   int* t_wr = reinterpret_cast<int*>(t_off + a.tbl);             // window origin per frame
   int* t_wc = t_wr + a.tbl;
 
@@ -412,7 +415,9 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       const int f = a.sc.good[k_lo + jj];
       const double dI = a.di[f], dJ = a.dj[f];
       t_off[jj] = f * plane;
-      t_ds[jj] = split_d(dI, dJ, a.n0, a.m0);
+      if (KA == 1) t_ds[jj] = split_d(dI, dJ, a.n0, a.m0);
+      t_di[jj] = dI;
+      t_dj[jj] = dJ;
       window_origin(a, g, dI, dJ, t_wr[jj], t_wc[jj]);
     }
     auto issue = [&](int jj) {  // frame k_lo + jj into slot jj % kNB
@@ -433,13 +438,20 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       for (int jj = 0; jj < min(kNB, nk); ++jj) issue(jj);
 
     const float W = live ? a.sc.w32[p] : 0.f;
+    // One-row windows (few trials per sample: the geometry is a large share)
+    // use the float32 split; larger ones keep the float64 geometry, which the
+    // compiler interleaves with the previous sample's trials (the split made
+    // the 11 x 11 loop 16 % slower).
     const USplit us = split_u(u0, u1);
     auto sample_of = [&](int jj, float& I, float& fwv) {
       const int64_t off = t_off[jj];
       I = live ? __ldg(a.sc.frames + off + p) : 0.f;
       fwv = (live && fwp) ? __ldg(fwp + off + p) : 1.f;
-      return make_sample_split<true, KA, KB, BC>(a, g, us, t_ds[jj], live ? fwv : -1.f,
-                                                 t_wr[jj], t_wc[jj]);
+      if (KA == 1)
+        return make_sample_split<true, KA, KB, BC>(a, g, us, t_ds[jj], live ? fwv : -1.f,
+                                                   t_wr[jj], t_wc[jj]);
+      return make_sample<true, KA, KB, BC>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f,
+                                           t_wr[jj], t_wc[jj]);
     };
     // One-frame-ahead pipeline of the per-sample geometry, stack value and
     // patch-valid lookup.  The loop body after the ring wait is one basic
@@ -620,10 +632,12 @@ __global__ void __launch_bounds__(256, 2) k_pix_slow_rows(PixArgs a,
         const double dI = a.di[f], dJ = a.dj[f];
         int wr0, wc0;
         window_origin(a, g, dI, dJ, wr0, wc0);
-        // classified exactly as the fast kernel did (split geometry); the
-        // exact trials use the float64 split of the reference
-        slow = !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast();
+        // classified exactly as the fast kernel did (the float32 split for
+        // one-row windows); the exact trials use the float64 split
         sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
+        slow = a.ka == 1
+                   ? !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast()
+                   : !sl.fast();
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
@@ -787,10 +801,12 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
         const double dI = a.di[f], dJ = a.dj[f];
         int wr0, wc0;
         window_origin(a, g, dI, dJ, wr0, wc0);
-        // classified exactly as the fast kernel did (split geometry); the
-        // exact trials use the float64 split of the reference
-        slow = !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast();
+        // classified exactly as the fast kernel did (the float32 split for
+        // one-row windows); the exact trials use the float64 split
         sl = make_sample(a, g, u0, u1, dI, dJ, fwl, wr0, wc0);
+        slow = a.ka == 1
+                   ? !make_sample_split(a, g, us, split_d(dI, dJ, a.n0, a.m0), fwl, wr0, wc0).fast()
+                   : !sl.fast();
         if (slow) Il = __ldg(a.sc.frames + f * plane + p);
       }
       unsigned mask = __ballot_sync(0xffffffffu, slow);
@@ -1156,10 +1172,10 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     a.tbl = a.n_full > 0 ? static_cast<int>(sc->n_good) : a.chunk;
     const int64_t units = a.n_full + (tiles - a.n_full) * a.n_chunks;
     size_t smem = sizeof(float) * kNB * slot_floats(a.box_r, a.box_c) + 128 +
-                  (sizeof(int4) + sizeof(int64_t) + 2 * sizeof(int)) * a.tbl;
+                  (sizeof(int4) + 3 * sizeof(double) + 2 * sizeof(int)) * a.tbl;
     if (a.n_full > 0)      // whole-tile units stage their trial sums in the ring
       smem = std::max(smem, sizeof(float) * nk * kThreads + 128 +
-                                (sizeof(int4) + sizeof(int64_t) + 2 * sizeof(int)) * a.tbl);
+                                (sizeof(int4) + 3 * sizeof(double) + 2 * sizeof(int)) * a.tbl);
     PXST_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem)));
     if (int e = part.alloc(sizeof(float) * a.n_chunks * nk * a.nq, s)) return e;
