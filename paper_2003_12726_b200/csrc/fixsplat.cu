@@ -2,7 +2,7 @@
 // and K4 (error maps, recon.py:388-438): see fixsplat.cuh for the number
 // format.
 //
-// One CTA per 16 x 32 detector tile and frame slice (grid.z).  The CTA walks
+// One CTA per 8 x 64 detector tile and frame slice (grid.z).  The CTA walks
 // its frames in batches of 8 and groups consecutive batches into "sessions"
 // whose joint object footprint (the tile's u bounding box shifted by each
 // frame's translation) fits a shared-memory region of RC cells and whose
@@ -30,7 +30,11 @@
 namespace pxst {
 namespace {
 
-constexpr int kXR = 16, kXC = 32, kXT = 256, kXW = kXT / 32;  // tile, threads, warps
+// Tile 8 rows x 64 columns: warp w takes row w, lane l its columns 2l and
+// 2l + 1 (one per pass e), so the 32 samples of one instruction are two
+// detector columns apart and land on distinct cells (adjacent columns often
+// share a cell at magnification < 1: same-address shared atomics serialise).
+constexpr int kXR = 8, kXC = 64, kXT = 256, kXW = kXT / 32;  // tile, threads, warps
 constexpr int kXB = 8;        // frames per batch
 #ifndef PXST_FIX_TAB
 #define PXST_FIX_TAB 128
@@ -165,8 +169,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   double u0[2], u1[2], Wv[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
-    const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kXR + 2 * warp + e;
-    const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kXC + lane;
+    const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kXR + warp;
+    const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kXC + 2 * lane + e;
     const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
     p[e] = in ? row * a.sc.fs + col : 0;
     live[e] = in && a.sc.work[p[e]] != 0;
