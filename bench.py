@@ -271,7 +271,7 @@ class Sequence:
             # the iteration's grid bbox and K2 tile spans were fetched on a side
             # stream while the previous iteration's error maps ran, and its
             # object was formed in the same pass over the stack as those maps
-            geom = state["geom"] or ds.geometry_async(u, di, dj)
+            geom = state["geom"] or ds.geometry_async(u, di, dj, cfg.update_translations)
             dref = state["dref"].resolve() if state["dref"] else ds.object_map(u, di, dj, geom=geom)
             u_new = u
             if cfg.update_pixel_map:
@@ -293,13 +293,13 @@ class Sequence:
                 if k3:
                     k3[1].record(stream)
             if state["it"] + 1 < cfg.iters:        # the sequence continues: fuse K4 + next K1
-                nxt = ds.geometry_async(u_new, di_new, dj_new)
+                nxt = ds.geometry_async(u_new, di_new, dj_new, cfg.update_translations)
                 _, nref = ds.error_maps_and_next_object(dref, u_new, di_new, dj_new, nxt)
             else:
                 # the next step restarts the sequence from the initial state:
                 # fetch that state's geometry now, behind these error maps, as
                 # every other iteration's is (no host wait at the restart)
-                nxt = ds.geometry_async(u_t, di_t, dj_t)
+                nxt = ds.geometry_async(u_t, di_t, dj_t, cfg.update_translations)
                 ds.error_maps(dref, u_new, di_new, dj_new)
         state.update(it=(state["it"] + 1) % max(cfg.iters, 1), u=u_new, di=di_new, dj=dj_new,
                      geom=nxt, dref=nref)

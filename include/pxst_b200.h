@@ -105,6 +105,12 @@ int pxst_stack_stats_parts(const pxst_scan* scan, const float* fw, const pxst_st
 int pxst_bbox(const pxst_scan* scan, const double* u, const double* di, const double* dj,
               double* out, void* stream);
 
+/* pxst_bbox and, in the same launch, the grid rule of recon.py:126-132:
+ * grid[4] (device, int64, nullable) = (n0, m0, os, of) -- what
+ * pxst_grid_rule computes from out. */
+int pxst_bbox_grid(const pxst_scan* scan, const double* u, const double* di, const double* dj,
+                   double* out, int64_t* grid, void* stream);
+
 /* Deterministic splat accumulators (K1 object numerator / denominator, K4
  * reference-plane numerator / denominator).  Every float64 term t of the
  * reference's bincount (interp.py:113-122) is rounded once to an integer

@@ -55,6 +55,8 @@ _SIGS = {
     "pxst_stack_stats_parts": (c_int, [POINTER(PxstScan), c_void_p, POINTER(PxstStats), c_int,
                                        c_void_p]),
     "pxst_bbox": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pxst_bbox_grid": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
     "pxst_accum_zero": (c_int, [POINTER(PxstAccum), c_int64, c_void_p]),
     "pxst_add_i64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "pxst_add_f64": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),

@@ -576,78 +576,102 @@ __global__ void k_abs_max(const float* __restrict__ frames, int64_t n, double* o
   }
 }
 
-// scratch[0] = max W over the work pixels of the ROI, scratch[1] = min
-// sigma2 over them (nullable sigma2), scratch[2] = max |reference| over its
-// valid cells (nullable reference).
-__global__ void k_scale_stats(pxst_scan sc, const double* __restrict__ sigma2,
-                              const double* __restrict__ fm64, const float* __restrict__ fm,
-                              const uint8_t* __restrict__ valid, int64_t n_ref, double* scratch) {
-  const int64_t cw = sc.roi[3] - sc.roi[2], n = (sc.roi[1] - sc.roi[0]) * cw;
-  double wmax = 0.0, smin = INFINITY, rmax = 0.0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = (sc.roi[0] + q / cw) * sc.fs + sc.roi[2] + q % cw;
-    if (!sc.work[p]) continue;
-    wmax = fmax(wmax, fabs(sc.w64[p]));
-    if (sigma2) smin = fmin(smin, sigma2[p]);
+// Scale statistics and quanta in one launch.  Every block reduces its share
+// of the ROI's work pixels (max W, min sigma2: kind 1 only) and of the
+// reference's valid cells (max |ref|) to part[3 * block]; the last block to
+// finish (ticket) folds the partials and writes the quanta:
+//   kind 0 (object): q_num from max |I| max W, q_den from max W^2;
+//   kind 1 (reference plane): q_num from the eps bound
+//   (max|I| + max W max(1, max|ref|))^2 / min sigma2, q_den from 1.
+// The same loops also write K4's grouped reference (g[r][c] = (v(r, c),
+// v(r + 1, c)), v = the float64 masked reference where valid, NaN elsewhere
+// and past the last row: one 16-byte load fetches a bilinear column pair and
+// the NaN doubles as the validity bit) and zero-fill an array.
+__global__ void __launch_bounds__(256) k_quanta_pass(QuantaJob j, double* __restrict__ part) {
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = t0; q < j.n_zero; q += stride) j.zero[q] = 0.0;
+  const int64_t n_ref = j.valid ? j.os * j.of : 0;
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  double rmax = 0.0;
+  for (int64_t q = t0; q < n_ref; q += stride) {
+    const bool ok = j.valid[q] != 0;
+    const double v = ok ? (j.fm64 ? j.fm64[q] : static_cast<double>(j.fm[q])) : nan;
+    if (ok) rmax = fmax(rmax, fabs(v));
+    if (j.grp) {
+      const int64_t q1 = q + j.of;
+      const double v1 = q1 < n_ref && j.valid[q1] ? (j.fm64 ? j.fm64[q1] : static_cast<double>(j.fm[q1]))
+                                                  : nan;
+      j.grp[q] = make_double2(v, v1);
+    }
   }
-  if (valid)
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_ref;
-         q += (int64_t)gridDim.x * blockDim.x)
-      if (valid[q]) rmax = fmax(rmax, fabs(fm64 ? fm64[q] : static_cast<double>(fm[q])));
+  if (!j.quanta) return;
+  const int64_t cw = j.sc.roi[3] - j.sc.roi[2], n = (j.sc.roi[1] - j.sc.roi[0]) * cw;
+  double wmax = 0.0, smin = INFINITY;
+  for (int64_t q = t0; q < n; q += stride) {
+    const int64_t p = (j.sc.roi[0] + q / cw) * j.sc.fs + j.sc.roi[2] + q % cw;
+    if (!j.sc.work[p]) continue;
+    wmax = fmax(wmax, fabs(j.sc.w64[p]));
+    if (j.sigma2) smin = fmin(smin, j.sigma2[p]);
+  }
   __shared__ double red[3][32];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   wmax = warp_max(wmax);
   smin = warp_min(smin);
   rmax = warp_max(rmax);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) { red[0][w] = wmax; red[1][w] = smin; red[2][w] = rmax; }
   __syncthreads();
-  if (threadIdx.x == 0) {   // one atomic per block (many per address serialise in L2)
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < nw; ++k) {
       wmax = fmax(wmax, red[0][k]);
       smin = fmin(smin, red[1][k]);
       rmax = fmax(rmax, red[2][k]);
     }
-    atomic_max_nonneg(scratch, wmax);
-    if (sigma2) atomic_min_nonneg(scratch + 1, smin);
-    atomic_max_nonneg(scratch + 2, rmax);
+    part[3 * blockIdx.x] = wmax;
+    part[3 * blockIdx.x + 1] = smin;
+    part[3 * blockIdx.x + 2] = rmax;
+    __threadfence();
+    s_last = atomicAdd(j.ticket, 1u) == gridDim.x - 1;
   }
-}
-
-__global__ void k_scale_init(double* d) {
-  if (threadIdx.x == 0) {
-    d[0] = 0.0;
-    d[1] = INFINITY;
-    d[2] = 0.0;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  wmax = 0.0; smin = INFINITY; rmax = 0.0;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+    wmax = fmax(wmax, __ldcg(part + 3 * k));
+    smin = fmin(smin, __ldcg(part + 3 * k + 1));
+    rmax = fmax(rmax, __ldcg(part + 3 * k + 2));
   }
-}
-
-// kind 0 (object): q_num from max |I| max W, q_den from max W^2.
-// kind 1 (reference plane): q_num from the eps bound
-// (max|I| + max W max(1, max|ref|))^2 / min sigma2, q_den from 1.
-__global__ void k_quanta(const double* __restrict__ absmax, const double* __restrict__ scratch,
-                         int kind, int k, double* quanta) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double amax = *absmax, wmax = scratch[0];
-  if (kind == 0) {
-    quanta[0] = fix_quantum(amax * wmax, k);
-    quanta[1] = fix_quantum(wmax * wmax, k);
+  wmax = warp_max(wmax);
+  smin = warp_min(smin);
+  rmax = warp_max(rmax);
+  __syncthreads();
+  if (lane == 0) { red[0][w] = wmax; red[1][w] = smin; red[2][w] = rmax; }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int k = 1; k < nw; ++k) {
+    wmax = fmax(wmax, red[0][k]);
+    smin = fmin(smin, red[1][k]);
+    rmax = fmax(rmax, red[2][k]);
+  }
+  const double amax = *j.absmax;
+  const int hk = fix_headroom(j.sc.n_good);
+  if (j.kind == 0) {
+    j.quanta[0] = fix_quantum(amax * wmax, hk);
+    j.quanta[1] = fix_quantum(wmax * wmax, hk);
   } else {
-    const double r = amax + wmax * fmax(1.0, scratch[2]);
-    const double s = scratch[1] > 0.0 && isfinite(scratch[1]) ? scratch[1] : 1.0;
-    quanta[0] = fix_quantum(r * r / s, k);
-    quanta[1] = fix_quantum(1.0, k);
+    const double r = amax + wmax * fmax(1.0, rmax);
+    const double sg = smin > 0.0 && isfinite(smin) ? smin : 1.0;
+    j.quanta[0] = fix_quantum(r * r / sg, hk);
+    j.quanta[1] = fix_quantum(1.0, hk);
   }
 }
 
 // ---------------------------------------------------------------------------
 // finish
 // ---------------------------------------------------------------------------
-// Normalise (interp.py:126-135): out = num/den where den > 0 else 0, with
-// num = num q + num_f q 2^-20 (likewise den).  The object's validity is "a
-// positive-weight term landed": den > 0, or a tiny-weight term marked the
-// cell (touched) -- such a cell whose weight rounds to zero keeps valid = 1
-// with value 0 and wsum = q 2^-62.
+// Normalise (fix_finish_cell) the first n cells, or the grid's when given.
 __global__ void k_fix_finish(FixAcc acc, const int64_t* __restrict__ grid, int64_t n, double* out,
                              double* wsum, float* fm, uint8_t* valid) {
   if (grid) {
@@ -655,20 +679,9 @@ __global__ void k_fix_finish(FixAcc acc, const int64_t* __restrict__ grid, int64
     if (!(grid[2] > 0 && grid[3] > 0)) return;
     n = gn < n ? gn : n;
   }
-  const double qn = acc.q[0], qd = acc.q[1];
-  const double qnf = qn * 0x1p-20, qdf = qd * 0x1p-20;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double d = static_cast<double>(acc.den[i]) * qd + static_cast<double>(acc.den_f[i]) * qdf;
-    const double nm = static_cast<double>(acc.num[i]) * qn + static_cast<double>(acc.num_f[i]) * qnf;
-    const bool pos = d > 0.0;
-    const bool ok = pos || (acc.touched && acc.touched[i] != 0);
-    const double v = pos ? nm / d : 0.0;
-    if (out) out[i] = v;
-    if (wsum) wsum[i] = pos ? d : (ok ? qd * 0x1p-62 : 0.0);
-    if (fm) fm[i] = ok ? static_cast<float>(v) : 0.f;
-    if (valid) valid[i] = ok ? 1 : 0;
-  }
+       i += (int64_t)gridDim.x * blockDim.x)
+    fix_finish_cell(acc, i, out, wsum, fm, valid);
 }
 
 }  // namespace
@@ -687,22 +700,38 @@ int launch_abs_max(const pxst_scan* sc, double* out, cudaStream_t s) {
   return PXST_OK;
 }
 
-int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma2,
-                  const pxst_ref* ref, int kind, double* quanta, cudaStream_t s) {
-  Scratch sc3;
-  if (int e = sc3.alloc(3 * sizeof(double), s)) return e;
-  double* d = sc3.as<double>();
-  k_scale_init<<<1, 32, 0, s>>>(d);     // (0, +inf, 0): max W, min sigma2, max |ref|
-  PXST_CHECK_LAUNCH();
-  const int64_t n_ref = ref ? ref->os * ref->of : 0;
-  const int64_t cw = sc->roi[3] - sc->roi[2], rw = sc->roi[1] - sc->roi[0];
-  k_scale_stats<<<std::min(grid_1d(std::max(rw * cw, n_ref), 256), 2 * 148), 256, 0, s>>>(
-      *sc, kind == 1 ? sigma2 : nullptr, ref ? ref->fm64 : nullptr, ref ? ref->fm : nullptr,
-      ref ? ref->valid : nullptr, n_ref, d);
-  PXST_CHECK_LAUNCH();
-  k_quanta<<<1, 32, 0, s>>>(absmax, d, kind, fix_headroom(sc->n_good), quanta);
+int launch_quanta_job(const QuantaJob& j, cudaStream_t s) {
+  const int64_t n_roi = (j.sc.roi[1] - j.sc.roi[0]) * (j.sc.roi[3] - j.sc.roi[2]);
+  const int64_t n_ref = j.valid ? j.os * j.of : 0;
+  const int g = std::min(grid_1d(std::max(std::max(n_roi, n_ref), j.n_zero), 256), 2 * 148);
+  Scratch part;
+  if (j.quanta)
+    if (int e = part.alloc(3 * sizeof(double) * g, s)) return e;
+  k_quanta_pass<<<g, 256, 0, s>>>(j, part.as<double>());
   PXST_CHECK_LAUNCH();
   return PXST_OK;
+}
+
+int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma2,
+                  const pxst_ref* ref, int kind, double* quanta, cudaStream_t s) {
+  Scratch t;
+  if (int e = t.alloc(sizeof(unsigned), s)) return e;
+  PXST_CHECK_CUDA(cudaMemsetAsync(t.p, 0, sizeof(unsigned), s));
+  QuantaJob j{};
+  j.sc = *sc;
+  j.sigma2 = kind == 1 ? sigma2 : nullptr;
+  if (ref) {
+    j.fm64 = ref->fm64;
+    j.fm = ref->fm;
+    j.valid = ref->valid;
+    j.os = ref->os;
+    j.of = ref->of;
+  }
+  j.absmax = absmax;
+  j.kind = kind;
+  j.quanta = quanta;
+  j.ticket = t.as<unsigned>();
+  return launch_quanta_job(j, s);
 }
 
 template <int MODE>

@@ -93,4 +93,45 @@ struct FixAcc {
   const double* q;
 };
 
+// Normalise one cell (interp.py:126-135): out = num/den where den > 0 else
+// 0, with num = num q + num_f q 2^-20 (likewise den).  The object's validity
+// is "a positive-weight term landed": den > 0, or a tiny-weight term marked
+// the cell (touched) -- such a cell whose weight rounds to zero keeps
+// valid = 1 with value 0 and wsum = q 2^-62.  Every output is nullable.
+__device__ __forceinline__ void fix_finish_cell(const FixAcc& acc, int64_t i, double* out,
+                                                double* wsum, float* fm, uint8_t* valid) {
+  const double qn = acc.q[0], qd = acc.q[1];
+  const double d = static_cast<double>(acc.den[i]) * qd +
+                   static_cast<double>(acc.den_f[i]) * (qd * 0x1p-20);
+  const double nm = static_cast<double>(acc.num[i]) * qn +
+                    static_cast<double>(acc.num_f[i]) * (qn * 0x1p-20);
+  const bool pos = d > 0.0;
+  const bool ok = pos || (acc.touched && acc.touched[i] != 0);
+  const double v = pos ? nm / d : 0.0;
+  if (out) out[i] = v;
+  if (wsum) wsum[i] = pos ? d : (ok ? qd * 0x1p-62 : 0.0);
+  if (fm) fm[i] = ok ? static_cast<float>(v) : 0.f;
+  if (valid) valid[i] = ok ? 1 : 0;
+}
+
+// One launch for the scale statistics and the quanta (and, in the same
+// grid-stride loops, K4's grouped reference and a zero fill): see
+// k_quanta_pass.  ticket must be zero when the kernel starts.
+struct QuantaJob {
+  pxst_scan sc;
+  const double* sigma2;         // nullable (object quanta: kind 0)
+  const double* fm64;           // reference (nullable valid: none)
+  const float* fm;
+  const uint8_t* valid;
+  int64_t os, of;
+  const double* absmax;
+  int kind;                     // 0 object, 1 reference plane
+  double* quanta;               // nullable: side jobs only
+  unsigned* ticket;
+  double2* grp;                 // nullable: g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid
+  double* zero;                 // nullable: zero[0, n_zero) = 0
+  int64_t n_zero;
+};
+int launch_quanta_job(const QuantaJob& j, cudaStream_t s);
+
 }  // namespace pxst

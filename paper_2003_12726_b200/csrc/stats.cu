@@ -85,22 +85,48 @@ __global__ void k_pixel_stats(pxst_scan sc, const float* __restrict__ fw,
   if (!sc.work[p]) return;
   const double w = sc.w64[p];
   const int64_t plane = sc.ss * sc.fs;
+  const float* fp = sc.frames + p;
+  const float* wp = fw ? fw + p : nullptr;
+  // Loads kU frames ahead of the adds (memory-level parallelism: one thread
+  // per pixel has too few loads in flight otherwise); the adds stay in frame
+  // order, so the sums are bit-identical to the sequential loop.
+  constexpr int kU = 8;
   double vs = 0.0, sum = 0.0;
-  for (int64_t k = 0; k < sc.n_good; ++k) {
-    const int64_t f = sc.good[k];
-    const double I = static_cast<double>(__ldg(sc.frames + f * plane + p));
-    const double d = I - w;
-    double t = d * d;
-    if (fw) t = static_cast<double>(__ldg(fw + f * plane + p)) * t;
-    vs += t;
-    sum += I;
+  for (int64_t k0 = 0; k0 < sc.n_good; k0 += kU) {
+    float I32[kU], F32[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int64_t k = k0 + j < sc.n_good ? k0 + j : sc.n_good - 1;
+      const int64_t off = static_cast<int64_t>(__ldg(sc.good + k)) * plane;
+      I32[j] = __ldg(fp + off);
+      F32[j] = wp ? __ldg(wp + off) : 1.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j)
+      if (k0 + j < sc.n_good) {
+        const double I = static_cast<double>(I32[j]);
+        const double d = I - w;
+        double t = d * d;
+        if (wp) t = static_cast<double>(F32[j]) * t;
+        vs += t;
+        sum += I;
+      }
   }
   const double mean = sum / static_cast<double>(sc.n_good);
   double ss = 0.0;
-  for (int64_t k = 0; k < sc.n_good; ++k) {
-    const int64_t f = sc.good[k];
-    const double d = static_cast<double>(__ldg(sc.frames + f * plane + p)) - mean;
-    ss += d * d;
+  for (int64_t k0 = 0; k0 < sc.n_good; k0 += kU) {
+    float I32[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const int64_t k = k0 + j < sc.n_good ? k0 + j : sc.n_good - 1;
+      I32[j] = __ldg(fp + static_cast<int64_t>(__ldg(sc.good + k)) * plane);
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j)
+      if (k0 + j < sc.n_good) {
+        const double d = static_cast<double>(I32[j]) - mean;
+        ss += d * d;
+      }
   }
   const double wmax = scalars[0];
   const double floor_ = 1e-8 * wmax * wmax;
@@ -184,9 +210,16 @@ __global__ void k_sum_final(const double* a, const double* b, int64_t n, double*
   if (threadIdx.x == 0) { *out_a = sa; *out_b = sb; }
 }
 
-// bbox partials over work pixels: min/max of u0, u1.
-__global__ void k_bbox_partial(pxst_scan sc, const double* __restrict__ u, double* part) {
+// bbox of the work pixels' u (min/max of u0, u1) and of the good frames'
+// translations, one launch: every block reduces its share of the ROI to
+// part[4 * block]; the last block to finish (ticket, zero at start) folds the
+// partials, reduces di / dj and writes out[8] and, when given, the grid rule
+// of recon.py:126-132: grid = (n0, m0, os, of).
+__global__ void k_bbox(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
+                       const double* __restrict__ dj, double* part, unsigned* ticket, double* out,
+                       int64_t* grid) {
   __shared__ double sh[32];
+  __shared__ bool s_last;
   const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
   const int64_t n = rw * cw, plane = sc.ss * sc.fs;
   double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
@@ -204,16 +237,16 @@ __global__ void k_bbox_partial(pxst_scan sc, const double* __restrict__ u, doubl
   if (threadIdx.x == 0) {
     double* o = part + 4 * blockIdx.x;
     o[0] = a0; o[1] = b0; o[2] = a1; o[3] = b1;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-}
-
-__global__ void k_bbox_final(pxst_scan sc, const double* part, int nb, const double* di,
-                             const double* dj, double* out) {
-  __shared__ double sh[32];
-  double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
-  for (int k = threadIdx.x; k < nb; k += blockDim.x) {
-    a0 = fmin(a0, part[4 * k]); b0 = fmax(b0, part[4 * k + 1]);
-    a1 = fmin(a1, part[4 * k + 2]); b1 = fmax(b1, part[4 * k + 3]);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  a0 = INFINITY; b0 = -INFINITY; a1 = INFINITY; b1 = -INFINITY;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+    a0 = fmin(a0, __ldcg(part + 4 * k)); b0 = fmax(b0, __ldcg(part + 4 * k + 1));
+    a1 = fmin(a1, __ldcg(part + 4 * k + 2)); b1 = fmax(b1, __ldcg(part + 4 * k + 3));
   }
   double c0 = INFINITY, d0 = -INFINITY, c1 = INFINITY, d1 = -INFINITY;
   for (int64_t k = threadIdx.x; k < sc.n_good; k += blockDim.x) {
@@ -227,6 +260,14 @@ __global__ void k_bbox_final(pxst_scan sc, const double* part, int nb, const dou
   if (threadIdx.x == 0) {
     out[0] = a0; out[1] = b0; out[2] = a1; out[3] = b1;
     out[4] = c0; out[5] = d0; out[6] = c1; out[7] = d1;
+    if (grid) {
+      const int64_t n0 = static_cast<int64_t>(floor(a0 - d0));
+      const int64_t m0 = static_cast<int64_t>(floor(a1 - d1));
+      grid[0] = n0;
+      grid[1] = m0;
+      grid[2] = static_cast<int64_t>(floor(b0 - c0)) - n0 + 2;
+      grid[3] = static_cast<int64_t>(floor(b1 - c1)) - m0 + 2;
+    }
   }
 }
 
@@ -326,17 +367,22 @@ extern "C" int pxst_stack_stats(const pxst_scan* sc, const float* fw, const pxst
   return pxst_stack_stats_parts(sc, fw, st, PXST_STATS_PIXEL | PXST_STATS_FRAME, stream);
 }
 
-extern "C" int pxst_bbox(const pxst_scan* sc, const double* u, const double* di,
-                         const double* dj, double* out, void* stream) {
+extern "C" int pxst_bbox_grid(const pxst_scan* sc, const double* u, const double* di,
+                              const double* dj, double* out, int64_t* grid, void* stream) {
   if (int e = check_scan(sc)) return e;
   PXST_REQUIRE(u && di && dj && out, "NULL pointer");
   cudaStream_t s = as_stream(stream);
   const int nb = partial_blocks(sc);
   Scratch part;
-  if (int e = part.alloc(sizeof(double) * 4 * nb, s)) return e;
-  k_bbox_partial<<<nb, kThreads, 0, s>>>(*sc, u, part.as<double>());
-  PXST_CHECK_LAUNCH();
-  k_bbox_final<<<1, 1024, 0, s>>>(*sc, part.as<double>(), nb, di, dj, out);
+  if (int e = part.alloc(sizeof(double) * 4 * nb + sizeof(unsigned), s)) return e;
+  unsigned* ticket = reinterpret_cast<unsigned*>(part.as<double>() + 4 * nb);
+  PXST_CHECK_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+  k_bbox<<<nb, kThreads, 0, s>>>(*sc, u, di, dj, part.as<double>(), ticket, out, grid);
   PXST_CHECK_LAUNCH();
   return PXST_OK;
+}
+
+extern "C" int pxst_bbox(const pxst_scan* sc, const double* u, const double* di,
+                         const double* dj, double* out, void* stream) {
+  return pxst_bbox_grid(sc, u, di, dj, out, nullptr, stream);
 }

@@ -191,8 +191,11 @@ class GeometryFuture:
 
     def spans3_hint(self, grow: int = 0):
         """K3's span hint (host int32[2]) of this geometry's u, widened by
-        `grow` rows / columns (a bound for a map moved by <= grow / 2 px)."""
+        `grow` rows / columns (a bound for a map moved by <= grow / 2 px);
+        None when the future was made without spans3."""
         self._event.synchronize()
+        if int(self._host2[2]) < 0:
+            return None
         h = torch.empty(2, dtype=torch.int32, pin_memory=True)
         h[0] = int(self._host2[2]) + grow
         h[1] = int(self._host2[3]) + grow
@@ -464,12 +467,12 @@ class DeviceScan:
                                  dj_t.data_ptr(), out.data_ptr(), stream_ptr()))
         return _grid_rule(to_host(out).tolist())
 
-    def geometry_async(self, u_t, di_t, dj_t) -> "GeometryFuture":
+    def geometry_async(self, u_t, di_t, dj_t, spans3: bool = True) -> "GeometryFuture":
         """Start the host-side geometry of an iteration on a side stream: the
-        object-grid bbox (recon.py:126-132) and K2's tile spans of u.  The
-        main stream is not blocked; reading the future waits only for these
-        two small reductions, so an iteration loop can fetch the next
-        iteration's geometry while the current error maps run."""
+        object-grid bbox (recon.py:126-132), K2's tile spans of u and (with
+        spans3) K3's.  The main stream is not blocked; reading the future
+        waits only for these small reductions, so an iteration loop can fetch
+        the next iteration's geometry while the current error maps run."""
         main = torch.cuda.current_stream(self.device)
         if self._side is None:
             self._side = torch.cuda.Stream(self.device)
@@ -484,16 +487,19 @@ class DeviceScan:
             dev2 = torch.empty(4, dtype=torch.int32, device=self.device)
             grid = torch.empty(4, dtype=torch.int64, device=self.device)
             sp = stream_ptr(side)
-            check(self.lib.pxst_bbox(ctypes.byref(self.c_scan), u_t.data_ptr(), di_t.data_ptr(),
-                                     dj_t.data_ptr(), dev8.data_ptr(), sp))
-            check(self.lib.pxst_grid_rule(dev8.data_ptr(), grid.data_ptr(), sp))
+            check(self.lib.pxst_bbox_grid(ctypes.byref(self.c_scan), u_t.data_ptr(),
+                                          di_t.data_ptr(), dj_t.data_ptr(), dev8.data_ptr(),
+                                          grid.data_ptr(), sp))
             grid_ready = torch.cuda.Event()      # what device-side consumers wait for
             grid_ready.record(side)
             host8.copy_(dev8, non_blocking=True)
             check(self.lib.pxst_tile_spans(ctypes.byref(self.c_scan), u_t.data_ptr(),
                                            dev2.data_ptr(), sp))
-            check(self.lib.pxst_tile_spans3(ctypes.byref(self.c_scan), u_t.data_ptr(),
-                                            dev2[2:].data_ptr(), sp))
+            if spans3:
+                check(self.lib.pxst_tile_spans3(ctypes.byref(self.c_scan), u_t.data_ptr(),
+                                                dev2[2:].data_ptr(), sp))
+            else:
+                dev2[2:].fill_(-1)
             host2.copy_(dev2, non_blocking=True)
             done = torch.cuda.Event()
             done.record(side)

@@ -269,7 +269,10 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
         raise ValueError("make_reference: empty good pixel/frame set")
     u_t = ds.upload_u(u.u, cache=True)
     di_t, dj_t = ds.upload_t(t.di, t.dj, cache=True)
-    gfut = ds.geometry_async(u_t, di_t, dj_t)
+    def needs_k3(i):      # K3's tile spans only for iterations that update translations
+        return i < max_iters and bool(schedule[i].update_translations)
+
+    gfut = ds.geometry_async(u_t, di_t, dj_t, spans3=needs_k3(0))
     dref = ds.object_map(u_t, di_t, dj_t, geom=gfut)
     history = [_metrics(*ds.error_maps(dref, u_t, di_t, dj_t))]
     if progress_cb:
@@ -295,7 +298,7 @@ def run_main_loop(scan: ScanData, w: Whitefield, m: PixelMask, u: PixelMap,
             di_t, dj_t = ds.translation_search(dref, u_t, di_t, dj_t, tw.half_ss, tw.half_fs,
                                                tw.subpixel_grid,
                                                span_hint=gfut.spans3_hint(grow))
-        gfut = ds.geometry_async(u_t, di_t, dj_t)       # next iteration's, overlaps K4
+        gfut = ds.geometry_async(u_t, di_t, dj_t, spans3=needs_k3(i + 1))   # next iteration's
         if i + 1 < max_iters:
             metrics, nref = ds.error_maps_and_next_object(dref, u_t, di_t, dj_t, gfut)
         else:
