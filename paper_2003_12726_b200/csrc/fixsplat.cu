@@ -703,7 +703,7 @@ int launch_abs_max(const pxst_scan* sc, double* out, cudaStream_t s) {
 int launch_quanta_job(const QuantaJob& j, cudaStream_t s) {
   const int64_t n_roi = (j.sc.roi[1] - j.sc.roi[0]) * (j.sc.roi[3] - j.sc.roi[2]);
   const int64_t n_ref = j.valid ? j.os * j.of : 0;
-  const int g = std::min(grid_1d(std::max(std::max(n_roi, n_ref), j.n_zero), 256), 2 * 148);
+  const int g = std::min(grid_1d(std::max(std::max(n_roi, n_ref), j.n_zero), 256), 8 * 148);
   Scratch part;
   if (j.quanta)
     if (int e = part.alloc(3 * sizeof(double) * g, s)) return e;

@@ -176,14 +176,16 @@ __device__ __forceinline__ void finish_pixel(const PixArgs& a, int64_t p, int be
 // 1. tile geometry
 // ---------------------------------------------------------------------------
 // With init_out, every ROI pixel also gets u_out = u, err_out = 0 (the
-// search's finishers then overwrite the work pixels).
-__global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out, unsigned* zero2 = nullptr) {
-  if (zero2 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;
-  __shared__ double red[kWarps][4];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = a.sc.roi[0] + (int64_t)blockIdx.y * kTR + tile_dr(threadIdx.x);
-  const int64_t col = a.sc.roi[2] + (int64_t)blockIdx.x * kTC + tile_dc(threadIdx.x);
-  const bool inroi = row < a.sc.roi[1] && col < a.sc.roi[3];
+// search's finishers then overwrite the work pixels).  One tile of kThreads
+// threads (tid); red = kWarps x 4 doubles of shared memory; every thread
+// reaches the one barrier.
+__device__ __forceinline__ void tile_geo_block(const PixArgs& a, TileGeo* geo, int init_out,
+                                               int64_t tile, bool on, int tid, double (*red)[4]) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t by = on ? tile / a.tiles_x : 0, bx = on ? tile % a.tiles_x : 0;
+  const int64_t row = a.sc.roi[0] + by * kTR + tile_dr(tid);
+  const int64_t col = a.sc.roi[2] + bx * kTC + tile_dc(tid);
+  const bool inroi = on && row < a.sc.roi[1] && col < a.sc.roi[3];
   const int64_t p = inroi ? row * a.sc.fs + col : 0;
   const bool live = inroi && a.sc.work[p] != 0;
   const int64_t plane = a.sc.ss * a.sc.fs;
@@ -193,19 +195,57 @@ __global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out, unsigned* zero
     a.err_out[p] = 0.0;
   }
   const double u0 = live ? a.u[p] : 0.0, u1 = live ? a.u[plane + p] : 0.0;
-  double mn0 = warp_min(live ? u0 : INFINITY), mx0 = warp_max(live ? u0 : -INFINITY);
-  double mn1 = warp_min(live ? u1 : INFINITY), mx1 = warp_max(live ? u1 : -INFINITY);
+  const double mn0 = warp_min(live ? u0 : INFINITY), mx0 = warp_max(live ? u0 : -INFINITY);
+  const double mn1 = warp_min(live ? u1 : INFINITY), mx1 = warp_max(live ? u1 : -INFINITY);
   if (lane == 0) { red[warp][0] = mn0; red[warp][1] = mx0; red[warp][2] = mn1; red[warp][3] = mx1; }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (tid != 0 || !on) return;
+  double r0 = red[0][0], r1 = red[0][1], r2 = red[0][2], r3 = red[0][3];
   for (int w = 1; w < kWarps; ++w) {
-    mn0 = fmin(red[0][0], red[w][0]); red[0][0] = mn0;
-    mx0 = fmax(red[0][1], red[w][1]); red[0][1] = mx0;
-    mn1 = fmin(red[0][2], red[w][2]); red[0][2] = mn1;
-    mx1 = fmax(red[0][3], red[w][3]); red[0][3] = mx1;
+    r0 = fmin(r0, red[w][0]);
+    r1 = fmax(r1, red[w][1]);
+    r2 = fmin(r2, red[w][2]);
+    r3 = fmax(r3, red[w][3]);
   }
-  mn0 = red[0][0]; mx0 = red[0][1]; mn1 = red[0][2]; mx1 = red[0][3];
-  geo[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = make_tile_geo(mn0, mx0, mn1, mx1);
+  geo[tile] = make_tile_geo(r0, r1, r2, r3);
+}
+
+__global__ void k_tile_geo(PixArgs a, TileGeo* geo, int init_out) {
+  __shared__ double red[kWarps][4];
+  tile_geo_block(a, geo, init_out, (int64_t)blockIdx.y * gridDim.x + blockIdx.x, true, threadIdx.x,
+                 red);
+}
+
+// K2's two preparation steps in one launch of 256-thread blocks: blocks
+// [0, n_pv) build the patch-valid map and NaN-encoded reference
+// (pv_tile_block), the rest the tile geometry (kTiles tiles per block) and
+// zero the slow-list counters.
+constexpr int kPrepTiles = 256 / kThreads;
+struct PvJob {
+  const uint8_t* valid;
+  const float* fm;
+  int os, of, lr, hr, lc, hc, nx;
+  uint8_t* pv;
+  float* fmn;
+};
+__global__ void __launch_bounds__(256) k_k2_prep(PixArgs a, TileGeo* geo, int init_out,
+                                                 unsigned* zero2, PvJob pj, int n_pv,
+                                                 int64_t tiles) {
+  __shared__ union {
+    PvShared pv;
+    double red[kPrepTiles][kWarps][4];
+  } sm;
+  if (blockIdx.x < n_pv) {
+    pv_tile_block(sm.pv, blockIdx.x % pj.nx, blockIdx.x / pj.nx, threadIdx.x & 31,
+                  threadIdx.x >> 5, pj.valid, pj.fm, pj.os, pj.of, pj.lr, pj.hr, pj.lc, pj.hc,
+                  pj.pv, pj.fmn);
+    return;
+  }
+  const int64_t b = blockIdx.x - n_pv;
+  if (b == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;
+  const int part = threadIdx.x / kThreads;
+  const int64_t tile = b * kPrepTiles + part;
+  tile_geo_block(a, geo, init_out, tile, tile < tiles, threadIdx.x % kThreads, sm.red[part]);
 }
 
 // window rows / cols a tile needs beyond its u span: the (Ka+1) x (Kb+1)
@@ -1098,8 +1138,6 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
     if (int e = fmn.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
     a.fmn = fmn.as<float>();
-    if (int e = make_pv(ref, -ra, ra + 1, -rb, rb + 1, pvbuf.as<uint8_t>(), fmn.as<float>(), s))
-      return e;
     a.pv = pvbuf.as<uint8_t>();
     if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
@@ -1117,9 +1155,21 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     }
     Scratch cnt;                 // slow-list count and work counter, zeroed by k_tile_geo
     if (int e = cnt.alloc(2 * sizeof(unsigned), s)) return e;
-    dim3 gt((unsigned)a.tiles_x, (unsigned)tiles_y);
-    k_tile_geo<<<gt, kThreads, 0, s>>>(a, geo.as<TileGeo>(), fast_init ? 1 : 0, cnt.as<unsigned>());
-    PXST_CHECK_LAUNCH();
+    {
+      // patch-valid map + NaN-encoded reference (make_pv) and the tile
+      // geometry in one launch
+      PXST_REQUIRE(2 * ra + 1 <= kPvMaxHalo && 2 * rb + 1 <= kPvMaxHalo, "patch extent too large");
+      PvJob pj{ref->valid, ref->fm, static_cast<int>(ref->os), static_cast<int>(ref->of),
+               -ra, ra + 1, -rb, rb + 1, static_cast<int>((ref->of + kPvC - 1) / kPvC),
+               pvbuf.as<uint8_t>(), fmn.as<float>()};
+      const int64_t n_pv = (int64_t)pj.nx * ((ref->os + kPvR - 1) / kPvR);
+      const int64_t blocks = n_pv + (tiles + kPrepTiles - 1) / kPrepTiles;
+      PXST_REQUIRE(blocks < (int64_t(1) << 31), "reference image too large");
+      k_k2_prep<<<(unsigned)blocks, 256, 0, s>>>(a, geo.as<TileGeo>(), fast_init ? 1 : 0,
+                                                 cnt.as<unsigned>(), pj, static_cast<int>(n_pv),
+                                                 tiles);
+      PXST_CHECK_LAUNCH();
+    }
     // Size the TMA box from the largest tile footprint (|du/dx| reaches ~1.8
     // at the edges of the config-3 map), capped at 24 KB per ring slot; tiles
     // beyond the cap take the exact path.

@@ -374,6 +374,46 @@ __device__ __forceinline__ int clamp_span(double v) {
   return v < 0.0 ? 0 : (v > 4096.0 ? 4096 : static_cast<int>(v));
 }
 
+// Patch-valid map tile (see make_pv): pv[i][j] = every cell of rows
+// [i+lr, i+hr] x cols [j+lc, j+hc] exists and is valid, as a separable AND
+// over a kPvR x kPvC output tile with its halo staged in shared memory;
+// optionally also the NaN-encoded float32 reference of the tile's cells
+// (fmn).  32 x 8 threads (tx, ty).
+constexpr int kPvC = 32, kPvR = 16, kPvMaxHalo = 64;
+struct PvShared {
+  uint8_t v[kPvR + kPvMaxHalo][kPvC + kPvMaxHalo];
+  uint8_t rowok[kPvR + kPvMaxHalo][kPvC];
+};
+__device__ __forceinline__ void pv_tile_block(PvShared& sm, int bx, int by, int tx, int ty,
+                                              const uint8_t* __restrict__ valid,
+                                              const float* __restrict__ fm, int os, int of, int lr,
+                                              int hr, int lc, int hc, uint8_t* __restrict__ pv,
+                                              float* __restrict__ fmn) {
+  const int i0 = by * kPvR, j0 = bx * kPvC;
+  const int th = kPvR + hr - lr, tw = kPvC + hc - lc;
+  for (int rr = ty; rr < th; rr += 8)
+    for (int cc = tx; cc < tw; cc += 32) {
+      const int r = i0 + lr + rr, c = j0 + lc + cc;
+      sm.v[rr][cc] = (r >= 0 && r < os && c >= 0 && c < of) ? valid[r * of + c] : 0;
+    }
+  __syncthreads();
+  for (int rr = ty; rr < th; rr += 8) {
+    uint8_t ok = 1;
+    for (int d = 0; d <= hc - lc; ++d) ok &= sm.v[rr][tx + d];
+    sm.rowok[rr][tx] = ok;
+  }
+  __syncthreads();
+  const int j = j0 + tx;
+  for (int rr = ty; rr < kPvR; rr += 8) {
+    const int i = i0 + rr;
+    if (i >= os || j >= of) continue;
+    uint8_t ok = 1;
+    for (int d = 0; d <= hr - lr; ++d) ok &= sm.rowok[rr + d][tx];
+    pv[i * of + j] = ok;
+    if (fmn) fmn[i * of + j] = valid[i * of + j] ? fm[i * of + j] : __int_as_float(0x7fc00000);
+  }
+}
+
 // Host helpers ---------------------------------------------------------------
 // Patch-valid map: pv[i][j] = every cell of rows [i+lr, i+hr] x cols
 // [j+lc, j+hc] exists and is valid; with fmn != NULL also the NaN-encoded

@@ -8,42 +8,14 @@
 namespace pxst {
 namespace {
 
-// Patch-valid map pv[i][j] = every cell of rows [i+lr, i+hr] x cols
-// [j+lc, j+hc] exists and is valid, as a separable AND over a 32 x 32 output
-// tile with its halo staged in shared memory (one launch); optionally also
-// the NaN-encoded float32 reference of the tile's cells (fmn).
-constexpr int kPvC = 32, kPvR = 16, kPvMaxHalo = 64;   // output tile: 16 rows x 32 cols
-
+// Patch-valid map (pv_tile_block), one 32 x 16 output tile per block.
 __global__ void __launch_bounds__(256) k_pv_tile(const uint8_t* __restrict__ valid,
                                                  const float* __restrict__ fm, int os, int of,
                                                  int lr, int hr, int lc, int hc,
                                                  uint8_t* __restrict__ pv, float* __restrict__ fmn) {
-  __shared__ uint8_t v[kPvR + kPvMaxHalo][kPvC + kPvMaxHalo];
-  __shared__ uint8_t rowok[kPvR + kPvMaxHalo][kPvC];
-  const int tx = threadIdx.x, ty = threadIdx.y;          // 32 x 8 threads
-  const int i0 = blockIdx.y * kPvR, j0 = blockIdx.x * kPvC;
-  const int th = kPvR + hr - lr, tw = kPvC + hc - lc;
-  for (int rr = ty; rr < th; rr += 8)
-    for (int cc = tx; cc < tw; cc += 32) {
-      const int r = i0 + lr + rr, c = j0 + lc + cc;
-      v[rr][cc] = (r >= 0 && r < os && c >= 0 && c < of) ? valid[r * of + c] : 0;
-    }
-  __syncthreads();
-  for (int rr = ty; rr < th; rr += 8) {
-    uint8_t ok = 1;
-    for (int d = 0; d <= hc - lc; ++d) ok &= v[rr][tx + d];
-    rowok[rr][tx] = ok;
-  }
-  __syncthreads();
-  const int j = j0 + tx;
-  for (int rr = ty; rr < kPvR; rr += 8) {
-    const int i = i0 + rr;
-    if (i >= os || j >= of) continue;
-    uint8_t ok = 1;
-    for (int d = 0; d <= hr - lr; ++d) ok &= rowok[rr + d][tx];
-    pv[i * of + j] = ok;
-    if (fmn) fmn[i * of + j] = valid[i * of + j] ? fm[i * of + j] : __int_as_float(0x7fc00000);
-  }
+  __shared__ PvShared sm;
+  pv_tile_block(sm, blockIdx.x, blockIdx.y, threadIdx.x, threadIdx.y, valid, fm, os, of, lr, hr,
+                lc, hc, pv, fmn);
 }
 
 __global__ void k_span_max(const TileGeo* __restrict__ geo, int64_t n, int* out) {

@@ -30,6 +30,30 @@ __device__ T block_reduce(T v, Op op, T* sh) {
   return v;  // valid in thread 0
 }
 
+// Max of N values at once (one pair of barriers for all N; min(x) is taken
+// as -max(-x)).  Result valid in warp 0.
+template <int N>
+__device__ void block_max_n(double (&v)[N], double (*sh)[32]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = fmax(v[i], __shfl_xor_sync(0xffffffffu, v[i], o));
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < N; ++i) sh[i][w] = v[i];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = lane < nw ? sh[i][lane] : -INFINITY;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = fmax(v[i], __shfl_xor_sync(0xffffffffu, v[i], o));
+  }
+}
+
 struct Sum {
   __device__ static double identity() { return 0.0; }
   __device__ double operator()(double a, double b) const { return a + b; }
@@ -218,46 +242,45 @@ __global__ void k_sum_final(const double* a, const double* b, int64_t n, double*
 __global__ void k_bbox(pxst_scan sc, const double* __restrict__ u, const double* __restrict__ di,
                        const double* __restrict__ dj, double* part, unsigned* ticket, double* out,
                        int64_t* grid) {
-  __shared__ double sh[32];
+  __shared__ double sh[8][32];
   __shared__ bool s_last;
   const int64_t rw = sc.roi[1] - sc.roi[0], cw = sc.roi[3] - sc.roi[2];
   const int64_t n = rw * cw, plane = sc.ss * sc.fs;
-  double a0 = INFINITY, b0 = -INFINITY, a1 = INFINITY, b1 = -INFINITY;
+  // (-min u0, max u0, -min u1, max u1)
+  double v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = (sc.roi[0] + k / cw) * sc.fs + sc.roi[2] + k % cw;
     if (!sc.work[p]) continue;
     const double x = u[p], y = u[plane + p];
-    a0 = fmin(a0, x); b0 = fmax(b0, x); a1 = fmin(a1, y); b1 = fmax(b1, y);
+    v[0] = fmax(v[0], -x); v[1] = fmax(v[1], x); v[2] = fmax(v[2], -y); v[3] = fmax(v[3], y);
   }
-  a0 = block_reduce(a0, Min(), sh);
-  b0 = block_reduce(b0, Max(), sh);
-  a1 = block_reduce(a1, Min(), sh);
-  b1 = block_reduce(b1, Max(), sh);
+  block_max_n<4>(v, sh);
   if (threadIdx.x == 0) {
     double* o = part + 4 * blockIdx.x;
-    o[0] = a0; o[1] = b0; o[2] = a1; o[3] = b1;
+    o[0] = v[0]; o[1] = v[1]; o[2] = v[2]; o[3] = v[3];
     __threadfence();
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  a0 = INFINITY; b0 = -INFINITY; a1 = INFINITY; b1 = -INFINITY;
-  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
-    a0 = fmin(a0, __ldcg(part + 4 * k)); b0 = fmax(b0, __ldcg(part + 4 * k + 1));
-    a1 = fmin(a1, __ldcg(part + 4 * k + 2)); b1 = fmax(b1, __ldcg(part + 4 * k + 3));
-  }
-  double c0 = INFINITY, d0 = -INFINITY, c1 = INFINITY, d1 = -INFINITY;
+  // (-min u0, max u0, -min u1, max u1, -min di, max di, -min dj, max dj)
+  double r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = -INFINITY;
+  for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = fmax(r[i], __ldcg(part + 4 * k + i));
   for (int64_t k = threadIdx.x; k < sc.n_good; k += blockDim.x) {
     const int64_t f = sc.good[k];
-    c0 = fmin(c0, di[f]); d0 = fmax(d0, di[f]); c1 = fmin(c1, dj[f]); d1 = fmax(d1, dj[f]);
+    const double a = di[f], b = dj[f];
+    r[4] = fmax(r[4], -a); r[5] = fmax(r[5], a); r[6] = fmax(r[6], -b); r[7] = fmax(r[7], b);
   }
-  a0 = block_reduce(a0, Min(), sh); b0 = block_reduce(b0, Max(), sh);
-  a1 = block_reduce(a1, Min(), sh); b1 = block_reduce(b1, Max(), sh);
-  c0 = block_reduce(c0, Min(), sh); d0 = block_reduce(d0, Max(), sh);
-  c1 = block_reduce(c1, Min(), sh); d1 = block_reduce(d1, Max(), sh);
+  block_max_n<8>(r, sh);
   if (threadIdx.x == 0) {
+    const double a0 = -r[0], b0 = r[1], a1 = -r[2], b1 = r[3];
+    const double c0 = -r[4], d0 = r[5], c1 = -r[6], d1 = r[7];
     out[0] = a0; out[1] = b0; out[2] = a1; out[3] = b1;
     out[4] = c0; out[5] = d0; out[6] = c1; out[7] = d1;
     if (grid) {
