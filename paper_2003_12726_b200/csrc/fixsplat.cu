@@ -69,6 +69,7 @@ struct FixArgs {
   const double* di;
   const double* dj;
   int64_t n0, m0, os, of;      // primary grid: the object (mode 0) or the reference (1, 2)
+  double n0d, m0d, os1, of1;   // (double) n0, m0, os - 1, of - 1: constant-bank operands
   int64_t k_lo, k_hi;          // good-frame range of the launch
   int64_t frames_per_z;        // frames per grid.z slice (multiple of kXB)
   FixAcc A;                    // mode 0: object; modes 1, 2: reference plane
@@ -122,6 +123,18 @@ __device__ __forceinline__ void region_term(unsigned* slo, int idx, double scale
   atomicAdd(reinterpret_cast<int*>(slo) + idx + HI, hi);
 }
 
+// The same term through a 32-bit shared-memory address (the hot path):
+// lo at [addr], hi at [addr + HIB]; value planes and the c0 + 1 corner are
+// immediate offsets (OFF) from one address register.
+template <int HIB, int OFF>
+__device__ __forceinline__ void region_red(unsigned addr, double scaled, double w) {
+  unsigned lo;
+  int hi;
+  fix_limbs(scaled, w, lo, hi);
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(lo), "n"(OFF));
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(hi), "n"(OFF + HIB));
+}
+
 // A term straight into the global images (no region; and tiny-weight
 // corners, |t| < 2^51 fine quanta).
 __device__ __forceinline__ void global_term(long long* g, long long* gf, int64_t cell,
@@ -135,8 +148,16 @@ __device__ __forceinline__ void global_term(long long* g, long long* gf, int64_t
 // (max|I| + max W max|ref|)^2 / min sigma^2, often 10^4 x the typical eps),
 // so a coarse-weight term below 2^21 coarse quanta goes to a second band in
 // units of q * 2^-20 (the fine image) and keeps >= 20 significant bits.
-__device__ __forceinline__ bool plane_band(double scaled, double w) {
-  return fabs(scaled * w) < 2097152.0;
+// The rule compares exponents: with scaled = m1 2^e1 and w = m2 2^e2
+// (m in [1, 2)), band <=> e1 + e2 < 20, so a band term is below 2^21 coarse
+// quanta (< 2^41 fine quanta) and a coarse term at least 2^20.  band_key is
+// the per-sample part: plane_band(key, w) = hi word of w below key.
+__device__ __forceinline__ int band_key(double scaled) {
+  const int e1 = (__double2hiint(scaled) >> 20) & 0x7ff;          // biased exponent, 0 for 0
+  return min(2 * 1023 + 20 - e1, 2047) << 20;   // (a zero / denormal eps: every term in the band)
+}
+__device__ __forceinline__ bool plane_band(int key, double w) {   // w >= 0
+  return __double2hiint(w) < key;
 }
 
 #ifndef PXST_FIX_OCC0
@@ -156,12 +177,13 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   __shared__ double s_frw[ERR ? kXW : 1][ERR ? kXTab : 1];   // per-frame sums of each warp
   __shared__ int s_cmax;
   __shared__ int4 s_sess[2];   // session footprint (R0, R1, C0, C1), (end frame, region)
+  __shared__ double s_cb[4];   // mode 2: (double) origin and last row / column of the next grid
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(slo));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   const int64_t plane = a.sc.ss * a.sc.fs;
-  const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
-  const double os1 = static_cast<double>(a.os - 1), of1 = static_cast<double>(a.of - 1);
+  const double n0d = a.n0d, m0d = a.m0d;
   const int of = static_cast<int>(a.of);
 
   int64_t p[2];
@@ -253,8 +275,12 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
     ofb = a.grid_b[3];
     splat_b = osb > 0 && ofb > 0 && osb * ofb <= a.cap_b;
   }
-  const double n0b = static_cast<double>(a.n0 - dn), m0b = static_cast<double>(a.m0 - dm);
-  const double osb1 = static_cast<double>(osb - 1), ofb1 = static_cast<double>(ofb - 1);
+  if (MODE == 2 && threadIdx.x == 0) {   // (read after the frame table's barrier)
+    s_cb[0] = static_cast<double>(a.n0 - dn);
+    s_cb[1] = static_cast<double>(a.m0 - dm);
+    s_cb[2] = static_cast<double>(osb - 1);
+    s_cb[3] = static_cast<double>(ofb - 1);
+  }
   double W2[2], vsc[2], isig[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -336,6 +362,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
       // stack values in flight); region / direct are two compiled bodies
       auto session = [&](auto region_c) {
         constexpr bool REG = decltype(region_c)::value;
+        constexpr int HIB = NV * RC * 4;           // lo -> hi limb, bytes
+        constexpr int VB = RC * 4;                 // value plane stride, bytes
         float In[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) In[e] = live[e] ? __ldg(a.sc.frames + t_off[s0] + p[e]) : 0.f;
@@ -351,27 +379,36 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const bool act = live[e];
-            const double x = u0[e] - dI - n0d;                // recon.py:138, 418
-            const double y = u1[e] - dJ - m0d;
-            const bool inA = act && x >= 0.0 && x <= os1 && y >= 0.0 && y <= of1;  // interp.py:67, 103-107
+            const double tx = u0[e] - dI, ty = u1[e] - dJ;
+            const double x = tx - a.n0d;                      // recon.py:138, 418
+            const double y = ty - a.m0d;
+            const bool inA = act && x >= 0.0 && x <= a.os1 && y >= 0.0 && y <= a.of1;  // interp.py:67, 103-107
             const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
             const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
             const double gx = 1.0 - fx, gy = 1.0 - fy;
             const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
             const double I = static_cast<double>(Ic[e]);
             double sAn, sAd;
+            int bkey = 0;
             if (ERR) {
-              double eps = 0.0;
-              if (act) {
-                // masked bilinear read (interp.py:53-85) of the grouped reference:
-                // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell
-                const double2 z2 = make_double2(0.0, 0.0);
-                const int64_t a00 = (int64_t)r0 * a.of + c0;
-                const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
-                const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
-                const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
-                double den = 0.0, nm = 0.0;
-                bool all = true;
+              // masked bilinear read (interp.py:53-85) of the grouped reference:
+              // g[r][c] = (v(r, c), v(r + 1, c)), NaN = invalid cell.  (A lane
+              // without a work pixel has I = 0, W = 1, 1/sigma2 = 0: eps = 0.)
+              const double2 z2 = make_double2(0.0, 0.0);
+              const int a00 = r0 * of + c0;                   // os * of < 2^31 (check_ref)
+              const double2 g0 = inA ? __ldg(a.grp + a00) : z2;
+              const double2 g1 = (inA && fy > 0.0) ? __ldg(a.grp + a00 + 1) : z2;
+              const double cv[4] = {g0.x, g1.x, g0.y, g1.y};
+              const bool anynan = (g0.x != g0.x) || (g1.x != g1.x) || (g0.y != g0.y) || (g1.y != g1.y);
+              double den, nm;
+              bool all = true;
+              if (!__any_sync(0xffffffffu, anynan)) {
+                // every corner of every lane valid: the same sums without selects
+                den = ((cw[0] + cw[1]) + cw[2]) + cw[3];
+                nm = fma(cw[3], cv[3], fma(cw[2], cv[2], fma(cw[1], cv[1], cw[0] * cv[0])));
+              } else {
+                den = 0.0;
+                nm = 0.0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   const bool m = cv[q] == cv[q];
@@ -379,15 +416,17 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
                   den = fma(cw[q], m ? 1.0 : 0.0, den);
                   nm = fma(cw[q], m ? cv[q] : 0.0, nm);
                 }
-                const bool ok = inA && den > 0.0;
-                const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
-                const double r = ok ? I - Wv[e] * v : I - Wv[e];       // recon.py:421
-                eps = (r * r) * isig[e];                                // recon.py:422
               }
+              const bool ok = inA && den > 0.0;
+              const double v = !ok ? 0.0 : (all ? nm * (2.0 - den) : nm / den);
+              const double r = I - Wv[e] * v;                           // recon.py:421
+              const double rr = ok ? r : I - Wv[e];
+              const double eps = (rr * rr) * isig[e];                   // recon.py:422
               pix[e] += eps;
               ef += eps;
               sAn = eps * qa_n;       // plane: value eps, weight 1 (recon.py:425)
               sAd = qa_d;
+              bkey = band_key(sAn);
             } else {
               dropped += (count_drop && act && !inA) ? 1u : 0u;
               sAn = I * vsc[e] * qa_n;   // value * weight = (I / W) W^2 (interp.py:112-122)
@@ -396,8 +435,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
             // hot path: every corner weight 0 (nothing to add) or >= kFineW;
             // the others, and the direct sessions, take the per-corner path
             // (smallest nonzero corner weight = min(fx, 1-fx) min(fy, 1-fy)
-            // over the axes with a nonzero fraction)
-            // (classified in float32: only the routing depends on it)
+            // over the axes with a nonzero fraction; classified in float32:
+            // only the routing depends on it)
             const bool hot = REG && small_corner_ok(fx, fy);
             // warp-uniform: skip the r0+1 / c0+1 corners when no lane weights
             // them (config 2: u_ss = x, every fx = 0)
@@ -406,26 +445,35 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
             if (inA && hot) {
               const int l = (r0 - R0) * nc + (c0 - C0);
               PXST_DCHECK(r0 >= R0 && c0 >= C0 && l >= 0 && l + nc + 1 < ncell);
-              const int dl[4] = {0, 1, nc, nc + 1};
-              const double sAnb = sAn * 0x1p20;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {   // (a zero-weight corner adds 0: no branch)
-                if (((q & 2) && !need_r1) || ((q & 1) && !need_c1)) continue;
+              const unsigned a0 = sbase + 4u * static_cast<unsigned>(l);
+              const unsigned a1 = a0 + 4u * static_cast<unsigned>(nc);
+              // one corner: numerator (plane: coarse or fine band by its size),
+              // denominator; a zero-weight corner adds 0 (no branch)
+              auto corner = [&](unsigned ad, auto off_c, double w) {
+                constexpr int OFF = decltype(off_c)::value;
                 if (ERR) {
-                  const bool band = plane_band(sAn, cw[q]);
-                  region_term<NV * RC>(slo, l + dl[q] + (band ? kBandV * RC : 0), band ? sAnb : sAn,
-                                       cw[q]);
+                  const bool band = plane_band(bkey, w);
+                  const unsigned an = ad + (band ? kBandV * VB : 0);
+                  const double sn = __hiloint2double(__double2hiint(sAn) + (band ? (20 << 20) : 0),
+                                                     __double2loint(sAn));
+                  region_red<HIB, OFF>(an, sn, w);
                 } else {
-                  region_term<NV * RC>(slo, l + dl[q], sAn, cw[q]);
+                  region_red<HIB, OFF>(ad, sAn, w);
                 }
-                region_term<NV * RC>(slo, l + dl[q] + RC, sAd, cw[q]);
+                region_red<HIB, OFF + VB>(ad, sAd, w);
+              };
+              corner(a0, std::integral_constant<int, 0>{}, cw[0]);
+              if (need_c1) corner(a0, std::integral_constant<int, 4>{}, cw[1]);
+              if (need_r1) {
+                corner(a1, std::integral_constant<int, 0>{}, cw[2]);
+                if (need_c1) corner(a1, std::integral_constant<int, 4>{}, cw[3]);
               }
             } else if (inA) {
               const int64_t cell = (int64_t)r0 * a.of + c0;
               const int64_t dcell[4] = {0, 1, a.of, a.of + 1};
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                if (ERR && cw[q] >= kFineW && plane_band(sAn, cw[q]))
+                if (ERR && cw[q] >= kFineW && plane_band(bkey, cw[q]))
                   red64(a.A.num_f + cell + dcell[q], fix_value(sAn * 0x1p20, cw[q]));
                 else
                   global_term(a.A.num, a.A.num_f, cell + dcell[q], sAn, cw[q]);
@@ -438,7 +486,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               // the next object's own position, as make_reference computes it
               // (recon.py:138: u - d - origin), so the terms equal a separate
               // object formation bit for bit
-              const double xb = u0[e] - dI - n0b, yb = u1[e] - dJ - m0b;
+              const double n0b = s_cb[0], m0b = s_cb[1], osb1 = s_cb[2], ofb1 = s_cb[3];
+              const double xb = tx - n0b, yb = ty - m0b;
               const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
               const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
               const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
@@ -452,12 +501,18 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
                 const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
                 PXST_DCHECK(l >= 0 && l + nc + 1 < ncell);
-                const int dl[4] = {0, 1, nc, nc + 1};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  if (((q & 2) && !need_r1b) || ((q & 1) && !need_c1b)) continue;
-                  region_term<NV * RC>(slo, l + dl[q] + 2 * RC, sBn, cwb[q]);
-                  region_term<NV * RC>(slo, l + dl[q] + 3 * RC, sBd, cwb[q]);
+                const unsigned b0 = sbase + 4u * static_cast<unsigned>(l) + 2 * VB;
+                const unsigned b1 = b0 + 4u * static_cast<unsigned>(nc);
+                auto cornerb = [&](unsigned ad, auto off_c, double w) {
+                  constexpr int OFF = decltype(off_c)::value;
+                  region_red<HIB, OFF>(ad, sBn, w);
+                  region_red<HIB, OFF + VB>(ad, sBd, w);
+                };
+                cornerb(b0, std::integral_constant<int, 0>{}, cwb[0]);
+                if (need_c1b) cornerb(b0, std::integral_constant<int, 4>{}, cwb[1]);
+                if (need_r1b) {
+                  cornerb(b1, std::integral_constant<int, 0>{}, cwb[2]);
+                  if (need_c1b) cornerb(b1, std::integral_constant<int, 4>{}, cwb[3]);
                 }
               } else if (inB) {
                 const int64_t cellb = (int64_t)r0b * ofb + c0b;
@@ -737,6 +792,10 @@ int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma
 template <int MODE>
 int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
   if (const char* v = getenv("PXST_FIX_NO_REGION")) a.no_region = v[0] == '1';
+  a.n0d = static_cast<double>(a.n0);
+  a.m0d = static_cast<double>(a.m0);
+  a.os1 = static_cast<double>(a.os - 1);
+  a.of1 = static_cast<double>(a.of - 1);
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2], rw = a.sc.roi[1] - a.sc.roi[0];
   dim3 g((unsigned)((cw + kXC - 1) / kXC), (unsigned)((rw + kXR - 1) / kXR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");

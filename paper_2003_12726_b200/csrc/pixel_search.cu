@@ -69,6 +69,8 @@ struct PixArgs {
   const uint8_t* valid;
   const uint8_t* pv;
   const float* fmn;          // NaN-encoded reference (slow fix-up)
+  const float2* fm2;         // padded (value, mask) reference (trial_pad), pad cells each side
+  int pad;
   int64_t os, of, n0, m0;
   const float* fw;           // nullable frame weights [n_frames, ss, fs]
   const double* var;         // normaliser [ss*fs]
@@ -227,6 +229,8 @@ struct PvJob {
   int os, of, lr, hr, lc, hc, nx;
   uint8_t* pv;
   float* fmn;
+  float2* fm2;
+  int pad;
 };
 __global__ void __launch_bounds__(256) k_k2_prep(PixArgs a, TileGeo* geo, int init_out,
                                                  unsigned* zero2, PvJob pj, int n_pv,
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(256) k_k2_prep(PixArgs a, TileGeo* geo, int in
   if (blockIdx.x < n_pv) {
     pv_tile_block(sm.pv, blockIdx.x % pj.nx, blockIdx.x / pj.nx, threadIdx.x & 31,
                   threadIdx.x >> 5, pj.valid, pj.fm, pj.os, pj.of, pj.lr, pj.hr, pj.lc, pj.hc,
-                  pj.pv, pj.fmn);
+                  pj.pv, pj.fmn, pj.fm2, pj.pad);
     return;
   }
   const int64_t b = blockIdx.x - n_pv;
@@ -804,6 +808,12 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
     tb[j] = t % a.kb;
     to[j] = ta[j] * of + tb[j];
   }
+  unsigned tp[NJ];      // the same offsets in the padded image
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int t = min(lane + 32 * j, nk - 1);
+    tp[j] = (t / a.kb) * (of + 2 * a.pad) + t % a.kb;
+  }
   for (;;) {
     unsigned e = 0;
     if (lane == 0) e = atomicAdd(next, 1u);
@@ -871,9 +881,27 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
                                             __shfl_sync(0xffffffffu, sl.fy, bsel), W,
                                             __shfl_sync(0xffffffffu, Il, bsel),
                                             __shfl_sync(0xffffffffu, fwl, bsel));
-        // warp-uniform: the whole window's 2x2 cells on the grid (the usual
-        // case: skipped samples touch invalid cells, not the grid's edge)
-        if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {
+        // warp-uniform: the window's 2x2 cells inside the padded (value,
+        // mask) image (every on-grid sample): two row pointers per trial,
+        // four 8-byte loads, no bounds tests or selects
+        if (a.fm2 && pr0 >= -a.pad && pc0 >= -a.pad && pr0 + a.ka < os + a.pad &&
+            pc0 + a.kb < of + a.pad) {
+          const int ofp = of + 2 * a.pad;
+          const unsigned w0 = static_cast<unsigned>((pr0 + a.pad) * ofp + (pc0 + a.pad));
+          const unsigned w1 = w0 + (es.fxp ? ofp : 0);
+          // (no trial-count guard: lanes past the window repeat its last
+          // trial, their sums are never read; the NJ trials' loads overlap)
+          float v[NJ];
+          if (es.fyp) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) v[j] = trial_pad<true>(a.fm2, w0 + tp[j], w1 + tp[j], 1, es);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) v[j] = trial_pad<false>(a.fm2, w0 + tp[j], w1 + tp[j], 0, es);
+          }
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) part[j] += v[j];
+        } else if (pr0 >= 0 && pc0 >= 0 && pr0 + a.ka < os && pc0 + a.kb < of) {
           const float* w0 = a.fmn + (pr0 * of + pc0);
 #pragma unroll
           for (int j = 0; j < NJ; ++j)
@@ -1134,10 +1162,19 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     PXST_REQUIRE(tiles_y <= kMaxGridY, "ROI too tall");
     const int64_t tiles = (int64_t)a.tiles_x * tiles_y;
 
-    Scratch pvbuf, geo, part, fmpad, fmn;
+    Scratch pvbuf, geo, part, fmpad, fmn, fm2;
     if (int e = pvbuf.alloc(ref->os * ref->of, s)) return e;
     if (int e = fmn.alloc(sizeof(float) * ref->os * ref->of, s)) return e;
     a.fmn = fmn.as<float>();
+    // padded (value, mask) copy for the lanes-over-trials fix-up (windows of
+    // more than 3 rows); the pad holds every trial corner of an on-grid sample
+    a.pad = max(ra, rb) + 2;
+    if (na > 3 && (ref->os + 2 * a.pad) * (ref->of + 2 * a.pad) < (int64_t(1) << 31) &&
+        !getenv("PXST_K2_NO_PAD")) {
+      if (int e = fm2.alloc(sizeof(float2) * (ref->os + 2 * a.pad) * (ref->of + 2 * a.pad), s))
+        return e;
+      a.fm2 = fm2.as<float2>();
+    }
     a.pv = pvbuf.as<uint8_t>();
     if (int e = geo.alloc(sizeof(TileGeo) * tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
@@ -1161,7 +1198,7 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
       PXST_REQUIRE(2 * ra + 1 <= kPvMaxHalo && 2 * rb + 1 <= kPvMaxHalo, "patch extent too large");
       PvJob pj{ref->valid, ref->fm, static_cast<int>(ref->os), static_cast<int>(ref->of),
                -ra, ra + 1, -rb, rb + 1, static_cast<int>((ref->of + kPvC - 1) / kPvC),
-               pvbuf.as<uint8_t>(), fmn.as<float>()};
+               pvbuf.as<uint8_t>(), fmn.as<float>(), fm2.as<float2>(), a.pad};
       const int64_t n_pv = (int64_t)pj.nx * ((ref->os + kPvR - 1) / kPvR);
       const int64_t blocks = n_pv + (tiles + kPrepTiles - 1) / kPrepTiles;
       PXST_REQUIRE(blocks < (int64_t(1) << 31), "reference image too large");

@@ -293,6 +293,37 @@ __device__ __forceinline__ float trial_patch(float v00, float v01, float v10, fl
 
 
 
+// Exact trial from the padded (value, mask) copy of the reference (fm2,
+// pv_tile_block): cell = (v, m) with m = 1 valid (v = the masked float32
+// value), m = 0 invalid (v = 0), m = -inf off the grid (the padding border,
+// v = 0).  num = sum w v and den = sum w m are plain FMA chains in
+// masked_read's corner order -- an invalid cell adds w * 0 to both, exactly
+// what the select forms above add -- and den > 0 holds iff every corner with
+// nonzero weight is on the grid and one of them is valid (a weighted off-grid
+// corner makes den -inf, or NaN with a zero weight: both fail the test), the
+// reference's rule (interp.py:67-85).  Callers alias zero-weight corners onto
+// weighted ones (dr = 0 when fx == 0, dc = 0 when fy == 0).  i0 / i1 = the
+// cell index of the trial's base in rows r0 / r0 + dr.
+template <bool DC1>
+__device__ __forceinline__ float trial_pad(const float2* __restrict__ fm2, unsigned i0,
+                                           unsigned i1, int dc, const ExactSample& e) {
+  // (unsigned 32-bit cell indices: one IMAD.WIDE per row pointer)
+  const float2* p0 = fm2 + i0;
+  const float2* p1 = fm2 + i1;
+  const float2 c00 = __ldg(p0), c01 = __ldg(p0 + (DC1 ? 1 : dc));
+  const float2 c10 = __ldg(p1), c11 = __ldg(p1 + (DC1 ? 1 : dc));
+  float den = e.w00 * c00.y;
+  float num = e.w00 * c00.x;
+  den = fmaf(e.w01, c01.y, den);
+  num = fmaf(e.w01, c01.x, num);
+  den = fmaf(e.w10, c10.y, den);
+  num = fmaf(e.w10, c10.x, num);
+  den = fmaf(e.w11, c11.y, den);
+  num = fmaf(e.w11, c11.x, num);
+  const float r = fmaf(-e.W, num * rcp_approx(den), e.I);
+  return den > 0.f ? e.fwv * (r * r) : e.fb;
+}
+
 // float64 3x3 least-squares paraboloid (recon.py:183-207); e is row-major
 // [ss offset -1,0,1][fs offset -1,0,1].  Offsets clipped to [-1, 1]; (0,0)
 // when the Hessian is not positive definite.
@@ -388,7 +419,8 @@ __device__ __forceinline__ void pv_tile_block(PvShared& sm, int bx, int by, int 
                                               const uint8_t* __restrict__ valid,
                                               const float* __restrict__ fm, int os, int of, int lr,
                                               int hr, int lc, int hc, uint8_t* __restrict__ pv,
-                                              float* __restrict__ fmn) {
+                                              float* __restrict__ fmn,
+                                              float2* __restrict__ fm2 = nullptr, int pad = 0) {
   const int i0 = by * kPvR, j0 = bx * kPvC;
   const int th = kPvR + hr - lr, tw = kPvC + hc - lc;
   for (int rr = ty; rr < th; rr += 8)
@@ -411,6 +443,22 @@ __device__ __forceinline__ void pv_tile_block(PvShared& sm, int bx, int by, int 
     for (int d = 0; d <= hr - lr; ++d) ok &= sm.rowok[rr + d][tx];
     pv[i * of + j] = ok;
     if (fmn) fmn[i * of + j] = valid[i * of + j] ? fm[i * of + j] : __int_as_float(0x7fc00000);
+  }
+  if (fm2) {
+    // padded (value, mask) copy (trial_pad): the tile's cells, and for tiles on
+    // the image's edge the pad-wide border next to them (mask -inf)
+    const int ofp = of + 2 * pad;
+    const int rlo = by == 0 ? -pad : 0, clo = bx == 0 ? -pad : 0;
+    const int rhi = i0 + kPvR >= os ? os - i0 + pad : kPvR;
+    const int chi = j0 + kPvC >= of ? of - j0 + pad : kPvC;
+    for (int rr = rlo + ty; rr < rhi; rr += 8)
+      for (int cc = clo + tx; cc < chi; cc += 32) {
+        const int i = i0 + rr, jj = j0 + cc;
+        float2 v = make_float2(0.f, __int_as_float(0xff800000));
+        if (i >= 0 && i < os && jj >= 0 && jj < of)
+          v = valid[i * of + jj] ? make_float2(fm[i * of + jj], 1.f) : make_float2(0.f, 0.f);
+        fm2[(int64_t)(i + pad) * ofp + (jj + pad)] = v;
+      }
   }
 }
 
