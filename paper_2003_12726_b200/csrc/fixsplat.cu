@@ -35,7 +35,7 @@ namespace {
 // detector columns apart and land on distinct cells (adjacent columns often
 // share a cell at magnification < 1: same-address shared atomics serialise).
 constexpr int kXR = 8, kXC = 64, kXT = 256, kXW = kXT / 32;  // tile, threads, warps
-constexpr int kXB = 8;        // frames per batch
+constexpr int kXB = 8;        // (frame-table chunks are multiples of this)
 #ifndef PXST_FIX_TAB
 #define PXST_FIX_TAB 128
 #endif
@@ -71,7 +71,7 @@ struct FixArgs {
   int64_t n0, m0, os, of;      // primary grid: the object (mode 0) or the reference (1, 2)
   double n0d, m0d, os1, of1;   // (double) n0, m0, os - 1, of - 1: constant-bank operands
   int64_t k_lo, k_hi;          // good-frame range of the launch
-  int64_t frames_per_z;        // frames per grid.z slice (multiple of kXB)
+  int64_t frames_per_z;        // frames per grid.z slice (fix_slices)
   FixAcc A;                    // mode 0: object; modes 1, 2: reference plane
   FixAcc B;                    // mode 2: next object
   const int64_t* grid_b;       // mode 2: device (n0, m0, os, of) of the next object
@@ -789,6 +789,31 @@ int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma
   return launch_quanta_job(j, s);
 }
 
+// Frame slices (grid.z) of a pass over nk frames with n_cta tiles when
+// `resident` CTAs fit the GPU: balanced slices (sizes differ by at most one
+// frame), their number chosen by a wave model -- ceil(CTAs / resident) waves,
+// each costing a slice's frames plus the per-CTA setup (bounding box,
+// histogram, frame table: about kSetupFrames frames' worth of instructions).
+// (Round 2 used ~3 waves of slices rounded up to 8 frames: 121 frames gave
+// five slices of 24 and one of a single frame, 13 % of the instructions.)
+constexpr int kSetupFrames = 4;
+static void fix_slices(int64_t nk, int64_t n_cta, int64_t resident, int64_t* n_z, int64_t* fpz) {
+  int64_t best_z = 1;
+  double best = 0.0;
+  const int64_t zmax = nk < 64 ? (nk < 1 ? 1 : nk) : 64;
+  for (int64_t z = 1; z <= zmax; ++z) {
+    const int64_t f = (nk + z - 1) / z;
+    const int64_t zz = (nk + f - 1) / f;                   // slices actually used
+    const int64_t waves = (n_cta * zz + resident - 1) / resident;
+    const double cost = static_cast<double>(waves) * static_cast<double>(f + kSetupFrames);
+    if (z == 1 || cost < best) { best = cost; best_z = zz; }
+  }
+  *fpz = (nk + best_z - 1) / best_z;
+  if (*fpz < 1) *fpz = 1;
+  *n_z = (nk + *fpz - 1) / *fpz;
+  if (*n_z < 1) *n_z = 1;
+}
+
 template <int MODE>
 int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
   if (const char* v = getenv("PXST_FIX_NO_REGION")) a.no_region = v[0] == '1';
@@ -812,14 +837,8 @@ int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
   PXST_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<MODE>, kXT,
                                                                 smem));
   const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  const int64_t n_batches = (nk + kXB - 1) / kXB;
-  int64_t n_z = (3 * resident + a.n_cta - 1) / a.n_cta;
-  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
-  n_z = n_z < 1 ? 1 : n_z;
-  a.frames_per_z = ((n_batches + n_z - 1) / n_z) * kXB;
-  if (a.frames_per_z < kXB) a.frames_per_z = kXB;
-  n_z = (nk + a.frames_per_z - 1) / a.frames_per_z;
-  if (n_z < 1) n_z = 1;
+  int64_t n_z;
+  fix_slices(nk, a.n_cta, resident, &n_z, &a.frames_per_z);
   g.z = static_cast<unsigned>(n_z);
   if (n_z_out) *n_z_out = static_cast<int>(n_z);
   if (nk <= 0) return PXST_OK;
@@ -848,14 +867,9 @@ int fix_pass_slices(const pxst_scan* sc, int64_t nk, int mode, int64_t* n_cta) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fix_pass<0>, kXT, smem);
   }
   const int64_t resident = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  const int64_t n_batches = (nk + kXB - 1) / kXB;
-  int64_t n_z = (3 * resident + ctas - 1) / ctas;
-  n_z = n_z < 1 ? 1 : (n_z > n_batches ? n_batches : n_z);
-  n_z = n_z < 1 ? 1 : n_z;
-  int64_t fpz = ((n_batches + n_z - 1) / n_z) * kXB;
-  if (fpz < kXB) fpz = kXB;
-  n_z = (nk + fpz - 1) / fpz;
-  return static_cast<int>(n_z < 1 ? 1 : n_z);
+  int64_t n_z, fpz;
+  fix_slices(nk, ctas, resident, &n_z, &fpz);
+  return static_cast<int>(n_z);
 }
 
 template int launch_fix_pass<0>(FixArgs&, int*, cudaStream_t);
