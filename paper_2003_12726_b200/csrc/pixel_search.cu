@@ -491,9 +491,18 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       const int64_t off = t_off[jj];
       I = live ? __ldg(a.sc.frames + off + p) : 0.f;
       fwv = (live && fwp) ? __ldg(fwp + off + p) : 1.f;
-      if (KA == 1)
-        return make_sample_split<true, KA, KB, BC>(a, g, us, t_ds[jj], live ? fwv : -1.f,
-                                                   t_wr[jj], t_wc[jj]);
+      // (fwv goes in as loaded and "live" into the pre flag: a select on the
+      // weight here would wait for this frame-ahead load -- and for the stack
+      // value sharing its scoreboard -- in the frame that issues it; ncu
+      // showed 32 % of the 1 x 17 kernel's stall samples on that select)
+      // (the two-dimensional windows keep the select: without it the 13 x 13
+      // kernel spilled, 91.0 -> 93.9 ms at config 3)
+      if (KA == 1) {
+        Sample sm_ = make_sample_split<true, KA, KB, BC>(a, g, us, t_ds[jj], fwv, t_wr[jj],
+                                                         t_wc[jj]);
+        sm_.pre = sm_.pre && live;
+        return sm_;
+      }
       return make_sample<true, KA, KB, BC>(a, g, u0, u1, t_di[jj], t_dj[jj], live ? fwv : -1.f,
                                            t_wr[jj], t_wc[jj]);
     };
