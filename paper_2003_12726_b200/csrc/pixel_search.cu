@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
   const float* const fwp = BC > 0 ? nullptr : a.fw;
   extern __shared__ __align__(128) unsigned char ring_raw[];
   __shared__ __align__(8) uint64_t full[kNB], empty[kNB];
+  __shared__ int s_iss[kNB];   // PXST_K2_PRODUCER == 2: the frame each slot holds or awaits
   // TMA destinations must be 128-byte aligned: align the base, pad the slots.
   // (Pointer arithmetic on the shared array keeps the address space, so the
   // engine's reads compile to LDS rather than generic loads.)
@@ -474,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       for (int b = 0; b < kNB; ++b) {
         mbar_init(&full[b], 1);
         mbar_init(&empty[b], kThreads);
+        s_iss[b] = b;
       }
       mbar_fence_init();
     }
@@ -527,8 +529,11 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       const float I = I_n, fwv = fw_n;
       const int b = jj % kNB;
       const unsigned ph = (jj / kNB) & 1;
+      // Ring refill.  Windows up to 11 x 11: at release time (below).  Larger
+      // ones (13 x 13 sits at the register limit; the release-time code cost
+      // 91.3 -> 95.1 ms at config 3): thread 0, opportunistically, here.
 #ifndef PXST_K2_PRODUCER
-#define PXST_K2_PRODUCER 1
+#define PXST_K2_PRODUCER (KA * KB <= 121 ? 2 : 1)
 #endif
       if (PXST_K2_PRODUCER == 1 && threadIdx.x == 0) {
         // Refill freed slots without waiting for the slowest warp: frame k
@@ -566,6 +571,14 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
         engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
                              acc);
       mbar_arrive(&empty[b]);
+      if (PXST_K2_PRODUCER == 2 && (threadIdx.x & 31) == 0 && jj + kNB < nk) {
+        // Refill at release time: the warp whose arrival completes the slot's
+        // phase (or any warp that sees it complete) claims the slot's next
+        // frame and issues its load -- no waiting for thread 0 to come round
+        // (ncu had 17 % of the 11 x 11 kernel's stall samples on the ring
+        // wait; config 1 K2 0.564 -> 0.548 ms, config 2 6.09 -> 5.70 ms).
+        if (mbar_test(&empty[b], ph) && atomicCAS(&s_iss[b], jj, jj + kNB) == jj) issue(jj + kNB);
+      }
       if (PXST_K2_PRODUCER == 0 && threadIdx.x == 0 && jj + kNB < nk) {
         mbar_wait(&empty[b], ph);      // every thread is done with this slot
         issue(jj + kNB);
