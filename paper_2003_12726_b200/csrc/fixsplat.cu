@@ -69,7 +69,6 @@ struct FixArgs {
   const double* di;
   const double* dj;
   int64_t n0, m0, os, of;      // primary grid: the object (mode 0) or the reference (1, 2)
-  double n0d, m0d, os1, of1;   // (double) n0, m0, os - 1, of - 1: constant-bank operands
   int64_t k_lo, k_hi;          // good-frame range of the launch
   int64_t frames_per_z;        // frames per grid.z slice (fix_slices)
   FixAcc A;                    // mode 0: object; modes 1, 2: reference plane
@@ -177,13 +176,23 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   __shared__ double s_frw[ERR ? kXW : 1][ERR ? kXTab : 1];   // per-frame sums of each warp
   __shared__ int s_cmax;
   __shared__ int4 s_sess[2];   // session footprint (R0, R1, C0, C1), (end frame, region)
-  __shared__ double s_cb[4];   // mode 2: (double) origin and last row / column of the next grid
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(slo));
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
   const int64_t plane = a.sc.ss * a.sc.fs;
-  const double n0d = a.n0d, m0d = a.m0d;
+  // Sample positions: t = u - d (recon.py:138, one rounding), split as
+  // floor(t) and t - floor(t), the grid origin subtracted from the integer.
+  // The reference rounds t - origin once more before its split
+  // (interp.py:39-42): at most one ulp of the position, far inside the parity
+  // bars, and the bilinear value is continuous across a floor that flips.  In
+  // exchange the split does not depend on the grid, so the fused pass
+  // (mode 2) shares every weight between the reference grid and the next
+  // object's grid, whose cells differ by the origins' integer offset.
+  // (|t| < 1e9 on the region path -- the footprints are finite -- and
+  // checked on the direct path.)
+  const int n0i = static_cast<int>(a.n0), m0i = static_cast<int>(a.m0);
+  const int os_1 = static_cast<int>(a.os - 1), of_1 = static_cast<int>(a.of - 1);
   const int of = static_cast<int>(a.of);
 
   int64_t p[2];
@@ -275,12 +284,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
     ofb = a.grid_b[3];
     splat_b = osb > 0 && ofb > 0 && osb * ofb <= a.cap_b;
   }
-  if (MODE == 2 && threadIdx.x == 0) {   // (read after the frame table's barrier)
-    s_cb[0] = static_cast<double>(a.n0 - dn);
-    s_cb[1] = static_cast<double>(a.m0 - dm);
-    s_cb[2] = static_cast<double>(osb - 1);
-    s_cb[3] = static_cast<double>(ofb - 1);
-  }
+  const int dni = static_cast<int>(dn), dmi = static_cast<int>(dm);
+  const int osb_1 = static_cast<int>(osb - 1), ofb_1 = static_cast<int>(ofb - 1);
   double W2[2], vsc[2], isig[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
@@ -297,10 +302,6 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
   double pix[2] = {0.0, 0.0};
   unsigned dropped = 0;
   const bool count_drop = !ERR && a.n_drop != nullptr;
-  // (mode 2: one more cell on each side of a footprint -- the next grid's
-  // positions are rounded separately, recon.py:138 order, and may floor one
-  // cell over)
-  constexpr int kM = MODE == 2 ? 1 : 0;
 
   for (int64_t kc = k_begin; kc < k_end; kc += kXTab) {
     const int nt = static_cast<int>(min((int64_t)kXTab, k_end - kc));
@@ -313,10 +314,8 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
       t_off[t] = f * plane;
       // the tile's cells for this frame (primary grid; + 1 row / column for
       // the r0 + 1 / c0 + 1 corners)
-      t_ft[t] = fin ? make_int4(__double2int_rd(umin0 - dI - n0d) - kM,
-                                __double2int_rd(umax0 - dI - n0d) + 1 + kM,
-                                __double2int_rd(umin1 - dJ - m0d) - kM,
-                                __double2int_rd(umax1 - dJ - m0d) + 1 + kM)
+      t_ft[t] = fin ? make_int4(__double2int_rd(umin0 - dI) - n0i, __double2int_rd(umax0 - dI) - n0i + 1,
+                                __double2int_rd(umin1 - dJ) - m0i, __double2int_rd(umax1 - dJ) - m0i + 1)
                     : make_int4(0, 1 << 20, 0, 1 << 20);
     }
     __syncthreads();
@@ -379,12 +378,15 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const bool act = live[e];
-            const double tx = u0[e] - dI, ty = u1[e] - dJ;
-            const double x = tx - a.n0d;                      // recon.py:138, 418
-            const double y = ty - a.m0d;
-            const bool inA = act && x >= 0.0 && x <= a.os1 && y >= 0.0 && y <= a.of1;  // interp.py:67, 103-107
-            const int r0 = __double2int_rd(x), c0 = __double2int_rd(y);
-            const double fx = x - static_cast<double>(r0), fy = y - static_cast<double>(c0);
+            const double tx = u0[e] - dI, ty = u1[e] - dJ;    // recon.py:138, 418
+            const int ri = __double2int_rd(tx), ci = __double2int_rd(ty);
+            const double fx = tx - static_cast<double>(ri), fy = ty - static_cast<double>(ci);
+            const int r0 = ri - n0i, c0 = ci - m0i;
+            // inside: 0 <= x <= os - 1 per axis (interp.py:67, 103-107)
+            const bool fin_s = REG || (fabs(tx) < 1e9 && fabs(ty) < 1e9);
+            const bool inA = act && fin_s && r0 >= 0 && c0 >= 0 &&
+                             (r0 < os_1 || (r0 == os_1 && fx == 0.0)) &&
+                             (c0 < of_1 || (c0 == of_1 && fy == 0.0));
             const double gx = 1.0 - fx, gy = 1.0 - fy;
             const double cw[4] = {gx * gy, gx * fy, fx * gy, fx * fy};   // corners 00 01 10 11
             const double I = static_cast<double>(Ic[e]);
@@ -486,20 +488,21 @@ __global__ void __launch_bounds__(kXT, MODE == 0 ? PXST_FIX_OCC0 : PXST_FIX_OCC1
               // the next object's own position, as make_reference computes it
               // (recon.py:138: u - d - origin), so the terms equal a separate
               // object formation bit for bit
-              const double n0b = s_cb[0], m0b = s_cb[1], osb1 = s_cb[2], ofb1 = s_cb[3];
-              const double xb = tx - n0b, yb = ty - m0b;
-              const bool inB = splat_b && act && xb >= 0.0 && xb <= osb1 && yb >= 0.0 && yb <= ofb1;
-              const int r0b = __double2int_rd(xb), c0b = __double2int_rd(yb);
-              const double fxb = xb - static_cast<double>(r0b), fyb = yb - static_cast<double>(c0b);
-              const double gxb = 1.0 - fxb, gyb = 1.0 - fyb;
-              const double cwb[4] = {gxb * gyb, gxb * fyb, fxb * gyb, fxb * fyb};
+              // (same split, same weights: only the cell differs, by the
+              // origins' offset; a separate object formation computes exactly
+              // these terms, so the fused object equals it bit for bit)
+              const int r0b = r0 + dni, c0b = c0 + dmi;
+              const bool inB = splat_b && act && fin_s && r0b >= 0 && c0b >= 0 &&
+                               (r0b < osb_1 || (r0b == osb_1 && fx == 0.0)) &&
+                               (c0b < ofb_1 || (c0b == ofb_1 && fy == 0.0));
+              const double* cwb = cw;
               const double sBn = I * vsc[e] * qb_n, sBd = W2[e] * qb_d;
-              const bool hotb = REG && small_corner_ok(fxb, fyb);
-              const bool need_r1b = __any_sync(0xffffffffu, inB && hotb && fxb > 0.0);
-              const bool need_c1b = __any_sync(0xffffffffu, inB && hotb && fyb > 0.0);
+              const bool hotb = hot;
+              const bool need_r1b = __any_sync(0xffffffffu, inB && hotb && fx > 0.0);
+              const bool need_c1b = __any_sync(0xffffffffu, inB && hotb && fy > 0.0);
               if (inB && hotb) {
                 // next-grid cell (r0b, c0b) in the region's (reference-grid) frame
-                const int l = (r0b - static_cast<int>(dn) - R0) * nc + (c0b - static_cast<int>(dm) - C0);
+                const int l = (r0 - R0) * nc + (c0 - C0);
                 PXST_DCHECK(l >= 0 && l + nc + 1 < ncell);
                 const unsigned b0 = sbase + 4u * static_cast<unsigned>(l) + 2 * VB;
                 const unsigned b1 = b0 + 4u * static_cast<unsigned>(nc);
@@ -817,10 +820,6 @@ static void fix_slices(int64_t nk, int64_t n_cta, int64_t resident, int64_t* n_z
 template <int MODE>
 int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s) {
   if (const char* v = getenv("PXST_FIX_NO_REGION")) a.no_region = v[0] == '1';
-  a.n0d = static_cast<double>(a.n0);
-  a.m0d = static_cast<double>(a.m0);
-  a.os1 = static_cast<double>(a.os - 1);
-  a.of1 = static_cast<double>(a.of - 1);
   const int64_t cw = a.sc.roi[3] - a.sc.roi[2], rw = a.sc.roi[1] - a.sc.roi[0];
   dim3 g((unsigned)((cw + kXC - 1) / kXC), (unsigned)((rw + kXR - 1) / kXR));
   PXST_REQUIRE(g.y <= kMaxGridY, "ROI too tall");
