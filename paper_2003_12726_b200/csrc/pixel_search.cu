@@ -1093,7 +1093,7 @@ struct FastEntry { int ka, kb; FastKernel fn; FastKernel fn72; };
 const FastEntry kFastTable[] = {
     PIX(1, 1),  PIX(3, 3),  PIX(5, 5),  PIX(7, 7),  PIX(9, 9),  PIX72(11, 11), PIX(13, 13),
     PIX(1, 3),  PIX(1, 5),  PIX(1, 7),  PIX(1, 9),  PIX(1, 11), PIX(1, 13),  PIX(1, 15),
-    PIX(1, 17), PIX(3, 1),  PIX(5, 1),  PIX(7, 1),  PIX(9, 1),  PIX(11, 1),  PIX(13, 1),
+    PIX72(1, 17), PIX(3, 1),  PIX(5, 1),  PIX(7, 1),  PIX(9, 1),  PIX(11, 1),  PIX(13, 1),
     PIX(15, 1), PIX(17, 1),
 };
 #undef PIX
