@@ -1087,9 +1087,9 @@ __global__ void k_pix_epilogue(PixArgs a, const T* __restrict__ part, int n_chun
 using FastKernel = void (*)(const __grid_constant__ CUtensorMap, PixArgs);
 // fn72: box_c == 72, no frame weights (11 x 11 only: the specialised 13 x 13
 // spilled at 255 registers, config 3 K2 93 -> 99 ms)
-struct FastEntry { int ka, kb; FastKernel fn; FastKernel fn72; };
-#define PIX(a, b) FastEntry{a, b, k_pix_fast<a, b>, nullptr}
-#define PIX72(a, b) FastEntry{a, b, k_pix_fast<a, b>, k_pix_fast<a, b, 72>}
+struct FastEntry { int ka, kb; FastKernel fn; FastKernel fn72; FastKernel fn40; };
+#define PIX(a, b) FastEntry{a, b, k_pix_fast<a, b>, nullptr, nullptr}
+#define PIX72(a, b) FastEntry{a, b, k_pix_fast<a, b>, k_pix_fast<a, b, 72>, k_pix_fast<a, b, 40>}
 const FastEntry kFastTable[] = {
     PIX(1, 1),  PIX(3, 3),  PIX(5, 5),  PIX(7, 7),  PIX(9, 9),  PIX72(11, 11), PIX(13, 13),
     PIX(1, 3),  PIX(1, 5),  PIX(1, 7),  PIX(1, 9),  PIX(1, 11), PIX(1, 13),  PIX(1, 15),
@@ -1101,7 +1101,8 @@ const FastEntry kFastTable[] = {
 
 FastKernel find_fast(int ka, int kb, int box_c = 0) {
   for (const auto& e : kFastTable)
-    if (e.ka == ka && e.kb == kb) return (box_c == 72 && e.fn72) ? e.fn72 : e.fn;
+    if (e.ka == ka && e.kb == kb)
+      return (box_c == 72 && e.fn72) ? e.fn72 : (box_c == 40 && e.fn40) ? e.fn40 : e.fn;
   return nullptr;
 }
 
@@ -1239,8 +1240,19 @@ int pixel_map_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref* 
     } else if (int e = tile_span_max(geo.as<TileGeo>(), tiles, span, s)) {
       return e;
     }
-    a.box_r = max(a.box_r, span[0] + need_rows2(na));
-    a.box_c = max(a.box_c, span[1] + need_cols2(nb));
+    // (exactly the largest tile's need: round 2 kept the defaults as a floor
+    // and fetched 17 x 72 cells per frame where config 2's tiles need 10 x 30
+    // -- its one-row kernel was bound by the L2 -> shared-memory traffic)
+#ifndef PXST_K2_TIGHT_BOX
+#define PXST_K2_TIGHT_BOX 1
+#endif
+    if (PXST_K2_TIGHT_BOX && span[0] >= 0 && span[1] >= 0) {
+      a.box_r = span[0] + need_rows2(na);
+      a.box_c = span[1] + need_cols2(nb);
+    } else {
+      a.box_r = max(a.box_r, span[0] + need_rows2(na));
+      a.box_c = max(a.box_c, span[1] + need_cols2(nb));
+    }
     a.box_c = (a.box_c + 23) / 32 * 32 + 8;            // pitch = 8 (mod 32)
     if (a.box_c > 256) a.box_c = 232;
     while (a.box_r > 16 && a.box_r * a.box_c * 4 > 24 * 1024) --a.box_r;
