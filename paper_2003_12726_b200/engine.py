@@ -26,6 +26,7 @@ inside the half-open ROI (numpy-slice clipped to the detector).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 import weakref
 import zlib
@@ -96,6 +97,25 @@ def clip_roi(roi, shape) -> tuple[int, int, int, int]:
         return 0, ss, 0, fs
     r0, r1, c0, c1 = (int(v) for v in (roi.ss_min, roi.ss_max, roi.fs_min, roi.fs_max))
     return min(r0, ss), min(r1, ss), min(c0, fs), min(c1, fs)
+
+
+def _nvtx(name: str):
+    """NVTX range around a kernel-launching method when ``PXST_NVTX=1`` (for
+    nsys / ncu --nvtx timelines); a no-op otherwise."""
+    def wrap(fn):
+        if os.environ.get("PXST_NVTX") != "1":
+            return fn
+
+        def inner(*a, **k):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **k)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        inner.__name__ = fn.__name__
+        inner.__doc__ = fn.__doc__
+        return inner
+    return wrap
 
 
 @dataclass
@@ -373,6 +393,7 @@ class DeviceScan:
                                          q.data_ptr(), stream_ptr()))
         return q
 
+    @_nvtx("pxst K0 stack statistics")
     def ready(self, frame_stats: bool = False) -> "DeviceScan":
         """Make the current stream wait for the whole stack and run the K0
         parts not yet run: the per-pixel part always (K2, K4), the per-frame
@@ -508,6 +529,7 @@ class DeviceScan:
         TRANSFER["d2h"] += 8 * 8 + 4 * 4
         return GeometryFuture(host8, host2, done, grid, grid_ready)
 
+    @_nvtx("pxst K1 object splat")
     def object_splat(self, u_t, di_t, dj_t, n0, m0, shape, frame_lo=0, frame_hi=None,
                      acc: "Accum | None" = None) -> Accum:
         """Fixed-point object accumulators (Accum, os*of cells) for a range of
@@ -566,6 +588,7 @@ class DeviceScan:
                                         ctypes.byref(st), stream_ptr()))
         return var_fw
 
+    @_nvtx("pxst K2 pixel-map search")
     def pixel_map_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                          subpixel_grid=None, refine=True, fw_t=None,
                          geom: "GeometryFuture | None" = None):
@@ -605,6 +628,7 @@ class DeviceScan:
         return u_out, err.view(self.ss, self.fs)
 
     # ------------------------------------------------------- K3 translations
+    @_nvtx("pxst K3 translation search")
     def translation_search(self, ref: DeviceRef, u_t, di_t, dj_t, half_ss, half_fs,
                            subpixel_grid=None, frame_lo=0, frame_hi=None, err_out=None,
                            span_hint=None):
@@ -666,6 +690,7 @@ class DeviceScan:
         return plane.view(*shape)
 
     # ---------------------------------------------------------- K4 error maps
+    @_nvtx("pxst K4 error maps")
     def error_maps(self, ref: DeviceRef, u_t, di_t, dj_t):
         self.ready()
         # pxst_error_maps zeroes per_frame / per_pixel / total and writes every
@@ -685,6 +710,7 @@ class DeviceScan:
         return (total, per_frame, per_pixel.view(self.ss, self.fs), plane.view(*ref.shape),
                 self.sigma2.view(self.ss, self.fs))
 
+    @_nvtx("pxst K4 error maps + next K1")
     def error_maps_and_next_object(self, ref: DeviceRef, u_t, di_t, dj_t,
                                    geom: "GeometryFuture", margin: int = 32):
         """K4 of (ref, u, t) fused with the next iteration's object formation
@@ -740,6 +766,7 @@ class DeviceScan:
                                                  stream_ptr()))
         return info
 
+    @_nvtx("pxst pixel-map regularisation")
     def regularise(self, u_t, opts):
         """The optional stages of recon.update_pixel_map, in its order."""
         if getattr(opts, "sigma", 0.0) > 0:
