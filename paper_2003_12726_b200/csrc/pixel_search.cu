@@ -523,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
     Sample s_n{};
     if (kAhead) s_n = sample_of(0, I_n, fw_n);
     int issued = min(kNB, nk);     // thread 0: frames [0, issued) are in flight or done
+    const unsigned full_a = smem_addr(full), empty_a = smem_addr(empty);   // see mbar_wait_a
     for (int jj = 0; jj < nk; ++jj) {
       if (!kAhead) s_n = sample_of(jj, I_n, fw_n);
       const Sample sm = s_n;
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
           ++issued;
         }
       }
-      mbar_wait(&full[b], ph);
+      mbar_wait_a(full_a + 8u * b, ph);
       const bool fast = sm.fast();
       any_slow |= live && !fast;
       const float fx = fast ? static_cast<float>(sm.fx) : 0.f;
@@ -570,14 +571,15 @@ __global__ void __launch_bounds__(kThreads, kCtaPerSm)
       else
         engine_fast2<KA, KB>(ring + b * box + off, ldw, fx, fy, sW * (1.f - fx), sW * fx, sI,
                              acc);
-      mbar_arrive(&empty[b]);
+      mbar_arrive_a(empty_a + 8u * b);
       if (PXST_K2_PRODUCER == 2 && (threadIdx.x & 31) == 0 && jj + kNB < nk) {
         // Refill at release time: the warp whose arrival completes the slot's
         // phase (or any warp that sees it complete) claims the slot's next
         // frame and issues its load -- no waiting for thread 0 to come round
         // (ncu had 17 % of the 11 x 11 kernel's stall samples on the ring
         // wait; config 1 K2 0.564 -> 0.548 ms, config 2 6.09 -> 5.70 ms).
-        if (mbar_test(&empty[b], ph) && atomicCAS(&s_iss[b], jj, jj + kNB) == jj) issue(jj + kNB);
+        if (mbar_test_a(empty_a + 8u * b, ph) && atomicCAS(&s_iss[b], jj, jj + kNB) == jj)
+          issue(jj + kNB);
       }
       if (PXST_K2_PRODUCER == 0 && threadIdx.x == 0 && jj + kNB < nk) {
         mbar_wait(&empty[b], ph);      // every thread is done with this slot
