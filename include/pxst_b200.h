@@ -167,6 +167,23 @@ int pxst_object_splat(const pxst_scan* scan, const double* u, const double* di,
 int pxst_object_finish(const pxst_accum* acc, int64_t n, double* i_ref, double* wsum, float* fm,
                        uint8_t* valid, void* stream);
 
+/* Single-process multi-GPU: the frame shards' all-reduce fused with
+ * pxst_object_finish (replaces the NCCL all-reduce of recon.py:133-141's
+ * numerator / denominator in the one-process driver).  accs[0..n_peers) are
+ * the accumulators of ALL peers (device pointers on n_peers <= 16 devices with
+ * peer access enabled; the same full-scan quanta on every peer).  The call
+ * runs on the stream's device and handles its slice of cells
+ * [cell_lo, cell_hi): it reads every peer's int64 terms where they lie (P2P
+ * loads), adds them (exact: the same bits on every device, in any order),
+ * normalises, and stores the slice's results into EVERY peer's output images
+ * i_ref[j] / wsum[j] / fm[j] / valid[j] (host arrays of n_peers device
+ * pointers, any array or entry nullable; P2P stores).  Once every device has
+ * run its slice and the devices have been synchronised, each holds the whole
+ * object.  Also finishes reference planes (K4 row shards). */
+int pxst_object_finish_peers(const pxst_accum* accs, int n_peers, int64_t cell_lo,
+                             int64_t cell_hi, double* const* i_ref, double* const* wsum,
+                             float* const* fm, uint8_t* const* valid, void* stream);
+
 /* Convenience: absmax + quanta + splat + finish over all good frames for a
  * known grid (recon.make_reference after the bbox of pxst_bbox). */
 int pxst_object_map(const pxst_scan* scan, const double* u, const double* di, const double* dj,

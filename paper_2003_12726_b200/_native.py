@@ -68,6 +68,8 @@ _SIGS = {
     "pxst_object_splat": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,
                                   c_int64, c_int64, c_int64, c_int64, c_int64,
                                   POINTER(PxstAccum), c_void_p, c_void_p]),
+    "pxst_object_finish_peers": (c_int, [POINTER(PxstAccum), c_int, c_int64, c_int64, c_void_p,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
     "pxst_object_finish": (c_int, [POINTER(PxstAccum), c_int64, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p]),
     "pxst_object_map": (c_int, [POINTER(PxstScan), c_void_p, c_void_p, c_void_p, c_int64,

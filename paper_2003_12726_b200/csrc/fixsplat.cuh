@@ -114,6 +114,8 @@ __device__ __forceinline__ void fix_finish_cell(const FixAcc& acc, int64_t i, do
   if (valid) valid[i] = ok ? 1 : 0;
 }
 
+constexpr int kMaxPeers = 16;   // GPUs of one process (pxst_object_finish_peers)
+
 // One launch for the scale statistics and the quanta (and, in the same
 // grid-stride loops, K4's grouped reference and a zero fill): see
 // k_quanta_pass.  ticket must be zero when the kernel starts.

@@ -17,6 +17,9 @@ template <int MODE> int launch_fix_pass(FixArgs& a, int* n_z_out, cudaStream_t s
 int launch_abs_max(const pxst_scan* sc, double* out, cudaStream_t s);
 int launch_quanta(const pxst_scan* sc, const double* absmax, const double* sigma2,
                   const pxst_ref* ref, int kind, double* quanta, cudaStream_t s);
+int launch_fix_finish_peers(const FixAcc* accs, int w, int64_t lo, int64_t hi, double* const* out,
+                            double* const* wsum, float* const* fm, uint8_t* const* valid,
+                            cudaStream_t s);
 int launch_fix_finish(const FixAcc& acc, const int64_t* grid, int64_t n, double* out, double* wsum,
                       float* fm, uint8_t* valid, cudaStream_t s);
 int launch_object_fix(const pxst_scan* sc, const double* u, const double* di, const double* dj,
@@ -140,6 +143,21 @@ extern "C" int pxst_object_finish(const pxst_accum* acc, int64_t n, double* i_re
   if (int e = check_accum(acc)) return e;
   PXST_REQUIRE(n > 0, "bad accumulator size");
   return launch_fix_finish(fix_acc(acc), nullptr, n, i_ref, wsum, fm, valid, as_stream(stream));
+}
+
+extern "C" int pxst_object_finish_peers(const pxst_accum* accs, int n_peers, int64_t cell_lo,
+                                        int64_t cell_hi, double* const* i_ref,
+                                        double* const* wsum, float* const* fm,
+                                        uint8_t* const* valid, void* stream) {
+  PXST_REQUIRE(accs && n_peers >= 1 && n_peers <= kMaxPeers, "peer count out of range");
+  PXST_REQUIRE(cell_lo >= 0 && cell_hi >= cell_lo, "bad cell range");
+  FixAcc fa[kMaxPeers];
+  for (int j = 0; j < n_peers; ++j) {
+    if (int e = check_accum(accs + j)) return e;
+    fa[j] = fix_acc(accs + j);
+  }
+  return launch_fix_finish_peers(fa, n_peers, cell_lo, cell_hi, i_ref, wsum, fm, valid,
+                                 as_stream(stream));
 }
 
 extern "C" int pxst_object_map(const pxst_scan* sc, const double* u,

@@ -10,15 +10,20 @@ translations; the work splits as in ``sharding.py``:
 phase                  partition           exchange (peer copies over NVLink /
                                            NVSwitch + library add kernels)
 =====================  ==================  ===================================
-K1 object formation    good-frame blocks   int64 fixed-point num/den: every
-                                           device adds its peers' images
-                                           (exact: the object is bit-identical
-                                           for any device count), touched: OR
+K1 object formation    good-frame blocks   int64 fixed-point num/den, touched:
+                                           ONE kernel per device reads every
+                                           peer's terms in place (P2P loads),
+                                           adds them (exact: the object is
+                                           bit-identical for any device
+                                           count), normalises its slice of the
+                                           cells and stores it into every
+                                           peer's images (P2P stores):
+                                           ``pxst_object_finish_peers``
 K2 pixel-map search    detector-row bands  u rows gathered on every device
 K3 translation search  good-frame blocks   (di, dj) of each block gathered
 K4 error maps          detector-row bands  per-frame sums added in device
                                            order; per-pixel rows gathered;
-                                           plane int64 images added (exact)
+                                           plane: the same fused peer finish
 =====================  ==================  ===================================
 
 A device id may repeat (``Devices([0, 0])``): two shares of the work on one
@@ -29,6 +34,9 @@ both devices' current streams); the sums are the library's
 """
 
 from __future__ import annotations
+
+import ctypes
+import os
 
 import numpy as np
 import torch
@@ -86,6 +94,21 @@ class MultiScan:
         self.good = [torch.as_tensor(d0.good_idx.astype(np.int64), device=ds.device)
                      for ds in self.scans]
         self.lib = _native.lib()
+        # the accumulators' all-reduce fused with their normalisation over peer
+        # memory (PXST_MULTI_FUSED=0: peer copies + add kernels + per-device finish)
+        self.fused_finish = os.environ.get("PXST_MULTI_FUSED", "1") != "0" and \
+            len(devices) <= 16
+        self._enable_peer_access()
+
+    def _enable_peer_access(self):
+        """Kernels of device a dereference pointers of device b: make torch
+        enable peer access for every ordered pair of distinct devices (it does
+        so on the first cross-device copy)."""
+        ids = sorted(set(self.devices.ids))
+        for a in ids:
+            for b in ids:
+                if a != b:
+                    torch.empty(1, device=f"cuda:{a}").copy_(torch.empty(1, device=f"cuda:{b}"))
 
     # ------------------------------------------------------------ plumbing
     def on(self, k):
@@ -112,6 +135,65 @@ class MultiScan:
                 for c in copies[k]:
                     check(self.lib.pxst_add_i64(ts[k].data_ptr(), c.data_ptr(), ts[k].numel(),
                                                 stream_ptr()))
+
+    def _finish_peers(self, accs, shape, origin=None):
+        """The all-reduce of the shards' fixed-point accumulators fused with the
+        normalisation (``pxst_object_finish_peers``): device k reads every
+        peer's int64 terms in place (P2P loads), adds them exactly, normalises
+        its 1/W slice of the cells and stores the results into every peer's
+        output images (P2P stores).  origin given: DeviceRefs (object map);
+        None: reference planes (float64).  Same bits as adding the peers'
+        accumulators and finishing on each device."""
+        W = len(accs)
+        os_, of = shape
+        n = os_ * of
+        outs = []
+        for k, ds in enumerate(self.scans):
+            with self.on(k):
+                i_ref = torch.empty(n, dtype=torch.float64, device=ds.device)
+                if origin is None:
+                    outs.append((i_ref, None, None, None))
+                else:
+                    outs.append((i_ref, torch.empty(n, dtype=torch.float64, device=ds.device),
+                                 torch.empty(n, dtype=torch.float32, device=ds.device),
+                                 torch.empty(n, dtype=torch.uint8, device=ds.device)))
+        ready = []
+        for k in range(W):                 # the peers' splats, in each device's stream order
+            with self.on(k):
+                ev = torch.cuda.Event()
+                ev.record()
+                ready.append(ev)
+        c_accs = (_native.PxstAccum * W)(*[a.c() for a in accs])
+
+        def ptrs(idx):
+            if outs[0][idx] is None:
+                return None
+            return (ctypes.c_void_p * W)(*[o[idx].data_ptr() for o in outs])
+        arrs = [ptrs(i) for i in range(4)]
+        bounds = [n * k // W for k in range(W + 1)]
+        done = []
+        for k in range(W):
+            with self.on(k):
+                st = torch.cuda.current_stream()
+                for j in range(W):
+                    if j != k:
+                        st.wait_event(ready[j])
+                check(self.lib.pxst_object_finish_peers(c_accs, W, bounds[k], bounds[k + 1],
+                                                        *arrs, stream_ptr()))
+                ev = torch.cuda.Event()
+                ev.record()
+                done.append(ev)
+        for k in range(W):                 # a device's images are complete once every peer's
+            with self.on(k):               # slice has landed
+                st = torch.cuda.current_stream()
+                for j in range(W):
+                    if j != k:
+                        st.wait_event(done[j])
+        if origin is None:
+            return [o[0].view(os_, of) for o in outs]
+        from .engine import DeviceRef
+        return [DeviceRef(o[0].view(os_, of), o[1].view(os_, of), o[2].view(os_, of),
+                          o[3].view(os_, of), (int(origin[0]), int(origin[1]))) for o in outs]
 
     def _or_peers_u8(self, ts):
         W = len(ts)
@@ -165,6 +247,8 @@ class MultiScan:
             lo, hi = self.frames[k]
             with self.on(k):
                 accs.append(ds.object_splat(us[k], dis[k], djs[k], n0, m0, shape, lo, hi))
+        if self.fused_finish:
+            return self._finish_peers(accs, shape, (n0, m0))
         self._add_peers_i64([a.data for a in accs])
         self._or_peers_u8([a.touched for a in accs])
         refs = []
@@ -220,11 +304,15 @@ class MultiScan:
         per_frame = self._sum_f64_ordered([p[0] for p in parts])
         per_pixel = self._gather_rows([p[1].reshape(1, *p[1].shape) for p in parts])
         accs = [p[2] for p in parts]
-        self._add_peers_i64([a.data for a in accs])
+        planes = None
+        if self.fused_finish:
+            planes = self._finish_peers(accs, refs[0].shape)
+        else:
+            self._add_peers_i64([a.data for a in accs])
         out = []
         for k, ds in enumerate(self.scans):
             with self.on(k):
-                plane = ds.plane_finish(accs[k], refs[k].shape)
+                plane = planes[k] if planes is not None else ds.plane_finish(accs[k], refs[k].shape)
                 good = self.good[k]
                 total = per_frame[k][good].sum().reshape(1) if len(good) else \
                     per_frame[k].new_zeros(1)

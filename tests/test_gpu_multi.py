@@ -1,7 +1,7 @@
 """Single-process multi-GPU loop (multigpu.py) on this
 one-GPU pool: ``Devices([0, 0])`` / ``[0, 0, 0]`` split the work into two /
-three shares on cuda:0 through the same code path 8 GPUs take (peer copies,
-library add kernels).  The object map and reference plane are exact integer
+three shares on cuda:0 through the same code path 8 GPUs take (peer-memory
+finish kernel, or peer copies and library add kernels).  The object map and reference plane are exact integer
 sums, so they equal the one-device results bit for bit for the same inputs;
 the loop's u and translations agree at the north-star bars."""
 
@@ -19,10 +19,16 @@ from paper_2003_12726_b200 import engine  # noqa: E402
 from paper_2003_12726_b200.multigpu import Devices, MultiScan  # noqa: E402
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("ids", [[0, 0], [0, 0, 0]])
-def test_multiscan_phases_match_one_device(scan1, ids):
+def test_multiscan_phases_match_one_device(scan1, ids, fused):
+    """fused: the accumulators' all-reduce fused with the normalisation over
+    peer memory (pxst_object_finish_peers: each share reads every peer's int64
+    terms in place and stores its slice into every peer's images); otherwise
+    peer copies + add kernels + a finish per device.  Both equal one device."""
     s = scan1
     ms = MultiScan(s.scan, s.w, s.m, None, Devices(ids))
+    ms.fused_finish = fused
     us, dis, djs = ms.upload(s.u0.u, s.t0.di, s.t0.dj)
     refs = ms.object_map(us, dis, djs)
     ds = engine.DeviceScan(s.scan.frames, s.scan.good_frames, s.w.w, s.m.mask)
