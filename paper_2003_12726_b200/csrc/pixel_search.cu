@@ -913,6 +913,8 @@ __global__ void __launch_bounds__(256, NJ <= 4 ? PXST_K2_SLOW_OCC : 2) k_pix_slo
           const int ofp = of + 2 * a.pad;
           const unsigned w0 = static_cast<unsigned>((pr0 + a.pad) * ofp + (pc0 + a.pad));
           const unsigned w1 = w0 + (es.fxp ? ofp : 0);
+          PXST_DCHECK(w1 + tp[NJ - 1] + 1 <
+                      static_cast<unsigned>((os + 2 * a.pad) * ofp));   // inside the padded image
           // (no trial-count guard: lanes past the window repeat its last
           // trial, their sums are never read; the NJ trials' loads overlap)
           float v[NJ];
