@@ -69,7 +69,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no extras)")
-    ap.add_argument("--extras", default="2,3",
+    ap.add_argument("--extras", default="2,3,4",
                     help="larger configs also measured in the same run (comma list, '' = none)")
     return ap.parse_args()
 
