@@ -57,6 +57,8 @@ struct TransArgs {
   const float* fmn;          // NaN-encoded reference (slow fix-up)
   int64_t os, of, n0, m0;
   const TileGeo* geo;        // [n_bands][n_ct]
+  const int4* rec16;         // per-pixel records in the fast kernel's (tile, e, thread) order:
+  const float2* rec8;        //   (floor u0, floor u1, frac u0, frac u1), (W or 0, pixel offset)
   int n_ct;                  // column tiles per band
   int64_t n_bands;
   int64_t n_tiles;           // n_bands * n_ct
@@ -153,6 +155,136 @@ __device__ __forceinline__ Sample3 make_sample3(const TransArgs& a, const TileGe
   return s;
 }
 
+// Per-pixel records (k_k3_records, once per call): what the fast kernel needs
+// of a pixel, in the order its threads read it -- record (it, e, tid) for tile
+// it, pixel slot e of thread tid (tile_pixel).
+// rec16 = (floor u0, floor u1, bits of frac u0, bits of frac u1) with u split
+// in float64 once (floor exact, fraction rounded to float32); rec8 = (W for a
+// work pixel else 0, bits of the pixel's 32-bit offset in a frame).  A frame's
+// CTA then needs one 16-byte and one 8-byte load per pixel plus the stack
+// value, and no 64-bit row / column arithmetic (ncu: half of the 7 x 7
+// kernel's instructions were per-sample loads, address arithmetic and float64
+// geometry).  i0 = kNoPixel marks pixels off the ROI / work set / not finite.
+constexpr int kNoPixel = 1 << 30;
+__device__ __forceinline__ int64_t rec_index(int64_t it, int e, int tid) {
+  return (it * 4 + e) * kThreads + tid;
+}
+// Pixel slot e of thread tid -> (row, column) inside the 16 x 64 tile, and back.
+// 0 (default): a warp = 32 pixels of one row (rows 2w + (e >> 1), columns
+// lane + 32 (e & 1)).  PXST_K3_BLOCKS = 1: a warp's lanes form a 4 x 8 pixel
+// block per slot (rows 4e .. 4e+3, columns 8w .. 8w+7, row pitch = 8 mod 32)
+// as in K2.  ncu puts 33 % of the row mapping's shared-memory wavefronts on
+// bank conflicts, yet the block mapping measured slower (config 3: 34.1 vs
+// 31.9 ms, config 4: 289 vs 285 ms): its stack reads are four 32-byte pieces
+// per warp instead of one 128-byte line.
+#ifndef PXST_K3_BLOCKS
+#define PXST_K3_BLOCKS 0
+#endif
+__device__ __forceinline__ void tile_pixel(int e, int tid, int& tr, int& tc) {
+  const int lane = tid & 31, warp = tid >> 5;
+  if (PXST_K3_BLOCKS) {
+    tr = 4 * e + (lane >> 3);
+    tc = 8 * warp + (lane & 7);
+  } else {
+    tr = 2 * warp + (e >> 1);
+    tc = lane + 32 * (e & 1);
+  }
+}
+__device__ __forceinline__ int64_t rec_index_of(int64_t it, int tr, int tc) {
+  if (PXST_K3_BLOCKS) return rec_index(it, tr >> 2, (tc >> 3) * 32 + ((tr & 3) << 3) + (tc & 7));
+  return rec_index(it, (tr & 1) * 2 + (tc >> 5), (tr >> 1) * 32 + (tc & 31));
+}
+__global__ void __launch_bounds__(kThreads) k_k3_records(pxst_scan sc, const double* __restrict__ u,
+                                                        int n_ct, int4* __restrict__ rec16,
+                                                        float2* __restrict__ rec8) {
+  const int64_t it = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const int64_t plane = sc.ss * sc.fs;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int tr, tc;
+    tile_pixel(e, threadIdx.x, tr, tc);
+    const int64_t row = sc.roi[0] + (int64_t)blockIdx.y * kTR + tr;
+    const int64_t col = sc.roi[2] + (int64_t)blockIdx.x * kTC + tc;
+    const bool in = row < sc.roi[1] && col < sc.roi[3];
+    const int64_t p = in ? row * sc.fs + col : 0;
+    bool live = in && sc.work[p] != 0 && plane < (int64_t(1) << 31);
+    int4 r = make_int4(kNoPixel, 0, 0, 0);
+    if (live) {
+      const double u0 = u[p], u1 = u[plane + p];
+      live = fabs(u0) < 1e9 && fabs(u1) < 1e9;
+      if (live) {
+        const double a = floor(u0), b = floor(u1);
+        r = make_int4(static_cast<int>(a), static_cast<int>(b),
+                      __float_as_int(static_cast<float>(u0 - a)),
+                      __float_as_int(static_cast<float>(u1 - b)));
+      }
+    }
+    const int64_t k = rec_index(it, e, threadIdx.x);
+    rec16[k] = r;
+    rec8[k] = make_float2(live ? sc.w32[p] : 0.f, __int_as_float(static_cast<int>(p)));
+  }
+}
+
+// Frame constants of the split geometry: d + origin + phase = id + fd per axis.
+struct FrameSplit {
+  int id0, id1;
+  float fd0, fd1;
+  bool ok;
+};
+__device__ __forceinline__ FrameSplit frame_split(const TransArgs& a, double dI, double dJ) {
+  const double x = (dI + static_cast<double>(a.n0)) + a.ph_a;
+  const double y = (dJ + static_cast<double>(a.m0)) + a.ph_b;
+  FrameSplit f;
+  f.ok = fabs(x) < 1e9 && fabs(y) < 1e9;
+  const double xa = f.ok ? floor(x) : 0.0, ya = f.ok ? floor(y) : 0.0;
+  f.id0 = static_cast<int>(xa);
+  f.id1 = static_cast<int>(ya);
+  f.fd0 = f.ok ? static_cast<float>(x - xa) : 0.f;
+  f.fd1 = f.ok ? static_cast<float>(y - ya) : 0.f;
+  return f;
+}
+
+// Sample geometry from a pixel record and the frame split: x = (iu - id) +
+// (fu - fd), one float32 subtract and a carry per axis.  The base may differ
+// from make_sample3's float64 floor by one where x is within ~1e-7 of an
+// integer; the trial positions, and so the bilinear values (continuous there:
+// a fast sample's patch is valid and on the grid), are the same to float32
+// rounding.  Both the fast kernel and the fix-up's classification use this
+// function; the fix-up's exact trials keep make_sample3's float64 split.
+struct Sample3f {
+  int i, j;
+  float fx, fy;
+  int lr, lc;
+  bool pre;
+  uint8_t pvb;
+  __device__ __forceinline__ bool fast() const { return pre && pvb != 0; }
+};
+__device__ __forceinline__ Sample3f make_sample3_split(const TransArgs& a, int4 r,
+                                                       const FrameSplit& f, bool fits, int wr0,
+                                                       int wc0) {
+  Sample3f s;
+  float dx = __int_as_float(r.z) - f.fd0, dy = __int_as_float(r.w) - f.fd1;
+  int i = r.x - f.id0, j = r.y - f.id1;
+  if (dx < 0.f) { dx += 1.f; --i; }
+  if (dy < 0.f) { dy += 1.f; --j; }
+  if (dx >= 1.f) { dx = 0.f; ++i; }
+  if (dy >= 1.f) { dy = 0.f; ++j; }
+  s.fx = dx;
+  s.fy = dy;
+  const bool on = r.x != kNoPixel && f.ok;
+  s.i = on ? i : -(1 << 30);
+  s.j = on ? j : -(1 << 30);
+  s.lr = s.i - a.mhi_a - wr0;
+  s.lc = s.j - a.mhi_b - wc0;
+  const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
+  const bool in = static_cast<unsigned>(s.i) < static_cast<unsigned>(os) &&
+                  static_cast<unsigned>(s.j) < static_cast<unsigned>(of);
+  s.pvb = fits ? __ldg(a.pv + (in ? s.i * of + s.j : 0)) : 0;
+  s.pre = fits && in && static_cast<unsigned>(s.lr) <= static_cast<unsigned>(a.box_r - a.ka - 1) &&
+          static_cast<unsigned>(s.lc) <= static_cast<unsigned>(a.box_c - a.kb - 1);
+  return s;
+}
+
 // full-grid trial index of phase-local engine trial (t, s)
 __device__ __forceinline__ int full_index(const TransArgs& a, int t, int s) {
   const int ia = a.q_a * (a.mhi_a - t) + a.rho_a + a.kh_a;
@@ -222,34 +354,28 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
   if (threadIdx.x == 0)
     for (int64_t it = 0; it < (a.n_tiles < kNB ? a.n_tiles : kNB); ++it) issue(it);
 
-  // One-tile-ahead pipeline of the per-pixel inputs (work flag, stack value,
-  // W, u): their global loads for tile it+1 are in flight while tile it runs.
+  // Per-pixel inputs from the records (k_k3_records) and the stack; windows of
+  // 9 x 9 and more (1 CTA per SM, registers to spare) fetch tile it + 1's while
+  // tile it runs.
   struct Raw3 {
-    float I[4], W[4];
-    double u0[4], u1[4];
-    bool live[4];
+    int4 r16[4];
+    float W[4], I[4];
   };
   auto load_raw = [&](int64_t it, Raw3& R) {
-    const int64_t band = it / a.n_ct;
-    const int ct = static_cast<int>(it % a.n_ct);
+    const int4* r16 = a.rec16 + rec_index(it, 0, threadIdx.x);
+    const float2* r8 = a.rec8 + rec_index(it, 0, threadIdx.x);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {   // this thread's 4 pixels: rows 2w, 2w+1; cols lane, lane+32
-      const int64_t row = a.sc.roi[0] + band * kTR + 2 * warp + (e >> 1);
-      const int64_t col = a.sc.roi[2] + (int64_t)ct * kTC + lane + 32 * (e & 1);
-      const bool in = row < a.sc.roi[1] && col < a.sc.roi[3];
-      const int64_t p = in ? row * a.sc.fs + col : 0;
-      R.live[e] = in && a.sc.work[p] != 0;
-      R.I[e] = __ldg(frame + p);
-      R.W[e] = a.sc.w32[p];
-      R.u0[e] = a.u[p];
-      R.u1[e] = a.u[plane + p];
+    for (int e = 0; e < 4; ++e) {
+      R.r16[e] = __ldg(r16 + e * kThreads);
+      const float2 w = __ldg(r8 + e * kThreads);
+      R.W[e] = w.x;
+      R.I[e] = __ldg(frame + static_cast<unsigned>(__float_as_int(w.y)));
     }
   };
-  // (The 2-CTA kernels, capped at 128 registers, have no room for the second
-  // set and load in place.)
   constexpr bool kPipe = !(KA * KB < PXST_K3_OCC2_BELOW);
   Raw3 nxt;
   if (kPipe) load_raw(0, nxt);
+  const FrameSplit fs_ = frame_split(a, dI, dJ);
 
   for (int64_t it = 0; it < a.n_tiles; ++it) {
     const int b = static_cast<int>(it % kNB);
@@ -262,24 +388,28 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
     } else {
       load_raw(it, cur);
     }
+    // the tile's window origin for this frame (as issue() computed it)
+    const bool fits = tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c);
+    const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
+    const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
     float I[4], W[4], fx[4], fy[4];
     int off[4];                        // patch origin offset in the slot, -1 = not fast
     bool tile_slow = false;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const bool live = cur.live[e];
-      I[e] = live ? cur.I[e] : 0.f;
-      W[e] = live ? cur.W[e] : 0.f;
-      const Sample3 sm = make_sample3(a, g, live ? cur.u0[e] : 0.0, live ? cur.u1[e] : 0.0, dI, dJ);
-      fx[e] = static_cast<float>(sm.fx);
-      fy[e] = static_cast<float>(sm.fy);
-      off[e] = (live && sm.fast) ? sm.lr * a.box_c + sm.lc : -1;
-      tile_slow |= live && !sm.fast;
+      const bool live = cur.r16[e].x != kNoPixel;
+      I[e] = cur.I[e];
+      W[e] = cur.W[e];                 // 0 off the work set
+      const Sample3f sm = make_sample3_split(a, cur.r16[e], fs_, fits, wr0, wc0);
+      fx[e] = sm.fx;
+      fy[e] = sm.fy;
+      off[e] = (live && sm.fast()) ? sm.lr * a.box_c + sm.lc : -1;
+      tile_slow |= live && !sm.fast();
       if (a.dbg && live) {   // [samples, !fits, !in-grid, !pv, !box]
         atomicAdd(a.dbg, 1ull);
-        if (!sm.fast) {
+        if (!sm.fast()) {
           const bool ing = sm.i >= 0 && sm.i < a.os && sm.j >= 0 && sm.j < a.of;
-          if (!tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c))
+          if (!fits)
             atomicAdd(a.dbg + 1, 1ull);
           else if (!ing) atomicAdd(a.dbg + 2, 1ull);
           else if (!a.pv[(int64_t)sm.i * a.of + sm.j]) atomicAdd(a.dbg + 3, 1ull);
@@ -358,6 +488,8 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
     const double dI = a.di[f], dJ = a.dj[f];
     const float* frame = a.sc.frames + f * plane;
     const unsigned long long* bits = a.tilebits + kk * a.tile_words;
+    const FrameSplit fs_ = frame_split(a, dI, dJ);
+    const double n0d = static_cast<double>(a.n0), m0d = static_cast<double>(a.m0);
     float part[kSlowPerLane];
 #pragma unroll
     for (int j = 0; j < kSlowPerLane; ++j) part[j] = 0.f;
@@ -368,6 +500,9 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
       const int64_t band = it / a.n_ct;
       const int ct = static_cast<int>(it % a.n_ct);
       const TileGeo g = a.geo[it];
+      const bool fits = tile_fits(g, need_rows3(a.ka), need_cols3(a.kb), a.box_r, a.box_c);
+      const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
+      const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
       const int64_t r_lo = a.sc.roi[0] + band * kTR;
       const int64_t r_hi = min(a.sc.roi[1], r_lo + kTR);
       const int64_t c_lo = (int64_t)ct * kTC;
@@ -384,9 +519,13 @@ __global__ void __launch_bounds__(32 * kSlowWarps) k_trans_slow(TransArgs a) {
           const int64_t rr = ql / (c_hi - c_lo), cc = c_lo + ql % (c_hi - c_lo);
           const int64_t p = (r_lo + rr) * a.sc.fs + a.sc.roi[2] + cc;
           if (a.sc.work[p]) {
-            sl = make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ);
-            slow = !sl.fast;
+            // skipped <=> the fast kernel's own test (the split geometry on the
+            // pixel's record); the exact trials use the float64 split
+            const int tr = static_cast<int>(rr), tc = static_cast<int>(cc - c_lo);
+            const int4 r16 = a.rec16[rec_index_of(it, tr, tc)];
+            slow = !make_sample3_split(a, r16, fs_, fits, wr0, wc0).fast();
             if (slow) {
+              sl = make_sample3(a, g, a.u[p], a.u[plane + p], dI, dJ);
               Il = __ldg(frame + p);
               Wl = a.sc.w32[p];
             }
@@ -693,6 +832,14 @@ int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
         *sc, u, geo.as<TileGeo>());
     PXST_CHECK_LAUNCH();
+    Scratch rec16, rec8;             // per-pixel records of the fast kernel (k_k3_records)
+    if (int e = rec16.alloc(sizeof(int4) * a.n_tiles * 4 * kThreads, s)) return e;
+    if (int e = rec8.alloc(sizeof(float2) * a.n_tiles * 4 * kThreads, s)) return e;
+    k_k3_records<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
+        *sc, u, a.n_ct, rec16.as<int4>(), rec8.as<float2>());
+    PXST_CHECK_LAUNCH();
+    a.rec16 = rec16.as<int4>();
+    a.rec8 = rec8.as<float2>();
     // Box from the largest tile footprint, <= 256 columns and <= 40 KB per
     // slot; tiles beyond the cap take the exact path.
     int span[2];
@@ -705,6 +852,10 @@ int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref
     a.box_r = max(a.box_r, span[0] + need_rows3(max_ka));
     a.box_c = max(a.box_c, span[1] + need_cols3(max_kb));
     a.box_c = (a.box_c + 3) / 4 * 4;
+    if (PXST_K3_BLOCKS) {        // row pitch = 8 (mod 32): a warp's 4 block rows tile the banks
+      const int c8 = (a.box_c + 23) / 32 * 32 + 8;
+      if (c8 <= 256) a.box_c = c8;     // (a TMA box dimension is at most 256)
+    }
     if (a.box_c > 256) a.box_c = 256;
     while (a.box_r > 16 && a.box_r * a.box_c * 4 > 40 * 1024) --a.box_r;
     // union patch box over phases, relative to floor(x_rho): rows

@@ -6,7 +6,7 @@ run() {
 import json,sys
 d=json.loads(sys.stdin.readline())
 x=d.get('extra_configs',{})
-print('%-14s ms/step %.4f  k2 %.4f frac %.4f  steps %s k2 %s' % ('$tag', d['ms_per_step'], d['roofline']['k2_ms'], d['roofline']['frac'], d['workload_detail']['step_ms'][:3], d['workload_detail']['k2_step_ms'][:3]), {k:(round(v['ms_per_iteration'],2), round(v['k2_ms'],3), round(v.get('k3_ms',0),2)) for k,v in x.items()})
+print('%-14s ms/step %.4f  k2 %.4f frac %.4f  steps %s k2 %s' % ('$tag', d['ms_per_step'], d['roofline']['k2_ms'], d['roofline']['frac'], d['workload_detail']['step_ms'][:3], d['workload_detail']['k2_step_ms'][:3]), {k:(round(v['ms_per_iteration'],2), round(v.get('k2_ms',0),3), round(v.get('k3_ms',0),2)) for k,v in x.items()})
 "
 }
 tag=base; run "$@"
