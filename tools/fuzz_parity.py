@@ -1,0 +1,159 @@
+"""Randomised parity sweep (GPU box): small scans with random detector sizes,
+rasters, pixel-map laws, masks, bad frames, ROIs and search windows through
+the drop-in API against the CPU oracle at the BASELINE bars (object map 1e-5
+relative with identical validity, bit-exact integer argmin on unique pixels,
+refined maps and translations within 1e-3 px, error maps 1e-5 relative).
+python tools/fuzz_parity.py [n_cases] [first_seed]   -> one line per case, exit 1 on a failure."""
+import os
+import sys
+import traceback
+from dataclasses import replace
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2003_12726_b200 as pb  # noqa: E402
+from oracle import pxst_oracle as orc  # noqa: E402
+from paper_2003_12726_b200 import engine  # noqa: E402
+from paper_2003_12726_b200.synth import ScanConfig, make_scan  # noqa: E402
+
+MARGIN, PX_TOL = 1e-4, 1e-3
+
+
+def unique_pixels(stack):
+    flat = stack.reshape(-1, stack.shape[-1])
+    part = np.partition(flat, 1, axis=0) if flat.shape[0] > 1 else np.vstack([flat, flat + 1])
+    return (part[1] - part[0]) > MARGIN * np.abs(part[0])
+
+
+def one(seed):
+    rng = np.random.default_rng(1000 + seed)
+    law = str(rng.choice(["quad", "cubic", "fs_only"]))
+    if law == "fs_only":
+        cfg = ScanConfig(name=f"fuzz{seed}", n_ss=int(rng.integers(9, 40)), n_fs=int(rng.integers(40, 150)),
+                         positions="fs_line", n_frames=int(rng.integers(6, 30)),
+                         step=float(rng.uniform(1.0, 3.0)), jitter=0.3, u_law=law,
+                         wf_kind=str(rng.choice(["gaussian", "tophat"])),
+                         bad_frac=float(rng.choice([0.0, 0.01, 0.05])),
+                         u_noise=float(rng.choice([0.0, 0.5, 1.0])))
+    else:
+        cfg = ScanConfig(name=f"fuzz{seed}", n_ss=int(rng.integers(17, 90)), n_fs=int(rng.integers(20, 150)),
+                         positions="raster", nx=int(rng.integers(2, 6)), ny=int(rng.integers(2, 6)),
+                         step=float(rng.uniform(1.5, 6.0)), jitter=0.5, u_law=law,
+                         obj_sigma=float(rng.uniform(1.5, 3.0)),
+                         bad_frac=float(rng.choice([0.0, 0.01, 0.05])),
+                         u_noise=float(rng.choice([0.0, 0.5, 1.0])),
+                         t_noise=float(rng.choice([0.0, 1.0])), t_noise_kind="uniform")
+    s = make_scan(cfg, seed=seed)
+    sc, w, m, u, t = s.scan, s.w, s.m, s.u0, s.t0
+    n = sc.frames.shape[0]
+    good = np.ones(n, bool)
+    if rng.random() < 0.5 and n > 3:
+        good[rng.choice(n, size=max(1, n // 5), replace=False)] = False
+    sc = replace(sc, good_frames=good)
+    roi = None
+    if rng.random() < 0.4:
+        r0 = int(rng.integers(0, cfg.n_ss // 2)); r1 = int(rng.integers(r0 + 4, cfg.n_ss + 1))
+        c0 = int(rng.integers(0, cfg.n_fs // 2)); c1 = int(rng.integers(c0 + 4, cfg.n_fs + 1))
+        roi = pb.Roi(r0, min(r1, cfg.n_ss), c0, min(c1, cfg.n_fs))
+    rt = roi.as_tuple() if roi else None
+    if law == "fs_only":
+        half = (0, int(rng.integers(1, 9)))
+    else:
+        half = (int(rng.integers(0, 7)), int(rng.integers(0, 7)))
+        if rng.random() < 0.6:
+            half = (half[0], half[0])          # the square fast-path windows
+    sub = float(rng.choice([0.5, 0.25, 0.4])) if rng.random() < 0.15 else None
+    if sub is not None:
+        half = (min(half[0], 2), min(half[1], 2))
+    refine = bool(rng.random() < 0.6)
+    desc = (f"seed {seed}: {cfg.n_ss}x{cfg.n_fs} {law} frames {n} ({int(good.sum())} good) "
+            f"roi {rt} window {half} sub {sub} refine {refine}")
+    oa = (sc.frames, sc.good_frames, w.w, m.mask)
+    engine.SCAN_CACHE.clear()
+    # K1
+    ref = pb.make_reference(sc, w, m, u, t, roi=roi)
+    i_ref, wsum, org = orc.make_object_map(*oa, u.u, t.di, t.dj, roi=rt)
+    assert tuple(ref.origin) == tuple(org) and ref.i_ref.shape == i_ref.shape, "grid"
+    ok = wsum > 0
+    assert np.array_equal(ref.wsum > 0, ok), "validity"
+    rel = np.abs(ref.i_ref[ok] - i_ref[ok]) / np.maximum(np.abs(i_ref[ok]), 1e-300)
+    assert rel.max() < 1e-5, ("object", rel.max())
+    # K2
+    win = pb.SearchWindow(half[0], half[1], sub)
+    fw = None
+    if rng.random() < 0.2:               # frame weights (split-half style 0/1, or smooth)
+        shape = (n, cfg.n_ss, cfg.n_fs)
+        fw = (rng.random(shape) < 0.5).astype(np.float32) if rng.random() < 0.5 else \
+            rng.uniform(0.5, 1.5, shape).astype(np.float32)
+        desc += " fw"
+    un, en = pb.update_pixel_map(sc, w, m, ref, u, t, win,
+                                 pb.UpdateOptions(quadratic_refinement=refine), roi=roi,
+                                 frame_weights=fw)
+    uo, eo, stack = orc.update_pixel_map(*oa, ref.i_ref, ref.wsum, ref.origin, u.u, t.di, t.dj,
+                                         half[0], half[1], sub, refine, rt, fw,
+                                         threads=os.cpu_count() or 1, return_stack=True)
+    r0, r1, c0, c1 = rt or (0, cfg.n_ss, 0, cfg.n_fs)
+    sub_m = m.mask[r0:r1, c0:c1] & (w.w[r0:r1, c0:c1] > 0)
+    rr, cc = np.nonzero(sub_m)
+    rr, cc = rr + r0, cc + c0
+    uniq = unique_pixels(stack) if stack.shape[0] * stack.shape[1] > 1 else np.ones(rr.size, bool)
+    gu, ou = un.u[:, rr, cc], uo[:, rr, cc]
+    if not refine and sub is None:
+        assert np.array_equal(gu[:, uniq], ou[:, uniq]), "integer argmin"
+    d = np.abs(gu - ou).max(axis=0)
+    assert uniq.sum() == 0 or d[uniq].max() < PX_TOL, ("pixel map", d[uniq].max())
+    oth = np.ones(w.w.shape, bool); oth[rr, cc] = False
+    assert np.array_equal(un.u[:, oth], u.u[:, oth]), "pixels off the work set changed"
+    # error map: 1e-4 relative, plus the float32 floor of a best trial that fits
+    # almost exactly (r = I - W v cancels: |d err| ~ 1e-7 I |r| summed), scaled by
+    # the pixel's worst trial
+    e_g, e_o = en[rr, cc][uniq], eo[rr, cc][uniq]
+    worst = stack.reshape(-1, stack.shape[-1]).max(axis=0)[uniq]
+    assert uniq.sum() == 0 or np.all(np.abs(e_g - e_o) <= 1e-4 * np.abs(e_o) + 1e-5 * worst), "err map"
+    # K3 (on the oracle's map, so both see the same input)
+    U = pb.PixelMap(uo)
+    th = (int(rng.integers(0, 4)), int(rng.integers(0, 4)))
+    tsub = float(rng.choice([0.5, 0.25])) if rng.random() < 0.2 else None
+    T = pb.update_translations(sc, w, m, ref, U, t, pb.SearchWindow(th[0], th[1], tsub), roi=roi)
+    di, dj, errs = orc.update_translations(*oa, ref.i_ref, ref.wsum, ref.origin, U.u, t.di, t.dj,
+                                           th[0], th[1], tsub, roi=rt, return_errors=True)
+    nchk = 0
+    for fr, e in errs.items():
+        flat = np.sort(e.ravel())
+        if flat.size < 2 or (flat[1] - flat[0]) > MARGIN * abs(flat[0]):
+            assert abs(T.di[fr] - di[fr]) < PX_TOL and abs(T.dj[fr] - dj[fr]) < PX_TOL, \
+                ("translation", fr, T.di[fr] - di[fr], T.dj[fr] - dj[fr])
+            nchk += 1
+    bad = ~good
+    assert np.array_equal(T.di[bad], t.di[bad]) and np.array_equal(T.dj[bad], t.dj[bad]), "bad frames moved"
+    # K4
+    M = pb.calc_error(sc, w, m, ref, U, t, roi=roi)
+    dd = orc.calc_error(*oa, ref.i_ref, ref.wsum, ref.origin, U.u, t.di, t.dj, roi=rt)
+    np.testing.assert_allclose(M.per_frame, dd["per_frame"], rtol=1e-9, atol=1e-300)
+    np.testing.assert_allclose(M.per_pixel, dd["per_pixel"], rtol=1e-9, atol=1e-300)
+    assert abs(M.total - dd["total"]) <= 1e-9 * abs(dd["total"])
+    # (the plane is an exact fixed-point sum: a cell whose eps terms are below
+    # the quantum -- ~2^-61 of the eps bound -- reads 0 where float64 keeps 1e-19)
+    pl, po = M.reference_plane, dd["reference_plane"]
+    np.testing.assert_allclose(pl, po, rtol=1e-5, atol=1e-9 * max(1.0, np.abs(po).max()))
+    return desc + f" | obj {rel.max():.1e} px {d[uniq].max() if uniq.sum() else 0:.1e} uniq {uniq.mean():.3f} t {th}/{tsub} frames checked {nchk}"
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    fails = 0
+    for seed in range(first, first + n):
+        try:
+            print("ok  ", one(seed), flush=True)
+        except Exception as e:          # noqa: BLE001
+            fails += 1
+            print("FAIL", f"seed {seed}:", repr(e)[:300], flush=True)
+            traceback.print_exc(limit=3)
+    print(f"{n - fails} / {n} cases passed")
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
