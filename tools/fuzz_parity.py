@@ -46,6 +46,13 @@ def one(seed):
                          t_noise=float(rng.choice([0.0, 1.0])), t_noise_kind="uniform")
     s = make_scan(cfg, seed=seed)
     sc, w, m, u, t = s.scan, s.w, s.m, s.u0, s.t0
+    hard = seed >= 1000      # seeds >= 1000: harder cases (see below)
+    if hard and rng.random() < 0.4:
+        # a dead block of the whitefield (W = 0: off the work set, recon.py:88-90)
+        W2 = w.w.copy()
+        a0, b0 = int(rng.integers(0, cfg.n_ss - 3)), int(rng.integers(0, cfg.n_fs - 3))
+        W2[a0:a0 + int(rng.integers(2, 20)), b0:b0 + int(rng.integers(2, 40))] = 0.0
+        w = replace(w, w=W2)
     n = sc.frames.shape[0]
     good = np.ones(n, bool)
     if rng.random() < 0.5 and n > 3:
@@ -67,13 +74,34 @@ def one(seed):
     if sub is not None:
         half = (min(half[0], 2), min(half[1], 2))
     refine = bool(rng.random() < 0.6)
+    if hard and sub is None and rng.random() < 0.3:
+        # wide windows: 15 x 15 / 17 x 17 (generic kernel), 1 x 17 and 17 x 1 rows
+        k = int(rng.choice([7, 8]))
+        half = [(k, k), (0, 8), (8, 0)][int(rng.integers(0, 3))] if law != "fs_only" else (0, 8)
     desc = (f"seed {seed}: {cfg.n_ss}x{cfg.n_fs} {law} frames {n} ({int(good.sum())} good) "
             f"roi {rt} window {half} sub {sub} refine {refine}")
     oa = (sc.frames, sc.good_frames, w.w, m.mask)
     engine.SCAN_CACHE.clear()
     # K1
-    ref = pb.make_reference(sc, w, m, u, t, roi=roi)
-    i_ref, wsum, org = orc.make_object_map(*oa, u.u, t.di, t.dj, roi=rt)
+    ref_roi, ref_rt = roi, rt
+    if hard and rng.random() < 0.35:
+        # the reference formed on a smaller detector rectangle than the one
+        # searched: many samples read invalid cells or leave the grid
+        # (interp.py:53-85 masked renormalisation, recon.py:160-166 fallback)
+        r0 = int(rng.integers(0, max(1, cfg.n_ss // 3))); c0 = int(rng.integers(0, max(1, cfg.n_fs // 3)))
+        ref_roi = pb.Roi(r0, int(rng.integers(r0 + 6, cfg.n_ss + 1)), c0, int(rng.integers(c0 + 6, cfg.n_fs + 1)))
+        ref_rt = ref_roi.as_tuple()
+        desc += f" ref-roi {ref_rt}"
+    try:
+        i_ref, wsum, org = orc.make_object_map(*oa, u.u, t.di, t.dj, roi=ref_rt)
+    except ValueError as exc:            # empty work set (recon.py:116-117): same error here
+        try:
+            pb.make_reference(sc, w, m, u, t, roi=ref_roi)
+        except ValueError as exc2:
+            assert str(exc2) == str(exc), (str(exc2), str(exc))
+            return desc + " | both raise: " + str(exc)
+        raise AssertionError("the oracle raised, the GPU path did not")
+    ref = pb.make_reference(sc, w, m, u, t, roi=ref_roi)
     assert tuple(ref.origin) == tuple(org) and ref.i_ref.shape == i_ref.shape, "grid"
     ok = wsum > 0
     assert np.array_equal(ref.wsum > 0, ok), "validity"
@@ -105,12 +133,17 @@ def one(seed):
     assert uniq.sum() == 0 or d[uniq].max() < PX_TOL, ("pixel map", d[uniq].max())
     oth = np.ones(w.w.shape, bool); oth[rr, cc] = False
     assert np.array_equal(un.u[:, oth], u.u[:, oth]), "pixels off the work set changed"
-    # error map: 1e-4 relative, plus the float32 floor of a best trial that fits
-    # almost exactly (r = I - W v cancels: |d err| ~ 1e-7 I |r| summed), scaled by
-    # the pixel's worst trial
+    # error map: 1e-4 relative, plus the float32 floor of the residual
+    # r = I - W v (|dr| ~ 1e-7 I): |d sum r^2| <~ 1e-6 sqrt(sum I^2 sum r^2), in
+    # the map's normalisation (recon.py:257-263: var = sum fw (I - W)^2)
+    I = sc.frames[good][:, rr, cc].astype(np.float64)
+    fwp = np.ones_like(I) if fw is None else fw[good][:, rr, cc].astype(np.float64)
+    var = (fwp * (I - w.w[rr, cc][None, :]) ** 2).sum(axis=0)
+    s_i2 = (fwp * I * I).sum(axis=0) / np.where(var > 0, var, 1.0)
     e_g, e_o = en[rr, cc][uniq], eo[rr, cc][uniq]
-    worst = stack.reshape(-1, stack.shape[-1]).max(axis=0)[uniq]
-    assert uniq.sum() == 0 or np.all(np.abs(e_g - e_o) <= 1e-4 * np.abs(e_o) + 1e-5 * worst), "err map"
+    tol = 1e-4 * np.abs(e_o) + 1e-6 * np.sqrt(s_i2[uniq] * np.abs(e_o)) + 1e-300
+    assert uniq.sum() == 0 or np.all(np.abs(e_g - e_o) <= tol), \
+        ("err map", float(np.max(np.abs(e_g - e_o) / tol)))
     # K3 (on the oracle's map, so both see the same input)
     U = pb.PixelMap(uo)
     th = (int(rng.integers(0, 4)), int(rng.integers(0, 4)))
