@@ -24,3 +24,12 @@ import fuzz_parity  # noqa: E402
 def test_random_cases_vs_oracle(block):
     for seed in range(8 * block, 8 * block + 8):
         fuzz_parity.one(seed)          # raises on the first bar that fails
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_hard_random_cases_vs_oracle(block):
+    """Seeds >= 1000: dead whitefield blocks, the reference formed on a smaller
+    rectangle than the one searched (invalid cells, samples off the grid, exact
+    ties), 15x15 / 17x17 / 1x17 / 17x1 windows."""
+    for seed in range(1000 + 8 * block, 1000 + 8 * block + 8):
+        fuzz_parity.one(seed)

@@ -129,6 +129,12 @@ def one(seed):
     gu, ou = un.u[:, rr, cc], uo[:, rr, cc]
     if not refine and sub is None:
         assert np.array_equal(gu[:, uniq], ou[:, uniq]), "integer argmin"
+    # every trial exactly equal (all of them on the (I - W)^2 fallback): the
+    # argmin is the first index on both sides (recon.py:265-269)
+    flat_s = stack.reshape(-1, stack.shape[-1])
+    alltie = flat_s.max(axis=0) == flat_s.min(axis=0)
+    if flat_s.shape[0] > 1 and alltie.any():
+        assert np.array_equal(gu[:, alltie], ou[:, alltie]), "exact ties -> first index"
     d = np.abs(gu - ou).max(axis=0)
     assert uniq.sum() == 0 or d[uniq].max() < PX_TOL, ("pixel map", d[uniq].max())
     oth = np.ones(w.w.shape, bool); oth[rr, cc] = False
