@@ -17,6 +17,7 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+import fuzz_loop  # noqa: E402
 import fuzz_parity  # noqa: E402
 
 
@@ -33,3 +34,11 @@ def test_hard_random_cases_vs_oracle(block):
     ties), 15x15 / 17x17 / 1x17 / 17x1 windows."""
     for seed in range(1000 + 8 * block, 1000 + 8 * block + 8):
         fuzz_parity.one(seed)
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_random_main_loops_vs_oracle(block):
+    """tools/fuzz_loop.py: run_main_loop over random schedules against the
+    oracle's loop, half of the cases also over two shares of the device."""
+    for seed in range(6 * block, 6 * block + 6):
+        fuzz_loop.one(seed)

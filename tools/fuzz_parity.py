@@ -26,6 +26,9 @@ def unique_pixels(stack):
     return (part[1] - part[0]) > MARGIN * np.abs(part[0])
 
 
+LAST = {}          # the running case's description (printed with a failure)
+
+
 def one(seed):
     rng = np.random.default_rng(1000 + seed)
     law = str(rng.choice(["quad", "cubic", "fs_only"]))
@@ -81,6 +84,7 @@ def one(seed):
     desc = (f"seed {seed}: {cfg.n_ss}x{cfg.n_fs} {law} frames {n} ({int(good.sum())} good) "
             f"roi {rt} window {half} sub {sub} refine {refine}")
     oa = (sc.frames, sc.good_frames, w.w, m.mask)
+    LAST["desc"] = desc
     engine.SCAN_CACHE.clear()
     # K1
     ref_roi, ref_rt = roi, rt
@@ -150,6 +154,21 @@ def one(seed):
     tol = 1e-4 * np.abs(e_o) + 1e-6 * np.sqrt(s_i2[uniq] * np.abs(e_o)) + 1e-300
     assert uniq.sum() == 0 or np.all(np.abs(e_g - e_o) <= tol), \
         ("err map", float(np.max(np.abs(e_g - e_o) / tol)))
+    # K2's optional stages (recon.py:298-311: Gaussian smoothing of the
+    # displacement, irrotational projection) on identical inputs: the oracle's
+    # raw map through the device kernels against the oracle's own stages
+    if seed % 3 == 0 and fw is None:
+        sigma = float(rng.choice([0.0, 1.5, 3.0]))
+        integ = bool(rng.random() < 0.7)
+        support = np.zeros(w.w.shape, bool)
+        support[rr, cc] = True
+        u_reg_o = orc.regularise_map(uo, support, sigma, integ)
+        ds = engine.SCAN_CACHE.get(sc, w, m, roi)
+        u_t = ds.upload_u(uo.copy())
+        ds.regularise(u_t, pb.UpdateOptions(True, integ, sigma))
+        dreg = np.abs(u_t.cpu().numpy() - u_reg_o).max()
+        assert dreg < 1e-8, ("regularised map", dreg, sigma, integ)
+        desc += f" reg(s{sigma},{'int' if integ else '-'}) {dreg:.0e}"
     # K3 (on the oracle's map, so both see the same input)
     U = pb.PixelMap(uo)
     th = (int(rng.integers(0, 4)), int(rng.integers(0, 4)))
@@ -188,7 +207,7 @@ def main():
             print("ok  ", one(seed), flush=True)
         except Exception as e:          # noqa: BLE001
             fails += 1
-            print("FAIL", f"seed {seed}:", repr(e)[:300], flush=True)
+            print("FAIL", f"seed {seed}:", repr(e)[:300], "|", LAST.get("desc", ""), flush=True)
             traceback.print_exc(limit=3)
     print(f"{n - fails} / {n} cases passed")
     sys.exit(1 if fails else 0)
