@@ -47,6 +47,14 @@ def one(seed):
                          bad_frac=float(rng.choice([0.0, 0.01, 0.05])),
                          u_noise=float(rng.choice([0.0, 0.5, 1.0])),
                          t_noise=float(rng.choice([0.0, 1.0])), t_noise_kind="uniform")
+    many = seed >= 2000      # seeds >= 2000: many frames on a small detector (> 128 and > 512
+    if many:                 # good frames: frame-table chunks, sessions, K2's float32 chunk split)
+        nx, ny = [(10, 14), (12, 12), (23, 23), (20, 27), (26, 27)][int(rng.integers(0, 5))]
+        cfg = ScanConfig(name=f"fuzz{seed}", n_ss=int(rng.integers(17, 48)), n_fs=int(rng.integers(20, 70)),
+                         positions="raster", nx=nx, ny=ny, step=float(rng.uniform(1.0, 2.5)), jitter=0.5,
+                         u_law=str(rng.choice(["quad", "cubic"])), bad_frac=0.01,
+                         u_noise=float(rng.choice([0.5, 1.0])), t_noise=1.0, t_noise_kind="uniform")
+        law = cfg.u_law
     s = make_scan(cfg, seed=seed)
     sc, w, m, u, t = s.scan, s.w, s.m, s.u0, s.t0
     hard = seed >= 1000      # seeds >= 1000: harder cases (see below)
@@ -73,6 +81,8 @@ def one(seed):
         half = (int(rng.integers(0, 7)), int(rng.integers(0, 7)))
         if rng.random() < 0.6:
             half = (half[0], half[0])          # the square fast-path windows
+    if many:
+        half = (min(half[0], 2), min(half[1], 2))      # (keeps the oracle's cost down)
     sub = float(rng.choice([0.5, 0.25, 0.4])) if rng.random() < 0.15 else None
     if sub is not None:
         half = (min(half[0], 2), min(half[1], 2))
