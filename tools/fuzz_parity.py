@@ -21,9 +21,16 @@ MARGIN, PX_TOL = 1e-4, 1e-3
 
 
 def unique_pixels(stack):
+    """Unique argmin: best and second-best trial apart by > MARGIN relative.
+    A best trial at the float64 rounding floor (an exact fit: the sample's
+    cells were formed by this sample alone, errors of 1e-21 against trials of
+    order 1) is not unique -- the reference's own choice among such residues
+    is decided by rounding -- so the margin is taken against at least 1e-9 of
+    the pixel's worst trial."""
     flat = stack.reshape(-1, stack.shape[-1])
     part = np.partition(flat, 1, axis=0) if flat.shape[0] > 1 else np.vstack([flat, flat + 1])
-    return (part[1] - part[0]) > MARGIN * np.abs(part[0])
+    floor = 1e-9 * flat.max(axis=0)
+    return (part[1] - part[0]) > MARGIN * np.maximum(np.abs(part[0]), floor)
 
 
 LAST = {}          # the running case's description (printed with a failure)
@@ -179,6 +186,25 @@ def one(seed):
         dreg = np.abs(u_t.cpu().numpy() - u_reg_o).max()
         assert dreg < 1e-8, ("regularised map", dreg, sigma, integ)
         desc += f" reg(s{sigma},{'int' if integ else '-'}) {dreg:.0e}"
+    # split-half uncertainty (analysis.py:294-361): the device SplitMix split of
+    # the samples and one search per half against the oracle's
+    if seed % 4 == 1 and sub is None and max(half) <= 4:
+        from paper_2003_12726_b200 import analysis
+        S = analysis.split_half_recon(sc, w, m, ref, u, t, win, seed=seed,
+                                      opts=pb.UpdateOptions(refine, False, 0.0), roi=roi)
+        ua, ub, hss, hfs, sg, st_a, st_b = orc.split_half_recon(
+            *oa, ref.i_ref, ref.wsum, ref.origin, u.u, t.di, t.dj, half[0], half[1], seed=seed,
+            quadratic_refinement=refine, roi=rt, threads=os.cpu_count() or 1, return_stacks=True)
+        nun = 0
+        for got, want, st in ((S.map_a.u, ua, st_a), (S.map_b.u, ub, st_b)):
+            uq = unique_pixels(st) if st.shape[0] * st.shape[1] > 1 else np.ones(rr.size, bool)
+            dd_ = np.abs(got[:, rr, cc] - want[:, rr, cc]).max(axis=0)
+            assert uq.sum() == 0 or dd_[uq].max() < PX_TOL, ("split-half map", dd_[uq].max())
+            assert np.array_equal(got[:, oth], want[:, oth]), "split-half: pixels off the work set"
+            nun += int((~uq).sum())
+        slack = 2 * nun + 2
+        assert np.abs(S.hist_ss - hss).sum() <= slack and np.abs(S.hist_fs - hfs).sum() <= slack, "split-half histograms"
+        desc += " split-half"
     # K3 (on the oracle's map, so both see the same input)
     U = pb.PixelMap(uo)
     th = (int(rng.integers(0, 4)), int(rng.integers(0, 4)))
