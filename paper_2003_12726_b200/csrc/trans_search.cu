@@ -78,7 +78,48 @@ struct TransArgs {
   unsigned* slow_list;       // frames (within the chunk) with flagged tiles
   unsigned* slow_n;
   unsigned long long* dbg;   // nullable debug counters (PXST_DEBUG)
+  const int* sat;            // summed-area table of pv == 0, [(os + 1)][(of + 1)] (nullable)
 };
+
+// Summed-area table of the patch-invalid cells (two passes: rows, then
+// columns), so a (tile, frame) can ask "is every sample base of this tile on a
+// patch-valid cell?" with four loads that do not depend on the samples'
+// geometry -- the per-sample patch-valid lookup was the one load of the fast
+// kernel that waits for the sample's own floor (28 % of the 7 x 7 kernel's
+// stall samples sat on the long scoreboard).
+__global__ void k_sat_rows(const uint8_t* __restrict__ pv, int os, int of, int* __restrict__ sat) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > os) return;
+  int* row = sat + (int64_t)r * (of + 1);
+  row[0] = 0;
+  if (r == 0) {
+    for (int c = 0; c < of; ++c) row[c + 1] = 0;
+    return;
+  }
+  int acc = 0;
+  const uint8_t* p = pv + (int64_t)(r - 1) * of;
+  for (int c = 0; c < of; ++c) {
+    acc += p[c] == 0 ? 1 : 0;
+    row[c + 1] = acc;
+  }
+}
+__global__ void k_sat_cols(int os, int of, int* __restrict__ sat) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > of) return;
+  int acc = 0;
+  for (int r = 0; r <= os; ++r) {
+    int* q = sat + (int64_t)r * (of + 1) + c;
+    acc += *q;
+    *q = acc;
+  }
+}
+// invalid cells among rows [r0, r1] x columns [c0, c1] (inclusive, inside the grid)
+__device__ __forceinline__ int sat_count(const int* __restrict__ sat, int of, int r0, int r1, int c0,
+                                         int c1) {
+  const int w = of + 1;
+  return __ldg(sat + (r1 + 1) * w + (c1 + 1)) - __ldg(sat + r0 * w + (c1 + 1)) -
+         __ldg(sat + (r1 + 1) * w + c0) + __ldg(sat + r0 * w + c0);
+}
 
 // Boxes cover a 16x64 tile's footprint; the host grows them from the measured spans.
 __host__ __device__ inline int box_rows3(int ka) { return ka + 24; }
@@ -261,7 +302,7 @@ struct Sample3f {
 };
 __device__ __forceinline__ Sample3f make_sample3_split(const TransArgs& a, int4 r,
                                                        const FrameSplit& f, bool fits, int wr0,
-                                                       int wc0) {
+                                                       int wc0, bool allv = false) {
   Sample3f s;
   float dx = __int_as_float(r.z) - f.fd0, dy = __int_as_float(r.w) - f.fd1;
   int i = r.x - f.id0, j = r.y - f.id1;
@@ -279,7 +320,9 @@ __device__ __forceinline__ Sample3f make_sample3_split(const TransArgs& a, int4 
   const int os = static_cast<int>(a.os), of = static_cast<int>(a.of);
   const bool in = static_cast<unsigned>(s.i) < static_cast<unsigned>(os) &&
                   static_cast<unsigned>(s.j) < static_cast<unsigned>(of);
-  s.pvb = fits ? __ldg(a.pv + (in ? s.i * of + s.j : 0)) : 0;
+  // allv (warp-uniform): every sample base of this tile and frame is on a
+  // patch-valid cell (sat_count == 0 over the tile's base rectangle): no lookup
+  s.pvb = allv ? 1 : (fits ? __ldg(a.pv + (in ? s.i * of + s.j : 0)) : 0);
   s.pre = fits && in && static_cast<unsigned>(s.lr) <= static_cast<unsigned>(a.box_r - a.ka - 1) &&
           static_cast<unsigned>(s.lc) <= static_cast<unsigned>(a.box_c - a.kb - 1);
   return s;
@@ -391,7 +434,18 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
     // the tile's window origin for this frame (as issue() computed it)
     const bool fits = tile_fits(g, need_rows3(KA), need_cols3(KB), a.box_r, a.box_c);
     const int wr0 = static_cast<int>(floor((g.umin0 - dI - n0d) - a.ph_a)) - a.mhi_a;
-    const int wc0 = align4_down(static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b)) - a.mhi_b);
+    const int jb = static_cast<int>(floor((g.umin1 - dJ - m0d) - a.ph_b));
+    const int wc0 = align4_down(jb - a.mhi_b);
+    // the tile's sample bases lie in rows [wr0 + mhi_a, + span_r + 1], columns
+    // [jb, + span_c + 1] (one more each side: the float32 split may move a
+    // base by one where x is within 1e-7 of an integer)
+    bool allv = false;
+    if (a.sat && fits) {
+      const int i0 = wr0 + a.mhi_a - 1, i1 = wr0 + a.mhi_a + g.span_r + 2;
+      const int j0 = jb - 1, j1 = jb + g.span_c + 2;
+      if (i0 >= 0 && j0 >= 0 && i1 < static_cast<int>(a.os) && j1 < static_cast<int>(a.of))
+        allv = sat_count(a.sat, static_cast<int>(a.of), i0, i1, j0, j1) == 0;
+    }
     float I[4], W[4], fx[4], fy[4];
     int off[4];                        // patch origin offset in the slot, -1 = not fast
     bool tile_slow = false;
@@ -400,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, (KA * KB < PXST_K3_OCC3_BELOW)   ? 3
       const bool live = cur.r16[e].x != kNoPixel;
       I[e] = cur.I[e];
       W[e] = cur.W[e];                 // 0 off the work set
-      const Sample3f sm = make_sample3_split(a, cur.r16[e], fs_, fits, wr0, wc0);
+      const Sample3f sm = make_sample3_split(a, cur.r16[e], fs_, fits, wr0, wc0, allv);
       fx[e] = sm.fx;
       fy[e] = sm.fy;
       off[e] = (live && sm.fast()) ? sm.lr * a.box_c + sm.lc : -1;
@@ -826,7 +880,7 @@ int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref
     a.q_a = qa; a.q_b = qb; a.kh_a = kha; a.kh_b = khb;
     a.tile_words = static_cast<int>((a.n_tiles + 63) / 64);
 
-    Scratch geo, pvbuf, fmnbuf, fmpad, lst, tb;
+    Scratch geo, pvbuf, fmnbuf, fmpad, lst, tb, satbuf;
     if (int e = geo.alloc(sizeof(TileGeo) * a.n_tiles, s)) return e;
     a.geo = geo.as<TileGeo>();
     k_tile_geo3<<<dim3((unsigned)a.n_ct, (unsigned)a.n_bands), kThreads, 0, s>>>(
@@ -867,6 +921,19 @@ int translation_search(const pxst_scan* sc, const pxst_stats* st, const pxst_ref
       return e;
     a.pv = pvbuf.as<uint8_t>();
     a.fmn = fmnbuf.as<float>();
+    // Off by default (PXST_K3_SAT=1 turns it on): measured neutral to slightly
+    // slower -- config 3 K3 31.15 ms without, 31.71 ms with; config 4 282.9 /
+    // 283.4 ms -- the four table loads cost what the skipped lookups save.
+    if (getenv("PXST_K3_SAT") && (ref->os + 1) * (ref->of + 1) < (int64_t(1) << 31)) {
+      if (int e = satbuf.alloc(sizeof(int) * (ref->os + 1) * (ref->of + 1), s)) return e;
+      const int os_i = static_cast<int>(ref->os), of_i = static_cast<int>(ref->of);
+      k_sat_rows<<<(os_i + 1 + 127) / 128, 128, 0, s>>>(pvbuf.as<uint8_t>(), os_i, of_i,
+                                                       satbuf.as<int>());
+      PXST_CHECK_LAUNCH();
+      k_sat_cols<<<(of_i + 1 + 127) / 128, 128, 0, s>>>(os_i, of_i, satbuf.as<int>());
+      PXST_CHECK_LAUNCH();
+      a.sat = satbuf.as<int>();
+    }
     // TMA descriptor (16-byte row pitch)
     const float* tbase = ref->fm;
     int64_t pitch = ref->of;
