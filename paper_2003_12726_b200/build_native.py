@@ -23,6 +23,20 @@ LIB = os.environ.get("PXST_LIB_OUT", os.path.join(HERE, "libpxst_b200.so"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
 FLAGS += os.environ.get("PXST_NVCC_EXTRA", "").split()
+# Per-file flags.  PXST_NVCC_FILE_FLAGS="a.cu=<flags>;b.cu=<flags>" replaces the
+# table (variant builds, tools/variant.sh).
+FILE_FLAGS = {
+    # ptxas's register-usage level (default 5) at 0-3 gives the K3 kernels a
+    # better allocation under their 128-register cap: config 3 K3 31.15 -> 30.5
+    # ms, config 4 282.9 -> 278.8 ms (measured side by side, tools/variant_bench.sh).
+    # The same level costs K2 6-14 % and the fixed-point pass ~8 %, so it is set
+    # for this file only; levels 8-10 help K2's 1 x 17 kernel (-2.4 %) but cost
+    # 13 x 13 up to 1 %: not taken.
+    "trans_search.cu": ["-Xptxas", "--register-usage-level=3"],
+}
+if "PXST_NVCC_FILE_FLAGS" in os.environ:
+    FILE_FLAGS = {k.strip(): v.split() for k, v in
+                  (kv.split("=", 1) for kv in os.environ["PXST_NVCC_FILE_FLAGS"].split(";") if kv)}
 
 
 def nvcc() -> str:
@@ -53,7 +67,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         o = os.path.join(BUILD, src[:-3] + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr):
-            cmd = [nv, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [nv, *ARCH, *FLAGS, *FILE_FLAGS.get(src, []), "-c", s, "-o", o]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
