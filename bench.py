@@ -310,7 +310,7 @@ def k3_trials(pb, ds, cfg):
     return ds.n_work * len(w.offsets(0)) * len(w.offsets(1)) * ds.n_good
 
 
-def extra_config(cfg_id, dev, steps=4, warmup=3):
+def extra_config(cfg_id, dev, steps=4, warmup=3, rank=0, world=1):
     """A larger BASELINE config measured in the same process as the headline
     (device-resident stack rendered on the GPU, the config's own iteration
     sequence, device-timed with CUDA events; its 3-8 GB stack is larger than
@@ -329,7 +329,11 @@ def extra_config(cfg_id, dev, steps=4, warmup=3):
     ds.ready(frame_stats=cfg.update_translations)
     ds.absmax()
     stream = torch.cuda.current_stream()
-    seq = Sequence(ds, cfg, u_t, di_t, dj_t, stream)
+    sharded = None
+    if world > 1:       # N ranks: every rank renders the same stack, the work is sharded
+        from paper_2003_12726_b200.sharding import DeviceExecutor, ShardedIteration
+        sharded = ShardedIteration(DeviceExecutor(ds), rank, world)
+    seq = Sequence(ds, cfg, u_t, di_t, dj_t, stream, sharded)
     for _ in range(warmup):
         seq.step()
     mk = lambda: torch.cuda.Event(enable_timing=True)   # noqa: E731
@@ -344,6 +348,12 @@ def extra_config(cfg_id, dev, steps=4, warmup=3):
         en[i].record(stream)
     torch.cuda.synchronize()
     ms = [a.elapsed_time(b) for a, b in zip(st, en)]
+    if world > 1:       # the slowest rank's time per iteration
+        import torch.distributed as dist
+        staged = dist.get_backend() == "gloo"
+        t = torch.tensor(ms, dtype=torch.float64, device="cpu" if staged else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = [float(x) for x in t.tolist()]
     out = {"workload": cfg.name, "iterations_timed": steps,
            "ms_per_iteration": float(np.mean(ms)), "step_ms": [round(x, 3) for x in ms],
            "setup_s": round(time.perf_counter() - t0, 1)}
@@ -353,8 +363,13 @@ def extra_config(cfg_id, dev, steps=4, warmup=3):
         tf = FLOP_PER_TRIAL * trials / (k2ms * 1e-3) / 1e12
         out.update(pixel_map_trials_per_iteration=trials,
                    trials_per_s=trials / (out["ms_per_iteration"] * 1e-3),
-                   k2_ms=k2ms, k2_tflops=tf, k2_frac=tf / THEORETICAL_FP32_TFLOPS)
-    if cfg.update_translations:
+                   k2_ms=k2ms, k2_tflops=tf, k2_frac=tf / world / THEORETICAL_FP32_TFLOPS)
+        # (N ranks: k2_ms is rank 0's time for its row band, k2_tflops the rate of
+        # all bands together, k2_frac that rate per GPU against one GPU's peak)
+    if world > 1:
+        out["parallelism"] = (f"{world} ranks: frames shard object formation and translations, "
+                              "detector rows the pixel map and error maps (this rank's K2 time)")
+    if cfg.update_translations and world == 1:
         tt = k3_trials(pb, ds, cfg)
         k3ms = float(np.mean([a.elapsed_time(b) for a, b in k3]))
         tf = FLOP_PER_TRIAL * tt / (k3ms * 1e-3) / 1e12
@@ -484,6 +499,18 @@ def run_ours(args, rank, world, local):
         k2_mean = float(np.mean(k2_ms))
     ms_per_step = total_ms / args.steps
     value = trials * args.steps / (total_ms * 1e-3)
+    extra_sharded = None
+    if not args.profile and world > 1 and args.extras:
+        # N ranks: the same larger configs, sharded over the ranks (config 3 is
+        # the one the 8-GPU scaling target is quoted on); every rank runs them,
+        # rank 0 reports the slowest rank's time per iteration
+        extra_sharded = {}
+        for cid in (int(c) for c in args.extras.split(",") if c.strip()):
+            try:
+                extra_sharded[f"cfg{cid}"] = extra_config(cid, dev, rank=rank, world=world)
+            except Exception as exc:
+                extra_sharded[f"cfg{cid}"] = {"error": repr(exc)[:300]}
+                raise            # (a rank that stopped would leave the others in a collective)
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -532,6 +559,8 @@ def run_ours(args, rank, world, local):
         pg = e2e(s, args, pb, engine, torch, trials, pinned_frames=False)
         out["e2e"]["pageable"] = {k: pg[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step",
                                                      "d2h_bytes_per_step", "path")}
+    if extra_sharded is not None:
+        out["extra_configs"] = extra_sharded
     if not args.profile and world == 1 and args.extras:
         # the larger configs, measured in this same run (builder-run numbers
         # alone were not driver-observed)
