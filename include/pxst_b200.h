@@ -306,6 +306,14 @@ int pxst_add_i64(int64_t* dst, const int64_t* src, int64_t n, void* stream);
 int pxst_add_f64(double* dst, const double* src, int64_t n, void* stream);
 int pxst_or_u8(uint8_t* dst, const uint8_t* src, int64_t n, void* stream);
 
+/* Mean and variance (ddof 0) of v[i] over the cells with valid[i] != 0, in a
+ * fixed summation order: out[3] (device) = (count, mean, variance).  The
+ * contrast var / mean^2 of the merged reference that
+ * geometry.fit_defocus_registration maximises (geometry.py:214-222:
+ * ref.i_ref[ref.valid] -> np.var / np.mean ** 2). */
+int pxst_masked_moments(const double* v, const uint8_t* valid, int64_t n, double* out,
+                        void* stream);
+
 /* Interpolation primitives (interp.py:53-85 and :88-123), for the drop-in
  * interp module and the parity tests.  gather: vals/ok at n points of the
  * masked image.  splat: float64 accumulation into acc_v/acc_w [os,of]

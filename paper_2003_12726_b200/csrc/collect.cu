@@ -27,10 +27,56 @@ __global__ void k_or_u8(uint8_t* __restrict__ dst, const uint8_t* __restrict__ s
     dst[i] |= src[i];
 }
 
+// Mean and variance (ddof 0, as numpy's var) of the cells flagged valid: one
+// block, every thread sums its strided share in a fixed order, a fixed tree
+// adds the threads -- deterministic; two passes (mean, then squared
+// deviations) like numpy.  out = (count, mean, var).
+__global__ void __launch_bounds__(1024) k_masked_moments(const double* __restrict__ v,
+                                                        const uint8_t* __restrict__ valid,
+                                                        int64_t n, double* __restrict__ out) {
+  __shared__ double sh[1024];
+  __shared__ double s_mean, s_cnt;
+  auto block_sum = [&](double x) {
+    sh[threadIdx.x] = x;
+    __syncthreads();
+    for (int o = 512; o > 0; o >>= 1) {
+      if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+      __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+  };
+  double c = 0.0, a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024)
+    if (valid[i]) { c += 1.0; a += v[i]; }
+  const double cnt = block_sum(c), sum = block_sum(a);
+  if (threadIdx.x == 0) { s_cnt = cnt; s_mean = cnt > 0.0 ? sum / cnt : 0.0; }
+  __syncthreads();
+  const double mean = s_mean;
+  double q = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024)
+    if (valid[i]) { const double d = v[i] - mean; q += d * d; }
+  const double ss = block_sum(q);
+  if (threadIdx.x == 0) {
+    out[0] = s_cnt;
+    out[1] = mean;
+    out[2] = s_cnt > 0.0 ? ss / s_cnt : 0.0;
+  }
+}
+
 }  // namespace
 }  // namespace pxst
 
 using namespace pxst;
+
+extern "C" int pxst_masked_moments(const double* v, const uint8_t* valid, int64_t n, double* out,
+                                   void* stream) {
+  PXST_REQUIRE(v && valid && out && n >= 0, "bad arguments");
+  k_masked_moments<<<1, 1024, 0, as_stream(stream)>>>(v, valid, n, out);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
 
 extern "C" int pxst_add_i64(int64_t* dst, const int64_t* src, int64_t n, void* stream) {
   PXST_REQUIRE(dst && src && n >= 0, "bad arguments");

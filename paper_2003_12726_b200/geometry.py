@@ -17,6 +17,7 @@ import torch
 
 from .data_model import Geometry, PixelMap, PixelMask, PixelTranslations, Roi, ScanData
 from .data_model import Whitefield
+from ._native import check, stream_ptr
 from .engine import SCAN_CACHE
 
 
@@ -69,7 +70,7 @@ def fit_defocus_registration(scan: ScanData, w: Whitefield, mask: PixelMask, z1_
     ds = SCAN_CACHE.get(scan, w, mask, roi)
     if ds.empty:
         raise ValueError("make_reference: empty good pixel/frame set")
-    stats = torch.zeros((len(cands), 2), dtype=torch.float64, device=ds.device)
+    stats = torch.zeros((len(cands), 3), dtype=torch.float64, device=ds.device)   # count, mean, var
     u_t = None
     for k, (za, zb) in enumerate(cands):
         geom = make_geometry(za, zb, scan)
@@ -79,11 +80,10 @@ def fit_defocus_registration(scan: ScanData, w: Whitefield, mask: PixelMask, z1_
         t = translations_to_pixels(scan, geom)
         di_t, dj_t = ds.upload_t(t.di, t.dj)
         ref = ds.object_map(u_t, di_t, dj_t)
-        vals = ref.i_ref[ref.valid.bool()]
-        mean = vals.mean()
-        stats[k, 0] = mean
-        stats[k, 1] = ((vals - mean) ** 2).mean()          # numpy var (ddof 0)
-    st = stats.cpu().numpy()
+        # mean and numpy-style variance (ddof 0) of the valid cells, on the device
+        check(ds.lib.pxst_masked_moments(ref.i_ref.data_ptr(), ref.valid.data_ptr(),
+                                         ref.i_ref.numel(), stats[k].data_ptr(), stream_ptr()))
+    st = stats.cpu().numpy()[:, 1:]
     contrast = np.where(st[:, 0] != 0, st[:, 1] / np.where(st[:, 0] != 0, st[:, 0] ** 2, 1.0),
                         0.0)
     best = int(contrast.argmax())
