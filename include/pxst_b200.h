@@ -306,6 +306,16 @@ int pxst_add_i64(int64_t* dst, const int64_t* src, int64_t n, void* stream);
 int pxst_add_f64(double* dst, const double* src, int64_t n, void* stream);
 int pxst_or_u8(uint8_t* dst, const uint8_t* src, int64_t n, void* stream);
 
+/* Frame stack of another element type -> float32 on the device.  The
+ * reference takes frames of any dtype and casts them where it reads them
+ * (recon.py:91 scan.frames[good][:, idx_ss, idx_fs].astype(np.float64)); the
+ * kernels read a float32 stack, so a stack of detector counts is uploaded in
+ * its own type (half the bytes for 16-bit counts, no host conversion pass)
+ * and converted here (round to nearest even, as numpy's astype(float32)). */
+enum { PXST_U8 = 1, PXST_I8, PXST_U16, PXST_I16, PXST_U32, PXST_I32, PXST_U64, PXST_I64,
+       PXST_F64 };
+int pxst_stack_to_f32(const void* src, int type_code, int64_t n, float* dst, void* stream);
+
 /* Mean and variance (ddof 0) of v[i] over the cells with valid[i] != 0, in a
  * fixed summation order: out[3] (device) = (count, mean, variance).  The
  * contrast var / mean^2 of the merged reference that

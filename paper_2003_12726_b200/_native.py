@@ -100,6 +100,7 @@ _SIGS = {
                                       c_void_p, c_void_p, c_void_p, c_int64, POINTER(PxstAccum),
                                       c_void_p]),
     "pxst_masked_moments": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "pxst_stack_to_f32": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p]),
     "pxst_grid_rule": (c_int, [c_void_p, c_void_p, c_void_p]),
     "pxst_error_partials": (c_int, [POINTER(PxstScan), POINTER(PxstStats), POINTER(PxstRef),
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -3,6 +3,8 @@
 // Integer sums are exact (the fixed-point splat images), so any order of the
 // peers gives the same bits; the float64 per-frame sums are added by every
 // device in the same fixed peer order.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pxst {
@@ -65,10 +67,49 @@ __global__ void __launch_bounds__(1024) k_masked_moments(const double* __restric
   }
 }
 
+// Frame stack of another element type -> the float32 stack the kernels read
+// (the reference takes any dtype and casts per use: recon.py:91
+// scan.frames[...].astype(np.float64)).  The stack is uploaded in its own
+// type -- half the bytes for 16-bit detector counts, no host-side conversion
+// pass -- and converted here, 4 elements per thread.
+template <class T>
+__global__ void k_to_f32(const T* __restrict__ src, int64_t n, float* __restrict__ dst) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = static_cast<float>(src[i]);       // round to nearest even, as numpy's astype
+}
+template <class T>
+int launch_to_f32(const void* src, int64_t n, float* dst, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  k_to_f32<T><<<blocks, 256, 0, s>>>(static_cast<const T*>(src), n, dst);
+  PXST_CHECK_LAUNCH();
+  return PXST_OK;
+}
+
 }  // namespace
 }  // namespace pxst
 
 using namespace pxst;
+
+extern "C" int pxst_stack_to_f32(const void* src, int type_code, int64_t n, float* dst,
+                                 void* stream) {
+  PXST_REQUIRE(src && dst && n >= 0, "bad arguments");
+  if (n == 0) return PXST_OK;
+  cudaStream_t s = as_stream(stream);
+  switch (type_code) {
+    case PXST_U8: return launch_to_f32<uint8_t>(src, n, dst, s);
+    case PXST_I8: return launch_to_f32<int8_t>(src, n, dst, s);
+    case PXST_U16: return launch_to_f32<uint16_t>(src, n, dst, s);
+    case PXST_I16: return launch_to_f32<int16_t>(src, n, dst, s);
+    case PXST_U32: return launch_to_f32<uint32_t>(src, n, dst, s);
+    case PXST_I32: return launch_to_f32<int32_t>(src, n, dst, s);
+    case PXST_U64: return launch_to_f32<unsigned long long>(src, n, dst, s);
+    case PXST_I64: return launch_to_f32<long long>(src, n, dst, s);
+    case PXST_F64: return launch_to_f32<double>(src, n, dst, s);
+    default: PXST_REQUIRE(false, "unknown element type code %d", type_code);
+  }
+  return PXST_OK;
+}
 
 extern "C" int pxst_masked_moments(const double* v, const uint8_t* valid, int64_t n, double* out,
                                    void* stream) {

@@ -51,6 +51,11 @@ def _device() -> torch.device:
 # Host<->device byte counters (bench.py's e2e accounting).
 TRANSFER = {"h2d": 0, "d2h": 0}
 
+# Element types a frame stack may be uploaded in (pxst_stack_to_f32's codes; float32 goes
+# as it is, anything else is converted on the host)
+_STACK_CODES = {"u1": 1, "b1": 1, "i1": 2, "u2": 3, "i2": 4, "u4": 5, "i4": 6, "u8": 7, "i8": 8,
+                "f8": 9}
+
 # Frame chunks in which a pageable stack is staged into pinned memory
 # (DeviceScan._upload_pageable); PXST_STAGE_CHUNKS=1: one piece, as before.
 _STAGE_CHUNKS = max(1, int(os.environ.get("PXST_STAGE_CHUNKS", "8")))
@@ -324,6 +329,11 @@ class DeviceScan:
         copy stream (one event per chunk), so object formation can splat the
         chunks that have landed while the rest is in flight; every other
         consumer waits for the whole stack (ready())."""
+        a = np.asarray(frames)
+        code = _STACK_CODES.get(a.dtype.str.lstrip("<>=|"))
+        if code is not None and a.dtype.isnative and a.flags.c_contiguous and a.flags.writeable \
+                and self.n_good > 0 and a.nbytes >= (1 << 20) and a.ndim == 3 and a.shape[0] >= 2:
+            return self._upload_native(a, code, dev)
         h = np.ascontiguousarray(frames, dtype=np.float32)
         t = torch.from_numpy(h) if h.flags.writeable else None
         if t is not None and not t.is_pinned() and self.n_good > 0 and h.nbytes >= (8 << 20) \
@@ -354,6 +364,37 @@ class DeviceScan:
         TRANSFER["h2d"] += h.nbytes
         out.record_stream(copy)
         self._upload.update(chunks=chunks, waited=False, host=t)
+        return out
+
+    def _upload_native(self, a: np.ndarray, code: int, dev):
+        """A stack of another element type (detector counts are usually 16- or
+        32-bit integers; the reference casts per use, recon.py:91): uploaded as
+        it is -- half the bytes for uint16, and no conversion pass over the
+        stack on the host -- then converted to the kernels' float32 on the
+        device (pxst_stack_to_f32, numpy's rounding)."""
+        n = a.shape[0]
+        raw = torch.from_numpy(a.view(np.uint8).reshape(n, -1))
+        pinned = raw.is_pinned()
+        raw_dev = torch.empty(raw.shape, dtype=torch.uint8, device=dev)
+        out = torch.empty(a.shape, dtype=torch.float32, device=dev)
+        pin = raw if pinned else torch.empty(raw.shape, dtype=torch.uint8, pin_memory=True)
+        copy = torch.cuda.Stream(dev)
+        copy.wait_stream(torch.cuda.current_stream(dev))
+        k = min(n, _STAGE_CHUNKS)
+        edges = [n * c // k for c in range(k + 1)]
+        with torch.cuda.stream(copy):
+            for lo, hi in zip(edges[:-1], edges[1:]):
+                if not pinned:
+                    pin[lo:hi].copy_(raw[lo:hi])
+                raw_dev[lo:hi].copy_(pin[lo:hi], non_blocking=True)
+            check(self.lib.pxst_stack_to_f32(raw_dev.data_ptr(), code, a.size, out.data_ptr(),
+                                             stream_ptr(copy)))
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        TRANSFER["h2d"] += a.nbytes
+        out.record_stream(copy)
+        raw_dev.record_stream(copy)
+        self._upload.update(chunks=[(0, self.n_good, ev)], waited=False, host=pin)
         return out
 
     def _upload_pageable(self, src: torch.Tensor, dev):

@@ -156,3 +156,26 @@ def test_in_place_mutation_detected(scan0):
     c, _ = pb.update_pixel_map(s.scan, s.w, s.m, ref3, u, s.t0, win)
     np.testing.assert_array_equal(b.u, c.u)
     assert not np.array_equal(a.u, b.u)
+
+
+@pytest.mark.parametrize("dtype", [np.uint16, np.int32, np.uint32, np.int64, np.float64])
+def test_frame_stack_of_another_dtype(scan1, dtype):
+    """The reference takes frames of any dtype and casts them where it reads
+    them (recon.py:91).  A stack of detector counts in its own element type is
+    uploaded as it is and converted on the device (pxst_stack_to_f32): same
+    bits as the float32 stack of the same counts."""
+    from dataclasses import replace
+    s = scan1
+    assert float(s.scan.frames.max()) < 65535 and np.all(s.scan.frames == np.rint(s.scan.frames))
+    sc_n = replace(s.scan, frames=s.scan.frames.astype(dtype))
+    win = pb.SearchWindow(2, 2)
+    outs = []
+    for sc in (s.scan, sc_n):
+        pb.clear_cache()
+        ref = pb.make_reference(sc, s.w, s.m, s.u0, s.t0)
+        u, e = pb.update_pixel_map(sc, s.w, s.m, ref, s.u0, s.t0, win)
+        m = pb.calc_error(sc, s.w, s.m, ref, u, s.t0)
+        outs.append((ref.i_ref, ref.wsum, u.u, e, m.per_frame, m.per_pixel, m.reference_plane))
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
+    pb.clear_cache()
