@@ -75,7 +75,21 @@ def to_device(a: np.ndarray, dtype: np.dtype, device) -> torch.Tensor:
         t = torch.from_numpy(h)
         if t.is_pinned():
             return t.to(device, non_blocking=True)
-    pin = torch.empty(h.shape, dtype=torch.from_numpy(h[:0].copy()).dtype, pin_memory=True)
+    tdt = torch.from_numpy(h[:0].copy()).dtype
+    pin = torch.empty(h.shape, dtype=tdt, pin_memory=True)
+    if h.flags.writeable and h.nbytes >= (8 << 20) and h.ndim >= 1 and h.shape[0] >= 2 \
+            and _STAGE_CHUNKS > 1:
+        # a large pageable array (e.g. frame weights [N, SS, FS]): staged in chunks by
+        # torch's threaded host copy, each chunk's DMA under the next chunk's staging
+        src = torch.from_numpy(h)
+        out = torch.empty(h.shape, dtype=tdt, device=device)
+        n = h.shape[0]
+        k = min(n, _STAGE_CHUNKS)
+        edges = [n * c // k for c in range(k + 1)]
+        for lo, hi in zip(edges[:-1], edges[1:]):
+            pin[lo:hi].copy_(src[lo:hi])
+            out[lo:hi].copy_(pin[lo:hi], non_blocking=True)
+        return out
     np.copyto(pin.numpy(), h)
     return pin.to(device, non_blocking=True)
 
