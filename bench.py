@@ -556,6 +556,9 @@ def run_ours(args, rank, world, local):
 
     if not args.profile and not args.no_e2e and world == 1 and host_data:
         out["e2e"] = e2e(s, args, pb, engine, torch, trials)
+        u16 = e2e(s, args, pb, engine, torch, trials, dtype=np.uint16)
+        out["e2e"]["uint16_stack"] = {k: u16[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step",
+                                                          "d2h_bytes_per_step", "path")}
         pg = e2e(s, args, pb, engine, torch, trials, pinned_frames=False)
         out["e2e"]["pageable"] = {k: pg[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step",
                                                      "d2h_bytes_per_step", "path")}
@@ -581,11 +584,20 @@ def run_ours(args, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
-def e2e(s, args, pb, engine, torch, trials, pinned_frames=True):
+def e2e(s, args, pb, engine, torch, trials, pinned_frames=True, dtype=None):
     """Public-API iteration from host buffers (pinned, or the plain pageable
     numpy stack a drop-in caller passes), uploads/downloads timed."""
     from dataclasses import replace
-    if pinned_frames:
+    if dtype is not None:
+        # the same counts in the detector's own element type, pinned (as raw bytes:
+        # torch has no pinned uint16 allocator), uploaded as they are
+        src = s.scan.frames.astype(dtype)
+        assert np.array_equal(src.astype(np.float32), s.scan.frames)
+        raw = torch.empty(src.nbytes, dtype=torch.uint8, pin_memory=True)
+        host = raw.numpy().view(dtype).reshape(src.shape)
+        host[...] = src
+        scan = replace(s.scan, frames=host)
+    elif pinned_frames:
         pinned = torch.empty(s.scan.frames.shape, dtype=torch.float32, pin_memory=True)
         pinned.numpy()[...] = s.scan.frames
         scan = replace(s.scan, frames=pinned.numpy())
@@ -622,7 +634,7 @@ def e2e(s, args, pb, engine, torch, trials, pinned_frames=True):
     return {"value": trials * steps / dt, "unit": "trials/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt / steps * 1e3, "steps": steps,
             "path": "make_reference -> update_pixel_map -> calc_error (drop-in API, numpy in/out,"
-                    f" {'pinned' if pinned_frames else 'pageable (plain numpy)'} host frames,"
+                    f" {(np.dtype(dtype).name + ' pinned') if dtype is not None else 'pinned' if pinned_frames else 'pageable (plain numpy)'} host frames,"
                     " device cache cleared each step)"}
 
 
