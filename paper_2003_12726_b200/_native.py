@@ -166,10 +166,26 @@ def check(rc: int) -> None:
     raise RuntimeError(f"pxst CUDA error ({rc}): {msg}")
 
 
+_RAW_STREAM = None
+
+
 def stream_ptr(stream=None) -> int:
+    """cudaStream_t of `stream` (default: torch's current stream on the current
+    device) as an integer.  The default goes through torch's raw-stream getter
+    when it has one: torch.cuda.current_stream() builds a Stream object and
+    resolves the device index in Python, ~15 us a call and ~16 calls per
+    iteration of the drop-in API."""
+    global _RAW_STREAM
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _RAW_STREAM is None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        dev = getattr(torch._C, "_cuda_getDevice", None)
+        _RAW_STREAM = (raw, dev) if raw is not None and dev is not None else False
+    if _RAW_STREAM:
+        return int(_RAW_STREAM[0](_RAW_STREAM[1]()))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def launch_count() -> int:
