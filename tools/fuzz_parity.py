@@ -76,6 +76,12 @@ def one(seed):
     if rng.random() < 0.5 and n > 3:
         good[rng.choice(n, size=max(1, n // 5), replace=False)] = False
     sc = replace(sc, good_frames=good)
+    if many and rng.random() < 0.7:
+        # the stack in a detector's own element type (uploaded as it is and
+        # converted on the device; the reference casts per use, recon.py:91)
+        dt = [np.uint16, np.int32, np.float64, np.int64][int(rng.integers(0, 4))]
+        assert np.array_equal(sc.frames.astype(dt).astype(np.float32), sc.frames)
+        sc = replace(sc, frames=sc.frames.astype(dt))
     roi = None
     if rng.random() < 0.4:
         r0 = int(rng.integers(0, cfg.n_ss // 2)); r1 = int(rng.integers(r0 + 4, cfg.n_ss + 1))
@@ -98,7 +104,7 @@ def one(seed):
         # wide windows: 15 x 15 / 17 x 17 (generic kernel), 1 x 17 and 17 x 1 rows
         k = int(rng.choice([7, 8]))
         half = [(k, k), (0, 8), (8, 0)][int(rng.integers(0, 3))] if law != "fs_only" else (0, 8)
-    desc = (f"seed {seed}: {cfg.n_ss}x{cfg.n_fs} {law} frames {n} ({int(good.sum())} good) "
+    desc = (f"seed {seed}: {cfg.n_ss}x{cfg.n_fs} {law} {sc.frames.dtype} frames {n} ({int(good.sum())} good) "
             f"roi {rt} window {half} sub {sub} refine {refine}")
     oa = (sc.frames, sc.good_frames, w.w, m.mask)
     LAST["desc"] = desc
